@@ -1,0 +1,328 @@
+/*
+ * roix_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU statement of what the ROIX hot path computes.  It exists to
+ * prove the CUDA path right: only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * `--impl reference` legs may load it.  It shares no code, header, table or constant with the
+ * product library (paper_2602_15917_b200/csrc); neither side includes the other.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n, G-n = a reading
+ * recorded in DESIGN.md §3 (and SURVEY.md §8c).  Build: gcc -O2 -ffp-contract=off (no fast-math)
+ * so every floating-point expression below is evaluated exactly as written, in IEEE binary64.
+ *
+ * Every function is the plain definition written out: one loop over the voxels in linear-index
+ * order i = (z*Y + y)*X + x, no blocking, no fusion.  Volumes are Z x Y x X, x fastest.
+ * Masks are one byte per voxel (0/1); bit-packing is done by the Python side with numpy.
+ *
+ * Status codes returned: 0 = ok, 1 = value/quotient outside the quantiser's range (G-4, G-7),
+ * 2 = non-finite input (G-32), 3 = capacity exceeded.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_OK 0
+#define OR_RANGE 1
+#define OR_NONFINITE 2
+#define OR_CAPACITY 3
+
+/* ---------------------------------------------------------------------------------------------
+ * a1 QUANTISE (BJ.north_star "code = round(x / 2eb), round-half-even"; G-1..G-4, G-7).
+ * Definition: code = the integer nearest to the exact real quotient x / s, s = fl32(2*eb), ties to
+ * the even integer.  Written out with exact binary64 arithmetic: x and s are binary32 values, so
+ * k*s (|k| < 2^24) and (2k+1)*s are exact products in binary64, and 2x is exact.
+ * Validity range (G-4): |x| >= 2^23 * s is rejected (status OR_RANGE) -- the same predicate the
+ * paper-independent reading fixes for both sides.
+ * ------------------------------------------------------------------------------------------- */
+static int rne_exact(double x, double s, double *code)
+{
+    if (!(fabs(x) < 8388608.0 * s)) return OR_RANGE; /* also catches NaN */
+    double k = floor(x / s);                          /* a first guess, then made exact: */
+    while (k * s > x) k -= 1.0;                       /*   k*s <= x            */
+    while ((k + 1.0) * s <= x) k += 1.0;              /*   x < (k+1)*s         */
+    double twice = 2.0 * x, mid = (2.0 * k + 1.0) * s;
+    if (twice > mid) *code = k + 1.0;                 /* above the half-way point */
+    else if (twice < mid) *code = k;                  /* below it */
+    else *code = (fmod(k, 2.0) == 0.0) ? k : k + 1.0; /* exactly half-way: the even one */
+    return OR_OK;
+}
+
+/* s = fl32(2 * eb): doubling a binary32 is exact unless it overflows. */
+static int step_of(float eb, double *s)
+{
+    float s32 = 2.0f * eb;
+    if (!(eb > 0.0f) || !isfinite(s32)) return OR_RANGE;
+    *s = (double)s32;
+    return OR_OK;
+}
+
+int oracle_quantize_u16(const uint16_t *x, uint64_t n, float eb, uint16_t *codes)
+{
+    double s, c;
+    if (step_of(eb, &s)) return OR_RANGE;
+    for (uint64_t i = 0; i < n; i++) {
+        if (rne_exact((double)x[i], s, &c)) return OR_RANGE;
+        if (c > 65535.0) return OR_RANGE; /* u16 codes (G-7) */
+        codes[i] = (uint16_t)c;
+    }
+    return OR_OK;
+}
+
+int oracle_quantize_f32(const float *x, uint64_t n, float eb, int32_t *codes)
+{
+    double s, c;
+    if (step_of(eb, &s)) return OR_RANGE;
+    for (uint64_t i = 0; i < n; i++) {
+        if (!isfinite(x[i])) return OR_NONFINITE;
+        if (rne_exact((double)x[i], s, &c)) return OR_RANGE;
+        codes[i] = (int32_t)c;
+    }
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * a0 RANGE (fp32 only; G-6): min and max over all voxels, non-finite rejected (G-32).
+ * Relative eb (G-6, SZ value-range convention): eb_abs = fl32(rel * (fl64(max) - fl64(min))).
+ * ------------------------------------------------------------------------------------------- */
+int oracle_range_f32(const float *x, uint64_t n, float *mn, float *mx)
+{
+    float lo = INFINITY, hi = -INFINITY;
+    for (uint64_t i = 0; i < n; i++) {
+        if (!isfinite(x[i])) return OR_NONFINITE;
+        if (x[i] < lo) lo = x[i];
+        if (x[i] > hi) hi = x[i];
+    }
+    *mn = lo;
+    *mx = hi;
+    return OR_OK;
+}
+
+float oracle_resolve_eb(float mn, float mx, double rel)
+{
+    return (float)(rel * ((double)mx - (double)mn));
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * a2 HISTOGRAM ("based on intensity distribution"; bin[v] = count of v).
+ * uint16: 65 536 raw bins, accumulated (+=) so slabs can be summed.
+ * ------------------------------------------------------------------------------------------- */
+void oracle_hist_u16(const uint16_t *x, uint64_t n, uint64_t *h)
+{
+    for (uint64_t i = 0; i < n; i++) h[x[i]] += 1;
+}
+
+/* I_max (Eq. 1, "the maximum pixel intensity"; 1 if the image is all-zero). */
+uint32_t oracle_imax_u16(const uint64_t *h)
+{
+    for (int v = 65535; v > 0; v--)
+        if (h[v]) return (uint32_t)v;
+    return 1;
+}
+
+/* Eq. 1 with round-half-up: norm8(v) = round_half_up(255 v / I_max).
+ * For integers, round_half_up(a/b) = floor((2a + b) / 2b) with a = 255 v, b = I_max. */
+uint32_t oracle_norm8_u16(uint32_t v, uint32_t imax)
+{
+    uint64_t a = 255ull * v, b = imax;
+    uint64_t r = (2 * a + b) / (2 * b);
+    return r > 255 ? 255 : (uint32_t)r;
+}
+
+/* fp32 input, G-30: norm8(x) = clamp(floor(fl64(fl64(x) * 255 / fl64(I_max)) + 0.5), 0, 255). */
+uint32_t oracle_norm8_f32(float x, float imax)
+{
+    double q = ((double)x * 255.0) / (double)imax;
+    double r = floor(q + 0.5);
+    if (!(r > 0.0)) return 0;
+    if (r > 255.0) return 255;
+    return (uint32_t)r;
+}
+
+/* The 256-bin histogram of norm8 values that Otsu runs on. */
+void oracle_hist8_from_u16(const uint64_t *h, uint32_t imax, uint64_t *h8)
+{
+    memset(h8, 0, 256 * sizeof(uint64_t));
+    for (uint32_t v = 0; v < 65536; v++) h8[oracle_norm8_u16(v, imax)] += h[v];
+}
+
+void oracle_hist8_f32(const float *x, uint64_t n, float imax, uint64_t *h8)
+{
+    for (uint64_t i = 0; i < n; i++) h8[oracle_norm8_f32(x[i], imax)] += 1;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * a4 BINARISE (Eq. 2; "bit = 1 iff pixel > threshold"), evaluated per voxel on
+ * the normalised intensity.  polarity 0 = HIGH (norm8 > t8), 1 = LOW (norm8 <= t8; G-10).
+ * ------------------------------------------------------------------------------------------- */
+void oracle_binarize_u16(const uint16_t *x, uint64_t n, uint32_t imax, uint32_t t8, int polarity, uint8_t *m)
+{
+    for (uint64_t i = 0; i < n; i++) {
+        uint32_t k = oracle_norm8_u16(x[i], imax);
+        m[i] = polarity ? (k <= t8) : (k > t8);
+    }
+}
+
+void oracle_binarize_f32(const float *x, uint64_t n, float imax, uint32_t t8, int polarity, uint8_t *m)
+{
+    for (uint64_t i = 0; i < n; i++) {
+        uint32_t k = oracle_norm8_f32(x[i], imax);
+        m[i] = polarity ? (k <= t8) : (k > t8);
+    }
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * a5 MORPHOLOGICAL CLEANUP (G-11): one opening, o = dilate(erode(m)), cross structuring element
+ * of radius 1: se = 6 -> the 6 face neighbours in 3-D; se = 4 -> the 4 in-plane neighbours.
+ * Out-of-volume neighbours are ignored (erosion: treated as 1; dilation: treated as 0).
+ *   e_i = m_i AND (AND over j in SE(i) inside the volume of m_j)
+ *   o_i = e_i OR  (OR  over j in SE(i) inside the volume of e_j)
+ * ------------------------------------------------------------------------------------------- */
+static const int SE6[6][3] = {{-1, 0, 0}, {1, 0, 0}, {0, -1, 0}, {0, 1, 0}, {0, 0, -1}, {0, 0, 1}};
+
+static int se_count(int se) { return se == 6 ? 6 : 4; } /* se 4: the y/x entries of SE6 only */
+static const int *se_off(int se, int k) { return se == 6 ? SE6[k] : SE6[k + 2]; }
+
+int oracle_open(const uint8_t *m, int64_t Z, int64_t Y, int64_t X, int se, uint8_t *o)
+{
+    if (se != 6 && se != 4) return OR_RANGE;
+    uint64_t n = (uint64_t)(Z * Y * X);
+    uint8_t *e = (uint8_t *)malloc(n ? n : 1);
+    if (!e) return OR_CAPACITY;
+    for (int64_t z = 0; z < Z; z++)
+        for (int64_t y = 0; y < Y; y++)
+            for (int64_t x = 0; x < X; x++) {
+                uint64_t i = (uint64_t)((z * Y + y) * X + x);
+                uint8_t v = m[i];
+                for (int k = 0; k < se_count(se); k++) {
+                    const int *d = se_off(se, k);
+                    int64_t zz = z + d[0], yy = y + d[1], xx = x + d[2];
+                    if (zz < 0 || zz >= Z || yy < 0 || yy >= Y || xx < 0 || xx >= X) continue;
+                    v &= m[(zz * Y + yy) * X + xx];
+                }
+                e[i] = v;
+            }
+    for (int64_t z = 0; z < Z; z++)
+        for (int64_t y = 0; y < Y; y++)
+            for (int64_t x = 0; x < X; x++) {
+                uint64_t i = (uint64_t)((z * Y + y) * X + x);
+                uint8_t v = e[i];
+                for (int k = 0; k < se_count(se); k++) {
+                    const int *d = se_off(se, k);
+                    int64_t zz = z + d[0], yy = y + d[1], xx = x + d[2];
+                    if (zz < 0 || zz >= Z || yy < 0 || yy >= Y || xx < 0 || xx >= X) continue;
+                    v |= e[(zz * Y + yy) * X + xx];
+                }
+                o[i] = v;
+            }
+    free(e);
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * a6 CONNECTED COMPONENTS (BJ "3-D connected-component labelling"; G-14): breadth-first flood
+ * fill from seeds taken in raster (linear-index) order.  A seed is the first voxel of its
+ * component met in that order, i.e. the component's minimum linear index -- the canonical label.
+ * conn: 6 / 18 / 26 (3-D neighbourhoods), 4 / 8 (in-plane, per z-plane).
+ * Outputs: comp[i] = ordinal of i's component in min-index order (UINT32_MAX for background),
+ * comp_min[c], comp_size[c]; returns the component count, or -1 on bad conn / capacity.
+ * ------------------------------------------------------------------------------------------- */
+static int neighbour_ok(int conn, int dz, int dy, int dx)
+{
+    int k = abs(dz) + abs(dy) + abs(dx);
+    if (k == 0) return 0;
+    switch (conn) {
+    case 6: return k == 1;
+    case 18: return k <= 2;
+    case 26: return 1;
+    case 4: return dz == 0 && k == 1;
+    case 8: return dz == 0;
+    default: return 0;
+    }
+}
+
+int64_t oracle_label(const uint8_t *o, int64_t Z, int64_t Y, int64_t X, int conn, uint32_t *comp,
+                     uint64_t *comp_min, uint64_t *comp_size, uint64_t cap)
+{
+    if (conn != 4 && conn != 6 && conn != 8 && conn != 18 && conn != 26) return -1;
+    uint64_t n = (uint64_t)(Z * Y * X);
+    int offs[26][3], noff = 0;
+    for (int dz = -1; dz <= 1; dz++)
+        for (int dy = -1; dy <= 1; dy++)
+            for (int dx = -1; dx <= 1; dx++)
+                if (neighbour_ok(conn, dz, dy, dx)) {
+                    offs[noff][0] = dz;
+                    offs[noff][1] = dy;
+                    offs[noff][2] = dx;
+                    noff++;
+                }
+    for (uint64_t i = 0; i < n; i++) comp[i] = UINT32_MAX;
+    uint64_t *queue = (uint64_t *)malloc((n ? n : 1) * sizeof(uint64_t));
+    if (!queue) return -1;
+    int64_t nc = 0;
+    for (uint64_t seed = 0; seed < n; seed++) {
+        if (!o[seed] || comp[seed] != UINT32_MAX) continue;
+        if ((uint64_t)nc >= cap) { free(queue); return -1; }
+        uint64_t head = 0, tail = 0, size = 0;
+        comp[seed] = (uint32_t)nc;
+        queue[tail++] = seed;
+        while (head < tail) {
+            uint64_t i = queue[head++];
+            size++;
+            int64_t x = (int64_t)(i % (uint64_t)X), y = (int64_t)((i / (uint64_t)X) % (uint64_t)Y),
+                    z = (int64_t)(i / ((uint64_t)X * (uint64_t)Y));
+            for (int k = 0; k < noff; k++) {
+                int64_t zz = z + offs[k][0], yy = y + offs[k][1], xx = x + offs[k][2];
+                if (zz < 0 || zz >= Z || yy < 0 || yy >= Y || xx < 0 || xx >= X) continue;
+                uint64_t j = (uint64_t)((zz * Y + yy) * X + xx);
+                if (o[j] && comp[j] == UINT32_MAX) {
+                    comp[j] = (uint32_t)nc;
+                    queue[tail++] = j;
+                }
+            }
+        }
+        comp_min[nc] = seed;
+        comp_size[nc] = size;
+        nc++;
+    }
+    free(queue);
+    return nc;
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * a7 FILTER + a8 EXTRACT (BJ "small-object removal", "stream compaction of the retained ROI
+ * voxels into a dense code stream"; G-13, G-17): kept(c) = size(c) >= min_size; K_i = 1 iff i is
+ * in a kept component; stream = codes of the voxels with K_i = 1 in increasing i.
+ * ------------------------------------------------------------------------------------------- */
+void oracle_filter(const uint32_t *comp, uint64_t n, const uint64_t *comp_size, uint64_t ncomp,
+                   uint64_t min_size, uint8_t *kept, uint8_t *K)
+{
+    for (uint64_t c = 0; c < ncomp; c++) kept[c] = comp_size[c] >= min_size;
+    for (uint64_t i = 0; i < n; i++) K[i] = comp[i] != UINT32_MAX && kept[comp[i]];
+}
+
+int64_t oracle_extract_u16(const uint16_t *x, const uint8_t *K, uint64_t n, float eb, uint16_t *stream)
+{
+    double s, c;
+    int64_t j = 0;
+    if (step_of(eb, &s)) return -1;
+    for (uint64_t i = 0; i < n; i++) {
+        if (!K[i]) continue;
+        if (rne_exact((double)x[i], s, &c) || c > 65535.0) return -1;
+        stream[j++] = (uint16_t)c;
+    }
+    return j;
+}
+
+int64_t oracle_extract_f32(const float *x, const uint8_t *K, uint64_t n, float eb, int32_t *stream)
+{
+    double s, c;
+    int64_t j = 0;
+    if (step_of(eb, &s)) return -1;
+    for (uint64_t i = 0; i < n; i++) {
+        if (!K[i]) continue;
+        if (!isfinite(x[i]) || rne_exact((double)x[i], s, &c)) return -1;
+        stream[j++] = (int32_t)c;
+    }
+    return j;
+}
