@@ -1,0 +1,217 @@
+/*
+ * roix.h -- C ABI of libroix, the B200 (sm_100a) implementation of the ROIX-Comp hot path.
+ *
+ * ROIX-Comp (arXiv 2602.15917; /root/reference/PAPER.md, cited P:<line>) reduces X-CT data by
+ * keeping only a region of interest (ROI) and storing it error-bounded.  The data-parallel hot path
+ * built here (BASELINE.json north_star) is, per volume x[Z][Y][X]:
+ *
+ *   a0 RANGE      fp32 only: global min/max, relative eb                    roix_range, roix_resolve
+ *   a2 HISTOGRAM  intensity histogram ("based on intensity distribution")  roix_histogram
+ *   a3 THRESHOLD  Eq. 1 8-bit normalisation + Otsu       roix_threshold
+ *   a4 BINARISE   Eq. 2 mask                                         \ roix_morph
+ *   a5 MORPH      morphological cleanup: one opening, cross SE (reading G-11)    /
+ *   a6 CCL        connected components, label = min linear index (G-14)        \ roix_label
+ *   a7 FILTER     drop components smaller than min_size (G-13)                  /
+ *   a1+a8 EXTRACT uniform error-bounded quantisation code = RNE(x / 2eb) of the kept voxels,
+ *                 compacted in increasing linear index (paper analogue P:305-337)  roix_extract
+ *   a1 alone      roix_quantize (every voxel)
+ *
+ * Conventions (all calls):
+ *  - Linear index i = (z*Y + y)*X + x, uint64.  Volumes are dense, x fastest.
+ *  - Bit-packed masks: bit (i mod 32) of uint32 word i/32, LSB first; pad bits are 0 (G-16).
+ *  - Memory: every buffer is allocated by the caller (device memory unless stated).  The library
+ *    never allocates, frees or synchronises; every call only enqueues work on `stream`, so a whole
+ *    pipeline can be captured in a CUDA graph.  Pointers x, codes and bit arrays must be 16-byte
+ *    aligned.  Workspaces are sized by the matching *_workspace() query (host-only, no GPU work).
+ *  - Data-dependent scalars (eb, I_max, threshold, counts, error bits) live in a caller-allocated
+ *    device struct roix_scalars so that no call needs a device->host read.
+ *  - Host-detectable errors return a roix_status immediately and launch nothing:
+ *      ROIX_E_INVALID      null pointer, misalignment, bad enum, bad size;
+ *      ROIX_E_UNSUPPORTED  a parameter combination this library does not implement;
+ *      ROIX_E_CUDA         a launch failed (text in roix_last_error()).
+ *  - Data-dependent errors set sticky bits in roix_scalars.err (ROIX_ERR_*).  Every kernel reads
+ *    err first and does nothing if it is non-zero, so no garbage propagates; check err after the
+ *    final synchronisation.
+ *  - Determinism: every output is a pure function of the inputs and parameters -- independent of
+ *    launch configuration, atomic ordering and the number of GPUs a volume is sharded over.
+ *  - n = 0 is valid everywhere and is a no-op.
+ */
+#ifndef ROIX_H
+#define ROIX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ROIX_VERSION 1
+
+typedef struct CUstream_st *roix_stream_t; /* a cudaStream_t; NULL = the legacy default stream */
+
+typedef enum { ROIX_OK = 0, ROIX_E_INVALID = 1, ROIX_E_UNSUPPORTED = 2, ROIX_E_CUDA = 3 } roix_status;
+
+/* sticky device error bits (roix_scalars.err) */
+#define ROIX_ERR_NONFINITE 1u  /* a NaN/Inf voxel in fp32 input (G-32)                              */
+#define ROIX_ERR_RANGE 2u      /* |x| >= 2^23 * s, or a u16 code > 65535, or eb invalid (G-4, G-7)   */
+#define ROIX_ERR_CAPACITY 4u   /* an output / workspace capacity was exceeded                        */
+#define ROIX_ERR_DEGENERATE 8u /* fewer than two populated normalised-intensity bins      */
+
+typedef enum { ROIX_U16 = 1, ROIX_F32 = 2 } roix_dtype;
+typedef enum { ROIX_POL_HIGH = 0, ROIX_POL_LOW = 1 } roix_polarity; /* ROI = norm8 > t8 / <= t8 (G-10) */
+
+/*
+ * Device-resident scalars of one volume.  Allocate sizeof(roix_scalars) bytes of device memory and
+ * initialise with roix_scalars_init before the first call on a volume.
+ */
+typedef struct roix_scalars {
+    uint32_t err;         /* sticky ROIX_ERR_* bits                                              */
+    uint32_t min_ord;     /* a0: ordered-integer encoding of the fp32 minimum (atomicMin target)  */
+    uint32_t max_ord;     /* a0: ordered-integer encoding of the fp32 maximum (atomicMax target)  */
+    uint32_t polarity;    /* a3: roix_polarity used by roix_morph                                */
+    float eb;             /* absolute error bound in input units (G-5, G-6)                      */
+    float s;              /* quantisation step fl32(2*eb) (G-3)                                  */
+    float s_inv;          /* fl32(1/s): fast-path reciprocal, always followed by an exact check   */
+    uint32_t s_int;       /* s when s is an integer in [1, 65535], else 0 (u16 integer fast path) */
+    uint32_t s_magic;     /* ceil(2^32 / s_int) for s_int >= 2: exact floor(v / s_int), v < 2^16 */
+    uint32_t reserved0;
+    float i_max;          /* Eq. 1 I_max: global max, 1 when <= 0 (G-8)                  */
+    uint32_t t8;          /* a3: Otsu threshold on the 8-bit normalised intensity                */
+    uint32_t thr_u16;     /* a4 raw form: first u16 value v with norm8(v) > t8                   */
+    float thr_f32;        /* a4 raw form: first fp32 value x with norm8(x) > t8                  */
+    uint64_t count;       /* a8: number of kept voxels (global, after roix_extract)              */
+    uint64_t n_components;/* a6: number of components (this slab's table)                        */
+    uint64_t n_kept;      /* a7: number of kept components                                       */
+    uint64_t n_runs;      /* a6: number of foreground x-runs found                               */
+    float edges[256];     /* fp32 only: edges[k] = smallest finite x with norm8(x) >= k (k>=1)   */
+} roix_scalars;
+
+/* Slab geometry: this buffer holds planes [z0, z0+nz) of a global volume of gz planes. */
+typedef struct roix_geom {
+    uint64_t nz, ny, nx;
+    uint64_t z0, gz;
+} roix_geom;
+
+const char *roix_status_string(roix_status s);
+const char *roix_last_error(void); /* thread-local text of the last failure */
+int roix_version(void);
+size_t roix_scalars_size(void);
+
+/*
+ * Initialise sc: clear err and counters, min/max to +inf/-inf, and set eb.  For absolute eb pass
+ * eb_abs > 0 (it is validated on the host: ROIX_E_INVALID if not finite and > 0).  For a relative
+ * eb (fp32 only) pass eb_abs = 0 and give rel_eb to roix_resolve.
+ */
+roix_status roix_scalars_init(roix_scalars *sc, float eb_abs, roix_stream_t stream);
+
+/*
+ * a0 RANGE (fp32; reading G-6/G-32).  Accumulates the min and max of x[0..n) into sc (call once
+ * per buffer; several buffers may be accumulated).  Non-finite voxels set ROIX_ERR_NONFINITE.
+ */
+roix_status roix_range(const float *x, uint64_t n, roix_scalars *sc, roix_stream_t stream);
+
+/*
+ * Resolve data-dependent scalars once the range is known (G-6, G-8, G-30):
+ *   - rel_eb > 0 (fp32): eb = fl32(rel_eb * (fl64(max) - fl64(min)));
+ *   - s = fl32(2 eb), s_inv, s_int/s_magic;
+ *   - fp32: I_max = max if max > 0 else 1, and edges[k] of norm8 (G-30) by bisection.
+ * For u16 input call it with rel_eb = 0 after roix_scalars_init (I_max comes from the histogram).
+ */
+roix_status roix_resolve(roix_scalars *sc, roix_dtype dtype, double rel_eb, roix_stream_t stream);
+
+/*
+ * a1 QUANTISE every voxel: codes[i] = RNE(x[i] / s), the integer nearest the exact real quotient,
+ * ties to even (BJ north_star; G-2..G-4).  u16 input -> uint16 codes, fp32 input -> int32 codes.
+ * Requires roix_resolve.  Out-of-range voxels set ROIX_ERR_RANGE (their code is unspecified).
+ */
+roix_status roix_quantize(const void *x, roix_dtype dtype, uint64_t n, roix_scalars *sc, void *codes,
+                          roix_stream_t stream);
+
+/*
+ * a2 HISTOGRAM, accumulated (+=) into hist:
+ *   u16:  nbins = 65536, hist[v] += #{i : x[i] = v}           (raw values; I_max and the 256-bin
+ *         norm8 histogram are derived from it exactly by roix_threshold);
+ *   fp32: nbins = 256,   hist[k] += #{i : norm8(x[i]) = k}     (requires roix_resolve).
+ * hist is uint64, caller-zeroed; for a sharded volume, sum the per-slab histograms (allreduce).
+ */
+roix_status roix_histogram(const void *x, roix_dtype dtype, uint64_t n, roix_scalars *sc, uint64_t *hist,
+                           uint32_t nbins, roix_stream_t stream);
+
+/*
+ * a3 THRESHOLD (Eq. 1 P:255-257 with round-half-up S:82; Otsu P:263-267 with k = 2, smallest t on
+ * ties S:170; reading G-8/G-9).  u16: I_max = largest populated bin (1 if none above 0),
+ * h8[norm8(v)] += hist[v] with norm8(v) = floor((510 v + I_max) / (2 I_max)).  fp32: hist is already
+ * h8.  Otsu maximises the between-class variance exactly (256-bit integer compares).  Writes t8,
+ * thr_u16/thr_f32, polarity, i_max (u16) into sc; fewer than two populated norm8 bins sets
+ * ROIX_ERR_DEGENERATE.
+ */
+roix_status roix_threshold(const uint64_t *hist, uint32_t nbins, roix_dtype dtype, roix_polarity polarity,
+                           roix_scalars *sc, roix_stream_t stream);
+
+/*
+ * a4+a5 BINARISE + OPEN (Eq. 2; G-11).  m = [norm8(x) > t8] (HIGH) or [<= t8] (LOW), evaluated as
+ * the equivalent raw compare against thr_*; o = dilate(erode(m)) with the radius-1 cross:
+ *   se = 6: 6 face neighbours (3-D);  se = 4: the 4 in-plane neighbours (2-D per z-plane).
+ * Out-of-volume neighbours are ignored (erosion border 1, dilation border 0).
+ * x holds the slab g (planes z0..z0+nz-1); o_bits receives its ceil(nz*ny*nx/32) words.
+ * Sharded 3-D volumes (se = 6, z0 > 0 or z0+nz < gz): halo_lo holds the binarised m of global
+ * planes z0-2, z0-1 and halo_hi of z0+nz, z0+nz+1 (each plane packed from bit 0 with
+ * ceil(ny*nx/32) words; produced by roix_binarize_planes on the neighbour); planes that do not
+ * exist in the global volume are ignored.  NULL halos are allowed only at global volume faces.
+ * row_runs (nullable, nz*ny uint32): receives the number of x-runs of o in each row -- the fused
+ * first step of roix_label, which then skips its own counting pass.
+ */
+roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
+                       const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
+                       roix_stream_t stream);
+
+/* Binarise planes [p0, p0+np) of the slab (slab-local plane numbers) into m_bits, each plane
+ * packed from bit 0 with ceil(ny*nx/32) words -- the halo planes roix_morph consumes. */
+roix_status roix_binarize_planes(const void *x, roix_dtype dtype, const roix_geom *g, uint64_t p0, uint64_t np,
+                                 roix_scalars *sc, uint32_t *m_bits, roix_stream_t stream);
+
+/*
+ * a6+a7 LABEL + FILTER.  Connected components of o under conn (6, 18, 26: 3-D; 4, 8: in-plane per
+ * z-plane), each named by its minimum global linear index (G-14).  Components of size < min_size
+ * are dropped (G-13).  Outputs (device):
+ *   keep_bits      K = o AND kept; may alias o_bits (in-place: only dropped voxels are cleared);
+ *   comp_min/comp_size/comp_kept  the component table in increasing min index, capacity comp_cap
+ *                  (any may be NULL to skip the table); counts in sc->n_components / n_kept;
+ *   labels         optional (nullable) uint64 per voxel: the component label, UINT64_MAX for
+ *                  background.
+ * Works on x-runs of o (maximal stretches of set bits in one row); run_capacity bounds their
+ * number (ROIX_ERR_CAPACITY if exceeded).  row_runs: the per-row run counts roix_morph produced
+ * for this o (nullable: then they are counted here).  ws/ws_bytes from roix_label_workspace.
+ */
+typedef struct roix_label_out {
+    uint32_t *keep_bits;
+    uint64_t *comp_min;
+    uint64_t *comp_size;
+    uint8_t *comp_kept;
+    uint64_t comp_cap;
+    uint64_t *labels;
+} roix_label_out;
+
+roix_status roix_label_workspace(const roix_geom *g, uint64_t run_capacity, size_t *ws_bytes);
+roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
+                       uint64_t min_size, uint64_t run_capacity, void *ws, size_t ws_bytes,
+                       const roix_label_out *out, roix_scalars *sc, roix_stream_t stream);
+
+/*
+ * a1+a8 EXTRACT.  For the set bits i_0 < i_1 < ... of keep_bits (n voxels), codes_out[j] =
+ * RNE(x[i_j] / s) (u16 -> uint16, fp32 -> int32), written at codes_out[offset + j].  Adds the
+ * number of set bits to sc->count.  Reads x only where keep_bits has set bits.  More than
+ * `capacity` codes sets ROIX_ERR_CAPACITY (nothing is written past capacity).
+ * offset: device pointer to a uint64 start position (NULL = 0) -- the rank's global offset when
+ * a sharded stream is assembled.  ws/ws_bytes from roix_extract_workspace.
+ */
+roix_status roix_extract_workspace(uint64_t n, size_t *ws_bytes);
+roix_status roix_extract(const void *x, roix_dtype dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
+                         void *codes_out, uint64_t capacity, const uint64_t *offset, void *ws, size_t ws_bytes,
+                         roix_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROIX_H */

@@ -1,0 +1,126 @@
+"""ctypes binding of libroix (include/roix.h): argument marshalling only -- every step of the path runs
+in the library's CUDA kernels.  Functions keep the C names; pointer arguments take integers (e.g. a
+torch tensor's ``data_ptr()``) and streams take ``torch.cuda.Stream.cuda_stream``.
+
+There is no CPU fallback: importing this module on a box without the built library raises.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libroix.so")
+
+ROIX_OK, ROIX_E_INVALID, ROIX_E_UNSUPPORTED, ROIX_E_CUDA = 0, 1, 2, 3
+ERR_NONFINITE, ERR_RANGE, ERR_CAPACITY, ERR_DEGENERATE = 1, 2, 4, 8
+U16, F32 = 1, 2
+POL_HIGH, POL_LOW = 0, 1
+
+
+class Scalars(ctypes.Structure):
+    """Mirror of roix_scalars (device-resident; read back with ``Scalars.from_buffer_copy``)."""
+    _fields_ = [("err", ctypes.c_uint32), ("min_ord", ctypes.c_uint32), ("max_ord", ctypes.c_uint32),
+                ("polarity", ctypes.c_uint32), ("eb", ctypes.c_float), ("s", ctypes.c_float),
+                ("s_inv", ctypes.c_float), ("s_int", ctypes.c_uint32), ("s_magic", ctypes.c_uint32),
+                ("reserved0", ctypes.c_uint32), ("i_max", ctypes.c_float), ("t8", ctypes.c_uint32),
+                ("thr_u16", ctypes.c_uint32), ("thr_f32", ctypes.c_float), ("count", ctypes.c_uint64),
+                ("n_components", ctypes.c_uint64), ("n_kept", ctypes.c_uint64), ("n_runs", ctypes.c_uint64),
+                ("edges", ctypes.c_float * 256)]
+
+
+class Geom(ctypes.Structure):
+    _fields_ = [("nz", ctypes.c_uint64), ("ny", ctypes.c_uint64), ("nx", ctypes.c_uint64),
+                ("z0", ctypes.c_uint64), ("gz", ctypes.c_uint64)]
+
+
+class LabelOut(ctypes.Structure):
+    _fields_ = [("keep_bits", ctypes.c_void_p), ("comp_min", ctypes.c_void_p), ("comp_size", ctypes.c_void_p),
+                ("comp_kept", ctypes.c_void_p), ("comp_cap", ctypes.c_uint64), ("labels", ctypes.c_void_p)]
+
+
+class RoixError(RuntimeError):
+    pass
+
+
+_lib = None
+_vp, _u64, _u32, _f32, _f64, _i32 = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_float,
+                                     ctypes.c_double, ctypes.c_int)
+_SIGS = {
+    "roix_status_string": (ctypes.c_char_p, [_i32]),
+    "roix_last_error": (ctypes.c_char_p, []),
+    "roix_version": (_i32, []),
+    "roix_scalars_size": (ctypes.c_size_t, []),
+    "roix_scalars_init": (_i32, [_vp, _f32, _vp]),
+    "roix_range": (_i32, [_vp, _u64, _vp, _vp]),
+    "roix_resolve": (_i32, [_vp, _i32, _f64, _vp]),
+    "roix_quantize": (_i32, [_vp, _i32, _u64, _vp, _vp, _vp]),
+    "roix_histogram": (_i32, [_vp, _i32, _u64, _vp, _vp, _u32, _vp]),
+    "roix_threshold": (_i32, [_vp, _u32, _i32, _i32, _vp, _vp]),
+    "roix_morph": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "roix_binarize_planes": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _u64, _vp, _vp, _vp]),
+    "roix_label_workspace": (_i32, [ctypes.POINTER(Geom), _u64, ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_label": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _u32, _u64, _u64, _vp, ctypes.c_size_t,
+                          ctypes.POINTER(LabelOut), _vp, _vp]),
+    "roix_extract_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_extract": (_i32, [_vp, _i32, _u64, _vp, _vp, _vp, _u64, _vp, _vp, ctypes.c_size_t, _vp]),
+}
+
+
+def load():
+    """Load the in-tree libroix.so (built by paper_2602_15917_b200.build / __graft_entry__.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RoixError("libroix.so is not built (run __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype, fn.argtypes = res, args
+    assert lib.roix_scalars_size() == ctypes.sizeof(Scalars), "roix_scalars layout mismatch"
+    _lib = lib
+    return lib
+
+
+def _check(status, name):
+    if status != ROIX_OK:
+        lib = load()
+        raise RoixError("%s: %s (%s)" % (name, lib.roix_status_string(status).decode(),
+                                         lib.roix_last_error().decode()))
+
+
+def _wrap(name):
+    def f(*args):
+        _check(getattr(load(), name)(*args), name)
+    f.__name__ = name
+    return f
+
+
+roix_scalars_init = _wrap("roix_scalars_init")
+roix_range = _wrap("roix_range")
+roix_resolve = _wrap("roix_resolve")
+roix_quantize = _wrap("roix_quantize")
+roix_histogram = _wrap("roix_histogram")
+roix_threshold = _wrap("roix_threshold")
+roix_morph = _wrap("roix_morph")
+roix_binarize_planes = _wrap("roix_binarize_planes")
+roix_label = _wrap("roix_label")
+roix_extract = _wrap("roix_extract")
+
+
+def roix_label_workspace(geom, run_capacity):
+    out = ctypes.c_size_t()
+    _check(load().roix_label_workspace(ctypes.byref(geom), run_capacity, ctypes.byref(out)), "roix_label_workspace")
+    return out.value
+
+
+def roix_extract_workspace(n):
+    out = ctypes.c_size_t()
+    _check(load().roix_extract_workspace(n, ctypes.byref(out)), "roix_extract_workspace")
+    return out.value
+
+
+def scalars_size():
+    return load().roix_scalars_size()
+
+
+EXPORTED = sorted(_SIGS)

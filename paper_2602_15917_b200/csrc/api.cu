@@ -1,0 +1,199 @@
+// api.cu -- the C ABI of libroix (include/roix.h): argument validation, workspace sizing and launches
+// on the caller's stream.  No allocation, no synchronisation.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.cuh"
+#include "roix.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+roix_status fail(roix_status s, const char *fmt, const char *what) {
+    snprintf(g_err, sizeof(g_err), fmt, what);
+    return s;
+}
+roix_status invalid(const char *what) { return fail(ROIX_E_INVALID, "invalid argument: %s", what); }
+roix_status unsupported(const char *what) { return fail(ROIX_E_UNSUPPORTED, "unsupported: %s", what); }
+roix_status cuda(cudaError_t e, const char *where) {
+    if (e == cudaSuccess) return ROIX_OK;
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return ROIX_E_CUDA;
+}
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+bool dtype_ok(roix_dtype d) { return d == ROIX_U16 || d == ROIX_F32; }
+bool geom_ok(const roix_geom *g) {
+    if (!g) return false;
+    if (g->nz == 0 || g->ny == 0 || g->nx == 0) return false;
+    if (g->z0 + g->nz > g->gz) return false;
+    // linear indices are uint64; keep nz*ny*nx and the bit count well inside
+    long double n = (long double)g->nz * g->ny * g->nx;
+    return n < 1.0e18L;
+}
+
+}  // namespace
+
+int num_sms() {
+    static int sms = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    });
+    return sms;
+}
+
+extern "C" {
+
+const char *roix_status_string(roix_status s) {
+    switch (s) {
+    case ROIX_OK: return "ok";
+    case ROIX_E_INVALID: return "invalid argument";
+    case ROIX_E_UNSUPPORTED: return "unsupported";
+    case ROIX_E_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+const char *roix_last_error(void) { return g_err; }
+int roix_version(void) { return ROIX_VERSION; }
+size_t roix_scalars_size(void) { return sizeof(roix_scalars); }
+
+roix_status roix_scalars_init(roix_scalars *sc, float eb_abs, roix_stream_t stream) {
+    if (!sc) return invalid("sc is NULL");
+    if (!(eb_abs >= 0.0f) || !std::isfinite(eb_abs)) return invalid("eb_abs must be finite and >= 0");
+    return cuda(launch_scalars_init(sc, eb_abs, (cudaStream_t)stream), "roix_scalars_init");
+}
+
+roix_status roix_range(const float *x, uint64_t n, roix_scalars *sc, roix_stream_t stream) {
+    if (!sc) return invalid("sc is NULL");
+    if (n == 0) return ROIX_OK;
+    if (!x || !aligned16(x)) return invalid("x must be a 16-byte aligned device pointer");
+    return cuda(launch_range(x, n, sc, (cudaStream_t)stream), "roix_range");
+}
+
+roix_status roix_resolve(roix_scalars *sc, roix_dtype dtype, double rel_eb, roix_stream_t stream) {
+    if (!sc) return invalid("sc is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if (!(rel_eb >= 0.0) || !std::isfinite(rel_eb)) return invalid("rel_eb must be finite and >= 0");
+    if (rel_eb > 0.0 && dtype != ROIX_F32) return unsupported("relative eb needs fp32 input");
+    return cuda(launch_resolve(sc, (int)dtype, rel_eb, (cudaStream_t)stream), "roix_resolve");
+}
+
+roix_status roix_quantize(const void *x, roix_dtype dtype, uint64_t n, roix_scalars *sc, void *codes,
+                          roix_stream_t stream) {
+    if (!sc) return invalid("sc is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if (n == 0) return ROIX_OK;
+    if (!x || !codes || !aligned16(x) || !aligned16(codes)) return invalid("x / codes must be 16-byte aligned");
+    return cuda(launch_quantize(x, (int)dtype, n, sc, codes, (cudaStream_t)stream), "roix_quantize");
+}
+
+roix_status roix_histogram(const void *x, roix_dtype dtype, uint64_t n, roix_scalars *sc, uint64_t *hist,
+                           uint32_t nbins, roix_stream_t stream) {
+    if (!sc || !hist) return invalid("sc / hist is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if ((dtype == ROIX_U16 && nbins != 65536) || (dtype == ROIX_F32 && nbins != 256))
+        return invalid("nbins must be 65536 (u16) or 256 (fp32)");
+    if (n == 0) return ROIX_OK;
+    if (!x || !aligned16(x)) return invalid("x must be a 16-byte aligned device pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == ROIX_U16) return cuda(launch_hist_u16((const uint16_t *)x, n, sc, hist, st), "roix_histogram");
+    return cuda(launch_hist_f32((const float *)x, n, sc, hist, st), "roix_histogram");
+}
+
+roix_status roix_threshold(const uint64_t *hist, uint32_t nbins, roix_dtype dtype, roix_polarity polarity,
+                           roix_scalars *sc, roix_stream_t stream) {
+    if (!sc || !hist) return invalid("sc / hist is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if ((dtype == ROIX_U16 && nbins != 65536) || (dtype == ROIX_F32 && nbins != 256))
+        return invalid("nbins must be 65536 (u16) or 256 (fp32)");
+    if (polarity != ROIX_POL_HIGH && polarity != ROIX_POL_LOW) return invalid("polarity");
+    return cuda(launch_threshold(hist, (int)dtype, (int)polarity, sc, (cudaStream_t)stream), "roix_threshold");
+}
+
+static roix_status check_halos(const roix_geom *g, uint32_t se, const uint32_t *lo, const uint32_t *hi) {
+    if (se != 6) return ROIX_OK;
+    if (g->z0 > 0 && !lo) return invalid("halo_lo required: the slab does not start at the volume face");
+    if (g->z0 + g->nz < g->gz && !hi) return invalid("halo_hi required: the slab does not end at the volume face");
+    return ROIX_OK;
+}
+
+roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
+                       const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
+                       roix_stream_t stream) {
+    if (!sc || !o_bits) return invalid("sc / o_bits is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (se != 6 && se != 4) return unsupported("se must be 6 (3-D cross) or 4 (in-plane cross)");
+    if (!x || !aligned16(x) || !aligned16(o_bits)) return invalid("x / o_bits must be 16-byte aligned");
+    roix_status s = check_halos(g, se, halo_lo, halo_hi);
+    if (s != ROIX_OK) return s;
+    if (g->nx > (1u << 30)) return unsupported("rows longer than 2^30 voxels");
+    return cuda(launch_morph(x, (int)dtype, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, (cudaStream_t)stream),
+                "roix_morph");
+}
+
+roix_status roix_binarize_planes(const void *x, roix_dtype dtype, const roix_geom *g, uint64_t p0, uint64_t np,
+                                 roix_scalars *sc, uint32_t *m_bits, roix_stream_t stream) {
+    if (!sc || !m_bits) return invalid("sc / m_bits is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (p0 + np > g->nz) return invalid("planes outside the slab");
+    if (np == 0) return ROIX_OK;
+    if (!x || !aligned16(x)) return invalid("x must be 16-byte aligned");
+    return cuda(launch_binarize_planes(x, (int)dtype, *g, p0, np, sc, m_bits, (cudaStream_t)stream),
+                "roix_binarize_planes");
+}
+
+roix_status roix_label_workspace(const roix_geom *g, uint64_t run_capacity, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (run_capacity == 0 || run_capacity >= 0xffffffffull) return invalid("run_capacity must be in [1, 2^32-1)");
+    if (g->nz * g->ny >= 0xffffffffull) return unsupported("more than 2^32-1 rows per slab");
+    *ws_bytes = label_workspace_bytes(*g, run_capacity);
+    return ROIX_OK;
+}
+
+roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
+                       uint64_t min_size, uint64_t run_capacity, void *ws, size_t ws_bytes,
+                       const roix_label_out *out, roix_scalars *sc, roix_stream_t stream) {
+    if (!sc || !o_bits || !out || !ws) return invalid("sc / o_bits / out / ws is NULL");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (conn != 4 && conn != 8 && conn != 6 && conn != 18 && conn != 26) return unsupported("conn (4, 8, 6, 18, 26)");
+    size_t need = 0;
+    roix_status s = roix_label_workspace(g, run_capacity, &need);
+    if (s != ROIX_OK) return s;
+    if (ws_bytes < need) return invalid("workspace too small (see roix_label_workspace)");
+    if (out->comp_min && (!out->comp_size || out->comp_cap == 0)) return invalid("comp_size / comp_cap");
+    if (g->z0 != 0 || g->nz != g->gz) {
+        if (conn != 4 && conn != 8) return unsupported("sharded 3-D labelling goes through the slab-merge path");
+    }
+    return cuda(launch_label(o_bits, row_runs, *g, conn, min_size, run_capacity, ws, *out, sc, (cudaStream_t)stream),
+                "roix_label");
+}
+
+roix_status roix_extract_workspace(uint64_t n, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    *ws_bytes = extract_workspace_bytes(n);
+    return ROIX_OK;
+}
+
+roix_status roix_extract(const void *x, roix_dtype dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
+                         void *codes_out, uint64_t capacity, const uint64_t *offset, void *ws, size_t ws_bytes,
+                         roix_stream_t stream) {
+    if (!sc || !keep_bits || !ws) return invalid("sc / keep_bits / ws is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if (n == 0) return ROIX_OK;
+    if (!x || !aligned16(x)) return invalid("x must be 16-byte aligned");
+    if (capacity > 0 && !codes_out) return invalid("codes_out is NULL");
+    if (ws_bytes < extract_workspace_bytes(n)) return invalid("workspace too small (see roix_extract_workspace)");
+    return cuda(launch_extract(x, (int)dtype, n, keep_bits, sc, codes_out, capacity, offset, ws, (cudaStream_t)stream),
+                "roix_extract");
+}
+
+}  // extern "C"

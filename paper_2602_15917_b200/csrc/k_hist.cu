@@ -1,0 +1,177 @@
+// k_hist.cu -- a2 HISTOGRAM ("based on intensity distribution") and the standalone
+// a1 QUANTISE pass (BJ north_star).
+//
+// u16: shared-memory privatised counters.  A CTA keeps uint32 counters for the value window
+// [0, 16384) (64 KiB, two CTAs per SM, 32 warps each -- measured on B200: 4.6 TB/s of input for
+// CT-like value distributions); values >= 16384 go straight to the global uint64 bins, which keeps
+// the result exact for every input while the common 10..14-bit CT range stays on chip.
+// fp32: 256 normalised-intensity bins (needs the edges of roix_resolve).
+#include <cfloat>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace roix {
+
+constexpr int HWIN = 16384;
+
+__device__ __forceinline__ void hist_add(uint32_t *sh, uint64_t *gh, uint32_t v) {
+    if (v < (uint32_t)HWIN) atomicAdd(&sh[v], 1u);
+    else atomicAdd((unsigned long long *)&gh[v], 1ull);
+}
+
+__global__ void __launch_bounds__(1024, 2) k_hist_u16(const uint16_t *__restrict__ x, uint64_t n, roix_scalars *sc,
+                                                       uint64_t *gh) {
+    extern __shared__ uint32_t sh[];
+    if (get_err(sc)) return;
+    for (int i = threadIdx.x; i < HWIN; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint4 *x8 = reinterpret_cast<const uint4 *>(x);
+    const uint64_t n8 = n / 8, stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + stride < n8; i += 2 * stride) {
+        uint4 a = __ldcs(x8 + i), b = __ldcs(x8 + i + stride);
+        uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            hist_add(sh, gh, w[k] & 0xffffu);
+            hist_add(sh, gh, w[k] >> 16);
+        }
+    }
+    for (; i < n8; i += stride) {
+        uint4 a = __ldcs(x8 + i);
+        uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            hist_add(sh, gh, w[k] & 0xffffu);
+            hist_add(sh, gh, w[k] >> 16);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 7)) hist_add(sh, gh, x[n8 * 8 + threadIdx.x]);
+    __syncthreads();
+    for (int b = threadIdx.x; b < HWIN; b += blockDim.x) {
+        uint32_t c = sh[b];
+        if (c) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)c);
+    }
+}
+
+// norm8 of a finite fp32 value from the edges table e[0..256] (e[0] = -inf, e[256] = +inf):
+// norm8(x) = #{k >= 1 : x >= e[k]} -- an estimate from x * 255 / I_max corrected against the edges.
+__device__ __forceinline__ int norm8_edges(float x, float scale, const float *e) {
+    int k = __float2int_rz(fminf(fmaxf(x * scale + 0.5f, 0.0f), 255.0f));
+    while (x >= e[k + 1]) k++;
+    while (x < e[k]) k--;
+    return k;
+}
+
+__global__ void __launch_bounds__(512) k_hist_f32(const float *__restrict__ x, uint64_t n, roix_scalars *sc,
+                                                  uint64_t *gh) {
+    __shared__ uint32_t sh[256];
+    __shared__ float e[257];
+    if (get_err(sc)) return;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        sh[i] = 0;
+        e[i] = i == 0 ? -INFINITY : sc->edges[i];
+    }
+    if (threadIdx.x == 0) e[256] = INFINITY;
+    const float scale = 255.0f / sc->i_max;
+    __syncthreads();
+    bool bad = false;
+    const float4 *x4 = reinterpret_cast<const float4 *>(x);
+    const uint64_t n4 = n / 4, stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 a = __ldcs(x4 + i);
+        float v[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            if (fabsf(v[k]) <= FLT_MAX) atomicAdd(&sh[norm8_edges(v[k], scale, e)], 1u);
+            else bad = true;
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+        float v = x[n4 * 4 + threadIdx.x];
+        if (fabsf(v) <= FLT_MAX) atomicAdd(&sh[norm8_edges(v, scale, e)], 1u);
+        else bad = true;
+    }
+    if (bad) set_err(sc, ROIX_ERR_NONFINITE);
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
+        uint32_t c = sh[b];
+        if (c) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)c);
+    }
+}
+
+// ---------------------------------------------------------------------------- a1 standalone pass
+__global__ void __launch_bounds__(512) k_quantize_u16(const uint16_t *__restrict__ x, uint64_t n, roix_scalars *sc,
+                                                      uint16_t *__restrict__ codes) {
+    if (get_err(sc)) return;
+    const QP q = load_qp(sc);
+    uint32_t err = 0;
+    const uint64_t n8 = n / 8, stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += stride) {
+        uint4 a = __ldcs(reinterpret_cast<const uint4 *>(x) + i);
+        uint32_t w[4] = {a.x, a.y, a.z, a.w}, o[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            o[k] = code_u16(w[k] & 0xffffu, q, err) | (code_u16(w[k] >> 16, q, err) << 16);
+        __stcs(reinterpret_cast<uint4 *>(codes) + i, make_uint4(o[0], o[1], o[2], o[3]));
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {
+        uint64_t j = n8 * 8 + threadIdx.x;
+        codes[j] = (uint16_t)code_u16(x[j], q, err);
+    }
+    if (err) set_err(sc, err);
+}
+
+__global__ void __launch_bounds__(512) k_quantize_f32(const float *__restrict__ x, uint64_t n, roix_scalars *sc,
+                                                      int32_t *__restrict__ codes) {
+    if (get_err(sc)) return;
+    const QP q = load_qp(sc);
+    uint32_t err = 0;
+    const uint64_t n4 = n / 4, stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+        float4 a = __ldcs(reinterpret_cast<const float4 *>(x) + i);
+        int4 o = make_int4(code_f32(a.x, q, err), code_f32(a.y, q, err), code_f32(a.z, q, err), code_f32(a.w, q, err));
+        __stcs(reinterpret_cast<int4 *>(codes) + i, o);
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+        uint64_t j = n4 * 4 + threadIdx.x;
+        codes[j] = code_f32(x[j], q, err);
+    }
+    if (err) set_err(sc, err);
+}
+
+}  // namespace roix
+
+using namespace roix;
+
+static int grid_for(uint64_t work_items, int threads, int per_sm) {
+    uint64_t need = (work_items + threads - 1) / threads;
+    uint64_t cap = (uint64_t)num_sms() * per_sm;
+    if (need < 1) need = 1;
+    return (int)(need < cap ? need : cap);
+}
+
+cudaError_t launch_hist_u16(const uint16_t *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_hist_u16, cudaFuncAttributeMaxDynamicSharedMemorySize, HWIN * 4);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_hist_u16<<<grid_for(n / 8, 1024, 2), 1024, HWIN * 4, st>>>(x, n, sc, hist);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hist_f32(const float *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st) {
+    k_hist_f32<<<grid_for(n / 4, 512, 4), 512, 0, st>>>(x, n, sc, hist);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_quantize(const void *x, int dtype, uint64_t n, roix_scalars *sc, void *codes, cudaStream_t st) {
+    if (dtype == ROIX_U16)
+        k_quantize_u16<<<grid_for(n / 8, 512, 4), 512, 0, st>>>((const uint16_t *)x, n, sc, (uint16_t *)codes);
+    else
+        k_quantize_f32<<<grid_for(n / 4, 512, 4), 512, 0, st>>>((const float *)x, n, sc, (int32_t *)codes);
+    return cudaGetLastError();
+}

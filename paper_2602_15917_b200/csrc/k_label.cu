@@ -1,0 +1,383 @@
+// k_label.cu -- a6 CONNECTED COMPONENTS + a7 FILTER on x-runs of the opened mask o.
+//
+// A run is a maximal stretch of set bits of o in one row (z, y).  Runs are stored in raster order
+// (row, then x), so run index order equals the order of their first voxel's linear index, and a
+// union-find that always links the larger index under the smaller one ends with every component's
+// root = its first run = the run holding the component's minimum linear index (the canonical label,
+// reading G-14).  Steps (one launch each, all on the caller's stream):
+//   count   runs per row (skipped when roix_morph already produced them)
+//   scan    row_start = exclusive prefix of the counts; n_runs; capacity check
+//   runs    (x0, x1, row) of every run
+//   union   each run links with the overlapping runs of its "previous" neighbour rows
+//           (lock-free union-by-min with atomicMin on uint32 parents)
+//   flatten parent[i] = root(i)
+//   sizes   size[root] += run length (warp-aggregated)
+//   table   roots in index order -> (min_index, size, kept = size >= min_size)  (G-13)
+//   clear   K = o with the bits of dropped components cleared (in place when K aliases o)
+//   labels  optional per-voxel uint64 labels
+#include "common.cuh"
+#include "kernels.cuh"
+#include "scan.cuh"
+
+namespace roix {
+
+struct LabelWS {
+    uint32_t *row_runs;   // [rows]
+    uint32_t *row_start;  // [rows + 1]
+    uint64_t *scan_tmp;   // [scan_tmp_len]
+    uint32_t *x0, *x1, *rrow, *parent, *cidx;  // [cap]
+    uint64_t *size;       // [cap]
+    uint8_t *kept;        // [cap]
+    uint64_t *ctr;        // [4]: 0 n_runs, 1 n_roots, 2 n_kept
+};
+
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
+    const uint64_t rows = g.nz * g.ny;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += align256(bytes);
+        return o;
+    };
+    size_t o_rr = take(rows * 4), o_rs = take((rows + 1) * 4);
+    size_t o_st = take(scan_tmp_elems(rows + 1 > cap ? rows + 1 : cap) * 8);
+    size_t o_x0 = take(cap * 4), o_x1 = take(cap * 4), o_rw = take(cap * 4), o_pa = take(cap * 4),
+           o_ci = take((cap + 1) * 4);
+    size_t o_sz = take(cap * 8), o_kp = take(cap), o_ct = take(4 * 8);
+    if (ws) {
+        char *b = (char *)base;
+        ws->row_runs = (uint32_t *)(b + o_rr);
+        ws->row_start = (uint32_t *)(b + o_rs);
+        ws->scan_tmp = (uint64_t *)(b + o_st);
+        ws->x0 = (uint32_t *)(b + o_x0);
+        ws->x1 = (uint32_t *)(b + o_x1);
+        ws->rrow = (uint32_t *)(b + o_rw);
+        ws->parent = (uint32_t *)(b + o_pa);
+        ws->cidx = (uint32_t *)(b + o_ci);
+        ws->size = (uint64_t *)(b + o_sz);
+        ws->kept = (uint8_t *)(b + o_kp);
+        ws->ctr = (uint64_t *)(b + o_ct);
+    }
+    return off;
+}
+
+struct LGeo {
+    uint64_t nz, ny, nx, z0;
+    uint32_t W;
+};
+
+// word k (row-local) of row r of a linear bit array, pad bits beyond X cleared; never reads past
+// word nwords - 1.
+__device__ __forceinline__ uint32_t row_word_safe(const uint32_t *bits, const LGeo &G, uint64_t r, uint32_t k,
+                                                  uint64_t nwords) {
+    uint64_t b = r * G.nx + 32ull * k;
+    uint32_t sh = (uint32_t)(b & 31);
+    uint64_t wi = b >> 5;
+    uint32_t lo = bits[wi];
+    uint32_t hi = (sh && wi + 1 < nwords) ? bits[wi + 1] : 0u;
+    uint32_t v = sh ? __funnelshift_r(lo, hi, sh) : lo;
+    uint64_t rem = G.nx - 32ull * k;
+    if (rem < 32) v &= low_mask((uint32_t)rem);
+    return v;
+}
+
+__global__ void k_count_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nwords, uint32_t *row_runs,
+                             roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t rows = G.nz * G.ny;
+    const uint64_t wpg = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wpg) {
+        uint32_t carry = 0, cnt = 0;
+        for (uint32_t k0 = 0; k0 < G.W; k0 += 32) {
+            uint32_t k = k0 + lane_id();
+            uint32_t w = k < G.W ? row_word_safe(o, G, r, k, nwords) : 0u;
+            uint32_t prev = __shfl_up_sync(FULL, w, 1);
+            if (lane_id() == 0) prev = carry;
+            carry = __shfl_sync(FULL, w, 31);
+            cnt += __popc(w & ~((w << 1) | (prev >> 31)));
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(FULL, cnt, d);
+        if (lane_id() == 0) row_runs[r] = cnt;
+    }
+}
+
+// after the scan: total runs -> ctr[0], sc->n_runs; capacity check
+__global__ void k_runs_total(const uint64_t *total, uint64_t cap, LabelWS W, roix_scalars *sc) {
+    uint64_t t = *total;
+    W.ctr[0] = t > cap ? 0 : t;  // over capacity: every later step sees no runs
+    W.ctr[1] = 0;
+    W.ctr[2] = 0;
+    sc->n_runs = t;
+    if (t > cap) set_err(sc, ROIX_ERR_CAPACITY);
+}
+
+__global__ void k_extract_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nwords, LabelWS W,
+                               roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t rows = G.nz * G.ny;
+    const uint64_t wpg = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint32_t lane = lane_id();
+    for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wpg) {
+        uint32_t base = W.row_start[r];
+        if (W.row_start[r + 1] == base) continue;
+        uint32_t carry = 0, sbase = 0, ebase = 0;
+        for (uint32_t k0 = 0; k0 < G.W; k0 += 32) {
+            uint32_t k = k0 + lane;
+            uint32_t w = k < G.W ? row_word_safe(o, G, r, k, nwords) : 0u;
+            uint32_t prev = __shfl_up_sync(FULL, w, 1);
+            if (lane == 0) prev = carry;
+            uint32_t next = __shfl_down_sync(FULL, w, 1);
+            if (lane == 31) next = (k + 1 < G.W) ? row_word_safe(o, G, r, k + 1, nwords) : 0u;
+            carry = __shfl_sync(FULL, w, 31);
+            uint32_t starts = w & ~((w << 1) | (prev >> 31));
+            uint32_t ends = w & ~((w >> 1) | (next << 31));
+            uint32_t ns = __popc(starts), ne = __popc(ends);
+            uint32_t is = warp_incl_scan(ns) - ns, ie = warp_incl_scan(ne) - ne;
+            uint32_t ps = base + sbase + is, pe = base + ebase + ie;
+            while (starts) {
+                uint32_t b = __ffs(starts) - 1;
+                starts &= starts - 1;
+                W.x0[ps] = 32 * k + b;
+                W.rrow[ps] = (uint32_t)r;
+                ps++;
+            }
+            while (ends) {
+                uint32_t b = __ffs(ends) - 1;
+                ends &= ends - 1;
+                W.x1[pe++] = 32 * k + b + 1;
+            }
+            sbase += __shfl_sync(FULL, is + ns, 31);
+            ebase += __shfl_sync(FULL, ie + ne, 31);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t find_root(const uint32_t *parent, uint32_t x) {
+    uint32_t p = parent[x];
+    while (p != x) {
+        x = p;
+        p = parent[x];
+    }
+    return x;
+}
+
+__device__ __forceinline__ uint32_t find_compress(uint32_t *parent, uint32_t x) {
+    // path halving: parent pointers only ever move to ancestors, so racing writes stay valid
+    uint32_t p = parent[x];
+    while (p != x) {
+        uint32_t gp = parent[p];
+        if (gp != p) parent[x] = gp;
+        x = p;
+        p = gp;
+    }
+    return x;
+}
+
+__device__ void unite(uint32_t *parent, uint32_t a, uint32_t b) {
+    while (true) {
+        a = find_compress(parent, a);
+        b = find_compress(parent, b);
+        if (a == b) return;
+        if (a < b) {
+            uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        uint32_t old = atomicMin(&parent[a], b);  // link the larger root under the smaller
+        if (old == a) return;
+        a = old;
+    }
+}
+
+__global__ void k_init_parent(LabelWS W, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        W.parent[i] = (uint32_t)i;
+        W.size[i] = 0;
+    }
+}
+
+struct Nb {
+    int dz, dy, ext;
+};
+
+// previous-row neighbourhoods per connectivity (rows (z, y-1) and (z-1, *))
+__constant__ Nb c_nb[5][4] = {
+    /* 4  */ {{0, -1, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}},
+    /* 8  */ {{0, -1, 1}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}},
+    /* 6  */ {{0, -1, 0}, {-1, 0, 0}, {0, 0, 0}, {0, 0, 0}},
+    /* 18 */ {{0, -1, 1}, {-1, 0, 1}, {-1, -1, 0}, {-1, 1, 0}},
+    /* 26 */ {{0, -1, 1}, {-1, -1, 1}, {-1, 0, 1}, {-1, 1, 1}},
+};
+__constant__ int c_nnb[5] = {1, 1, 2, 4, 4};
+
+__global__ void k_union(LGeo G, int ci, LabelWS W, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    const int nnb = c_nnb[ci];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = W.rrow[i];
+        const int64_t z = r / G.ny, y = r % G.ny;
+        const uint32_t a0 = W.x0[i], a1 = W.x1[i];
+        for (int q = 0; q < nnb; q++) {
+            const Nb nb = c_nb[ci][q];
+            const int64_t zz = z + nb.dz, yy = y + nb.dy;
+            if (zz < 0 || yy < 0 || yy >= (int64_t)G.ny) continue;
+            const uint64_t nr = (uint64_t)zz * G.ny + yy;
+            uint32_t lo = W.row_start[nr], hi = W.row_start[nr + 1];
+            // first run j with x1[j] + ext > a0 (x1 is increasing along a row)
+            while (lo < hi) {
+                uint32_t mid = (lo + hi) >> 1;
+                if (W.x1[mid] + nb.ext > a0) hi = mid;
+                else lo = mid + 1;
+            }
+            for (uint32_t j = lo; j < W.row_start[nr + 1] && W.x0[j] < a1 + nb.ext; j++) unite(W.parent, (uint32_t)i, j);
+        }
+    }
+}
+
+__global__ void k_flatten_sizes(LabelWS W, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // grid-stride over whole warps so that the warp-level aggregation below is convergent
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
+        const uint64_t i = i0 + lane_id();
+        uint32_t root = 0xffffffffu, len = 0;
+        if (i < n) {
+            root = find_root(W.parent, (uint32_t)i);
+            W.parent[i] = root;
+            len = W.x1[i] - W.x0[i];
+        }
+        uint32_t grp = __match_any_sync(FULL, root);
+        uint32_t tot = __reduce_add_sync(grp, len);
+        if (i < n && (__ffs(grp) - 1) == (int)lane_id()) atomicAdd((unsigned long long *)&W.size[root], (unsigned long long)tot);
+    }
+}
+
+// cidx flags: 1 for roots
+__global__ void k_root_flags(LabelWS W, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        W.cidx[i] = W.parent[i] == (uint32_t)i;
+}
+
+__global__ void k_table(LGeo G, uint64_t min_size, LabelWS W, const uint32_t *cscan, roix_label_out out,
+                        roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    uint32_t nk = 0;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (W.parent[i] != (uint32_t)i) continue;
+        const uint64_t sz = W.size[i];
+        const uint8_t kp = sz >= min_size;
+        W.kept[i] = kp;
+        nk += kp;
+        const uint64_t c = cscan[i];
+        if (out.comp_min && c < out.comp_cap) {
+            out.comp_min[c] = ((G.z0 * G.ny) + W.rrow[i]) * G.nx + W.x0[i];
+            out.comp_size[c] = sz;
+            if (out.comp_kept) out.comp_kept[c] = kp;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) nk += __shfl_xor_sync(FULL, nk, d);
+    if (lane_id() == 0 && nk) atomicAdd((unsigned long long *)&W.ctr[2], (unsigned long long)nk);
+}
+
+__global__ void k_table_total(const uint64_t *nroots, LabelWS W, roix_label_out out, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    sc->n_components = *nroots;
+    sc->n_kept = W.ctr[2];
+    if (out.comp_min && *nroots > out.comp_cap) set_err(sc, ROIX_ERR_CAPACITY);
+}
+
+// K: clear the bits of every run whose component was dropped
+__global__ void k_clear_dropped(LGeo G, LabelWS W, uint32_t *K, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (W.kept[W.parent[i]]) continue;
+        uint64_t b = (uint64_t)W.rrow[i] * G.nx + W.x0[i], e = (uint64_t)W.rrow[i] * G.nx + W.x1[i];
+        while (b < e) {
+            uint64_t wi = b >> 5;
+            uint32_t s = (uint32_t)(b & 31);
+            uint32_t take = (uint32_t)min((uint64_t)(32 - s), e - b);
+            atomicAnd(&K[wi], ~(low_mask(take) << s));
+            b += take;
+        }
+    }
+}
+
+__global__ void k_labels(LGeo G, LabelWS W, uint64_t *labels, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t rt = W.parent[i];
+        const uint64_t lab = ((G.z0 * G.ny) + W.rrow[rt]) * G.nx + W.x0[rt];
+        const uint64_t base = (uint64_t)W.rrow[i] * G.nx;
+        for (uint32_t x = W.x0[i]; x < W.x1[i]; x++) labels[base + x] = lab;
+    }
+}
+
+}  // namespace roix
+
+using namespace roix;
+
+size_t label_workspace_bytes(const roix_geom &g, uint64_t cap) { return carve(nullptr, g, cap, nullptr); }
+
+static int ctas(uint64_t work, int threads) {
+    uint64_t need = (work + threads - 1) / threads;
+    uint64_t cap = (uint64_t)num_sms() * 8;
+    if (need < 1) need = 1;
+    return (int)(need < cap ? need : cap);
+}
+
+cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
+                         uint64_t min_size, uint64_t cap, void *ws, const roix_label_out &out, roix_scalars *sc,
+                         cudaStream_t st) {
+    LabelWS W;
+    carve(ws, g, cap, &W);
+    LGeo G;
+    G.nz = g.nz;
+    G.ny = g.ny;
+    G.nx = g.nx;
+    G.z0 = g.z0;
+    G.W = (uint32_t)((g.nx + 31) / 32);
+    const uint64_t rows = g.nz * g.ny, n = rows * g.nx, nwords = (n + 31) / 32;
+    int ci = conn == 4 ? 0 : conn == 8 ? 1 : conn == 6 ? 2 : conn == 18 ? 3 : 4;
+    cudaError_t e;
+    const uint32_t *rr = row_runs;
+    if (!rr) {
+        k_count_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W.row_runs, sc);
+        rr = W.row_runs;
+    }
+    // row_start = exclusive scan of the counts; total at scan_tmp[...]
+    if ((e = scan_u32(rr, W.row_start, rows, W.scan_tmp, st)) != cudaSuccess) return e;
+    k_runs_total<<<1, 1, 0, st>>>(scan_total_ptr(W.scan_tmp, rows), cap, W, sc);
+    const int runs_grid = num_sms() * 8;
+    k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, sc);
+    k_init_parent<<<runs_grid, 256, 0, st>>>(W, sc);
+    k_union<<<runs_grid, 256, 0, st>>>(G, ci, W, sc);
+    k_flatten_sizes<<<runs_grid, 256, 0, st>>>(W, sc);
+    k_root_flags<<<runs_grid, 256, 0, st>>>(W, sc);
+    if ((e = scan_u32_dev(W.cidx, W.cidx, W.ctr, cap, W.scan_tmp, st)) != cudaSuccess) return e;
+    k_table<<<runs_grid, 256, 0, st>>>(G, min_size, W, W.cidx, out, sc);
+    k_table_total<<<1, 1, 0, st>>>(scan_total_ptr(W.scan_tmp, cap), W, out, sc);
+    if (out.keep_bits) {
+        if (out.keep_bits != o_bits &&
+            (e = cudaMemcpyAsync(out.keep_bits, o_bits, nwords * 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+            return e;
+        k_clear_dropped<<<runs_grid, 256, 0, st>>>(G, W, out.keep_bits, sc);
+    }
+    if (out.labels) {
+        if ((e = cudaMemsetAsync(out.labels, 0xff, n * 8, st)) != cudaSuccess) return e;
+        k_labels<<<runs_grid, 256, 0, st>>>(G, W, out.labels, sc);
+    }
+    return cudaGetLastError();
+}

@@ -1,0 +1,160 @@
+// k_threshold.cu -- a3 THRESHOLD: Eq. 1 normalisation (round-half-up S:82) folded into
+// a 256-bin histogram, then 2-class Otsu (k = 2 reading G-9) with exact integer scores.
+//
+// Otsu's criterion sigma_B^2(t) = w0 w1 (mu0 - mu1)^2 equals D(t)^2 / (N^2 n0 n1) with
+// D = N s0 - n0 S (n0, s0: count and intensity sum of bins <= t; N, S: totals).  Candidates are
+// compared as D_a^2 n0_b n1_b  vs  D_b^2 n0_a n1_a  in 384-bit integers, the smallest t winning ties
+// (S:170), so the result is exact for any histogram with N < 2^39.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace roix {
+
+struct U384 {
+    uint64_t w[6];
+};
+
+__device__ __forceinline__ void mul_add(uint64_t a, uint64_t b, uint64_t *acc, int pos, int len) {
+    // acc[pos..] += a*b (128-bit product), carry propagated within len limbs
+    uint64_t lo = a * b, hi = __umul64hi(a, b);
+    uint64_t s = acc[pos] + lo;
+    uint64_t c = s < lo;
+    acc[pos] = s;
+    if (pos + 1 >= len) return;
+    uint64_t h = hi + c;  // hi <= 2^64 - 2: no overflow
+    s = acc[pos + 1] + h;
+    c = s < h;
+    acc[pos + 1] = s;
+    for (int k = pos + 2; k < len && c; k++) {
+        acc[k] += 1;
+        c = acc[k] == 0;
+    }
+}
+
+// (a1:a0)^2 * (b1:b0), all operands 128-bit, result 384-bit
+__device__ U384 sq_times(uint64_t a0, uint64_t a1, uint64_t b0, uint64_t b1) {
+    uint64_t sq[4] = {0, 0, 0, 0};
+    mul_add(a0, a0, sq, 0, 4);
+    mul_add(a0, a1, sq, 1, 4);
+    mul_add(a1, a0, sq, 1, 4);
+    mul_add(a1, a1, sq, 2, 4);
+    U384 r = {{0, 0, 0, 0, 0, 0}};
+    for (int i = 0; i < 4; i++) {
+        mul_add(sq[i], b0, r.w, i, 6);
+        mul_add(sq[i], b1, r.w, i + 1, 6);
+    }
+    return r;
+}
+
+__device__ __forceinline__ int cmp384(const U384 &a, const U384 &b) {
+    for (int i = 5; i >= 0; i--) {
+        if (a.w[i] != b.w[i]) return a.w[i] > b.w[i] ? 1 : -1;
+    }
+    return 0;
+}
+
+struct Cand {
+    uint64_t d0, d1;   // |D|
+    uint64_t n0, n1;   // class counts
+    int t;             // threshold, -1 = invalid
+};
+
+// is a strictly preferable to b?
+__device__ bool better(const Cand &a, const Cand &b) {
+    if (a.t < 0) return false;
+    if (b.t < 0) return true;
+    // den = n0 * n1 (< 2^78)
+    uint64_t ad0 = a.n0 * a.n1, ad1 = __umul64hi(a.n0, a.n1);
+    uint64_t bd0 = b.n0 * b.n1, bd1 = __umul64hi(b.n0, b.n1);
+    U384 lhs = sq_times(a.d0, a.d1, bd0, bd1);
+    U384 rhs = sq_times(b.d0, b.d1, ad0, ad1);
+    int c = cmp384(lhs, rhs);
+    return c > 0 || (c == 0 && a.t < b.t);
+}
+
+__global__ void __launch_bounds__(256) k_threshold(const uint64_t *__restrict__ hist, int dtype, int polarity,
+                                                    roix_scalars *sc) {
+    __shared__ uint64_t h8[256];
+    __shared__ uint64_t scan_n[256], scan_s[256];
+    __shared__ Cand cand[256];
+    __shared__ uint32_t s_imax;
+    const int t = threadIdx.x;
+    if (get_err(sc)) return;
+    uint32_t imax = 1;
+    if (dtype == ROIX_U16) {
+        // I_max = the largest populated value (Eq. 1); 1 if none above 0
+        if (t == 0) s_imax = 0;
+        __syncthreads();
+        for (int v = 256 * t + 255; v >= 256 * t; v--)
+            if (hist[v]) {
+                atomicMax(&s_imax, (uint32_t)v);
+                break;
+            }
+        __syncthreads();
+        imax = s_imax ? s_imax : 1;
+        // norm8(v) >= k  <=>  v >= e_k = ceil(I_max (2k - 1) / 510): h8[k] sums [e_k, e_{k+1})
+        uint64_t lo = t == 0 ? 0 : ((uint64_t)imax * (2 * t - 1) + 509) / 510;
+        uint64_t hi = t == 255 ? 65536 : ((uint64_t)imax * (2 * t + 1) + 509) / 510;
+        if (hi > 65536) hi = 65536;
+        uint64_t acc = 0;
+        for (uint64_t v = lo; v < hi; v++) acc += hist[v];
+        h8[t] = acc;
+    } else {
+        h8[t] = hist[t];
+    }
+    __syncthreads();
+    // inclusive prefix sums of counts and intensity sums over bins 0..t
+    uint64_t vn = h8[t], vs = (uint64_t)t * h8[t];
+    scan_n[t] = vn;
+    scan_s[t] = vs;
+    __syncthreads();
+    for (int d = 1; d < 256; d <<= 1) {
+        uint64_t an = t >= d ? scan_n[t - d] : 0, as = t >= d ? scan_s[t - d] : 0;
+        __syncthreads();
+        scan_n[t] += an;
+        scan_s[t] += as;
+        __syncthreads();
+    }
+    const uint64_t N = scan_n[255], S = scan_s[255];
+    Cand c;
+    c.t = -1;
+    c.d0 = c.d1 = c.n0 = c.n1 = 0;
+    if (t < 255) {
+        uint64_t n0 = scan_n[t], s0 = scan_s[t];
+        if (n0 > 0 && n0 < N) {
+            unsigned __int128 a = (unsigned __int128)N * s0, b = (unsigned __int128)n0 * S;
+            unsigned __int128 d = a >= b ? a - b : b - a;
+            c.d0 = (uint64_t)d;
+            c.d1 = (uint64_t)(d >> 64);
+            c.n0 = n0;
+            c.n1 = N - n0;
+            c.t = t;
+        }
+    }
+    cand[t] = c;
+    __syncthreads();
+    for (int stride = 128; stride > 0; stride >>= 1) {
+        if (t < stride && better(cand[t + stride], cand[t])) cand[t] = cand[t + stride];
+        __syncthreads();
+    }
+    if (t == 0) {
+        int t8 = cand[0].t;
+        sc->polarity = (uint32_t)polarity;
+        if (dtype == ROIX_U16) sc->i_max = (float)imax;
+        if (t8 < 0) {
+            set_err(sc, ROIX_ERR_DEGENERATE);
+            sc->t8 = 0;
+            return;
+        }
+        sc->t8 = (uint32_t)t8;
+        if (dtype == ROIX_U16) sc->thr_u16 = (uint32_t)(((uint64_t)imax * (2 * t8 + 1) + 509) / 510);
+        else sc->thr_f32 = sc->edges[t8 + 1];
+    }
+}
+
+}  // namespace roix
+
+cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st) {
+    roix::k_threshold<<<1, 256, 0, st>>>(hist, dtype, polarity, sc);
+    return cudaGetLastError();
+}

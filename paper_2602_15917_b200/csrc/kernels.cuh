@@ -1,0 +1,35 @@
+// kernels.cuh -- host-side launch entry points of the libroix kernels (called by api.cu).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "roix.h"
+
+int num_sms();  // SM count of the current device (cached)
+
+cudaError_t launch_scalars_init(roix_scalars *sc, float eb, cudaStream_t st);
+cudaError_t launch_range(const float *x, uint64_t n, roix_scalars *sc, cudaStream_t st);
+cudaError_t launch_resolve(roix_scalars *sc, int dtype, double rel_eb, cudaStream_t st);
+
+cudaError_t launch_quantize(const void *x, int dtype, uint64_t n, roix_scalars *sc, void *codes, cudaStream_t st);
+
+cudaError_t launch_hist_u16(const uint16_t *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st);
+cudaError_t launch_hist_f32(const float *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st);
+
+cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st);
+
+cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
+                         const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
+                         cudaStream_t st);
+cudaError_t launch_binarize_planes(const void *x, int dtype, const roix_geom &g, uint64_t p0, uint64_t np,
+                                   roix_scalars *sc, uint32_t *m_bits, cudaStream_t st);
+
+size_t label_workspace_bytes(const roix_geom &g, uint64_t cap);
+cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
+                         uint64_t min_size, uint64_t cap, void *ws, const roix_label_out &out, roix_scalars *sc,
+                         cudaStream_t st);
+
+size_t extract_workspace_bytes(uint64_t n);
+cudaError_t launch_extract(const void *x, int dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
+                           void *codes, uint64_t capacity, const uint64_t *offset, void *ws, cudaStream_t st);

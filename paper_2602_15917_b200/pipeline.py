@@ -1,0 +1,156 @@
+"""The ROIX hot path on one GPU, composed from the libroix C ABI (include/roix.h).
+
+    histogram -> Otsu threshold -> binarise + opening -> CCL + filter -> quantise + compact
+    (Fig. 2 P:210-217 order; BASELINE.json north_star)
+
+PyTorch provides device memory and the stream; every step runs in libroix's kernels, enqueued on
+one stream without host synchronisation (so the whole step can be captured in a CUDA graph).
+"""
+import ctypes
+import dataclasses
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+# kernels libroix launches per call (used for the bench's gpu_launches count)
+LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 1, "threshold": 1, "morph": 1,
+            "label": 15, "extract": 2}
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+@dataclasses.dataclass
+class Result:
+    codes: torch.Tensor        # dense code stream (count,), uint16 bits in int16 storage or int32
+    keep_bits: torch.Tensor    # packed K, int32 words (bit i%32 of word i//32)
+    count: int
+    t8: int
+    i_max: float
+    eb: float
+    thr: float
+    n_components: int
+    n_kept: int
+    n_runs: int
+    comp_min: torch.Tensor
+    comp_size: torch.Tensor
+    comp_kept: torch.Tensor
+    scalars: L.Scalars
+
+
+class Pipeline:
+    """Preallocated buffers + the enqueue sequence for volumes of one shape / dtype / parameter set."""
+
+    def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
+                 run_capacity=None, code_capacity=None, device=None, labels=False):
+        L.load()
+        self.shape = tuple(int(v) for v in shape)
+        Z, Y, X = self.shape
+        self.n = Z * Y * X
+        self.dtype = dtype
+        self.cdtype = L.U16 if dtype == "u16" else L.F32
+        if (eb > 0) == (rel_eb > 0):
+            raise ValueError("give exactly one of eb (absolute) and rel_eb (relative, fp32)")
+        self.eb, self.rel_eb = float(eb), float(rel_eb)
+        self.conn, self.se, self.min_size, self.polarity = int(conn), int(se), int(min_size), int(polarity)
+        self.device = torch.device(device or "cuda")
+        dev = self.device
+        self.geom = L.Geom(Z, Y, X, 0, Z)
+        self.nwords = (self.n + 31) // 32
+        self.sc = torch.zeros(L.scalars_size(), dtype=torch.uint8, device=dev)
+        self.nbins = 65536 if dtype == "u16" else 256
+        self.hist = torch.zeros(self.nbins, dtype=torch.int64, device=dev)
+        self.o = torch.empty(self.nwords + 4, dtype=torch.int32, device=dev)   # o, then K in place
+        self.row_runs = torch.empty(Z * Y, dtype=torch.int32, device=dev)
+        rows = Z * Y
+        worst = rows * ((X + 1) // 2)
+        if run_capacity is None:
+            run_capacity = min(worst, max(1 << 22, self.n // 256))
+        self._alloc_label(max(1, min(int(run_capacity), worst if worst > 0 else 1)))
+        self.code_capacity = self.n if code_capacity is None else int(code_capacity)
+        cdt = torch.int16 if dtype == "u16" else torch.int32
+        self.codes = torch.empty(max(self.code_capacity, 8), dtype=cdt, device=dev)
+        self.ex_ws = torch.empty(L.roix_extract_workspace(self.n), dtype=torch.uint8, device=dev)
+        self.labels = torch.empty(self.n, dtype=torch.int64, device=dev) if labels else None
+
+    def _alloc_label(self, cap):
+        self.run_capacity = cap
+        self.ws_bytes = L.roix_label_workspace(self.geom, cap)
+        self.label_ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.comp_cap = cap
+        dev = self.device
+        self.comp_min = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.comp_size = torch.empty(cap, dtype=torch.int64, device=dev)
+        self.comp_kept = torch.empty(cap, dtype=torch.uint8, device=dev)
+
+    # -------------------------------------------------------------------------------- enqueue
+    def enqueue(self, x, stream=None):
+        """Enqueue the whole path for x (device tensor, shape (Z, Y, X); u16 bits in int16/uint16
+        storage or float32) on `stream` (default: torch's current stream).  No host sync."""
+        assert x.is_cuda and x.numel() == self.n and x.is_contiguous()
+        st = ctypes.c_void_p((stream or torch.cuda.current_stream(self.device)).cuda_stream)
+        sc, xp, n = _ptr(self.sc), _ptr(x), self.n
+        L.roix_scalars_init(sc, self.eb, st)
+        if self.cdtype == L.F32:
+            L.roix_range(xp, n, sc, st)
+        L.roix_resolve(sc, self.cdtype, self.rel_eb, st)
+        self.hist.zero_()
+        L.roix_histogram(xp, self.cdtype, n, sc, _ptr(self.hist), self.nbins, st)
+        L.roix_threshold(_ptr(self.hist), self.nbins, self.cdtype, self.polarity, sc, st)
+        L.roix_morph(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o),
+                     _ptr(self.row_runs), st)
+        out = L.LabelOut(self.o.data_ptr(), self.comp_min.data_ptr(), self.comp_size.data_ptr(),
+                         self.comp_kept.data_ptr(), self.comp_cap,
+                         self.labels.data_ptr() if self.labels is not None else None)
+        L.roix_label(_ptr(self.o), _ptr(self.row_runs), ctypes.byref(self.geom), self.conn, self.min_size,
+                     self.run_capacity, _ptr(self.label_ws), self.ws_bytes, ctypes.byref(out), sc, st)
+        L.roix_extract(xp, self.cdtype, n, _ptr(self.o), sc, _ptr(self.codes), self.code_capacity, None,
+                       _ptr(self.ex_ws), self.ex_ws.numel(), st)
+
+    def launches(self):
+        k = sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
+                                      "extract"))
+        return k + (LAUNCHES["range"] if self.cdtype == L.F32 else 0)
+
+    def scalars(self):
+        return L.Scalars.from_buffer_copy(bytes(self.sc.cpu().numpy()))
+
+    def run(self, x, stream=None, check=True):
+        """Enqueue, synchronise and collect.  Grows the run capacity and retries once if the
+        labelling workspace was too small."""
+        self.enqueue(x, stream)
+        torch.cuda.synchronize(self.device)
+        s = self.scalars()
+        if s.err & L.ERR_CAPACITY and s.n_runs > self.run_capacity:
+            self._alloc_label(int(s.n_runs))
+            self.enqueue(x, stream)
+            torch.cuda.synchronize(self.device)
+            s = self.scalars()
+        if check and s.err:
+            raise L.RoixError("device error bits 0x%x" % s.err)
+        return self.collect(s)
+
+    def collect(self, s=None):
+        s = s or self.scalars()
+        cnt = int(s.count)
+        nc = int(min(s.n_components, self.comp_cap))
+        thr = float(s.thr_u16) if self.cdtype == L.U16 else float(s.thr_f32)
+        return Result(codes=self.codes[:cnt], keep_bits=self.o[: self.nwords], count=cnt, t8=int(s.t8),
+                      i_max=float(s.i_max), eb=float(s.eb), thr=thr, n_components=int(s.n_components),
+                      n_kept=int(s.n_kept), n_runs=int(s.n_runs), comp_min=self.comp_min[:nc],
+                      comp_size=self.comp_size[:nc], comp_kept=self.comp_kept[:nc], scalars=s)
+
+
+def run(x, **kw):
+    """One-shot convenience: Pipeline(x.shape, dtype, **kw).run(x)."""
+    dtype = "f32" if x.dtype == torch.float32 else "u16"
+    return Pipeline(tuple(x.shape), dtype, device=x.device, **kw).run(x)
+
+
+def unpack_bits(words, n):
+    """Host helper: packed int32 words -> uint8 mask of n voxels (LSB-first, G-16)."""
+    w = words.detach().cpu().numpy().view(np.uint8)
+    return np.unpackbits(w, bitorder="little")[:n]

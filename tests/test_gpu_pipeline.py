@@ -1,0 +1,116 @@
+"""-m gpu: the whole path (paper_2602_15917_b200.Pipeline, every step through the C ABI) against the
+composed oracle on the seeded synthetic phantoms of BASELINE.json's configs: C1 and C2 at full size,
+C3 / C4 / C5 scaled down (same recipe, every length scaled) so the oracle finishes in seconds.
+Full-size C3-C5 are covered by tests/test_gpu_fullsize.py (sampled / property checks)."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from gpu_util import dev, ptr, st, words_to_mask
+from paper_2602_15917_b200 import Pipeline
+from paper_2602_15917_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    from paper_2602_15917_b200 import build
+
+    build.build()
+    oracle.build()
+    synth.build()
+
+
+CASES = [synth.CONFIGS["C1"], synth.CONFIGS["C2"], synth.scaled("C3", 0.25, frames=4),
+         synth.scaled("C4", 0.125), synth.scaled("C5", 0.125), synth.scaled("C4", 0.0625), synth.scaled("C1", 0.37)]
+
+
+def _check(cfg, p, x, res):
+    x_np = synth.to_numpy(x, cfg)
+    ref = oracle.pipeline(x_np, eb=cfg.eb or None, rel_eb=cfg.rel_eb or None, conn=cfg.conn, se=cfg.se,
+                          min_size=cfg.min_size, polarity=cfg.polarity)
+    s = res.scalars
+    assert s.err == 0
+    assert res.t8 == ref["t8"] and res.i_max == ref["i_max"] and res.eb == ref["eb"]
+    if cfg.dtype == "u16":
+        np.testing.assert_array_equal(p.hist.cpu().numpy(), ref["hist"].astype(np.int64))
+    # o: re-run the fused binarise+open with the pipeline's threshold
+    o = torch.full_like(p.o, -1)
+    L.roix_morph(ptr(x), p.cdtype, ctypes.byref(p.geom), p.se, None, None, ptr(p.sc), ptr(o), None, st())
+    np.testing.assert_array_equal(words_to_mask(o, p.n).reshape(cfg.shape), ref["o"])
+    np.testing.assert_array_equal(words_to_mask(res.keep_bits, p.n).reshape(cfg.shape), ref["K"])
+    np.testing.assert_array_equal(res.comp_min.cpu().numpy(), ref["comp_min"].astype(np.int64))
+    np.testing.assert_array_equal(res.comp_size.cpu().numpy(), ref["comp_size"].astype(np.int64))
+    np.testing.assert_array_equal(res.comp_kept.cpu().numpy(), ref["kept"])
+    assert res.count == ref["count"]
+    got = res.codes.cpu().numpy()
+    np.testing.assert_array_equal(got.view(np.uint16) if cfg.dtype == "u16" else got, ref["stream"])
+    return ref
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=lambda c: c.name)
+def test_pipeline_vs_oracle(cfg):
+    x = synth.generate(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se,
+                 min_size=cfg.min_size, polarity=cfg.polarity)
+    res = p.run(x)
+    ref = _check(cfg, p, x, res)
+    # the step reduces the data (paper: spatial reduction 1.5x-8.5x)
+    assert 0 < ref["count"] < p.n
+
+
+def test_slab_generation_is_g_invariant():
+    cfg = synth.scaled("C5", 0.0625)
+    full = synth.generate(cfg)
+    Z = cfg.shape[0]
+    for G in (2, 4, 8):
+        parts = [synth.generate(cfg, z0=g * Z // G, nz=(g + 1) * Z // G - g * Z // G) for g in range(G)]
+        assert torch.equal(torch.cat(parts), full)
+
+
+def test_determinism_repeated_runs():
+    cfg = synth.scaled("C4", 0.0625)
+    x = synth.generate(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size)
+    first = p.run(x)
+    codes0, k0 = first.codes.clone(), first.keep_bits.clone()
+    t0 = (first.comp_min.clone(), first.comp_size.clone())
+    for _ in range(5):
+        r = p.run(x)
+        assert torch.equal(r.codes, codes0) and torch.equal(r.keep_bits, k0)
+        assert torch.equal(r.comp_min, t0[0]) and torch.equal(r.comp_size, t0[1])
+
+
+def test_edge_cases():
+    # degenerate: constant volume -> DEGENERATE error, raised
+    x = dev(np.full((4, 8, 40), 9, np.uint16))
+    p = Pipeline((4, 8, 40), "u16", eb=1.0)
+    with pytest.raises(L.RoixError):
+        p.run(x)
+    # empty ROI after cleanup: a checkerboard of two levels opens to nothing -> count 0, valid
+    z, y, xx = np.indices((4, 8, 40))
+    cb = np.where((z + y + xx) % 2 == 0, 1000, 10).astype(np.uint16)
+    r = Pipeline((4, 8, 40), "u16", eb=1.0).run(dev(cb))
+    assert r.count == 0 and r.n_components == 0
+    assert not words_to_mask(r.keep_bits, cb.size).any()
+    # a single bright cube: kept iff its (opened) size reaches min_size -- boundary sizes min-1 / min
+    v = np.full((6, 9, 41), 100, np.uint16)
+    v[1:5, 2:6, 3:7] = 3000
+    size = int(oracle.pipeline(v, eb=2.0, min_size=1)["comp_size"][0])    # 4^3 cube opens to 32 voxels
+    assert size == 32
+    for ms, kept in [(size, True), (size + 1, False)]:
+        r = Pipeline(v.shape, "u16", eb=2.0, min_size=ms).run(dev(v))
+        ref = oracle.pipeline(v, eb=2.0, min_size=ms)
+        assert r.count == ref["count"] == (size if kept else 0)
+    # all foreground except one voxel; ragged n (not a multiple of 8 or 32)
+    v = np.full((3, 7, 13), 2000, np.uint16)
+    v[1, 3, 6] = 5
+    r = Pipeline(v.shape, "u16", eb=0.5, min_size=1).run(dev(v))
+    ref = oracle.pipeline(v, eb=0.5, min_size=1)
+    assert r.count == ref["count"]
+    np.testing.assert_array_equal(r.codes.cpu().numpy().view(np.uint16), ref["stream"])

@@ -1,0 +1,346 @@
+"""-m gpu: each C-ABI call against the oracle, element by element, on seeded inputs that span several
+tiles and ragged tails.  Bit-exact everywhere (integer, mask and index outputs; the fp32 quantiser is
+exact by construction, G-4)."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gpu_util import (dev, dtype_code, ord2f, gpu_threshold, host_u16, mask_to_words, new_sc, ptr, read_sc, st,
+                      words_to_mask, write_sc)
+from paper_2602_15917_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    from paper_2602_15917_b200 import build
+
+    build.build()
+    oracle.build()
+
+
+def _quantize_gpu(x_np, eb):
+    x = dev(x_np)
+    sc = new_sc(eb)
+    L.roix_resolve(ptr(sc), dtype_code(x_np), 0.0, st())
+    out = torch.empty(x_np.size + 8, dtype=torch.int16 if x_np.dtype == np.uint16 else torch.int32, device="cuda")
+    L.roix_quantize(ptr(x), dtype_code(x_np), x_np.size, ptr(sc), ptr(out), st())
+    s = read_sc(sc)
+    o = out[: x_np.size].cpu().numpy()
+    return (o.view(np.uint16) if x_np.dtype == np.uint16 else o), s
+
+
+# ------------------------------------------------------------------------------------- a1 quantise
+@pytest.mark.parametrize("eb", [0.5, 1.0, 1.5, 2.0, 2.5, 3.0, 4.0, 0.75, 1.25, 100.0, 2047.5, 6.3])
+def test_quantize_u16_exhaustive(eb):
+    x = np.concatenate([np.arange(65536), np.arange(5)]).astype(np.uint16)   # ragged tail (n % 8 = 5)
+    got, s = _quantize_gpu(x, eb)
+    assert s.err == 0
+    np.testing.assert_array_equal(got, oracle.quantize(x, eb))
+
+
+def test_quantize_u16_range_error():
+    x = np.arange(65536, dtype=np.uint16)
+    _, s = _quantize_gpu(x, 0.25)            # s = 0.5: codes above 65535 -> ERR_RANGE (oracle raises too)
+    assert s.err & L.ERR_RANGE
+    with pytest.raises(oracle.OracleError):
+        oracle.quantize(x, 0.25)
+
+
+@pytest.mark.parametrize("eb", [1.3e-3, 0.01, 0.37, 5.0])
+def test_quantize_f32_random_ties_near_ties(eb):
+    rng = np.random.default_rng(17)
+    s = np.float32(2 * np.float32(eb))
+    k = rng.integers(-3000, 3000, 20000)
+    ties = ((k + 0.5) * np.float64(s)).astype(np.float32)
+    x = np.concatenate([rng.normal(0.5, 0.4, 100003), rng.uniform(-1000, 1000, 50001) * s, ties,
+                        np.nextafter(ties, np.float32(np.inf)), np.nextafter(ties, np.float32(-np.inf)),
+                        [0.0, -0.0, np.float32(1e-30), -np.float32(1e-30)]]).astype(np.float32)
+    got, sc = _quantize_gpu(x, eb)
+    assert sc.err == 0
+    np.testing.assert_array_equal(got, oracle.quantize(x, eb))
+
+
+def test_quantize_f32_nonfinite_and_range():
+    x = np.array([1.0, np.nan, 2.0], np.float32)
+    _, s = _quantize_gpu(x, 1.0)
+    assert s.err & L.ERR_NONFINITE
+    x = np.array([1.0, 2.0 ** 24], np.float32)
+    _, s = _quantize_gpu(x, 0.5)
+    assert s.err & L.ERR_RANGE
+
+
+# ------------------------------------------------------------------------ a0 range, eb, norm8 edges
+def test_range_resolve_edges():
+    rng = np.random.default_rng(3)
+    x_np = np.concatenate([rng.normal(0.02, 0.005, 300001), rng.uniform(0.3, 1.2, 7777)]).astype(np.float32)
+    x, sc, h = gpu_threshold(x_np, rel_eb=1e-3)
+    s = read_sc(sc)
+    mn, mx = oracle.value_range(x_np)
+    assert ord2f(s.min_ord) == mn and ord2f(s.max_ord) == mx
+    assert s.eb == oracle.resolve_eb(mn, mx, 1e-3)
+    assert s.i_max == oracle.imax_f32(mx)
+    # edges[k] = smallest float with norm8 >= k (checked with the oracle's norm8)
+    for k in range(1, 256):
+        e = np.float32(s.edges[k])
+        assert oracle.norm8_f32(e, s.i_max) >= k
+        assert oracle.norm8_f32(np.nextafter(e, np.float32(-np.inf)), s.i_max) < k
+    np.testing.assert_array_equal(h.cpu().numpy(), oracle.hist8_f32(x_np, s.i_max).astype(np.int64))
+
+
+def test_range_nonfinite():
+    x_np = np.ones(1000, np.float32)
+    x_np[999] = np.inf
+    x = dev(x_np)
+    sc = new_sc(0.0)
+    L.roix_range(ptr(x), x_np.size, ptr(sc), st())
+    assert read_sc(sc).err & L.ERR_NONFINITE
+
+
+# ---------------------------------------------------------------------------- a2 histogram, a3 Otsu
+def test_histogram_u16_full_range_and_accumulate():
+    rng = np.random.default_rng(5)
+    x_np = np.concatenate([rng.normal(400, 60, 500000).clip(0, 4095), rng.integers(0, 65536, 300000),
+                           [65535, 16383, 16384, 0]]).astype(np.uint16)
+    x = dev(x_np)
+    sc = new_sc(1.0)
+    h = torch.zeros(65536, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        L.roix_histogram(ptr(x), L.U16, x_np.size, ptr(sc), ptr(h), 65536, st())
+    ref = oracle.hist_u16(x_np).astype(np.int64)
+    np.testing.assert_array_equal(h.cpu().numpy(), 2 * ref)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_threshold_u16_vs_oracle(seed):
+    rng = np.random.default_rng(seed)
+    bg = rng.normal(rng.uniform(200, 800), rng.uniform(20, 80), 200000)
+    fg = rng.normal(rng.uniform(1500, 3500), rng.uniform(40, 120), int(rng.integers(5000, 100000)))
+    x_np = np.concatenate([bg, fg]).clip(0, 65535 if seed % 2 else 4095).astype(np.uint16)
+    for pol in (0, 1):
+        x, sc, h = gpu_threshold(x_np, eb=2.0, polarity=pol)
+        s = read_sc(sc)
+        hist = oracle.hist_u16(x_np)
+        imax = oracle.imax_u16(hist)
+        t8 = oracle.otsu2(oracle.hist8_from_u16(hist, imax))
+        assert s.err == 0 and s.i_max == imax and s.t8 == t8 and s.polarity == pol
+        # raw threshold: the first value whose norm8 exceeds t8
+        assert oracle.norm8_u16(s.thr_u16, imax) > t8 >= oracle.norm8_u16(s.thr_u16 - 1, imax)
+
+
+def test_threshold_degenerate():
+    for v in (0, 7):
+        x_np = np.full(1000, v, np.uint16)
+        _, sc, _ = gpu_threshold(x_np)
+        assert read_sc(sc).err & L.ERR_DEGENERATE
+        with pytest.raises(oracle.Degenerate):
+            h = oracle.hist_u16(x_np)
+            oracle.otsu2(oracle.hist8_from_u16(h, oracle.imax_u16(h)))
+
+
+def test_threshold_f32_vs_oracle():
+    rng = np.random.default_rng(9)
+    x_np = np.concatenate([rng.normal(0.02, 0.005, 400000), rng.uniform(0.3, 1.2, 90000)]).astype(np.float32)
+    x, sc, h = gpu_threshold(x_np, rel_eb=1e-3)
+    s = read_sc(sc)
+    h8 = oracle.hist8_f32(x_np, oracle.imax_f32(x_np.max()))
+    t8 = oracle.otsu2(h8)
+    assert s.t8 == t8
+    assert oracle.norm8_f32(s.thr_f32, s.i_max) > t8
+    assert oracle.norm8_f32(np.nextafter(np.float32(s.thr_f32), np.float32(-np.inf)), s.i_max) <= t8
+
+
+# ------------------------------------------------------------------------- a4 + a5 binarise + open
+MORPH_SHAPES = [(1, 1, 1), (1, 1, 40), (2, 3, 5), (3, 5, 7), (5, 33, 65), (7, 64, 64), (9, 17, 100),
+                (4, 70, 139), (3, 20, 1390), (11, 9, 256), (6, 40, 96), (33, 8, 32)]
+
+
+def _morph_gpu(x_np, thr, pol, se):
+    Z, Y, X = x_np.shape
+    x = dev(x_np)
+    sc = new_sc(1.0)
+    s = read_sc(sc)
+    s.polarity = pol
+    if x_np.dtype == np.uint16:
+        s.thr_u16 = thr
+    else:
+        s.thr_f32 = thr
+    write_sc(sc, s)
+    n = x_np.size
+    o = torch.full(((n + 31) // 32 + 4,), -1, dtype=torch.int32, device="cuda")   # garbage-initialised
+    runs = torch.full((Z * Y,), -1, dtype=torch.int32, device="cuda")
+    g = L.Geom(Z, Y, X, 0, Z)
+    L.roix_morph(ptr(x), dtype_code(x_np), ctypes.byref(g), se, None, None, ptr(sc), ptr(o), ptr(runs), st())
+    assert read_sc(sc).err == 0
+    return o, runs
+
+
+def _runs_per_row(mask3):
+    Z, Y, X = mask3.shape
+    m = mask3.reshape(Z * Y, X).astype(np.int8)
+    d = np.diff(np.concatenate([np.zeros((Z * Y, 1), np.int8), m], axis=1), axis=1)
+    return (d == 1).sum(axis=1)
+
+
+@pytest.mark.parametrize("shape", MORPH_SHAPES)
+@pytest.mark.parametrize("se", [6, 4])
+@pytest.mark.parametrize("dt", ["u16", "f32"])
+def test_morph_random_masks(shape, se, dt):
+    rng = np.random.default_rng(abs(hash((shape, se, dt))) % 2 ** 32)
+    for p, pol in [(0.75, 0), (0.6, 1), (0.9, 0)]:
+        m = rng.random(shape) < p
+        if dt == "u16":
+            x_np = np.where(m, rng.integers(1000, 4000, shape), rng.integers(0, 999, shape)).astype(np.uint16)
+            thr = 1000
+        else:
+            x_np = np.where(m, rng.uniform(0.5, 1.0, shape), rng.uniform(-1.0, 0.4999, shape)).astype(np.float32)
+            thr = np.float32(0.5)
+        mm = m if pol == 0 else ~m
+        ref = oracle.opening(mm.astype(np.uint8), se)
+        o, runs = _morph_gpu(x_np, thr, pol, se)
+        n = x_np.size
+        got = words_to_mask(o, n).reshape(shape)
+        np.testing.assert_array_equal(got, ref)
+        w = o.cpu().numpy().view(np.uint32)
+        if n % 32:
+            assert w[n // 32] >> (n % 32) == 0           # pad bits zero (G-16)
+        np.testing.assert_array_equal(runs.cpu().numpy(), _runs_per_row(ref))
+
+
+def test_binarize_planes_halo_layout():
+    rng = np.random.default_rng(2)
+    shape = (6, 13, 37)
+    x_np = rng.integers(0, 2000, shape).astype(np.uint16)
+    x = dev(x_np)
+    sc = new_sc(1.0)
+    s = read_sc(sc)
+    s.thr_u16 = 1000
+    write_sc(sc, s)
+    g = L.Geom(*shape, 0, shape[0])
+    pw = (13 * 37 + 31) // 32
+    out = torch.full((3 * pw,), -1, dtype=torch.int32, device="cuda")
+    L.roix_binarize_planes(ptr(x), L.U16, ctypes.byref(g), 2, 3, ptr(sc), ptr(out), st())
+    torch.cuda.synchronize()
+    for p in range(3):
+        ref = oracle.pack_bits((x_np[2 + p] >= 1000).astype(np.uint8))
+        np.testing.assert_array_equal(out[p * pw:(p + 1) * pw].cpu().numpy().view(np.uint32), ref)
+
+
+# --------------------------------------------------------------------------------- a6 + a7 label
+LABEL_SHAPES = [(1, 1, 1), (1, 1, 70), (2, 3, 5), (4, 9, 33), (6, 17, 64), (10, 10, 10), (3, 31, 97), (5, 40, 130)]
+
+
+def _label_gpu(mask, conn, min_size, with_runs, inplace=True, labels=True):
+    Z, Y, X = mask.shape
+    n = mask.size
+    o = mask_to_words(mask.astype(np.uint8))
+    g = L.Geom(Z, Y, X, 0, Z)
+    cap = max(1, Z * Y * ((X + 1) // 2))
+    wsb = L.roix_label_workspace(g, cap)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    cmin = torch.full((cap,), -7, dtype=torch.int64, device="cuda")
+    csz = torch.full((cap,), -7, dtype=torch.int64, device="cuda")
+    ckp = torch.full((cap,), 9, dtype=torch.uint8, device="cuda")
+    lab = torch.empty(n, dtype=torch.int64, device="cuda") if labels else None
+    K = o if inplace else torch.full_like(o, -1)
+    runs = None
+    if with_runs:
+        m3 = mask.reshape(Z * Y, X).astype(np.int8)
+        d = np.diff(np.concatenate([np.zeros((Z * Y, 1), np.int8), m3], axis=1), axis=1)
+        runs = torch.from_numpy((d == 1).sum(axis=1).astype(np.int32)).cuda()
+    out = L.LabelOut(K.data_ptr(), cmin.data_ptr(), csz.data_ptr(), ckp.data_ptr(), cap,
+                     lab.data_ptr() if labels else None)
+    sc = new_sc(1.0)
+    L.roix_label(ptr(o), ptr(runs), ctypes.byref(g), conn, min_size, cap, ptr(ws), wsb, ctypes.byref(out), ptr(sc),
+                 st())
+    s = read_sc(sc)
+    nc = int(s.n_components)
+    return s, K, cmin[:nc].cpu().numpy(), csz[:nc].cpu().numpy(), ckp[:nc].cpu().numpy(), lab
+
+
+@pytest.mark.parametrize("conn", [6, 18, 26, 4, 8])
+@pytest.mark.parametrize("shape", LABEL_SHAPES)
+def test_label_random_vs_oracle(conn, shape):
+    rng = np.random.default_rng(abs(hash((conn, shape))) % 2 ** 32)
+    for p, min_size, with_runs in [(0.3, 1, False), (0.5, 3, True), (0.7, 10, True)]:
+        mask = (rng.random(shape) < p).astype(np.uint8)
+        s, K, cmin, csz, ckp, lab = _label_gpu(mask, conn, min_size, with_runs)
+        assert s.err == 0
+        comp, rmin, rsz = oracle.label(mask, conn)
+        kept, rK = oracle.filter_components(comp, rsz, min_size)
+        np.testing.assert_array_equal(cmin, rmin.astype(np.int64))
+        np.testing.assert_array_equal(csz, rsz.astype(np.int64))
+        np.testing.assert_array_equal(ckp, kept)
+        np.testing.assert_array_equal(words_to_mask(K, mask.size).reshape(shape), rK)
+        exp = np.full(mask.size, -1, np.int64)
+        fg = comp.ravel() != np.iinfo(np.uint32).max
+        exp[fg] = rmin[comp.ravel()[fg]].astype(np.int64)
+        np.testing.assert_array_equal(lab.cpu().numpy(), exp)
+        assert s.n_kept == int(kept.sum())
+
+
+def test_label_not_inplace_and_checkerboard():
+    z, y, x = np.indices((6, 8, 40))
+    cb = ((z + y + x) % 2 == 0).astype(np.uint8)
+    for conn, ncomp in [(6, cb.sum()), (18, 1), (26, 1), (4, cb.sum()), (8, 6)]:
+        s, K, cmin, csz, ckp, _ = _label_gpu(cb, conn, 2, False, inplace=False, labels=False)
+        assert s.n_components == ncomp
+        exp = oracle.filter_components(*[oracle.label(cb, conn)[i] for i in (0, 2)], 2)[1]
+        np.testing.assert_array_equal(words_to_mask(K, cb.size).reshape(cb.shape), exp)
+
+
+def test_label_capacity_error():
+    mask = np.ones((2, 4, 64), np.uint8)
+    mask[:, :, ::2] = 0                                  # 256 runs
+    o = mask_to_words(mask)
+    g = L.Geom(2, 4, 64, 0, 2)
+    wsb = L.roix_label_workspace(g, 100)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    out = L.LabelOut(o.data_ptr(), None, None, None, 0, None)
+    sc = new_sc(1.0)
+    L.roix_label(ptr(o), None, ctypes.byref(g), 6, 1, 100, ptr(ws), wsb, ctypes.byref(out), ptr(sc), st())
+    s = read_sc(sc)
+    assert s.err & L.ERR_CAPACITY and s.n_runs == 256
+
+
+# ---------------------------------------------------------------------------------- a8 extract
+@pytest.mark.parametrize("n", [1, 31, 1000, 8192, 8193, 100003, 1 << 20])
+@pytest.mark.parametrize("dt", ["u16", "f32"])
+def test_extract_vs_oracle(n, dt):
+    rng = np.random.default_rng(n)
+    K = (rng.random(n) < rng.uniform(0.05, 0.9)).astype(np.uint8)
+    K[: min(n, 40)] = 1
+    if dt == "u16":
+        x_np, eb = rng.integers(0, 65536, n).astype(np.uint16), 2.0
+    else:
+        x_np, eb = rng.normal(0, 3, n).astype(np.float32), 0.01
+    x = dev(x_np)
+    sc = new_sc(eb)
+    L.roix_resolve(ptr(sc), dtype_code(x_np), 0.0, st())
+    kw = mask_to_words(K)
+    ref = oracle.extract(x_np, K, eb)
+    out = torch.full((n + 8,), -1, dtype=torch.int16 if dt == "u16" else torch.int32, device="cuda")
+    wsb = L.roix_extract_workspace(n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    L.roix_extract(ptr(x), dtype_code(x_np), n, ptr(kw), ptr(sc), ptr(out), n, None, ptr(ws), wsb, st())
+    s = read_sc(sc)
+    assert s.err == 0 and s.count == ref.size
+    got = out[: ref.size].cpu().numpy()
+    np.testing.assert_array_equal(got.view(np.uint16) if dt == "u16" else got, ref)
+    # capacity: writes stop at capacity and the error bit is set
+    cap = ref.size // 2
+    out2 = torch.full((n + 8,), -1, dtype=out.dtype, device="cuda")
+    sc2 = new_sc(eb)
+    L.roix_resolve(ptr(sc2), dtype_code(x_np), 0.0, st())
+    L.roix_extract(ptr(x), dtype_code(x_np), n, ptr(kw), ptr(sc2), ptr(out2), cap, None, ptr(ws), wsb, st())
+    s2 = read_sc(sc2)
+    if ref.size > cap:
+        assert s2.err & L.ERR_CAPACITY
+    got2 = out2.cpu().numpy()
+    got2 = got2.view(np.uint16) if dt == "u16" else got2
+    np.testing.assert_array_equal(got2[:cap], ref[:cap])
+    assert np.all(out2.cpu().numpy()[cap:] == -1)
