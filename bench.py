@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- ROI-extraction GB/s of input (quantise -> compact) on B200, % of HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl roix|reference]
+
+A step is one pass of the whole hot path (range [fp32] -> histogram -> Otsu threshold -> binarise +
+opening -> CCL + small-object filter -> quantise + compact) over one synthetic volume of a
+BASELINE.json config (default configs[1] = C2, 512^3 fp32; inputs > L2, so no L2 flush between
+steps).  N > 1: launched by torchrun; the volume is z-slab sharded over the ranks (NCCL), whole-job
+throughput, max-over-ranks device time.  Rank 0 prints one JSON line.
+
+--impl reference times the oracle (oracle/, plain single-threaded C + exact-rational Otsu) on the
+host cores, on a bounded sample of the same workload -- the reference arm of this tier.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ROI-extraction GB/s of input (quantize->compact) at 1/2/4/8 B200; % of HBM peak"
+UNIT = "GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--scale", type=float, default=1.0, help="profiling aid: a scaled phantom of the config")
+    ap.add_argument("--impl", default="roix", choices=["roix", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="replay the step as a CUDA graph")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, uuid):
+        self.uuid, self.rows, self.proc = uuid, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.uuid, "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([v.strip() for v in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.12)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r for r in self.rows if len(r) >= 7 and r[0].isdigit()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [int(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": int(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------- algorithmic bytes
+def alg_bytes(cfg, n, count):
+    """what the method must move per step (bytes), per stage.  s = input bytes,
+    c = code bytes, f = kept fraction; o and K written and read once each (N/8 bytes each way)."""
+    s = cfg.itemsize
+    c = 2 if cfg.dtype == "u16" else 4
+    out = {"histogram": s * n, "morph": s * n + n / 8, "label": n / 8, "extract": n / 8 + count * s + count * c}
+    if cfg.dtype == "f32":
+        out["range"] = s * n
+    return out
+
+
+def cpu_info():
+    return {"cores_available": os.cpu_count()}
+
+
+# ------------------------------------------------------------------------------- oracle timing
+def time_oracle(x_np, cfg, budget_s=15.0, max_reps=1):
+    """Time the oracle pipeline (single-threaded) on x_np; returns (seconds per pass, passes)."""
+    import oracle
+
+    oracle.build()
+    times = []
+    for _ in range(max_reps):
+        t0 = time.perf_counter()
+        oracle.pipeline(x_np, eb=cfg.eb or None, rel_eb=cfg.rel_eb or None, conn=cfg.conn, se=cfg.se,
+                        min_size=cfg.min_size, polarity=cfg.polarity)
+        times.append(time.perf_counter() - t0)
+        if sum(times) > budget_s:
+            break
+    return min(times), len(times)
+
+
+def sample_planes(cfg, target_voxels):
+    Z, Y, X = cfg.shape
+    return max(1, min(Z, int(target_voxels // (Y * X))))
+
+
+def reference_arm(args, cfg):
+    """--impl reference: the oracle on the host cores, each step a bounded sample of the workload."""
+    import synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+
+    nz = sample_planes(cfg, 6e6)
+    have_gpu = torch.cuda.is_available()
+    if have_gpu:
+        x = synth.generate(cfg, z0=0, nz=nz)
+        x_np = synth.to_numpy(x, cfg)
+    else:
+        rng = np.random.default_rng(cfg.seed)
+        x_np = (rng.normal(400, 60, (nz,) + cfg.shape[1:]).clip(0, 65535).astype(np.uint16) if cfg.dtype == "u16"
+                else rng.normal(0.02, 0.005, (nz,) + cfg.shape[1:]).astype(np.float32))
+    import oracle
+
+    oracle.build()
+    for _ in range(max(0, min(args.warmup, 1))):
+        time_oracle(x_np, cfg)
+    ts = []
+    for _ in range(args.steps):
+        t, _ = time_oracle(x_np, cfg)
+        ts.append(t)
+    per = sum(ts) / len(ts)
+    value = x_np.nbytes / per / 1e9
+    sample = "%s planes [0,%d) of %s (%d voxels, %.1f MB), whole oracle pipeline per step" % (
+        cfg.name, nz, "x".join(map(str, cfg.shape)), x_np.size, x_np.nbytes / 1e6)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u16" if cfg.dtype == "u16" else "f32",
+            "data": "synthetic", "config": {"workload": cfg.name, "shape": list(cfg.shape), "sample_planes": nz},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    import synth
+
+    cfg = synth.CONFIGS[args.config] if args.scale == 1.0 else synth.scaled(args.config, args.scale)
+    if args.impl == "reference":
+        reference_arm(args, cfg)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2602_15917_b200 import Pipeline, build
+    from paper_2602_15917_b200 import _lib as L
+
+    build.build()
+    synth.build()
+    Z, Y, X = cfg.shape
+    z0 = rank * Z // world
+    z1 = (rank + 1) * Z // world
+    x = synth.generate(cfg, z0=z0, nz=z1 - z0, device=dev)
+    torch.cuda.synchronize()
+    kw = dict(eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=cfg.polarity)
+    if world > 1:
+        from paper_2602_15917_b200.sharded import ShardedPipeline
+
+        p = ShardedPipeline(cfg.shape, cfg.dtype, z0=z0, nz=z1 - z0, group=dist.group.WORLD, device=dev, **kw)
+    else:
+        p = Pipeline(cfg.shape, cfg.dtype, device=dev, **kw)
+    res = p.run(x)                          # sizes workspaces (retry on capacity), checks err
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        p.enqueue(x)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, per-stage CUDA events on the launching stream
+    ev = []
+
+    def mark(stage):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        ev[-1].append((stage, e))
+
+    uuid = torch.cuda.get_device_properties(dev).uuid
+    uuid = "GPU-" + str(uuid) if not str(uuid).startswith("GPU-") else str(uuid)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(uuid) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for _ in range(args.steps):
+            s0 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            ev.append([("start", s0)])
+            p.enqueue(x, mark=mark)
+        end = torch.cuda.Event(enable_timing=True)
+        end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms_local = start.elapsed_time(end)
+    stage_ms = {}
+    for step in ev:
+        for (a, ea), (b, eb_) in zip(step[:-1], step[1:]):
+            stage_ms[b] = stage_ms.get(b, 0.0) + ea.elapsed_time(eb_)
+    stage_ms = {k: v / args.steps for k, v in stage_ms.items()}
+    s = p.scalars()
+    if s.err:
+        raise SystemExit("device error bits 0x%x during the timed steps" % s.err)
+    count_local = int(s.count) if world == 1 else int(p.local_count())
+    if world > 1:
+        t = torch.tensor([ms_local], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        c = torch.tensor([count_local], device=dev, dtype=torch.int64)
+        dist.all_reduce(c)
+        count = int(c.item())
+    else:
+        ms_total = ms_local
+        count = count_local
+    ms_step = ms_total / args.steps
+    n = cfg.n
+    value = cfg.nbytes / (ms_step * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    # whole-step algorithmic bytes and the dominant kernel's roofline
+    ab = alg_bytes(cfg, n // world, count_local)
+    dom = max((k for k in ab if k in stage_ms), key=lambda k: stage_ms[k])
+    achieved = ab[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic_%s.json" % cfg.name)
+    if os.path.exists(tf):
+        traffic = json.load(open(tf)).get(dom)
+    step_alg = sum(ab.values()) * world
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u16" if cfg.dtype == "u16" else "f32", "data": "synthetic",
+        "config": {"workload": cfg.name, "shape": list(cfg.shape), "input_dtype": cfg.dtype, "eb": cfg.eb,
+                   "rel_eb": cfg.rel_eb, "conn": cfg.conn, "se": cfg.se, "min_size": cfg.min_size,
+                   "polarity": "LOW" if cfg.polarity else "HIGH", "parallelism": "zslab%d" % world,
+                   "l2": "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
+        "step_roofline": {"alg_bytes_per_step": step_alg, "achieved": step_alg / (ms_step * 1e-3) / 1e9,
+                          "frac": step_alg / (ms_step * 1e-3) / 1e9 / peak},
+        "stage_ms": stage_ms, "kept": count, "kept_fraction": count / n, "spatial_reduction": n / max(count, 1),
+        "t8": int(s.t8), "gpu_launches": p.launches() * args.steps,
+    }
+    clocks = clk.summary()
+    line["clocks"] = clocks
+    # ---- end to end through the public API with host buffers (N = 1)
+    if not args.no_e2e and world == 1:
+        line["e2e"] = e2e(p, x, cfg, args)
+    # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1
+    if not args.no_cpu_baseline and world == 1 and rank == 0:
+        nz = sample_planes(cfg, 6e6)
+        x_np = synth.to_numpy(x[:nz], cfg)
+        t, reps = time_oracle(x_np, cfg)
+        line["cpu_baseline"] = {"value": x_np.nbytes / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": "%s planes [0,%d) (%d voxels, %.1f MB), whole oracle pipeline, best of %d" %
+                                          (cfg.name, nz, x_np.size, x_np.nbytes / 1e6, reps)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e(p, x, cfg, args):
+    """Same metric through the public API with HOST buffers: every step copies the input from
+    pinned host memory, runs the path, and reads the result (count, code stream, kept mask) back."""
+    import torch
+
+    from paper_2602_15917_b200 import _lib as L
+
+    xh = x.cpu().pin_memory()
+    xd = torch.empty_like(x)
+    cnt_h = torch.empty(1, dtype=torch.int64).pin_memory()
+    out_h = torch.empty(p.codes.numel(), dtype=p.codes.dtype).pin_memory()
+    mask_h = torch.empty(p.nwords, dtype=torch.int32).pin_memory()
+    stream = torch.cuda.current_stream()
+    steps = max(3, min(args.steps, 10))
+    d2h = 0
+
+    def one():
+        nonlocal d2h
+        xd.copy_(xh, non_blocking=True)
+        p.enqueue(xd)
+        off = L.Scalars.count.offset
+        sc = p.sc[off:off + 8].view(torch.int64)      # roix_scalars.count
+        cnt_h.copy_(sc, non_blocking=True)
+        stream.synchronize()
+        c = int(cnt_h[0])
+        out_h[:c].copy_(p.codes[:c], non_blocking=True)
+        mask_h.copy_(p.o[: p.nwords], non_blocking=True)
+        stream.synchronize()
+        d2h = c * p.codes.element_size() + p.nwords * 4 + 8
+
+    one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": cfg.nbytes / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": cfg.nbytes, "d2h_bytes_per_step": d2h,
+            "ms_per_step": dt * 1e3, "steps": steps}
+
+
+if __name__ == "__main__":
+    main()

@@ -87,28 +87,37 @@ class Pipeline:
         self.comp_kept = torch.empty(cap, dtype=torch.uint8, device=dev)
 
     # -------------------------------------------------------------------------------- enqueue
-    def enqueue(self, x, stream=None):
+    def enqueue(self, x, stream=None, mark=None):
         """Enqueue the whole path for x (device tensor, shape (Z, Y, X); u16 bits in int16/uint16
-        storage or float32) on `stream` (default: torch's current stream).  No host sync."""
+        storage or float32) on `stream` (default: torch's current stream).  No host sync.
+        mark(stage) is called after each stage is enqueued (the bench records CUDA events there)."""
         assert x.is_cuda and x.numel() == self.n and x.is_contiguous()
+        mark = mark or (lambda stage: None)
         st = ctypes.c_void_p((stream or torch.cuda.current_stream(self.device)).cuda_stream)
         sc, xp, n = _ptr(self.sc), _ptr(x), self.n
         L.roix_scalars_init(sc, self.eb, st)
         if self.cdtype == L.F32:
             L.roix_range(xp, n, sc, st)
+            mark("range")
         L.roix_resolve(sc, self.cdtype, self.rel_eb, st)
         self.hist.zero_()
+        mark("setup")
         L.roix_histogram(xp, self.cdtype, n, sc, _ptr(self.hist), self.nbins, st)
+        mark("histogram")
         L.roix_threshold(_ptr(self.hist), self.nbins, self.cdtype, self.polarity, sc, st)
+        mark("threshold")
         L.roix_morph(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o),
                      _ptr(self.row_runs), st)
+        mark("morph")
         out = L.LabelOut(self.o.data_ptr(), self.comp_min.data_ptr(), self.comp_size.data_ptr(),
                          self.comp_kept.data_ptr(), self.comp_cap,
                          self.labels.data_ptr() if self.labels is not None else None)
         L.roix_label(_ptr(self.o), _ptr(self.row_runs), ctypes.byref(self.geom), self.conn, self.min_size,
                      self.run_capacity, _ptr(self.label_ws), self.ws_bytes, ctypes.byref(out), sc, st)
+        mark("label")
         L.roix_extract(xp, self.cdtype, n, _ptr(self.o), sc, _ptr(self.codes), self.code_capacity, None,
                        _ptr(self.ex_ws), self.ex_ws.numel(), st)
+        mark("extract")
 
     def launches(self):
         k = sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
