@@ -161,10 +161,12 @@ roix_status roix_threshold(const uint64_t *hist, uint32_t nbins, roix_dtype dtyp
  * exist in the global volume are ignored.  NULL halos are allowed only at global volume faces.
  * row_runs (nullable, nz*ny uint32): receives the number of x-runs of o in each row -- the fused
  * first step of roix_label, which then skips its own counting pass.
+ * ws/ws_bytes (roix_morph_workspace): holds the binarised mask m between the two kernels.
  */
+roix_status roix_morph_workspace(const roix_geom *g, size_t *ws_bytes);
 roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
                        const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
-                       roix_stream_t stream);
+                       void *ws, size_t ws_bytes, roix_stream_t stream);
 
 /* Binarise planes [p0, p0+np) of the slab (slab-local plane numbers) into m_bits, each plane
  * packed from bit 0 with ceil(ny*nx/32) words -- the halo planes roix_morph consumes. */

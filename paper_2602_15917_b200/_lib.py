@@ -55,7 +55,8 @@ _SIGS = {
     "roix_quantize": (_i32, [_vp, _i32, _u64, _vp, _vp, _vp]),
     "roix_histogram": (_i32, [_vp, _i32, _u64, _vp, _vp, _u32, _vp]),
     "roix_threshold": (_i32, [_vp, _u32, _i32, _i32, _vp, _vp]),
-    "roix_morph": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "roix_morph_workspace": (_i32, [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_morph": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "roix_binarize_planes": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _u64, _vp, _vp, _vp]),
     "roix_label_workspace": (_i32, [ctypes.POINTER(Geom), _u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_label": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _u32, _u64, _u64, _vp, ctypes.c_size_t,
@@ -110,6 +111,12 @@ roix_extract = _wrap("roix_extract")
 def roix_label_workspace(geom, run_capacity):
     out = ctypes.c_size_t()
     _check(load().roix_label_workspace(ctypes.byref(geom), run_capacity, ctypes.byref(out)), "roix_label_workspace")
+    return out.value
+
+
+def roix_morph_workspace(geom):
+    out = ctypes.c_size_t()
+    _check(load().roix_morph_workspace(ctypes.byref(geom), ctypes.byref(out)), "roix_morph_workspace")
     return out.value
 
 

@@ -123,10 +123,17 @@ static roix_status check_halos(const roix_geom *g, uint32_t se, const uint32_t *
     return ROIX_OK;
 }
 
+roix_status roix_morph_workspace(const roix_geom *g, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    if (!geom_ok(g)) return invalid("geometry");
+    *ws_bytes = morph_workspace_bytes(*g);
+    return ROIX_OK;
+}
+
 roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
-                       const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
-                       roix_stream_t stream) {
-    if (!sc || !o_bits) return invalid("sc / o_bits is NULL");
+                       const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
+                       size_t ws_bytes, roix_stream_t stream) {
+    if (!sc || !o_bits || !ws) return invalid("sc / o_bits / ws is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (!geom_ok(g)) return invalid("geometry");
     if (se != 6 && se != 4) return unsupported("se must be 6 (3-D cross) or 4 (in-plane cross)");
@@ -134,7 +141,8 @@ roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint
     roix_status s = check_halos(g, se, halo_lo, halo_hi);
     if (s != ROIX_OK) return s;
     if (g->nx > (1u << 30)) return unsupported("rows longer than 2^30 voxels");
-    return cuda(launch_morph(x, (int)dtype, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, (cudaStream_t)stream),
+    if (ws_bytes < morph_workspace_bytes(*g) || !aligned16(ws)) return invalid("workspace (see roix_morph_workspace)");
+    return cuda(launch_morph(x, (int)dtype, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, ws, (cudaStream_t)stream),
                 "roix_morph");
 }
 
@@ -190,7 +198,7 @@ roix_status roix_extract(const void *x, roix_dtype dtype, uint64_t n, const uint
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (n == 0) return ROIX_OK;
     if (!x || !aligned16(x)) return invalid("x must be 16-byte aligned");
-    if (capacity > 0 && !codes_out) return invalid("codes_out is NULL");
+    if (capacity > 0 && (!codes_out || !aligned16(codes_out))) return invalid("codes_out must be 16-byte aligned");
     if (ws_bytes < extract_workspace_bytes(n)) return invalid("workspace too small (see roix_extract_workspace)");
     return cuda(launch_extract(x, (int)dtype, n, keep_bits, sc, codes_out, capacity, offset, ws, (cudaStream_t)stream),
                 "roix_extract");

@@ -1,42 +1,76 @@
 // k_extract.cu -- a1+a8 EXTRACT: uniform error-bounded quantisation (BJ north_star, G-2..G-4) of the
 // kept voxels, compacted into a dense code stream in increasing linear index (G-17).
 //
-// Single pass with a decoupled look-back scan (Merrill & Garland 2016): a CTA takes the next tile of
-// 8192 voxels (256 mask words), publishes its count, looks back over its predecessors' published
-// aggregates / inclusive prefixes (32 at a time, one warp), then quantises its kept voxels into a
-// shared-memory staging buffer and stores the tile's codes contiguously.  x is loaded only for the
-// 16-byte groups of voxels whose mask byte (u16) / nibble (fp32) is non-zero, so DRAM reads x only
-// under kept 32-byte sectors.
+// Tiles of 8192 voxels (256 mask words).  Pass 1 counts the kept voxels of every tile (reads K:
+// N/8 bytes), a scan turns the counts into output offsets, pass 2 quantises each tile's kept voxels
+// into a shared-memory staging buffer and stores them contiguously with 16-byte stores.  (A single
+// pass with a decoupled look-back was measured first: with ~1200 tiles in flight the look-back
+// walked back hundreds of tiles and serialised the CTAs; the extra N/8-byte read costs far less.)
+// x is loaded only for the 16-byte groups of voxels whose mask byte (u16) / nibble (fp32) is
+// non-zero, so DRAM reads x only under kept 32-byte sectors.
 #include "common.cuh"
 #include "kernels.cuh"
+#include "scan.cuh"
 
 namespace roix {
 
 constexpr int EX_THREADS = 256;
 constexpr int EX_WORDS = 256;            // mask words per tile
 constexpr int EX_TILE = EX_WORDS * 32;   // voxels per tile
-constexpr uint64_t ST_AGG = 1ull << 62, ST_INC = 2ull << 62, ST_MASK = 3ull << 62, VAL_MASK = ST_AGG - 1;
 
 struct ExWS {
-    unsigned long long *flags;  // [ntiles]
-    uint32_t *ticket;
+    uint32_t *tcount;   // [ntiles + 1]: per-tile counts, then exclusive offsets (scan output)
+    uint64_t *scan_tmp; // scan workspace
     uint32_t *err_snap;
 };
 
 static size_t ex_carve(void *base, uint64_t n, ExWS *w) {
     uint64_t ntiles = (n + EX_TILE - 1) / EX_TILE;
-    size_t fbytes = ((ntiles * 8) + 255) & ~(size_t)255;
+    size_t a = (((ntiles + 1) * 4) + 255) & ~(size_t)255;
+    size_t b = ((scan_tmp_elems(ntiles) * 8) + 255) & ~(size_t)255;
     if (w) {
-        w->flags = (unsigned long long *)base;
-        w->ticket = (uint32_t *)((char *)base + fbytes);
-        w->err_snap = w->ticket + 1;
+        w->tcount = (uint32_t *)base;
+        w->scan_tmp = (uint64_t *)((char *)base + a);
+        w->err_snap = (uint32_t *)((char *)base + a + b);
     }
-    return fbytes + 256;
+    return a + b + 256;
 }
 
-__global__ void k_extract_prep(ExWS w, const roix_scalars *sc) {
-    *w.ticket = 0;
-    *w.err_snap = sc->err;
+// pass 1: kept voxels per tile -- one warp per tile (256 words = 32 lanes x 2 x 16-byte loads),
+// two tiles in flight per warp; also snapshots the error word for pass 2
+__global__ void __launch_bounds__(EX_THREADS) k_extract_count(const uint32_t *__restrict__ K, uint64_t n,
+                                                              uint64_t ntiles, ExWS w, const roix_scalars *sc) {
+    const uint64_t nwords = (n + 31) / 32;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *w.err_snap = sc->err;
+    const uint64_t wpg = (uint64_t)gridDim.x * (EX_THREADS / 32);
+    const uint32_t lane = lane_id();
+    const uint4 *K4 = reinterpret_cast<const uint4 *>(K);
+    for (uint64_t t0 = (uint64_t)blockIdx.x * (EX_THREADS / 32) + (threadIdx.x >> 5); t0 < ntiles; t0 += 2 * wpg) {
+        uint32_t c[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const uint64_t t = t0 + u * wpg;
+            if (t >= ntiles) continue;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint64_t wi = t * EX_WORDS + (h * 32 + lane) * 4;   // first word of this 16-byte load
+                if (wi + 4 <= nwords) {
+                    uint4 v = __ldcs(K4 + wi / 4);
+                    c[u] += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+                } else {
+                    for (uint64_t k = wi; k < nwords && k < wi + 4; k++) c[u] += __popc(K[k]);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            uint32_t v = c[u];
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+            const uint64_t t = t0 + u * wpg;
+            if (lane == 0 && t < ntiles) w.tcount[t] = v;
+        }
+    }
 }
 
 template <typename T, typename C>
@@ -45,96 +79,72 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract(const T *__restrict__ x,
                                                         C *__restrict__ out, uint64_t capacity, const uint64_t *offset) {
     constexpr int VPL = 16 / sizeof(T);   // voxels per 16-byte group
     constexpr int GPW = 32 / VPL;         // groups per mask word
-    constexpr int CHUNKS = 32 / VPL;      // 32-group chunks per warp (a warp covers 32 words = 1024 voxels)
-    __shared__ C stage[EX_TILE];
+    constexpr int CH = 32 / VPL;          // 32-group chunks per warp (a warp covers 32 words = 1024 voxels)
+    constexpr int PADE = 16 / sizeof(C);  // staging is shifted by base % PADE so that stores are 16-byte aligned
+    __shared__ __align__(16) C stage[EX_TILE + 2 * PADE];
     __shared__ uint32_t warp_tot[EX_THREADS / 32];
-    __shared__ uint64_t s_excl;
-    __shared__ uint32_t s_tile;
+    if (*w.err_snap) return;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = atomicAdd(w.ticket, 1u);
-    __syncthreads();
-    const uint64_t tile = s_tile;
-    const bool skip = *w.err_snap != 0;
+    const uint64_t tile = blockIdx.x;
     const uint64_t nwords = (n + 31) / 32;
     const uint64_t wbase = tile * EX_WORDS + warp * 32;
-    uint32_t word = 0;
-    if (!skip && wbase + lane < nwords) word = K[wbase + lane];
+    const uint32_t word = wbase + lane < nwords ? K[wbase + lane] : 0u;
+    // issue every x load of this warp before any dependent work
+    uint32_t m[CH];
+    uint4 d[CH];
+    const uint64_t gbase = wbase * 32;  // first voxel of the warp
+#pragma unroll
+    for (int c = 0; c < CH; c++) {
+        const uint32_t g = c * 32 + lane;
+        const uint32_t wv = __shfl_sync(FULL, word, g / GPW);
+        m[c] = (wv >> ((g % GPW) * VPL)) & ((1u << VPL) - 1u);
+        d[c] = make_uint4(0, 0, 0, 0);
+        const uint64_t v0 = gbase + (uint64_t)g * VPL;
+        if (m[c] && v0 + VPL <= n) d[c] = __ldcs(reinterpret_cast<const uint4 *>(x + v0));
+    }
     const uint32_t cnt = __popc(word);
     const uint32_t incl = warp_incl_scan(cnt);
     if (lane == 31) warp_tot[warp] = incl;
+    const uint64_t base = (offset ? *offset : 0) + w.tcount[tile];
+    const uint32_t shift = (uint32_t)(base % PADE);
+    C *st = stage + shift;
     __syncthreads();
-    uint32_t wpre = 0, total = 0;
+    uint32_t run = 0, total = 0;
+#pragma unroll
     for (int k = 0; k < EX_THREADS / 32; k++) {
         uint32_t t = warp_tot[k];
-        if (k < (int)warp) wpre += t;
+        if (k < (int)warp) run += t;
         total += t;
     }
-    // publish the aggregate, look back, publish the inclusive prefix
-    if (warp == 0) {
-        uint64_t excl = 0;
-        if (tile == 0) {
-            if (lane == 0) atomicExch(&w.flags[0], ST_INC | total);
-        } else {
-            if (lane == 0) atomicExch(&w.flags[tile], ST_AGG | total);
-            int64_t p = (int64_t)tile - 1;
-            while (true) {
-                int64_t idx = p - lane;
-                uint64_t f = idx >= 0 ? *((volatile unsigned long long *)&w.flags[idx]) : ST_INC;
-                uint32_t inc = __ballot_sync(FULL, (f & ST_MASK) == ST_INC);
-                uint32_t zero = __ballot_sync(FULL, (f & ST_MASK) == 0);
-                int L = inc ? __ffs(inc) - 1 : 31;
-                uint32_t upto = L == 31 ? FULL : ((2u << L) - 1u);
-                if (zero & upto) continue;  // a predecessor has not published yet
-                uint64_t v = (lane <= (uint32_t)L) ? (f & VAL_MASK) : 0;
-#pragma unroll
-                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
-                excl += v;
-                if (inc) break;
-                p -= 32;
-            }
-            __threadfence();
-            if (lane == 0) atomicExch(&w.flags[tile], ST_INC | (excl + total));
-        }
-        if (lane == 0) s_excl = excl;
-    }
-    __syncthreads();
-    if (skip) return;
-    const uint64_t excl = s_excl;
-    const uint64_t base = (offset ? *offset : 0) + excl;
     const QP q = load_qp(sc);
     uint32_t err = 0;
-    // quantise the kept voxels of this warp's 32 words into stage[wpre ...]
-    uint32_t run = wpre;
-    const uint64_t gbase = wbase * 32;  // first voxel of the warp
-    for (int c = 0; c < CHUNKS; c++) {
-        const uint32_t g = c * 32 + lane;                       // group within the warp
-        const uint32_t wsrc = g / GPW, sh = (g % GPW) * VPL;
-        const uint32_t wv = __shfl_sync(FULL, word, wsrc);
-        const uint32_t m = (wv >> sh) & ((1u << VPL) - 1u);
-        const uint32_t pc = __popc(m);
+#pragma unroll
+    for (int c = 0; c < CH; c++) {
+        const uint32_t pc = __popc(m[c]);
         const uint32_t pos = warp_incl_scan(pc) - pc + run;
-        run += __shfl_sync(FULL, pos + pc, 31) - run;
-        if (m) {
+        run = __shfl_sync(FULL, pos + pc, 31);
+        if (m[c]) {
+            const uint32_t g = c * 32 + lane;
             const uint64_t v0 = gbase + (uint64_t)g * VPL;
             uint32_t p = pos;
             if (v0 + VPL <= n) {
-                uint4 d = __ldcs(reinterpret_cast<const uint4 *>(x + v0));
                 if constexpr (sizeof(T) == 2) {
-                    uint32_t ww[4] = {d.x, d.y, d.z, d.w};
+                    uint32_t ww[4] = {d[c].x, d[c].y, d[c].z, d[c].w};
 #pragma unroll
                     for (int k = 0; k < 8; k++)
-                        if (m >> k & 1) stage[p++] = (C)code_u16((ww[k >> 1] >> ((k & 1) * 16)) & 0xffffu, q, err);
+                        if (m[c] >> k & 1) st[p++] = (C)code_u16((ww[k >> 1] >> ((k & 1) * 16)) & 0xffffu, q, err);
                 } else {
-                    float ff[4] = {__uint_as_float(d.x), __uint_as_float(d.y), __uint_as_float(d.z), __uint_as_float(d.w)};
+                    float ff[4] = {__uint_as_float(d[c].x), __uint_as_float(d[c].y), __uint_as_float(d[c].z),
+                                   __uint_as_float(d[c].w)};
 #pragma unroll
                     for (int k = 0; k < 4; k++)
-                        if (m >> k & 1) stage[p++] = (C)code_f32(ff[k], q, err);
+                        if (m[c] >> k & 1) st[p++] = (C)code_f32(ff[k], q, err);
                 }
             } else {
                 for (int k = 0; k < VPL; k++)
-                    if (m >> k & 1) {
-                        if constexpr (sizeof(T) == 2) stage[p++] = (C)code_u16(x[v0 + k], q, err);
-                        else stage[p++] = (C)code_f32(x[v0 + k], q, err);
+                    if (m[c] >> k & 1) {
+                        if constexpr (sizeof(T) == 2) st[p++] = (C)code_u16(x[v0 + k], q, err);
+                        else st[p++] = (C)code_f32(x[v0 + k], q, err);
                     }
             }
         }
@@ -142,9 +152,20 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract(const T *__restrict__ x,
     if (base + total > capacity) err |= ROIX_ERR_CAPACITY;
     if (err) set_err(sc, err);
     __syncthreads();
+    // store [base, base + lim): scalar head up to the 16-byte boundary, 16-byte body, scalar tail
     const uint64_t lim = base < capacity ? min((uint64_t)total, capacity - base) : 0;
-    for (uint64_t j = threadIdx.x; j < lim; j += EX_THREADS) out[base + j] = stage[j];
-    if (tile == ntiles - 1 && threadIdx.x == 0) atomicAdd((unsigned long long *)&sc->count, excl + total);
+    const uint32_t head = (uint32_t)min((uint64_t)((PADE - shift) % PADE), lim);
+    if (threadIdx.x < head) out[base + threadIdx.x] = st[threadIdx.x];
+    const uint64_t nvec = (lim - head) / PADE;
+    const uint4 *sv = reinterpret_cast<const uint4 *>(st + head);   // 16-byte aligned: (shift + head) % PADE == 0
+    uint4 *ov = reinterpret_cast<uint4 *>(out + base + head);
+    for (uint64_t j = threadIdx.x; j < nvec; j += EX_THREADS) __stcs(ov + j, sv[j]);
+    for (uint64_t j = head + nvec * PADE + threadIdx.x; j < lim; j += EX_THREADS) out[base + j] = st[j];
+}
+
+// count: total kept voxels (scan total) added to sc->count
+__global__ void k_extract_total(const uint64_t *total, const ExWS w, roix_scalars *sc) {
+    if (*w.err_snap == 0) sc->count += *total;
 }
 
 }  // namespace roix
@@ -158,15 +179,17 @@ cudaError_t launch_extract(const void *x, int dtype, uint64_t n, const uint32_t 
     ExWS w;
     ex_carve(ws, n, &w);
     const uint64_t ntiles = (n + EX_TILE - 1) / EX_TILE;
-    cudaError_t e = cudaMemsetAsync(w.flags, 0, ntiles * 8, st);
-    if (e != cudaSuccess) return e;
-    k_extract_prep<<<1, 1, 0, st>>>(w, sc);
     if (ntiles > 0x7fffffffull) return cudaErrorInvalidValue;
+    uint64_t cg = (uint64_t)num_sms() * 8, need = (ntiles + 15) / 16;
+    k_extract_count<<<(unsigned)(need < cg ? (need ? need : 1) : cg), EX_THREADS, 0, st>>>(keep_bits, n, ntiles, w, sc);
+    cudaError_t e = scan_u32(w.tcount, w.tcount, ntiles, w.scan_tmp, st);
+    if (e != cudaSuccess) return e;
     if (dtype == ROIX_U16)
         k_extract<uint16_t, uint16_t><<<(unsigned)ntiles, EX_THREADS, 0, st>>>(
             (const uint16_t *)x, n, ntiles, keep_bits, w, sc, (uint16_t *)codes, capacity, offset);
     else
         k_extract<float, int32_t><<<(unsigned)ntiles, EX_THREADS, 0, st>>>((const float *)x, n, ntiles, keep_bits, w, sc,
                                                                           (int32_t *)codes, capacity, offset);
+    k_extract_total<<<1, 1, 0, st>>>(scan_total_ptr(w.scan_tmp, ntiles), w, sc);
     return cudaGetLastError();
 }

@@ -28,8 +28,13 @@ struct LabelWS {
     uint32_t *x0, *x1, *rrow, *parent, *cidx;  // [cap]
     uint64_t *size;       // [cap]
     uint8_t *kept;        // [cap]
-    uint64_t *ctr;        // [4]: 0 n_runs, 1 n_roots, 2 n_kept
+    uint64_t *ctr;        // [4]: 0 n_runs, 1 n_cross_pairs, 2 n_kept
+    uint2 *pairs;         // [pair_cap]: run pairs that cross union blocks
+    uint64_t pair_cap;
 };
+
+constexpr int UB_RUNS = 16384;    // runs per union block (their parents live in shared memory)
+constexpr int UB_THREADS = 512;
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
@@ -46,6 +51,8 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
     size_t o_x0 = take(cap * 4), o_x1 = take(cap * 4), o_rw = take(cap * 4), o_pa = take(cap * 4),
            o_ci = take((cap + 1) * 4);
     size_t o_sz = take(cap * 8), o_kp = take(cap), o_ct = take(4 * 8);
+    const uint64_t pair_cap = 2 * cap + 1024;
+    size_t o_pr = take(pair_cap * 8);
     if (ws) {
         char *b = (char *)base;
         ws->row_runs = (uint32_t *)(b + o_rr);
@@ -59,6 +66,8 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
         ws->size = (uint64_t *)(b + o_sz);
         ws->kept = (uint8_t *)(b + o_kp);
         ws->ctr = (uint64_t *)(b + o_ct);
+        ws->pairs = (uint2 *)(b + o_pr);
+        ws->pair_cap = pair_cap;
     }
     return off;
 }
@@ -108,49 +117,96 @@ __global__ void k_count_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nw
 __global__ void k_runs_total(const uint64_t *total, uint64_t cap, LabelWS W, roix_scalars *sc) {
     uint64_t t = *total;
     W.ctr[0] = t > cap ? 0 : t;  // over capacity: every later step sees no runs
-    W.ctr[1] = 0;
+    W.ctr[1] = 0;  // cross-block pairs
     W.ctr[2] = 0;
     sc->n_runs = t;
     if (t > cap) set_err(sc, ROIX_ERR_CAPACITY);
 }
 
-__global__ void k_extract_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nwords, LabelWS W,
-                               roix_scalars *sc) {
+// Warp per group of RIF consecutive rows: the offsets and (for rows of <= 128 words) all words of
+// the RIF rows are loaded before any of them is processed, so each warp keeps RIF rows of loads in
+// flight.  Longer rows are streamed 32 words at a time.
+constexpr int RIF = 4, RW = 4;   // rows in flight per warp; words per lane kept in registers per row
+__device__ __forceinline__ void runs_of_chunk(uint32_t cw, uint32_t next_lane31, uint32_t &carry, uint32_t k,
+                                              uint32_t b0, uint32_t &sbase, uint32_t &ebase, uint32_t r,
+                                              uint32_t *__restrict__ x0, uint32_t *__restrict__ x1,
+                                              uint32_t *__restrict__ rrow) {
+    const uint32_t lane = lane_id();
+    uint32_t prev = __shfl_up_sync(FULL, cw, 1);
+    if (lane == 0) prev = carry;
+    uint32_t next = __shfl_down_sync(FULL, cw, 1);
+    if (lane == 31) next = next_lane31;
+    carry = __shfl_sync(FULL, cw, 31);
+    uint32_t starts = cw & ~((cw << 1) | (prev >> 31));
+    uint32_t ends = cw & ~((cw >> 1) | (next << 31));
+    const uint32_t ns = __popc(starts), ne = __popc(ends);
+    const uint32_t is = warp_incl_scan(ns) - ns, ie = warp_incl_scan(ne) - ne;
+    uint32_t ps = b0 + sbase + is, pe = b0 + ebase + ie;
+    while (starts) {
+        const uint32_t bb = __ffs(starts) - 1;
+        starts &= starts - 1;
+        x0[ps] = 32 * k + bb;
+        rrow[ps] = r;
+        ps++;
+    }
+    while (ends) {
+        const uint32_t bb = __ffs(ends) - 1;
+        ends &= ends - 1;
+        x1[pe++] = 32 * k + bb + 1;
+    }
+    sbase += __shfl_sync(FULL, is + ns, 31);
+    ebase += __shfl_sync(FULL, ie + ne, 31);
+}
+
+__global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nwords,
+                                                      LabelWS W, roix_scalars *sc) {
     if (get_err(sc)) return;
     const uint64_t rows = G.nz * G.ny;
+    const uint64_t ngroups = (rows + RIF - 1) / RIF;
     const uint64_t wpg = (uint64_t)gridDim.x * (blockDim.x >> 5);
     const uint32_t lane = lane_id();
-    for (uint64_t r = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += wpg) {
-        uint32_t base = W.row_start[r];
-        if (W.row_start[r + 1] == base) continue;
-        uint32_t carry = 0, sbase = 0, ebase = 0;
-        for (uint32_t k0 = 0; k0 < G.W; k0 += 32) {
-            uint32_t k = k0 + lane;
-            uint32_t w = k < G.W ? row_word_safe(o, G, r, k, nwords) : 0u;
-            uint32_t prev = __shfl_up_sync(FULL, w, 1);
-            if (lane == 0) prev = carry;
-            uint32_t next = __shfl_down_sync(FULL, w, 1);
-            if (lane == 31) next = (k + 1 < G.W) ? row_word_safe(o, G, r, k + 1, nwords) : 0u;
-            carry = __shfl_sync(FULL, w, 31);
-            uint32_t starts = w & ~((w << 1) | (prev >> 31));
-            uint32_t ends = w & ~((w >> 1) | (next << 31));
-            uint32_t ns = __popc(starts), ne = __popc(ends);
-            uint32_t is = warp_incl_scan(ns) - ns, ie = warp_incl_scan(ne) - ne;
-            uint32_t ps = base + sbase + is, pe = base + ebase + ie;
-            while (starts) {
-                uint32_t b = __ffs(starts) - 1;
-                starts &= starts - 1;
-                W.x0[ps] = 32 * k + b;
-                W.rrow[ps] = (uint32_t)r;
-                ps++;
+    uint32_t *__restrict__ x0 = W.x0;
+    uint32_t *__restrict__ x1 = W.x1;
+    uint32_t *__restrict__ rrow = W.rrow;
+    const uint32_t *__restrict__ rs = W.row_start;
+    const bool regs = G.W <= 32 * RW;
+    for (uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gi < ngroups; gi += wpg) {
+        const uint64_t r0 = gi * RIF;
+        // offsets of the group's rows: lanes 0..RIF load row_start[r0 .. r0+RIF]
+        uint32_t off = 0;
+        if (lane <= RIF && r0 + lane <= rows) off = rs[r0 + lane];
+        uint32_t wv[RIF][RW];
+#pragma unroll
+        for (int q = 0; q < RIF; q++) {
+            const uint32_t a = __shfl_sync(FULL, off, q), b = __shfl_sync(FULL, off, q + 1);
+            const bool live = regs && r0 + q < rows && b != a;
+#pragma unroll
+            for (int h = 0; h < RW; h++) {
+                const uint32_t k = h * 32 + lane;
+                wv[q][h] = (live && k < G.W) ? row_word_safe(o, G, r0 + q, k, nwords) : 0u;
             }
-            while (ends) {
-                uint32_t b = __ffs(ends) - 1;
-                ends &= ends - 1;
-                W.x1[pe++] = 32 * k + b + 1;
+        }
+#pragma unroll
+        for (int q = 0; q < RIF; q++) {
+            const uint64_t r = r0 + q;
+            const uint32_t b0 = __shfl_sync(FULL, off, q), b1 = __shfl_sync(FULL, off, q + 1);
+            if (r >= rows || b1 == b0) continue;
+            uint32_t carry = 0, sbase = 0, ebase = 0;
+            if (regs) {
+#pragma unroll
+                for (int h = 0; h < RW; h++) {
+                    if (h * 32 >= (int)G.W) break;
+                    const uint32_t nxt = h + 1 < RW ? __shfl_sync(FULL, wv[q][h + 1], 0) : 0u;
+                    runs_of_chunk(wv[q][h], nxt, carry, h * 32 + lane, b0, sbase, ebase, (uint32_t)r, x0, x1, rrow);
+                }
+            } else {
+                for (uint32_t k0 = 0; k0 < G.W; k0 += 32) {
+                    const uint32_t k = k0 + lane;
+                    const uint32_t cw = k < G.W ? row_word_safe(o, G, r, k, nwords) : 0u;
+                    const uint32_t nxt = (k0 + 32 < G.W) ? row_word_safe(o, G, r, k0 + 32, nwords) : 0u;
+                    runs_of_chunk(cw, nxt, carry, k, b0, sbase, ebase, (uint32_t)r, x0, x1, rrow);
+                }
             }
-            sbase += __shfl_sync(FULL, is + ns, 31);
-            ebase += __shfl_sync(FULL, ie + ne, 31);
         }
     }
 }
@@ -192,15 +248,6 @@ __device__ void unite(uint32_t *parent, uint32_t a, uint32_t b) {
     }
 }
 
-__global__ void k_init_parent(LabelWS W, roix_scalars *sc) {
-    if (get_err(sc)) return;
-    const uint64_t n = W.ctr[0];
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        W.parent[i] = (uint32_t)i;
-        W.size[i] = 0;
-    }
-}
-
 struct Nb {
     int dz, dy, ext;
 };
@@ -215,28 +262,113 @@ __constant__ Nb c_nb[5][4] = {
 };
 __constant__ int c_nnb[5] = {1, 1, 2, 4, 4};
 
-__global__ void k_union(LGeo G, int ci, LabelWS W, roix_scalars *sc) {
+__device__ __forceinline__ uint32_t sfind(uint32_t *lp, uint32_t x) {
+    uint32_t p = lp[x];
+    while (p != x) {
+        uint32_t gp = lp[p];
+        if (gp != p) lp[x] = gp;
+        x = p;
+        p = gp;
+    }
+    return x;
+}
+
+__device__ __forceinline__ void sunite(uint32_t *lp, uint32_t a, uint32_t b) {
+    while (true) {
+        a = sfind(lp, a);
+        b = sfind(lp, b);
+        if (a == b) return;
+        if (a < b) {
+            uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        uint32_t old = atomicMin(&lp[a], b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+// Union, phase 1: a CTA owns the runs [base, base + UB_RUNS) and their parent pointers in shared
+// memory.  Neighbour pairs inside the block are united there; pairs reaching an earlier block are
+// queued.  The block's runs then point (globally) at their block-local root.
+__global__ void __launch_bounds__(UB_THREADS) k_union_local(LGeo G, int ci, LabelWS W, roix_scalars *sc) {
+    extern __shared__ uint32_t lp[];
     if (get_err(sc)) return;
     const uint64_t n = W.ctr[0];
+    const uint64_t base = (uint64_t)blockIdx.x * UB_RUNS;
+    if (base >= n) return;
+    const uint32_t cnt = (uint32_t)min((uint64_t)UB_RUNS, n - base);
+    for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) lp[k] = k;
+    __syncthreads();
     const int nnb = c_nnb[ci];
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t r = W.rrow[i];
-        const int64_t z = r / G.ny, y = r % G.ny;
-        const uint32_t a0 = W.x0[i], a1 = W.x1[i];
-        for (int q = 0; q < nnb; q++) {
-            const Nb nb = c_nb[ci][q];
-            const int64_t zz = z + nb.dz, yy = y + nb.dy;
-            if (zz < 0 || yy < 0 || yy >= (int64_t)G.ny) continue;
-            const uint64_t nr = (uint64_t)zz * G.ny + yy;
-            uint32_t lo = W.row_start[nr], hi = W.row_start[nr + 1];
-            // first run j with x1[j] + ext > a0 (x1 is increasing along a row)
-            while (lo < hi) {
-                uint32_t mid = (lo + hi) >> 1;
-                if (W.x1[mid] + nb.ext > a0) hi = mid;
-                else lo = mid + 1;
+    for (uint32_t k0 = 0; k0 < cnt; k0 += blockDim.x) {
+        const uint32_t k = k0 + threadIdx.x;
+        const bool act = k < cnt;
+        uint2 pend[8];
+        int np = 0;
+        if (act) {
+            const uint64_t i = base + k;
+            const uint32_t r = W.rrow[i];
+            const int64_t z = r / G.ny, y = r % G.ny;
+            const uint32_t a0 = W.x0[i], a1 = W.x1[i];
+            for (int q = 0; q < nnb; q++) {
+                const Nb nb = c_nb[ci][q];
+                const int64_t zz = z + nb.dz, yy = y + nb.dy;
+                if (zz < 0 || yy < 0 || yy >= (int64_t)G.ny) continue;
+                const uint64_t nr = (uint64_t)zz * G.ny + yy;
+                uint32_t lo = W.row_start[nr], hi = W.row_start[nr + 1];
+                const uint32_t end = hi;
+                while (lo < hi) {
+                    uint32_t mid = (lo + hi) >> 1;
+                    if (W.x1[mid] + nb.ext > a0) hi = mid;
+                    else lo = mid + 1;
+                }
+                for (uint32_t j = lo; j < end && W.x0[j] < a1 + nb.ext; j++) {
+                    if (j >= base) sunite(lp, k, (uint32_t)(j - base));
+                    else if (np < 8) pend[np++] = make_uint2((uint32_t)i, j);
+                    else {  // flush (rare: more than 8 cross-block overlaps of one run)
+                        unsigned long long at = atomicAdd((unsigned long long *)&W.ctr[1], 8ull);
+                        for (int t = 0; t < 8; t++)
+                            if (at + t < W.pair_cap) W.pairs[at + t] = pend[t];
+                        np = 0;
+                        pend[np++] = make_uint2((uint32_t)i, j);
+                    }
+                }
             }
-            for (uint32_t j = lo; j < W.row_start[nr + 1] && W.x0[j] < a1 + nb.ext; j++) unite(W.parent, (uint32_t)i, j);
         }
+        // warp-aggregated append of the queued cross-block pairs
+        const uint32_t tot = warp_incl_scan((uint32_t)np);
+        unsigned long long at = 0;
+        const uint32_t wsum = __shfl_sync(FULL, tot, 31);
+        if (lane_id() == 31 && wsum) at = atomicAdd((unsigned long long *)&W.ctr[1], (unsigned long long)wsum);
+        at = __shfl_sync(FULL, at, 31) + (tot - np);
+        for (int t = 0; t < np; t++)
+            if (at + t < W.pair_cap) W.pairs[at + t] = pend[t];
+    }
+    __syncthreads();
+    for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+        uint32_t r = k, p = lp[r];
+        while (p != r) {
+            r = p;
+            p = lp[r];
+        }
+        W.parent[base + k] = (uint32_t)(base + r);
+        W.size[base + k] = 0;
+    }
+}
+
+// Union, phase 2: the queued cross-block pairs, lock-free union-by-min on the global parents.
+__global__ void k_union_cross(LabelWS W, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t np = W.ctr[1];
+    if (np > W.pair_cap) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_err(sc, ROIX_ERR_CAPACITY);
+        return;
+    }
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint2 pr = W.pairs[i];
+        unite(W.parent, pr.x, pr.y);
     }
 }
 
@@ -362,8 +494,18 @@ cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const
     k_runs_total<<<1, 1, 0, st>>>(scan_total_ptr(W.scan_tmp, rows), cap, W, sc);
     const int runs_grid = num_sms() * 8;
     k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, sc);
-    k_init_parent<<<runs_grid, 256, 0, st>>>(W, sc);
-    k_union<<<runs_grid, 256, 0, st>>>(G, ci, W, sc);
+    {
+        static bool attr = false;
+        if (!attr) {
+            if ((e = cudaFuncSetAttribute(k_union_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          UB_RUNS * 4)) != cudaSuccess)
+                return e;
+            attr = true;
+        }
+        const uint64_t nub = (cap + UB_RUNS - 1) / UB_RUNS;
+        k_union_local<<<(unsigned)nub, UB_THREADS, UB_RUNS * 4, st>>>(G, ci, W, sc);
+        k_union_cross<<<runs_grid, 256, 0, st>>>(W, sc);
+    }
     k_flatten_sizes<<<runs_grid, 256, 0, st>>>(W, sc);
     k_root_flags<<<runs_grid, 256, 0, st>>>(W, sc);
     if ((e = scan_u32_dev(W.cidx, W.cidx, W.ctr, cap, W.scan_tmp, st)) != cudaSuccess) return e;

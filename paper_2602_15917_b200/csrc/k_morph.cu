@@ -1,18 +1,17 @@
-// k_morph.cu -- a4 BINARISE (Eq. 2) fused with a5 MORPHOLOGICAL CLEANUP (reading G-11:
-// one opening o = dilate(erode(m)), radius-1 cross, out-of-volume neighbours ignored).
+// k_morph.cu -- a4 BINARISE (Eq. 2) and a5 MORPHOLOGICAL CLEANUP (reading G-11: one
+// opening o = dilate(erode(m)), radius-1 cross, out-of-volume neighbours ignored).
 //
-// Layout in shared memory: one row of X voxels = W = ceil(X/32) words, bit x%32 of word x/32,
-// plus a guard word on each side (row stride WS = W + 2).  m rows carry guard/pad bits = 1 (erosion
-// border 1); e and o rows carry 0 (dilation border 0).  Erosion and dilation are word-wise
-// AND / OR of the row, its +-1 x-shifts (funnel shifts with the neighbour words) and the
-// neighbouring rows / planes.
-//
-//  k_morph3d (se = 6): a CTA owns a band of TY rows of every plane of a z-chunk and marches along z
-//    with rings of 3 m-planes and 3 e-planes; x is read once per voxel (plus 2 halo rows per band
-//    side, mostly L2 hits from the neighbouring band, and 2 halo planes per chunk side).
-//  k_morph2d (se = 4, in-plane): a CTA owns a contiguous range of rows and marches along them with
-//    rings of m and e rows; the output rows of one step are contiguous bits of o.
-// Both count the x-runs of every output row (fused first step of a6 CCL).
+//  k_binarize: a pure stream over x (16-byte loads, one mask word per lane, coalesced 128-byte
+//    stores) writing the packed mask m.
+//  k_open3d (se = 6): a CTA owns a band of TY rows of every plane of a z-chunk and marches along z
+//    with rings of 3 m-planes and 3 e-planes in shared memory; m is re-read only for 2 halo rows per
+//    band side and 2 halo planes per chunk side (bits: 1/16 of the input bytes for u16).
+//  k_open2d (se = 4, in-plane): a CTA owns a range of rows and marches along them.
+// Shared-memory rows: W = ceil(X/32) words plus a guard word on each side (stride WS = W + 2); m rows
+// carry guard/pad bits = 1 (erosion border 1), e/o rows 0 (dilation border 0).  Erosion and
+// dilation are word-wise AND / OR of the row, its +-1 x-shifts (funnel shifts across the
+// neighbouring words) and the neighbouring rows / planes.  Both open kernels count the x-runs of
+// every output row (the fused first step of a6 CCL).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -20,11 +19,14 @@ namespace roix {
 
 struct MorphArgs {
     uint64_t nz, ny, nx, z0, gz;
+    const uint32_t *m;       // binarised slab, linear bits
+    uint64_t m_words;
     uint32_t W, WS;          // words per row, row stride in shared memory
     int TY;                  // 3-D: rows per band
     uint64_t zchunk;         // 3-D: planes per CTA
     uint64_t rows_per_cta;   // 2-D: rows per CTA
     int aligned_out;         // 1: plain stores of whole words; 0: atomicOr into zeroed o
+    int async;               // 3-D: rows are whole 16-byte units (X % 128 == 0): cp.async prefetch
     const uint32_t *halo_lo, *halo_hi;
     uint32_t *o;
     uint32_t *row_runs;
@@ -125,22 +127,6 @@ __device__ void binarize_row(const T *__restrict__ xrow, uint64_t X, uint32_t W,
     __syncwarp();
 }
 
-// Warp-level: row y of a packed plane (bits from 0) -> dst words, pad bits 1 (an m row of a halo).
-__device__ void halo_row(const uint32_t *plane, uint64_t ny, uint64_t X, uint64_t y, uint32_t W, uint32_t *dst) {
-    const uint64_t pw = (ny * X + 31) / 32;
-    const uint64_t b0 = y * X;
-    const uint32_t sh = (uint32_t)(b0 & 31);
-    for (uint32_t k = lane_id(); k < W; k += 32) {
-        uint64_t wi = b0 / 32 + k;
-        uint32_t lo = plane[wi], hi = (wi + 1 < pw) ? plane[wi + 1] : 0u;
-        dst[k] = __funnelshift_r(lo, hi, sh);
-    }
-    __syncwarp();
-    uint32_t tail = (uint32_t)(X - 32ull * (W - 1));
-    if (lane_id() == 0 && tail < 32) dst[W - 1] |= ~low_mask(tail);
-    __syncwarp();
-}
-
 __device__ __forceinline__ void fill_row(uint32_t *dst, uint32_t W, uint32_t v) {
     for (uint32_t k = lane_id(); k < W; k += 32) dst[k] = v;
     __syncwarp();
@@ -183,51 +169,156 @@ __device__ __forceinline__ void write_row_atomic(uint32_t *o, uint64_t bitpos, u
     if (sh) atomicOr(&o[(b >> 5) + 1], w >> (32 - sh));
 }
 
-// ------------------------------------------------------------------------------------ 3-D kernel
+
+// ------------------------------------------------------------------------------------ binarise
+// One warp iteration = 32 mask words = 1024 voxels; lane l loads the 16-byte groups c*32 + l
+// (c < CH), packs their VPL-bit masks into P = sum_c b_c << (c VPL), then lane j gathers word j from
+// the GPW lanes that hold its groups.
 template <typename T>
-__global__ void __launch_bounds__(256) k_morph3d(const T *__restrict__ x, MorphArgs A, roix_scalars *sc) {
-    extern __shared__ uint32_t smem[];
+__global__ void __launch_bounds__(256) k_binarize(const T *__restrict__ x, uint64_t n, roix_scalars *sc,
+                                                  uint32_t *__restrict__ m) {
     if (get_err(sc)) return;
+    constexpr int VPL = Cmp<T>::VPL, CH = 32 / VPL, GPW = 32 / VPL;
     const Cmp<T> cmp(sc);
+    const uint32_t lane = lane_id();
+    const uint64_t iters = (n + 1023) / 1024;
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
+    const uint64_t nwords = (n + 31) / 32;
+    for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < iters; it += wstride) {
+        const uint64_t g0 = it * 32 * CH;  // first 16-byte group of the iteration
+        uint32_t P = 0;
+        if ((it + 1) * 1024 <= n) {
+            uint4 v[CH];
+#pragma unroll
+            for (int c = 0; c < CH; c++) v[c] = __ldcs(x4 + g0 + c * 32 + lane);
+#pragma unroll
+            for (int c = 0; c < CH; c++) P |= cmp.bits(v[c]) << (c * VPL);
+        } else {
+            for (int c = 0; c < CH; c++) {
+                const uint64_t v0 = (g0 + c * 32 + lane) * VPL;
+                uint32_t b = 0;
+                if (v0 + VPL <= n) b = cmp.bits(__ldcs(x4 + g0 + c * 32 + lane));
+                else
+                    for (int k = 0; k < VPL; k++)
+                        if (v0 + k < n) b |= cmp.bit1(x[v0 + k]) << k;
+                P |= b << (c * VPL);
+            }
+        }
+        // word j = chunk c = j / VPL, groups (j % VPL) * GPW + i of that chunk
+        const uint32_t c = lane / VPL, src0 = (lane % VPL) * GPW;
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 0; i < GPW; i++) {
+            uint32_t q = __shfl_sync(FULL, P, src0 + i);
+            w |= ((q >> (c * VPL)) & ((1u << VPL) - 1u)) << (i * VPL);
+        }
+        const uint64_t wi = it * 32 + lane;
+        if (wi < nwords) m[wi] = w;
+    }
+}
+
+// Warp-level: row words of a linear bit array starting at bit `bit0` (X bits), pad bits = 1 (m rows).
+__device__ __forceinline__ void load_m_row(const uint32_t *__restrict__ src, uint64_t src_words, uint64_t bit0,
+                                           uint64_t X, uint32_t W, uint32_t *dst) {
+    const uint32_t sh = (uint32_t)(bit0 & 31);
+    const uint64_t w0 = bit0 >> 5;
+    const uint32_t tail = (uint32_t)(X - 32ull * (W - 1));
+    for (uint32_t k = lane_id(); k < W; k += 32) {
+        const uint64_t wi = w0 + k;
+        uint32_t v = src[wi];
+        if (sh) v = __funnelshift_r(v, (wi + 1 < src_words) ? src[wi + 1] : 0u, sh);
+        if (k == W - 1 && tail < 32) v |= ~low_mask(tail);
+        dst[k] = v;
+    }
+}
+
+// ------------------------------------------------------------------------------------ 3-D opening
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr int MSLOTS = 8, PF = 4;  // m ring slots; planes prefetched ahead (PF + 3 <= MSLOTS)
+
+// Rings: m has MSLOTS plane slots (m(p+1..p+PF) are in flight with cp.async while e(p-1) and o(p-2)
+// are computed), e has 3.  Row data starts 4 words into its slot (16-byte aligned for cp.async), with the
+// guard words at data[-1] and data[W].  A.async: rows are whole 16-byte units in global memory
+// (X % 128 == 0); otherwise rows are loaded synchronously with funnel shifts.
+__global__ void __launch_bounds__(256) k_open3d(MorphArgs A, roix_scalars *sc) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    if (get_err(sc)) return;
     const int TY = A.TY;
-    const uint32_t W = A.W, WS = A.WS;
+    const uint32_t W = A.W, WS = A.WS;             // WS: multiple of 4, >= W + 8
     const int MR = TY + 4, ER = TY + 2;            // m rows y0-2.., e rows y0-1..
-    uint32_t *mring = smem;                          // [3][MR][WS]
-    uint32_t *ering = mring + 3 * MR * WS;           // [3][ER][WS]
-    uint32_t *stage = ering + 3 * ER * WS;           // [8][WS]
+    uint32_t *mring = smem;                          // [MSLOTS][MR][WS]
+    uint32_t *ering = mring + MSLOTS * MR * WS;      // [3][ER][WS]
     const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    uint32_t *mystage = stage + warp * WS;
     const int64_t y0 = (int64_t)blockIdx.x * TY;
     const int64_t zs = (int64_t)blockIdx.y * A.zchunk;
     const int64_t ze = min((int64_t)A.nz, zs + (int64_t)A.zchunk);
     const int64_t Y = A.ny, X = A.nx;
     if (zs >= ze) return;
-    // guards: m rows 1 (erosion border), e rows 0
-    for (int i = threadIdx.x; i < 3 * MR; i += blockDim.x) {
-        mring[i * WS] = FULL;
-        mring[i * WS + W + 1] = FULL;
+    for (int i = threadIdx.x; i < MSLOTS * MR; i += blockDim.x) {
+        mring[i * WS + 3] = FULL;
+        mring[i * WS + 4 + W] = FULL;
     }
     for (int i = threadIdx.x; i < 3 * ER; i += blockDim.x) {
-        ering[i * WS] = 0;
-        ering[i * WS + W + 1] = 0;
+        ering[i * WS + 3] = 0;
+        ering[i * WS + 4 + W] = 0;
     }
     __syncthreads();
-    auto mrow = [&](int64_t p, int r) { return mring + ((p + 3) % 3 * MR + r) * WS + 1; };
-    auto erow = [&](int64_t p, int r) { return ering + ((p + 3) % 3 * ER + r) * WS + 1; };
+    auto mrow = [&](int64_t p, int r) { return mring + (((p + MSLOTS) & (MSLOTS - 1)) * MR + r) * WS + 4; };
+    auto erow = [&](int64_t p, int r) { return ering + ((p + 3) % 3 * ER + r) * WS + 4; };
     const uint64_t plane_w = (A.ny * A.nx + 31) / 32;
-    for (int64_t p = zs - 2; p <= ze + 1; p++) {
-        // 1. m(p), rows y0-2 .. y0+TY+1
+    const uint32_t tail = (uint32_t)(X - 32ll * (W - 1));
+    const bool async = A.async;
+    // enqueue the rows of m(p) (cp.async, or synchronous loads in the generic path)
+    auto fetch = [&](int64_t p) {
         const int64_t gp = (int64_t)A.z0 + p;
         for (int r = warp; r < MR; r += nw) {
             const int64_t y = y0 - 2 + r;
             uint32_t *dst = mrow(p, r);
-            if (y < 0 || y >= Y || gp < 0 || gp >= (int64_t)A.gz) fill_row(dst, W, FULL);
-            else if (p < 0) halo_row(A.halo_lo + (uint64_t)(p + 2) * plane_w, A.ny, A.nx, y, W, dst);
-            else if (p >= (int64_t)A.nz) halo_row(A.halo_hi + (uint64_t)(p - A.nz) * plane_w, A.ny, A.nx, y, W, dst);
-            else binarize_row(x + ((uint64_t)p * A.ny + y) * A.nx, A.nx, W, cmp, dst, mystage);
+            const uint32_t *src;
+            uint64_t bit0, swords;
+            if (y < 0 || y >= Y || gp < 0 || gp >= (int64_t)A.gz) {
+                fill_row(dst, W, FULL);
+                continue;
+            } else if (p < 0) {
+                src = A.halo_lo;
+                swords = 2 * plane_w;
+                bit0 = (uint64_t)(p + 2) * plane_w * 32 + y * A.nx;
+            } else if (p >= (int64_t)A.nz) {
+                src = A.halo_hi;
+                swords = 2 * plane_w;
+                bit0 = (uint64_t)(p - A.nz) * plane_w * 32 + y * A.nx;
+            } else {
+                src = A.m;
+                swords = A.m_words;
+                bit0 = ((uint64_t)p * A.ny + y) * A.nx;
+            }
+            if (async) {
+                const uint4 *s4 = reinterpret_cast<const uint4 *>(src + (bit0 >> 5));
+                for (uint32_t k = lane_id(); k < W / 4; k += 32) cp_async16(dst + 4 * k, s4 + k);
+            } else {
+                load_m_row(src, swords, bit0, A.nx, W, dst);
+            }
         }
+        cp_async_commit();
+    };
+    for (int k = 0; k < PF; k++) {
+        if (zs - 2 + k <= ze + 1) fetch(zs - 2 + k);
+        else cp_async_commit();
+    }
+    for (int64_t p = zs - 2; p <= ze + 1; p++) {
+        if (p + PF <= ze + 1) fetch(p + PF);
+        else cp_async_commit();     // empty group: keeps the group count uniform
+        cp_async_wait<PF>();        // m(p) has landed; m(p+1..p+PF) may still be in flight
         __syncthreads();
-        // 2. e(q = p-1), rows y0-1 .. y0+TY
+        // e(q = p-1), rows y0-1 .. y0+TY
         const int64_t q = p - 1;
         if (q >= zs - 1) {
             const int64_t gq = (int64_t)A.z0 + q;
@@ -241,15 +332,15 @@ __global__ void __launch_bounds__(256) k_morph3d(const T *__restrict__ x, MorphA
                 }
                 const uint32_t *c = mrow(q, r + 1), *a = mrow(q, r), *b = mrow(q, r + 2);
                 const uint32_t *f = mrow(q - 1, r + 1), *g = mrow(q + 1, r + 1);
-                for (uint32_t k = lane_id(); k < W; k += 32) dst[k] = erode_word(c, a, b, f, g, k);
-                __syncwarp();
-                uint32_t tail = (uint32_t)(X - 32ll * (W - 1));
-                if (lane_id() == 0 && tail < 32) dst[W - 1] &= low_mask(tail);
-                __syncwarp();
+                for (uint32_t k = lane_id(); k < W; k += 32) {
+                    uint32_t v = erode_word(c, a, b, f, g, k);
+                    if (k == W - 1 && tail < 32) v &= low_mask(tail);
+                    dst[k] = v;
+                }
             }
         }
         __syncthreads();
-        // 3. o(z = p-2), rows y0 .. y0+TY-1
+        // o(z = p-2), rows y0 .. y0+TY-1
         const int64_t z = p - 2;
         if (z >= zs && z < ze) {
             for (int r = warp; r < TY; r += nw) {
@@ -260,7 +351,6 @@ __global__ void __launch_bounds__(256) k_morph3d(const T *__restrict__ x, MorphA
                 const uint64_t row = (uint64_t)z * A.ny + y;
                 const uint64_t bitpos = row * A.nx;
                 uint32_t carry = 0, runs = 0;
-                const uint32_t tail = (uint32_t)(X - 32ll * (W - 1));
                 for (uint32_t k0 = 0; k0 < W; k0 += 32) {
                     uint32_t k = k0 + lane_id();
                     uint32_t w = 0;
@@ -281,27 +371,24 @@ __global__ void __launch_bounds__(256) k_morph3d(const T *__restrict__ x, MorphA
                 }
             }
         }
-        // the next iteration's first __syncthreads orders these reads before ring slots are reused
+        // the next iteration's fetch writes m(p+1+PF) into the slot of m(p+1+PF-MSLOTS), last read
+        // by e(p+2+PF-MSLOTS) <= e(p-1), which every warp finished before the barrier above
     }
 }
 
-// ------------------------------------------------------------------------------------ 2-D kernel
+// ------------------------------------------------------------------------------------ 2-D opening
 // Rows r = q*Y + y of the slab (q = plane); neighbours only within the same plane.  S = rows per
-// step = warps per CTA.  Output rows of a step are contiguous bits [c X, (c+S) X) of o; they are
+// step = warps per CTA.  The output rows of a step are contiguous bits [c X, (c+S) X) of o; they are
 // assembled from the o rows in shared memory into whole words.
-template <typename T>
-__global__ void __launch_bounds__(256) k_morph2d(const T *__restrict__ x, MorphArgs A, roix_scalars *sc) {
+__global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     extern __shared__ uint32_t smem[];
     if (get_err(sc)) return;
-    const Cmp<T> cmp(sc);
     const uint32_t W = A.W, WS = A.WS;
     const int S = blockDim.x >> 5, warp = threadIdx.x >> 5;
     const int MS = S + 4, ES = S + 2;
     uint32_t *mring = smem;            // [MS][WS]
     uint32_t *ering = mring + MS * WS; // [ES][WS]
     uint32_t *orow = ering + ES * WS;  // [S][WS]
-    uint32_t *stage = orow + S * WS;   // [S][WS]
-    uint32_t *mystage = stage + warp * WS;
     const int64_t Y = A.ny, X = A.nx;
     const int64_t rows = (int64_t)(A.nz * A.ny);
     const int64_t r0 = (int64_t)blockIdx.x * A.rows_per_cta;
@@ -321,7 +408,7 @@ __global__ void __launch_bounds__(256) k_morph2d(const T *__restrict__ x, MorphA
     auto load_m = [&](int64_t r) {
         uint32_t *dst = mrow(r);
         if (r < 0 || r >= rows) fill_row(dst, W, FULL);
-        else binarize_row(x + (uint64_t)r * A.nx, A.nx, W, cmp, dst, mystage);
+        else load_m_row(A.m, A.m_words, (uint64_t)r * A.nx, A.nx, W, dst);
     };
     const uint32_t tail = (uint32_t)(X - 32ll * (W - 1));
     auto comp_e = [&](int64_t r) {
@@ -334,10 +421,11 @@ __global__ void __launch_bounds__(256) k_morph2d(const T *__restrict__ x, MorphA
         const uint32_t *c = mrow(r);
         // out-of-plane neighbours are ignored (border 1): use the row itself
         const uint32_t *a = y > 0 ? mrow(r - 1) : c, *b = y < Y - 1 ? mrow(r + 1) : c;
-        for (uint32_t k = lane_id(); k < W; k += 32) dst[k] = erode_word(c, a, b, nullptr, nullptr, k);
-        __syncwarp();
-        if (lane_id() == 0 && tail < 32) dst[W - 1] &= low_mask(tail);
-        __syncwarp();
+        for (uint32_t k = lane_id(); k < W; k += 32) {
+            uint32_t v = erode_word(c, a, b, nullptr, nullptr, k);
+            if (k == W - 1 && tail < 32) v &= low_mask(tail);
+            dst[k] = v;
+        }
     };
     // prologue: m rows r0-2 .. r0+1, e rows r0-1, r0
     for (int i = warp; i < 4; i += S) load_m(r0 - 2 + i);
@@ -382,7 +470,6 @@ __global__ void __launch_bounds__(256) k_morph2d(const T *__restrict__ x, MorphA
         const uint64_t B0 = (uint64_t)c0 * A.nx, B1 = (uint64_t)cend * A.nx;
         const uint64_t w0 = B0 >> 5, w1 = (B1 + 31) >> 5;
         for (uint64_t wi = w0 + threadIdx.x; wi < w1; wi += blockDim.x) {
-            // 32 bits at absolute positions [32 wi, 32 wi + 32) clipped to [B0, B1)
             uint64_t lo = max(wi * 32, B0), hi = min(wi * 32 + 32, B1);
             uint32_t val = 0;
             uint64_t pos = lo;
@@ -440,10 +527,12 @@ static cudaError_t set_smem(K kern, size_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-template <typename T>
-static cudaError_t morph_t(const T *x, const roix_geom &g, uint32_t se, const uint32_t *hlo, const uint32_t *hhi,
-                           roix_scalars *sc, uint32_t *o, uint32_t *runs, cudaStream_t st) {
-    MorphArgs A;
+size_t morph_workspace_bytes(const roix_geom &g) { return ((g.nz * g.ny * g.nx + 31) / 32 + 64) * 4; }
+
+cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
+                         const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
+                         cudaStream_t st) {
+    MorphArgs A = {};
     A.nz = g.nz;
     A.ny = g.ny;
     A.nx = g.nx;
@@ -451,63 +540,76 @@ static cudaError_t morph_t(const T *x, const roix_geom &g, uint32_t se, const ui
     A.gz = g.gz;
     A.W = (uint32_t)((g.nx + 31) / 32);
     A.WS = A.W + 2;
-    A.halo_lo = hlo;
-    A.halo_hi = hhi;
-    A.o = o;
-    A.row_runs = runs;
-    const uint64_t nwords = (g.nz * g.ny * g.nx + 31) / 32;
-    int occ = 0;
+    A.halo_lo = halo_lo;
+    A.halo_hi = halo_hi;
+    A.o = o_bits;
+    A.row_runs = row_runs;
+    const uint64_t n = g.nz * g.ny * g.nx;
+    const uint64_t nwords = (n + 31) / 32;
+    uint32_t *m = (uint32_t *)ws;
+    A.m = m;
+    A.m_words = nwords;
     cudaError_t e;
+    // a4: stream x -> m
+    {
+        uint64_t iters = (n + 1023) / 1024;
+        uint64_t blocks = (iters + 7) / 8;
+        uint64_t cap = (uint64_t)num_sms() * 8;
+        if (blocks > cap) blocks = cap;
+        if (dtype == ROIX_U16) k_binarize<uint16_t><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x, n, sc, m);
+        else k_binarize<float><<<(unsigned)blocks, 256, 0, st>>>((const float *)x, n, sc, m);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
+    int occ = 0;
     if (se == 6) {
-        // band height: as tall as fits ~100 KB of rings (2 CTAs / SM), at most 64 rows
+        // band height: the largest of 64/32/16/8 rows whose rings fit ~100 KB (2+ CTAs per SM) and
+        // that still gives >= 1.5 CTAs per SM with z-chunks of >= 64 planes
+        const uint64_t chunks_max = g.nz >= 128 ? g.nz / 64 : 1;
+        A.WS = (A.W + 8 + 3) / 4 * 4;
+        A.async = (g.nx % 128 == 0);
         int TY = 64;
-        while (TY > 4 && (size_t)(3 * (TY + 4) + 3 * (TY + 2) + 8) * A.WS * 4 > 100 * 1024) TY /= 2;
+        auto smem_of = [&](int ty) { return (size_t)(MSLOTS * (ty + 4) + 3 * (ty + 2)) * A.WS * 4; };
+        while (TY > 4 && smem_of(TY) > 72 * 1024) TY /= 2;
+        while (TY > 8 && ((g.ny + TY - 1) / TY) * chunks_max < (uint64_t)(1.5 * num_sms())) TY /= 2;
         if ((uint64_t)TY > g.ny) TY = (int)g.ny;
         A.TY = TY;
-        size_t sm = (size_t)(3 * (TY + 4) + 3 * (TY + 2) + 8) * A.WS * 4;
+        size_t sm = smem_of(TY);
         if (sm > 220 * 1024) return cudaErrorInvalidConfiguration;
-        if ((e = set_smem(k_morph3d<T>, sm)) != cudaSuccess) return e;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_morph3d<T>, 256, sm)) != cudaSuccess) return e;
+        if ((e = set_smem(k_open3d, sm)) != cudaSuccess) return e;
+        cudaFuncSetAttribute(k_open3d, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_open3d, 256, sm)) != cudaSuccess) return e;
         if (occ < 1) occ = 1;
         uint64_t bands = (g.ny + TY - 1) / TY;
         uint64_t slots = (uint64_t)num_sms() * occ;
-        uint64_t chunks = slots / bands;
+        uint64_t chunks = (slots + bands - 1) / bands;
         if (chunks < 1) chunks = 1;
-        if (chunks > g.nz) chunks = g.nz;
+        if (chunks > chunks_max) chunks = chunks_max;
         A.zchunk = (g.nz + chunks - 1) / chunks;
         chunks = (g.nz + A.zchunk - 1) / A.zchunk;
         A.aligned_out = (g.nx % 32 == 0);
-        if (!A.aligned_out && (e = cudaMemsetAsync(o, 0, nwords * 4, st)) != cudaSuccess) return e;
+        if (!A.aligned_out && (e = cudaMemsetAsync(o_bits, 0, nwords * 4, st)) != cudaSuccess) return e;
         dim3 grid((unsigned)bands, (unsigned)chunks);
-        k_morph3d<T><<<grid, 256, sm, st>>>(x, A, sc);
+        k_open3d<<<grid, 256, sm, st>>>(A, sc);
     } else {
         const int S = 8;
-        size_t sm = (size_t)((S + 4) + (S + 2) + S + S) * A.WS * 4;
+        size_t sm = (size_t)((S + 4) + (S + 2) + S) * A.WS * 4;
         if (sm > 220 * 1024) return cudaErrorInvalidConfiguration;
-        if ((e = set_smem(k_morph2d<T>, sm)) != cudaSuccess) return e;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_morph2d<T>, 32 * S, sm)) != cudaSuccess) return e;
+        if ((e = set_smem(k_open2d, sm)) != cudaSuccess) return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_open2d, 32 * S, sm)) != cudaSuccess) return e;
         if (occ < 1) occ = 1;
         const uint64_t rows = g.nz * g.ny;
         uint64_t slots = (uint64_t)num_sms() * occ;
-        // rows per CTA: a multiple of 32 so that every CTA's bit range starts on a word whenever
-        // 32 | 32 X (always) -- i.e. c X is word aligned at CTA starts for any X
+        // rows per CTA: a multiple of 32, so every CTA's bit range starts on a word boundary
         uint64_t rpc = (rows + slots - 1) / slots;
         rpc = (rpc + 31) / 32 * 32;
         A.rows_per_cta = rpc;
         uint64_t ctas = (rows + rpc - 1) / rpc;
         // whole words at every step iff S*X is a multiple of 32 (CTA starts are, see above)
         A.aligned_out = ((uint64_t)S * g.nx) % 32 == 0;
-        if (!A.aligned_out && (e = cudaMemsetAsync(o, 0, nwords * 4, st)) != cudaSuccess) return e;
-        k_morph2d<T><<<(unsigned)ctas, 32 * S, sm, st>>>(x, A, sc);
+        if (!A.aligned_out && (e = cudaMemsetAsync(o_bits, 0, nwords * 4, st)) != cudaSuccess) return e;
+        k_open2d<<<(unsigned)ctas, 32 * S, sm, st>>>(A, sc);
     }
     return cudaGetLastError();
-}
-
-cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
-                         const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
-                         cudaStream_t st) {
-    if (dtype == ROIX_U16) return morph_t((const uint16_t *)x, g, se, halo_lo, halo_hi, sc, o_bits, row_runs, st);
-    return morph_t((const float *)x, g, se, halo_lo, halo_hi, sc, o_bits, row_runs, st);
 }
 
 cudaError_t launch_binarize_planes(const void *x, int dtype, const roix_geom &g, uint64_t p0, uint64_t np,

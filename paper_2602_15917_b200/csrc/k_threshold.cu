@@ -72,55 +72,64 @@ __device__ bool better(const Cand &a, const Cand &b) {
     return c > 0 || (c == 0 && a.t < b.t);
 }
 
-__global__ void __launch_bounds__(256) k_threshold(const uint64_t *__restrict__ hist, int dtype, int polarity,
-                                                    roix_scalars *sc) {
-    __shared__ uint64_t h8[256];
+__global__ void __launch_bounds__(1024) k_threshold(const uint64_t *__restrict__ hist, int dtype, int polarity,
+                                                     roix_scalars *sc) {
+    __shared__ unsigned long long h8[256];
     __shared__ uint64_t scan_n[256], scan_s[256];
     __shared__ Cand cand[256];
     __shared__ uint32_t s_imax;
     const int t = threadIdx.x;
     if (get_err(sc)) return;
+    if (t < 256) h8[t] = 0;
+    if (t == 0) s_imax = 0;
+    __syncthreads();
     uint32_t imax = 1;
     if (dtype == ROIX_U16) {
         // I_max = the largest populated value (Eq. 1); 1 if none above 0
-        if (t == 0) s_imax = 0;
-        __syncthreads();
-        for (int v = 256 * t + 255; v >= 256 * t; v--)
-            if (hist[v]) {
-                atomicMax(&s_imax, (uint32_t)v);
-                break;
-            }
+        uint32_t mymax = 0;
+#pragma unroll 8
+        for (int v = t; v < 65536; v += 1024)
+            if (hist[v]) mymax = (uint32_t)v;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) mymax = max(mymax, __shfl_xor_sync(FULL, mymax, d));
+        if (lane_id() == 0 && mymax) atomicMax(&s_imax, mymax);
         __syncthreads();
         imax = s_imax ? s_imax : 1;
-        // norm8(v) >= k  <=>  v >= e_k = ceil(I_max (2k - 1) / 510): h8[k] sums [e_k, e_{k+1})
-        uint64_t lo = t == 0 ? 0 : ((uint64_t)imax * (2 * t - 1) + 509) / 510;
-        uint64_t hi = t == 255 ? 65536 : ((uint64_t)imax * (2 * t + 1) + 509) / 510;
-        if (hi > 65536) hi = 65536;
-        uint64_t acc = 0;
-        for (uint64_t v = lo; v < hi; v++) acc += hist[v];
-        h8[t] = acc;
-    } else {
+        // fold: h8[norm8(v)] += hist[v], norm8(v) = round_half_up(255 v / I_max) = floor((510 v + I) / 2I)
+        const uint32_t two_i = 2 * imax;
+#pragma unroll 8
+        for (int v = t; v <= (int)imax; v += 1024) {
+            uint64_t c = hist[v];
+            if (c) atomicAdd(&h8[(510u * (uint32_t)v + imax) / two_i], (unsigned long long)c);
+        }
+    } else if (t < 256) {
         h8[t] = hist[t];
     }
     __syncthreads();
+    // threads >= 256 stay for the barriers only
+    const bool act = t < 256;
+    const int ti = act ? t : 255;
     // inclusive prefix sums of counts and intensity sums over bins 0..t
-    uint64_t vn = h8[t], vs = (uint64_t)t * h8[t];
-    scan_n[t] = vn;
-    scan_s[t] = vs;
+    if (act) {
+        scan_n[t] = h8[t];
+        scan_s[t] = (uint64_t)t * h8[t];
+    }
     __syncthreads();
     for (int d = 1; d < 256; d <<= 1) {
-        uint64_t an = t >= d ? scan_n[t - d] : 0, as = t >= d ? scan_s[t - d] : 0;
+        uint64_t an = (act && t >= d) ? scan_n[t - d] : 0, as = (act && t >= d) ? scan_s[t - d] : 0;
         __syncthreads();
-        scan_n[t] += an;
-        scan_s[t] += as;
+        if (act) {
+            scan_n[t] += an;
+            scan_s[t] += as;
+        }
         __syncthreads();
     }
     const uint64_t N = scan_n[255], S = scan_s[255];
     Cand c;
     c.t = -1;
     c.d0 = c.d1 = c.n0 = c.n1 = 0;
-    if (t < 255) {
-        uint64_t n0 = scan_n[t], s0 = scan_s[t];
+    if (ti < 255 && act) {
+        uint64_t n0 = scan_n[ti], s0 = scan_s[ti];
         if (n0 > 0 && n0 < N) {
             unsigned __int128 a = (unsigned __int128)N * s0, b = (unsigned __int128)n0 * S;
             unsigned __int128 d = a >= b ? a - b : b - a;
@@ -128,10 +137,10 @@ __global__ void __launch_bounds__(256) k_threshold(const uint64_t *__restrict__ 
             c.d1 = (uint64_t)(d >> 64);
             c.n0 = n0;
             c.n1 = N - n0;
-            c.t = t;
+            c.t = ti;
         }
     }
-    cand[t] = c;
+    if (act) cand[t] = c;
     __syncthreads();
     for (int stride = 128; stride > 0; stride >>= 1) {
         if (t < stride && better(cand[t + stride], cand[t])) cand[t] = cand[t + stride];
@@ -155,6 +164,6 @@ __global__ void __launch_bounds__(256) k_threshold(const uint64_t *__restrict__ 
 }  // namespace roix
 
 cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st) {
-    roix::k_threshold<<<1, 256, 0, st>>>(hist, dtype, polarity, sc);
+    roix::k_threshold<<<1, 1024, 0, st>>>(hist, dtype, polarity, sc);
     return cudaGetLastError();
 }

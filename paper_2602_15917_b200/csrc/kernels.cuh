@@ -19,8 +19,9 @@ cudaError_t launch_hist_f32(const float *x, uint64_t n, roix_scalars *sc, uint64
 
 cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st);
 
+size_t morph_workspace_bytes(const roix_geom &g);
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
-                         const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
+                         const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
                          cudaStream_t st);
 cudaError_t launch_binarize_planes(const void *x, int dtype, const roix_geom &g, uint64_t p0, uint64_t np,
                                    roix_scalars *sc, uint32_t *m_bits, cudaStream_t st);

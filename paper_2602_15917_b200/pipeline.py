@@ -15,8 +15,8 @@ import torch
 from . import _lib as L
 
 # kernels libroix launches per call (used for the bench's gpu_launches count)
-LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 1, "threshold": 1, "morph": 1,
-            "label": 15, "extract": 2}
+LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 1, "threshold": 1, "morph": 2,
+            "label": 16, "extract": 6}
 
 
 def _ptr(t):
@@ -65,6 +65,7 @@ class Pipeline:
         self.hist = torch.zeros(self.nbins, dtype=torch.int64, device=dev)
         self.o = torch.empty(self.nwords + 4, dtype=torch.int32, device=dev)   # o, then K in place
         self.row_runs = torch.empty(Z * Y, dtype=torch.int32, device=dev)
+        self.morph_ws = torch.empty(L.roix_morph_workspace(self.geom), dtype=torch.uint8, device=dev)
         rows = Z * Y
         worst = rows * ((X + 1) // 2)
         if run_capacity is None:
@@ -107,7 +108,7 @@ class Pipeline:
         L.roix_threshold(_ptr(self.hist), self.nbins, self.cdtype, self.polarity, sc, st)
         mark("threshold")
         L.roix_morph(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o),
-                     _ptr(self.row_runs), st)
+                     _ptr(self.row_runs), _ptr(self.morph_ws), self.morph_ws.numel(), st)
         mark("morph")
         out = L.LabelOut(self.o.data_ptr(), self.comp_min.data_ptr(), self.comp_size.data_ptr(),
                          self.comp_kept.data_ptr(), self.comp_cap,
@@ -133,8 +134,9 @@ class Pipeline:
         self.enqueue(x, stream)
         torch.cuda.synchronize(self.device)
         s = self.scalars()
-        if s.err & L.ERR_CAPACITY and s.n_runs > self.run_capacity:
-            self._alloc_label(int(s.n_runs))
+        if s.err & L.ERR_CAPACITY and s.count <= self.code_capacity:
+            # the labelling workspace (runs, or the cross-block pair queue sized from it) was too small
+            self._alloc_label(int(max(s.n_runs, 2 * self.run_capacity)))
             self.enqueue(x, stream)
             torch.cuda.synchronize(self.device)
             s = self.scalars()

@@ -58,7 +58,7 @@ def test_host_validation_without_gpu(lib):
     assert lib.roix_histogram(ctypes.c_void_p(16), 1, 10, ctypes.c_void_p(16), ctypes.c_void_p(16), 256,
                               None) == L.ROIX_E_INVALID            # wrong nbins for u16
     assert lib.roix_morph(ctypes.c_void_p(16), 1, ctypes.byref(g), 5, None, None, ctypes.c_void_p(16),
-                          ctypes.c_void_p(16), None, None) == L.ROIX_E_UNSUPPORTED
+                          ctypes.c_void_p(16), None, ctypes.c_void_p(16), 1 << 20, None) == L.ROIX_E_UNSUPPORTED
     assert b"se" in lib.roix_last_error()
     assert lib.roix_scalars_init(ctypes.c_void_p(16), ctypes.c_float(-1.0), None) == L.ROIX_E_INVALID
     assert lib.roix_resolve(ctypes.c_void_p(16), 1, ctypes.c_double(0.1), None) == L.ROIX_E_UNSUPPORTED

@@ -41,7 +41,8 @@ def _check(cfg, p, x, res):
         np.testing.assert_array_equal(p.hist.cpu().numpy(), ref["hist"].astype(np.int64))
     # o: re-run the fused binarise+open with the pipeline's threshold
     o = torch.full_like(p.o, -1)
-    L.roix_morph(ptr(x), p.cdtype, ctypes.byref(p.geom), p.se, None, None, ptr(p.sc), ptr(o), None, st())
+    L.roix_morph(ptr(x), p.cdtype, ctypes.byref(p.geom), p.se, None, None, ptr(p.sc), ptr(o), None, ptr(p.morph_ws),
+                 p.morph_ws.numel(), st())
     np.testing.assert_array_equal(words_to_mask(o, p.n).reshape(cfg.shape), ref["o"])
     np.testing.assert_array_equal(words_to_mask(res.keep_bits, p.n).reshape(cfg.shape), ref["K"])
     np.testing.assert_array_equal(res.comp_min.cpu().numpy(), ref["comp_min"].astype(np.int64))

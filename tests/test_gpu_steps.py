@@ -174,7 +174,9 @@ def _morph_gpu(x_np, thr, pol, se):
     o = torch.full(((n + 31) // 32 + 4,), -1, dtype=torch.int32, device="cuda")   # garbage-initialised
     runs = torch.full((Z * Y,), -1, dtype=torch.int32, device="cuda")
     g = L.Geom(Z, Y, X, 0, Z)
-    L.roix_morph(ptr(x), dtype_code(x_np), ctypes.byref(g), se, None, None, ptr(sc), ptr(o), ptr(runs), st())
+    ws = torch.empty(L.roix_morph_workspace(g), dtype=torch.uint8, device="cuda")
+    L.roix_morph(ptr(x), dtype_code(x_np), ctypes.byref(g), se, None, None, ptr(sc), ptr(o), ptr(runs), ptr(ws),
+                 ws.numel(), st())
     assert read_sc(sc).err == 0
     return o, runs
 
