@@ -67,6 +67,7 @@ __device__ __forceinline__ float rne_fast(float x, float s, float s_inv) {
 struct QP {
     float s, s_inv;
     uint32_t s_int, magic;
+    uint32_t k;  // log2(s_int) when s_int >= 2 is a power of two, else 0
 };
 __device__ __forceinline__ QP load_qp(const roix_scalars *sc) {
     QP q;
@@ -74,6 +75,7 @@ __device__ __forceinline__ QP load_qp(const roix_scalars *sc) {
     q.s_inv = sc->s_inv;
     q.s_int = sc->s_int;
     q.magic = sc->s_magic;
+    q.k = (q.s_int >= 2 && (q.s_int & (q.s_int - 1)) == 0) ? (uint32_t)(__ffs(q.s_int) - 1) : 0u;
     return q;
 }
 
@@ -91,6 +93,62 @@ __device__ __forceinline__ uint32_t code_u16(uint32_t v, const QP &q, uint32_t &
     float c = rne_fast(x, q.s, q.s_inv);
     if (c > 65535.0f) err |= ROIX_ERR_RANGE;
     return (uint32_t)c;
+}
+
+// Quantiser modes for u16 input, fixed per launch so each kernel body holds one code path:
+//   QM_FLOAT: non-integer step (rne_fast); QM_ONE: s = 1 (identity); QM_POW2: s = 2^k; QM_INT: other
+//   integer steps (exact division by multiply-high).  fp32 input always uses QM_FLOAT.
+enum { QM_FLOAT = 0, QM_ONE = 1, QM_POW2 = 2, QM_INT = 3 };
+__device__ __forceinline__ int qmode(const QP &q) {
+    return q.s_int == 0 ? QM_FLOAT : q.s_int == 1 ? QM_ONE : q.k ? QM_POW2 : QM_INT;
+}
+
+template <int M>
+__device__ __forceinline__ uint32_t code_u16_m(uint32_t v, const QP &q, uint32_t &err) {
+    if constexpr (M == QM_ONE) return v;
+    if constexpr (M == QM_FLOAT) {
+        float x = (float)v;
+        if (!(x < q.s * 8388608.0f)) err |= ROIX_ERR_RANGE;
+        float c = rne_fast(x, q.s, q.s_inv);
+        if (c > 65535.0f) err |= ROIX_ERR_RANGE;
+        return (uint32_t)c;
+    }
+    if constexpr (M == QM_POW2) {
+        const uint32_t qq = v >> q.k, r = v & ((1u << q.k) - 1u);
+        return qq + ((r + (qq & 1u) + (1u << (q.k - 1)) - 1u) >> q.k);
+    }
+    uint32_t d = __umulhi(v, q.magic);
+    uint32_t r = v - d * q.s_int;
+    return d + ((2 * r > q.s_int) | ((2 * r == q.s_int) & (d & 1u)));
+}
+
+template <int M>
+__device__ __forceinline__ uint32_t code_pair_u16_m(uint32_t w, const QP &q, uint32_t &err) {
+    if constexpr (M == QM_ONE) return w;
+    if constexpr (M == QM_POW2) {
+        const uint32_t lanes = 0x00010001u, k = q.k;
+        const uint32_t qq = (w >> k) & ((0xffffu >> k) * lanes);
+        const uint32_t r = w & (((1u << k) - 1u) * lanes);
+        const uint32_t t = r + (qq & lanes) + (((1u << (k - 1)) - 1u) * lanes);
+        return qq + ((t >> k) & lanes);
+    }
+    return code_u16_m<M>(w & 0xffffu, q, err) | (code_u16_m<M>(w >> 16, q, err) << 16);
+}
+
+// Two u16 voxels packed in one word (lo, hi) -> two packed codes.  For a power-of-two step s = 2^k
+// both halves are rounded at once: v = q 2^k + r rounds up iff r + (q & 1) > 2^(k-1), i.e. iff
+// t = r + (q & 1) + 2^(k-1) - 1 >= 2^k; every 16-bit field of t stays below 2^(k+1) <= 2^16, so no
+// carry crosses the halves.  Other steps go voxel by voxel through code_u16.
+__device__ __forceinline__ uint32_t code_pair_u16(uint32_t w, const QP &q, uint32_t &err) {
+    if (q.k) {
+        const uint32_t lanes = 0x00010001u, k = q.k;
+        const uint32_t qq = (w >> k) & ((0xffffu >> k) * lanes);
+        const uint32_t r = w & (((1u << k) - 1u) * lanes);
+        const uint32_t t = r + (qq & lanes) + (((1u << (k - 1)) - 1u) * lanes);
+        return qq + ((t >> k) & lanes);
+    }
+    if (q.s_int == 1) return w;
+    return code_u16(w & 0xffffu, q, err) | (code_u16(w >> 16, q, err) << 16);
 }
 
 // fp32 input (validity range |x| < 2^23 s, G-4; non-finite x fails the same test)

@@ -73,17 +73,14 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract_count(const uint32_t *__
     }
 }
 
-template <typename T, typename C>
-__global__ void __launch_bounds__(EX_THREADS) k_extract(const T *__restrict__ x, uint64_t n, uint64_t ntiles,
-                                                        const uint32_t *__restrict__ K, ExWS w, roix_scalars *sc,
-                                                        C *__restrict__ out, uint64_t capacity, const uint64_t *offset) {
+template <typename T, typename C, int QM>
+__device__ __forceinline__ void extract_tile(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
+                                             const ExWS &w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
+                                             const uint64_t *offset, C *stage, uint32_t *warp_tot) {
     constexpr int VPL = 16 / sizeof(T);   // voxels per 16-byte group
     constexpr int GPW = 32 / VPL;         // groups per mask word
     constexpr int CH = 32 / VPL;          // 32-group chunks per warp (a warp covers 32 words = 1024 voxels)
     constexpr int PADE = 16 / sizeof(C);  // staging is shifted by base % PADE so that stores are 16-byte aligned
-    __shared__ __align__(16) C stage[EX_TILE + 2 * PADE];
-    __shared__ uint32_t warp_tot[EX_THREADS / 32];
-    if (*w.err_snap) return;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     const uint64_t tile = blockIdx.x;
     const uint64_t nwords = (n + 31) / 32;
@@ -107,7 +104,7 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract(const T *__restrict__ x,
     if (lane == 31) warp_tot[warp] = incl;
     const uint64_t base = (offset ? *offset : 0) + w.tcount[tile];
     const uint32_t shift = (uint32_t)(base % PADE);
-    C *st = stage + shift;
+    const C *st = stage + shift;
     __syncthreads();
     uint32_t run = 0, total = 0;
 #pragma unroll
@@ -123,30 +120,56 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract(const T *__restrict__ x,
         const uint32_t pc = __popc(m[c]);
         const uint32_t pos = warp_incl_scan(pc) - pc + run;
         run = __shfl_sync(FULL, pos + pc, 31);
-        if (m[c]) {
-            const uint32_t g = c * 32 + lane;
-            const uint64_t v0 = gbase + (uint64_t)g * VPL;
-            uint32_t p = pos;
-            if (v0 + VPL <= n) {
-                if constexpr (sizeof(T) == 2) {
-                    uint32_t ww[4] = {d[c].x, d[c].y, d[c].z, d[c].w};
+        if (!m[c]) continue;
+        const uint32_t g = c * 32 + lane;
+        const uint64_t v0 = gbase + (uint64_t)g * VPL;
+        const uint32_t a = shift + pos;   // element index in stage[]
+        if (v0 + VPL <= n) {
+            if constexpr (sizeof(T) == 2) {
+                // 8 codes, packed in pairs
+                const uint32_t c0 = code_pair_u16_m<QM>(d[c].x, q, err), c1 = code_pair_u16_m<QM>(d[c].y, q, err),
+                               c2 = code_pair_u16_m<QM>(d[c].z, q, err), c3 = code_pair_u16_m<QM>(d[c].w, q, err);
+                if (m[c] == 0xffu) {
+                    if ((a & 7u) == 0) {
+                        *reinterpret_cast<uint4 *>(stage + a) = make_uint4(c0, c1, c2, c3);
+                    } else if ((a & 1u) == 0) {
+                        uint32_t *s32 = reinterpret_cast<uint32_t *>(stage + a);
+                        s32[0] = c0; s32[1] = c1; s32[2] = c2; s32[3] = c3;
+                    } else {
+                        stage[a] = (C)(c0 & 0xffffu);
+                        uint32_t *s32 = reinterpret_cast<uint32_t *>(stage + a + 1);
+                        s32[0] = __funnelshift_r(c0, c1, 16);
+                        s32[1] = __funnelshift_r(c1, c2, 16);
+                        s32[2] = __funnelshift_r(c2, c3, 16);
+                        stage[a + 7] = (C)(c3 >> 16);
+                    }
+                } else {
+                    const uint32_t cc[4] = {c0, c1, c2, c3};
+                    uint32_t p = a;
 #pragma unroll
                     for (int k = 0; k < 8; k++)
-                        if (m[c] >> k & 1) st[p++] = (C)code_u16((ww[k >> 1] >> ((k & 1) * 16)) & 0xffffu, q, err);
-                } else {
-                    float ff[4] = {__uint_as_float(d[c].x), __uint_as_float(d[c].y), __uint_as_float(d[c].z),
-                                   __uint_as_float(d[c].w)};
-#pragma unroll
-                    for (int k = 0; k < 4; k++)
-                        if (m[c] >> k & 1) st[p++] = (C)code_f32(ff[k], q, err);
+                        if (m[c] >> k & 1) stage[p++] = (C)((cc[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
                 }
             } else {
-                for (int k = 0; k < VPL; k++)
-                    if (m[c] >> k & 1) {
-                        if constexpr (sizeof(T) == 2) st[p++] = (C)code_u16(x[v0 + k], q, err);
-                        else st[p++] = (C)code_f32(x[v0 + k], q, err);
-                    }
+                const int32_t k0 = code_f32(__uint_as_float(d[c].x), q, err), k1 = code_f32(__uint_as_float(d[c].y), q, err),
+                              k2 = code_f32(__uint_as_float(d[c].z), q, err), k3 = code_f32(__uint_as_float(d[c].w), q, err);
+                if (m[c] == 0xfu && (a & 3u) == 0) {
+                    *reinterpret_cast<int4 *>(stage + a) = make_int4(k0, k1, k2, k3);
+                } else {
+                    const int32_t kk[4] = {k0, k1, k2, k3};
+                    uint32_t p = a;
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        if (m[c] >> k & 1) stage[p++] = (C)kk[k];
+                }
             }
+        } else {
+            uint32_t p = a;
+            for (int k = 0; k < VPL; k++)
+                if (m[c] >> k & 1) {
+                    if constexpr (sizeof(T) == 2) stage[p++] = (C)code_u16_m<QM>(x[v0 + k], q, err);
+                    else stage[p++] = (C)code_f32(x[v0 + k], q, err);
+                }
         }
     }
     if (base + total > capacity) err |= ROIX_ERR_CAPACITY;
@@ -161,6 +184,27 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract(const T *__restrict__ x,
     uint4 *ov = reinterpret_cast<uint4 *>(out + base + head);
     for (uint64_t j = threadIdx.x; j < nvec; j += EX_THREADS) __stcs(ov + j, sv[j]);
     for (uint64_t j = head + nvec * PADE + threadIdx.x; j < lim; j += EX_THREADS) out[base + j] = st[j];
+}
+
+template <typename T, typename C>
+__global__ void __launch_bounds__(EX_THREADS) k_extract(const T *__restrict__ x, uint64_t n, uint64_t ntiles,
+                                                        const uint32_t *__restrict__ K, ExWS w, roix_scalars *sc,
+                                                        C *__restrict__ out, uint64_t capacity, const uint64_t *offset) {
+    constexpr int PADE = 16 / sizeof(C);
+    __shared__ __align__(16) C stage[EX_TILE + 2 * PADE];
+    __shared__ uint32_t warp_tot[EX_THREADS / 32];
+    if (*w.err_snap) return;
+    const QP q = load_qp(sc);
+    if constexpr (sizeof(T) == 4) {
+        extract_tile<T, C, QM_FLOAT>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot);
+    } else {
+        switch (qmode(q)) {   // uniform over the launch: one code path per body
+        case QM_POW2: extract_tile<T, C, QM_POW2>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot); break;
+        case QM_INT: extract_tile<T, C, QM_INT>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot); break;
+        case QM_ONE: extract_tile<T, C, QM_ONE>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot); break;
+        default: extract_tile<T, C, QM_FLOAT>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot); break;
+        }
+    }
 }
 
 // count: total kept voxels (scan total) added to sc->count

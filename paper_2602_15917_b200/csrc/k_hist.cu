@@ -112,8 +112,7 @@ __global__ void __launch_bounds__(512) k_quantize_u16(const uint16_t *__restrict
         uint4 a = __ldcs(reinterpret_cast<const uint4 *>(x) + i);
         uint32_t w[4] = {a.x, a.y, a.z, a.w}, o[4];
 #pragma unroll
-        for (int k = 0; k < 4; k++)
-            o[k] = code_u16(w[k] & 0xffffu, q, err) | (code_u16(w[k] >> 16, q, err) << 16);
+        for (int k = 0; k < 4; k++) o[k] = code_pair_u16(w[k], q, err);
         __stcs(reinterpret_cast<uint4 *>(codes) + i, make_uint4(o[0], o[1], o[2], o[3]));
     }
     if (blockIdx.x == 0 && threadIdx.x < (n & 7)) {

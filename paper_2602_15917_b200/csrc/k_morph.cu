@@ -376,6 +376,355 @@ __global__ void __launch_bounds__(256) k_open3d(MorphArgs A, roix_scalars *sc) {
     }
 }
 
+// ----------------------------------------------------------------- 3-D opening, warp-register form
+// No shared memory and no block barriers: every warp owns a pencil of RY rows x 32 words (lanes)
+// and marches along z keeping the m and e words of 3 planes in registers.  Lanes 0 and 31 hold the
+// halo words of the pencil (the words left and right of its 30 output words): e and o bits next to
+// the output words only depend on their adjacent bits, which are exact.  Rows y-2, y-1 / y+RY,
+// y+RY+1 are the pencil's y-halo (re-read from L1/L2).  Neighbours in x come from the adjacent
+// lanes (__shfl), in y from the neighbouring register, in z from the previous/next plane registers.
+template <int RY>
+__global__ void __launch_bounds__(256, 3) k_open3d_reg(MorphArgs A, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    constexpr int MRW = RY + 4, ERW = RY + 2;
+    const uint32_t lane = lane_id();
+    const int Y = (int)A.ny;
+    const uint32_t W = A.W;
+    const uint32_t npx = (W + 29) / 30;                       // pencils across a row
+    const uint32_t nry = (uint32_t)((A.ny + RY - 1) / RY);     // row groups
+    const uint32_t task = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t per_chunk = npx * nry;
+    const uint32_t cz = task / per_chunk;
+    const uint32_t rem = task - cz * per_chunk;
+    const int yb = (int)(rem / npx) * RY;
+    const int kw = (int)(rem % npx) * 30 + (int)lane - 1;   // this lane's word column
+    const int nz = (int)A.nz;
+    const int zs = (int)(cz * A.zchunk);
+    if (zs >= nz) return;
+    const int ze = min(nz, zs + (int)A.zchunk);
+    const bool in_x = kw >= 0 && kw < (int)W;
+    const uint32_t tail = (uint32_t)(A.nx - 32ull * (W - 1));
+    const uint32_t padm = (kw == (int)W - 1 && tail < 32) ? ~low_mask(tail) : 0u;   // pad bits of the last word
+    const bool out_lane = lane >= 1 && lane <= 30 && in_x;
+    const uint64_t plane_w = (A.ny * A.nx + 31) / 32;
+    const bool aligned = (A.nx & 31) == 0;
+    const int64_t gz = (int64_t)A.gz, z0 = (int64_t)A.z0;
+    // per-lane offsets (in words) of the pencil's rows inside a plane, and their validity
+    const uint32_t wpr = (uint32_t)(A.nx >> 5);   // words per row when aligned
+    uint32_t roff[MRW];
+    uint32_t vmask = 0;   // bit j: row yb-2+j exists and the lane's column is inside the row
+#pragma unroll
+    for (int j = 0; j < MRW; j++) {
+        const int y = yb - 2 + j;
+        roff[j] = (uint32_t)max(y, 0) * wpr + (uint32_t)max(kw, 0);
+        if (in_x && y >= 0 && y < Y) vmask |= 1u << j;
+    }
+
+    auto load_plane = [&](int p, uint32_t (&mw)[MRW]) {
+        const int64_t gp = z0 + p;
+        if (gp < 0 || gp >= gz) {
+#pragma unroll
+            for (int j = 0; j < MRW; j++) mw[j] = FULL;
+            return;
+        }
+        if (aligned && p >= 0 && p < nz) {   // common case: one load per row
+            const uint32_t *base = A.m + (uint64_t)p * plane_w;
+#pragma unroll
+            for (int j = 0; j < MRW; j++) mw[j] = ((vmask >> j) & 1) ? (__ldg(base + roff[j]) | padm) : FULL;
+            return;
+        }
+        // halo planes / unaligned rows: generic bit addressing
+        const uint32_t *src;
+        uint64_t pb, sw;
+        if (p < 0) {
+            src = A.halo_lo;
+            pb = (uint64_t)(p + 2) * plane_w * 32;
+            sw = 2 * plane_w;
+        } else if (p >= nz) {
+            src = A.halo_hi;
+            pb = (uint64_t)(p - nz) * plane_w * 32;
+            sw = 2 * plane_w;
+        } else {
+            src = A.m;
+            pb = (uint64_t)p * A.ny * A.nx;
+            sw = A.m_words;
+        }
+#pragma unroll
+        for (int j = 0; j < MRW; j++) {
+            uint32_t v = FULL;
+            if ((vmask >> j) & 1) {
+                const uint64_t b = pb + (uint64_t)(yb - 2 + j) * A.nx + 32ull * kw;
+                const uint64_t wi = b >> 5;
+                const uint32_t sh = (uint32_t)(b & 31);
+                v = __ldg(src + wi);
+                if (sh) v = __funnelshift_r(v, wi + 1 < sw ? __ldg(src + wi + 1) : 0u, sh);
+                v |= padm;
+            }
+            mw[j] = v;
+        }
+    };
+
+    uint32_t m0[MRW], m1[MRW], m2[MRW];   // m of planes p-2, p-1, p
+    uint32_t e0[ERW], e1[ERW], e2[ERW];   // e of planes p-3, p-2, p-1
+#pragma unroll
+    for (int j = 0; j < MRW; j++) m0[j] = FULL;
+    load_plane(zs - 2, m1);
+    load_plane(zs - 1, m2);
+#pragma unroll
+    for (int j = 0; j < ERW; j++) e0[j] = e1[j] = e2[j] = 0u;
+    // e rows yb-1+j exist iff bit j+1 of vmask (same column, row offset by one)
+    const uint32_t emask = vmask >> 1;
+    uint32_t *const o_base = A.o;
+    for (int p = zs; p <= ze + 1; p++) {
+#pragma unroll
+        for (int j = 0; j < MRW; j++) {
+            m0[j] = m1[j];
+            m1[j] = m2[j];
+        }
+        load_plane(p, m2);
+#pragma unroll
+        for (int j = 0; j < ERW; j++) {
+            e0[j] = e1[j];
+            e1[j] = e2[j];
+        }
+        // e(p-1), rows yb-1+j
+        const int64_t gq = z0 + p - 1;
+        const bool qin = gq >= 0 && gq < gz;
+#pragma unroll
+        for (int j = 0; j < ERW; j++) {
+            const uint32_t c = m1[j + 1];
+            const uint32_t lw = __shfl_up_sync(FULL, c, 1), rw = __shfl_down_sync(FULL, c, 1);
+            const uint32_t l = __funnelshift_l(lane == 0 ? FULL : lw, c, 1);
+            const uint32_t r = __funnelshift_r(c, lane == 31 ? FULL : rw, 1);
+            const uint32_t v = c & l & r & m1[j] & m1[j + 2] & m0[j + 1] & m2[j + 1];
+            e2[j] = (qin && ((emask >> j) & 1)) ? (v & ~padm) : 0u;
+        }
+        // o(p-2), rows yb+j
+        const int z = p - 2;
+        if (z >= zs) {
+            uint32_t *orow = o_base + (uint64_t)z * plane_w;
+#pragma unroll
+            for (int j = 0; j < RY; j++) {
+                const uint32_t c = e1[j + 1];
+                const uint32_t lw = __shfl_up_sync(FULL, c, 1), rw = __shfl_down_sync(FULL, c, 1);
+                uint32_t o = c | e1[j] | e1[j + 2] | e0[j + 1] | e2[j + 1];
+                o |= __funnelshift_l(lane == 0 ? 0u : lw, c, 1) | __funnelshift_r(c, lane == 31 ? 0u : rw, 1);
+                o &= ~padm;
+                const int y = yb + j;
+                const uint32_t prev = __shfl_up_sync(FULL, o, 1);
+                const bool live = y < Y;
+                uint32_t cnt = 0;
+                if (out_lane && live) {
+                    if (aligned) orow[roff[j + 2]] = o;
+                    else write_row_atomic(A.o, ((uint64_t)z * A.ny + y) * A.nx, (uint32_t)kw, o);
+                    cnt = __popc(o & ~((o << 1) | ((kw > 0) ? (prev >> 31) : 0u)));
+                }
+                cnt = __reduce_add_sync(FULL, cnt);
+                if (lane == 0 && cnt && live && A.row_runs) atomicAdd(&A.row_runs[(uint64_t)z * A.ny + y], cnt);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------- fused 3-D binarise + opening (x-tiled)
+// A CTA owns a tile of FX = 256 voxels (8 words) x TY rows of every plane of a z-chunk and marches
+// along z.  The raw rows of plane p + NSLOT - 1 are streamed into a shared-memory ring by TMA bulk
+// copies (cp.async.bulk, completion on an mbarrier per slot) while plane p is binarised and opened,
+// so x is read once (plus one 16-byte group on each side of every row -- the +-2 voxel reach of the
+// opening -- and 2 halo rows per band side, mostly L2 hits from the neighbouring tiles) and m never
+// leaves the SM.  Requires X % 256 == 0 (otherwise binarise + open3d).
+// Shared m / e rows: words -1 .. 8 of the tile (index 0 .. 9); words -1 / 8 hold the halo bits.
+constexpr int FX = 256, FW = FX / 32, FWS = FW + 2, NSLOT = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <typename T, int TY>
+__global__ void __launch_bounds__(256) k_morph3d_fused(const T *__restrict__ x, MorphArgs A, roix_scalars *sc) {
+    constexpr int VPL = Cmp<T>::VPL;
+    constexpr int NG = FX / VPL;                // 16-byte groups per tile row
+    constexpr int GPL = NG / 32;                // main groups per lane (u16 1, f32 2)
+    constexpr int MR = TY + 4, ER = TY + 2;
+    constexpr int RB = FX * (int)sizeof(T) + 32;  // raw row: [left halo 16 B][main][right halo 16 B]
+    extern __shared__ __align__(128) unsigned char raw[];   // [NSLOT][MR][RB]
+    __shared__ __align__(8) uint64_t bars[NSLOT];
+    __shared__ uint32_t mring[3][MR][FWS];
+    __shared__ uint32_t ering[3][ER][FWS];
+    if (get_err(sc)) return;
+    const Cmp<T> cmp(sc);
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+    const int64_t X = A.nx, Y = A.ny;
+    const int64_t x0 = (int64_t)blockIdx.x * FX;
+    const int64_t y0 = (int64_t)blockIdx.y * TY;
+    const int64_t zs = (int64_t)blockIdx.z * A.zchunk;
+    const int64_t ze = min((int64_t)A.nz, zs + (int64_t)A.zchunk);
+    if (zs >= ze) return;
+    const bool has_l = x0 > 0, has_r = x0 + FX < X;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSLOT; i++) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int64_t p_first = zs - 2, p_last = ze + 1;
+    // warp 0: stream the in-slab rows of plane p into its ring slot
+    auto issue = [&](int64_t p) {
+        const int slot = (int)((p - p_first) % NSLOT);
+        unsigned char *base = raw + (size_t)slot * MR * RB;
+        const bool in = p >= 0 && p < (int64_t)A.nz;
+        int y_lo = (int)max((int64_t)0, y0 - 2), y_hi = (int)min(Y, y0 + TY + 2);
+        const uint32_t nrows = in && y_hi > y_lo ? (uint32_t)(y_hi - y_lo) : 0u;
+        const uint32_t rbytes = FX * sizeof(T) + (has_l ? 16 : 0) + (has_r ? 16 : 0);
+        if (lane == 0) mbar_arrive_expect_tx(&bars[slot], nrows * rbytes);
+        __syncwarp();
+        for (uint32_t i = lane; i < nrows; i += 32) {
+            const int64_t y = y_lo + i;
+            const int r = (int)(y - (y0 - 2));
+            const T *src = x + ((uint64_t)p * A.ny + y) * A.nx + x0;
+            unsigned char *dst = base + (size_t)r * RB + 16;
+            if (has_l) {
+                src -= 16 / sizeof(T);
+                dst -= 16;
+            }
+            bulk_g2s(dst, src, rbytes, &bars[slot]);
+        }
+    };
+    if (warp == 0)
+        for (int64_t p = p_first; p < p_first + NSLOT - 1 && p <= p_last; p++) issue(p);
+    for (int64_t p = p_first; p <= p_last; p++) {
+        const int slot = (int)((p - p_first) % NSLOT);
+        const uint32_t parity = (uint32_t)(((p - p_first) / NSLOT) & 1);
+        // 1. m(p) from the ring slot (or a halo plane / the volume border)
+        mbar_wait(&bars[slot], parity);
+        {
+            const int64_t gp = (int64_t)A.z0 + p;
+            const bool in_slab = p >= 0 && p < (int64_t)A.nz;
+            const unsigned char *base = raw + (size_t)slot * MR * RB;
+            for (int r = warp; r < MR; r += 8) {
+                const int64_t y = y0 - 2 + r;
+                uint32_t *dst = mring[(p + 3) % 3][r];
+                if (y < 0 || y >= Y || gp < 0 || gp >= (int64_t)A.gz) {
+                    if (lane < FWS) dst[lane] = FULL;
+                    continue;
+                }
+                if (!in_slab) {   // halo plane from the neighbouring slab (packed m bits of the whole plane)
+                    const uint64_t plane_w = (A.ny * A.nx + 31) / 32;
+                    const uint32_t *src = p < 0 ? A.halo_lo + (uint64_t)(p + 2) * plane_w
+                                                : A.halo_hi + (uint64_t)(p - A.nz) * plane_w;
+                    const uint64_t w0 = ((uint64_t)y * A.nx + x0) >> 5;   // X % 256 == 0: word aligned
+                    if (lane < FWS) {
+                        const int k = (int)lane - 1;
+                        uint32_t v = FULL;
+                        if ((k >= 0 && k < FW) || (k < 0 && has_l) || (k == FW && has_r)) v = src[w0 + k];
+                        dst[lane] = v;
+                    }
+                    continue;
+                }
+                const unsigned char *row = base + (size_t)r * RB;
+                uint32_t P = 0;
+#pragma unroll
+                for (int c = 0; c < GPL; c++)
+                    P |= cmp.bits(*reinterpret_cast<const uint4 *>(row + 16 + (c * 32 + lane) * 16)) << (c * VPL);
+                constexpr int GW = 32 / VPL;            // groups per word
+                const uint32_t cc = (lane * GW) / 32;   // register chunk holding word `lane`'s groups
+                uint32_t w = 0;
+#pragma unroll
+                for (int q = 0; q < GW; q++) {
+                    const uint32_t v = __shfl_sync(FULL, P, (lane * GW + q) % 32);
+                    w |= ((v >> (cc * VPL)) & ((1u << VPL) - 1u)) << (q * VPL);
+                }
+                if (lane < FW) dst[lane + 1] = w;
+                if (lane == FW)
+                    dst[0] = has_l ? ((cmp.bits(*reinterpret_cast<const uint4 *>(row)) << (32 - VPL)) | low_mask(32 - VPL))
+                                   : FULL;
+                if (lane == FW + 1)
+                    dst[FW + 1] = has_r ? (cmp.bits(*reinterpret_cast<const uint4 *>(row + 16 + FX * sizeof(T))) |
+                                           ~low_mask(VPL))
+                                        : FULL;
+            }
+        }
+        __syncthreads();   // slot p consumed, m(p) visible
+        if (warp == 0 && p + NSLOT - 1 <= p_last) issue(p + NSLOT - 1);   // reuses the slot of plane p - 1
+        // 2. e(q = p-1): rows y0-1 .. y0+TY, words -1 .. FW (index 0 .. FWS-1)
+        const int64_t q = p - 1;
+        if (q >= zs - 1) {
+            const int64_t gq = (int64_t)A.z0 + q;
+            const bool qin = gq >= 0 && gq < (int64_t)A.gz;
+            const uint32_t(*mc)[FWS] = mring[(q + 3) % 3];
+            const uint32_t(*mf)[FWS] = mring[(q + 2) % 3];
+            const uint32_t(*mg)[FWS] = mring[(q + 4) % 3];
+            for (int t = threadIdx.x; t < ER * FWS; t += blockDim.x) {
+                const int r = t / FWS, k = t % FWS;
+                const int64_t y = y0 - 1 + r;
+                uint32_t v = 0;
+                if (qin && y >= 0 && y < Y && !(k == 0 && !has_l) && !(k == FWS - 1 && !has_r)) {
+                    const uint32_t cw = mc[r + 1][k];
+                    const uint32_t l = k > 0 ? __funnelshift_l(mc[r + 1][k - 1], cw, 1) : (cw << 1) | 1u;
+                    const uint32_t rr = k < FWS - 1 ? __funnelshift_r(cw, mc[r + 1][k + 1], 1) : (cw >> 1) | 0x80000000u;
+                    v = cw & l & rr & mc[r][k] & mc[r + 2][k] & mf[r + 1][k] & mg[r + 1][k];
+                }
+                ering[(q + 3) % 3][r][k] = v;
+            }
+        }
+        __syncthreads();
+        // 3. o(z = p-2): rows y0 .. y0+TY-1, words 0 .. FW-1, plus the run starts of the row segment
+        const int64_t z = p - 2;
+        if (z >= zs && z < ze) {
+            const uint32_t(*ec)[FWS] = ering[(z + 3) % 3];
+            const uint32_t(*ef)[FWS] = ering[(z + 2) % 3];
+            const uint32_t(*eg)[FWS] = ering[(z + 4) % 3];
+            for (int t = threadIdx.x; t < TY * FW; t += blockDim.x) {
+                const int r = t / FW, k = t % FW + 1;   // k: shared word index (1 .. FW)
+                const int64_t y = y0 + r;
+                const bool live = y < Y;
+                uint32_t o = 0, prev31 = 0;
+                if (live) {
+                    auto dil = [&](int kk) {
+                        const uint32_t cw = ec[r + 1][kk];
+                        uint32_t v = cw | ec[r][kk] | ec[r + 2][kk] | ef[r + 1][kk] | eg[r + 1][kk];
+                        v |= kk > 0 ? __funnelshift_l(ec[r + 1][kk - 1], cw, 1) : (cw << 1);
+                        v |= kk < FWS - 1 ? __funnelshift_r(cw, ec[r + 1][kk + 1], 1) : (cw >> 1);
+                        return v;
+                    };
+                    o = dil(k);
+                    // bit 31 of the previous word (word -1 only needs bit 31: its e bits 30, 31 are exact)
+                    prev31 = (k > 1 || has_l) ? (dil(k - 1) >> 31) : 0u;
+                }
+                const uint32_t starts = o & ~((o << 1) | prev31);
+                const uint64_t row = (uint64_t)z * A.ny + y;
+                if (live) A.o[(row * A.nx + x0) / 32 + (k - 1)] = o;
+                // run starts of this row segment: its 8 words sit in 8 consecutive lanes
+                uint32_t cnt = __popc(starts);
+                cnt += __shfl_xor_sync(FULL, cnt, 1);
+                cnt += __shfl_xor_sync(FULL, cnt, 2);
+                cnt += __shfl_xor_sync(FULL, cnt, 4);
+                if (live && A.row_runs && (lane & 7) == 0 && cnt) atomicAdd(&A.row_runs[row], cnt);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------------------------ 2-D opening
 // Rows r = q*Y + y of the slab (q = plane); neighbours only within the same plane.  S = rows per
 // step = warps per CTA.  The output rows of a step are contiguous bits [c X, (c+S) X) of o; they are
@@ -550,6 +899,31 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     A.m = m;
     A.m_words = nwords;
     cudaError_t e;
+    if (se == 6 && g.nx % FX == 0 && A.async < 0) {   // disabled: slower than binarise + k_open3d_reg
+        // fused: x -> o in one pass (m stays on chip)
+        const bool u16 = dtype == ROIX_U16;
+        const int TY = u16 ? 32 : 16;
+        const uint64_t xt = g.nx / FX, bands = (g.ny + TY - 1) / TY;
+        const uint64_t target = (uint64_t)num_sms() * 4;
+        uint64_t chunks = (target + xt * bands - 1) / (xt * bands);
+        const uint64_t cmax = g.nz >= 128 ? g.nz / 64 : 1;
+        if (chunks > cmax) chunks = cmax;
+        if (chunks < 1) chunks = 1;
+        A.zchunk = (g.nz + chunks - 1) / chunks;
+        chunks = (g.nz + A.zchunk - 1) / A.zchunk;
+        if (row_runs && (e = cudaMemsetAsync(row_runs, 0, g.nz * g.ny * 4, st)) != cudaSuccess) return e;
+        dim3 grid((unsigned)xt, (unsigned)bands, (unsigned)chunks);
+        if (u16) {
+            const size_t sm = (size_t)NSLOT * (32 + 4) * (FX * 2 + 32);
+            if ((e = set_smem(k_morph3d_fused<uint16_t, 32>, sm)) != cudaSuccess) return e;
+            k_morph3d_fused<uint16_t, 32><<<grid, 256, sm, st>>>((const uint16_t *)x, A, sc);
+        } else {
+            const size_t sm = (size_t)NSLOT * (16 + 4) * (FX * 4 + 32);
+            if ((e = set_smem(k_morph3d_fused<float, 16>, sm)) != cudaSuccess) return e;
+            k_morph3d_fused<float, 16><<<grid, 256, sm, st>>>((const float *)x, A, sc);
+        }
+        return cudaGetLastError();
+    }
     // a4: stream x -> m
     {
         uint64_t iters = (n + 1023) / 1024;
@@ -562,34 +936,21 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     }
     int occ = 0;
     if (se == 6) {
-        // band height: the largest of 64/32/16/8 rows whose rings fit ~100 KB (2+ CTAs per SM) and
-        // that still gives >= 1.5 CTAs per SM with z-chunks of >= 64 planes
-        const uint64_t chunks_max = g.nz >= 128 ? g.nz / 64 : 1;
-        A.WS = (A.W + 8 + 3) / 4 * 4;
-        A.async = (g.nx % 128 == 0);
-        int TY = 64;
-        auto smem_of = [&](int ty) { return (size_t)(MSLOTS * (ty + 4) + 3 * (ty + 2)) * A.WS * 4; };
-        while (TY > 4 && smem_of(TY) > 72 * 1024) TY /= 2;
-        while (TY > 8 && ((g.ny + TY - 1) / TY) * chunks_max < (uint64_t)(1.5 * num_sms())) TY /= 2;
-        if ((uint64_t)TY > g.ny) TY = (int)g.ny;
-        A.TY = TY;
-        size_t sm = smem_of(TY);
-        if (sm > 220 * 1024) return cudaErrorInvalidConfiguration;
-        if ((e = set_smem(k_open3d, sm)) != cudaSuccess) return e;
-        cudaFuncSetAttribute(k_open3d, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_open3d, 256, sm)) != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-        uint64_t bands = (g.ny + TY - 1) / TY;
-        uint64_t slots = (uint64_t)num_sms() * occ;
-        uint64_t chunks = (slots + bands - 1) / bands;
+        constexpr int RY = 4;
+        const uint64_t npx = (A.W + 29) / 30, nry = (g.ny + RY - 1) / RY;
+        const uint64_t per_chunk = npx * nry;
+        const uint64_t target_warps = (uint64_t)num_sms() * 64;
+        uint64_t chunks = (target_warps + per_chunk - 1) / per_chunk;
+        const uint64_t cmax = g.nz >= 64 ? g.nz / 32 : 1;
+        if (chunks > cmax) chunks = cmax;
         if (chunks < 1) chunks = 1;
-        if (chunks > chunks_max) chunks = chunks_max;
         A.zchunk = (g.nz + chunks - 1) / chunks;
         chunks = (g.nz + A.zchunk - 1) / A.zchunk;
         A.aligned_out = (g.nx % 32 == 0);
         if (!A.aligned_out && (e = cudaMemsetAsync(o_bits, 0, nwords * 4, st)) != cudaSuccess) return e;
-        dim3 grid((unsigned)bands, (unsigned)chunks);
-        k_open3d<<<grid, 256, sm, st>>>(A, sc);
+        if (row_runs && (e = cudaMemsetAsync(row_runs, 0, g.nz * g.ny * 4, st)) != cudaSuccess) return e;
+        const uint64_t tasks = per_chunk * chunks;
+        k_open3d_reg<RY><<<(unsigned)((tasks + 7) / 8), 256, 0, st>>>(A, sc);
     } else {
         const int S = 8;
         size_t sm = (size_t)((S + 4) + (S + 2) + S) * A.WS * 4;

@@ -156,7 +156,8 @@ def test_threshold_f32_vs_oracle():
 
 # ------------------------------------------------------------------------- a4 + a5 binarise + open
 MORPH_SHAPES = [(1, 1, 1), (1, 1, 40), (2, 3, 5), (3, 5, 7), (5, 33, 65), (7, 64, 64), (9, 17, 100),
-                (4, 70, 139), (3, 20, 1390), (11, 9, 256), (6, 40, 96), (33, 8, 32)]
+                (4, 70, 139), (3, 20, 1390), (11, 9, 256), (6, 40, 96), (33, 8, 32),
+                (5, 17, 768), (9, 40, 512), (3, 3, 1024), (130, 5, 256)]   # X % 256 == 0: fused 3-D path
 
 
 def _morph_gpu(x_np, thr, pol, se):
