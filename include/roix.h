@@ -201,6 +201,48 @@ roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const r
                        const roix_label_out *out, roix_scalars *sc, roix_stream_t stream);
 
 /*
+ * Sharded labelling (z-slab decomposition over GPUs).  roix_label above equals
+ * roix_label_local followed by roix_label_finish with an empty merge map.  For a volume split into
+ * z-slabs (one per rank), each rank:
+ *   1. roix_label_local on its slab (runs, union-find, sizes of the slab-local components);
+ *   2. roix_label_boundary(side = 1) exports the runs of its last plane (to rank + 1);
+ *   3. roix_label_link pairs its first-plane components with the previous rank's last-plane runs;
+ *   4. roix_label_boundary_roots lists (label, size) of its components touching either slab face;
+ *   5. all ranks gather every pair list and root table, and roix_merge (host, deterministic
+ *      union-by-min) maps each boundary label to its merged label and total size;
+ *   6. roix_label_finish applies the map: table entries live on the rank holding the component's
+ *      minimum index; small-object removal uses the merged sizes.
+ * Labels are global linear indices (uint64).  ws / run_capacity are those of roix_label_local.
+ */
+typedef struct roix_brun {
+    uint32_t y, x0, x1, pad; /* row within the plane, run [x0, x1)                    */
+    uint64_t label;          /* global label (min linear index) of its local component  */
+} roix_brun;
+
+roix_status roix_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
+                             uint64_t run_capacity, void *ws, size_t ws_bytes, roix_scalars *sc,
+                             roix_stream_t stream);
+roix_status roix_label_boundary(const void *ws, const roix_geom *g, uint64_t run_capacity, int side, roix_brun *out,
+                                uint64_t out_cap, uint64_t *count, roix_scalars *sc, roix_stream_t stream);
+roix_status roix_label_link(const void *ws, const roix_geom *g, uint64_t run_capacity, uint32_t conn,
+                            const roix_brun *prev, const uint64_t *n_prev, uint64_t *pairs, uint64_t pair_cap,
+                            uint64_t *n_pairs, roix_scalars *sc, roix_stream_t stream);
+roix_status roix_label_boundary_roots(const void *ws, const roix_geom *g, uint64_t run_capacity, uint64_t *labels,
+                                      uint64_t *sizes, uint64_t out_cap, uint64_t *count, roix_scalars *sc,
+                                      roix_stream_t stream);
+/* HOST memory, no GPU work: pairs[2k], pairs[2k+1] are labels of one component; labels / sizes the
+ * boundary components of all slabs.  Outputs (capacity nlabels): the distinct labels in increasing
+ * order with their merged label and total size; *nout = their number.  ROIX_E_INVALID if a pair
+ * names a label missing from `labels`. */
+roix_status roix_merge(const uint64_t *pairs, uint64_t npairs, const uint64_t *labels, const uint64_t *sizes,
+                       uint64_t nlabels, uint64_t *out_label, uint64_t *out_final, uint64_t *out_total,
+                       uint64_t *nout);
+roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64_t min_size, uint64_t run_capacity,
+                              void *ws, size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
+                              const uint64_t *map_total, uint64_t nmap, const roix_label_out *out, roix_scalars *sc,
+                              roix_stream_t stream);
+
+/*
  * a1+a8 EXTRACT.  For the set bits i_0 < i_1 < ... of keep_bits (n voxels), codes_out[j] =
  * RNE(x[i_j] / s) (u16 -> uint16, fp32 -> int32), written at codes_out[offset + j].  Adds the
  * number of set bits to sc->count.  Reads x only where keep_bits has set bits.  More than

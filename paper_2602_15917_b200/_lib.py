@@ -37,6 +37,11 @@ class LabelOut(ctypes.Structure):
                 ("comp_kept", ctypes.c_void_p), ("comp_cap", ctypes.c_uint64), ("labels", ctypes.c_void_p)]
 
 
+class BRun(ctypes.Structure):
+    _fields_ = [("y", ctypes.c_uint32), ("x0", ctypes.c_uint32), ("x1", ctypes.c_uint32), ("pad", ctypes.c_uint32),
+                ("label", ctypes.c_uint64)]
+
+
 class RoixError(RuntimeError):
     pass
 
@@ -61,6 +66,13 @@ _SIGS = {
     "roix_label_workspace": (_i32, [ctypes.POINTER(Geom), _u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_label": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _u32, _u64, _u64, _vp, ctypes.c_size_t,
                           ctypes.POINTER(LabelOut), _vp, _vp]),
+    "roix_label_local": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _u32, _u64, _vp, ctypes.c_size_t, _vp, _vp]),
+    "roix_label_boundary": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _i32, _vp, _u64, _vp, _vp, _vp]),
+    "roix_label_link": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _vp]),
+    "roix_label_boundary_roots": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, _vp, _u64, _vp, _vp, _vp]),
+    "roix_merge": (_i32, [_vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
+    "roix_label_finish": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _u64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _u64,
+                                 ctypes.POINTER(LabelOut), _vp, _vp]),
     "roix_extract_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_extract": (_i32, [_vp, _i32, _u64, _vp, _vp, _vp, _u64, _vp, _vp, ctypes.c_size_t, _vp]),
 }
@@ -106,6 +118,29 @@ roix_morph = _wrap("roix_morph")
 roix_binarize_planes = _wrap("roix_binarize_planes")
 roix_label = _wrap("roix_label")
 roix_extract = _wrap("roix_extract")
+roix_label_local = _wrap("roix_label_local")
+roix_label_boundary = _wrap("roix_label_boundary")
+roix_label_link = _wrap("roix_label_link")
+roix_label_boundary_roots = _wrap("roix_label_boundary_roots")
+roix_label_finish = _wrap("roix_label_finish")
+
+
+def roix_merge(pairs, labels, sizes):
+    """Host merge (numpy uint64 arrays): pairs (k, 2), labels (m,), sizes (m,) ->
+    (labels, final_labels, totals) for the distinct labels in increasing order."""
+    import numpy as np
+
+    pairs = np.ascontiguousarray(pairs, dtype=np.uint64).reshape(-1)
+    labels = np.ascontiguousarray(labels, dtype=np.uint64)
+    sizes = np.ascontiguousarray(sizes, dtype=np.uint64)
+    m = labels.size
+    ol, of, ot = (np.empty(max(m, 1), np.uint64) for _ in range(3))
+    nout = ctypes.c_uint64()
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(load().roix_merge(p(pairs), pairs.size // 2, p(labels), p(sizes), m, p(ol), p(of), p(ot),
+                             ctypes.byref(nout)), "roix_merge")
+    k = nout.value
+    return ol[:k].copy(), of[:k].copy(), ot[:k].copy()
 
 
 def roix_label_workspace(geom, run_capacity):

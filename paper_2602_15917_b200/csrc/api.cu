@@ -3,7 +3,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 #include "roix.h"
@@ -179,10 +181,130 @@ roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const r
     if (ws_bytes < need) return invalid("workspace too small (see roix_label_workspace)");
     if (out->comp_min && (!out->comp_size || out->comp_cap == 0)) return invalid("comp_size / comp_cap");
     if (g->z0 != 0 || g->nz != g->gz) {
-        if (conn != 4 && conn != 8) return unsupported("sharded 3-D labelling goes through the slab-merge path");
+        if (conn != 4 && conn != 8) return unsupported("sharded 3-D labelling: use roix_label_local ... finish");
     }
     return cuda(launch_label(o_bits, row_runs, *g, conn, min_size, run_capacity, ws, *out, sc, (cudaStream_t)stream),
                 "roix_label");
+}
+
+static roix_status label_common(const roix_geom *g, uint64_t cap, const void *ws, size_t ws_bytes) {
+    if (!ws) return invalid("ws is NULL");
+    size_t need = 0;
+    roix_status s = roix_label_workspace(g, cap, &need);
+    if (s != ROIX_OK) return s;
+    if (ws_bytes < need) return invalid("workspace too small (see roix_label_workspace)");
+    return ROIX_OK;
+}
+
+roix_status roix_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
+                             uint64_t run_capacity, void *ws, size_t ws_bytes, roix_scalars *sc,
+                             roix_stream_t stream) {
+    if (!sc || !o_bits) return invalid("sc / o_bits is NULL");
+    if (conn != 4 && conn != 8 && conn != 6 && conn != 18 && conn != 26) return unsupported("conn (4, 8, 6, 18, 26)");
+    roix_status s = label_common(g, run_capacity, ws, ws_bytes);
+    if (s != ROIX_OK) return s;
+    return cuda(launch_label_local(o_bits, row_runs, *g, conn, run_capacity, ws, sc, (cudaStream_t)stream),
+                "roix_label_local");
+}
+
+roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64_t min_size, uint64_t run_capacity,
+                              void *ws, size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
+                              const uint64_t *map_total, uint64_t nmap, const roix_label_out *out, roix_scalars *sc,
+                              roix_stream_t stream) {
+    if (!sc || !o_bits || !out) return invalid("sc / o_bits / out is NULL");
+    if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
+    if (out->comp_min && (!out->comp_size || out->comp_cap == 0)) return invalid("comp_size / comp_cap");
+    roix_status s = label_common(g, run_capacity, ws, ws_bytes);
+    if (s != ROIX_OK) return s;
+    return cuda(launch_label_finish(o_bits, *g, min_size, run_capacity, ws, map_label, map_final, map_total, nmap, *out,
+                                    sc, (cudaStream_t)stream),
+                "roix_label_finish");
+}
+
+roix_status roix_label_boundary(const void *ws, const roix_geom *g, uint64_t run_capacity, int side, roix_brun *out,
+                                uint64_t out_cap, uint64_t *count, roix_scalars *sc, roix_stream_t stream) {
+    if (!sc || !count || (out_cap && !out)) return invalid("sc / count / out is NULL");
+    if (side != 0 && side != 1) return invalid("side must be 0 (first plane) or 1 (last plane)");
+    roix_status s = label_common(g, run_capacity, ws, (size_t)-1);
+    if (s != ROIX_OK) return s;
+    return cuda(launch_label_boundary(ws, *g, run_capacity, side, out, out_cap, count, sc, (cudaStream_t)stream),
+                "roix_label_boundary");
+}
+
+roix_status roix_label_link(const void *ws, const roix_geom *g, uint64_t run_capacity, uint32_t conn,
+                            const roix_brun *prev, const uint64_t *n_prev, uint64_t *pairs, uint64_t pair_cap,
+                            uint64_t *n_pairs, roix_scalars *sc, roix_stream_t stream) {
+    if (!sc || !prev || !n_prev || !n_pairs || (pair_cap && !pairs)) return invalid("NULL pointer");
+    if (conn != 6 && conn != 18 && conn != 26) return unsupported("cross-slab links need a 3-D conn (6, 18, 26)");
+    roix_status s = label_common(g, run_capacity, ws, (size_t)-1);
+    if (s != ROIX_OK) return s;
+    return cuda(launch_label_link(ws, *g, run_capacity, conn, prev, n_prev, pairs, pair_cap, n_pairs, sc,
+                                  (cudaStream_t)stream),
+                "roix_label_link");
+}
+
+roix_status roix_label_boundary_roots(const void *ws, const roix_geom *g, uint64_t run_capacity, uint64_t *labels,
+                                      uint64_t *sizes, uint64_t out_cap, uint64_t *count, roix_scalars *sc,
+                                      roix_stream_t stream) {
+    if (!sc || !count || (out_cap && (!labels || !sizes))) return invalid("NULL pointer");
+    roix_status s = label_common(g, run_capacity, ws, (size_t)-1);
+    if (s != ROIX_OK) return s;
+    return cuda(launch_label_boundary_roots(ws, *g, run_capacity, labels, sizes, out_cap, count, sc,
+                                            (cudaStream_t)stream),
+                "roix_label_boundary_roots");
+}
+
+// Host union-find over the boundary components of all slabs: union by minimum label, so every
+// merged component is named by its minimum global linear index (G-14) whatever the pair order.
+roix_status roix_merge(const uint64_t *pairs, uint64_t npairs, const uint64_t *labels, const uint64_t *sizes,
+                       uint64_t nlabels, uint64_t *out_label, uint64_t *out_final, uint64_t *out_total,
+                       uint64_t *nout) {
+    if (!nout || (nlabels && (!labels || !sizes || !out_label || !out_final || !out_total)) || (npairs && !pairs))
+        return invalid("NULL pointer");
+    std::vector<std::pair<uint64_t, uint64_t>> ls(nlabels);
+    for (uint64_t i = 0; i < nlabels; i++) ls[i] = {labels[i], sizes[i]};
+    std::sort(ls.begin(), ls.end());
+    std::vector<uint64_t> L, S;
+    for (auto &p : ls)
+        if (L.empty() || L.back() != p.first) {
+            L.push_back(p.first);
+            S.push_back(p.second);
+        }
+    const size_t m = L.size();
+    std::vector<uint64_t> parent(m);
+    for (size_t i = 0; i < m; i++) parent[i] = i;
+    auto find = [&](uint64_t a) {
+        while (parent[a] != a) {
+            parent[a] = parent[parent[a]];
+            a = parent[a];
+        }
+        return a;
+    };
+    auto index = [&](uint64_t lab, uint64_t *out) {
+        auto it = std::lower_bound(L.begin(), L.end(), lab);
+        if (it == L.end() || *it != lab) return false;
+        *out = (uint64_t)(it - L.begin());
+        return true;
+    };
+    for (uint64_t k = 0; k < npairs; k++) {
+        uint64_t a, b;
+        if (!index(pairs[2 * k], &a) || !index(pairs[2 * k + 1], &b)) return invalid("pair label not in the tables");
+        a = find(a);
+        b = find(b);
+        if (a == b) continue;
+        if (a < b) parent[b] = a;   // indices are in label order: the smaller label wins
+        else parent[a] = b;
+    }
+    std::vector<uint64_t> tot(m, 0);
+    for (size_t i = 0; i < m; i++) tot[find(i)] += S[i];
+    for (size_t i = 0; i < m; i++) {
+        const uint64_t r = find(i);
+        out_label[i] = L[i];
+        out_final[i] = L[r];
+        out_total[i] = tot[r];
+    }
+    *nout = m;
+    return ROIX_OK;
 }
 
 roix_status roix_extract_workspace(uint64_t n, size_t *ws_bytes) {

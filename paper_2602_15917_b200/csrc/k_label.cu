@@ -391,35 +391,75 @@ __global__ void k_flatten_sizes(LabelWS W, roix_scalars *sc) {
     }
 }
 
-// cidx flags: 1 for roots
-__global__ void k_root_flags(LabelWS W, roix_scalars *sc) {
-    if (get_err(sc)) return;
-    const uint64_t n = W.ctr[0];
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        W.cidx[i] = W.parent[i] == (uint32_t)i;
+// ------------------------------------------------------------------ finish: table, filter, K
+// Merge map (sharded volumes): sorted global labels of this slab's boundary components with their
+// merged label (the global minimum index of the merged component) and total size.  nmap = 0 on a
+// single GPU.
+struct MapView {
+    const uint64_t *label, *final_label, *total;
+    uint64_t n;
+};
+
+__device__ __forceinline__ uint64_t gidx(const LGeo &G, const LabelWS &W, uint32_t i) {
+    return ((G.z0 * G.ny) + W.rrow[i]) * G.nx + W.x0[i];
 }
 
-__global__ void k_table(LGeo G, uint64_t min_size, LabelWS W, const uint32_t *cscan, roix_label_out out,
-                        roix_scalars *sc) {
+// (final label, total size) of local root i
+__device__ __forceinline__ void resolve_root(const LGeo &G, const LabelWS &W, const MapView &M, uint32_t i,
+                                             uint64_t &fin, uint64_t &tot) {
+    const uint64_t L = gidx(G, W, i);
+    fin = L;
+    tot = W.size[i];
+    uint64_t lo = 0, hi = M.n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (M.label[mid] < L) lo = mid + 1;
+        else hi = mid;
+    }
+    if (lo < M.n && M.label[lo] == L) {
+        fin = M.final_label[lo];
+        tot = M.total[lo];
+    }
+}
+
+// cidx flags: 1 for local roots that own a table entry (their label is the merged component's label)
+__global__ void k_root_flags(LGeo G, LabelWS W, MapView M, uint64_t min_size, roix_scalars *sc) {
     if (get_err(sc)) return;
     const uint64_t n = W.ctr[0];
     uint32_t nk = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (W.parent[i] != (uint32_t)i) continue;
-        const uint64_t sz = W.size[i];
-        const uint8_t kp = sz >= min_size;
-        W.kept[i] = kp;
-        nk += kp;
-        const uint64_t c = cscan[i];
-        if (out.comp_min && c < out.comp_cap) {
-            out.comp_min[c] = ((G.z0 * G.ny) + W.rrow[i]) * G.nx + W.x0[i];
-            out.comp_size[c] = sz;
-            if (out.comp_kept) out.comp_kept[c] = kp;
+        uint32_t f = 0;
+        if (W.parent[i] == (uint32_t)i) {
+            uint64_t fin, tot;
+            resolve_root(G, W, M, (uint32_t)i, fin, tot);
+            const uint8_t kp = tot >= min_size;
+            W.kept[i] = kp;
+            f = fin == gidx(G, W, (uint32_t)i);
+            nk += f & kp;
         }
+        W.cidx[i] = f;
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) nk += __shfl_xor_sync(FULL, nk, d);
     if (lane_id() == 0 && nk) atomicAdd((unsigned long long *)&W.ctr[2], (unsigned long long)nk);
+}
+
+__global__ void k_table(LGeo G, LabelWS W, MapView M, const uint32_t *cscan, roix_label_out out, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    if (!out.comp_min) return;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (W.parent[i] != (uint32_t)i) continue;
+        uint64_t fin, tot;
+        resolve_root(G, W, M, (uint32_t)i, fin, tot);
+        if (fin != gidx(G, W, (uint32_t)i)) continue;
+        const uint64_t c = cscan[i];
+        if (c < out.comp_cap) {
+            out.comp_min[c] = fin;
+            out.comp_size[c] = tot;
+            if (out.comp_kept) out.comp_kept[c] = W.kept[i];
+        }
+    }
 }
 
 __global__ void k_table_total(const uint64_t *nroots, LabelWS W, roix_label_out out, roix_scalars *sc) {
@@ -446,15 +486,113 @@ __global__ void k_clear_dropped(LGeo G, LabelWS W, uint32_t *K, roix_scalars *sc
     }
 }
 
-__global__ void k_labels(LGeo G, LabelWS W, uint64_t *labels, roix_scalars *sc) {
+__global__ void k_labels(LGeo G, LabelWS W, MapView M, uint64_t *labels, roix_scalars *sc) {
     if (get_err(sc)) return;
     const uint64_t n = W.ctr[0];
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t rt = W.parent[i];
-        const uint64_t lab = ((G.z0 * G.ny) + W.rrow[rt]) * G.nx + W.x0[rt];
+        uint64_t lab, tot;
+        resolve_root(G, W, M, W.parent[i], lab, tot);
         const uint64_t base = (uint64_t)W.rrow[i] * G.nx;
         for (uint32_t x = W.x0[i]; x < W.x1[i]; x++) labels[base + x] = lab;
     }
+}
+
+// ------------------------------------------------------------------ sharded volumes: slab faces
+// runs of the slab's first (side 0) or last (side 1) plane, with their local root's global label
+__global__ void k_boundary_runs(LGeo G, LabelWS W, int side, roix_brun *out, uint64_t cap, uint64_t *count,
+                                roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t r0 = side ? (G.nz - 1) * G.ny : 0, r1 = r0 + G.ny;
+    const uint32_t a = W.row_start[r0], b = W.row_start[r1];
+    const uint64_t nb = W.ctr[0] ? (uint64_t)(b - a) : 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *count = nb;
+        if (nb > cap) set_err(sc, ROIX_ERR_CAPACITY);
+    }
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nb && k < cap; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = a + (uint32_t)k;
+        roix_brun rr;
+        rr.y = (uint32_t)(W.rrow[i] - r0);
+        rr.x0 = W.x0[i];
+        rr.x1 = W.x1[i];
+        rr.pad = 0;
+        rr.label = gidx(G, W, W.parent[i]);
+        out[k] = rr;
+    }
+}
+
+// pairs (label of this slab's first-plane component, label of the previous slab's last-plane one)
+__global__ void k_link(LGeo G, LabelWS W, int ci, const roix_brun *prev, const uint64_t *n_prev, uint64_t *pairs,
+                       uint64_t pair_cap, uint64_t *n_pairs, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint32_t a = W.row_start[0], b = W.row_start[G.ny];
+    const uint64_t np = *n_prev;
+    if (!W.ctr[0]) return;
+    // cross-plane neighbourhood rows (dz = -1) per connectivity: dy range and x extension
+    const int dymax = (ci == 4 || ci == 3) ? 1 : 0;   // 26: all dy; 18: dy != 0 only without x extension
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < (uint64_t)(b - a); k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = a + (uint32_t)k;
+        const int64_t y = W.rrow[i];
+        const uint32_t x0 = W.x0[i], x1 = W.x1[i];
+        const uint64_t mylab = gidx(G, W, W.parent[i]);
+        for (int dy = -dymax; dy <= dymax; dy++) {
+            const int64_t yy = y + dy;
+            if (yy < 0 || yy >= (int64_t)G.ny) continue;
+            const uint32_t ext = (ci == 4 || (ci == 3 && dy == 0)) ? 1u : 0u;
+            // first prev run with (y, x1 + ext) > (yy, x0)
+            uint64_t lo = 0, hi = np;
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) >> 1;
+                const roix_brun r = prev[mid];
+                if ((int64_t)r.y < yy || ((int64_t)r.y == yy && r.x1 + ext <= x0)) lo = mid + 1;
+                else hi = mid;
+            }
+            for (uint64_t j = lo; j < np; j++) {
+                const roix_brun r = prev[j];
+                if ((int64_t)r.y != yy || r.x0 >= x1 + ext) break;
+                const unsigned long long at = atomicAdd((unsigned long long *)n_pairs, 1ull);
+                if (at < pair_cap) {
+                    pairs[2 * at] = mylab;
+                    pairs[2 * at + 1] = r.label;
+                } else {
+                    set_err(sc, ROIX_ERR_CAPACITY);
+                }
+            }
+        }
+    }
+}
+
+// (label, size) of the local components touching the slab's first or last plane
+__global__ void k_mark_boundary(LGeo G, LabelWS W, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    if (!W.ctr[0]) return;
+    const uint32_t ranges[4] = {W.row_start[0], W.row_start[G.ny], W.row_start[(G.nz - 1) * G.ny],
+                                W.row_start[G.nz * G.ny]};
+    for (int s = 0; s < 2; s++)
+        for (uint64_t i = ranges[2 * s] + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ranges[2 * s + 1];
+             i += (uint64_t)gridDim.x * blockDim.x)
+            W.kept[W.parent[i]] = 2;   // scratch mark (kept[] is rewritten by the finish phase)
+}
+
+__global__ void k_boundary_roots(LGeo G, LabelWS W, uint64_t *labels, uint64_t *sizes, uint64_t cap, uint64_t *count,
+                                 roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (W.parent[i] != (uint32_t)i || W.kept[i] != 2) continue;
+        const unsigned long long at = atomicAdd((unsigned long long *)count, 1ull);
+        if (at < cap) {
+            labels[at] = gidx(G, W, (uint32_t)i);
+            sizes[at] = W.size[i];
+        } else {
+            set_err(sc, ROIX_ERR_CAPACITY);
+        }
+    }
+}
+
+__global__ void k_clear_marks(LabelWS W) {
+    const uint64_t n = W.ctr[0];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) W.kept[i] = 0;
 }
 
 }  // namespace roix
@@ -470,46 +608,64 @@ static int ctas(uint64_t work, int threads) {
     return (int)(need < cap ? need : cap);
 }
 
-cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
-                         uint64_t min_size, uint64_t cap, void *ws, const roix_label_out &out, roix_scalars *sc,
-                         cudaStream_t st) {
-    LabelWS W;
-    carve(ws, g, cap, &W);
+static LGeo make_geo(const roix_geom &g) {
     LGeo G;
     G.nz = g.nz;
     G.ny = g.ny;
     G.nx = g.nx;
     G.z0 = g.z0;
     G.W = (uint32_t)((g.nx + 31) / 32);
+    return G;
+}
+
+static int conn_index(uint32_t conn) { return conn == 4 ? 0 : conn == 8 ? 1 : conn == 6 ? 2 : conn == 18 ? 3 : 4; }
+
+// a6 on the slab: runs, union (block-local then cross-block), flatten, sizes
+cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
+                               uint64_t cap, void *ws, roix_scalars *sc, cudaStream_t st) {
+    LabelWS W;
+    carve(ws, g, cap, &W);
+    const LGeo G = make_geo(g);
     const uint64_t rows = g.nz * g.ny, n = rows * g.nx, nwords = (n + 31) / 32;
-    int ci = conn == 4 ? 0 : conn == 8 ? 1 : conn == 6 ? 2 : conn == 18 ? 3 : 4;
+    const int ci = conn_index(conn);
     cudaError_t e;
     const uint32_t *rr = row_runs;
     if (!rr) {
         k_count_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W.row_runs, sc);
         rr = W.row_runs;
     }
-    // row_start = exclusive scan of the counts; total at scan_tmp[...]
     if ((e = scan_u32(rr, W.row_start, rows, W.scan_tmp, st)) != cudaSuccess) return e;
     k_runs_total<<<1, 1, 0, st>>>(scan_total_ptr(W.scan_tmp, rows), cap, W, sc);
     const int runs_grid = num_sms() * 8;
     k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, sc);
-    {
-        static bool attr = false;
-        if (!attr) {
-            if ((e = cudaFuncSetAttribute(k_union_local, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          UB_RUNS * 4)) != cudaSuccess)
-                return e;
-            attr = true;
-        }
-        const uint64_t nub = (cap + UB_RUNS - 1) / UB_RUNS;
-        k_union_local<<<(unsigned)nub, UB_THREADS, UB_RUNS * 4, st>>>(G, ci, W, sc);
-        k_union_cross<<<runs_grid, 256, 0, st>>>(W, sc);
+    static bool attr = false;
+    if (!attr) {
+        if ((e = cudaFuncSetAttribute(k_union_local, cudaFuncAttributeMaxDynamicSharedMemorySize, UB_RUNS * 4)) !=
+            cudaSuccess)
+            return e;
+        attr = true;
     }
+    const uint64_t nub = (cap + UB_RUNS - 1) / UB_RUNS;
+    k_union_local<<<(unsigned)nub, UB_THREADS, UB_RUNS * 4, st>>>(G, ci, W, sc);
+    k_union_cross<<<runs_grid, 256, 0, st>>>(W, sc);
     k_flatten_sizes<<<runs_grid, 256, 0, st>>>(W, sc);
-    k_root_flags<<<runs_grid, 256, 0, st>>>(W, sc);
+    return cudaGetLastError();
+}
+
+// a7: resolve every local root through the merge map, component table, kept flags, K, labels
+cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint64_t min_size, uint64_t cap, void *ws,
+                                const uint64_t *map_label, const uint64_t *map_final, const uint64_t *map_total,
+                                uint64_t nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st) {
+    LabelWS W;
+    carve(ws, g, cap, &W);
+    const LGeo G = make_geo(g);
+    const uint64_t n = g.nz * g.ny * g.nx, nwords = (n + 31) / 32;
+    const MapView M = {map_label, map_final, map_total, nmap};
+    const int runs_grid = num_sms() * 8;
+    cudaError_t e;
+    k_root_flags<<<runs_grid, 256, 0, st>>>(G, W, M, min_size, sc);
     if ((e = scan_u32_dev(W.cidx, W.cidx, W.ctr, cap, W.scan_tmp, st)) != cudaSuccess) return e;
-    k_table<<<runs_grid, 256, 0, st>>>(G, min_size, W, W.cidx, out, sc);
+    k_table<<<runs_grid, 256, 0, st>>>(G, W, M, W.cidx, out, sc);
     k_table_total<<<1, 1, 0, st>>>(scan_total_ptr(W.scan_tmp, cap), W, out, sc);
     if (out.keep_bits) {
         if (out.keep_bits != o_bits &&
@@ -519,7 +675,49 @@ cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const
     }
     if (out.labels) {
         if ((e = cudaMemsetAsync(out.labels, 0xff, n * 8, st)) != cudaSuccess) return e;
-        k_labels<<<runs_grid, 256, 0, st>>>(G, W, out.labels, sc);
+        k_labels<<<runs_grid, 256, 0, st>>>(G, W, M, out.labels, sc);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
+                         uint64_t min_size, uint64_t cap, void *ws, const roix_label_out &out, roix_scalars *sc,
+                         cudaStream_t st) {
+    cudaError_t e = launch_label_local(o_bits, row_runs, g, conn, cap, ws, sc, st);
+    if (e != cudaSuccess) return e;
+    return launch_label_finish(o_bits, g, min_size, cap, ws, nullptr, nullptr, nullptr, 0, out, sc, st);
+}
+
+cudaError_t launch_label_boundary(const void *ws, const roix_geom &g, uint64_t cap, int side, roix_brun *out,
+                                  uint64_t out_cap, uint64_t *count, roix_scalars *sc, cudaStream_t st) {
+    LabelWS W;
+    carve((void *)ws, g, cap, &W);
+    k_boundary_runs<<<num_sms() * 2, 256, 0, st>>>(make_geo(g), W, side, out, out_cap, count, sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_label_link(const void *ws, const roix_geom &g, uint64_t cap, uint32_t conn, const roix_brun *prev,
+                              const uint64_t *n_prev, uint64_t *pairs, uint64_t pair_cap, uint64_t *n_pairs,
+                              roix_scalars *sc, cudaStream_t st) {
+    LabelWS W;
+    carve((void *)ws, g, cap, &W);
+    cudaError_t e = cudaMemsetAsync(n_pairs, 0, 8, st);
+    if (e != cudaSuccess) return e;
+    k_link<<<num_sms() * 2, 256, 0, st>>>(make_geo(g), W, conn_index(conn), prev, n_prev, pairs, pair_cap, n_pairs, sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_label_boundary_roots(const void *ws, const roix_geom &g, uint64_t cap, uint64_t *labels,
+                                        uint64_t *sizes, uint64_t out_cap, uint64_t *count, roix_scalars *sc,
+                                        cudaStream_t st) {
+    LabelWS W;
+    carve((void *)ws, g, cap, &W);
+    const LGeo G = make_geo(g);
+    cudaError_t e = cudaMemsetAsync(count, 0, 8, st);
+    if (e != cudaSuccess) return e;
+    const int grid = num_sms() * 8;
+    k_clear_marks<<<grid, 256, 0, st>>>(W);
+    k_mark_boundary<<<grid, 256, 0, st>>>(G, W, sc);
+    k_boundary_roots<<<grid, 256, 0, st>>>(G, W, labels, sizes, out_cap, count, sc);
     return cudaGetLastError();
 }

@@ -34,3 +34,17 @@ cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const
 size_t extract_workspace_bytes(uint64_t n);
 cudaError_t launch_extract(const void *x, int dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
                            void *codes, uint64_t capacity, const uint64_t *offset, void *ws, cudaStream_t st);
+
+cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
+                               uint64_t cap, void *ws, roix_scalars *sc, cudaStream_t st);
+cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint64_t min_size, uint64_t cap, void *ws,
+                                const uint64_t *map_label, const uint64_t *map_final, const uint64_t *map_total,
+                                uint64_t nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st);
+cudaError_t launch_label_boundary(const void *ws, const roix_geom &g, uint64_t cap, int side, roix_brun *out,
+                                  uint64_t out_cap, uint64_t *count, roix_scalars *sc, cudaStream_t st);
+cudaError_t launch_label_link(const void *ws, const roix_geom &g, uint64_t cap, uint32_t conn, const roix_brun *prev,
+                              const uint64_t *n_prev, uint64_t *pairs, uint64_t pair_cap, uint64_t *n_pairs,
+                              roix_scalars *sc, cudaStream_t st);
+cudaError_t launch_label_boundary_roots(const void *ws, const roix_geom &g, uint64_t cap, uint64_t *labels,
+                                        uint64_t *sizes, uint64_t out_cap, uint64_t *count, roix_scalars *sc,
+                                        cudaStream_t st);

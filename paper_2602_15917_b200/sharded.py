@@ -1,0 +1,312 @@
+"""The ROIX hot path on a z-slab sharded volume.
+
+Slab g of G holds planes [floor(g Z / G), floor((g+1) Z / G)).  Every global dependency of the path
+is one exchange step:
+
+  X2  fp32 range       all-reduce MIN / MAX of the slab ranges           (relative eb, I_max)
+  X1  histogram        all-reduce SUM of the slab histograms             (identical Otsu threshold)
+  X3  morphology halo  each slab sends its first / last two binarised planes to its z-neighbours
+  X4  CCL merge        each slab sends its last plane's runs to the next slab, which links them with
+                       its first plane; all pair lists and boundary-component tables are gathered and
+                       every rank runs the same union-by-min (roix_merge), so merged labels and sizes
+                       agree everywhere; small-object removal then uses the merged sizes
+  X5  stream offsets   all-gather of the slab counts (rank g's codes start at sum_{r<g} count_r)
+
+The per-slab work is a generator (``slab_program``) that yields at each exchange; ``DistComm`` runs one
+slab per process over torch.distributed (NCCL on B200s, gloo on CPU), ``SimComm`` runs all slabs in one
+process on one GPU, in lockstep (the G-invariance tests).  Every compute step is a libroix call.
+"""
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .pipeline import Pipeline, _ptr
+
+
+def slab_bounds(Z, G, g):
+    return g * Z // G, (g + 1) * Z // G
+
+
+class SlabState(Pipeline):
+    """Pipeline buffers for one slab, plus the exchange buffers of the sharded path."""
+
+    def __init__(self, shape, dtype, *, z0, nz, rank, world, **kw):
+        Z, Y, X = shape
+        self.global_shape = tuple(shape)
+        self.rank, self.world, self.z0, self.nz = rank, world, z0, nz
+        super().__init__((nz, Y, X), dtype, **kw)
+        self.geom = L.Geom(nz, Y, X, z0, Z)            # slab geometry in the global volume
+        self.ws_bytes = L.roix_label_workspace(self.geom, self.run_capacity)
+        self.label_ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+        self.plane_w = (Y * X + 31) // 32
+        dev = self.device
+        self.halo_send = torch.zeros(2, 2 * self.plane_w + 4, dtype=torch.int32, device=dev)   # [lo, hi]
+        self.halo_recv = torch.zeros(2, 2 * self.plane_w + 4, dtype=torch.int32, device=dev)
+        self.brun_cap = Y * ((X + 1) // 2) + 1
+        self.brun = torch.empty(self.brun_cap * 3, dtype=torch.int64, device=dev)   # roix_brun = 24 bytes
+        self.brun_prev = torch.empty_like(self.brun)
+        self.counts = torch.zeros(4, dtype=torch.int64, device=dev)   # [n_brun, n_prev, n_pairs, n_roots]
+        self.pair_cap = 4 * self.brun_cap
+        self.pairs = torch.empty(2 * self.pair_cap, dtype=torch.int64, device=dev)
+        self.root_cap = 2 * self.brun_cap
+        self.root_lab = torch.empty(self.root_cap, dtype=torch.int64, device=dev)
+        self.root_size = torch.empty(self.root_cap, dtype=torch.int64, device=dev)
+
+    def _alloc_label(self, cap):
+        super()._alloc_label(cap)
+        if hasattr(self, "global_shape"):
+            self.ws_bytes = L.roix_label_workspace(self.geom, cap)
+            self.label_ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+
+    def cptr(self, i):
+        return ctypes.c_void_p(self.counts.data_ptr() + 8 * i)
+
+
+def slab_program(S, x, stream=None):
+    """Generator: enqueue this slab's work; yield at every exchange (see module doc)."""
+    st = ctypes.c_void_p((stream or torch.cuda.current_stream(S.device)).cuda_stream)
+    sc, xp, n = _ptr(S.sc), _ptr(x), S.n
+    G, g = S.world, S.rank
+    L.roix_scalars_init(sc, S.eb, st)
+    if S.cdtype == L.F32:
+        L.roix_range(xp, n, sc, st)
+        yield ("minmax", S.sc)                                    # X2
+    L.roix_resolve(sc, S.cdtype, S.rel_eb, st)
+    S.hist.zero_()
+    L.roix_histogram(xp, S.cdtype, n, sc, _ptr(S.hist), S.nbins, st)
+    yield ("sum", S.hist)                                         # X1
+    L.roix_threshold(_ptr(S.hist), S.nbins, S.cdtype, S.polarity, sc, st)
+    halo_lo = halo_hi = None
+    if S.se == 6 and G > 1:
+        if S.nz < 2:
+            raise ValueError("every slab needs >= 2 planes for the opening's halo")
+        pw = S.plane_w
+        L.roix_binarize_planes(xp, S.cdtype, ctypes.byref(S.geom), 0, 2, sc, _ptr(S.halo_send[0]), st)
+        L.roix_binarize_planes(xp, S.cdtype, ctypes.byref(S.geom), S.nz - 2, 2, sc, _ptr(S.halo_send[1]), st)
+        yield ("halo", S.halo_send, S.halo_recv)                  # X3
+        if g > 0:
+            halo_lo = _ptr(S.halo_recv[0])
+        if g < G - 1:
+            halo_hi = _ptr(S.halo_recv[1])
+        assert pw > 0
+    L.roix_morph(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o), _ptr(S.row_runs),
+                 _ptr(S.morph_ws), S.morph_ws.numel(), st)
+    out = L.LabelOut(S.o.data_ptr(), S.comp_min.data_ptr(), S.comp_size.data_ptr(), S.comp_kept.data_ptr(),
+                     S.comp_cap, S.labels.data_ptr() if S.labels is not None else None)
+    geo = ctypes.byref(S.geom)
+    if S.conn in (6, 18, 26) and G > 1:
+        ws, wsb, cap = _ptr(S.label_ws), S.ws_bytes, S.run_capacity
+        L.roix_label_local(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, cap, ws, wsb, sc, st)
+        L.roix_label_boundary(ws, geo, cap, 1, _ptr(S.brun), S.brun_cap, S.cptr(0), sc, st)
+        yield ("shift", S)                                        # X4a: last-plane runs -> next slab
+        S.counts[2].zero_()
+        if g > 0:
+            L.roix_label_link(ws, geo, cap, S.conn, _ptr(S.brun_prev), S.cptr(1), _ptr(S.pairs), S.pair_cap,
+                              S.cptr(2), sc, st)
+        L.roix_label_boundary_roots(ws, geo, cap, _ptr(S.root_lab), _ptr(S.root_size), S.root_cap, S.cptr(3),
+                                    sc, st)
+        gathered = yield ("gather_tables", S)                     # X4b: every slab's pairs and roots
+        pairs, labels, sizes = gathered
+        ml, mf, mt = L.roix_merge(pairs, labels, sizes)
+        S.map = torch.from_numpy(np.stack([ml, mf, mt]).view(np.int64)).to(S.device)
+        L.roix_label_finish(_ptr(S.o), geo, S.min_size, cap, ws, wsb, _ptr(S.map[0]), _ptr(S.map[1]),
+                            _ptr(S.map[2]), ml.size, ctypes.byref(out), sc, st)
+    else:
+        L.roix_label(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, S.min_size, S.run_capacity, _ptr(S.label_ws),
+                     S.ws_bytes, ctypes.byref(out), sc, st)
+    L.roix_extract(xp, S.cdtype, n, _ptr(S.o), sc, _ptr(S.codes), S.code_capacity, None, _ptr(S.ex_ws),
+                   S.ex_ws.numel(), st)
+    counts = yield ("counts", S)                                  # X5
+    S.offset = int(sum(counts[:g]))
+    S.global_count = int(sum(counts))
+
+
+def _count_of(S):
+    off = L.Scalars.count.offset
+    return S.sc[off:off + 8].view(torch.int64)
+
+
+def _read_tables(S):
+    if S.device.type == "cuda":
+        torch.cuda.synchronize(S.device)
+    c = S.counts.cpu().numpy()
+    npairs, nroots = int(min(c[2], S.pair_cap)), int(min(c[3], S.root_cap))
+    pairs = S.pairs[: 2 * npairs].cpu().numpy().view(np.uint64).reshape(-1, 2)
+    return pairs, S.root_lab[:nroots].cpu().numpy().view(np.uint64), S.root_size[:nroots].cpu().numpy().view(np.uint64)
+
+
+# ------------------------------------------------------------------------------------- comms
+class SimComm:
+    """All slabs in one process on one device, advanced in lockstep (no kernel waits on another)."""
+
+    def run(self, states, xs):
+        gens = [slab_program(S, x) for S, x in zip(states, xs)]
+        msgs = [next(gen) for gen in gens]
+        while True:
+            kind = msgs[0][0]
+            assert all(m[0] == kind for m in msgs), "slabs diverged"
+            replies = self._do(kind, msgs, states)
+            nxt = []
+            done = 0
+            for gen, rep in zip(gens, replies):
+                try:
+                    nxt.append(gen.send(rep))
+                except StopIteration:
+                    done += 1
+            if done:
+                assert done == len(gens)
+                return
+            msgs = nxt
+
+    def _do(self, kind, msgs, states):
+        G = len(msgs)
+        if kind == "minmax":
+            lo = min(int(m[1][4:8].view(torch.int32).cpu().numpy().view(np.uint32)[0]) for m in msgs)
+            hi = max(int(m[1][8:12].view(torch.int32).cpu().numpy().view(np.uint32)[0]) for m in msgs)
+            for m in msgs:
+                m[1][4:12].copy_(torch.from_numpy(np.array([lo, hi], np.uint32).view(np.uint8)).to(m[1].device))
+            return [None] * G
+        if kind == "sum":
+            tot = sum(m[1] for m in msgs)
+            for m in msgs:
+                m[1].copy_(tot)
+            return [None] * G
+        if kind == "halo":
+            for g, m in enumerate(msgs):
+                if g > 0:
+                    m[2][0].copy_(msgs[g - 1][1][1])    # previous slab's last two planes
+                if g < G - 1:
+                    m[2][1].copy_(msgs[g + 1][1][0])    # next slab's first two planes
+            return [None] * G
+        if kind == "shift":
+            for g in range(1, G):
+                states[g].brun_prev.copy_(states[g - 1].brun)
+                states[g].counts[1].copy_(states[g - 1].counts[0])
+            return [None] * G
+        if kind == "gather_tables":
+            tabs = [_read_tables(S) for S in states]
+            pairs = np.concatenate([t[0] for t in tabs]).reshape(-1, 2)
+            labels = np.concatenate([t[1] for t in tabs])
+            sizes = np.concatenate([t[2] for t in tabs])
+            return [(pairs, labels, sizes)] * G
+        if kind == "counts":
+            c = [int(_count_of(S).item()) for S in states]
+            return [c] * G
+        raise ValueError(kind)
+
+
+class DistComm:
+    """One slab per process over torch.distributed (NCCL between B200s; gloo on CPU for tests)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist, self.group = dist, group
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+
+    def run(self, S, x):
+        gen = slab_program(S, x)
+        rep = None
+        try:
+            msg = next(gen)
+            while True:
+                rep = self._do(msg, S)
+                msg = gen.send(rep)
+        except StopIteration:
+            return
+
+    def _do(self, msg, S):
+        d, grp = self.dist, self.group
+        kind = msg[0]
+        if kind == "minmax":
+            v = msg[1][4:12].view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+            lo, hi = v[0:1].clone(), v[1:2].clone()
+            d.all_reduce(lo, op=d.ReduceOp.MIN, group=grp)
+            d.all_reduce(hi, op=d.ReduceOp.MAX, group=grp)
+            v = torch.cat([lo, hi])
+            msg[1][4:12].view(torch.int32).copy_(torch.where(v >= 2 ** 31, v - 2 ** 32, v).to(torch.int32))
+            return None
+        if kind == "sum":
+            d.all_reduce(msg[1], group=grp)
+            return None
+        if kind == "halo":
+            send, recv = msg[1], msg[2]
+            ops = []
+            g, G = self.rank, self.world
+            if g > 0:
+                ops += [d.P2POp(d.isend, send[0], g - 1, grp), d.P2POp(d.irecv, recv[0], g - 1, grp)]
+            if g < G - 1:
+                ops += [d.P2POp(d.isend, send[1], g + 1, grp), d.P2POp(d.irecv, recv[1], g + 1, grp)]
+            if ops:
+                for r in d.batch_isend_irecv(ops):
+                    r.wait()
+            return None
+        if kind == "shift":
+            # counts first, then only the used part of every slab's last-plane run list
+            allc = [torch.empty_like(S.counts[0:1]) for _ in range(self.world)]
+            d.all_gather(allc, S.counts[0:1].contiguous(), group=grp)
+            cnt = [int(c.item()) for c in allc]
+            m = max(1, min(max(cnt), S.brun_cap))
+            allb = [torch.empty(3 * m, dtype=torch.int64, device=S.device) for _ in range(self.world)]
+            d.all_gather(allb, S.brun[: 3 * m].contiguous(), group=grp)
+            if self.rank > 0:
+                S.brun_prev[: 3 * m].copy_(allb[self.rank - 1])
+                S.counts[1:2].copy_(allc[self.rank - 1])
+            return None
+        if kind == "gather_tables":
+            pairs, labels, sizes = _read_tables(S)
+            objs = [None] * self.world
+            d.all_gather_object(objs, (pairs, labels, sizes), group=grp)
+            return (np.concatenate([o[0] for o in objs]).reshape(-1, 2), np.concatenate([o[1] for o in objs]),
+                    np.concatenate([o[2] for o in objs]))
+        if kind == "counts":
+            c = _count_of(S).clone()
+            allc = [torch.empty_like(c) for _ in range(self.world)]
+            d.all_gather(allc, c, group=grp)
+            return [int(t.item()) for t in allc]
+        raise ValueError(kind)
+
+
+class ShardedPipeline:
+    """One rank's slab of a z-sharded volume over a torch.distributed group (used by bench.py)."""
+
+    def __init__(self, shape, dtype, *, z0, nz, group=None, device=None, **kw):
+        self.comm = DistComm(group)
+        self.S = SlabState(shape, dtype, z0=z0, nz=nz, rank=self.comm.rank, world=self.comm.world, device=device, **kw)
+
+    def enqueue(self, x, mark=None):
+        self.comm.run(self.S, x)
+
+    def run(self, x):
+        self.enqueue(x)
+        torch.cuda.synchronize(self.S.device)
+        s = self.S.scalars()
+        if s.err:
+            raise L.RoixError("device error bits 0x%x" % s.err)
+        return self.S.collect(s)
+
+    def scalars(self):
+        return self.S.scalars()
+
+    def local_count(self):
+        return int(self.S.scalars().count)
+
+    def launches(self):
+        return self.S.launches() + 8
+
+
+def run_simulated(x_full, G, *, shape=None, dtype=None, **kw):
+    """All G slabs of a volume on this GPU, in lockstep -- the G-invariance tests."""
+    Z = x_full.shape[0]
+    dtype = dtype or ("f32" if x_full.dtype == torch.float32 else "u16")
+    states, xs = [], []
+    for g in range(G):
+        z0, z1 = slab_bounds(Z, G, g)
+        states.append(SlabState(tuple(x_full.shape), dtype, z0=z0, nz=z1 - z0, rank=g, world=G,
+                                device=x_full.device, **kw))
+        xs.append(x_full[z0:z1].contiguous())
+    SimComm().run(states, xs)
+    torch.cuda.synchronize()
+    return states
