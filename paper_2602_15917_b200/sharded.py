@@ -306,7 +306,7 @@ def run_simulated(x_full, G, *, shape=None, dtype=None, **kw):
         z0, z1 = slab_bounds(Z, G, g)
         states.append(SlabState(tuple(x_full.shape), dtype, z0=z0, nz=z1 - z0, rank=g, world=G,
                                 device=x_full.device, **kw))
-        xs.append(x_full[z0:z1].contiguous())
+        xs.append(x_full[z0:z1].clone())   # fresh (16-byte aligned) allocation per slab
     SimComm().run(states, xs)
     torch.cuda.synchronize()
     return states
