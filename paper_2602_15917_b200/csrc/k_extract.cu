@@ -19,7 +19,8 @@ constexpr int EX_WORDS = 256;            // mask words per tile
 constexpr int EX_TILE = EX_WORDS * 32;   // voxels per tile
 
 struct ExWS {
-    uint32_t *tcount;   // [ntiles + 1]: per-tile counts, then exclusive offsets (scan output)
+    uint32_t *tcount;   // [ntiles]: per-tile counts
+    uint64_t *toff;     // [ntiles + 1]: exclusive offsets (scan output; totals exceed 2^32 at C3-C5)
     uint64_t *scan_tmp; // scan workspace
     uint32_t *err_snap;
 };
@@ -27,13 +28,15 @@ struct ExWS {
 static size_t ex_carve(void *base, uint64_t n, ExWS *w) {
     uint64_t ntiles = (n + EX_TILE - 1) / EX_TILE;
     size_t a = (((ntiles + 1) * 4) + 255) & ~(size_t)255;
+    size_t a2 = (((ntiles + 1) * 8) + 255) & ~(size_t)255;
     size_t b = ((scan_tmp_elems(ntiles) * 8) + 255) & ~(size_t)255;
     if (w) {
         w->tcount = (uint32_t *)base;
-        w->scan_tmp = (uint64_t *)((char *)base + a);
-        w->err_snap = (uint32_t *)((char *)base + a + b);
+        w->toff = (uint64_t *)((char *)base + a);
+        w->scan_tmp = (uint64_t *)((char *)base + a + a2);
+        w->err_snap = (uint32_t *)((char *)base + a + a2 + b);
     }
-    return a + b + 256;
+    return a + a2 + b + 256;
 }
 
 // pass 1: kept voxels per tile -- one warp per tile (256 words = 32 lanes x 2 x 16-byte loads),
@@ -102,7 +105,7 @@ __device__ __forceinline__ void extract_tile(const T *__restrict__ x, uint64_t n
     const uint32_t cnt = __popc(word);
     const uint32_t incl = warp_incl_scan(cnt);
     if (lane == 31) warp_tot[warp] = incl;
-    const uint64_t base = (offset ? *offset : 0) + w.tcount[tile];
+    const uint64_t base = (offset ? *offset : 0) + w.toff[tile];
     const uint32_t shift = (uint32_t)(base % PADE);
     const C *st = stage + shift;
     __syncthreads();
@@ -226,7 +229,7 @@ cudaError_t launch_extract(const void *x, int dtype, uint64_t n, const uint32_t 
     if (ntiles > 0x7fffffffull) return cudaErrorInvalidValue;
     uint64_t cg = (uint64_t)num_sms() * 8, need = (ntiles + 15) / 16;
     k_extract_count<<<(unsigned)(need < cg ? (need ? need : 1) : cg), EX_THREADS, 0, st>>>(keep_bits, n, ntiles, w, sc);
-    cudaError_t e = scan_u32(w.tcount, w.tcount, ntiles, w.scan_tmp, st);
+    cudaError_t e = scan_u32_u64(w.tcount, w.toff, ntiles, w.scan_tmp, st);
     if (e != cudaSuccess) return e;
     if (dtype == ROIX_U16)
         k_extract<uint16_t, uint16_t><<<(unsigned)ntiles, EX_THREADS, 0, st>>>(

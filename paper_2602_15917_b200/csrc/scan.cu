@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(uint64_t *tmp, uint64_t nb
     if (threadIdx.x == 0) tmp[nb] = carry;
 }
 
-__global__ void __launch_bounds__(SCAN_T) k_scan_down(const uint32_t *in, uint32_t *out, const uint64_t *len_dev,
+template <typename O>
+__global__ void __launch_bounds__(SCAN_T) k_scan_down(const uint32_t *in, O *out, const uint64_t *len_dev,
                                                       uint64_t len, const uint64_t *tmp, uint64_t nb) {
     __shared__ uint64_t sh[SCAN_T / 32];
     const uint64_t n = len_dev ? *len_dev : len;
@@ -83,29 +84,35 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_down(const uint32_t *in, uint32
 #pragma unroll
         for (int k = 0; k < SCAN_V; k++) {
             uint64_t i = base + (uint64_t)threadIdx.x * SCAN_V + k;
-            if (i < n) out[i] = (uint32_t)run;
+            if (i < n) out[i] = (O)run;
             run += v[k];
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         uint64_t t = tmp[nb];
-        out[n] = t > 0xffffffffull ? 0xffffffffu : (uint32_t)t;
+        out[n] = sizeof(O) == 4 ? (O)(t > 0xffffffffull ? 0xffffffffull : t) : (O)t;
     }
 }
 
-cudaError_t scan_impl(const uint32_t *in, uint32_t *out, const uint64_t *len_dev, uint64_t len, uint64_t maxlen,
-                             uint64_t *tmp, cudaStream_t st) {
+template <typename O>
+cudaError_t scan_impl(const uint32_t *in, O *out, const uint64_t *len_dev, uint64_t len, uint64_t maxlen, uint64_t *tmp,
+                      cudaStream_t st) {
     const uint64_t nb = scan_nblocks(maxlen);
     if (nb == 0) {
         // empty: total 0
         cudaError_t e = cudaMemsetAsync(tmp, 0, 8, st);
         if (e != cudaSuccess) return e;
-        return cudaMemsetAsync(out, 0, 4, st);
+        return cudaMemsetAsync(out, 0, sizeof(O), st);
     }
     k_scan_reduce<<<(unsigned)nb, SCAN_T, 0, st>>>(in, len_dev, len, tmp);
     k_scan_blocks<<<1, 1024, 0, st>>>(tmp, nb);
-    k_scan_down<<<(unsigned)nb, SCAN_T, 0, st>>>(in, out, len_dev, len, tmp, nb);
+    k_scan_down<O><<<(unsigned)nb, SCAN_T, 0, st>>>(in, out, len_dev, len, tmp, nb);
     return cudaGetLastError();
 }
+
+template cudaError_t scan_impl<uint32_t>(const uint32_t *, uint32_t *, const uint64_t *, uint64_t, uint64_t, uint64_t *,
+                                         cudaStream_t);
+template cudaError_t scan_impl<uint64_t>(const uint32_t *, uint64_t *, const uint64_t *, uint64_t, uint64_t, uint64_t *,
+                                         cudaStream_t);
 
 }  // namespace roix

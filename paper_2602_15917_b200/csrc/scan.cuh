@@ -13,11 +13,16 @@ __host__ __device__ inline uint64_t scan_nblocks(uint64_t maxlen) { return (maxl
 inline uint64_t scan_tmp_elems(uint64_t maxlen) { return scan_nblocks(maxlen) + 2; }
 inline const uint64_t *scan_total_ptr(const uint64_t *tmp, uint64_t maxlen) { return tmp + scan_nblocks(maxlen); }
 
-cudaError_t scan_impl(const uint32_t *in, uint32_t *out, const uint64_t *len_dev, uint64_t len, uint64_t maxlen,
-                      uint64_t *tmp, cudaStream_t st);
+template <typename O>
+cudaError_t scan_impl(const uint32_t *in, O *out, const uint64_t *len_dev, uint64_t len, uint64_t maxlen, uint64_t *tmp,
+                      cudaStream_t st);
 
 // host-known length; out must hold len + 1 elements
 inline cudaError_t scan_u32(const uint32_t *in, uint32_t *out, uint64_t len, uint64_t *tmp, cudaStream_t st) {
+    return scan_impl(in, out, nullptr, len, len, tmp, st);
+}
+// uint64 offsets (totals beyond 2^32); out must hold len + 1 elements
+inline cudaError_t scan_u32_u64(const uint32_t *in, uint64_t *out, uint64_t len, uint64_t *tmp, cudaStream_t st) {
     return scan_impl(in, out, nullptr, len, len, tmp, st);
 }
 // device-resident length (<= maxlen); out must hold maxlen + 1 elements

@@ -4,6 +4,7 @@ the launch configuration bench.py times, checked against the oracle where it can
 planes of the opening recomputed from 5 binarised planes, the code stream of sampled planes) and
 by properties that hold at any size for the rest (component table, kept mask)."""
 import ctypes
+import gc
 
 import numpy as np
 import pytest
@@ -45,6 +46,8 @@ def _plane_bits(words, bit0, nbits):
 @pytest.mark.parametrize("name", ["C3", "C4", "C5"])
 def test_fullsize(name):
     cfg = synth.CONFIGS[name]
+    gc.collect()
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if cfg.nbytes * 2.3 > free:
         pytest.skip("not enough device memory on this GPU")
@@ -117,5 +120,6 @@ def test_fullsize(name):
             for rid in np.unique(run_id[yy][run_id[yy] > 0]):
                 vals = kz2[yy][run_id[yy] == rid]
                 assert vals.min() == vals.max()
-    del x, p, o
+    del x, p, o, r, flat
+    gc.collect()
     torch.cuda.empty_cache()
