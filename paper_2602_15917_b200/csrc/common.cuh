@@ -44,7 +44,7 @@ __host__ __device__ __forceinline__ float ord2f(uint32_t o) {
 // Exact path (reading G-4): q = div.rn(x, s) is correctly rounded, and for |x/s| < 2^23 every
 // half-integer is representable, so fl(x/s) lands on k+1/2 only when x/s is within half an ulp of
 // it; then the sign of the residual x - q*s (one fma rounding, sign-exact) decides.
-__device__ __forceinline__ float rne_exact(float x, float s) {
+static __device__ __noinline__ float rne_exact(float x, float s) {
     float q = __fdiv_rn(x, s);
     float c = rintf(q);
     float fl = floorf(q);

@@ -76,102 +76,103 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract_count(const uint32_t *__
     }
 }
 
+// One tile = 256 mask words; warp w owns words 32w .. 32w+31 and lane l the word 32w + l, i.e. 32
+// consecutive voxels.  A lane loads only the 16-byte groups of its voxels with a kept bit, quantises
+// them branch-free, and writes its codes to the staging buffer at its position (the kept voxels of
+// the warps and words before it).  Groups are written in a lane-rotated order so the 16-byte shared
+// stores of neighbouring lanes (64 B / 128 B apart) hit different banks.
 template <typename T, typename C, int QM>
 __device__ __forceinline__ void extract_tile(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
                                              const ExWS &w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
                                              const uint64_t *offset, C *stage, uint32_t *warp_tot) {
     constexpr int VPL = 16 / sizeof(T);   // voxels per 16-byte group
-    constexpr int GPW = 32 / VPL;         // groups per mask word
-    constexpr int CH = 32 / VPL;          // 32-group chunks per warp (a warp covers 32 words = 1024 voxels)
+    constexpr int NG = 32 / VPL;          // groups per mask word (u16 4, f32 8)
     constexpr int PADE = 16 / sizeof(C);  // staging is shifted by base % PADE so that stores are 16-byte aligned
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     const uint64_t tile = blockIdx.x;
     const uint64_t nwords = (n + 31) / 32;
-    const uint64_t wbase = tile * EX_WORDS + warp * 32;
-    const uint32_t word = wbase + lane < nwords ? K[wbase + lane] : 0u;
-    // issue every x load of this warp before any dependent work
-    uint32_t m[CH];
-    uint4 d[CH];
-    const uint64_t gbase = wbase * 32;  // first voxel of the warp
+    const uint64_t wi = tile * EX_WORDS + warp * 32 + lane;
+    const uint32_t word = wi < nwords ? K[wi] : 0u;
+    const uint64_t v0 = wi * 32;            // first voxel of this lane's word
+    const bool full_word = v0 + 32 <= n;
+    // d[j] holds group (j + rot) % NG: the lane-rotated order (static register indices)
+    const int rot = (int)(sizeof(T) == 2 ? (lane >> 1) : lane);
+    uint4 d[NG];
 #pragma unroll
-    for (int c = 0; c < CH; c++) {
-        const uint32_t g = c * 32 + lane;
-        const uint32_t wv = __shfl_sync(FULL, word, g / GPW);
-        m[c] = (wv >> ((g % GPW) * VPL)) & ((1u << VPL) - 1u);
-        d[c] = make_uint4(0, 0, 0, 0);
-        const uint64_t v0 = gbase + (uint64_t)g * VPL;
-        if (m[c] && v0 + VPL <= n) d[c] = __ldcs(reinterpret_cast<const uint4 *>(x + v0));
+    for (int j = 0; j < NG; j++) {
+        const int g = (j + rot) & (NG - 1);
+        d[j] = make_uint4(0, 0, 0, 0);
+        if (((word >> (g * VPL)) & ((1u << VPL) - 1u)) && full_word)
+            d[j] = __ldg(reinterpret_cast<const uint4 *>(x + v0) + g);
     }
     const uint32_t cnt = __popc(word);
     const uint32_t incl = warp_incl_scan(cnt);
     if (lane == 31) warp_tot[warp] = incl;
     const uint64_t base = (offset ? *offset : 0) + w.toff[tile];
     const uint32_t shift = (uint32_t)(base % PADE);
-    const C *st = stage + shift;
     __syncthreads();
-    uint32_t run = 0, total = 0;
+    uint32_t wpre = 0, total = 0;
 #pragma unroll
     for (int k = 0; k < EX_THREADS / 32; k++) {
         uint32_t t = warp_tot[k];
-        if (k < (int)warp) run += t;
+        if (k < (int)warp) wpre += t;
         total += t;
     }
     const QP q = load_qp(sc);
     uint32_t err = 0;
+    const uint32_t a0 = shift + wpre + incl - cnt;   // stage index of this lane's first code
+    if (word) {
+        if (full_word) {
 #pragma unroll
-    for (int c = 0; c < CH; c++) {
-        const uint32_t pc = __popc(m[c]);
-        const uint32_t pos = warp_incl_scan(pc) - pc + run;
-        run = __shfl_sync(FULL, pos + pc, 31);
-        if (!m[c]) continue;
-        const uint32_t g = c * 32 + lane;
-        const uint64_t v0 = gbase + (uint64_t)g * VPL;
-        const uint32_t a = shift + pos;   // element index in stage[]
-        if (v0 + VPL <= n) {
-            if constexpr (sizeof(T) == 2) {
-                // 8 codes, packed in pairs
-                const uint32_t c0 = code_pair_u16_m<QM>(d[c].x, q, err), c1 = code_pair_u16_m<QM>(d[c].y, q, err),
-                               c2 = code_pair_u16_m<QM>(d[c].z, q, err), c3 = code_pair_u16_m<QM>(d[c].w, q, err);
-                if (m[c] == 0xffu) {
-                    if ((a & 7u) == 0) {
-                        *reinterpret_cast<uint4 *>(stage + a) = make_uint4(c0, c1, c2, c3);
-                    } else if ((a & 1u) == 0) {
-                        uint32_t *s32 = reinterpret_cast<uint32_t *>(stage + a);
-                        s32[0] = c0; s32[1] = c1; s32[2] = c2; s32[3] = c3;
+            for (int j = 0; j < NG; j++) {
+                const int g = (j + rot) & (NG - 1);   // rotated order
+                const uint32_t mg = (word >> (g * VPL)) & ((1u << VPL) - 1u);
+                if (!mg) continue;
+                const uint32_t a = a0 + __popc(word & low_mask(g * VPL));
+                if constexpr (sizeof(T) == 2) {
+                    const uint32_t c0 = code_pair_u16_m<QM>(d[j].x, q, err), c1 = code_pair_u16_m<QM>(d[j].y, q, err),
+                                   c2 = code_pair_u16_m<QM>(d[j].z, q, err), c3 = code_pair_u16_m<QM>(d[j].w, q, err);
+                    if (mg == 0xffu) {
+                        if ((a & 7u) == 0) {
+                            *reinterpret_cast<uint4 *>(stage + a) = make_uint4(c0, c1, c2, c3);
+                        } else if ((a & 1u) == 0) {
+                            uint32_t *s32 = reinterpret_cast<uint32_t *>(stage + a);
+                            s32[0] = c0; s32[1] = c1; s32[2] = c2; s32[3] = c3;
+                        } else {
+                            stage[a] = (C)(c0 & 0xffffu);
+                            uint32_t *s32 = reinterpret_cast<uint32_t *>(stage + a + 1);
+                            s32[0] = __funnelshift_r(c0, c1, 16);
+                            s32[1] = __funnelshift_r(c1, c2, 16);
+                            s32[2] = __funnelshift_r(c2, c3, 16);
+                            stage[a + 7] = (C)(c3 >> 16);
+                        }
                     } else {
-                        stage[a] = (C)(c0 & 0xffffu);
-                        uint32_t *s32 = reinterpret_cast<uint32_t *>(stage + a + 1);
-                        s32[0] = __funnelshift_r(c0, c1, 16);
-                        s32[1] = __funnelshift_r(c1, c2, 16);
-                        s32[2] = __funnelshift_r(c2, c3, 16);
-                        stage[a + 7] = (C)(c3 >> 16);
+                        const uint32_t cc[4] = {c0, c1, c2, c3};
+                        uint32_t pp = a;
+#pragma unroll
+                        for (int k = 0; k < 8; k++)
+                            if (mg >> k & 1) stage[pp++] = (C)((cc[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
                     }
                 } else {
-                    const uint32_t cc[4] = {c0, c1, c2, c3};
-                    uint32_t p = a;
+                    const int32_t k0 = code_f32(__uint_as_float(d[j].x), q, err), k1 = code_f32(__uint_as_float(d[j].y), q, err),
+                                  k2 = code_f32(__uint_as_float(d[j].z), q, err), k3 = code_f32(__uint_as_float(d[j].w), q, err);
+                    if (mg == 0xfu && (a & 3u) == 0) {
+                        *reinterpret_cast<int4 *>(stage + a) = make_int4(k0, k1, k2, k3);
+                    } else {
+                        const int32_t kk[4] = {k0, k1, k2, k3};
+                        uint32_t pp = a;
 #pragma unroll
-                    for (int k = 0; k < 8; k++)
-                        if (m[c] >> k & 1) stage[p++] = (C)((cc[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
-                }
-            } else {
-                const int32_t k0 = code_f32(__uint_as_float(d[c].x), q, err), k1 = code_f32(__uint_as_float(d[c].y), q, err),
-                              k2 = code_f32(__uint_as_float(d[c].z), q, err), k3 = code_f32(__uint_as_float(d[c].w), q, err);
-                if (m[c] == 0xfu && (a & 3u) == 0) {
-                    *reinterpret_cast<int4 *>(stage + a) = make_int4(k0, k1, k2, k3);
-                } else {
-                    const int32_t kk[4] = {k0, k1, k2, k3};
-                    uint32_t p = a;
-#pragma unroll
-                    for (int k = 0; k < 4; k++)
-                        if (m[c] >> k & 1) stage[p++] = (C)kk[k];
+                        for (int k = 0; k < 4; k++)
+                            if (mg >> k & 1) stage[pp++] = (C)kk[k];
+                    }
                 }
             }
-        } else {
-            uint32_t p = a;
-            for (int k = 0; k < VPL; k++)
-                if (m[c] >> k & 1) {
-                    if constexpr (sizeof(T) == 2) stage[p++] = (C)code_u16_m<QM>(x[v0 + k], q, err);
-                    else stage[p++] = (C)code_f32(x[v0 + k], q, err);
+        } else {   // the volume's last, partial word
+            uint32_t pp = a0;
+            for (int k = 0; k < 32; k++)
+                if ((word >> k & 1) && v0 + k < n) {
+                    if constexpr (sizeof(T) == 2) stage[pp++] = (C)code_u16_m<QM>(x[v0 + k], q, err);
+                    else stage[pp++] = (C)code_f32(x[v0 + k], q, err);
                 }
         }
     }
@@ -181,6 +182,7 @@ __device__ __forceinline__ void extract_tile(const T *__restrict__ x, uint64_t n
     // store [base, base + lim): scalar head up to the 16-byte boundary, 16-byte body, scalar tail
     const uint64_t lim = base < capacity ? min((uint64_t)total, capacity - base) : 0;
     const uint32_t head = (uint32_t)min((uint64_t)((PADE - shift) % PADE), lim);
+    const C *st = stage + shift;
     if (threadIdx.x < head) out[base + threadIdx.x] = st[threadIdx.x];
     const uint64_t nvec = (lim - head) / PADE;
     const uint4 *sv = reinterpret_cast<const uint4 *>(st + head);   // 16-byte aligned: (shift + head) % PADE == 0

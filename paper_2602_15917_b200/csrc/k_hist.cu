@@ -57,10 +57,18 @@ __global__ void __launch_bounds__(1024, 2) k_hist_u16(const uint16_t *__restrict
 
 // norm8 of a finite fp32 value from the edges table e[0..256] (e[0] = -inf, e[256] = +inf):
 // norm8(x) = #{k >= 1 : x >= e[k]} -- an estimate from x * 255 / I_max corrected against the edges.
-__device__ __forceinline__ int norm8_edges(float x, float scale, const float *e) {
+// x * fl(255 / I_max) is within ~3e-5 of the exact 255 x / I_max for x <= I_max, so the estimate is
+// within one bin of norm8(x) and one correction in each direction is exact.  `exact_est` is false
+// only for a subnormal I_max (255 / I_max overflows); the edges are then walked.
+__device__ __forceinline__ int norm8_edges(float x, float scale, const float *e, bool exact_est) {
     int k = __float2int_rz(fminf(fmaxf(x * scale + 0.5f, 0.0f), 255.0f));
-    while (x >= e[k + 1]) k++;
-    while (x < e[k]) k--;
+    if (exact_est) {
+        k += (x >= e[k + 1]);
+        k -= (x < e[k]);
+    } else {
+        while (x >= e[k + 1]) k++;
+        while (x < e[k]) k--;
+    }
     return k;
 }
 
@@ -75,6 +83,7 @@ __global__ void __launch_bounds__(512) k_hist_f32(const float *__restrict__ x, u
     }
     if (threadIdx.x == 0) e[256] = INFINITY;
     const float scale = 255.0f / sc->i_max;
+    const bool ex = scale <= 1e30f;
     __syncthreads();
     bool bad = false;
     const float4 *x4 = reinterpret_cast<const float4 *>(x);
@@ -84,13 +93,13 @@ __global__ void __launch_bounds__(512) k_hist_f32(const float *__restrict__ x, u
         float v[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            if (fabsf(v[k]) <= FLT_MAX) atomicAdd(&sh[norm8_edges(v[k], scale, e)], 1u);
+            if (fabsf(v[k]) <= FLT_MAX) atomicAdd(&sh[norm8_edges(v[k], scale, e, ex)], 1u);
             else bad = true;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
         float v = x[n4 * 4 + threadIdx.x];
-        if (fabsf(v) <= FLT_MAX) atomicAdd(&sh[norm8_edges(v, scale, e)], 1u);
+        if (fabsf(v) <= FLT_MAX) atomicAdd(&sh[norm8_edges(v, scale, e, ex)], 1u);
         else bad = true;
     }
     if (bad) set_err(sc, ROIX_ERR_NONFINITE);

@@ -33,8 +33,8 @@ struct LabelWS {
     uint64_t pair_cap;
 };
 
-constexpr int UB_RUNS = 16384;    // runs per union block (their parents live in shared memory)
-constexpr int UB_THREADS = 512;
+constexpr int UB_RUNS = 4096;     // runs per union block (their parents live in shared memory)
+constexpr int UB_THREADS = 256;
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
@@ -139,8 +139,10 @@ __device__ __forceinline__ void runs_of_chunk(uint32_t cw, uint32_t next_lane31,
     carry = __shfl_sync(FULL, cw, 31);
     uint32_t starts = cw & ~((cw << 1) | (prev >> 31));
     uint32_t ends = cw & ~((cw >> 1) | (next << 31));
+    if (!__any_sync(FULL, (starts | ends) != 0)) return;   // no run boundary in these 32 words
     const uint32_t ns = __popc(starts), ne = __popc(ends);
-    const uint32_t is = warp_incl_scan(ns) - ns, ie = warp_incl_scan(ne) - ne;
+    const uint32_t both = warp_incl_scan(ns | (ne << 16));  // both counts <= 32 * 16: one scan
+    const uint32_t is = (both & 0xffffu) - ns, ie = (both >> 16) - ne;
     uint32_t ps = b0 + sbase + is, pe = b0 + ebase + ie;
     while (starts) {
         const uint32_t bb = __ffs(starts) - 1;
@@ -154,8 +156,9 @@ __device__ __forceinline__ void runs_of_chunk(uint32_t cw, uint32_t next_lane31,
         ends &= ends - 1;
         x1[pe++] = 32 * k + bb + 1;
     }
-    sbase += __shfl_sync(FULL, is + ns, 31);
-    ebase += __shfl_sync(FULL, ie + ne, 31);
+    const uint32_t tot = __shfl_sync(FULL, both, 31);
+    sbase += tot & 0xffffu;
+    ebase += tot >> 16;
 }
 
 __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nwords,
@@ -296,9 +299,9 @@ __global__ void __launch_bounds__(UB_THREADS) k_union_local(LGeo G, int ci, Labe
     extern __shared__ uint32_t lp[];
     if (get_err(sc)) return;
     const uint64_t n = W.ctr[0];
-    const uint64_t base = (uint64_t)blockIdx.x * UB_RUNS;
-    if (base >= n) return;
+    for (uint64_t base = (uint64_t)blockIdx.x * UB_RUNS; base < n; base += (uint64_t)gridDim.x * UB_RUNS) {
     const uint32_t cnt = (uint32_t)min((uint64_t)UB_RUNS, n - base);
+    __syncthreads();   // the previous block of runs is finished with lp[]
     for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) lp[k] = k;
     __syncthreads();
     const int nnb = c_nnb[ci];
@@ -355,6 +358,7 @@ __global__ void __launch_bounds__(UB_THREADS) k_union_local(LGeo G, int ci, Labe
         }
         W.parent[base + k] = (uint32_t)(base + r);
         W.size[base + k] = 0;
+    }
     }
 }
 
@@ -645,7 +649,8 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
             return e;
         attr = true;
     }
-    const uint64_t nub = (cap + UB_RUNS - 1) / UB_RUNS;
+    uint64_t nub = (cap + UB_RUNS - 1) / UB_RUNS;
+    if (nub > (uint64_t)num_sms() * 6) nub = (uint64_t)num_sms() * 6;   // persistent over blocks of runs
     k_union_local<<<(unsigned)nub, UB_THREADS, UB_RUNS * 4, st>>>(G, ci, W, sc);
     k_union_cross<<<runs_grid, 256, 0, st>>>(W, sc);
     k_flatten_sizes<<<runs_grid, 256, 0, st>>>(W, sc);

@@ -464,12 +464,13 @@ __global__ void __launch_bounds__(256, 3) k_open3d_reg(MorphArgs A, roix_scalars
         }
     };
 
-    uint32_t m0[MRW], m1[MRW], m2[MRW];   // m of planes p-2, p-1, p
-    uint32_t e0[ERW], e1[ERW], e2[ERW];   // e of planes p-3, p-2, p-1
+    uint32_t m0[MRW], m1[MRW], m2[MRW], mn[MRW];   // m of planes p-2, p-1, p; mn: plane p+1 in flight
+    uint32_t e0[ERW], e1[ERW], e2[ERW];            // e of planes p-3, p-2, p-1
 #pragma unroll
     for (int j = 0; j < MRW; j++) m0[j] = FULL;
     load_plane(zs - 2, m1);
     load_plane(zs - 1, m2);
+    load_plane(zs, mn);
 #pragma unroll
     for (int j = 0; j < ERW; j++) e0[j] = e1[j] = e2[j] = 0u;
     // e rows yb-1+j exist iff bit j+1 of vmask (same column, row offset by one)
@@ -480,8 +481,9 @@ __global__ void __launch_bounds__(256, 3) k_open3d_reg(MorphArgs A, roix_scalars
         for (int j = 0; j < MRW; j++) {
             m0[j] = m1[j];
             m1[j] = m2[j];
+            m2[j] = mn[j];
         }
-        load_plane(p, m2);
+        if (p + 1 <= ze + 1) load_plane(p + 1, mn);   // prefetch: consumed in the next iteration
 #pragma unroll
         for (int j = 0; j < ERW; j++) {
             e0[j] = e1[j];
@@ -941,7 +943,7 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         const uint64_t per_chunk = npx * nry;
         const uint64_t target_warps = (uint64_t)num_sms() * 64;
         uint64_t chunks = (target_warps + per_chunk - 1) / per_chunk;
-        const uint64_t cmax = g.nz >= 64 ? g.nz / 32 : 1;
+        const uint64_t cmax = g.nz >= 16 ? g.nz / 8 : 1;   // >= 8 planes per warp (4 halo planes re-read from L2)
         if (chunks > cmax) chunks = cmax;
         if (chunks < 1) chunks = 1;
         A.zchunk = (g.nz + chunks - 1) / chunks;

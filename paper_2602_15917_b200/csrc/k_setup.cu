@@ -41,11 +41,12 @@ __global__ void __launch_bounds__(512) k_range(const float *__restrict__ x, uint
     const float4 *x4 = reinterpret_cast<const float4 *>(x);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i + stride < n4; i += 2 * stride) {
-        float4 a = __ldcs(x4 + i), b = __ldcs(x4 + i + stride);
-        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    for (; i + 3 * stride < n4; i += 4 * stride) {
+        float4 a = __ldcs(x4 + i), b = __ldcs(x4 + i + stride), c = __ldcs(x4 + i + 2 * stride),
+               d = __ldcs(x4 + i + 3 * stride);
+        float v[16] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
+        for (int k = 0; k < 16; k++) {
             bad |= !(fabsf(v[k]) <= FLT_MAX);
             lo = fminf(lo, v[k]);
             hi = fmaxf(hi, v[k]);
