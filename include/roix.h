@@ -84,6 +84,11 @@ typedef struct roix_scalars {
     uint64_t n_components;/* a6: number of components (this slab's table)                        */
     uint64_t n_kept;      /* a7: number of kept components                                       */
     uint64_t n_runs;      /* a6: number of foreground x-runs found                               */
+    uint32_t spec_lo;     /* fused a2+a4: speculative raw-threshold window (u16 value / fp32 bits)  */
+    uint32_t spec_hi;
+    uint32_t spec_state;  /* 0 none, 1 window set, 2 mask resolved, 3 fallback binarisation       */
+    uint32_t reserved1;
+    uint64_t n_uncertain; /* fused a2+a4: voxels inside the window (resolved after the threshold)  */
     float edges[256];     /* fp32 only: edges[k] = smallest finite x with norm8(x) >= k (k>=1)   */
 } roix_scalars;
 
@@ -167,6 +172,24 @@ roix_status roix_morph_workspace(const roix_geom *g, size_t *ws_bytes);
 roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
                        const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
                        void *ws, size_t ws_bytes, roix_stream_t stream);
+
+/*
+ * a2+a4 fused by speculation (one read of x instead of two).  A 1/64 sample of x gives Otsu a window
+ * for the raw threshold; one pass then accumulates the full histogram into `hist` (exactly as
+ * roix_histogram) and writes into ws the mask bits that are certain for any threshold inside the
+ * window, queueing the voxels inside it.  After roix_threshold (on the -- possibly all-reduced --
+ * histogram), roix_morph_prebinarized resolves the queued voxels with the exact threshold, or
+ * re-binarises x when the threshold fell outside the window or the queue overflowed, then opens.
+ * The mask is exactly that of roix_morph in every case.  ws: roix_histogram_binarize_workspace bytes,
+ * the same buffer for both calls.
+ */
+roix_status roix_histogram_binarize_workspace(const roix_geom *g, size_t *ws_bytes);
+roix_status roix_histogram_binarize(const void *x, roix_dtype dtype, const roix_geom *g, roix_polarity polarity,
+                                    roix_scalars *sc, uint64_t *hist, uint32_t nbins, void *ws, size_t ws_bytes,
+                                    roix_stream_t stream);
+roix_status roix_morph_prebinarized(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se,
+                                    const uint32_t *halo_lo, const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits,
+                                    uint32_t *row_runs, void *ws, size_t ws_bytes, roix_stream_t stream);
 
 /* Binarise planes [p0, p0+np) of the slab (slab-local plane numbers) into m_bits, each plane
  * packed from bit 0 with ceil(ny*nx/32) words -- the halo planes roix_morph consumes. */

@@ -24,7 +24,8 @@ class Scalars(ctypes.Structure):
                 ("reserved0", ctypes.c_uint32), ("i_max", ctypes.c_float), ("t8", ctypes.c_uint32),
                 ("thr_u16", ctypes.c_uint32), ("thr_f32", ctypes.c_float), ("count", ctypes.c_uint64),
                 ("n_components", ctypes.c_uint64), ("n_kept", ctypes.c_uint64), ("n_runs", ctypes.c_uint64),
-                ("edges", ctypes.c_float * 256)]
+                ("spec_lo", ctypes.c_uint32), ("spec_hi", ctypes.c_uint32), ("spec_state", ctypes.c_uint32),
+                ("reserved1", ctypes.c_uint32), ("n_uncertain", ctypes.c_uint64), ("edges", ctypes.c_float * 256)]
 
 
 class Geom(ctypes.Structure):
@@ -62,6 +63,11 @@ _SIGS = {
     "roix_threshold": (_i32, [_vp, _u32, _i32, _i32, _vp, _vp]),
     "roix_morph_workspace": (_i32, [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_size_t)]),
     "roix_morph": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "roix_histogram_binarize_workspace": (_i32, [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_histogram_binarize": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _i32, _vp, _vp, _u32, _vp, ctypes.c_size_t,
+                                       _vp]),
+    "roix_morph_prebinarized": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp,
+                                       ctypes.c_size_t, _vp]),
     "roix_binarize_planes": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _u64, _vp, _vp, _vp]),
     "roix_label_workspace": (_i32, [ctypes.POINTER(Geom), _u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_label": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _u32, _u64, _u64, _vp, ctypes.c_size_t,
@@ -116,6 +122,8 @@ roix_histogram = _wrap("roix_histogram")
 roix_threshold = _wrap("roix_threshold")
 roix_morph = _wrap("roix_morph")
 roix_binarize_planes = _wrap("roix_binarize_planes")
+roix_histogram_binarize = _wrap("roix_histogram_binarize")
+roix_morph_prebinarized = _wrap("roix_morph_prebinarized")
 roix_label = _wrap("roix_label")
 roix_extract = _wrap("roix_extract")
 roix_label_local = _wrap("roix_label_local")
@@ -146,6 +154,13 @@ def roix_merge(pairs, labels, sizes):
 def roix_label_workspace(geom, run_capacity):
     out = ctypes.c_size_t()
     _check(load().roix_label_workspace(ctypes.byref(geom), run_capacity, ctypes.byref(out)), "roix_label_workspace")
+    return out.value
+
+
+def roix_histogram_binarize_workspace(geom):
+    out = ctypes.c_size_t()
+    _check(load().roix_histogram_binarize_workspace(ctypes.byref(geom), ctypes.byref(out)),
+           "roix_histogram_binarize_workspace")
     return out.value
 
 

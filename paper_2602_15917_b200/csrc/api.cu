@@ -144,8 +144,45 @@ roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint
     if (s != ROIX_OK) return s;
     if (g->nx > (1u << 30)) return unsupported("rows longer than 2^30 voxels");
     if (ws_bytes < morph_workspace_bytes(*g) || !aligned16(ws)) return invalid("workspace (see roix_morph_workspace)");
-    return cuda(launch_morph(x, (int)dtype, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, ws, (cudaStream_t)stream),
+    return cuda(launch_morph(x, (int)dtype, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, ws, 0, (cudaStream_t)stream),
                 "roix_morph");
+}
+
+roix_status roix_histogram_binarize_workspace(const roix_geom *g, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    if (!geom_ok(g)) return invalid("geometry");
+    *ws_bytes = fused_workspace_bytes(*g);
+    return ROIX_OK;
+}
+
+roix_status roix_histogram_binarize(const void *x, roix_dtype dtype, const roix_geom *g, roix_polarity polarity,
+                                    roix_scalars *sc, uint64_t *hist, uint32_t nbins, void *ws, size_t ws_bytes,
+                                    roix_stream_t stream) {
+    if (!sc || !hist || !ws) return invalid("sc / hist / ws is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if (!geom_ok(g)) return invalid("geometry");
+    if ((dtype == ROIX_U16 && nbins != 65536) || (dtype == ROIX_F32 && nbins != 256))
+        return invalid("nbins must be 65536 (u16) or 256 (fp32)");
+    if (polarity != ROIX_POL_HIGH && polarity != ROIX_POL_LOW) return invalid("polarity");
+    if (!x || !aligned16(x) || !aligned16(ws)) return invalid("x / ws must be 16-byte aligned");
+    if (ws_bytes < fused_workspace_bytes(*g)) return invalid("workspace (see roix_histogram_binarize_workspace)");
+    return cuda(launch_histogram_binarize(x, (int)dtype, *g, (int)polarity, sc, hist, ws, (cudaStream_t)stream),
+                "roix_histogram_binarize");
+}
+
+roix_status roix_morph_prebinarized(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se,
+                                    const uint32_t *halo_lo, const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits,
+                                    uint32_t *row_runs, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    if (!sc || !o_bits || !ws) return invalid("sc / o_bits / ws is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (se != 6 && se != 4) return unsupported("se must be 6 (3-D cross) or 4 (in-plane cross)");
+    if (!x || !aligned16(x) || !aligned16(o_bits)) return invalid("x / o_bits must be 16-byte aligned");
+    roix_status s = check_halos(g, se, halo_lo, halo_hi);
+    if (s != ROIX_OK) return s;
+    if (ws_bytes < fused_workspace_bytes(*g)) return invalid("workspace (see roix_histogram_binarize_workspace)");
+    return cuda(launch_morph(x, (int)dtype, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, ws, 1, (cudaStream_t)stream),
+                "roix_morph_prebinarized");
 }
 
 roix_status roix_binarize_planes(const void *x, roix_dtype dtype, const roix_geom *g, uint64_t p0, uint64_t np,

@@ -1,0 +1,307 @@
+// k_fused.cu -- a2 HISTOGRAM fused with a4 BINARISE by speculation (one read of x instead of two).
+//
+// The threshold of Eq. 2 depends on the histogram of all voxels, so a plain pipeline reads
+// x twice.  Here a sample of the volume (1/64 of it, in 64 equal segments) gives Otsu a speculative
+// window [lo, hi] for the raw threshold (k_spec).  One pass then accumulates the full histogram and
+// writes, for every voxel, the mask bit that is already certain for any threshold inside the window
+// (HIGH: x >= hi -> 1, x < lo -> 0; LOW mirrored); voxels with lo <= x < hi are "uncertain" and their
+// indices are queued.  After the exact threshold is known, k_spec_fix resolves the queued voxels; if
+// the exact threshold fell outside the window or the queue overflowed, the plain binarisation pass
+// runs instead (k_binarize checks spec_state), so the mask is exactly that of Eq. 2 either way.
+#include <cfloat>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace roix {
+
+constexpr int FHWIN = 16384;   // u16 shared-histogram window (as k_hist_u16)
+
+struct FusedWS {
+    uint32_t *m;          // [nwords + 64] mask words (shared with roix_morph's workspace layout)
+    uint64_t *shist;      // [65536] sample histogram
+    uint64_t *unc;        // [ucap] uncertain voxel indices
+    uint64_t ucap;
+};
+
+static size_t fused_carve(void *base, uint64_t n, FusedWS *w) {
+    const uint64_t nwords = (n + 31) / 32;
+    const size_t a = ((nwords + 64) * 4 + 255) & ~(size_t)255;
+    const size_t b = 65536 * 8;
+    const uint64_t ucap = n / 512 > (1u << 16) ? n / 512 : (1u << 16);
+    if (w) {
+        w->m = (uint32_t *)base;
+        w->shist = (uint64_t *)((char *)base + a);
+        w->unc = (uint64_t *)((char *)base + a + b);
+        w->ucap = ucap;
+    }
+    return a + b + ucap * 8;
+}
+
+// ---------------------------------------------------------------------------------- sample pass
+// every rs-th row of X voxels (rows spread over y and z): a representative 1/rs of the volume
+__device__ __forceinline__ int norm8_edges_f(float x, float scale, const float *e) {
+    int k = __float2int_rz(fminf(fmaxf(x * scale + 0.5f, 0.0f), 255.0f));
+    while (x >= e[k + 1]) k++;
+    while (x < e[k]) k--;
+    return k;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) k_sample_hist(const T *__restrict__ x, uint64_t X, uint64_t nrows, uint64_t rs,
+                                                     roix_scalars *sc, uint64_t *gh) {
+    __shared__ uint32_t sh[2048];
+    __shared__ float e[257];
+    if (get_err(sc)) return;
+    const bool f32 = sizeof(T) == 4;
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
+    if (f32) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) e[i] = i == 0 ? -INFINITY : sc->edges[i];
+        if (threadIdx.x == 0) e[256] = INFINITY;
+    }
+    const float scale = f32 ? 255.0f / sc->i_max : 0.0f;
+    __syncthreads();
+    const uint64_t ns = (nrows + rs - 1) / rs, total = ns * X, stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const uint64_t r = (i / X) * rs, c = i % X;
+        const T v = x[r * X + c];
+        if constexpr (sizeof(T) == 2) {
+            if ((uint32_t)v < 2048u) atomicAdd(&sh[v], 1u);
+            else atomicAdd((unsigned long long *)&gh[v], 1ull);
+        } else {
+            if (fabsf(v) <= FLT_MAX) atomicAdd(&sh[norm8_edges_f(v, scale, e)], 1u);
+        }
+    }
+    __syncthreads();
+    const int nb = f32 ? 256 : 2048;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        if (sh[b]) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)sh[b]);
+}
+
+// ------------------------------------------------------------------------------ the fused pass
+// Warp iteration = 1024 voxels = 32 mask words (as k_binarize): lane l loads the 16-byte groups
+// c * 32 + l, counts them into the shared histogram and packs their certain / uncertain bits.
+template <typename T>
+struct Spec;
+template <>
+struct Spec<uint16_t> {
+    static constexpr int VPL = 8;
+    uint32_t lo, hi;
+    bool low;
+    __device__ Spec(const roix_scalars *sc) : lo(sc->spec_lo), hi(sc->spec_hi), low(sc->polarity != 0) {}
+    __device__ __forceinline__ void bits(uint32_t v, uint32_t &cert, uint32_t &unc) const {
+        const bool ge_hi = v >= hi, ge_lo = v >= lo;
+        cert = low ? !ge_lo : ge_hi;
+        unc = ge_lo && !ge_hi;
+    }
+};
+template <>
+struct Spec<float> {
+    static constexpr int VPL = 4;
+    float lo, hi;
+    bool low;
+    __device__ Spec(const roix_scalars *sc) : low(sc->polarity != 0) {
+        memcpy(&lo, &sc->spec_lo, 4);
+        memcpy(&hi, &sc->spec_hi, 4);
+    }
+    __device__ __forceinline__ void bits(float v, uint32_t &cert, uint32_t &unc) const {
+        const bool ge_hi = v >= hi, ge_lo = v >= lo;
+        cert = low ? !ge_lo : ge_hi;
+        unc = ge_lo && !ge_hi;
+    }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(512, 3) k_hist_bin(const T *__restrict__ x, uint64_t n, roix_scalars *sc,
+                                                       uint64_t *gh, FusedWS W) {
+    extern __shared__ uint32_t sh[];   // u16: FHWIN bins; f32: 256 bins + 257 edges
+    constexpr int VPL = Spec<T>::VPL, CH = 32 / VPL, GPW = 32 / VPL;
+    if (get_err(sc)) return;
+    const bool f32 = sizeof(T) == 4;
+    float *e = reinterpret_cast<float *>(sh + 256);
+    const int nb = f32 ? 256 : FHWIN;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
+    if (f32) {
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) e[i] = i == 0 ? -INFINITY : sc->edges[i];
+        if (threadIdx.x == 0) e[256] = INFINITY;
+    }
+    const float scale = f32 ? 255.0f / sc->i_max : 0.0f;
+    const bool spec = sc->spec_state == 1;
+    const Spec<T> sp(sc);
+    __syncthreads();
+    const uint32_t lane = lane_id();
+    const uint64_t iters = (n + 1023) / 1024, nwords = (n + 31) / 32;
+    const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
+    bool bad = false;
+    for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < iters; it += wstride) {
+        const uint64_t g0 = it * 32 * CH;
+        uint32_t Pc = 0, Pu = 0;
+        constexpr int B = CH < 4 ? CH : 4;   // loads in flight per batch
+        uint4 v[B];
+        const bool whole = (it + 1) * 1024 <= n;
+#pragma unroll
+        for (int c = 0; c < CH; c++) {
+            if (c % B == 0) {
+#pragma unroll
+                for (int u = 0; u < B; u++) v[u] = whole ? __ldcs(x4 + g0 + (c + u) * 32 + lane) : make_uint4(0, 0, 0, 0);
+            }
+            const uint64_t vb = (g0 + c * 32 + lane) * VPL;
+            T vals[VPL];
+            uint32_t valid = (1u << VPL) - 1u;
+            if (whole) {
+                const uint4 vv = v[c % B];
+                if constexpr (sizeof(T) == 2) {
+                    const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+                    for (int k = 0; k < 8; k++) vals[k] = (T)((w[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
+                } else {
+                    vals[0] = __uint_as_float(vv.x);
+                    vals[1] = __uint_as_float(vv.y);
+                    vals[2] = __uint_as_float(vv.z);
+                    vals[3] = __uint_as_float(vv.w);
+                }
+            } else {
+                valid = 0;
+#pragma unroll
+                for (int k = 0; k < VPL; k++) {
+                    vals[k] = (T)0;
+                    if (vb + k < n) {
+                        vals[k] = x[vb + k];
+                        valid |= 1u << k;
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < VPL; k++) {
+                if (!((valid >> k) & 1)) continue;
+                if constexpr (sizeof(T) == 2) {
+                    const uint32_t val = vals[k];
+                    if (val < (uint32_t)FHWIN) atomicAdd(&sh[val], 1u);
+                    else atomicAdd((unsigned long long *)&gh[val], 1ull);
+                } else {
+                    const float val = vals[k];
+                    if (fabsf(val) <= FLT_MAX) atomicAdd(&sh[norm8_edges_f(val, scale, e)], 1u);
+                    else bad = true;
+                }
+                uint32_t cb, ub;
+                sp.bits(vals[k], cb, ub);
+                Pc |= cb << (c * VPL + k);
+                Pu |= ub << (c * VPL + k);
+            }
+        }
+        if (!spec) continue;
+        // word j = groups j * GPW .. of chunk c = j / VPL (see k_binarize)
+        const uint32_t cc = lane / VPL, src0 = (lane % VPL) * GPW;
+        uint32_t wc = 0, wu = 0;
+#pragma unroll
+        for (int i = 0; i < GPW; i++) {
+            const uint32_t qc = __shfl_sync(FULL, Pc, src0 + i), qu = __shfl_sync(FULL, Pu, src0 + i);
+            wc |= ((qc >> (cc * VPL)) & ((1u << VPL) - 1u)) << (i * VPL);
+            wu |= ((qu >> (cc * VPL)) & ((1u << VPL) - 1u)) << (i * VPL);
+        }
+        const uint64_t wi = it * 32 + lane;
+        if (wi < nwords) W.m[wi] = wc;
+        // queue the uncertain voxels (rare: they lie inside the threshold window)
+        if (__any_sync(FULL, wu != 0)) {
+            const uint32_t cnt = __popc(wu);
+            const uint32_t incl = warp_incl_scan(cnt);
+            unsigned long long at = 0;
+            if (lane == 31 && incl) at = atomicAdd((unsigned long long *)&sc->n_uncertain, (unsigned long long)incl);
+            at = __shfl_sync(FULL, at, 31) + incl - cnt;
+            uint32_t bits = wu;
+            while (bits) {
+                const uint32_t b = __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (at < W.ucap) W.unc[at] = wi * 32 + b;
+                at++;
+            }
+        }
+    }
+    if (bad) set_err(sc, ROIX_ERR_NONFINITE);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nb; b += blockDim.x)
+        if (sh[b]) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)sh[b]);
+}
+
+// After the exact threshold: resolve the queued voxels, or flag the plain binarisation.
+__global__ void k_spec_check(roix_scalars *sc, int dtype, uint64_t ucap) {
+    if (get_err(sc)) return;
+    if (sc->spec_state != 1) {
+        sc->spec_state = 3;
+        return;
+    }
+    bool ok = sc->n_uncertain <= ucap;
+    if (dtype == ROIX_U16) ok = ok && sc->spec_lo <= sc->thr_u16 && sc->thr_u16 <= sc->spec_hi;
+    else ok = ok && __uint_as_float(sc->spec_lo) <= sc->thr_f32 && sc->thr_f32 <= __uint_as_float(sc->spec_hi);
+    sc->spec_state = ok ? 2 : 3;
+}
+
+template <typename T>
+__global__ void k_spec_fix(const T *__restrict__ x, roix_scalars *sc, FusedWS W) {
+    if (get_err(sc) || sc->spec_state != 2) return;
+    const uint64_t nu = sc->n_uncertain;
+    const bool low = sc->polarity != 0;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nu; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = W.unc[k];
+        bool ge;
+        if constexpr (sizeof(T) == 2) ge = (uint32_t)x[i] >= sc->thr_u16;
+        else ge = x[i] >= sc->thr_f32;
+        if (ge != low) atomicOr(&W.m[i >> 5], 1u << (i & 31));
+    }
+}
+
+}  // namespace roix
+
+using namespace roix;
+
+size_t fused_workspace_bytes(const roix_geom &g) { return fused_carve(nullptr, g.nz * g.ny * g.nx, nullptr); }
+
+cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom &g, int polarity, roix_scalars *sc,
+                                      uint64_t *hist, void *ws, cudaStream_t st) {
+    FusedWS W;
+    const uint64_t n = g.nz * g.ny * g.nx;
+    fused_carve(ws, n, &W);
+    cudaError_t e;
+    // 1. sample histogram: every rs-th row (about 1/64 of the voxels, at least 4096 rows when possible)
+    if ((e = cudaMemsetAsync(W.shist, 0, 65536 * 8, st)) != cudaSuccess) return e;
+    const uint64_t nrows = g.nz * g.ny;
+    uint64_t rs = nrows / 4096 < 64 ? (nrows / 4096 ? nrows / 4096 : 1) : 64;
+    static bool attr = false;
+    if (!attr) {
+        if ((e = cudaFuncSetAttribute(k_hist_bin<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, FHWIN * 4)) !=
+            cudaSuccess)
+            return e;
+        attr = true;
+    }
+    const int sms = num_sms();
+    if (dtype == ROIX_U16)
+        k_sample_hist<uint16_t><<<sms * 2, 512, 0, st>>>((const uint16_t *)x, g.nx, nrows, rs, sc, W.shist);
+    else
+        k_sample_hist<float><<<sms * 2, 512, 0, st>>>((const float *)x, g.nx, nrows, rs, sc, W.shist);
+    // 2. speculative window
+    if ((e = launch_spec(W.shist, dtype, polarity, sc, st)) != cudaSuccess) return e;
+    // 3. full histogram + certain mask bits + uncertain queue
+    const uint64_t iters = (n + 1023) / 1024;
+    uint64_t blocks = (iters + 15) / 16;
+    if (blocks > (uint64_t)sms * 3) blocks = (uint64_t)sms * 3;
+    if (blocks < 1) blocks = 1;
+    if (dtype == ROIX_U16)
+        k_hist_bin<uint16_t><<<(unsigned)blocks, 512, FHWIN * 4, st>>>((const uint16_t *)x, n, sc, hist, W);
+    else
+        k_hist_bin<float><<<(unsigned)blocks, 512, (256 + 257) * 4, st>>>((const float *)x, n, sc, hist, W);
+    return cudaGetLastError();
+}
+
+// the mask of the fused pass, completed with the exact threshold (called by roix_morph_prebinarized)
+cudaError_t launch_spec_resolve(const void *x, int dtype, const roix_geom &g, roix_scalars *sc, void *ws,
+                                cudaStream_t st) {
+    FusedWS W;
+    fused_carve(ws, g.nz * g.ny * g.nx, &W);
+    k_spec_check<<<1, 1, 0, st>>>(sc, dtype, W.ucap);
+    const int blocks = num_sms() * 2;
+    if (dtype == ROIX_U16) k_spec_fix<uint16_t><<<blocks, 256, 0, st>>>((const uint16_t *)x, sc, W);
+    else k_spec_fix<float><<<blocks, 256, 0, st>>>((const float *)x, sc, W);
+    return cudaGetLastError();
+}

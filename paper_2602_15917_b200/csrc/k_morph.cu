@@ -176,8 +176,9 @@ __device__ __forceinline__ void write_row_atomic(uint32_t *o, uint64_t bitpos, u
 // the GPW lanes that hold its groups.
 template <typename T>
 __global__ void __launch_bounds__(256) k_binarize(const T *__restrict__ x, uint64_t n, roix_scalars *sc,
-                                                  uint32_t *__restrict__ m) {
+                                                  uint32_t *__restrict__ m, int skip_if_resolved) {
     if (get_err(sc)) return;
+    if (skip_if_resolved && sc->spec_state == 2) return;   // the fused pass already produced m
     constexpr int VPL = Cmp<T>::VPL, CH = 32 / VPL, GPW = 32 / VPL;
     const Cmp<T> cmp(sc);
     const uint32_t lane = lane_id();
@@ -882,7 +883,7 @@ size_t morph_workspace_bytes(const roix_geom &g) { return ((g.nz * g.ny * g.nx +
 
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
                          const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
-                         cudaStream_t st) {
+                         int prebinarized, cudaStream_t st) {
     MorphArgs A = {};
     A.nz = g.nz;
     A.ny = g.ny;
@@ -926,14 +927,16 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         }
         return cudaGetLastError();
     }
-    // a4: stream x -> m
+    // a4: stream x -> m (after a fused speculative pass: resolve its window, binarise only on a miss)
+    if (prebinarized && (e = launch_spec_resolve(x, dtype, g, sc, ws, st)) != cudaSuccess) return e;
     {
         uint64_t iters = (n + 1023) / 1024;
         uint64_t blocks = (iters + 7) / 8;
         uint64_t cap = (uint64_t)num_sms() * 8;
         if (blocks > cap) blocks = cap;
-        if (dtype == ROIX_U16) k_binarize<uint16_t><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x, n, sc, m);
-        else k_binarize<float><<<(unsigned)blocks, 256, 0, st>>>((const float *)x, n, sc, m);
+        if (dtype == ROIX_U16)
+            k_binarize<uint16_t><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x, n, sc, m, prebinarized);
+        else k_binarize<float><<<(unsigned)blocks, 256, 0, st>>>((const float *)x, n, sc, m, prebinarized);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     int occ = 0;

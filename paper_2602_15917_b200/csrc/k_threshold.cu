@@ -72,14 +72,15 @@ __device__ bool better(const Cand &a, const Cand &b) {
     return c > 0 || (c == 0 && a.t < b.t);
 }
 
-__global__ void __launch_bounds__(1024) k_threshold(const uint64_t *__restrict__ hist, int dtype, int polarity,
-                                                     roix_scalars *sc) {
+// Exact 2-class Otsu over a 1024-thread block.  u16: hist has 65536 raw bins (I_max and the norm8
+// fold are derived here); fp32: hist is the 256-bin norm8 histogram.  Returns t8 (-1 if fewer than
+// two populated bins) and I_max (u16).  Every thread of the block must call it.
+__device__ void otsu_block(const uint64_t *__restrict__ hist, int dtype, uint32_t *imax_out, int *t8_out) {
     __shared__ unsigned long long h8[256];
     __shared__ uint64_t scan_n[256], scan_s[256];
     __shared__ Cand cand[256];
     __shared__ uint32_t s_imax;
     const int t = threadIdx.x;
-    if (get_err(sc)) return;
     if (t < 256) h8[t] = 0;
     if (t == 0) s_imax = 0;
     __syncthreads();
@@ -146,8 +147,22 @@ __global__ void __launch_bounds__(1024) k_threshold(const uint64_t *__restrict__
         if (t < stride && better(cand[t + stride], cand[t])) cand[t] = cand[t + stride];
         __syncthreads();
     }
-    if (t == 0) {
-        int t8 = cand[0].t;
+    *imax_out = imax;
+    *t8_out = cand[0].t;
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t thr_u16_of(uint32_t imax, int t8) {
+    return (uint32_t)(((uint64_t)imax * (2 * t8 + 1) + 509) / 510);   // first v with norm8(v) > t8
+}
+
+__global__ void __launch_bounds__(1024) k_threshold(const uint64_t *__restrict__ hist, int dtype, int polarity,
+                                                     roix_scalars *sc) {
+    if (get_err(sc)) return;
+    uint32_t imax;
+    int t8;
+    otsu_block(hist, dtype, &imax, &t8);
+    if (threadIdx.x == 0) {
         sc->polarity = (uint32_t)polarity;
         if (dtype == ROIX_U16) sc->i_max = (float)imax;
         if (t8 < 0) {
@@ -156,8 +171,38 @@ __global__ void __launch_bounds__(1024) k_threshold(const uint64_t *__restrict__
             return;
         }
         sc->t8 = (uint32_t)t8;
-        if (dtype == ROIX_U16) sc->thr_u16 = (uint32_t)(((uint64_t)imax * (2 * t8 + 1) + 509) / 510);
+        if (dtype == ROIX_U16) sc->thr_u16 = thr_u16_of(imax, t8);
         else sc->thr_f32 = sc->edges[t8 + 1];
+    }
+}
+
+// Speculative threshold window from a sample histogram (roix_histogram_binarize): the exact raw
+// threshold is expected within [spec_lo, spec_hi] -- Otsu on the sample +- SPEC_D norm8 bins, and for
+// u16 an I_max up to 1/8 above the sample maximum.  spec_state = 1 (window set) or 3 (no window).
+constexpr int SPEC_D = 3;
+__global__ void __launch_bounds__(1024) k_spec(const uint64_t *__restrict__ shist, int dtype, int polarity,
+                                                roix_scalars *sc) {
+    if (get_err(sc)) return;
+    uint32_t imax;
+    int t8;
+    otsu_block(shist, dtype, &imax, &t8);
+    if (threadIdx.x == 0) {
+        sc->polarity = (uint32_t)polarity;
+        sc->n_uncertain = 0;
+        if (t8 < 0) {
+            sc->spec_state = 3;
+            return;
+        }
+        const int tlo = max(t8 - SPEC_D, 0), thi = min(t8 + SPEC_D, 254);
+        if (dtype == ROIX_U16) {
+            const uint32_t ihi = min(65535u, imax + imax / 8 + 64);
+            sc->spec_lo = thr_u16_of(imax, tlo);
+            sc->spec_hi = thr_u16_of(ihi, thi);
+        } else {
+            sc->spec_lo = __float_as_uint(sc->edges[tlo + 1]);
+            sc->spec_hi = __float_as_uint(sc->edges[thi + 1]);
+        }
+        sc->spec_state = 1;
     }
 }
 
@@ -165,5 +210,10 @@ __global__ void __launch_bounds__(1024) k_threshold(const uint64_t *__restrict__
 
 cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st) {
     roix::k_threshold<<<1, 1024, 0, st>>>(hist, dtype, polarity, sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spec(const uint64_t *shist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st) {
+    roix::k_spec<<<1, 1024, 0, st>>>(shist, dtype, polarity, sc);
     return cudaGetLastError();
 }

@@ -22,7 +22,13 @@ cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix
 size_t morph_workspace_bytes(const roix_geom &g);
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
                          const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
-                         cudaStream_t st);
+                         int prebinarized, cudaStream_t st);
+cudaError_t launch_spec(const uint64_t *shist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st);
+size_t fused_workspace_bytes(const roix_geom &g);
+cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom &g, int polarity, roix_scalars *sc,
+                                      uint64_t *hist, void *ws, cudaStream_t st);
+cudaError_t launch_spec_resolve(const void *x, int dtype, const roix_geom &g, roix_scalars *sc, void *ws,
+                                cudaStream_t st);
 cudaError_t launch_binarize_planes(const void *x, int dtype, const roix_geom &g, uint64_t p0, uint64_t np,
                                    roix_scalars *sc, uint32_t *m_bits, cudaStream_t st);
 

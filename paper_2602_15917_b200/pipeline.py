@@ -15,7 +15,7 @@ import torch
 from . import _lib as L
 
 # kernels libroix launches per call (used for the bench's gpu_launches count)
-LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 1, "threshold": 1, "morph": 2,
+LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 3, "threshold": 1, "morph": 4,
             "label": 16, "extract": 6}
 
 
@@ -45,7 +45,7 @@ class Pipeline:
     """Preallocated buffers + the enqueue sequence for volumes of one shape / dtype / parameter set."""
 
     def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
-                 run_capacity=None, code_capacity=None, device=None, labels=False):
+                 run_capacity=None, code_capacity=None, device=None, labels=False, fused=False):
         L.load()
         self.shape = tuple(int(v) for v in shape)
         Z, Y, X = self.shape
@@ -65,7 +65,12 @@ class Pipeline:
         self.hist = torch.zeros(self.nbins, dtype=torch.int64, device=dev)
         self.o = torch.empty(self.nwords + 4, dtype=torch.int32, device=dev)   # o, then K in place
         self.row_runs = torch.empty(Z * Y, dtype=torch.int32, device=dev)
-        self.morph_ws = torch.empty(L.roix_morph_workspace(self.geom), dtype=torch.uint8, device=dev)
+        # fused (speculative) histogram + binarisation: one read of x for a2 + a4 (roix_histogram_binarize);
+        # off by default: on B200 the histogram pass is bound by shared-memory atomics, and the fused pass
+        # (3x slower than the plain histogram at C4) loses to histogram + streaming binarisation
+        self.fused = bool(fused)
+        wsb = L.roix_histogram_binarize_workspace(self.geom) if self.fused else L.roix_morph_workspace(self.geom)
+        self.morph_ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         rows = Z * Y
         worst = rows * ((X + 1) // 2)
         if run_capacity is None:
@@ -103,12 +108,18 @@ class Pipeline:
         L.roix_resolve(sc, self.cdtype, self.rel_eb, st)
         self.hist.zero_()
         mark("setup")
-        L.roix_histogram(xp, self.cdtype, n, sc, _ptr(self.hist), self.nbins, st)
+        ws, wsb = _ptr(self.morph_ws), self.morph_ws.numel()
+        if self.fused:
+            L.roix_histogram_binarize(xp, self.cdtype, ctypes.byref(self.geom), self.polarity, sc, _ptr(self.hist),
+                                      self.nbins, ws, wsb, st)
+        else:
+            L.roix_histogram(xp, self.cdtype, n, sc, _ptr(self.hist), self.nbins, st)
         mark("histogram")
         L.roix_threshold(_ptr(self.hist), self.nbins, self.cdtype, self.polarity, sc, st)
         mark("threshold")
-        L.roix_morph(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o),
-                     _ptr(self.row_runs), _ptr(self.morph_ws), self.morph_ws.numel(), st)
+        morph = L.roix_morph_prebinarized if self.fused else L.roix_morph
+        morph(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o), _ptr(self.row_runs),
+              ws, wsb, st)
         mark("morph")
         out = L.LabelOut(self.o.data_ptr(), self.comp_min.data_ptr(), self.comp_size.data_ptr(),
                          self.comp_kept.data_ptr(), self.comp_cap,

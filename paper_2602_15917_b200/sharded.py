@@ -38,6 +38,8 @@ class SlabState(Pipeline):
         self.rank, self.world, self.z0, self.nz = rank, world, z0, nz
         super().__init__((nz, Y, X), dtype, **kw)
         self.geom = L.Geom(nz, Y, X, z0, Z)            # slab geometry in the global volume
+        wsb = L.roix_histogram_binarize_workspace(self.geom) if self.fused else L.roix_morph_workspace(self.geom)
+        self.morph_ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
         self.ws_bytes = L.roix_label_workspace(self.geom, self.run_capacity)
         self.label_ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
         self.plane_w = (Y * X + 31) // 32
@@ -75,7 +77,12 @@ def slab_program(S, x, stream=None):
         yield ("minmax", S.sc)                                    # X2
     L.roix_resolve(sc, S.cdtype, S.rel_eb, st)
     S.hist.zero_()
-    L.roix_histogram(xp, S.cdtype, n, sc, _ptr(S.hist), S.nbins, st)
+    mws, mwsb = _ptr(S.morph_ws), S.morph_ws.numel()
+    if S.fused:
+        L.roix_histogram_binarize(xp, S.cdtype, ctypes.byref(S.geom), S.polarity, sc, _ptr(S.hist), S.nbins, mws,
+                                  mwsb, st)
+    else:
+        L.roix_histogram(xp, S.cdtype, n, sc, _ptr(S.hist), S.nbins, st)
     yield ("sum", S.hist)                                         # X1
     L.roix_threshold(_ptr(S.hist), S.nbins, S.cdtype, S.polarity, sc, st)
     halo_lo = halo_hi = None
@@ -91,8 +98,8 @@ def slab_program(S, x, stream=None):
         if g < G - 1:
             halo_hi = _ptr(S.halo_recv[1])
         assert pw > 0
-    L.roix_morph(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o), _ptr(S.row_runs),
-                 _ptr(S.morph_ws), S.morph_ws.numel(), st)
+    morph = L.roix_morph_prebinarized if S.fused else L.roix_morph
+    morph(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o), _ptr(S.row_runs), mws, mwsb, st)
     out = L.LabelOut(S.o.data_ptr(), S.comp_min.data_ptr(), S.comp_size.data_ptr(), S.comp_kept.data_ptr(),
                      S.comp_cap, S.labels.data_ptr() if S.labels is not None else None)
     geo = ctypes.byref(S.geom)

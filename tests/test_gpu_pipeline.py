@@ -115,3 +115,42 @@ def test_edge_cases():
     ref = oracle.pipeline(v, eb=0.5, min_size=1)
     assert r.count == ref["count"]
     np.testing.assert_array_equal(r.codes.cpu().numpy().view(np.uint16), ref["stream"])
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C1"], synth.CONFIGS["C2"], synth.scaled("C3", 0.25, frames=4),
+                                 synth.scaled("C5", 0.125)], ids=lambda c: c.name)
+def test_fused_histogram_binarize_equals_two_pass(cfg):
+    """roix_histogram_binarize + roix_morph_prebinarized give exactly the two-pass result."""
+    x = synth.generate(cfg)
+    kw = dict(eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=cfg.polarity)
+    a = Pipeline(cfg.shape, cfg.dtype, fused=True, **kw)
+    ra = a.run(x)
+    b = Pipeline(cfg.shape, cfg.dtype, fused=False, **kw)
+    rb = b.run(x)
+    assert ra.scalars.spec_state in (2, 3)     # resolved, or fell back to the plain binarisation
+    assert torch.equal(a.hist, b.hist) and ra.t8 == rb.t8
+    assert torch.equal(ra.keep_bits, rb.keep_bits) and torch.equal(ra.codes, rb.codes)
+    assert torch.equal(ra.comp_min, rb.comp_min) and torch.equal(ra.comp_size, rb.comp_size)
+
+
+def test_fused_speculation_miss_falls_back():
+    """A volume whose sampled rows are unrepresentative (objects only in the odd rows; the sample
+    takes every 2nd row here): the window misses the exact threshold or the queue overflows, and the
+    plain binarisation runs -- same result as the two-pass path and the oracle."""
+    rng = np.random.default_rng(3)
+    Z, Y, X = 64, 128, 256
+    v = rng.normal(300, 30, (Z, Y, X))
+    odd = v[:, 1::2, :]
+    obj = rng.random(odd.shape) < 0.3
+    odd[obj] = rng.normal(3000, 50, obj.sum())
+    v[:, 1::2, :] = odd
+    v = v.clip(0, 65535).astype(np.uint16)
+    x = dev(v)
+    for pol in (0, 1):
+        kw = dict(eb=2.0, conn=6, se=6, min_size=4, polarity=pol)
+        ra = Pipeline(v.shape, "u16", fused=True, **kw).run(x)
+        rb = Pipeline(v.shape, "u16", fused=False, **kw).run(x)
+        assert ra.scalars.spec_state == 3
+        assert torch.equal(ra.keep_bits, rb.keep_bits) and torch.equal(ra.codes, rb.codes)
+        ref = oracle.pipeline(v, eb=2.0, conn=6, se=6, min_size=4, polarity=pol)
+        assert ra.count == ref["count"]
