@@ -278,6 +278,19 @@ roix_status roix_extract(const void *x, roix_dtype dtype, uint64_t n, const uint
                          void *codes_out, uint64_t capacity, const uint64_t *offset, void *ws, size_t ws_bytes,
                          roix_stream_t stream);
 
+/*
+ * a1+a8 EXTRACT from the labelling's kept runs (the pipeline's form of roix_extract).  After
+ * roix_label (or roix_label_finish) on the same ws, writes exactly what roix_extract(x, K) writes for
+ * the K that call produced -- codes_out[offset + j] = RNE(x[i_j] / s) for the kept voxels i_0 < i_1 <
+ * ... of the slab -- and adds their number to sc->count, but reads neither K nor any voxel of x
+ * outside the kept runs: x is read run by run with 16-byte loads (the kept runs in raster order are
+ * the kept voxels in increasing linear index, G-17).  g, run_capacity, ws, ws_bytes: those of the
+ * labelling (ws is also scratch here).  capacity / offset / errors: as roix_extract.
+ */
+roix_status roix_extract_runs(const void *x, roix_dtype dtype, const roix_geom *g, uint64_t run_capacity, void *ws,
+                              size_t ws_bytes, roix_scalars *sc, void *codes_out, uint64_t capacity,
+                              const uint64_t *offset, roix_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

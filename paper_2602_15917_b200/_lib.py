@@ -81,6 +81,8 @@ _SIGS = {
                                  ctypes.POINTER(LabelOut), _vp, _vp]),
     "roix_extract_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_extract": (_i32, [_vp, _i32, _u64, _vp, _vp, _vp, _u64, _vp, _vp, ctypes.c_size_t, _vp]),
+    "roix_extract_runs": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _u64, _vp,
+                                 _vp]),
 }
 
 
@@ -126,6 +128,7 @@ roix_histogram_binarize = _wrap("roix_histogram_binarize")
 roix_morph_prebinarized = _wrap("roix_morph_prebinarized")
 roix_label = _wrap("roix_label")
 roix_extract = _wrap("roix_extract")
+roix_extract_runs = _wrap("roix_extract_runs")
 roix_label_local = _wrap("roix_label_local")
 roix_label_boundary = _wrap("roix_label_boundary")
 roix_label_link = _wrap("roix_label_link")

@@ -363,4 +363,18 @@ roix_status roix_extract(const void *x, roix_dtype dtype, uint64_t n, const uint
                 "roix_extract");
 }
 
+roix_status roix_extract_runs(const void *x, roix_dtype dtype, const roix_geom *g, uint64_t run_capacity, void *ws,
+                              size_t ws_bytes, roix_scalars *sc, void *codes_out, uint64_t capacity,
+                              const uint64_t *offset, roix_stream_t stream) {
+    if (!sc) return invalid("sc is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    roix_status s = label_common(g, run_capacity, ws, ws_bytes);
+    if (s != ROIX_OK) return s;
+    if (!x || !aligned16(x)) return invalid("x must be 16-byte aligned");
+    if (capacity > 0 && (!codes_out || !aligned16(codes_out))) return invalid("codes_out must be 16-byte aligned");
+    return cuda(launch_extract_runs(x, (int)dtype, *g, run_capacity, ws, sc, codes_out, capacity, offset,
+                                    (cudaStream_t)stream),
+                "roix_extract_runs");
+}
+
 }  // extern "C"

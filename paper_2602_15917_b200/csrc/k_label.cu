@@ -31,10 +31,13 @@ struct LabelWS {
     uint64_t *ctr;        // [4]: 0 n_runs, 1 n_cross_pairs, 2 n_kept
     uint2 *pairs;         // [pair_cap]: run pairs that cross union blocks
     uint64_t pair_cap;
+    uint32_t *klen;       // [cap]: kept length of every run (roix_extract_runs)
+    uint64_t *koff;       // [cap + 1]: their exclusive prefix
+    uint32_t *cfirst;     // [gather_chunks_max(n) + 1]: first run of every output chunk
 };
 
 constexpr int UB_RUNS = 4096;     // runs per union block (their parents live in shared memory)
-constexpr int UB_THREADS = 256;
+constexpr int UB_THREADS = 1024;   // 4 runs per thread: short dependent chains
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
@@ -53,6 +56,7 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
     size_t o_sz = take(cap * 8), o_kp = take(cap), o_ct = take(4 * 8);
     const uint64_t pair_cap = 2 * cap + 1024;
     size_t o_pr = take(pair_cap * 8);
+    size_t o_kl = take(cap * 4), o_ko = take((cap + 1) * 8), o_cf = take((gather_chunks_max(rows * g.nx) + 1) * 4);
     if (ws) {
         char *b = (char *)base;
         ws->row_runs = (uint32_t *)(b + o_rr);
@@ -68,6 +72,9 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
         ws->ctr = (uint64_t *)(b + o_ct);
         ws->pairs = (uint2 *)(b + o_pr);
         ws->pair_cap = pair_cap;
+        ws->klen = (uint32_t *)(b + o_kl);
+        ws->koff = (uint64_t *)(b + o_ko);
+        ws->cfirst = (uint32_t *)(b + o_cf);
     }
     return off;
 }
@@ -208,6 +215,109 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
                     const uint32_t cw = k < G.W ? row_word_safe(o, G, r, k, nwords) : 0u;
                     const uint32_t nxt = (k0 + 32 < G.W) ? row_word_safe(o, G, r, k0 + 32, nwords) : 0u;
                     runs_of_chunk(cw, nxt, carry, k, b0, sbase, ebase, (uint32_t)r, x0, x1, rrow);
+                }
+            }
+        }
+    }
+}
+
+// Whole-row form (X % 32 == 0, W = L KW words, L a power of two <= 32): a warp holds S = 32 / L row
+// segments, lane sl of a segment the KW consecutive words [KW sl, KW sl + KW) of a row; each segment
+// takes RR consecutive rows per iteration, all their loads issued before any row is processed.  Run
+// starts / ends of every word come from one shfl each way; one packed segment scan gives every
+// lane's first start / end slot.
+template <int L, int KW, int RR>
+__global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__restrict__ o, LGeo G, LabelWS W,
+                                                           roix_scalars *sc) {
+    if (get_err(sc)) return;
+    constexpr int S = 32 / L;
+    const uint32_t lane = lane_id(), sl = lane & (L - 1), seg = lane / L;
+    const uint64_t rows = G.nz * G.ny;
+    const uint64_t ngroups = (rows + S * RR - 1) / (S * RR);
+    const uint64_t wpg = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    uint32_t *__restrict__ x0 = W.x0;
+    uint32_t *__restrict__ x1 = W.x1;
+    uint32_t *__restrict__ rrow = W.rrow;
+    const uint32_t *__restrict__ rs = W.row_start;
+    for (uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gi < ngroups; gi += wpg) {
+        const uint64_t r0 = (gi * S + seg) * RR;   // this segment's first row
+        // row offsets rs[r0 .. r0 + RR]: one per lane when the segment is wide enough, else all per lane
+        uint32_t off = 0, offs[RR + 1];
+        if constexpr (L > RR) {
+            if (sl <= (uint32_t)RR && r0 + sl <= rows) off = __ldg(rs + r0 + sl);
+        } else {
+#pragma unroll
+            for (int q = 0; q <= RR; q++) offs[q] = r0 + q <= rows ? __ldg(rs + r0 + q) : 0u;
+        }
+        auto row_off = [&](int q) {
+            if constexpr (L > RR) return __shfl_sync(FULL, off, q, L);
+            else return offs[q];
+        };
+        uint32_t wv[RR][KW];
+#pragma unroll
+        for (int q = 0; q < RR; q++) {
+            const uint32_t a = row_off(q), b = row_off(q + 1);
+            const bool live = r0 + q < rows && b != a;
+            const uint32_t *src = o + (r0 + q) * (uint64_t)(L * KW) + KW * sl;
+#pragma unroll
+            for (int i = 0; i < KW; i++) wv[q][i] = 0u;
+            if (live) {
+                if constexpr (KW == 1) {
+                    wv[q][0] = __ldg(src);
+                } else if constexpr (KW == 2) {
+                    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src));
+                    wv[q][0] = v.x;
+                    wv[q][1] = v.y;
+                } else {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src));
+                    wv[q][0] = v.x;
+                    wv[q][1] = v.y;
+                    wv[q][2] = v.z;
+                    wv[q][3] = v.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RR; q++) {
+            const uint64_t r = r0 + q;
+            const uint32_t b0 = row_off(q);
+            uint32_t left = __shfl_up_sync(FULL, wv[q][KW - 1], 1, L);
+            uint32_t right = __shfl_down_sync(FULL, wv[q][0], 1, L);
+            if (sl == 0) left = 0u;
+            if (sl == L - 1) right = 0u;
+            uint32_t st[KW], en[KW], ns = 0, ne = 0;
+#pragma unroll
+            for (int i = 0; i < KW; i++) {
+                const uint32_t c = wv[q][i];
+                st[i] = c & ~__funnelshift_l(i ? wv[q][i - 1] : left, c, 1);
+                en[i] = c & ~__funnelshift_r(c, i < KW - 1 ? wv[q][i + 1] : right, 1);
+                ns += __popc(st[i]);
+                ne += __popc(en[i]);
+            }
+            // inclusive segment scan of (starts | ends << 16); both <= 16 KW per lane
+            uint32_t both = ns | (ne << 16);
+#pragma unroll
+            for (int d = 1; d < L; d <<= 1) {
+                const uint32_t t = __shfl_up_sync(FULL, both, d, L);
+                if (sl >= (uint32_t)d) both += t;
+            }
+            uint32_t ps = b0 + (both & 0xffffu) - ns, pe = b0 + (both >> 16) - ne;
+#pragma unroll
+            for (int i = 0; i < KW; i++) {
+                const uint32_t xb = 32 * (KW * sl + i);
+                uint32_t m = st[i];
+                while (m) {
+                    const uint32_t bb = __ffs(m) - 1;
+                    m &= m - 1;
+                    x0[ps] = xb + bb;
+                    rrow[ps] = (uint32_t)r;
+                    ps++;
+                }
+                m = en[i];
+                while (m) {
+                    const uint32_t bb = __ffs(m) - 1;
+                    m &= m - 1;
+                    x1[pe++] = xb + bb + 1;
                 }
             }
         }
@@ -641,7 +751,25 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
     if ((e = scan_u32(rr, W.row_start, rows, W.scan_tmp, st)) != cudaSuccess) return e;
     k_runs_total<<<1, 1, 0, st>>>(scan_total_ptr(W.scan_tmp, rows), cap, W, sc);
     const int runs_grid = num_sms() * 8;
-    k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, sc);
+    const uint32_t Wd = G.W;
+    if (g.nx % 32 == 0 && ((Wd <= 32 && (Wd & (Wd - 1)) == 0) || Wd == 64 || Wd == 128)) {
+        const uint32_t L = Wd < 32 ? Wd : 32;
+        const int grid = ctas(rows * L / 4, 256);   // ~4 rows per warp iteration
+#define ROIX_RUNS_ROWS(LL, KK, RR) k_extract_runs_rows<LL, KK, RR><<<grid, 256, 0, st>>>(o_bits, G, W, sc)
+        switch (Wd) {
+        case 1: ROIX_RUNS_ROWS(1, 1, 4); break;
+        case 2: ROIX_RUNS_ROWS(2, 1, 4); break;
+        case 4: ROIX_RUNS_ROWS(4, 1, 4); break;
+        case 8: ROIX_RUNS_ROWS(8, 1, 4); break;
+        case 16: ROIX_RUNS_ROWS(16, 1, 4); break;
+        case 32: ROIX_RUNS_ROWS(32, 1, 4); break;
+        case 64: ROIX_RUNS_ROWS(32, 2, 4); break;
+        default: ROIX_RUNS_ROWS(32, 4, 2); break;
+        }
+#undef ROIX_RUNS_ROWS
+    } else {
+        k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, sc);
+    }
     static bool attr = false;
     if (!attr) {
         if ((e = cudaFuncSetAttribute(k_union_local, cudaFuncAttributeMaxDynamicSharedMemorySize, UB_RUNS * 4)) !=
@@ -650,7 +778,7 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
         attr = true;
     }
     uint64_t nub = (cap + UB_RUNS - 1) / UB_RUNS;
-    if (nub > (uint64_t)num_sms() * 6) nub = (uint64_t)num_sms() * 6;   // persistent over blocks of runs
+    if (nub > (uint64_t)num_sms() * 2) nub = (uint64_t)num_sms() * 2;   // persistent over blocks of runs
     k_union_local<<<(unsigned)nub, UB_THREADS, UB_RUNS * 4, st>>>(G, ci, W, sc);
     k_union_cross<<<runs_grid, 256, 0, st>>>(W, sc);
     k_flatten_sizes<<<runs_grid, 256, 0, st>>>(W, sc);
@@ -691,6 +819,20 @@ cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const
     cudaError_t e = launch_label_local(o_bits, row_runs, g, conn, cap, ws, sc, st);
     if (e != cudaSuccess) return e;
     return launch_label_finish(o_bits, g, min_size, cap, ws, nullptr, nullptr, nullptr, 0, out, sc, st);
+}
+
+cudaError_t launch_extract_runs(const void *x, int dtype, const roix_geom &g, uint64_t cap, void *ws, roix_scalars *sc,
+                                void *codes, uint64_t capacity, const uint64_t *offset, cudaStream_t st) {
+    LabelWS W;
+    carve(ws, g, cap, &W);
+    RunsView R;
+    R.n_runs = W.ctr;
+    R.x0 = W.x0;
+    R.x1 = W.x1;
+    R.rrow = W.rrow;
+    R.parent = W.parent;
+    R.kept = W.kept;
+    return launch_gather(x, dtype, g.nx, R, cap, W.klen, W.koff, W.cfirst, W.scan_tmp, sc, codes, capacity, offset, st);
 }
 
 cudaError_t launch_label_boundary(const void *ws, const roix_geom &g, uint64_t cap, int side, roix_brun *out,

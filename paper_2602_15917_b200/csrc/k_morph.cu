@@ -14,6 +14,7 @@
 // every output row (the fused first step of a6 CCL).
 #include "common.cuh"
 #include "kernels.cuh"
+#include "async.cuh"
 
 namespace roix {
 
@@ -234,147 +235,184 @@ __device__ __forceinline__ void load_m_row(const uint32_t *__restrict__ src, uin
     }
 }
 
-// ------------------------------------------------------------------------------------ 3-D opening
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-    unsigned s = (unsigned)__cvta_generic_to_shared(dst);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+// ------------------------------------------------------- 3-D opening, whole-row warps (X % 32 == 0)
+// A warp owns S = 32 / L row segments; segment s holds RY consecutive rows of one plane and its lane
+// sl the KW consecutive words [KW sl, KW sl + KW) of each row (W = L KW words per row: every row is
+// complete inside its segment, so no x-halo).  The warp marches along z over its z-chunk keeping in
+// registers m of planes p-1, p, p+1 (rows yb-2 .. yb+RY+1) and e of planes p-2, p-1, p (rows yb-1 ..
+// yb+RY).  The three slots of each ring rotate by renaming (the z-loop is unrolled by 3), so there
+// are no register moves.  x-neighbour words come from the adjacent lanes (one shfl each way per
+// row), y-neighbours from the adjacent register rows, z-neighbours from the other slots.  Each
+// segment also writes the x-run count of every output row (the first step of a6 CCL) with a plain
+// store: a row belongs to exactly one warp.
+template <int KW>
+struct WordsT;
+template <>
+struct WordsT<1> {
+    static __device__ __forceinline__ void ld(const uint32_t *p, uint32_t (&w)[1]) { w[0] = __ldg(p); }
+    static __device__ __forceinline__ void st(uint32_t *p, const uint32_t (&w)[1]) { *p = w[0]; }
+};
+template <>
+struct WordsT<2> {
+    static __device__ __forceinline__ void ld(const uint32_t *p, uint32_t (&w)[2]) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+        w[0] = v.x;
+        w[1] = v.y;
+    }
+    static __device__ __forceinline__ void st(uint32_t *p, const uint32_t (&w)[2]) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(w[0], w[1]);
+    }
+};
+template <>
+struct WordsT<4> {
+    static __device__ __forceinline__ void ld(const uint32_t *p, uint32_t (&w)[4]) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p));
+        w[0] = v.x;
+        w[1] = v.y;
+        w[2] = v.z;
+        w[3] = v.w;
+    }
+    static __device__ __forceinline__ void st(uint32_t *p, const uint32_t (&w)[4]) {
+        *reinterpret_cast<uint4 *>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+};
 
-constexpr int MSLOTS = 8, PF = 4;  // m ring slots; planes prefetched ahead (PF + 3 <= MSLOTS)
-
-// Rings: m has MSLOTS plane slots (m(p+1..p+PF) are in flight with cp.async while e(p-1) and o(p-2)
-// are computed), e has 3.  Row data starts 4 words into its slot (16-byte aligned for cp.async), with the
-// guard words at data[-1] and data[W].  A.async: rows are whole 16-byte units in global memory
-// (X % 128 == 0); otherwise rows are loaded synchronously with funnel shifts.
-__global__ void __launch_bounds__(256) k_open3d(MorphArgs A, roix_scalars *sc) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    if (get_err(sc)) return;
-    const int TY = A.TY;
-    const uint32_t W = A.W, WS = A.WS;             // WS: multiple of 4, >= W + 8
-    const int MR = TY + 4, ER = TY + 2;            // m rows y0-2.., e rows y0-1..
-    uint32_t *mring = smem;                          // [MSLOTS][MR][WS]
-    uint32_t *ering = mring + MSLOTS * MR * WS;      // [3][ER][WS]
-    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int64_t y0 = (int64_t)blockIdx.x * TY;
-    const int64_t zs = (int64_t)blockIdx.y * A.zchunk;
-    const int64_t ze = min((int64_t)A.nz, zs + (int64_t)A.zchunk);
-    const int64_t Y = A.ny, X = A.nx;
-    if (zs >= ze) return;
-    for (int i = threadIdx.x; i < MSLOTS * MR; i += blockDim.x) {
-        mring[i * WS + 3] = FULL;
-        mring[i * WS + 4 + W] = FULL;
-    }
-    for (int i = threadIdx.x; i < 3 * ER; i += blockDim.x) {
-        ering[i * WS + 3] = 0;
-        ering[i * WS + 4 + W] = 0;
-    }
-    __syncthreads();
-    auto mrow = [&](int64_t p, int r) { return mring + (((p + MSLOTS) & (MSLOTS - 1)) * MR + r) * WS + 4; };
-    auto erow = [&](int64_t p, int r) { return ering + ((p + 3) % 3 * ER + r) * WS + 4; };
-    const uint64_t plane_w = (A.ny * A.nx + 31) / 32;
-    const uint32_t tail = (uint32_t)(X - 32ll * (W - 1));
-    const bool async = A.async;
-    // enqueue the rows of m(p) (cp.async, or synchronous loads in the generic path)
-    auto fetch = [&](int64_t p) {
-        const int64_t gp = (int64_t)A.z0 + p;
-        for (int r = warp; r < MR; r += nw) {
-            const int64_t y = y0 - 2 + r;
-            uint32_t *dst = mrow(p, r);
-            const uint32_t *src;
-            uint64_t bit0, swords;
-            if (y < 0 || y >= Y || gp < 0 || gp >= (int64_t)A.gz) {
-                fill_row(dst, W, FULL);
-                continue;
-            } else if (p < 0) {
-                src = A.halo_lo;
-                swords = 2 * plane_w;
-                bit0 = (uint64_t)(p + 2) * plane_w * 32 + y * A.nx;
-            } else if (p >= (int64_t)A.nz) {
-                src = A.halo_hi;
-                swords = 2 * plane_w;
-                bit0 = (uint64_t)(p - A.nz) * plane_w * 32 + y * A.nx;
-            } else {
-                src = A.m;
-                swords = A.m_words;
-                bit0 = ((uint64_t)p * A.ny + y) * A.nx;
-            }
-            if (async) {
-                const uint4 *s4 = reinterpret_cast<const uint4 *>(src + (bit0 >> 5));
-                for (uint32_t k = lane_id(); k < W / 4; k += 32) cp_async16(dst + 4 * k, s4 + k);
-            } else {
-                load_m_row(src, swords, bit0, A.nx, W, dst);
-            }
-        }
-        cp_async_commit();
-    };
-    for (int k = 0; k < PF; k++) {
-        if (zs - 2 + k <= ze + 1) fetch(zs - 2 + k);
-        else cp_async_commit();
-    }
-    for (int64_t p = zs - 2; p <= ze + 1; p++) {
-        if (p + PF <= ze + 1) fetch(p + PF);
-        else cp_async_commit();     // empty group: keeps the group count uniform
-        cp_async_wait<PF>();        // m(p) has landed; m(p+1..p+PF) may still be in flight
-        __syncthreads();
-        // e(q = p-1), rows y0-1 .. y0+TY
-        const int64_t q = p - 1;
-        if (q >= zs - 1) {
-            const int64_t gq = (int64_t)A.z0 + q;
-            const bool qin = gq >= 0 && gq < (int64_t)A.gz;
-            for (int r = warp; r < ER; r += nw) {
-                const int64_t y = y0 - 1 + r;
-                uint32_t *dst = erow(q, r);
-                if (!qin || y < 0 || y >= Y) {
-                    fill_row(dst, W, 0u);
-                    continue;
-                }
-                const uint32_t *c = mrow(q, r + 1), *a = mrow(q, r), *b = mrow(q, r + 2);
-                const uint32_t *f = mrow(q - 1, r + 1), *g = mrow(q + 1, r + 1);
-                for (uint32_t k = lane_id(); k < W; k += 32) {
-                    uint32_t v = erode_word(c, a, b, f, g, k);
-                    if (k == W - 1 && tail < 32) v &= low_mask(tail);
-                    dst[k] = v;
-                }
-            }
-        }
-        __syncthreads();
-        // o(z = p-2), rows y0 .. y0+TY-1
-        const int64_t z = p - 2;
-        if (z >= zs && z < ze) {
-            for (int r = warp; r < TY; r += nw) {
-                const int64_t y = y0 + r;
-                if (y >= Y) break;
-                const uint32_t *c = erow(z, r + 1), *a = erow(z, r), *b = erow(z, r + 2);
-                const uint32_t *f = erow(z - 1, r + 1), *g = erow(z + 1, r + 1);
-                const uint64_t row = (uint64_t)z * A.ny + y;
-                const uint64_t bitpos = row * A.nx;
-                uint32_t carry = 0, runs = 0;
-                for (uint32_t k0 = 0; k0 < W; k0 += 32) {
-                    uint32_t k = k0 + lane_id();
-                    uint32_t w = 0;
-                    if (k < W) {
-                        w = dilate_word(c, a, b, f, g, k);
-                        if (k == W - 1 && tail < 32) w &= low_mask(tail);
-                    }
-                    runs += count_runs_words(w, carry);
-                    if (k < W) {
-                        if (A.aligned_out) A.o[(bitpos >> 5) + k] = w;
-                        else write_row_atomic(A.o, bitpos, k, w);
-                    }
-                }
-                if (A.row_runs) {
+// bit x <- bit x-1 (l) and bit x <- bit x+1 (r) of the lane's KW words; `pad` enters at the row ends
+template <int L, int KW>
+__device__ __forceinline__ void xnbr(const uint32_t (&c)[KW], uint32_t sl, uint32_t pad, uint32_t (&l)[KW],
+                                     uint32_t (&r)[KW]) {
+    uint32_t left = __shfl_up_sync(FULL, c[KW - 1], 1, L);
+    uint32_t right = __shfl_down_sync(FULL, c[0], 1, L);
+    if (sl == 0) left = pad;
+    if (sl == L - 1) right = pad;
 #pragma unroll
-                    for (int d = 16; d > 0; d >>= 1) runs += __shfl_xor_sync(FULL, runs, d);
-                    if (lane_id() == 0) A.row_runs[row] = runs;
-                }
+    for (int i = 0; i < KW; i++) {
+        l[i] = __funnelshift_l(i ? c[i - 1] : left, c[i], 1);
+        r[i] = __funnelshift_r(c[i], i < KW - 1 ? c[i + 1] : right, 1);
+    }
+}
+
+template <int L>
+__device__ __forceinline__ uint32_t seg_sum(uint32_t v) {
+    if constexpr (L == 32) {
+        return __reduce_add_sync(FULL, v);
+    } else {
+#pragma unroll
+        for (int d = L / 2; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+        return v;
+    }
+}
+
+template <int L, int KW, int RY>
+__global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open3d_rows(MorphArgs A, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    constexpr int S = 32 / L, MR = RY + 4, ER = RY + 2;
+    using WT = WordsT<KW>;
+    const uint32_t lane = lane_id(), sl = lane & (L - 1), seg = lane / L;
+    const int Y = (int)A.ny;
+    const uint32_t W = L * KW;
+    const uint32_t tiles_y = (uint32_t)((A.ny + S * RY - 1) / (S * RY));
+    const uint32_t task = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t cz = task / tiles_y;
+    const int yb = (int)((task - cz * tiles_y) * (S * RY) + seg * RY);   // this segment's first row
+    const int nz = (int)A.nz;
+    const int zs = (int)(cz * A.zchunk);
+    if (zs >= nz) return;
+    const int ze = min(nz, zs + (int)A.zchunk);
+    const uint64_t plane_w = A.ny * (uint64_t)W;
+    const int64_t gz = (int64_t)A.gz, z0 = (int64_t)A.z0;
+    const int roff = (yb - 2) * (int)W + (int)(KW * sl);   // word offset of slot row 0 in its plane
+    uint32_t vm = 0;   // bit j: m row yb-2+j is inside the plane
+#pragma unroll
+    for (int j = 0; j < MR; j++)
+        if (yb - 2 + j >= 0 && yb - 2 + j < Y) vm |= 1u << j;
+    const uint32_t ve = vm >> 1;   // bit i: e row yb-1+i is inside the plane
+
+    uint32_t m[3][MR][KW], e[3][ER][KW];
+    auto load = [&](int p, uint32_t (&dst)[MR][KW]) {
+        const int64_t gp = z0 + p;
+        const uint32_t *pb = nullptr;
+        if (gp >= 0 && gp < gz) {
+            if (p < 0) pb = A.halo_lo + (uint64_t)(p + 2) * plane_w;
+            else if (p >= nz) pb = A.halo_hi + (uint64_t)(p - nz) * plane_w;
+            else pb = A.m + (uint64_t)p * plane_w;
+        }
+#pragma unroll
+        for (int j = 0; j < MR; j++) {
+            if (pb && ((vm >> j) & 1)) {
+                WT::ld(pb + roff + j * (int)W, dst[j]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < KW; i++) dst[j][i] = FULL;
             }
         }
-        // the next iteration's fetch writes m(p+1+PF) into the slot of m(p+1+PF-MSLOTS), last read
-        // by e(p+2+PF-MSLOTS) <= e(p-1), which every warp finished before the barrier above
+    };
+    // e(p) into E from m(p-1) = MP, m(p) = MC, m(p+1) = MN
+    auto erode = [&](int p, const uint32_t (&MP)[MR][KW], const uint32_t (&MC)[MR][KW],
+                     const uint32_t (&MN)[MR][KW], uint32_t (&E)[ER][KW]) {
+        const int64_t gp = z0 + p;
+        const bool pin = gp >= 0 && gp < gz;
+#pragma unroll
+        for (int r = 0; r < ER; r++) {
+            uint32_t l[KW], rr[KW];
+            xnbr<L, KW>(MC[r + 1], sl, FULL, l, rr);
+            const bool live = pin && ((ve >> r) & 1);
+#pragma unroll
+            for (int i = 0; i < KW; i++) {
+                const uint32_t v = MC[r + 1][i] & l[i] & rr[i] & MC[r][i] & MC[r + 2][i] & MP[r + 1][i] & MN[r + 1][i];
+                E[r][i] = live ? v : 0u;
+            }
+        }
+    };
+    // o(q) from e(q-1) = EP, e(q) = EC, e(q+1) = EN; stores o and the run counts of its rows
+    auto dilate = [&](int q, const uint32_t (&EP)[ER][KW], const uint32_t (&EC)[ER][KW],
+                      const uint32_t (&EN)[ER][KW]) {
+        uint32_t *ob = A.o + (uint64_t)q * plane_w + roff + 2 * W;
+        const uint64_t rbase = (uint64_t)q * A.ny + yb;
+#pragma unroll
+        for (int j = 0; j < RY; j++) {
+            uint32_t l[KW], rr[KW], o[KW];
+            xnbr<L, KW>(EC[j + 1], sl, 0u, l, rr);
+#pragma unroll
+            for (int i = 0; i < KW; i++)
+                o[i] = EC[j + 1][i] | l[i] | rr[i] | EC[j][i] | EC[j + 2][i] | EP[j + 1][i] | EN[j + 1][i];
+            // run starts: set bits whose left neighbour is clear
+            uint32_t left = __shfl_up_sync(FULL, o[KW - 1], 1, L);
+            if (sl == 0) left = 0u;
+            uint32_t cnt = 0;
+#pragma unroll
+            for (int i = 0; i < KW; i++) cnt += __popc(o[i] & ~__funnelshift_l(i ? o[i - 1] : left, o[i], 1));
+            cnt = seg_sum<L>(cnt);
+            if (yb + j < Y) {
+                WT::st(ob + j * (int)W, o);
+                if (sl == 0 && A.row_runs) A.row_runs[rbase + j] = cnt;
+            }
+        }
+    };
+#pragma unroll
+    for (int s = 0; s < 3; s++)
+#pragma unroll
+        for (int r = 0; r < ER; r++)
+#pragma unroll
+            for (int i = 0; i < KW; i++) e[s][r][i] = 0u;
+    load(zs - 2, m[0]);
+    load(zs - 1, m[1]);
+    load(zs, m[2]);
+    // step p: e(p) from m(p-1..p+1); m(p+2) into the freed slot; o(p-1) from e(p-2..p)
+#define ROIX_OPEN_STEP(A0, A1, A2)                                  \
+    {                                                               \
+        if (p > ze) break;                                          \
+        erode(p, m[A0], m[A1], m[A2], e[A2]);                       \
+        if (p + 2 <= ze + 1) load(p + 2, m[A0]);                    \
+        if (p - 1 >= zs) dilate(p - 1, e[A0], e[A1], e[A2]);        \
+        p++;                                                        \
     }
+    for (int p = zs - 1;;) {
+        ROIX_OPEN_STEP(0, 1, 2)
+        ROIX_OPEN_STEP(1, 2, 0)
+        ROIX_OPEN_STEP(2, 0, 1)
+    }
+#undef ROIX_OPEN_STEP
 }
 
 // ----------------------------------------------------------------- 3-D opening, warp-register form
@@ -538,30 +576,6 @@ __global__ void __launch_bounds__(256, 3) k_open3d_reg(MorphArgs A, roix_scalars
 // leaves the SM.  Requires X % 256 == 0 (otherwise binarise + open3d).
 // Shared m / e rows: words -1 .. 8 of the tile (index 0 .. 9); words -1 / 8 hold the halo bits.
 constexpr int FX = 256, FW = FX / 32, FWS = FW + 2, NSLOT = 4;
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred P1;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        " @!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 
 template <typename T, int TY>
 __global__ void __launch_bounds__(256) k_morph3d_fused(const T *__restrict__ x, MorphArgs A, roix_scalars *sc) {
@@ -940,7 +954,35 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     int occ = 0;
-    if (se == 6) {
+    const uint32_t Wd = A.W;
+    const bool rows_kernel = g.nx % 32 == 0 && (Wd <= 32 ? (Wd & (Wd - 1)) == 0 : (Wd == 64 || Wd == 128));
+    if (se == 6 && rows_kernel) {
+        // whole-row warps: S = 32 / L segments of RY rows each
+        const uint32_t L = Wd < 32 ? Wd : 32, KW = Wd / L;
+        const uint32_t RY = KW == 4 ? 2 : 4;
+        const uint64_t tiles_y = (g.ny + (32 / L) * RY - 1) / ((32 / L) * RY);
+        const uint64_t target_warps = (uint64_t)num_sms() * 48;
+        uint64_t chunks = (target_warps + tiles_y - 1) / tiles_y;
+        const uint64_t cmax = g.nz >= 16 ? g.nz / 8 : 1;   // >= 8 planes per warp (3 halo planes re-read)
+        if (chunks > cmax) chunks = cmax;
+        if (chunks < 1) chunks = 1;
+        A.zchunk = (g.nz + chunks - 1) / chunks;
+        chunks = (g.nz + A.zchunk - 1) / A.zchunk;
+        const unsigned blocks = (unsigned)((tiles_y * chunks + 7) / 8);
+#define ROIX_OPEN_ROWS(LL, KK, RR) k_open3d_rows<LL, KK, RR><<<blocks, 256, 0, st>>>(A, sc)
+        switch (Wd) {
+        case 1: ROIX_OPEN_ROWS(1, 1, 4); break;
+        case 2: ROIX_OPEN_ROWS(2, 1, 4); break;
+        case 4: ROIX_OPEN_ROWS(4, 1, 4); break;
+        case 8: ROIX_OPEN_ROWS(8, 1, 4); break;
+        case 16: ROIX_OPEN_ROWS(16, 1, 4); break;
+        case 32: ROIX_OPEN_ROWS(32, 1, 4); break;
+        case 64: ROIX_OPEN_ROWS(32, 2, 4); break;
+        default: ROIX_OPEN_ROWS(32, 4, 2); break;
+        }
+#undef ROIX_OPEN_ROWS
+    } else if (se == 6) {
+        // general rows (X % 32 != 0 or other widths): 30-word pencils with halo lanes
         constexpr int RY = 4;
         const uint64_t npx = (A.W + 29) / 30, nry = (g.ny + RY - 1) / RY;
         const uint64_t per_chunk = npx * nry;

@@ -31,4 +31,10 @@ inline cudaError_t scan_u32_dev(const uint32_t *in, uint32_t *out, const uint64_
     return scan_impl(in, out, len_dev, 0, maxlen, tmp, st);
 }
 
+// device-resident length, uint64 offsets; out must hold maxlen + 1 elements
+inline cudaError_t scan_u64_dev(const uint32_t *in, uint64_t *out, const uint64_t *len_dev, uint64_t maxlen,
+                                uint64_t *tmp, cudaStream_t st) {
+    return scan_impl(in, out, len_dev, 0, maxlen, tmp, st);
+}
+
 }  // namespace roix

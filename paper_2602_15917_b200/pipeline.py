@@ -16,7 +16,7 @@ from . import _lib as L
 
 # kernels libroix launches per call (used for the bench's gpu_launches count)
 LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 3, "threshold": 1, "morph": 4,
-            "label": 16, "extract": 6}
+            "label": 16, "extract": 7}
 
 
 def _ptr(t):
@@ -79,7 +79,6 @@ class Pipeline:
         self.code_capacity = self.n if code_capacity is None else int(code_capacity)
         cdt = torch.int16 if dtype == "u16" else torch.int32
         self.codes = torch.empty(max(self.code_capacity, 8), dtype=cdt, device=dev)
-        self.ex_ws = torch.empty(L.roix_extract_workspace(self.n), dtype=torch.uint8, device=dev)
         self.labels = torch.empty(self.n, dtype=torch.int64, device=dev) if labels else None
 
     def _alloc_label(self, cap):
@@ -127,8 +126,9 @@ class Pipeline:
         L.roix_label(_ptr(self.o), _ptr(self.row_runs), ctypes.byref(self.geom), self.conn, self.min_size,
                      self.run_capacity, _ptr(self.label_ws), self.ws_bytes, ctypes.byref(out), sc, st)
         mark("label")
-        L.roix_extract(xp, self.cdtype, n, _ptr(self.o), sc, _ptr(self.codes), self.code_capacity, None,
-                       _ptr(self.ex_ws), self.ex_ws.numel(), st)
+        # a1+a8 from the kept runs of a6/a7 (reads exactly the kept voxels of x; K is not re-read)
+        L.roix_extract_runs(xp, self.cdtype, ctypes.byref(self.geom), self.run_capacity, _ptr(self.label_ws),
+                            self.ws_bytes, sc, _ptr(self.codes), self.code_capacity, None, st)
         mark("extract")
 
     def launches(self):

@@ -123,8 +123,8 @@ def slab_program(S, x, stream=None):
     else:
         L.roix_label(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, S.min_size, S.run_capacity, _ptr(S.label_ws),
                      S.ws_bytes, ctypes.byref(out), sc, st)
-    L.roix_extract(xp, S.cdtype, n, _ptr(S.o), sc, _ptr(S.codes), S.code_capacity, None, _ptr(S.ex_ws),
-                   S.ex_ws.numel(), st)
+    L.roix_extract_runs(xp, S.cdtype, geo, S.run_capacity, _ptr(S.label_ws), S.ws_bytes, sc, _ptr(S.codes),
+                        S.code_capacity, None, st)
     counts = yield ("counts", S)                                  # X5
     S.offset = int(sum(counts[:g]))
     S.global_count = int(sum(counts))

@@ -157,7 +157,10 @@ def test_threshold_f32_vs_oracle():
 # ------------------------------------------------------------------------- a4 + a5 binarise + open
 MORPH_SHAPES = [(1, 1, 1), (1, 1, 40), (2, 3, 5), (3, 5, 7), (5, 33, 65), (7, 64, 64), (9, 17, 100),
                 (4, 70, 139), (3, 20, 1390), (11, 9, 256), (6, 40, 96), (33, 8, 32),
-                (5, 17, 768), (9, 40, 512), (3, 3, 1024), (130, 5, 256)]   # X % 256 == 0: fused 3-D path
+                (5, 17, 768), (9, 40, 512), (3, 3, 1024), (130, 5, 256),
+                # whole-row 3-D kernel (X % 32 == 0, W = X/32 a power of two <= 128): every segment width,
+                # ragged row tiles, several z-chunks
+                (17, 13, 128), (19, 7, 2048), (3, 5, 4096), (20, 37, 512), (18, 11, 64), (40, 3, 32)]
 
 
 def _morph_gpu(x_np, thr, pol, se):
@@ -347,3 +350,65 @@ def test_extract_vs_oracle(n, dt):
     got2 = got2.view(np.uint16) if dt == "u16" else got2
     np.testing.assert_array_equal(got2[:cap], ref[:cap])
     assert np.all(out2.cpu().numpy()[cap:] == -1)
+
+
+# ---------------------------------------------------------- a8 extract from the labelling's runs
+def _blobby(rng, shape, p, run):
+    """Masks whose x-runs are mostly long (runs of `run` voxels merged at random phases)."""
+    Z, Y, X = shape
+    base = rng.random((Z, Y, X // run + 2)) < p
+    m = np.repeat(base, run, axis=2)
+    sh = rng.integers(0, run, (Z, Y))
+    out = np.empty(shape, np.uint8)
+    for z in range(Z):
+        for y in range(Y):
+            out[z, y] = m[z, y, sh[z, y]: sh[z, y] + X]
+    return out
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 7, 33), (6, 17, 64), (9, 40, 512), (4, 24, 2048), (5, 13, 1000),
+                                   (2, 3, 9000)])
+@pytest.mark.parametrize("dt", ["u16", "f32"])
+def test_extract_runs_vs_oracle(shape, dt):
+    """roix_extract_runs (the pipeline's a8) writes exactly oracle.extract(x, K) for the K that the
+    labelling kept, at any stream offset (all 16-byte phases) and with capacity overflow."""
+    rng = np.random.default_rng(abs(hash((shape, dt))) % 2 ** 32)
+    n = int(np.prod(shape))
+    for mask, min_size, conn in [(_blobby(rng, shape, 0.6, 37), 5, 6), ((rng.random(shape) < 0.5).astype(np.uint8), 2, 26),
+                                 (np.ones(shape, np.uint8), 1, 6), (np.zeros(shape, np.uint8), 1, 6)]:
+        Z, Y, X = shape
+        g = L.Geom(Z, Y, X, 0, Z)
+        cap = max(1, Z * Y * ((X + 1) // 2))
+        wsb = L.roix_label_workspace(g, cap)
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        o = mask_to_words(mask)
+        out = L.LabelOut(o.data_ptr(), None, None, None, 0, None)
+        sc = new_sc(1.0)
+        L.roix_label(ptr(o), None, ctypes.byref(g), conn, min_size, cap, ptr(ws), wsb, ctypes.byref(out), ptr(sc), st())
+        comp, rmin, rsz = oracle.label(mask, conn)
+        _, rK = oracle.filter_components(comp, rsz, min_size)
+        if dt == "u16":
+            x_np, eb = rng.integers(0, 65536, shape).astype(np.uint16), 2.0
+        else:
+            x_np, eb = rng.normal(0, 3, shape).astype(np.float32), 0.01
+        ref = oracle.extract(x_np.ravel(), rK.ravel(), eb)
+        x = dev(x_np)
+        for off, capacity in [(0, n), (3, n + 3), (5, n + 5), (7, n + 7), (1, ref.size // 2 + 1)]:
+            sc2 = new_sc(eb)
+            L.roix_resolve(ptr(sc2), dtype_code(x_np), 0.0, st())
+            offd = torch.tensor([off], dtype=torch.int64, device="cuda")
+            buf = torch.full((n + 16,), -1, dtype=torch.int16 if dt == "u16" else torch.int32, device="cuda")
+            L.roix_extract_runs(ptr(x), dtype_code(x_np), ctypes.byref(g), cap, ptr(ws), wsb, ptr(sc2), ptr(buf),
+                                capacity, ptr(offd), st())
+            s2 = read_sc(sc2)
+            got = buf.cpu().numpy()
+            got = got.view(np.uint16) if dt == "u16" else got
+            if off + ref.size > capacity:
+                assert s2.err & L.ERR_CAPACITY
+                lim = capacity - off
+                np.testing.assert_array_equal(got[off:capacity], ref[:lim])
+            else:
+                assert s2.err == 0 and s2.count == ref.size
+                np.testing.assert_array_equal(got[off:off + ref.size], ref)
+            raw = buf.cpu().numpy()
+            assert np.all(raw[:off] == -1) and np.all(raw[min(capacity, off + ref.size):] == -1)
