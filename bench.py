@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--graph", action="store_true", help="replay each timed step as a CUDA graph")
+    ap.add_argument("--extract", default="mask", choices=["mask", "runs"], help="a8 form (see Pipeline)")
     return ap.parse_args()
 
 
@@ -209,7 +210,7 @@ def main():
 
         p = ShardedPipeline(cfg.shape, cfg.dtype, z0=z0, nz=z1 - z0, group=dist.group.WORLD, device=dev, **kw)
     else:
-        p = Pipeline(cfg.shape, cfg.dtype, device=dev, **kw)
+        p = Pipeline(cfg.shape, cfg.dtype, device=dev, extract=args.extract, **kw)
     res = p.run(x)                          # sizes workspaces (retry on capacity), checks err
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):

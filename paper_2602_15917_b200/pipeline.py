@@ -16,7 +16,7 @@ from . import _lib as L
 
 # kernels libroix launches per call (used for the bench's gpu_launches count)
 LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 3, "threshold": 1, "morph": 4,
-            "label": 16, "extract": 7}
+            "label": 16, "extract": 6, "extract_runs": 7}
 
 
 def _ptr(t):
@@ -45,7 +45,7 @@ class Pipeline:
     """Preallocated buffers + the enqueue sequence for volumes of one shape / dtype / parameter set."""
 
     def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
-                 run_capacity=None, code_capacity=None, device=None, labels=False, fused=False):
+                 run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="mask"):
         L.load()
         self.shape = tuple(int(v) for v in shape)
         Z, Y, X = self.shape
@@ -69,6 +69,11 @@ class Pipeline:
         # off by default: on B200 the histogram pass is bound by shared-memory atomics, and the fused pass
         # (3x slower than the plain histogram at C4) loses to histogram + streaming binarisation
         self.fused = bool(fused)
+        # a8 form: "mask" = roix_extract over K (tiles of the kept mask), "runs" = roix_extract_runs over
+        # the labelling's kept runs (reads neither K nor x outside them)
+        if extract not in ("mask", "runs"):
+            raise ValueError("extract must be 'mask' or 'runs'")
+        self.extract = extract
         wsb = L.roix_histogram_binarize_workspace(self.geom) if self.fused else L.roix_morph_workspace(self.geom)
         self.morph_ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
         rows = Z * Y
@@ -79,6 +84,7 @@ class Pipeline:
         self.code_capacity = self.n if code_capacity is None else int(code_capacity)
         cdt = torch.int16 if dtype == "u16" else torch.int32
         self.codes = torch.empty(max(self.code_capacity, 8), dtype=cdt, device=dev)
+        self.ex_ws = torch.empty(L.roix_extract_workspace(self.n), dtype=torch.uint8, device=dev)
         self.labels = torch.empty(self.n, dtype=torch.int64, device=dev) if labels else None
 
     def _alloc_label(self, cap):
@@ -126,14 +132,18 @@ class Pipeline:
         L.roix_label(_ptr(self.o), _ptr(self.row_runs), ctypes.byref(self.geom), self.conn, self.min_size,
                      self.run_capacity, _ptr(self.label_ws), self.ws_bytes, ctypes.byref(out), sc, st)
         mark("label")
-        # a1+a8 from the kept runs of a6/a7 (reads exactly the kept voxels of x; K is not re-read)
-        L.roix_extract_runs(xp, self.cdtype, ctypes.byref(self.geom), self.run_capacity, _ptr(self.label_ws),
-                            self.ws_bytes, sc, _ptr(self.codes), self.code_capacity, None, st)
+        if self.extract == "runs":
+            # a1+a8 from the kept runs of a6/a7 (reads exactly the kept voxels of x; K is not re-read)
+            L.roix_extract_runs(xp, self.cdtype, ctypes.byref(self.geom), self.run_capacity, _ptr(self.label_ws),
+                                self.ws_bytes, sc, _ptr(self.codes), self.code_capacity, None, st)
+        else:
+            L.roix_extract(xp, self.cdtype, n, _ptr(self.o), sc, _ptr(self.codes), self.code_capacity, None,
+                           _ptr(self.ex_ws), self.ex_ws.numel(), st)
         mark("extract")
 
     def launches(self):
         k = sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
-                                      "extract"))
+                                      "extract" if self.extract == "mask" else "extract_runs"))
         return k + (LAUNCHES["range"] if self.cdtype == L.F32 else 0)
 
     def scalars(self):
