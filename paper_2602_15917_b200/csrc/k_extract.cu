@@ -91,6 +91,7 @@ __device__ __forceinline__ void extract_tile(const T *__restrict__ x, uint64_t n
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
     const uint64_t tile = blockIdx.x;
     const uint64_t nwords = (n + 31) / 32;
+    if (w.toff[tile + 1] == w.toff[tile]) return;   // empty tile (background): nothing to load or store
     const uint64_t wi = tile * EX_WORDS + warp * 32 + lane;
     const uint32_t word = wi < nwords ? K[wi] : 0u;
     const uint64_t v0 = wi * 32;            // first voxel of this lane's word

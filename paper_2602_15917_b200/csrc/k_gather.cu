@@ -7,20 +7,20 @@
 //   1. k_kept_len     klen[r] = x1 - x0 if run r's component is kept, else 0
 //   2. scan           koff = exclusive prefix of klen (uint64): run r's codes are [koff[r], koff[r+1])
 //   3. k_chunk_first  cfirst[c] = the run holding the first code of output chunk c
-//   4. k_gather       persistent warps over output chunks of 32 x 4 groups of V = 16 / sizeof(x)
-//                     consecutive codes.  A chunk's runs (<= 31; more: element-wise path) sit in
-//                     the warp's registers, one per lane; each lane finds its groups' runs by a
-//                     5-step shfl search, loads a group inside one run as one or two 16-byte loads
-//                     of x (all 4 groups in flight, the next chunk's run table behind them),
-//                     quantises V codes in registers and writes one 16-byte streaming store.
-//                     Groups across a run boundary (and the stream's ragged ends) go element by
-//                     element.  (A TMA-staged variant -- producer warps bulk-copying each run into
-//                     a shared-memory ring -- was measured slower on B200.)
+//   4. k_gather       persistent CTAs over output chunks of 16 KB of x.  Producer warps (one per
+//                     stage of a 4-stage shared-memory ring) read a chunk's runs and stage the kept
+//                     x of each with one bulk copy (cp.async.bulk on the TMA engine, completion on
+//                     the stage's mbarrier); consumer warps take groups of V = 16 / sizeof(x)
+//                     consecutive codes: a group inside one run is two 16-byte shared loads, V codes
+//                     quantised in registers and one 16-byte streaming store; groups across a run
+//                     boundary (and the stream's ragged ends) go element by element.  Chunks
+//                     touching more than GT_RBS non-empty runs take a direct element-wise path.
 // Output positions are handled in the global stream space p = offset + j so that every group is
 // 16-byte aligned in codes_out whatever the rank's offset.
 #include "common.cuh"
 #include "kernels.cuh"
 #include "scan.cuh"
+#include "async.cuh"
 
 namespace roix {
 
@@ -86,201 +86,251 @@ __device__ __forceinline__ uint4 code_group(uint4 v, const QP &q, uint32_t &err)
     }
 }
 
-constexpr int GW_G = 4;   // groups per lane per warp chunk
+constexpr int GT_CW = 8;                       // consumer warps
+constexpr int GT_S = 4;                        // ring stages = producer warps (warp GT_CW + s fills stage s)
+constexpr int GT_THREADS = 32 * (GT_CW + GT_S);
+constexpr int GT_GPT = 4;                      // groups per consumer thread per chunk
+constexpr int GT_RBS = 96;                     // non-empty runs per chunk on the bulk path
+constexpr uint32_t GT_XB = 16384 + 32 * GT_RBS;   // staged x bytes per stage (alignment slack per run)
 
 template <typename T>
-__host__ __device__ constexpr uint64_t gw_ch() { return (uint64_t)32 * GW_G * gr_v<T>(); }   // codes per warp chunk
+__host__ __device__ constexpr uint64_t gt_ch() { return (uint64_t)32 * GT_CW * GT_GPT * gr_v<T>(); }   // 16 KB of x
 
-// Run table of one warp chunk (chunk-relative positions r = j - jc0, jc0 = c * CH - a): lane l < nb
-// holds run rb + l -- kof = its first code's position, clamped to [0, CH + 1], and xb = the x element
-// of position 0 if that run extended there (x element of position r = xb + r); lane nb holds the end
-// of run re; lanes above nb hold UINT32_MAX.  slow: the chunk touches more than 31 runs.
-struct WTable {
-    uint32_t kof;
-    int64_t xb;
-    uint64_t rb, re;
-    uint32_t slow;
+struct GtStage {
+    uint64_t jc, je, rb, re;   // chunk outputs [jc, je); runs rb..re touch it
+    uint32_t n, slow;          // table entries; 1: direct path
 };
 
-__device__ __forceinline__ void wt_range(const uint32_t *cfirst, uint64_t c, uint64_t nchunks, uint64_t nruns,
-                                         uint64_t &rb, uint64_t &re) {
-    rb = cfirst[c];
-    re = c + 1 < nchunks ? cfirst[c + 1] : nruns - 1;
-}
+struct GtSmem {
+    uint4 x[GT_S][GT_XB / 16];
+    uint32_t rlo[GT_S][GT_RBS + 1];   // entry k: outputs [jc + rlo[k], jc + rlo[k+1]) of one run
+    uint32_t sidx[GT_S][GT_RBS];      // shared-memory element index of output jc + rlo[k]
+    GtStage hdr[GT_S];
+    uint64_t full[GT_S], empty[GT_S];
+};
 
-__device__ __forceinline__ WTable wt_load(const RunsView &R, const uint64_t *koff, uint64_t nx, uint64_t rb,
-                                          uint64_t re, int64_t jc0, uint32_t ch) {
-    WTable t;
-    const uint32_t lane = lane_id();
-    const uint64_t nb = re - rb + 1;
-    t.rb = rb;
-    t.re = re;
-    t.slow = nb > 31;
-    t.kof = 0xffffffffu;
-    t.xb = 0;
-    if (!t.slow && lane <= nb) {
-        const uint64_t r = rb + lane;
-        const int64_t ko = (int64_t)koff[r];
-        const int64_t rel = ko - jc0;
-        t.kof = rel < 0 ? 0u : (rel > (int64_t)ch ? ch + 1 : (uint32_t)rel);
-        if (lane < nb) t.xb = (int64_t)((uint64_t)R.rrow[r] * nx + R.x0[r]) - ko + jc0;
-    }
-    return t;
-}
-
-// code of output j from the runs [rb, re] in global memory (chunks touching more than 31 runs)
-template <typename T, int QM>
-__device__ __forceinline__ uint32_t code_at(const T *x, const RunsView &R, uint64_t nx, const uint64_t *koff,
-                                            uint64_t rb, uint64_t re, uint64_t j, const QP &q, uint32_t &err) {
-    uint64_t lo = rb, hi = re + 1;
+// largest k in [lo, hi) with a[k] <= v (a[lo] <= v < a[hi])
+__device__ __forceinline__ int ufind(const uint32_t *a, int lo, int hi, uint32_t v) {
     while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (koff[mid] <= j) lo = mid;
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= v) lo = mid;
         else hi = mid;
     }
-    const uint64_t v = (uint64_t)R.rrow[lo] * nx + R.x0[lo] + (j - koff[lo]);
-    return code1<T, QM>(x[v], q, err);
-}
-
-// codes of the group at chunk position r, element by element through the shared-memory copy of the
-// run table (positions in [r_lo, r_hi); stores below r_cap)
-template <typename T, typename C, int QM>
-__device__ __noinline__ void gather_elems(const T *__restrict__ x, C *__restrict__ out, uint64_t pbase, uint32_t r,
-                                          uint32_t r_lo, uint32_t r_hi, uint32_t r_cap, const uint32_t *s_kof,
-                                          const int64_t *s_xb, const QP &q, uint32_t &err) {
-    constexpr int V = gr_v<T>();
-    uint32_t h = 0;
-    for (uint32_t e = 0; e < (uint32_t)V; e++) {
-        const uint32_t rj = r + e;
-        if (rj < r_lo || rj >= r_hi) continue;
-        while (s_kof[h + 1] <= rj) h++;
-        const uint32_t cd = code1<T, QM>(x[(uint64_t)(s_xb[h] + rj)], q, err);
-        if (rj < r_cap) out[pbase + rj] = (C)cd;
-    }
+    return lo;
 }
 
 template <typename T, typename C, int QM>
-__device__ __forceinline__ void gather_w(const T *__restrict__ x, const RunsView &R, uint64_t nx,
-                                         const uint64_t *__restrict__ koff, const uint32_t *__restrict__ cfirst,
-                                         roix_scalars *sc, C *__restrict__ out, uint64_t capacity, uint64_t base_off,
-                                         const QP &q, uint32_t *s_kof, int64_t *s_xb) {
+__device__ __forceinline__ void gather_tma(const T *__restrict__ x, const RunsView &R, uint64_t nx,
+                                           const uint64_t *__restrict__ koff, const uint32_t *__restrict__ cfirst,
+                                           roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
+                                           uint64_t base_off, const QP &q, GtSmem &sm) {
     constexpr int V = gr_v<T>();
-    constexpr uint32_t LV = V == 8 ? 3 : 2;
-    constexpr uint32_t CH = (uint32_t)gw_ch<T>();
-    const uint32_t lane = lane_id();
+    constexpr uint64_t CH = gt_ch<T>();
+    const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
     const uint64_t nruns = *R.n_runs;
     const uint64_t total = nruns ? koff[nruns] : 0;
     const uint64_t a = base_off % V;
     const uint64_t nchunks = total ? (total + a + CH - 1) / CH : 0;
-    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
-    const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
-    uint32_t err = 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && base_off + total > capacity) err |= ROIX_ERR_CAPACITY;
-    uint64_t c = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (c < nchunks) {
-        uint64_t rb, re;
-        wt_range(cfirst, c, nchunks, nruns, rb, re);
-        WTable tb = wt_load(R, koff, nx, rb, re, (int64_t)(c * CH) - (int64_t)a, CH);
-        for (; c < nchunks; c += nw) {
-            const uint64_t cn = c + nw;
-            uint64_t rb2 = 0, re2 = 0;
-            if (cn < nchunks) wt_range(cfirst, cn, nchunks, nruns, rb2, re2);   // next chunk's runs
-            const int64_t jc0 = (int64_t)(c * CH) - (int64_t)a;
-            const uint64_t pbase = base_off + (uint64_t)jc0;                       // output of position 0
-            const uint32_t r_lo = jc0 < 0 ? (uint32_t)(-jc0) : 0u;
-            const uint32_t r_hi = (uint32_t)min((int64_t)CH, (int64_t)total - jc0);
-            const uint32_t r_cap = capacity > pbase ? (uint32_t)min((uint64_t)CH, capacity - pbase) : 0u;
-            if (!tb.slow) {
-                __syncwarp();
-                s_kof[lane] = tb.kof;
-                if (lane == 0) s_kof[32] = 0xffffffffu;
-                s_xb[lane] = tb.xb;
-                __syncwarp();
-                bool whole[GW_G];
-                uint32_t kk[GW_G];
-                uint4 b0[GW_G], b1[GW_G];
-#pragma unroll
-                for (int u = 0; u < GW_G; u++) {
-                    const uint32_t r = (lane + 32u * u) * V;
-                    const uint32_t rs = max(r, r_lo);
-                    // run of position rs: the largest lane k with kof_k <= rs (lanes hold increasing kof)
-                    uint32_t k = 0;
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const uint32_t kv = __shfl_sync(FULL, tb.kof, k + step);
-                        if (kv <= rs) k += step;
-                    }
-                    const uint32_t kend = __shfl_sync(FULL, tb.kof, (k + 1) & 31);
-                    const int64_t xb = __shfl_sync(FULL, tb.xb, k);
-                    whole[u] = r >= r_lo && r + V <= r_hi && kend >= r + V;
-                    const uint64_t v = (uint64_t)(xb + r);
-                    kk[u] = (uint32_t)v & (V - 1);
-                    b0[u] = b1[u] = make_uint4(0, 0, 0, 0);
-                    if (whole[u]) {
-                        b0[u] = __ldcs(x4 + (v >> LV));
-                        if (kk[u]) b1[u] = __ldcs(x4 + (v >> LV) + 1);
-                    }
+    if (warp >= GT_CW) {
+        // ------------------------------------------------------------------ producer of stage s
+        // Chunk k+S's first 32 runs are loaded while chunk k's copies fly, and chunk k+2S's run range
+        // (cfirst) one round earlier still, so issuing a chunk's copies never waits on a global load.
+        const int s = (int)warp - GT_CW;
+        char *xs = reinterpret_cast<char *>(sm.x[s]);
+        auto chunk_of = [&](uint64_t k) { return (uint64_t)blockIdx.x + k * gridDim.x; };
+        auto range = [&](uint64_t k, uint64_t &rb, uint64_t &re) {
+            const uint64_t c = chunk_of(k);
+            rb = re = 0;
+            if (c < nchunks) {
+                rb = cfirst[c];
+                re = c + 1 < nchunks ? cfirst[c + 1] : nruns - 1;
+            }
+        };
+        // per lane: run rb + lane of the prefetched chunk (koff, koff + 1, row, x0)
+        struct RunPF {
+            uint64_t rb, re, k0, k1;
+            uint32_t row, x0;
+        };
+        auto runs = [&](uint64_t rb, uint64_t re, uint64_t w) {
+            RunPF p;
+            p.rb = rb;
+            p.re = re;
+            p.k0 = p.k1 = 0;
+            p.row = p.x0 = 0;
+            const uint64_t r = w + lane;
+            if (r <= re) {
+                p.k0 = koff[r];
+                p.k1 = koff[r + 1];
+                p.row = R.rrow[r];
+                p.x0 = R.x0[r];
+            }
+            return p;
+        };
+        uint64_t rb1, re1, rb2, re2;
+        range(s, rb1, re1);
+        RunPF P = runs(rb1, re1, rb1);
+        range(s + GT_S, rb2, re2);
+        for (uint64_t k = s, i = 0;; k += GT_S, i++) {
+            const uint64_t c = chunk_of(k);
+            if (c >= nchunks) break;
+            if (i > 0) mbar_wait(&sm.empty[s], (uint32_t)((i - 1) & 1));
+            const uint64_t jc = c * CH > a ? c * CH - a : 0, je = min(total, (c + 1) * CH - a);
+            const uint64_t rb = P.rb, re = P.re;
+            uint32_t n = 0, cursor = 0, slow = 0;
+            for (uint64_t w = rb; w <= re; w += 32) {
+                const RunPF q = w == rb ? P : runs(rb, re, w);   // windows past the first: rare
+                uint64_t lo = 0, hi = 0, xb = 0;
+                if (w + lane <= re) {
+                    lo = max(q.k0, jc);
+                    hi = min(q.k1, je);
+                    if (hi > lo) xb = (uint64_t)q.row * nx + q.x0 + (lo - q.k0);   // x element of output lo
                 }
-                WTable tn = tb;
-                if (cn < nchunks) tn = wt_load(R, koff, nx, rb2, re2, (int64_t)(cn * CH) - (int64_t)a, CH);
+                const bool ne = hi > lo;
+                const uint32_t bal = __ballot_sync(FULL, ne);
+                if (n + __popc(bal) > (uint32_t)GT_RBS) {
+                    slow = 1;
+                    break;
+                }
+                uint32_t len = 0, b_lo = 0;
+                uint64_t src = 0;
+                if (ne) {
+                    const uint64_t e0 = xb * sizeof(T), e1 = (xb + (hi - lo)) * sizeof(T);
+                    src = e0 & ~15ull;
+                    len = (uint32_t)(((e1 + 15) & ~15ull) - src);
+                    b_lo = (uint32_t)(e0 - src);
+                }
+                const uint32_t incl = warp_incl_scan(len);
+                const uint32_t tot = __shfl_sync(FULL, incl, 31);
+                const uint32_t my = cursor + incl - len;
+                if (ne) {
+                    const uint32_t idx = n + __popc(bal & low_mask(lane));
+                    sm.rlo[s][idx] = (uint32_t)(lo - jc);
+                    sm.sidx[s][idx] = (my + b_lo) / (uint32_t)sizeof(T);
+                }
+                if (lane == 0 && tot) mbar_expect_tx(&sm.full[s], tot);
+                __syncwarp();
+                if (ne) bulk_g2s(xs + my, reinterpret_cast<const char *>(x) + src, len, &sm.full[s]);
+                cursor += tot;
+                n += __popc(bal);
+            }
+            if (lane == 0) {
+                sm.rlo[s][slow ? 0 : n] = (uint32_t)(je - jc);
+                GtStage h;
+                h.jc = jc;
+                h.je = je;
+                h.rb = rb;
+                h.re = re;
+                h.n = n;
+                h.slow = slow;
+                sm.hdr[s] = h;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.full[s]);
+            // prefetch: runs of chunk k + S (range known), range of chunk k + 2S
+            P = runs(rb2, re2, rb2);
+            range(k + 2 * GT_S, rb2, re2);
+        }
+        return;
+    }
+    // ---------------------------------------------------------------------- consumers
+    const uint32_t t = threadIdx.x;
+    uint32_t err = 0;
+    if (blockIdx.x == 0 && t == 0 && base_off + total > capacity) err |= ROIX_ERR_CAPACITY;
+    for (uint64_t k = 0;; k++) {
+        const uint64_t c = blockIdx.x + k * gridDim.x;
+        if (c >= nchunks) break;
+        const int s = (int)(k % GT_S);
+        mbar_wait(&sm.full[s], (uint32_t)((k / GT_S) & 1));
+        const GtStage h = sm.hdr[s];
+        const int64_t jc0 = (int64_t)(c * CH) - (int64_t)a;   // stream-aligned chunk origin (<= h.jc)
+        if (!h.slow) {
+            const uint32_t *rlo = sm.rlo[s], *sidx = sm.sidx[s];
+            const T *xs = reinterpret_cast<const T *>(sm.x[s]);
+            const int n = (int)h.n;
+            int hint = 0;
 #pragma unroll
-                for (int u = 0; u < GW_G; u++) {
-                    const uint32_t r = (lane + 32u * u) * V;
-                    if (whole[u]) {
-                        const uint4 cv = code_group<T, QM>(window16<T>(b0[u], b1[u], kk[u]), q, err);
-                        if (r + V <= r_cap) {
-                            __stcs(reinterpret_cast<uint4 *>(out + pbase + r), cv);
-                        } else {
-                            const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
+            for (int u = 0; u < GT_GPT; u++) {
+                const int64_t jg = jc0 + (int64_t)(t + u * 32 * GT_CW) * V;   // group start (16-byte aligned in out)
+                const uint64_t j = jg < (int64_t)h.jc ? h.jc : (uint64_t)jg;
+                if (j >= h.je) break;
+                const uint32_t rj = (uint32_t)(j - h.jc);
+                if (rlo[hint + 1] <= rj) hint = ufind(rlo, hint + 1, n, rj);
+                const uint64_t p = base_off + (uint64_t)jg;
+                const bool whole = jg >= (int64_t)h.jc && (uint64_t)jg + V <= h.je && rlo[hint + 1] >= rj + V;
+                if (whole) {
+                    const uint32_t si = sidx[hint] + (rj - rlo[hint]);
+                    const uint32_t kk = si % V;
+                    const uint4 *b = reinterpret_cast<const uint4 *>(xs + (si - kk));
+                    const uint4 b0 = b[0];
+                    const uint4 b1 = kk ? b[1] : b0;
+                    const uint4 cv = code_group<T, QM>(window16<T>(b0, b1, kk), q, err);
+                    if (p + V <= capacity) {
+                        __stcs(reinterpret_cast<uint4 *>(out + p), cv);
+                    } else {
+                        const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
-                            for (int e = 0; e < V; e++)
-                                if (r + e < r_cap)
-                                    out[pbase + r + e] = (C)(sizeof(C) == 2 ? (cw[e >> 1] >> ((e & 1) * 16)) & 0xffffu
-                                                                            : cw[e]);
+                        for (int e = 0; e < V; e++) {
+                            const uint32_t cd = sizeof(C) == 2 ? (cw[e >> 1] >> ((e & 1) * 16)) & 0xffffu : cw[e];
+                            if (p + e < capacity) out[p + e] = (C)cd;
                         }
                     }
+                } else {
+                    int hh = hint;
+                    for (uint64_t jj = j; jj < (uint64_t)(jg + V) && jj < h.je; jj++) {
+                        const uint32_t r2 = (uint32_t)(jj - h.jc);
+                        if (rlo[hh + 1] <= r2) hh = ufind(rlo, hh + 1, n, r2);
+                        const uint32_t cd = code1<T, QM>(xs[sidx[hh] + (r2 - rlo[hh])], q, err);
+                        if (base_off + jj < capacity) out[base_off + jj] = (C)cd;
+                    }
                 }
-                // groups across a run boundary / at the stream's ends (a warp-uniform branch)
-#pragma unroll
-                for (int u = 0; u < GW_G; u++) {
-                    const uint32_t r = (lane + 32u * u) * V;
-                    const bool need = !whole[u] && r + V > r_lo && r < r_hi;
-                    if (__any_sync(FULL, need) && need)
-                        gather_elems<T, C, QM>(x, out, pbase, r, r_lo, r_hi, r_cap, s_kof, s_xb, q, err);
+            }
+        } else {
+            // many short runs: element by element, binary search over the chunk's runs in koff
+            for (uint64_t jj = h.jc + t; jj < h.je; jj += 32 * GT_CW) {
+                uint64_t lo = h.rb, hi = h.re + 1;
+                while (hi - lo > 1) {
+                    const uint64_t mid = (lo + hi) >> 1;
+                    if (koff[mid] <= jj) lo = mid;
+                    else hi = mid;
                 }
-                tb = tn;
-            } else {
-                for (uint32_t r = max(r_lo, 0u) + lane; r < r_hi; r += 32) {
-                    const uint32_t cd = code_at<T, QM>(x, R, nx, koff, tb.rb, tb.re, (uint64_t)(jc0 + r), q, err);
-                    if (r < r_cap) out[pbase + r] = (C)cd;
-                }
-                if (cn < nchunks) tb = wt_load(R, koff, nx, rb2, re2, (int64_t)(cn * CH) - (int64_t)a, CH);
+                const uint64_t v = (uint64_t)R.rrow[lo] * nx + R.x0[lo] + (jj - koff[lo]);
+                const uint32_t cd = code1<T, QM>(x[v], q, err);
+                if (base_off + jj < capacity) out[base_off + jj] = (C)cd;
             }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[s]);
     }
     if (err) set_err(sc, err);
 }
 
 template <typename T, typename C>
-__global__ void __launch_bounds__(256, 2) k_gather(const T *__restrict__ x, const RunsView R, uint64_t nx,
-                                                   const uint64_t *__restrict__ koff, const uint32_t *__restrict__ cfirst,
-                                                   roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
-                                                   const uint64_t *offset) {
-    // each warp's run table, mirrored in shared memory for the element-wise (divergent) cases
-    __shared__ uint32_t s_kof[8][33];
-    __shared__ int64_t s_xb[8][32];
-    if (get_err(sc)) return;
+__global__ void __launch_bounds__(GT_THREADS) k_gather(const T *__restrict__ x, const RunsView R, uint64_t nx,
+                                                       const uint64_t *__restrict__ koff,
+                                                       const uint32_t *__restrict__ cfirst, roix_scalars *sc,
+                                                       C *__restrict__ out, uint64_t capacity, const uint64_t *offset) {
+    extern __shared__ uint4 gt_dyn[];
+    GtSmem &sm = *reinterpret_cast<GtSmem *>(gt_dyn);
+    __shared__ uint32_t skip;
+    if (threadIdx.x == 0) {
+        skip = get_err(sc);   // read once: other CTAs may set error bits while this one starts
+        for (int s = 0; s < GT_S; s++) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], GT_CW);
+        }
+    }
+    __syncthreads();
+    if (skip) return;
     const QP q = load_qp(sc);
     const uint64_t base_off = offset ? *offset : 0;
-    const int w = threadIdx.x >> 5;
     if constexpr (sizeof(T) == 4) {
-        gather_w<T, C, QM_FLOAT>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, s_kof[w], s_xb[w]);
+        gather_tma<T, C, QM_FLOAT>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, sm);
     } else {
         switch (qmode(q)) {
-        case QM_POW2: gather_w<T, C, QM_POW2>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, s_kof[w], s_xb[w]); break;
-        case QM_INT: gather_w<T, C, QM_INT>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, s_kof[w], s_xb[w]); break;
-        case QM_ONE: gather_w<T, C, QM_ONE>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, s_kof[w], s_xb[w]); break;
-        default: gather_w<T, C, QM_FLOAT>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, s_kof[w], s_xb[w]); break;
+        case QM_POW2: gather_tma<T, C, QM_POW2>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, sm); break;
+        case QM_INT: gather_tma<T, C, QM_INT>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, sm); break;
+        case QM_ONE: gather_tma<T, C, QM_ONE>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, sm); break;
+        default: gather_tma<T, C, QM_FLOAT>(x, R, nx, koff, cfirst, sc, out, capacity, base_off, q, sm); break;
         }
     }
 }
@@ -295,13 +345,16 @@ __global__ void k_gather_total(const RunsView R, const uint64_t *koff, roix_scal
 
 using namespace roix;
 
-uint64_t gather_chunks_max(uint64_t n) { return (n + 16) / gw_ch<float>() + 2; }
+uint64_t gather_chunks_max(uint64_t n) { return (n + 16) / gt_ch<float>() + 2; }
 
 template <typename T, typename C>
 static cudaError_t gather_grid(int *grid) {
-    int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<T, C>, 256, 0);
+    const size_t smem = sizeof(GtSmem);
+    cudaError_t e = cudaFuncSetAttribute(k_gather<T, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<T, C>, GT_THREADS, smem)) != cudaSuccess)
+        return e;
     *grid = num_sms() * (occ > 0 ? occ : 1);
     return cudaSuccess;
 }
@@ -316,14 +369,14 @@ cudaError_t launch_gather(const void *x, int dtype, uint64_t nx, const RunsView 
     static int g16 = 0, g32 = 0;
     if (dtype == ROIX_U16) {
         if (!g16 && (e = gather_grid<uint16_t, uint16_t>(&g16)) != cudaSuccess) return e;
-        k_chunk_first<<<grid, 256, 0, st>>>(R, koff, offset, gw_ch<uint16_t>(), gr_v<uint16_t>(), cfirst, sc);
-        k_gather<uint16_t, uint16_t><<<g16, 256, 0, st>>>((const uint16_t *)x, R, nx, koff, cfirst, sc,
-                                                         (uint16_t *)codes, capacity, offset);
+        k_chunk_first<<<grid, 256, 0, st>>>(R, koff, offset, gt_ch<uint16_t>(), gr_v<uint16_t>(), cfirst, sc);
+        k_gather<uint16_t, uint16_t><<<g16, GT_THREADS, sizeof(GtSmem), st>>>(
+            (const uint16_t *)x, R, nx, koff, cfirst, sc, (uint16_t *)codes, capacity, offset);
     } else {
         if (!g32 && (e = gather_grid<float, int32_t>(&g32)) != cudaSuccess) return e;
-        k_chunk_first<<<grid, 256, 0, st>>>(R, koff, offset, gw_ch<float>(), gr_v<float>(), cfirst, sc);
-        k_gather<float, int32_t><<<g32, 256, 0, st>>>((const float *)x, R, nx, koff, cfirst, sc, (int32_t *)codes,
-                                                      capacity, offset);
+        k_chunk_first<<<grid, 256, 0, st>>>(R, koff, offset, gt_ch<float>(), gr_v<float>(), cfirst, sc);
+        k_gather<float, int32_t><<<g32, GT_THREADS, sizeof(GtSmem), st>>>(
+            (const float *)x, R, nx, koff, cfirst, sc, (int32_t *)codes, capacity, offset);
     }
     k_gather_total<<<1, 1, 0, st>>>(R, koff, sc);
     return cudaGetLastError();

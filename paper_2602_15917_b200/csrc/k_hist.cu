@@ -61,52 +61,96 @@ __global__ void __launch_bounds__(1024, 2) k_hist_u16(const uint16_t *__restrict
 // within one bin of norm8(x) and one correction in each direction is exact.  `exact_est` is false
 // only for a subnormal I_max (255 / I_max overflows); the edges are then walked.
 __device__ __forceinline__ int norm8_edges(float x, float scale, const float *e, bool exact_est) {
-    int k = __float2int_rz(fminf(fmaxf(x * scale + 0.5f, 0.0f), 255.0f));
+    const float t = fminf(fmaxf(x * scale + 0.5f, 0.0f), 255.0f);   // NaN -> 0 (flagged by the caller)
+    int k = __float2int_rz(t);
     if (exact_est) {
-        k += (x >= e[k + 1]);
-        k -= (x < e[k]);
+        // t is within ~1e-4 of the exact 255 x / I_max + 1/2 (x <= I_max); away from an integer the
+        // estimate is the bin, next to one the edges decide
+        const float fr = t - (float)k;
+        if (fr < 1e-3f || fr > 0.999f) {
+            k = min(k + (x >= e[k + 1]), 255);   // (x = +inf would step past 255)
+            k -= (x < e[k]);
+        }
     } else {
-        while (x >= e[k + 1]) k++;
-        while (x < e[k]) k--;
+        while (k < 255 && x >= e[k + 1]) k++;
+        while (k > 0 && x < e[k]) k--;
     }
     return k;
 }
 
-__global__ void __launch_bounds__(512) k_hist_f32(const float *__restrict__ x, uint64_t n, roix_scalars *sc,
+// 256 bins x 32 lane slots: lane l increments slot l of its bin, so the lanes of a warp never hit
+// the same shared-memory word or bank (CT volumes put most voxels into a few normalised bins -- air,
+// one material -- which would otherwise serialise 32-way on one counter).
+__global__ void __launch_bounds__(512, 3) k_hist_f32(const float *__restrict__ x, uint64_t n, roix_scalars *sc,
                                                   uint64_t *gh) {
-    __shared__ uint32_t sh[256];
+    __shared__ uint32_t sh[256 * 32];
     __shared__ float e[257];
     if (get_err(sc)) return;
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-        sh[i] = 0;
-        e[i] = i == 0 ? -INFINITY : sc->edges[i];
-    }
+    for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) sh[i] = 0;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) e[i] = i == 0 ? -INFINITY : sc->edges[i];
     if (threadIdx.x == 0) e[256] = INFINITY;
     const float scale = 255.0f / sc->i_max;
     const bool ex = scale <= 1e30f;
     __syncthreads();
+    uint32_t *my = sh + lane_id();
     bool bad = false;
     const float4 *x4 = reinterpret_cast<const float4 *>(x);
     const uint64_t n4 = n / 4, stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ex && i + stride < n4) {
+        // branch-free body: a non-finite voxel only sets the (sticky, fatal) error bit; its count
+        // lands in a clamped bin of a histogram that is then discarded.  The next pair of loads is
+        // issued before the current pair is binned.
+        float4 a = __ldcs(x4 + i), b = __ldcs(x4 + i + stride);
+        while (true) {
+            const uint64_t in = i + 2 * stride;
+            const bool more = in + stride < n4;
+            float4 na = a, nb = b;
+            if (more) {
+                na = __ldcs(x4 + in);
+                nb = __ldcs(x4 + in + stride);
+            }
+            float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                bad |= !(fabsf(v[k]) <= FLT_MAX);
+                atomicAdd(my + 32 * norm8_edges(v[k], scale, e, true), 1u);
+            }
+            i = in;
+            if (!more) break;
+            a = na;
+            b = nb;
+        }
+    }
+    for (; i + stride < n4; i += 2 * stride) {
+        float4 a = __ldcs(x4 + i), b = __ldcs(x4 + i + stride);
+        float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            if (fabsf(v[k]) <= FLT_MAX) atomicAdd(my + 32 * norm8_edges(v[k], scale, e, ex), 1u);
+            else bad = true;
+        }
+    }
+    for (; i < n4; i += stride) {
         float4 a = __ldcs(x4 + i);
         float v[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            if (fabsf(v[k]) <= FLT_MAX) atomicAdd(&sh[norm8_edges(v[k], scale, e, ex)], 1u);
+            if (fabsf(v[k]) <= FLT_MAX) atomicAdd(my + 32 * norm8_edges(v[k], scale, e, ex), 1u);
             else bad = true;
         }
     }
     if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
         float v = x[n4 * 4 + threadIdx.x];
-        if (fabsf(v) <= FLT_MAX) atomicAdd(&sh[norm8_edges(v, scale, e, ex)], 1u);
+        if (fabsf(v) <= FLT_MAX) atomicAdd(my + 32 * norm8_edges(v, scale, e, ex), 1u);
         else bad = true;
     }
     if (bad) set_err(sc, ROIX_ERR_NONFINITE);
     __syncthreads();
-    for (int b = threadIdx.x; b < 256; b += blockDim.x) {
-        uint32_t c = sh[b];
-        if (c) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)c);
+    // bin b = warp-sum of its 32 slots
+    for (int b = threadIdx.x >> 5; b < 256; b += blockDim.x >> 5) {
+        const uint32_t c = __reduce_add_sync(FULL, sh[b * 32 + lane_id()]);
+        if (lane_id() == 0 && c) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)c);
     }
 }
 
@@ -172,7 +216,7 @@ cudaError_t launch_hist_u16(const uint16_t *x, uint64_t n, roix_scalars *sc, uin
 }
 
 cudaError_t launch_hist_f32(const float *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st) {
-    k_hist_f32<<<grid_for(n / 4, 512, 4), 512, 0, st>>>(x, n, sc, hist);
+    k_hist_f32<<<grid_for(n / 4, 512, 3), 512, 0, st>>>(x, n, sc, hist);
     return cudaGetLastError();
 }
 

@@ -45,15 +45,19 @@ __global__ void __launch_bounds__(512) k_range(const float *__restrict__ x, uint
     const float4 *x4 = reinterpret_cast<const float4 *>(x);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (; i + 3 * stride < n4; i += 4 * stride) {
-        float4 a = __ldcs(x4 + i), b = __ldcs(x4 + i + stride), c = __ldcs(x4 + i + 2 * stride),
-               d = __ldcs(x4 + i + 3 * stride);
-        float v[16] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w, d.x, d.y, d.z, d.w};
+    for (; i + 7 * stride < n4; i += 8 * stride) {   // 8 x 16 bytes in flight per thread
+        float4 a[8];
 #pragma unroll
-        for (int k = 0; k < 16; k++) {
-            bad |= !(fabsf(v[k]) <= FLT_MAX);
-            lo = fminf(lo, v[k]);
-            hi = fmaxf(hi, v[k]);
+        for (int u = 0; u < 8; u++) a[u] = __ldcs(x4 + i + u * stride);
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const float v[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                bad |= !(fabsf(v[k]) <= FLT_MAX);
+                lo = fminf(lo, v[k]);
+                hi = fmaxf(hi, v[k]);
+            }
         }
     }
     for (; i < n4; i += stride) {
@@ -151,7 +155,7 @@ cudaError_t launch_scalars_init(roix_scalars *sc, float eb, cudaStream_t st) {
 }
 
 cudaError_t launch_range(const float *x, uint64_t n, roix_scalars *sc, cudaStream_t st) {
-    int blocks = num_sms() * 4;
+    int blocks = num_sms() * 3;
     uint64_t need = (n / 4 + 511) / 512;
     if ((uint64_t)blocks > need) blocks = (int)(need > 0 ? need : 1);
     k_range<<<blocks, 512, 0, st>>>(x, n, sc);

@@ -1,7 +1,9 @@
-// scan.cuh -- exclusive prefix sum of uint32 counts (three launches: tile sums, scan of the tile
-// sums in one CTA, tile-local scans).  out[len] receives the total (saturated to uint32); the exact
-// uint64 total is kept at scan_total_ptr(tmp, maxlen).  The length may live in device memory
-// (scan_u32_dev): elements at or past it are treated as 0 and not written.
+// scan.cuh -- exclusive prefix sum of uint32 counts in one pass (decoupled look-back: every tile
+// publishes its aggregate, then its inclusive prefix, and each tile's first warp sums its
+// predecessors' published values 32 at a time).  out[len] receives the total (saturated to uint32 for
+// uint32 outputs); the exact uint64 total is kept at scan_total_ptr(tmp, maxlen).  The length may
+// live in device memory (scan_u32_dev / scan_u64_dev): elements at or past it are treated as 0 and
+// not written.  in and out may alias.
 #pragma once
 #include "common.cuh"
 
@@ -9,7 +11,8 @@ namespace roix {
 
 constexpr int SCAN_T = 256, SCAN_V = 8, SCAN_TILE = SCAN_T * SCAN_V;
 
-__host__ __device__ inline uint64_t scan_nblocks(uint64_t maxlen) { return (maxlen + SCAN_TILE - 1) / SCAN_TILE; }
+// tiles of a scan of up to maxlen elements (one more than needed, so the tile holding index len exists)
+__host__ __device__ inline uint64_t scan_nblocks(uint64_t maxlen) { return maxlen / SCAN_TILE + 1; }
 inline uint64_t scan_tmp_elems(uint64_t maxlen) { return scan_nblocks(maxlen) + 2; }
 inline const uint64_t *scan_total_ptr(const uint64_t *tmp, uint64_t maxlen) { return tmp + scan_nblocks(maxlen); }
 
