@@ -109,6 +109,13 @@ def alg_bytes(cfg, n, count):
     return out
 
 
+# the C-ABI call each timed stage is (its kernels: profiles/*/launches_*.txt)
+STAGE_CALLS = {"range": "roix_range (k_range)", "histogram": "roix_histogram (k_hist_*)",
+               "morph": "roix_morph (k_binarize + k_open3d_rows/k_open2d)",
+               "label": "roix_label (runs, union-find, filter: 9 kernels)",
+               "extract": "roix_extract (k_extract_count + scan + k_extract)"}
+
+
 def cpu_info():
     return {"cores_available": os.cpu_count()}
 
@@ -291,10 +298,14 @@ def main():
     ab = alg_bytes(cfg, n // world, count_local)
     dom = max((k for k in ab if k in stage_ms), key=lambda k: stage_ms[k])
     achieved = ab[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    # DRAM bytes per launch of the dominant stage, from the committed ncu launch list of this config
+    # (scripts/ncu_traffic.py): dram__bytes_read.sum + dram__bytes_write.sum over its kernels
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic_%s.json" % cfg.name)
-    if os.path.exists(tf):
-        traffic = json.load(open(tf)).get(dom)
+    if os.path.exists(tf) and args.scale == 1.0 and world == 1:
+        st_ = json.load(open(tf)).get("stages", {}).get(dom)
+        if st_:
+            traffic = st_["dram_bytes"]
     step_alg = sum(ab.values()) * world
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -304,8 +315,10 @@ def main():
                    "rel_eb": cfg.rel_eb, "conn": cfg.conn, "se": cfg.se, "min_size": cfg.min_size,
                    "polarity": "LOW" if cfg.polarity else "HIGH", "parallelism": "zslab%d" % world,
                    "l2": "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src},
+        "roofline": {"bound": "hbm", "kernel": STAGE_CALLS.get(dom, dom), "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "alg_bytes": ab[dom],
+                     "peak_source": peak_src},
+        "stage_frac": {k: ab[k] / (stage_ms[k] * 1e-3) / 1e9 / peak for k in ab if k in stage_ms},
         "step_roofline": {"alg_bytes_per_step": step_alg, "achieved": step_alg / (ms_step * 1e-3) / 1e9,
                           "frac": step_alg / (ms_step * 1e-3) / 1e9 / peak},
         "stage_ms": stage_ms, "kept": count, "kept_fraction": count / n, "spatial_reduction": n / max(count, 1),

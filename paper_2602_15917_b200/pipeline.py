@@ -15,8 +15,8 @@ import torch
 from . import _lib as L
 
 # kernels libroix launches per call (used for the bench's gpu_launches count)
-LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 3, "threshold": 1, "morph": 4,
-            "label": 16, "extract": 6, "extract_runs": 7}
+LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 1, "threshold": 1, "morph": 2,
+            "label": 11, "extract": 4, "extract_runs": 5}
 
 
 def _ptr(t):

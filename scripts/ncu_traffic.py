@@ -1,52 +1,70 @@
-"""Summarise an ncu report: per-kernel duration and DRAM bytes, and per-stage traffic of the bench's
-dominant stage (written to profiles/ncu_traffic_<config>.json for bench.py's roofline.traffic)."""
+"""Per-stage DRAM traffic of one bench step from an ncu launch list (--metrics gpu__time_duration.sum,
+dram__bytes_read.sum,dram__bytes_write.sum --csv): writes profiles/ncu_traffic_<config>.json, read by
+bench.py for roofline.traffic (bytes per launch of the dominant stage).
+
+    python scripts/ncu_traffic.py gpurun_out/launches_C2.csv C2
+"""
 import csv
 import json
-import subprocess
+import os
 import sys
 
+# kernels of each pipeline stage (one C-ABI call each; see paper_2602_15917_b200/pipeline.py)
 STAGE = {
     "range": ["k_range"],
     "histogram": ["k_hist_u16", "k_hist_f32"],
     "threshold": ["k_threshold"],
-    "morph": ["k_binarize", "k_open3d_reg", "k_open2d", "k_open3d"],
-    "label": ["k_extract_runs", "k_union_local", "k_union_cross", "k_flatten_sizes", "k_root_flags", "k_table",
-              "k_clear_dropped", "k_runs_total", "k_table_total"],
-    "extract": ["k_extract_count", "k_extract"],
+    "morph": ["k_binarize", "k_open3d_reg", "k_open3d_rows", "k_open2d"],
+    "label": ["k_scan_dlb", "k_runs_total", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross",
+              "k_flatten_sizes", "k_root_flags", "k_table", "k_table_total", "k_clear_dropped"],
+    "extract": ["k_extract_count", "k_extract", "k_extract_total"],
 }
 
 
-def rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    r = list(csv.reader(out.splitlines()))
-    h = r[0]
-    res = []
-    for v in r[2:]:
-        d = dict(zip(h, v))
-        name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("roix::", "").split("<")[0]
-        res.append({"kernel": name, "ms": float(d.get("gpu__time_duration.sum", "nan")) / 1e6 if False else
-                    float(d.get("gpu__time_duration.sum", "nan")),
-                    "dram_read": float(d.get("dram__bytes_read.sum", "nan")),
-                    "dram_write": float(d.get("dram__bytes_write.sum", "nan")),
-                    "units": (r[1][h.index("gpu__time_duration.sum")], r[1][h.index("dram__bytes_read.sum")])})
-    return res
+def steps(path):
+    rows = [r for r in csv.reader(open(path)) if r and not r[0].startswith("==")]
+    h = rows[0]
+    data, order = {}, []
+    for r in rows[1:]:
+        d = dict(zip(h, r))
+        name = d["Kernel Name"].split("(")[0].replace("void ", "").replace("roix::", "").split("<")[0].strip()
+        k = (int(d["ID"]), name)
+        if k not in data:
+            order.append(k)
+        unit = d.get("Metric Unit", "")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(unit, 1)
+        data.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * scale
+    starts = [i for i, k in enumerate(order) if k[1] == "k_scalars_init"]
+    return data, order, starts
 
 
-def main(rep, config, out):
-    rs = rows(rep)
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
-    per = {}
-    for r in rs:
-        f = scale.get(r["units"][1], 1)
-        per.setdefault(r["kernel"], []).append((r["dram_read"] + r["dram_write"]) * f)
-    stages = {}
-    for st, ks in STAGE.items():
-        b = sum(sum(per[k]) / len(per[k]) for k in ks if k in per)
-        if any(k in per for k in ks):
-            stages[st] = b
-    json.dump(stages, open(out, "w"), indent=1)
-    print(json.dumps(stages))
+def main(path, config, out_dir="profiles"):
+    data, order, starts = steps(path)
+    s0, s1 = starts[-1], len(order)          # the last complete step of the run
+    kern = order[s0:s1]
+    # the scan kernel appears in label and extract: attribute by position (label precedes extract)
+    res, stage_of = {}, {}
+    cur = None
+    for k in kern:
+        for st, names in STAGE.items():
+            if k[1] in names and not (k[1] == "k_scan_dlb" and cur == "extract"):
+                cur = st
+                break
+        stage_of[k] = cur
+    for k in kern:
+        st = stage_of[k]
+        if st is None:
+            continue
+        m = data[k]
+        res.setdefault(st, {"dram_bytes": 0.0, "ns": 0.0, "kernels": []})
+        res[st]["dram_bytes"] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
+        res[st]["ns"] += m.get("gpu__time_duration.sum", 0)
+        res[st]["kernels"].append(k[1])
+    os.makedirs(out_dir, exist_ok=True)
+    dst = os.path.join(out_dir, "ncu_traffic_%s.json" % config)
+    json.dump({"source": os.path.basename(path), "stages": res}, open(dst, "w"), indent=1)
+    print(json.dumps({k: (round(v["dram_bytes"] / 1e6, 1), round(v["ns"] / 1e3, 1)) for k, v in res.items()}))
 
 
 if __name__ == "__main__":
-    main(*sys.argv[1:4])
+    main(*sys.argv[1:])
