@@ -215,7 +215,8 @@ def main():
     if world > 1:
         from paper_2602_15917_b200.sharded import ShardedPipeline
 
-        p = ShardedPipeline(cfg.shape, cfg.dtype, z0=z0, nz=z1 - z0, group=dist.group.WORLD, device=dev, **kw)
+        p = ShardedPipeline(cfg.shape, cfg.dtype, z0=z0, nz=z1 - z0, group=dist.group.WORLD, device=dev,
+                            extract=args.extract, **kw)
     else:
         p = Pipeline(cfg.shape, cfg.dtype, device=dev, extract=args.extract, **kw)
     res = p.run(x)                          # sizes workspaces (retry on capacity), checks err
@@ -326,9 +327,9 @@ def main():
     }
     clocks = clk.summary()
     line["clocks"] = clocks
-    # ---- end to end through the public API with host buffers (N = 1)
-    if not args.no_e2e and world == 1:
-        line["e2e"] = e2e(p, x, cfg, args)
+    # ---- end to end through the public API with host buffers (every rank its slab; max over ranks)
+    if not args.no_e2e:
+        line["e2e"] = e2e(p, x, cfg, args, world)
     # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1
     if not args.no_cpu_baseline and world == 1 and rank == 0:
         nz = sample_planes(cfg, 6e6)
@@ -343,18 +344,20 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e(p, x, cfg, args):
-    """Same metric through the public API with HOST buffers: every step copies the input from
-    pinned host memory, runs the path, and reads the result (count, code stream, kept mask) back."""
+def e2e(p, x, cfg, args, world=1):
+    """Same metric through the public API with HOST buffers: every step copies the input (this rank's
+    slab) from pinned host memory, runs the path, and reads the result (count, code stream, kept
+    mask) back.  N > 1: wall time max over ranks, bytes summed over ranks."""
     import torch
 
     from paper_2602_15917_b200 import _lib as L
 
+    P = getattr(p, "S", p)                       # the slab state of a sharded pipeline
     xh = x.cpu().pin_memory()
     xd = torch.empty_like(x)
     cnt_h = torch.empty(1, dtype=torch.int64).pin_memory()
-    out_h = torch.empty(p.codes.numel(), dtype=p.codes.dtype).pin_memory()
-    mask_h = torch.empty(p.nwords, dtype=torch.int32).pin_memory()
+    out_h = torch.empty(P.codes.numel(), dtype=P.codes.dtype).pin_memory()
+    mask_h = torch.empty(P.nwords, dtype=torch.int32).pin_memory()
     stream = torch.cuda.current_stream()
     steps = max(3, min(args.steps, 10))
     d2h = 0
@@ -364,22 +367,34 @@ def e2e(p, x, cfg, args):
         xd.copy_(xh, non_blocking=True)
         p.enqueue(xd)
         off = L.Scalars.count.offset
-        sc = p.sc[off:off + 8].view(torch.int64)      # roix_scalars.count
+        sc = P.sc[off:off + 8].view(torch.int64)      # roix_scalars.count (this slab's)
         cnt_h.copy_(sc, non_blocking=True)
         stream.synchronize()
         c = int(cnt_h[0])
-        out_h[:c].copy_(p.codes[:c], non_blocking=True)
-        mask_h.copy_(p.o[: p.nwords], non_blocking=True)
+        out_h[:c].copy_(P.codes[:c], non_blocking=True)
+        mask_h.copy_(P.o[: P.nwords], non_blocking=True)
         stream.synchronize()
-        d2h = c * p.codes.element_size() + p.nwords * 4 + 8
+        d2h = c * P.codes.element_size() + P.nwords * 4 + 8
 
     one()
     torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         one()
     dt = (time.perf_counter() - t0) / steps
-    return {"value": cfg.nbytes / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": cfg.nbytes, "d2h_bytes_per_step": d2h,
+    h2d = x.numel() * x.element_size()
+    if world > 1:
+        v = torch.tensor([dt, float(h2d), float(d2h)], dtype=torch.float64, device=x.device)
+        t = v[0:1].clone()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        b = v[1:3].clone()
+        dist.all_reduce(b)
+        dt, h2d, d2h = float(t.item()), int(b[0].item()), int(b[1].item())
+    return {"value": cfg.nbytes / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": dt * 1e3, "steps": steps}
 
 

@@ -66,8 +66,10 @@ class SlabState(Pipeline):
         return ctypes.c_void_p(self.counts.data_ptr() + 8 * i)
 
 
-def slab_program(S, x, stream=None):
-    """Generator: enqueue this slab's work; yield at every exchange (see module doc)."""
+def slab_program(S, x, stream=None, mark=None):
+    """Generator: enqueue this slab's work; yield at every exchange (see module doc).  mark(stage) is
+    called after each stage is enqueued (bench.py records CUDA events there)."""
+    mark = mark or (lambda stage: None)
     st = ctypes.c_void_p((stream or torch.cuda.current_stream(S.device)).cuda_stream)
     sc, xp, n = _ptr(S.sc), _ptr(x), S.n
     G, g = S.world, S.rank
@@ -75,8 +77,10 @@ def slab_program(S, x, stream=None):
     if S.cdtype == L.F32:
         L.roix_range(xp, n, sc, st)
         yield ("minmax", S.sc)                                    # X2
+        mark("range")
     L.roix_resolve(sc, S.cdtype, S.rel_eb, st)
     S.hist.zero_()
+    mark("setup")
     mws, mwsb = _ptr(S.morph_ws), S.morph_ws.numel()
     if S.fused:
         L.roix_histogram_binarize(xp, S.cdtype, ctypes.byref(S.geom), S.polarity, sc, _ptr(S.hist), S.nbins, mws,
@@ -84,7 +88,9 @@ def slab_program(S, x, stream=None):
     else:
         L.roix_histogram(xp, S.cdtype, n, sc, _ptr(S.hist), S.nbins, st)
     yield ("sum", S.hist)                                         # X1
+    mark("histogram")
     L.roix_threshold(_ptr(S.hist), S.nbins, S.cdtype, S.polarity, sc, st)
+    mark("threshold")
     halo_lo = halo_hi = None
     if S.se == 6 and G > 1:
         if S.nz < 2:
@@ -100,6 +106,7 @@ def slab_program(S, x, stream=None):
         assert pw > 0
     morph = L.roix_morph_prebinarized if S.fused else L.roix_morph
     morph(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o), _ptr(S.row_runs), mws, mwsb, st)
+    mark("morph")
     out = L.LabelOut(S.o.data_ptr(), S.comp_min.data_ptr(), S.comp_size.data_ptr(), S.comp_kept.data_ptr(),
                      S.comp_cap, S.labels.data_ptr() if S.labels is not None else None)
     geo = ctypes.byref(S.geom)
@@ -123,9 +130,15 @@ def slab_program(S, x, stream=None):
     else:
         L.roix_label(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, S.min_size, S.run_capacity, _ptr(S.label_ws),
                      S.ws_bytes, ctypes.byref(out), sc, st)
-    L.roix_extract_runs(xp, S.cdtype, geo, S.run_capacity, _ptr(S.label_ws), S.ws_bytes, sc, _ptr(S.codes),
-                        S.code_capacity, None, st)
+    mark("label")
+    if S.extract == "runs":
+        L.roix_extract_runs(xp, S.cdtype, geo, S.run_capacity, _ptr(S.label_ws), S.ws_bytes, sc, _ptr(S.codes),
+                            S.code_capacity, None, st)
+    else:
+        L.roix_extract(xp, S.cdtype, n, _ptr(S.o), sc, _ptr(S.codes), S.code_capacity, None, _ptr(S.ex_ws),
+                       S.ex_ws.numel(), st)
     counts = yield ("counts", S)                                  # X5
+    mark("extract")
     S.offset = int(sum(counts[:g]))
     S.global_count = int(sum(counts))
 
@@ -213,8 +226,8 @@ class DistComm:
         self.dist, self.group = dist, group
         self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
 
-    def run(self, S, x):
-        gen = slab_program(S, x)
+    def run(self, S, x, mark=None):
+        gen = slab_program(S, x, mark=mark)
         rep = None
         try:
             msg = next(gen)
@@ -284,7 +297,7 @@ class ShardedPipeline:
         self.S = SlabState(shape, dtype, z0=z0, nz=nz, rank=self.comm.rank, world=self.comm.world, device=device, **kw)
 
     def enqueue(self, x, mark=None):
-        self.comm.run(self.S, x)
+        self.comm.run(self.S, x, mark=mark)
 
     def run(self, x):
         self.enqueue(x)
