@@ -40,7 +40,9 @@ def parse():
     ap.add_argument("--impl", default="roix", choices=["roix", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--graph", action="store_true", help="replay each timed step as a CUDA graph")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="enqueue every timed step from the host (default at N = 1: each step is a CUDA graph "
+                         "replay; N > 1 always enqueues, the exchanges synchronise with the host)")
     ap.add_argument("--extract", default="mask", choices=["mask", "runs"], help="a8 form (see Pipeline)")
     return ap.parse_args()
 
@@ -185,6 +187,7 @@ def reference_arm(args, cfg):
 # ------------------------------------------------------------------------------------ GPU arm
 def main():
     args = parse()
+    args.graph = not args.no_graph and int(os.environ.get("WORLD_SIZE", "1")) == 1
     import synth
 
     cfg = synth.CONFIGS[args.config] if args.scale == 1.0 else synth.scaled(args.config, args.scale)
