@@ -114,7 +114,7 @@ def alg_bytes(cfg, n, count):
 # the C-ABI call each timed stage is (its kernels: profiles/*/launches_*.txt)
 STAGE_CALLS = {"range": "roix_range (k_range)", "histogram": "roix_histogram (k_hist_*)",
                "morph": "roix_morph (k_binarize + k_open3d_rows/k_open2d)",
-               "label": "roix_label (runs, union-find, filter: 9 kernels)",
+               "label": "roix_label (runs, union-find, filter: 7 kernels)",
                "extract": "roix_extract (k_extract_count + scan + k_extract)"}
 
 

@@ -120,15 +120,6 @@ __global__ void k_count_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nw
     }
 }
 
-// after the scan: total runs -> ctr[0], sc->n_runs; capacity check
-__global__ void k_runs_total(const uint64_t *total, uint64_t cap, LabelWS W, roix_scalars *sc) {
-    uint64_t t = *total;
-    W.ctr[0] = t > cap ? 0 : t;  // over capacity: every later step sees no runs
-    W.ctr[1] = 0;  // cross-block pairs
-    W.ctr[2] = 0;
-    sc->n_runs = t;
-    if (t > cap) set_err(sc, ROIX_ERR_CAPACITY);
-}
 
 // Warp per group of RIF consecutive rows: the offsets and (for rows of <= 128 words) all words of
 // the RIF rows are loaded before any of them is processed, so each warp keeps RIF rows of loads in
@@ -168,9 +159,25 @@ __device__ __forceinline__ void runs_of_chunk(uint32_t cw, uint32_t next_lane31,
     ebase += tot >> 16;
 }
 
+// after the row scan: total runs -> ctr[0], sc->n_runs, capacity check (block 0); over capacity no
+// run is written and every later step sees none
+__device__ __forceinline__ bool runs_total(const uint64_t *total, uint64_t cap, const LabelWS &W, roix_scalars *sc) {
+    const uint64_t t = *total;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        W.ctr[0] = t > cap ? 0 : t;
+        W.ctr[1] = 0;   // cross-block pairs
+        W.ctr[2] = 0;
+        sc->n_runs = t;
+        if (t > cap) set_err(sc, ROIX_ERR_CAPACITY);
+    }
+    return t <= cap;
+}
+
 __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nwords,
-                                                      LabelWS W, roix_scalars *sc) {
+                                                      LabelWS W, const uint64_t *total, uint64_t cap,
+                                                      roix_scalars *sc) {
     if (get_err(sc)) return;
+    if (!runs_total(total, cap, W, sc)) return;
     const uint64_t rows = G.nz * G.ny;
     const uint64_t ngroups = (rows + RIF - 1) / RIF;
     const uint64_t wpg = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -228,8 +235,9 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
 // lane's first start / end slot.
 template <int L, int KW, int RR>
 __global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__restrict__ o, LGeo G, LabelWS W,
-                                                           roix_scalars *sc) {
+                                                           const uint64_t *total, uint64_t cap, roix_scalars *sc) {
     if (get_err(sc)) return;
+    if (!runs_total(total, cap, W, sc)) return;
     constexpr int S = 32 / L;
     const uint32_t lane = lane_id(), sl = lane & (L - 1), seg = lane / L;
     const uint64_t rows = G.nz * G.ny;
@@ -558,44 +566,42 @@ __global__ void k_root_flags(LGeo G, LabelWS W, MapView M, uint64_t min_size, ro
     if (lane_id() == 0 && nk) atomicAdd((unsigned long long *)&W.ctr[2], (unsigned long long)nk);
 }
 
-__global__ void k_table(LGeo G, LabelWS W, MapView M, const uint32_t *cscan, roix_label_out out, roix_scalars *sc) {
+// a7 outputs, one pass over the runs: the component table (entries owned by roots whose final label
+// is their own first voxel, at their scanned index: increasing min index), and K = o with the bits of
+// every run of a dropped component cleared (in place when K aliases o)
+__global__ void k_table_clear(LGeo G, LabelWS W, MapView M, const uint32_t *cscan, const uint64_t *nroots,
+                              roix_label_out out, roix_scalars *sc) {
     if (get_err(sc)) return;
-    const uint64_t n = W.ctr[0];
-    if (!out.comp_min) return;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (W.parent[i] != (uint32_t)i) continue;
-        uint64_t fin, tot;
-        resolve_root(G, W, M, (uint32_t)i, fin, tot);
-        if (fin != gidx(G, W, (uint32_t)i)) continue;
-        const uint64_t c = cscan[i];
-        if (c < out.comp_cap) {
-            out.comp_min[c] = fin;
-            out.comp_size[c] = tot;
-            if (out.comp_kept) out.comp_kept[c] = W.kept[i];
-        }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->n_components = *nroots;
+        sc->n_kept = W.ctr[2];
+        if (out.comp_min && *nroots > out.comp_cap) set_err(sc, ROIX_ERR_CAPACITY);
     }
-}
-
-__global__ void k_table_total(const uint64_t *nroots, LabelWS W, roix_label_out out, roix_scalars *sc) {
-    if (get_err(sc)) return;
-    sc->n_components = *nroots;
-    sc->n_kept = W.ctr[2];
-    if (out.comp_min && *nroots > out.comp_cap) set_err(sc, ROIX_ERR_CAPACITY);
-}
-
-// K: clear the bits of every run whose component was dropped
-__global__ void k_clear_dropped(LGeo G, LabelWS W, uint32_t *K, roix_scalars *sc) {
-    if (get_err(sc)) return;
     const uint64_t n = W.ctr[0];
+    uint32_t *K = out.keep_bits;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (W.kept[W.parent[i]]) continue;
-        uint64_t b = (uint64_t)W.rrow[i] * G.nx + W.x0[i], e = (uint64_t)W.rrow[i] * G.nx + W.x1[i];
-        while (b < e) {
-            uint64_t wi = b >> 5;
-            uint32_t s = (uint32_t)(b & 31);
-            uint32_t take = (uint32_t)min((uint64_t)(32 - s), e - b);
-            atomicAnd(&K[wi], ~(low_mask(take) << s));
-            b += take;
+        const uint32_t p = W.parent[i];
+        if (out.comp_min && p == (uint32_t)i) {
+            uint64_t fin, tot;
+            resolve_root(G, W, M, (uint32_t)i, fin, tot);
+            if (fin == gidx(G, W, (uint32_t)i)) {
+                const uint64_t c = cscan[i];
+                if (c < out.comp_cap) {
+                    out.comp_min[c] = fin;
+                    out.comp_size[c] = tot;
+                    if (out.comp_kept) out.comp_kept[c] = W.kept[i];
+                }
+            }
+        }
+        if (K && !W.kept[p]) {
+            uint64_t b = (uint64_t)W.rrow[i] * G.nx + W.x0[i], e = (uint64_t)W.rrow[i] * G.nx + W.x1[i];
+            while (b < e) {
+                const uint64_t wi = b >> 5;
+                const uint32_t sh = (uint32_t)(b & 31);
+                const uint32_t take = (uint32_t)min((uint64_t)(32 - sh), e - b);
+                atomicAnd(&K[wi], ~(low_mask(take) << sh));
+                b += take;
+            }
         }
     }
 }
@@ -749,13 +755,14 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
         rr = W.row_runs;
     }
     if ((e = scan_u32(rr, W.row_start, rows, W.scan_tmp, st)) != cudaSuccess) return e;
-    k_runs_total<<<1, 1, 0, st>>>(scan_total_ptr(W.scan_tmp, rows), cap, W, sc);
+    const uint64_t *rtot = scan_total_ptr(W.scan_tmp, rows);
     const int runs_grid = num_sms() * 8;
     const uint32_t Wd = G.W;
     if (g.nx % 32 == 0 && ((Wd <= 32 && (Wd & (Wd - 1)) == 0) || Wd == 64 || Wd == 128)) {
         const uint32_t L = Wd < 32 ? Wd : 32;
         const int grid = ctas(rows * L / 4, 256);   // ~4 rows per warp iteration
-#define ROIX_RUNS_ROWS(LL, KK, RR) k_extract_runs_rows<LL, KK, RR><<<grid, 256, 0, st>>>(o_bits, G, W, sc)
+#define ROIX_RUNS_ROWS(LL, KK, RR) \
+    k_extract_runs_rows<LL, KK, RR><<<grid, 256, 0, st>>>(o_bits, G, W, rtot, cap, sc)
         switch (Wd) {
         case 1: ROIX_RUNS_ROWS(1, 1, 4); break;
         case 2: ROIX_RUNS_ROWS(2, 1, 4); break;
@@ -768,7 +775,7 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
         }
 #undef ROIX_RUNS_ROWS
     } else {
-        k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, sc);
+        k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, rtot, cap, sc);
     }
     static bool attr = false;
     if (!attr) {
@@ -798,14 +805,10 @@ cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint
     cudaError_t e;
     k_root_flags<<<runs_grid, 256, 0, st>>>(G, W, M, min_size, sc);
     if ((e = scan_u32_dev(W.cidx, W.cidx, W.ctr, cap, W.scan_tmp, st)) != cudaSuccess) return e;
-    k_table<<<runs_grid, 256, 0, st>>>(G, W, M, W.cidx, out, sc);
-    k_table_total<<<1, 1, 0, st>>>(scan_total_ptr(W.scan_tmp, cap), W, out, sc);
-    if (out.keep_bits) {
-        if (out.keep_bits != o_bits &&
-            (e = cudaMemcpyAsync(out.keep_bits, o_bits, nwords * 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
-            return e;
-        k_clear_dropped<<<runs_grid, 256, 0, st>>>(G, W, out.keep_bits, sc);
-    }
+    if (out.keep_bits && out.keep_bits != o_bits &&
+        (e = cudaMemcpyAsync(out.keep_bits, o_bits, nwords * 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return e;
+    k_table_clear<<<runs_grid, 256, 0, st>>>(G, W, M, W.cidx, scan_total_ptr(W.scan_tmp, cap), out, sc);
     if (out.labels) {
         if ((e = cudaMemsetAsync(out.labels, 0xff, n * 8, st)) != cudaSuccess) return e;
         k_labels<<<runs_grid, 256, 0, st>>>(G, W, M, out.labels, sc);
