@@ -68,6 +68,7 @@ def _load():
         "oracle_filter": (None, [vp, u64, vp, u64, u64, vp, vp]),
         "oracle_extract_u16": (i64, [vp, vp, u64, f32, vp]),
         "oracle_extract_f32": (i64, [vp, vp, u64, f32, vp]),
+        "oracle_row_spans": (i64, [vp, vp, i32, i64, i64, i64, f32, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -222,6 +223,28 @@ def extract(x, K, eb):
     if n < 0:
         raise OracleError("extract failed")
     return out[:n]
+
+
+def row_spans(x, K, eb):
+    """NEXT-1: the geometry records (i, x_start, x_end exclusive) of every
+    row i = z*Y + y of K with a set bit, in increasing i, and the pixel sections -- the codes of
+    x[i][x_start:x_end], interior gaps included -- concatenated.  Returns (spans (m, 3) int64,
+    codes)."""
+    x = np.ascontiguousarray(x)
+    K = _c(K, np.uint8)
+    assert x.ndim == 3 and K.shape == x.shape
+    Z, Y, X = x.shape
+    is_f32 = x.dtype == np.float32
+    if not is_f32:
+        x = _c(x, np.uint16)
+    spans = np.empty((Z * Y + 1, 3), np.int64)
+    codes = np.empty(x.size + 1, np.int32 if is_f32 else np.uint16)
+    nc = ctypes.c_int64()
+    m = _load().oracle_row_spans(_p(K), _p(x), int(is_f32), Z, Y, X, float(eb), _p(spans), _p(codes),
+                                 ctypes.byref(nc))
+    if m < 0:
+        raise OracleError("row_spans failed")
+    return spans[:m].copy(), codes[: nc.value].copy()
 
 
 def pack_bits(mask):

@@ -326,3 +326,46 @@ int64_t oracle_extract_f32(const float *x, const uint8_t *K, uint64_t n, float e
     }
     return j;
 }
+
+/* ------------------------------------------------------------------ NEXT-1: row spans
+ * The paper's ROI representation: for every row i = z*Y + y of K holding a set bit, the
+ * geometry record G(i) = [i, x_start, x_end] with x_start the leftmost and x_end the rightmost set
+ * column + 1 (exclusive: n_i = x_end - x_start, S DESIGN DECISIONS), and the pixel section
+ * P(i) = [p_0 .. p_{n_i - 1}], p_j the value at column x_start + j -- interior gaps included --
+ * here quantised with the a1 quantiser.  spans: 3 int64 per record, in increasing i; returns the
+ * number of records and writes the total section length to *ncodes; -1 on a quantiser range error.
+ */
+int64_t oracle_row_spans(const uint8_t *K, const void *x, int is_f32, int64_t Z, int64_t Y, int64_t X, float eb,
+                         int64_t *spans, void *codes, int64_t *ncodes)
+{
+    double s, c;
+    int64_t m = 0, nc = 0;
+    if (step_of(eb, &s)) return -1;
+    for (int64_t i = 0; i < Z * Y; i++) {
+        const uint8_t *row = K + i * X;
+        int64_t x0 = -1, x1 = -1;
+        for (int64_t xx = 0; xx < X; xx++)
+            if (row[xx]) {
+                if (x0 < 0) x0 = xx;
+                x1 = xx + 1;
+            }
+        if (x0 < 0) continue;
+        spans[3 * m] = i;
+        spans[3 * m + 1] = x0;
+        spans[3 * m + 2] = x1;
+        m++;
+        for (int64_t xx = x0; xx < x1; xx++) {
+            if (is_f32) {
+                const float v = ((const float *)x)[i * X + xx];
+                if (!isfinite(v) || rne_exact((double)v, s, &c)) return -1;
+                ((int32_t *)codes)[nc++] = (int32_t)c;
+            } else {
+                const uint16_t v = ((const uint16_t *)x)[i * X + xx];
+                if (rne_exact((double)v, s, &c) || c > 65535.0) return -1;
+                ((uint16_t *)codes)[nc++] = (uint16_t)c;
+            }
+        }
+    }
+    *ncodes = nc;
+    return m;
+}
