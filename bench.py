@@ -44,6 +44,7 @@ def parse():
                     help="enqueue every timed step from the host (default at N = 1: each step is a CUDA graph "
                          "replay; N > 1 always enqueues, the exchanges synchronise with the host)")
     ap.add_argument("--extract", default="mask", choices=["mask", "runs"], help="a8 form (see Pipeline)")
+    ap.add_argument("--spans", action="store_true", help="also produce the NEXT-1 row spans (roix_row_spans)")
     return ap.parse_args()
 
 
@@ -221,7 +222,7 @@ def main():
         p = ShardedPipeline(cfg.shape, cfg.dtype, z0=z0, nz=z1 - z0, group=dist.group.WORLD, device=dev,
                             extract=args.extract, **kw)
     else:
-        p = Pipeline(cfg.shape, cfg.dtype, device=dev, extract=args.extract, **kw)
+        p = Pipeline(cfg.shape, cfg.dtype, device=dev, extract=args.extract, spans=args.spans, **kw)
     res = p.run(x)                          # sizes workspaces (retry on capacity), checks err
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):

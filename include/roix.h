@@ -291,6 +291,28 @@ roix_status roix_extract_runs(const void *x, roix_dtype dtype, const roix_geom *
                               size_t ws_bytes, roix_scalars *sc, void *codes_out, uint64_t capacity,
                               const uint64_t *offset, roix_stream_t stream);
 
+/*
+ * NEXT-1 ROW SPANS: the paper's ROI representation.  For every row
+ * i = z*Y + y (global: z counts from the volume's first plane) of keep_bits holding a set bit, in
+ * increasing i: the geometry record spans[k] = {i, x_start, x_end} -- x_start the leftmost set column,
+ * x_end the rightmost + 1 (exclusive, n_i = x_end - x_start) -- and the pixel section: the codes
+ * RNE(x / s) of x[i][x_start .. x_end), interior gaps included, concatenated in codes (uint16 for
+ * u16 input, int32 for fp32).  counts (device, 2 uint64): number of records, total section length.
+ * Requires roix_resolve (the step s).  More than span_cap records or code_cap codes sets
+ * ROIX_ERR_CAPACITY (nothing is written past either capacity).  ws/ws_bytes from
+ * roix_row_spans_workspace.  keep_bits / x: the slab g, as roix_label / roix_extract.
+ */
+typedef struct roix_span {
+    uint64_t row;     /* i = z*Y + y                              */
+    uint32_t x_start; /* leftmost set column                      */
+    uint32_t x_end;   /* rightmost set column + 1 (exclusive)     */
+} roix_span;
+
+roix_status roix_row_spans_workspace(const roix_geom *g, size_t *ws_bytes);
+roix_status roix_row_spans(const uint32_t *keep_bits, const void *x, roix_dtype dtype, const roix_geom *g,
+                           roix_scalars *sc, roix_span *spans, uint64_t span_cap, void *codes, uint64_t code_cap,
+                           uint64_t *counts, void *ws, size_t ws_bytes, roix_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

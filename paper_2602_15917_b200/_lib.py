@@ -81,6 +81,9 @@ _SIGS = {
                                  ctypes.POINTER(LabelOut), _vp, _vp]),
     "roix_extract_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_extract": (_i32, [_vp, _i32, _u64, _vp, _vp, _vp, _u64, _vp, _vp, ctypes.c_size_t, _vp]),
+    "roix_row_spans_workspace": (_i32, [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_row_spans": (_i32, [_vp, _vp, _i32, ctypes.POINTER(Geom), _vp, _vp, _u64, _vp, _u64, _vp, _vp,
+                              ctypes.c_size_t, _vp]),
     "roix_extract_runs": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _u64, _vp,
                                  _vp]),
 }
@@ -129,6 +132,7 @@ roix_morph_prebinarized = _wrap("roix_morph_prebinarized")
 roix_label = _wrap("roix_label")
 roix_extract = _wrap("roix_extract")
 roix_extract_runs = _wrap("roix_extract_runs")
+roix_row_spans = _wrap("roix_row_spans")
 roix_label_local = _wrap("roix_label_local")
 roix_label_boundary = _wrap("roix_label_boundary")
 roix_label_link = _wrap("roix_label_link")
@@ -176,6 +180,12 @@ def roix_morph_workspace(geom):
 def roix_extract_workspace(n):
     out = ctypes.c_size_t()
     _check(load().roix_extract_workspace(n, ctypes.byref(out)), "roix_extract_workspace")
+    return out.value
+
+
+def roix_row_spans_workspace(geom):
+    out = ctypes.c_size_t()
+    _check(load().roix_row_spans_workspace(ctypes.byref(geom), ctypes.byref(out)), "roix_row_spans_workspace")
     return out.value
 
 

@@ -377,4 +377,29 @@ roix_status roix_extract_runs(const void *x, roix_dtype dtype, const roix_geom *
                 "roix_extract_runs");
 }
 
+roix_status roix_row_spans_workspace(const roix_geom *g, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (g->nz * g->ny >= 0xffffffffull) return unsupported("more than 2^32-1 rows per slab");
+    if (g->nx >= 0xffffffffull) return unsupported("rows longer than 2^32-1 voxels");
+    *ws_bytes = row_spans_workspace_bytes(*g);
+    return ROIX_OK;
+}
+
+roix_status roix_row_spans(const uint32_t *keep_bits, const void *x, roix_dtype dtype, const roix_geom *g,
+                           roix_scalars *sc, roix_span *spans, uint64_t span_cap, void *codes, uint64_t code_cap,
+                           uint64_t *counts, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    if (!sc || !keep_bits || !counts || !ws) return invalid("sc / keep_bits / counts / ws is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    size_t need = 0;
+    roix_status s = roix_row_spans_workspace(g, &need);
+    if (s != ROIX_OK) return s;
+    if (ws_bytes < need) return invalid("workspace too small (see roix_row_spans_workspace)");
+    if (!x || !aligned16(x)) return invalid("x must be 16-byte aligned");
+    if ((span_cap && !spans) || (code_cap && !codes)) return invalid("spans / codes is NULL");
+    return cuda(launch_row_spans(keep_bits, x, (int)dtype, *g, sc, spans, span_cap, codes, code_cap, counts, ws,
+                                 (cudaStream_t)stream),
+                "roix_row_spans");
+}
+
 }  // extern "C"

@@ -68,3 +68,8 @@ cudaError_t launch_gather(const void *x, int dtype, uint64_t nx, const RunsView 
                           uint64_t capacity, const uint64_t *offset, cudaStream_t st);
 cudaError_t launch_extract_runs(const void *x, int dtype, const roix_geom &g, uint64_t cap, void *ws, roix_scalars *sc,
                                 void *codes, uint64_t capacity, const uint64_t *offset, cudaStream_t st);
+
+size_t row_spans_workspace_bytes(const roix_geom &g);
+cudaError_t launch_row_spans(const uint32_t *K, const void *x, int dtype, const roix_geom &g, roix_scalars *sc,
+                             roix_span *spans, uint64_t span_cap, void *codes, uint64_t code_cap, uint64_t *counts,
+                             void *ws, cudaStream_t st);

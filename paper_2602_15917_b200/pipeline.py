@@ -45,7 +45,8 @@ class Pipeline:
     """Preallocated buffers + the enqueue sequence for volumes of one shape / dtype / parameter set."""
 
     def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
-                 run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="mask"):
+                 run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="mask",
+                 spans=False):
         L.load()
         self.shape = tuple(int(v) for v in shape)
         Z, Y, X = self.shape
@@ -85,6 +86,13 @@ class Pipeline:
         cdt = torch.int16 if dtype == "u16" else torch.int32
         self.codes = torch.empty(max(self.code_capacity, 8), dtype=cdt, device=dev)
         self.ex_ws = torch.empty(L.roix_extract_workspace(self.n), dtype=torch.uint8, device=dev)
+        # NEXT-1 (optional): the paper's row-span representation of K (roix_row_spans)
+        self.spans_on = bool(spans)
+        if self.spans_on:
+            self.span_ws = torch.empty(L.roix_row_spans_workspace(self.geom), dtype=torch.uint8, device=dev)
+            self.span_rec = torch.empty(2 * Z * Y + 2, dtype=torch.int64, device=dev)   # roix_span: 16 bytes
+            self.span_codes = torch.empty(max(self.n, 8), dtype=cdt, device=dev)
+            self.span_counts = torch.zeros(2, dtype=torch.int64, device=dev)
         self.labels = torch.empty(self.n, dtype=torch.int64, device=dev) if labels else None
 
     def _alloc_label(self, cap):
@@ -140,10 +148,24 @@ class Pipeline:
             L.roix_extract(xp, self.cdtype, n, _ptr(self.o), sc, _ptr(self.codes), self.code_capacity, None,
                            _ptr(self.ex_ws), self.ex_ws.numel(), st)
         mark("extract")
+        if self.spans_on:
+            Z, Y, X = self.shape
+            L.roix_row_spans(_ptr(self.o), xp, self.cdtype, ctypes.byref(self.geom), sc, _ptr(self.span_rec), Z * Y,
+                             _ptr(self.span_codes), self.span_codes.numel(), _ptr(self.span_counts),
+                             _ptr(self.span_ws), self.span_ws.numel(), st)
+            mark("spans")
+
+    def row_spans(self):
+        """(records (m, 3) int64: row, x_start, x_end; section codes) of the last run (spans=True)."""
+        ns, nc = (int(v) for v in self.span_counts.cpu())
+        sp = self.span_rec[: 2 * ns].view(-1, 2).cpu()
+        rec = torch.stack([sp[:, 0], sp[:, 1] & 0xffffffff, sp[:, 1] >> 32], dim=1)
+        return rec, self.span_codes[:nc]
 
     def launches(self):
-        k = sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
-                                      "extract" if self.extract == "mask" else "extract_runs"))
+        k = 4 if self.spans_on else 0   # roix_row_spans: extent, 2 scans, write
+        k += sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
+                                       "extract" if self.extract == "mask" else "extract_runs"))
         return k + (LAUNCHES["range"] if self.cdtype == L.F32 else 0)
 
     def scalars(self):

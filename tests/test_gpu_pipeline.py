@@ -154,3 +154,21 @@ def test_fused_speculation_miss_falls_back():
         assert torch.equal(ra.keep_bits, rb.keep_bits) and torch.equal(ra.codes, rb.codes)
         ref = oracle.pipeline(v, eb=2.0, conn=6, se=6, min_size=4, polarity=pol)
         assert ra.count == ref["count"]
+
+
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C1"], synth.scaled("C4", 0.0625), synth.scaled("C2", 0.25)],
+                         ids=lambda c: c.name)
+def test_pipeline_row_spans_vs_oracle(cfg):
+    """NEXT-1 inside the pipeline: the row spans of K (the paper's geometry + pixel sections)."""
+    x = synth.generate(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se,
+                 min_size=cfg.min_size, polarity=cfg.polarity, spans=True)
+    res = p.run(x)
+    K = words_to_mask(res.keep_bits, p.n).reshape(cfg.shape)
+    rs, rc = oracle.row_spans(synth.to_numpy(x, cfg), K, res.eb)
+    rec, codes = p.row_spans()
+    np.testing.assert_array_equal(rec.numpy(), rs)
+    got = codes.cpu().numpy()
+    np.testing.assert_array_equal(got.view(np.uint16) if cfg.dtype == "u16" else got, rc)
+    # the spans cover K: at least as many codes as the kept voxels
+    assert rc.size >= res.count

@@ -412,3 +412,70 @@ def test_extract_runs_vs_oracle(shape, dt):
                 np.testing.assert_array_equal(got[off:off + ref.size], ref)
             raw = buf.cpu().numpy()
             assert np.all(raw[:off] == -1) and np.all(raw[min(capacity, off + ref.size):] == -1)
+
+
+# ------------------------------------------------------------------- NEXT-1 row spans
+def _spans_gpu(x_np, K, eb, z0=0, gz=None, span_cap=None, code_cap=None):
+    Z, Y, X = x_np.shape
+    g = L.Geom(Z, Y, X, z0, gz if gz is not None else Z)
+    wsb = L.roix_row_spans_workspace(g)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    rows = Z * Y
+    scap = rows if span_cap is None else span_cap
+    ccap = x_np.size if code_cap is None else code_cap
+    spans = torch.full((max(scap, 1) * 2 + 2,), -1, dtype=torch.int64, device="cuda")   # 16-byte records
+    codes = torch.full((max(ccap, 1) + 8,), -1, dtype=torch.int16 if x_np.dtype == np.uint16 else torch.int32,
+                       device="cuda")
+    counts = torch.zeros(2, dtype=torch.int64, device="cuda")
+    sc = new_sc(eb)
+    L.roix_resolve(ptr(sc), dtype_code(x_np), 0.0, st())
+    kw = mask_to_words(K)
+    x = dev(x_np)
+    L.roix_row_spans(ptr(kw), ptr(x), dtype_code(x_np), ctypes.byref(g), ptr(sc), ptr(spans), scap, ptr(codes), ccap,
+                     ptr(counts), ptr(ws), wsb, st())
+    s = read_sc(sc)
+    ns, nc = (int(v) for v in counts.cpu().numpy())
+    sp = spans.cpu().numpy()
+    rec = np.stack([sp[0:2 * ns:2], sp[1:2 * ns:2] & 0xffffffff, sp[1:2 * ns:2] >> 32], axis=1) if ns else \
+        np.zeros((0, 3), np.int64)
+    cd = codes.cpu().numpy()
+    return s, rec, (cd.view(np.uint16) if x_np.dtype == np.uint16 else cd), ns, nc, sp
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (2, 3, 5), (3, 7, 33), (4, 9, 64), (2, 5, 1000), (3, 40, 512),
+                                   (2, 3, 2100)])
+@pytest.mark.parametrize("dt", ["u16", "f32"])
+def test_row_spans_vs_oracle(shape, dt):
+    rng = np.random.default_rng(abs(hash((shape, dt, "spans"))) % 2 ** 32)
+    for K in (_blobby(rng, shape, 0.3, 29), (rng.random(shape) < 0.05).astype(np.uint8), np.zeros(shape, np.uint8),
+              np.ones(shape, np.uint8)):
+        if dt == "u16":
+            x_np, eb = rng.integers(0, 65536, shape).astype(np.uint16), 2.0
+        else:
+            x_np, eb = rng.normal(0, 3, shape).astype(np.float32), 0.01
+        rs, rc = oracle.row_spans(x_np, K, eb)
+        s, rec, cd, ns, nc, _ = _spans_gpu(x_np, K, eb)
+        assert s.err == 0
+        assert ns == len(rs) and nc == rc.size
+        np.testing.assert_array_equal(rec, rs)
+        np.testing.assert_array_equal(cd[:nc], rc)
+
+
+def test_row_spans_global_rows_and_capacity():
+    rng = np.random.default_rng(11)
+    shape = (3, 6, 40)
+    K = (rng.random(shape) < 0.3).astype(np.uint8)
+    x_np = rng.integers(0, 4096, shape).astype(np.uint16)
+    rs, rc = oracle.row_spans(x_np, K, 1.0)
+    # a slab starting at global plane 5: row indices are global (z0 * Y + local row)
+    s, rec, cd, ns, nc, _ = _spans_gpu(x_np, K, 1.0, z0=5, gz=12)
+    assert s.err == 0
+    np.testing.assert_array_equal(rec[:, 0], rs[:, 0] + 5 * shape[1])
+    np.testing.assert_array_equal(cd[:nc], rc)
+    # capacities: error bit, nothing written past either capacity
+    s, rec, cd, ns, nc, sp = _spans_gpu(x_np, K, 1.0, span_cap=3, code_cap=10)
+    assert s.err & L.ERR_CAPACITY and ns == len(rs) and nc == rc.size
+    np.testing.assert_array_equal(sp[0:6:2], rs[:3, 0])
+    assert np.all(sp[6:] == -1)
+    np.testing.assert_array_equal(cd[:10], rc[:10])
+    assert np.all(cd.view(np.int16)[10:] == -1)
