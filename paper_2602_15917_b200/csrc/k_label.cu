@@ -33,7 +33,6 @@ struct LabelWS {
     uint64_t pair_cap;
     uint32_t *klen;       // [cap]: kept length of every run (roix_extract_runs)
     uint64_t *koff;       // [cap + 1]: their exclusive prefix
-    uint32_t *cfirst;     // [gather_chunks_max(n) + 1]: first run of every output chunk
 };
 
 constexpr int UB_RUNS = 4096;     // runs per union block (their parents live in shared memory)
@@ -56,7 +55,7 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
     size_t o_sz = take(cap * 8), o_kp = take(cap), o_ct = take(4 * 8);
     const uint64_t pair_cap = 2 * cap + 1024;
     size_t o_pr = take(pair_cap * 8);
-    size_t o_kl = take(cap * 4), o_ko = take((cap + 1) * 8), o_cf = take((gather_chunks_max(rows * g.nx) + 1) * 4);
+    size_t o_kl = take(cap * 4), o_ko = take((cap + 1) * 8);
     if (ws) {
         char *b = (char *)base;
         ws->row_runs = (uint32_t *)(b + o_rr);
@@ -74,7 +73,6 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
         ws->pair_cap = pair_cap;
         ws->klen = (uint32_t *)(b + o_kl);
         ws->koff = (uint64_t *)(b + o_ko);
-        ws->cfirst = (uint32_t *)(b + o_cf);
     }
     return off;
 }
@@ -835,7 +833,8 @@ cudaError_t launch_extract_runs(const void *x, int dtype, const roix_geom &g, ui
     R.rrow = W.rrow;
     R.parent = W.parent;
     R.kept = W.kept;
-    return launch_gather(x, dtype, g.nx, R, cap, W.klen, W.koff, W.cfirst, W.scan_tmp, sc, codes, capacity, offset, st);
+    R.err_snap = reinterpret_cast<uint32_t *>(W.ctr + 3);
+    return launch_gather(x, dtype, g.nx, R, cap, W.klen, W.koff, W.scan_tmp, sc, codes, capacity, offset, st);
 }
 
 cudaError_t launch_label_boundary(const void *ws, const roix_geom &g, uint64_t cap, int side, roix_brun *out,

@@ -6,11 +6,12 @@
 //   k_row_extent  one warp per row: the first and last set bit from a min / max reduction over the
 //                 row's words (ffs / clz); len[i] = x_end - x_start (0 for an empty row)
 //   scans         span index = prefix count of non-empty rows, code offset = prefix of len (uint64)
-//   k_span_write  one warp per non-empty row: its record, then its section with coalesced loads of
-//                 x and coalesced stores of the codes
+//   k_span_write  one warp per non-empty row: its record, then its section (warp_segment: 16-byte
+//                 loads of x, codes quantised in registers, 16-byte stores)
 #include "common.cuh"
 #include "kernels.cuh"
 #include "scan.cuh"
+#include "segment.cuh"
 
 namespace roix {
 
@@ -18,6 +19,7 @@ struct SpanWS {
     uint32_t *start, *len, *nonempty, *sidx;   // [rows], [rows], [rows], [rows + 1]
     uint64_t *coff;                            // [rows + 1]
     uint64_t *tmp_a, *tmp_b;                   // scan workspaces
+    uint32_t *err_snap;                        // error bits before k_span_write
 };
 
 static size_t span_carve(void *base, uint64_t rows, SpanWS *w) {
@@ -29,6 +31,7 @@ static size_t span_carve(void *base, uint64_t rows, SpanWS *w) {
     };
     const size_t o_st = take(rows * 4), o_ln = take(rows * 4), o_ne = take(rows * 4), o_si = take((rows + 1) * 4);
     const size_t o_co = take((rows + 1) * 8), o_ta = take(scan_tmp_elems(rows) * 8), o_tb = take(scan_tmp_elems(rows) * 8);
+    const size_t o_es = take(4);
     if (w) {
         char *b = (char *)base;
         w->start = (uint32_t *)(b + o_st);
@@ -38,6 +41,7 @@ static size_t span_carve(void *base, uint64_t rows, SpanWS *w) {
         w->coff = (uint64_t *)(b + o_co);
         w->tmp_a = (uint64_t *)(b + o_ta);
         w->tmp_b = (uint64_t *)(b + o_tb);
+        w->err_snap = (uint32_t *)(b + o_es);
     }
     return off;
 }
@@ -57,6 +61,7 @@ __device__ __forceinline__ uint32_t span_row_word(const uint32_t *bits, uint64_t
 
 __global__ void __launch_bounds__(256) k_row_extent(const uint32_t *__restrict__ K, uint64_t rows, uint64_t X,
                                                     SpanWS w, roix_scalars *sc) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *w.err_snap = get_err(sc);
     if (get_err(sc)) return;
     const uint32_t lane = lane_id();
     const uint32_t W = (uint32_t)((X + 31) / 32);
@@ -109,13 +114,7 @@ __device__ __forceinline__ void span_rows(const T *__restrict__ x, uint64_t rows
             sp.x_end = x0 + len;
             spans[si] = sp;
         }
-        const T *xr = x + r * X + x0;
-        for (uint32_t j = lane; j < len; j += 32) {
-            uint32_t cd;
-            if constexpr (sizeof(T) == 2) cd = code_u16_m<QM>(__ldcs(xr + j), q, err);
-            else cd = (uint32_t)code_f32(__ldcs(xr + j), q, err);
-            if (co + j < code_cap) codes[co + j] = (C)cd;
-        }
+        warp_segment<T, C, QM, 2>(x, r * X + x0, codes, co, len, code_cap, q, err);
     }
     if (err) set_err(sc, err);
 }
@@ -124,7 +123,7 @@ template <typename T, typename C>
 __global__ void __launch_bounds__(256) k_span_write(const T *__restrict__ x, uint64_t rows, uint64_t X, uint64_t row0,
                                                     SpanWS w, roix_scalars *sc, roix_span *spans, uint64_t span_cap,
                                                     C *__restrict__ codes, uint64_t code_cap, uint64_t *counts) {
-    if (get_err(sc)) return;
+    if (*w.err_snap) return;   // (not get_err: this kernel's own capacity bit must not stop its other CTAs)
     if constexpr (sizeof(T) == 4) {
         span_rows<T, C, QM_FLOAT>(x, rows, X, row0, w, sc, spans, span_cap, codes, code_cap, counts);
     } else {

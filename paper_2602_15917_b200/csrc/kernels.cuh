@@ -13,6 +13,7 @@ struct RunsView {
     const uint64_t *n_runs;                       // device: number of runs
     const uint32_t *x0, *x1, *rrow, *parent;      // run [x0, x1) of slab row rrow; parent = its local root
     const uint8_t *kept;                          // kept flag, valid at roots
+    uint32_t *err_snap;                           // error bits before the gather (its own must not stop it)
 };
 
 cudaError_t launch_scalars_init(roix_scalars *sc, float eb, cudaStream_t st);
@@ -62,9 +63,8 @@ cudaError_t launch_label_boundary_roots(const void *ws, const roix_geom &g, uint
                                         uint64_t *sizes, uint64_t out_cap, uint64_t *count, roix_scalars *sc,
                                         cudaStream_t st);
 
-uint64_t gather_chunks_max(uint64_t n);
 cudaError_t launch_gather(const void *x, int dtype, uint64_t nx, const RunsView &R, uint64_t cap, uint32_t *klen,
-                          uint64_t *koff, uint32_t *cfirst, uint64_t *scan_tmp, roix_scalars *sc, void *codes,
+                          uint64_t *koff, uint64_t *scan_tmp, roix_scalars *sc, void *codes,
                           uint64_t capacity, const uint64_t *offset, cudaStream_t st);
 cudaError_t launch_extract_runs(const void *x, int dtype, const roix_geom &g, uint64_t cap, void *ws, roix_scalars *sc,
                                 void *codes, uint64_t capacity, const uint64_t *offset, cudaStream_t st);
