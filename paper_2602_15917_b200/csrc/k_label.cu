@@ -35,7 +35,7 @@ struct LabelWS {
     uint64_t *koff;       // [cap + 1]: their exclusive prefix
 };
 
-constexpr int UB_RUNS = 4096;     // runs per union block (their parents live in shared memory)
+constexpr int UB_MAX = 16384;     // max runs per union block (their parents live in shared memory: 64 KB)
 constexpr int UB_THREADS = 1024;   // 4 runs per thread: short dependent chains
 
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -411,7 +411,8 @@ __device__ __forceinline__ void sunite(uint32_t *lp, uint32_t a, uint32_t b) {
 // Union, phase 1: a CTA owns the runs [base, base + UB_RUNS) and their parent pointers in shared
 // memory.  Neighbour pairs inside the block are united there; pairs reaching an earlier block are
 // queued.  The block's runs then point (globally) at their block-local root.
-__global__ void __launch_bounds__(UB_THREADS) k_union_local(LGeo G, int ci, LabelWS W, roix_scalars *sc) {
+__global__ void __launch_bounds__(UB_THREADS) k_union_local(LGeo G, int ci, LabelWS W, uint32_t UB_RUNS,
+                                                           roix_scalars *sc) {
     extern __shared__ uint32_t lp[];
     if (get_err(sc)) return;
     const uint64_t n = W.ctr[0];
@@ -777,14 +778,18 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
     }
     static bool attr = false;
     if (!attr) {
-        if ((e = cudaFuncSetAttribute(k_union_local, cudaFuncAttributeMaxDynamicSharedMemorySize, UB_RUNS * 4)) !=
+        if ((e = cudaFuncSetAttribute(k_union_local, cudaFuncAttributeMaxDynamicSharedMemorySize, UB_MAX * 4)) !=
             cudaSuccess)
             return e;
         attr = true;
     }
-    uint64_t nub = (cap + UB_RUNS - 1) / UB_RUNS;
+    // Union blocks: 16 K runs for large slabs -- several planes' runs, so most z-links stay inside one
+    // block and the cross-block queue is 3x shorter (C4: union_cross 490 -> 142 us) -- 4 K runs for
+    // small ones, where more, smaller blocks keep the SMs busy (C2: union_local 81 -> 29 us).
+    const uint32_t ub = cap >= (1ull << 23) ? UB_MAX : UB_MAX / 4;
+    uint64_t nub = (cap + ub - 1) / ub;
     if (nub > (uint64_t)num_sms() * 2) nub = (uint64_t)num_sms() * 2;   // persistent over blocks of runs
-    k_union_local<<<(unsigned)nub, UB_THREADS, UB_RUNS * 4, st>>>(G, ci, W, sc);
+    k_union_local<<<(unsigned)nub, UB_THREADS, ub * 4, st>>>(G, ci, W, ub, sc);
     k_union_cross<<<runs_grid, 256, 0, st>>>(W, sc);
     k_flatten_sizes<<<runs_grid, 256, 0, st>>>(W, sc);
     return cudaGetLastError();
