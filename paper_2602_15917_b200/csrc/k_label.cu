@@ -28,7 +28,8 @@ struct LabelWS {
     uint32_t *x0, *x1, *rrow, *parent, *cidx;  // [cap]
     uint64_t *size;       // [cap]
     uint8_t *kept;        // [cap]
-    uint64_t *ctr;        // [4]: 0 n_runs, 1 n_cross_pairs, 2 n_kept
+    uint64_t *ctr;        // [8]: 0 n_runs, 1 n_cross_pairs, 2 n_kept, 3 gather error snapshot, 4 n_block_roots
+    uint32_t *broots;     // [cap]: the block-local roots left by k_union_local
     uint2 *pairs;         // [pair_cap]: run pairs that cross union blocks
     uint64_t pair_cap;
     uint32_t *klen;       // [cap]: kept length of every run (roix_extract_runs)
@@ -52,7 +53,7 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
     size_t o_st = take(scan_tmp_elems(rows + 1 > cap ? rows + 1 : cap) * 8);
     size_t o_x0 = take(cap * 4), o_x1 = take(cap * 4), o_rw = take(cap * 4), o_pa = take(cap * 4),
            o_ci = take((cap + 1) * 4);
-    size_t o_sz = take(cap * 8), o_kp = take(cap), o_ct = take(4 * 8);
+    size_t o_sz = take(cap * 8), o_kp = take(cap), o_ct = take(8 * 8), o_br = take(cap * 4);
     const uint64_t pair_cap = 2 * cap + 1024;
     size_t o_pr = take(pair_cap * 8);
     size_t o_kl = take(cap * 4), o_ko = take((cap + 1) * 8);
@@ -69,6 +70,7 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
         ws->size = (uint64_t *)(b + o_sz);
         ws->kept = (uint8_t *)(b + o_kp);
         ws->ctr = (uint64_t *)(b + o_ct);
+        ws->broots = (uint32_t *)(b + o_br);
         ws->pairs = (uint2 *)(b + o_pr);
         ws->pair_cap = pair_cap;
         ws->klen = (uint32_t *)(b + o_kl);
@@ -165,6 +167,7 @@ __device__ __forceinline__ bool runs_total(const uint64_t *total, uint64_t cap, 
         W.ctr[0] = t > cap ? 0 : t;
         W.ctr[1] = 0;   // cross-block pairs
         W.ctr[2] = 0;
+        W.ctr[4] = 0;   // block roots
         sc->n_runs = t;
         if (t > cap) set_err(sc, ROIX_ERR_CAPACITY);
     }
@@ -467,14 +470,25 @@ __global__ void __launch_bounds__(UB_THREADS) k_union_local(LGeo G, int ci, Labe
             if (at + t < W.pair_cap) W.pairs[at + t] = pend[t];
     }
     __syncthreads();
-    for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) {
-        uint32_t r = k, p = lp[r];
-        while (p != r) {
-            r = p;
-            p = lp[r];
+    for (uint32_t k0 = 0; k0 < cnt; k0 += blockDim.x) {   // whole warps (the root list append below)
+        const uint32_t k = k0 + threadIdx.x;
+        bool root = false;
+        if (k < cnt) {
+            uint32_t r = k, p = lp[r];
+            while (p != r) {
+                r = p;
+                p = lp[r];
+            }
+            W.parent[base + k] = (uint32_t)(base + r);
+            W.size[base + k] = 0;
+            root = r == k;
         }
-        W.parent[base + k] = (uint32_t)(base + r);
-        W.size[base + k] = 0;
+        // block-local roots -> W.broots: only they can be linked further by k_union_cross
+        const uint32_t bal = __ballot_sync(FULL, root);
+        unsigned long long at = 0;
+        if (lane_id() == 0 && bal) at = atomicAdd((unsigned long long *)&W.ctr[4], (unsigned long long)__popc(bal));
+        at = __shfl_sync(FULL, at, 0);
+        if (root) W.broots[at + __popc(bal & low_mask(lane_id()))] = (uint32_t)(base + k);
     }
     }
 }
@@ -493,22 +507,63 @@ __global__ void k_union_cross(LabelWS W, roix_scalars *sc) {
     }
 }
 
+// After k_union_cross: every block-local root points at its final root (compressing on the way).
+// Every other run's parent is then one of those block roots (unions only ever link roots, and path
+// halving only moves a pointer to an ancestor), so two hops reach the final root.
+// Union by min index makes parent values strictly decrease towards a root, so every pointer update
+// here is an atomicMin: a thread's halving step can never overwrite another's final root pointer
+// with an intermediate ancestor.
+__global__ void k_resolve_broots(LabelWS W, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t nb = W.ctr[4];
+    uint32_t *par = W.parent;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nb; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t b = W.broots[t];
+        uint32_t x = b, p = par[x];
+        while (p != x) {   // find with path halving
+            const uint32_t gp = par[p];
+            if (gp != p) atomicMin(&par[x], gp);
+            x = p;
+            p = gp;
+        }
+        atomicMin(&par[b], x);
+    }
+}
+
+// Final roots (two hops) and component sizes.  A warp owns FL_J x 32 consecutive runs (lane l: runs
+// l, l + 32, ...); each lane sums run lengths while the root stays the same and flushes on a change,
+// then the lanes holding the same root merge their sums (match.any) -- one atomic per root per warp,
+// so a component spanning the whole volume (C4's matrix) is not one hot address hit per run.
+constexpr int FL_J = 16;
 __global__ void k_flatten_sizes(LabelWS W, roix_scalars *sc) {
     if (get_err(sc)) return;
     const uint64_t n = W.ctr[0];
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    // grid-stride over whole warps so that the warp-level aggregation below is convergent
-    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < n; i0 += stride) {
-        const uint64_t i = i0 + lane_id();
-        uint32_t root = 0xffffffffu, len = 0;
-        if (i < n) {
-            root = find_root(W.parent, (uint32_t)i);
+    const uint32_t lane = lane_id();
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    // runs per lane: up to FL_J, fewer when there are not enough runs to keep every warp busy
+    const int J = (int)min((uint64_t)FL_J, max((uint64_t)1, n / (nw * 32)));
+    for (uint64_t b0 = ((uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 * J); b0 < n;
+         b0 += nw * 32 * J) {
+        uint32_t cur = 0xffffffffu;
+        uint64_t sum = 0;
+#pragma unroll 4
+        for (int j = 0; j < J; j++) {
+            const uint64_t i = b0 + (uint64_t)j * 32 + lane;
+            if (i >= n) break;
+            const uint32_t root = W.parent[W.parent[i]];   // two hops after k_resolve_broots
             W.parent[i] = root;
-            len = W.x1[i] - W.x0[i];
+            const uint32_t len = W.x1[i] - W.x0[i];
+            if (root != cur) {
+                if (sum) atomicAdd((unsigned long long *)&W.size[cur], (unsigned long long)sum);
+                cur = root;
+                sum = 0;
+            }
+            sum += len;
         }
-        uint32_t grp = __match_any_sync(FULL, root);
-        uint32_t tot = __reduce_add_sync(grp, len);
-        if (i < n && (__ffs(grp) - 1) == (int)lane_id()) atomicAdd((unsigned long long *)&W.size[root], (unsigned long long)tot);
+        const uint32_t grp = __match_any_sync(FULL, cur);
+        const uint64_t tot = __reduce_add_sync(grp, (uint32_t)sum);   // per-warp sums fit 32 bits
+        if (cur != 0xffffffffu && (__ffs(grp) - 1) == (int)lane && tot)
+            atomicAdd((unsigned long long *)&W.size[cur], (unsigned long long)tot);
     }
 }
 
@@ -791,6 +846,7 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
     if (nub > (uint64_t)num_sms() * 2) nub = (uint64_t)num_sms() * 2;   // persistent over blocks of runs
     k_union_local<<<(unsigned)nub, UB_THREADS, ub * 4, st>>>(G, ci, W, ub, sc);
     k_union_cross<<<runs_grid, 256, 0, st>>>(W, sc);
+    k_resolve_broots<<<runs_grid, 256, 0, st>>>(W, sc);
     k_flatten_sizes<<<runs_grid, 256, 0, st>>>(W, sc);
     return cudaGetLastError();
 }

@@ -15,7 +15,7 @@ STAGE = {
     "histogram": ["k_hist_u16", "k_hist_f32"],
     "threshold": ["k_threshold"],
     "morph": ["k_binarize", "k_open3d_reg", "k_open3d_rows", "k_open2d"],
-    "label": ["k_scan_dlb", "k_runs_total", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross",
+    "label": ["k_scan_dlb", "k_runs_total", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross", "k_resolve_broots",
               "k_flatten_sizes", "k_root_flags", "k_table", "k_table_total", "k_clear_dropped", "k_table_clear"],
     "extract": ["k_extract_count", "k_extract", "k_extract_total"],
 }
