@@ -69,6 +69,7 @@ def _load():
         "oracle_extract_u16": (i64, [vp, vp, u64, f32, vp]),
         "oracle_extract_f32": (i64, [vp, vp, u64, f32, vp]),
         "oracle_row_spans": (i64, [vp, vp, i32, i64, i64, i64, f32, vp, vp, vp]),
+        "oracle_greedy_quantize": (i64, [vp, u64, f64, u32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -245,6 +246,17 @@ def row_spans(x, K, eb):
     if m < 0:
         raise OracleError("row_spans failed")
     return spans[:m].copy(), codes[: nc.value].copy()
+
+
+def greedy_quantize(D, E, qmax=65535):
+    """NEXT-2: the paper's greedy absolute-error-bounded quantiser on a uint16
+    sequence: (Q, group_start) with |Q - D| <= E, groups the greedy left-to-right maximal runs with a
+    non-empty interval intersection, Q = floor((u + l) / 2) of the group, clipped to [0, qmax]."""
+    D = _c(np.asarray(D).reshape(-1), np.uint16)
+    Q = np.empty(max(D.size, 1), np.uint16)
+    gs = np.empty(max(D.size, 1), np.uint8)
+    _load().oracle_greedy_quantize(_p(D), D.size, float(E), int(qmax), _p(Q), _p(gs))
+    return Q[: D.size].copy(), gs[: D.size].copy()
 
 
 def pack_bits(mask):

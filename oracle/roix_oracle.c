@@ -369,3 +369,46 @@ int64_t oracle_row_spans(const uint8_t *K, const void *x, int is_f32, int64_t Z,
     *ncodes = nc;
     return m;
 }
+
+/* ----------------------------------------------- NEXT-2: greedy absolute-error-bounded quantiser
+ * PAPER.md §4.2.3 Steps 1-5, literally: l = -inf, u = +inf, head = 0; for each i the
+ * intersection [max(l, D[i] - E), min(u, D[i] + E)]; when it is empty the group [head, i) gets
+ * Q = floor((u + l) / 2) and a new group starts at i with [D[i] - E, D[i] + E]; the final group
+ * likewise; Q clipped to [0, qmax] (Step 5: 255 for 8-bit data; 65535 here for 16-bit data).
+ * E >= 0 (S:299 admits 0); group_start[i] = 1 where a group begins.  Returns the group count. */
+int64_t oracle_greedy_quantize(const uint16_t *D, uint64_t m, double E, uint32_t qmax, uint16_t *Q, uint8_t *group_start)
+{
+    double l = -INFINITY, u = INFINITY;
+    uint64_t head = 0;
+    int64_t groups = 0;
+    for (uint64_t i = 0; i < m; i++) {
+        const double lo = (double)D[i] - E, hi = (double)D[i] + E;
+        const double ln = l > lo ? l : lo, un = u < hi ? u : hi;
+        group_start[i] = 0;
+        if (un < ln) {
+            double q = floor((u + l) / 2.0);
+            if (q < 0) q = 0;
+            if (q > qmax) q = qmax;
+            for (uint64_t j = head; j < i; j++) Q[j] = (uint16_t)q;
+            l = lo;
+            u = hi;
+            head = i;
+            group_start[i] = 1;
+            groups++;
+        } else {
+            l = ln;
+            u = un;
+        }
+        if (i == 0) {
+            group_start[0] = 1;
+            groups++;
+        }
+    }
+    if (m) {
+        double q = floor((u + l) / 2.0);
+        if (q < 0) q = 0;
+        if (q > qmax) q = qmax;
+        for (uint64_t j = head; j < m; j++) Q[j] = (uint16_t)q;
+    }
+    return groups;
+}
