@@ -45,6 +45,9 @@ def parse():
                          "replay; N > 1 always enqueues, the exchanges synchronise with the host)")
     ap.add_argument("--extract", default="mask", choices=["mask", "runs"], help="a8 form (see Pipeline)")
     ap.add_argument("--spans", action="store_true", help="also produce the NEXT-1 row spans (roix_row_spans)")
+    ap.add_argument("--greedy", type=float, default=None, metavar="E",
+                    help="NEXT-2 extra line item: time the paper's greedy quantiser (error E) on the raw pixel "
+                         "sections of K's row spans (u16 configs)")
     return ap.parse_args()
 
 
@@ -331,6 +334,8 @@ def main():
     }
     clocks = clk.summary()
     line["clocks"] = clocks
+    if args.greedy is not None and world == 1 and cfg.dtype == "u16":
+        line["next2_greedy"] = next2(p, x, cfg, args)
     # ---- end to end through the public API with host buffers (every rank its slab; max over ranks)
     if not args.no_e2e:
         line["e2e"] = e2e(p, x, cfg, args, world)
@@ -346,6 +351,51 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def next2(p, x, cfg, args):
+    """NEXT-2: the row spans of K with their raw pixel values (step 1: codes = values), then the paper's
+    greedy quantiser on that one concatenated stream (S Open Questions), timed alone with CUDA events."""
+    import ctypes
+
+    import torch
+
+    from paper_2602_15917_b200 import _lib as L
+
+    dev = x.device
+    Z, Y, X = cfg.shape
+    sc = torch.zeros(L.scalars_size(), dtype=torch.uint8, device=dev)
+    st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    sp = lambda t: ctypes.c_void_p(t.data_ptr())
+    L.roix_scalars_init(sp(sc), 0.5, st)
+    L.roix_resolve(sp(sc), L.U16, 0.0, st)
+    g = L.Geom(Z, Y, X, 0, Z)
+    ws = torch.empty(L.roix_row_spans_workspace(g), dtype=torch.uint8, device=dev)
+    rec = torch.empty(2 * Z * Y + 2, dtype=torch.int64, device=dev)
+    D = torch.empty(cfg.n + 8, dtype=torch.int16, device=dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=dev)
+    L.roix_row_spans(sp(p.o), sp(x), L.U16, ctypes.byref(g), sp(sc), sp(rec), Z * Y, sp(D), D.numel(), sp(cnt), sp(ws),
+                     ws.numel(), st)
+    n = int(cnt[1].item())
+    gws = torch.empty(L.roix_greedy_workspace(n), dtype=torch.uint8, device=dev)
+    Q = torch.empty(n + 8, dtype=torch.int16, device=dev)
+    gb = torch.empty((n + 31) // 32 + 2, dtype=torch.int32, device=dev)
+    ng = torch.zeros(1, dtype=torch.int64, device=dev)
+    run = lambda: L.roix_greedy_quantize(sp(D), n, args.greedy, 65535, sp(Q), sp(gb), sp(ng), sp(gws), gws.numel(), st)
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    groups = int(ng.item())
+    return {"E": args.greedy, "elements": n, "groups": groups, "ms": ms,
+            "gb_s_in": 2 * n / (ms * 1e-3) / 1e9, "alg_bytes": 2 * n * 2 + n / 8,
+            "frac": (4 * n + n / 8) / (ms * 1e-3) / 1e9 / peaks()[0]}
 
 
 def e2e(p, x, cfg, args, world=1):

@@ -313,6 +313,19 @@ roix_status roix_row_spans(const uint32_t *keep_bits, const void *x, roix_dtype 
                            roix_scalars *sc, roix_span *spans, uint64_t span_cap, void *codes, uint64_t code_cap,
                            uint64_t *counts, void *ws, size_t ws_bytes, roix_stream_t stream);
 
+/*
+ * NEXT-2 GREEDY QUANTISER: the paper's absolute-error-bounded quantiser (§4.2.3 Steps 1-5,
+ * P:340-399) on a uint16 sequence D[0..n) (device): groups are the greedy left-to-right
+ * maximal runs whose intervals [D - E, D + E] intersect (range max - min <= 2E); Q[i] = floor((u + l)
+ * / 2) = floor((max + min) / 2) of i's group, clipped to [0, qmax] (Step 5: 255 for 8-bit data).
+ * group_bits (device, ceil(n/32) words): bit i set where a group starts; *ngroups (device): their
+ * number.  E >= 0 and finite (S:299 admits 0: runs of equal values).  |Q - D| <= E for integer E and
+ * whenever frac(E) < 1/2 (G-35).  ws/ws_bytes from roix_greedy_workspace.
+ */
+roix_status roix_greedy_workspace(uint64_t n, size_t *ws_bytes);
+roix_status roix_greedy_quantize(const uint16_t *D, uint64_t n, double E, uint32_t qmax, uint16_t *Q, uint32_t *group_bits,
+                                 uint64_t *ngroups, void *ws, size_t ws_bytes, roix_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,8 @@ _SIGS = {
     "roix_row_spans_workspace": (_i32, [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_size_t)]),
     "roix_row_spans": (_i32, [_vp, _vp, _i32, ctypes.POINTER(Geom), _vp, _vp, _u64, _vp, _u64, _vp, _vp,
                               ctypes.c_size_t, _vp]),
+    "roix_greedy_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_greedy_quantize": (_i32, [_vp, _u64, _f64, _u32, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "roix_extract_runs": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _u64, _vp,
                                  _vp]),
 }
@@ -133,6 +135,7 @@ roix_label = _wrap("roix_label")
 roix_extract = _wrap("roix_extract")
 roix_extract_runs = _wrap("roix_extract_runs")
 roix_row_spans = _wrap("roix_row_spans")
+roix_greedy_quantize = _wrap("roix_greedy_quantize")
 roix_label_local = _wrap("roix_label_local")
 roix_label_boundary = _wrap("roix_label_boundary")
 roix_label_link = _wrap("roix_label_link")
@@ -186,6 +189,12 @@ def roix_extract_workspace(n):
 def roix_row_spans_workspace(geom):
     out = ctypes.c_size_t()
     _check(load().roix_row_spans_workspace(ctypes.byref(geom), ctypes.byref(out)), "roix_row_spans_workspace")
+    return out.value
+
+
+def roix_greedy_workspace(n):
+    out = ctypes.c_size_t()
+    _check(load().roix_greedy_workspace(n, ctypes.byref(out)), "roix_greedy_workspace")
     return out.value
 
 

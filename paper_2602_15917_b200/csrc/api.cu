@@ -402,4 +402,20 @@ roix_status roix_row_spans(const uint32_t *keep_bits, const void *x, roix_dtype 
                 "roix_row_spans");
 }
 
+roix_status roix_greedy_workspace(uint64_t n, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    *ws_bytes = greedy_workspace_bytes(n);
+    return ROIX_OK;
+}
+
+roix_status roix_greedy_quantize(const uint16_t *D, uint64_t n, double E, uint32_t qmax, uint16_t *Q, uint32_t *group_bits,
+                                 uint64_t *ngroups, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    if (!ngroups || !ws || !group_bits) return invalid("ngroups / group_bits / ws is NULL");
+    if (!(E >= 0.0) || !std::isfinite(E)) return invalid("E must be finite and >= 0");
+    if (qmax > 65535) return invalid("qmax must be <= 65535");
+    if (n && (!D || !Q)) return invalid("D / Q is NULL");
+    if (ws_bytes < greedy_workspace_bytes(n)) return invalid("workspace too small (see roix_greedy_workspace)");
+    return cuda(launch_greedy(D, n, E, qmax, Q, group_bits, ngroups, ws, (cudaStream_t)stream), "roix_greedy_quantize");
+}
+
 }  // extern "C"

@@ -73,3 +73,7 @@ size_t row_spans_workspace_bytes(const roix_geom &g);
 cudaError_t launch_row_spans(const uint32_t *K, const void *x, int dtype, const roix_geom &g, roix_scalars *sc,
                              roix_span *spans, uint64_t span_cap, void *codes, uint64_t code_cap, uint64_t *counts,
                              void *ws, cudaStream_t st);
+
+size_t greedy_workspace_bytes(uint64_t n);
+cudaError_t launch_greedy(const uint16_t *D, uint64_t n, double E, uint32_t qmax, uint16_t *Q, uint32_t *group_bits,
+                          uint64_t *ngroups, void *ws, cudaStream_t st);

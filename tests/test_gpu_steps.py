@@ -479,3 +479,39 @@ def test_row_spans_global_rows_and_capacity():
     assert np.all(sp[6:] == -1)
     np.testing.assert_array_equal(cd[:10], rc[:10])
     assert np.all(cd.view(np.int16)[10:] == -1)
+
+
+# ------------------------------------------------------ NEXT-2 greedy quantiser (Steps 1-5)
+def _greedy_gpu(D, E, qmax=65535):
+    n = D.size
+    wsb = L.roix_greedy_workspace(n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    d = dev(D) if n else torch.empty(8, dtype=torch.int16, device="cuda")
+    q = torch.full((max(n, 1) + 8,), -1, dtype=torch.int16, device="cuda")
+    gb = torch.full(((n + 31) // 32 + 2,), -1, dtype=torch.int32, device="cuda")
+    ng = torch.zeros(1, dtype=torch.int64, device="cuda")
+    L.roix_greedy_quantize(ptr(d), n, float(E), qmax, ptr(q), ptr(gb), ptr(ng), ptr(ws), wsb, st())
+    torch.cuda.synchronize()
+    return q.cpu().numpy().view(np.uint16)[:n], words_to_mask(gb, n), int(ng.item())
+
+
+@pytest.mark.parametrize("E", [0, 0.4, 1, 2, 17.5, 300, 70000])
+def test_greedy_vs_oracle(E):
+    rng = np.random.default_rng(int(E * 7) % 2 ** 31)
+    seqs = [np.zeros(0, np.uint16), np.array([5, 5, 7], np.uint16), np.full(1000, 77, np.uint16),
+            rng.integers(0, 65536, 5000).astype(np.uint16),
+            np.clip(np.cumsum(rng.integers(-3, 4, 100003)) + 30000, 0, 65535).astype(np.uint16),
+            np.clip(rng.normal(2500, 100, 70001), 0, 65535).astype(np.uint16),
+            np.repeat(rng.integers(0, 4000, 300), rng.integers(1, 200, 300)).astype(np.uint16)]
+    for D in seqs:
+        rq, rg = oracle.greedy_quantize(D, E)
+        q, g, ng = _greedy_gpu(D, E)
+        np.testing.assert_array_equal(q, rq)
+        np.testing.assert_array_equal(g, rg)
+        assert ng == int(rg.sum())
+
+
+def test_greedy_8bit_spec_examples():
+    for D, E, Q in [([10, 12, 20], 2, [11, 11, 20]), ([255, 251], 3, [253, 253]), ([0, 255], 200, [127, 127])]:
+        q, g, ng = _greedy_gpu(np.array(D, np.uint16), E, 255)
+        np.testing.assert_array_equal(q, Q)
