@@ -16,7 +16,7 @@ from . import _lib as L
 
 # kernels libroix launches per call (used for the bench's gpu_launches count)
 LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 1, "threshold": 1, "morph": 2,
-            "label": 10, "extract": 4, "extract_runs": 5}
+            "label": 9, "extract": 4, "extract_runs": 5}
 
 
 def _ptr(t):
