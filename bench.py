@@ -406,6 +406,8 @@ def e2e(p, x, cfg, args, world=1):
 
     from paper_2602_15917_b200 import _lib as L
 
+    if world == 1:
+        return e2e_pipelined(p, x, cfg, args)
     P = getattr(p, "S", p)                       # the slab state of a sharded pipeline
     xh = x.cpu().pin_memory()
     xd = torch.empty_like(x)
@@ -450,6 +452,76 @@ def e2e(p, x, cfg, args, world=1):
         dt, h2d, d2h = float(t.item()), int(b[0].item()), int(b[1].item())
     return {"value": cfg.nbytes / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": dt * 1e3, "steps": steps}
+
+
+def e2e_pipelined(p, x, cfg, args):
+    """e2e at N = 1 with the steps overlapped the way a streaming user runs them: volume i+1 copies in
+    (pinned host -> device, its own stream and input buffer) while volume i is processed and its result
+    (count, code stream, kept mask) copies out on a third stream.  Every step still moves its whole
+    input in and its whole result out; the time per step is the wall time of the loop / steps."""
+    import torch
+
+    from paper_2602_15917_b200 import _lib as L
+
+    dev = x.device
+    xh = x.cpu().pin_memory()
+    xd = [torch.empty_like(x), torch.empty_like(x)]
+    cnt_h = [torch.empty(1, dtype=torch.int64).pin_memory() for _ in range(2)]
+    out_h = torch.empty(p.codes.numel(), dtype=p.codes.dtype).pin_memory()
+    mask_h = torch.empty(p.nwords, dtype=torch.int32).pin_memory()
+    s_in, s_run, s_out = (torch.cuda.Stream(dev) for _ in range(3))
+    off = L.Scalars.count.offset
+    cnt_d = p.sc[off:off + 8].view(torch.int64)      # roix_scalars.count
+    steps = max(3, min(args.steps, 10))
+    total = steps + 1                                # one untimed warm-up step first
+    ev_in = [torch.cuda.Event() for _ in range(total)]
+    ev_run = [torch.cuda.Event() for _ in range(total)]
+    ev_out = [torch.cuda.Event() for _ in range(total)]
+    d2h = [0]
+
+    def h2d(i):
+        with torch.cuda.stream(s_in):
+            if i >= 2:
+                s_in.wait_event(ev_run[i - 2])       # the input buffer is free again
+            xd[i % 2].copy_(xh, non_blocking=True)
+            ev_in[i].record(s_in)
+
+    def run(i):
+        s_run.wait_event(ev_in[i])
+        if i >= 1:
+            s_run.wait_event(ev_out[i - 1])          # the previous result has been read out
+        p.enqueue(xd[i % 2], stream=s_run)
+        with torch.cuda.stream(s_run):
+            cnt_h[i % 2].copy_(cnt_d, non_blocking=True)
+            ev_run[i].record(s_run)
+
+    def d2h_(i):
+        ev_run[i].synchronize()
+        c = int(cnt_h[i % 2][0])
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_run[i])
+            out_h[:c].copy_(p.codes[:c], non_blocking=True)
+            mask_h.copy_(p.o[: p.nwords], non_blocking=True)
+            ev_out[i].record(s_out)
+        d2h[0] = c * p.codes.element_size() + p.nwords * 4 + 8
+
+    h2d(0)
+    run(0)
+    t0 = None
+    for i in range(total):
+        if i == 1:
+            ev_out[0].synchronize()
+            t0 = time.perf_counter()                 # timed: steps 1 .. total-1
+        if i + 1 < total:
+            h2d(i + 1)
+        d2h_(i)
+        if i + 1 < total:
+            run(i + 1)
+    ev_out[total - 1].synchronize()
+    dt = (time.perf_counter() - t0) / (total - 1)
+    return {"value": cfg.nbytes / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": x.numel() * x.element_size(),
+            "d2h_bytes_per_step": d2h[0], "ms_per_step": dt * 1e3, "steps": total - 1,
+            "overlap": "h2d(i+1) || run(i) || d2h(i-1)"}
 
 
 if __name__ == "__main__":

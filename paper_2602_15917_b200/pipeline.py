@@ -111,8 +111,11 @@ class Pipeline:
         storage or float32) on `stream` (default: torch's current stream).  No host sync.
         mark(stage) is called after each stage is enqueued (the bench records CUDA events there)."""
         assert x.is_cuda and x.numel() == self.n and x.is_contiguous()
+        if stream is not None and stream != torch.cuda.current_stream(self.device):
+            with torch.cuda.stream(stream):      # torch ops here (hist.zero_) go to the same stream
+                return self.enqueue(x, None, mark)
         mark = mark or (lambda stage: None)
-        st = ctypes.c_void_p((stream or torch.cuda.current_stream(self.device)).cuda_stream)
+        st = ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         sc, xp, n = _ptr(self.sc), _ptr(x), self.n
         L.roix_scalars_init(sc, self.eb, st)
         if self.cdtype == L.F32:
