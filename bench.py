@@ -45,6 +45,8 @@ def parse():
                          "replay; N > 1 always enqueues, the exchanges synchronise with the host)")
     ap.add_argument("--extract", default="mask", choices=["mask", "runs"], help="a8 form (see Pipeline)")
     ap.add_argument("--spans", action="store_true", help="also produce the NEXT-1 row spans (roix_row_spans)")
+    ap.add_argument("--no-next4", action="store_true",
+                    help="skip the NEXT-4 items (reconstruction timing, quality vs the phantom's ground truth)")
     ap.add_argument("--greedy", type=float, default=None, metavar="E",
                     help="NEXT-2 extra line item: time the paper's greedy quantiser (error E) on the raw pixel "
                          "sections of K's row spans (u16 configs)")
@@ -336,6 +338,8 @@ def main():
     line["clocks"] = clocks
     if args.greedy is not None and world == 1 and cfg.dtype == "u16":
         line["next2_greedy"] = next2(p, x, cfg, args)
+    if not args.no_next4 and world == 1:
+        line["next4"] = next4(p, x, cfg, args, count)
     # ---- end to end through the public API with host buffers (every rank its slab; max over ranks)
     if not args.no_e2e:
         line["e2e"] = e2e(p, x, cfg, args, world)
@@ -396,6 +400,54 @@ def next2(p, x, cfg, args):
     return {"E": args.greedy, "elements": n, "groups": groups, "ms": ms,
             "gb_s_in": 2 * n / (ms * 1e-3) / 1e9, "alg_bytes": 2 * n * 2 + n / 8,
             "frac": (4 * n + n / 8) / (ms * 1e-3) / 1e9 / peaks()[0]}
+
+
+def next4(p, x, cfg, args, count):
+    """NEXT-4 line items, after the timed region: (1) roix_decode -- the volume reconstructed from the
+    step's kept mask + code stream, timed alone with CUDA events; (2) roix_confusion of K
+    against the phantom's ground truth (synth regenerates x bit-identically with its truth mask) and
+    Eqs. 7-14 (P:509-547)."""
+    import torch
+
+    import synth
+
+    dev = x.device
+    tw = torch.empty(synth.truth_words(cfg) + 4, dtype=torch.int32, device=dev)
+    synth.generate(cfg, out=x, device=dev, truth=tw)     # same voxel values, plus the truth bits
+    q = p.quality(tw)
+    xh = torch.empty_like(x)
+    p.decode(xh)
+    cnt = torch.empty(4, dtype=torch.int64, device=dev)
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    reps = max(3, args.steps)
+    ms_dec = timed(lambda: p.decode(xh), reps)
+    ms_conf = timed(lambda: p.confusion(tw, counts=cnt), reps)
+    if p.scalars().err:
+        raise SystemExit("device error bits 0x%x in NEXT-4" % p.scalars().err)
+    n = cfg.n
+    csize = 2 if cfg.dtype == "u16" else 4
+    dec_bytes = n / 8 + count * csize + n * cfg.itemsize   # K once, the codes, every voxel of x^ written
+    peak = peaks()[0]
+    return {"decode": {"call": "roix_decode", "ms": ms_dec, "alg_bytes": dec_bytes,
+                       "achieved_gbs": dec_bytes / (ms_dec * 1e-3) / 1e9,
+                       "frac": dec_bytes / (ms_dec * 1e-3) / 1e9 / peak},
+            "confusion": {"call": "roix_confusion", "ms": ms_conf, "alg_bytes": n / 4,
+                          "frac": n / 4 / (ms_conf * 1e-3) / 1e9 / peak},
+            "quality_vs_truth": {k: q[k] for k in ("dsc", "iou", "sensitivity", "specificity", "accuracy", "kappa",
+                                                   "auc")},
+            "counts": q["counts"], "spatial_reduction": q["spatial_reduction_voxels"]}
 
 
 def e2e(p, x, cfg, args, world=1):

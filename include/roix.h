@@ -57,6 +57,7 @@ typedef enum { ROIX_OK = 0, ROIX_E_INVALID = 1, ROIX_E_UNSUPPORTED = 2, ROIX_E_C
 #define ROIX_ERR_RANGE 2u      /* |x| >= 2^23 * s, or a u16 code > 65535, or eb invalid (G-4, G-7)   */
 #define ROIX_ERR_CAPACITY 4u   /* an output / workspace capacity was exceeded                        */
 #define ROIX_ERR_DEGENERATE 8u /* fewer than two populated normalised-intensity bins      */
+#define ROIX_ERR_FORMAT 16u    /* roix_decode_spans: records out of order / outside the slab / empty   */
 
 typedef enum { ROIX_U16 = 1, ROIX_F32 = 2 } roix_dtype;
 typedef enum { ROIX_POL_HIGH = 0, ROIX_POL_LOW = 1 } roix_polarity; /* ROI = norm8 > t8 / <= t8 (G-10) */
@@ -325,6 +326,57 @@ roix_status roix_row_spans(const uint32_t *keep_bits, const void *x, roix_dtype 
 roix_status roix_greedy_workspace(uint64_t n, size_t *ws_bytes);
 roix_status roix_greedy_quantize(const uint16_t *D, uint64_t n, double E, uint32_t qmax, uint16_t *Q, uint32_t *group_bits,
                                  uint64_t *ngroups, void *ws, size_t ws_bytes, roix_stream_t stream);
+
+/*
+ * NEXT-4 RECONSTRUCTION ("each row is precisely restored using the preserved metadata";
+ * SPEC S:359-367 reconstruct_image without a background: the ROI on a zero canvas).  The decoded value
+ * of a code c, with s = sc->s = fl32(2 eb) (set by roix_scalars_init + roix_resolve with the eb the
+ * codes were made with; G-37):
+ *   u16 input   x^ = min(65535, RNE(c * s)): c * s_int when s is an integer, else the exact binary64
+ *               product rounded half to even -- |x - x^| <= eb for integer s (eb + 1/2 otherwise);
+ *   fp32 input  x^ = fl32(fl32(c) * s), one correctly rounded fp32 multiply.
+ *
+ * roix_decode: the mask form (roix_extract's output).  xhat[i] = x^(codes[j]) for the j-th set bit i
+ * of keep_bits[0..n) (in increasing i), 0 elsewhere; every voxel of xhat[0..n) (dtype's type) is
+ * written.  ncodes: elements readable at codes; more kept voxels than ncodes sets ROIX_ERR_CAPACITY
+ * and writes nothing.  ws/ws_bytes from roix_decode_workspace.
+ */
+roix_status roix_decode_workspace(uint64_t n, size_t *ws_bytes);
+roix_status roix_decode(const uint32_t *keep_bits, const void *codes, uint64_t ncodes, roix_dtype dtype, uint64_t n,
+                        roix_scalars *sc, void *xhat, void *ws, size_t ws_bytes, roix_stream_t stream);
+
+/*
+ * roix_decode_spans: the span form (roix_row_spans' output, the paper's representation).  xhat is the
+ * slab g ([nz][ny][nx], dtype's type), every voxel written: row i = z*Y + y (global) of a record gets
+ * x^ of its section's codes over [x_start, x_end), every other voxel 0.  counts (device, 2 uint64) =
+ * (number of records, total section length) as roix_row_spans wrote them; spans hold span_cap
+ * records and codes code_cap codes.  Records must have strictly increasing rows inside the slab and
+ * 0 <= x_start < x_end <= nx, and the lengths must sum to counts[1]: else ROIX_ERR_FORMAT; more than
+ * span_cap records or code_cap codes: ROIX_ERR_CAPACITY.  Nothing is decoded after either error.
+ * ws/ws_bytes from roix_decode_spans_workspace.
+ */
+roix_status roix_decode_spans_workspace(const roix_geom *g, size_t *ws_bytes);
+roix_status roix_decode_spans(const roix_span *spans, uint64_t span_cap, const void *codes, uint64_t code_cap,
+                              const uint64_t *counts, roix_dtype dtype, const roix_geom *g, roix_scalars *sc,
+                              void *xhat, void *ws, size_t ws_bytes, roix_stream_t stream);
+
+/*
+ * NEXT-4 ROI QUALITY METRICS.  roix_confusion: the per-voxel tally of two
+ * bit-packed masks of n voxels (device) into counts (device, 4 uint64) = (tp, fp, fn, tn): tp =
+ * #(pred & truth), fp = #(pred & ~truth), fn = #(~pred & truth), tn = n - tp - fp - fn.  Pad bits past
+ * n are ignored.
+ */
+roix_status roix_confusion(const uint32_t *pred_bits, const uint32_t *truth_bits, uint64_t n, uint64_t *counts,
+                           roix_stream_t stream);
+
+/*
+ * roix_overlap_metrics (host only, no GPU work): Eqs. 7-14 from counts (host, 4 uint64: tp, fp, fn, tn)
+ * into out (host, 7 doubles): dsc = 2tp/(2tp+fp+fn), iou = tp/(tp+fp+fn), sensitivity = tp/(tp+fn),
+ * specificity = tn/(tn+fp), accuracy = (tp+tn)/N, kappa = ((tp+tn) - f_c)/(N - f_c) with f_c =
+ * ((tn+fn)(tn+fp) + (fp+tp)(fn+tp))/N, auc = 1 - (fp/(fp+tn) + fn/(fn+tp))/2; N = tp+fp+fn+tn.  Ratios
+ * of exact 128-bit integers; a zero denominator gives NaN.
+ */
+roix_status roix_overlap_metrics(const uint64_t *counts, double *out);
 
 #ifdef __cplusplus
 }

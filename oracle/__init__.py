@@ -9,6 +9,7 @@ Pieces:
 * ``roix_oracle.c`` (single-threaded C, -O2 -ffp-contract=off): quantiser, range, histograms,
   norm8, binarisation, opening, BFS labelling, filter, extraction.
 * ``otsu.py``: exact-rational 2-class Otsu.
+* ``reconstruct.py``: NEXT-4 decode (mask and span forms), confusion counts and Eqs. 7-14.
 * ``pipeline()`` below: the steps composed in the paper's order (Fig. 2):
   histogram -> normalise (Eq. 1) -> Otsu -> binarise (Eq. 2) -> opening -> CCL -> filter -> extract.
 
@@ -24,6 +25,8 @@ import subprocess
 import numpy as np
 
 from .otsu import Degenerate, otsu2  # noqa: F401
+from .reconstruct import (confusion, decode_mask, decode_spans, decode_value, overlap_metrics,  # noqa: F401
+                          spatial_reduction, step)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "roix_oracle.c")

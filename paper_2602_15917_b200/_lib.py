@@ -11,7 +11,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libroix.so")
 
 ROIX_OK, ROIX_E_INVALID, ROIX_E_UNSUPPORTED, ROIX_E_CUDA = 0, 1, 2, 3
-ERR_NONFINITE, ERR_RANGE, ERR_CAPACITY, ERR_DEGENERATE = 1, 2, 4, 8
+ERR_NONFINITE, ERR_RANGE, ERR_CAPACITY, ERR_DEGENERATE, ERR_FORMAT = 1, 2, 4, 8, 16
 U16, F32 = 1, 2
 POL_HIGH, POL_LOW = 0, 1
 
@@ -88,6 +88,13 @@ _SIGS = {
     "roix_greedy_quantize": (_i32, [_vp, _u64, _f64, _u32, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "roix_extract_runs": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _u64, _vp,
                                  _vp]),
+    "roix_decode_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_decode": (_i32, [_vp, _vp, _u64, _i32, _u64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "roix_decode_spans_workspace": (_i32, [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_decode_spans": (_i32, [_vp, _u64, _vp, _u64, _vp, _i32, ctypes.POINTER(Geom), _vp, _vp, _vp,
+                                 ctypes.c_size_t, _vp]),
+    "roix_confusion": (_i32, [_vp, _vp, _u64, _vp, _vp]),
+    "roix_overlap_metrics": (_i32, [ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_double)]),
 }
 
 
@@ -136,6 +143,9 @@ roix_extract = _wrap("roix_extract")
 roix_extract_runs = _wrap("roix_extract_runs")
 roix_row_spans = _wrap("roix_row_spans")
 roix_greedy_quantize = _wrap("roix_greedy_quantize")
+roix_decode = _wrap("roix_decode")
+roix_decode_spans = _wrap("roix_decode_spans")
+roix_confusion = _wrap("roix_confusion")
 roix_label_local = _wrap("roix_label_local")
 roix_label_boundary = _wrap("roix_label_boundary")
 roix_label_link = _wrap("roix_label_link")
@@ -196,6 +206,29 @@ def roix_greedy_workspace(n):
     out = ctypes.c_size_t()
     _check(load().roix_greedy_workspace(n, ctypes.byref(out)), "roix_greedy_workspace")
     return out.value
+
+
+def roix_decode_workspace(n):
+    out = ctypes.c_size_t()
+    _check(load().roix_decode_workspace(n, ctypes.byref(out)), "roix_decode_workspace")
+    return out.value
+
+
+def roix_decode_spans_workspace(geom):
+    out = ctypes.c_size_t()
+    _check(load().roix_decode_spans_workspace(ctypes.byref(geom), ctypes.byref(out)), "roix_decode_spans_workspace")
+    return out.value
+
+
+METRICS = ("dsc", "iou", "sensitivity", "specificity", "accuracy", "kappa", "auc")
+
+
+def roix_overlap_metrics(counts):
+    """Eqs. 7-14 from host confusion counts (tp, fp, fn, tn) -> dict of METRICS (NaN: undefined)."""
+    c = (ctypes.c_uint64 * 4)(*[int(v) for v in counts])
+    out = (ctypes.c_double * 7)()
+    _check(load().roix_overlap_metrics(c, out), "roix_overlap_metrics")
+    return dict(zip(METRICS, list(out)))
 
 
 def scalars_size():

@@ -418,4 +418,78 @@ roix_status roix_greedy_quantize(const uint16_t *D, uint64_t n, double E, uint32
     return cuda(launch_greedy(D, n, E, qmax, Q, group_bits, ngroups, ws, (cudaStream_t)stream), "roix_greedy_quantize");
 }
 
+roix_status roix_decode_workspace(uint64_t n, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    *ws_bytes = decode_workspace_bytes(n);
+    return ROIX_OK;
+}
+
+roix_status roix_decode(const uint32_t *keep_bits, const void *codes, uint64_t ncodes, roix_dtype dtype, uint64_t n,
+                        roix_scalars *sc, void *xhat, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    if (!sc || !ws) return invalid("sc / ws is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if (ws_bytes < decode_workspace_bytes(n)) return invalid("workspace too small (see roix_decode_workspace)");
+    if (n && (!keep_bits || !aligned16(keep_bits) || !xhat || !aligned16(xhat)))
+        return invalid("keep_bits / xhat must be 16-byte aligned device pointers");
+    if (ncodes && (!codes || !aligned16(codes))) return invalid("codes must be a 16-byte aligned device pointer");
+    return cuda(launch_decode(keep_bits, codes, ncodes, (int)dtype, n, sc, xhat, ws, (cudaStream_t)stream),
+                "roix_decode");
+}
+
+roix_status roix_decode_spans_workspace(const roix_geom *g, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (g->nz * g->ny >= 0xffffffffull) return unsupported("more than 2^32-1 rows per slab");
+    if (g->nx >= 0xffffffffull) return unsupported("rows longer than 2^32-1 voxels");
+    *ws_bytes = decode_spans_workspace_bytes(*g);
+    return ROIX_OK;
+}
+
+roix_status roix_decode_spans(const roix_span *spans, uint64_t span_cap, const void *codes, uint64_t code_cap,
+                              const uint64_t *counts, roix_dtype dtype, const roix_geom *g, roix_scalars *sc,
+                              void *xhat, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    if (!sc || !counts || !ws) return invalid("sc / counts / ws is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    size_t need = 0;
+    roix_status s = roix_decode_spans_workspace(g, &need);
+    if (s != ROIX_OK) return s;
+    if (ws_bytes < need) return invalid("workspace too small (see roix_decode_spans_workspace)");
+    if (!xhat || !aligned16(xhat)) return invalid("xhat must be a 16-byte aligned device pointer");
+    if ((span_cap && !spans) || (code_cap && !codes)) return invalid("spans / codes is NULL");
+    return cuda(launch_decode_spans(spans, span_cap, codes, code_cap, counts, (int)dtype, *g, sc, xhat, ws,
+                                    (cudaStream_t)stream),
+                "roix_decode_spans");
+}
+
+roix_status roix_confusion(const uint32_t *pred_bits, const uint32_t *truth_bits, uint64_t n, uint64_t *counts,
+                           roix_stream_t stream) {
+    if (!counts) return invalid("counts is NULL");
+    if (n && (!pred_bits || !truth_bits || !aligned16(pred_bits) || !aligned16(truth_bits)))
+        return invalid("pred_bits / truth_bits must be 16-byte aligned device pointers");
+    return cuda(launch_confusion(pred_bits, truth_bits, n, counts, (cudaStream_t)stream), "roix_confusion");
+}
+
+static double ratio128(__int128 num, __int128 den) {
+    if (den == 0) return std::nan("");
+    return (double)((long double)num / (long double)den);
+}
+
+roix_status roix_overlap_metrics(const uint64_t *counts, double *out) {
+    if (!counts || !out) return invalid("counts / out is NULL");
+    const __int128 tp = counts[0], fp = counts[1], fn = counts[2], tn = counts[3];
+    const __int128 N = tp + fp + fn + tn;
+    out[0] = ratio128(2 * tp, 2 * tp + fp + fn);   // Eq. 7 DSC
+    out[1] = ratio128(tp, tp + fp + fn);           // Eq. 8 IoU
+    out[2] = ratio128(tp, tp + fn);                // Eq. 9 sensitivity
+    out[3] = ratio128(tn, tn + fp);                // Eq. 10 specificity
+    out[4] = ratio128(tp + tn, N);                 // Eq. 11 accuracy
+    // Eq. 12-13: kappa = ((tp+tn) - S/N) / (N - S/N) = (N(tp+tn) - S) / (N^2 - S), S = N f_c
+    const __int128 S = (tn + fn) * (tn + fp) + (fp + tp) * (fn + tp);
+    out[5] = N == 0 ? std::nan("") : ratio128(N * (tp + tn) - S, N * N - S);
+    // Eq. 14: auc = 1 - (fp/(fp+tn) + fn/(fn+tp))/2 = (2AB - fp B - fn A) / (2AB), A = fp+tn, B = fn+tp
+    const __int128 A = fp + tn, B = fn + tp;
+    out[6] = (A == 0 || B == 0) ? std::nan("") : ratio128(2 * A * B - fp * B - fn * A, 2 * A * B);
+    return ROIX_OK;
+}
+
 }  // extern "C"

@@ -77,3 +77,13 @@ cudaError_t launch_row_spans(const uint32_t *K, const void *x, int dtype, const 
 size_t greedy_workspace_bytes(uint64_t n);
 cudaError_t launch_greedy(const uint16_t *D, uint64_t n, double E, uint32_t qmax, uint16_t *Q, uint32_t *group_bits,
                           uint64_t *ngroups, void *ws, cudaStream_t st);
+
+size_t decode_workspace_bytes(uint64_t n);
+cudaError_t launch_decode(const uint32_t *K, const void *codes, uint64_t ncodes, int dtype, uint64_t n,
+                          roix_scalars *sc, void *xhat, void *ws, cudaStream_t st);
+size_t decode_spans_workspace_bytes(const roix_geom &g);
+cudaError_t launch_decode_spans(const roix_span *spans, uint64_t span_cap, const void *codes, uint64_t code_cap,
+                                const uint64_t *counts, int dtype, const roix_geom &g, roix_scalars *sc, void *xhat,
+                                void *ws, cudaStream_t st);
+cudaError_t launch_confusion(const uint32_t *pred, const uint32_t *truth, uint64_t n, uint64_t *counts,
+                             cudaStream_t st);

@@ -165,6 +165,60 @@ class Pipeline:
         rec = torch.stack([sp[:, 0], sp[:, 1] & 0xffffffff, sp[:, 1] >> 32], dim=1)
         return rec, self.span_codes[:nc]
 
+    # ------------------------------------------------------------------ NEXT-4 reconstruction / quality
+    def _stream(self, stream):
+        return ctypes.c_void_p((stream or torch.cuda.current_stream(self.device)).cuda_stream)
+
+    def decode(self, out=None, stream=None, from_spans=False):
+        """Reconstruct the last run's volume: x^ = code * s on the ROI, 0 elsewhere.
+        from_spans=False decodes the kept mask + dense code stream (roix_decode); True decodes the
+        paper's row spans (roix_decode_spans, needs spans=True): every column of a span's
+        [x_start, x_end) is restored, interior gaps included.  Returns out (shape, input dtype)."""
+        tdt = torch.int16 if self.dtype == "u16" else torch.float32
+        if out is None:
+            out = torch.empty(self.shape, dtype=tdt, device=self.device)
+        assert out.is_contiguous() and out.numel() == self.n and out.dtype in (tdt, torch.uint16)
+        st = self._stream(stream)
+        if from_spans:
+            if not self.spans_on:
+                raise ValueError("from_spans needs Pipeline(spans=True)")
+            if not hasattr(self, "dspan_ws"):
+                self.dspan_ws = torch.empty(max(1, L.roix_decode_spans_workspace(self.geom)), dtype=torch.uint8,
+                                            device=self.device)
+            Z, Y, _ = self.shape
+            L.roix_decode_spans(_ptr(self.span_rec), Z * Y, _ptr(self.span_codes), self.span_codes.numel(),
+                                _ptr(self.span_counts), self.cdtype, ctypes.byref(self.geom), _ptr(self.sc),
+                                _ptr(out), _ptr(self.dspan_ws), self.dspan_ws.numel(), st)
+        else:
+            if not hasattr(self, "dec_ws"):
+                self.dec_ws = torch.empty(max(1, L.roix_decode_workspace(self.n)), dtype=torch.uint8,
+                                          device=self.device)
+            L.roix_decode(_ptr(self.o), _ptr(self.codes), self.code_capacity, self.cdtype, self.n, _ptr(self.sc),
+                          _ptr(out), _ptr(self.dec_ws), self.dec_ws.numel(), st)
+        return out
+
+    def confusion(self, truth_words, stream=None, counts=None):
+        """Enqueue roix_confusion of the last run's K against a packed ground-truth mask (e.g. from
+        synth.generate(..., truth=...)); returns the device int64[4] (tp, fp, fn, tn)."""
+        if counts is None:
+            counts = torch.empty(4, dtype=torch.int64, device=self.device)
+        assert truth_words.numel() >= self.nwords
+        L.roix_confusion(_ptr(self.o), _ptr(truth_words), self.n, _ptr(counts), self._stream(stream))
+        return counts
+
+    def quality(self, truth_words):
+        """Eqs. 7-14 of the last run's K against ground truth, plus the spatial reduction
+        N / kept (Fig. 4) and, with spans=True, the paper's (rows * X) / sum(x_end - x_start)."""
+        c = tuple(int(v) for v in self.confusion(truth_words).cpu())
+        m = L.roix_overlap_metrics(c)
+        m["counts"] = dict(zip(("tp", "fp", "fn", "tn"), c))
+        kept = c[0] + c[1]
+        m["spatial_reduction_voxels"] = self.n / kept if kept else float("nan")
+        if self.spans_on:
+            area = int(self.span_counts[1].item())
+            m["spatial_reduction"] = self.n / area if area else float("nan")
+        return m
+
     def launches(self):
         k = 4 if self.spans_on else 0   # roix_row_spans: extent, 2 scans, write
         k += sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",

@@ -166,7 +166,8 @@ def rings(cfg):
 class _Params(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("seed", ctypes.c_uint32), ("gz", ctypes.c_uint64), ("ny", ctypes.c_uint64),
                 ("nx", ctypes.c_uint64), ("z0", ctypes.c_uint64), ("nz", ctypes.c_uint64), ("nobj", ctypes.c_int),
-                ("obj", ctypes.c_void_p), ("p", ctypes.c_float * 16), ("nring", ctypes.c_int), ("ring", ctypes.c_void_p)]
+                ("obj", ctypes.c_void_p), ("p", ctypes.c_float * 16), ("nring", ctypes.c_int), ("ring", ctypes.c_void_p),
+                ("truth", ctypes.c_void_p)]
 
 
 def build(force=False):
@@ -192,8 +193,20 @@ def _load():
 _MODE = {"C1": 1, "C5": 2, "C2": 3, "C3": 4, "C4": 5}
 
 
-def generate(cfg, z0=0, nz=None, out=None, device="cuda"):
-    """Generate planes [z0, z0+nz) of cfg's volume on the GPU into a torch tensor (nz, Y, X)."""
+def truth_words(cfg, nz=None):
+    """uint32 words of a packed ground-truth mask of nz planes (default: the whole volume)."""
+    Z, Y, X = cfg.shape
+    return ((Z if nz is None else nz) * Y * X + 31) // 32
+
+
+def generate(cfg, z0=0, nz=None, out=None, device="cuda", truth=None):
+    """Generate planes [z0, z0+nz) of cfg's volume on the GPU into a torch tensor (nz, Y, X).
+
+    truth (optional): an int32 device tensor of truth_words(cfg, nz) words, overwritten with the
+    slab's ground-truth region of interest, bit-packed like the product's masks (bit i % 32 of word
+    i // 32, LSB first, pad bits 0; i slab-local).  Ground truth = the voxel lies inside an object
+    (C1, C2, C5: the ellipsoids; painter's order does not matter, every object is foreground), inside
+    the sample's shadow (C3), or in the porous cylinder's solid matrix, pores excluded (C4)."""
     import torch
 
     Z, Y, X = cfg.shape
@@ -230,6 +243,10 @@ def generate(cfg, z0=0, nz=None, out=None, device="cuda"):
         p[5] = 40.0 * s + 1.0
     for k, v in enumerate(p):
         P.p[k] = v
+    if truth is not None:
+        assert truth.dtype == torch.int32 and truth.numel() >= truth_words(cfg, nz) and truth.is_contiguous()
+        truth.zero_()
+        P.truth = truth.data_ptr()
     stream = torch.cuda.current_stream(out.device).cuda_stream
     rc = _load().synth_generate(ctypes.byref(P), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream))
     if rc != 0:

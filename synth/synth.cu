@@ -30,6 +30,8 @@ struct synth_params {
     float p[16];          // mode parameters
     int nring;
     const float *ring;    // device: (R_j, w_j, sigma_j) triples
+    uint32_t *truth;      // device, optional (NULL): ground-truth ROI bits of the slab, packed like the
+                          // product's masks (bit i%32 of word i/32, slab-local i); the caller zeroes it
 };
 }
 
@@ -150,7 +152,10 @@ __global__ void synth_rows(synth_params P, void *out) {
     const int nl = nlist;
     const uint64_t rowbase = row * P.nx;                       // slab-local linear index of x = 0
     const uint64_t gbase = (z * P.ny + y) * P.nx;              // global linear index of x = 0
-    for (uint64_t x = threadIdx.x; x < P.nx; x += blockDim.x) {
+    for (uint64_t x0 = 0; x0 < P.nx; x0 += blockDim.x) {
+        const uint64_t x = x0 + threadIdx.x;
+        const bool valid = x < P.nx;
+        bool truth = false;   // ground truth: the voxel belongs to the phantom's region of interest
         const uint64_t gi = gbase + x;
         const float fx = (float)x;
         float z1, z2;
@@ -171,11 +176,13 @@ __global__ void synth_rows(synth_params P, void *out) {
         case 1: {  // C1: Poisson(lambda) ~ lambda + sqrt(lambda) z2, 12-bit
             float lam = hit < 0 ? P.p[0] + P.p[1] * z1 : P.obj[hit].mu + P.p[2] * z1;
             lam = fmaxf(lam, 0.0f);
-            ((uint16_t *)out)[rowbase + x] = clamp_u16(lam + sqrtf(lam) * z2, P.p[3]);
+            if (valid) ((uint16_t *)out)[rowbase + x] = clamp_u16(lam + sqrtf(lam) * z2, P.p[3]);
+            truth = hit >= 0;
         } break;
         case 2: {  // C5: Gaussian background / inclusions, 16-bit
             float v = (hit < 0 ? P.p[0] : P.obj[hit].mu) + P.p[1] * z1;
-            ((uint16_t *)out)[rowbase + x] = clamp_u16(v, 65535.0f);
+            if (valid) ((uint16_t *)out)[rowbase + x] = clamp_u16(v, 65535.0f);
+            truth = hit >= 0;
         } break;
         case 3: {  // C2: fp32 attenuation, textured objects, ring artefacts
             float v;
@@ -191,7 +198,8 @@ __global__ void synth_rows(synth_params P, void *out) {
             float ring = 0.0f;
             for (int j = 0; j < P.nring; j++)
                 if (fabsf(rho - P.ring[3 * j]) <= 0.5f * P.ring[3 * j + 1]) ring += P.ring[3 * j + 2];
-            ((float *)out)[rowbase + x] = v + P.p[5] * ring;
+            if (valid) ((float *)out)[rowbase + x] = v + P.p[5] * ring;
+            truth = hit >= 0;
         } break;
         case 4: {  // C3: detector frames, flat field with a rotating elliptical sample shadow
             float g = 0.97f + 0.06f * hash_unit((uint32_t)y, (uint32_t)x, 0x6a1u, P.seed);
@@ -201,15 +209,27 @@ __global__ void synth_rows(synth_params P, void *out) {
             float ry = (fy - P.p[4]) / P.p[3], rx = (fx - P.p[5]) / a;
             float r2 = ry * ry + rx * rx;
             float E = r2 < 1.0f ? g * (P.p[6] - P.p[7] * sqrtf(1.0f - r2)) : P.p[8] * g;
-            ((uint16_t *)out)[rowbase + x] = clamp_u16(E + sqrtf(E) * z1, P.p[9]);
+            if (valid) ((uint16_t *)out)[rowbase + x] = clamp_u16(E + sqrtf(E) * z1, P.p[9]);
+            truth = r2 < 1.0f;   // the sample's shadow
         } break;
         case 5: {  // C4: porous cylinder in air
             float dy = fy - P.p[0], dx = fx - P.p[1];
             float v;
-            if (dy * dy + dx * dx <= P.p[2] * P.p[2]) v = hit >= 0 ? 300.0f + 50.0f * z1 : 2500.0f + 100.0f * z1;
+            const bool cyl = dy * dy + dx * dx <= P.p[2] * P.p[2];
+            if (cyl) v = hit >= 0 ? 300.0f + 50.0f * z1 : 2500.0f + 100.0f * z1;
             else v = 200.0f + 40.0f * z1;
-            ((uint16_t *)out)[rowbase + x] = clamp_u16(v, 65535.0f);
+            if (valid) ((uint16_t *)out)[rowbase + x] = clamp_u16(v, 65535.0f);
+            truth = cyl && hit < 0;   // the solid matrix (pores and air are background)
         } break;
+        }
+        if (P.truth) {   // 32 consecutive voxels per warp: their bits land in at most two words
+            const unsigned b = __ballot_sync(0xffffffffu, valid && truth);
+            if ((threadIdx.x & 31u) == 0 && b) {
+                const uint64_t li = rowbase + x;
+                const uint32_t sh = (uint32_t)(li & 31);
+                atomicOr(&P.truth[li >> 5], b << sh);
+                if (sh && (b >> (32 - sh))) atomicOr(&P.truth[(li >> 5) + 1], b >> (32 - sh));
+            }
         }
     }
 }

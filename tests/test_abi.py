@@ -69,3 +69,27 @@ def test_sass_is_sm100a(lib):
 
     out = subprocess.run(["cuobjdump", "--list-elf", L.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_overlap_metrics_host_vs_oracle(lib):
+    """roix_overlap_metrics is host-only: Eqs. 7-14 against the oracle's exact rationals, the S:438-440
+    golden values and 128-bit intermediates (N^2 > 2^64)."""
+    import numpy as np
+
+    import oracle
+    from paper_2602_15917_b200 import _lib as L
+
+    m = L.roix_overlap_metrics((40, 10, 10, 40))    # S:438 (tp, fp, fn, tn)
+    assert abs(m["kappa"] - 0.6) <= 1e-12 and abs(m["auc"] - 0.8) <= 1e-12 and m["accuracy"] == 0.8
+    m = L.roix_overlap_metrics((5, 5, 5, 85))       # S:440
+    assert m["dsc"] == 0.5 and abs(m["iou"] - 1 / 3) <= 1e-16
+    rng = np.random.default_rng(1)
+    cases = [(0, 0, 0, 0), (0, 0, 0, 9), (9, 0, 0, 0), (3 << 33, 5 << 30, 7 << 29, 11 << 33),
+             (1 << 35, 1, 1, 1 << 35)] + [tuple(int(v) for v in rng.integers(0, 1 << int(rng.integers(1, 36)), 4))
+                                           for _ in range(300)]
+    for c in cases:
+        want = oracle.overlap_metrics(*c)
+        got = L.roix_overlap_metrics(c)
+        for k in L.METRICS:
+            np.testing.assert_allclose(got[k], want[k], rtol=2e-16, atol=0, equal_nan=True, err_msg="%s %s" % (k, c))
+    assert lib.roix_overlap_metrics(None, None) == L.ROIX_E_INVALID

@@ -172,3 +172,81 @@ def test_pipeline_row_spans_vs_oracle(cfg):
     np.testing.assert_array_equal(got.view(np.uint16) if cfg.dtype == "u16" else got, rc)
     # the spans cover K: at least as many codes as the kept voxels
     assert rc.size >= res.count
+
+
+# ------------------------------------------------------------------ NEXT-4 reconstruction and quality
+QCASES = [synth.CONFIGS["C1"], synth.CONFIGS["C2"], synth.scaled("C3", 0.25, frames=4), synth.scaled("C4", 0.0625),
+          synth.scaled("C5", 0.0625)]
+
+
+@pytest.mark.parametrize("cfg", QCASES, ids=lambda c: c.name)
+def test_pipeline_decode_vs_oracle(cfg):
+    """P:410-412 / S:359-367: both reconstructions of the pipeline's output (mask + code stream, and the
+    paper's row spans) against the oracle's decode of the oracle's own K / stream / spans."""
+    x = synth.generate(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se,
+                 min_size=cfg.min_size, polarity=cfg.polarity, spans=True)
+    res = p.run(x)
+    x_np = synth.to_numpy(x, cfg)
+    ref = oracle.pipeline(x_np, eb=cfg.eb or None, rel_eb=cfg.rel_eb or None, conn=cfg.conn, se=cfg.se,
+                          min_size=cfg.min_size, polarity=cfg.polarity)
+    npdt = np.uint16 if cfg.dtype == "u16" else np.float32
+    s = oracle.step(ref["eb"])
+    want = oracle.decode_mask(ref["K"], ref["stream"], s, npdt)
+    got = p.decode()
+    torch.cuda.synchronize()
+    assert p.scalars().err == 0
+    g = got.cpu().numpy()
+    g = g.view(np.uint16) if cfg.dtype == "u16" else g
+    np.testing.assert_array_equal(g, want)
+    # the error bound on the ROI (G-37): integer steps for u16: eb exactly; fp32: |x - code s| <= s/2
+    # exactly, plus half an ulp of x^ from the fp32 product
+    K = ref["K"].astype(bool)
+    d = np.abs(g.astype(np.float64) - x_np.astype(np.float64))[K]
+    if cfg.dtype == "u16":
+        assert d.size == 0 or d.max() <= ref["eb"]
+    else:
+        assert np.all(d <= s / 2 + np.spacing(np.abs(g[K])).astype(np.float64) / 2)
+    rs, rc = oracle.row_spans(x_np, ref["K"], ref["eb"])
+    want_sp = oracle.decode_spans(rs, rc, cfg.shape, s, npdt)
+    got_sp = p.decode(from_spans=True)
+    torch.cuda.synchronize()
+    assert p.scalars().err == 0
+    gs = got_sp.cpu().numpy()
+    np.testing.assert_array_equal(gs.view(np.uint16) if cfg.dtype == "u16" else gs, want_sp)
+    np.testing.assert_array_equal((gs.view(np.uint16) if cfg.dtype == "u16" else gs)[K], g[K])
+
+
+@pytest.mark.parametrize("cfg", QCASES, ids=lambda c: c.name)
+def test_quality_vs_ground_truth(cfg):
+    """the confusion of K against the generator's ground truth (roix_confusion) equals the
+    oracle's tally of the same masks; the segmentation is good on these phantoms (sanity, not a pin)."""
+    tw = torch.empty(synth.truth_words(cfg) + 4, dtype=torch.int32, device="cuda")
+    x = synth.generate(cfg, truth=tw)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se,
+                 min_size=cfg.min_size, polarity=cfg.polarity, spans=True)
+    res = p.run(x)
+    q = p.quality(tw)
+    K = words_to_mask(res.keep_bits, p.n)
+    T = words_to_mask(tw, p.n)
+    c = oracle.confusion(K, T)
+    assert tuple(q["counts"].values()) == c
+    want = oracle.overlap_metrics(*c)
+    for k in L.METRICS:
+        np.testing.assert_allclose(q[k], want[k], rtol=2e-16, equal_nan=True, err_msg=k)
+    assert q["dsc"] > 0.9, q
+    assert q["spatial_reduction_voxels"] == p.n / res.count
+    assert 1.0 <= q["spatial_reduction"] <= q["spatial_reduction_voxels"]
+
+
+def test_truth_slab_invariance():
+    cfg = synth.scaled("C4", 0.0625)
+    Z, Y, X = cfg.shape
+    tw = torch.empty(synth.truth_words(cfg), dtype=torch.int32, device="cuda")
+    synth.generate(cfg, truth=tw)
+    full = words_to_mask(tw, cfg.n).reshape(cfg.shape)
+    assert 0 < full.sum() < full.size
+    for z0, nz in ((0, 3), (5, 7), (Z - 2, 2)):
+        t = torch.empty(synth.truth_words(cfg, nz), dtype=torch.int32, device="cuda")
+        synth.generate(cfg, z0=z0, nz=nz, truth=t)
+        np.testing.assert_array_equal(words_to_mask(t, nz * Y * X).reshape(nz, Y, X), full[z0:z0 + nz])

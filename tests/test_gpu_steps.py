@@ -515,3 +515,185 @@ def test_greedy_8bit_spec_examples():
     for D, E, Q in [([10, 12, 20], 2, [11, 11, 20]), ([255, 251], 3, [253, 253]), ([0, 255], 200, [127, 127])]:
         q, g, ng = _greedy_gpu(np.array(D, np.uint16), E, 255)
         np.testing.assert_array_equal(q, Q)
+
+
+# ------------------------------------- NEXT-4 decode and confusion
+def _untouched(a, dt):
+    """the -1 fill of the output buffers (int16 -1 for u16, -1.0 for f32) is still there"""
+    return bool(np.all(a.view(np.int16) == -1)) if dt == "u16" else bool(np.all(a == -1.0))
+
+
+def _decode_gpu(K, codes_np, dt, eb, n=None, ncodes=None):
+    n = K.size if n is None else n
+    npdt = np.uint16 if dt == "u16" else np.float32
+    sc = new_sc(eb)
+    L.roix_resolve(ptr(sc), L.U16 if dt == "u16" else L.F32, 0.0, st())
+    kw = mask_to_words(K)
+    codes = dev(np.concatenate([codes_np, np.zeros(8, codes_np.dtype)]))
+    ncodes = codes_np.size if ncodes is None else ncodes
+    xh = torch.full((n + 16,), -1, dtype=torch.int16 if dt == "u16" else torch.float32, device="cuda")
+    wsb = L.roix_decode_workspace(n)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    L.roix_decode(ptr(kw), ptr(codes), ncodes, L.U16 if dt == "u16" else L.F32, n, ptr(sc), ptr(xh), ptr(ws), wsb,
+                  st())
+    s = read_sc(sc)
+    out = xh.cpu().numpy()
+    return s, (out.view(np.uint16) if dt == "u16" else out), npdt
+
+
+@pytest.mark.parametrize("n", [1, 33, 8192, 8193, 100003, 1 << 20])
+@pytest.mark.parametrize("dt", ["u16", "f32"])
+def test_decode_mask_vs_oracle(n, dt):
+    rng = np.random.default_rng(n * 3 + (dt == "f32"))
+    shape = (1, 1, n)
+    for K in (_blobby(rng, shape, 0.3, 40) if n > 64 else (rng.random(shape) < 0.5).astype(np.uint8),
+              (rng.random(shape) < 0.03).astype(np.uint8), np.zeros(shape, np.uint8), np.ones(shape, np.uint8)):
+        if dt == "u16":
+            x_np, eb = rng.integers(0, 65536, shape).astype(np.uint16), 2.0
+        else:
+            x_np, eb = rng.normal(0, 3, shape).astype(np.float32), 0.01
+        codes = oracle.extract(x_np, K, eb)
+        want = oracle.decode_mask(K, codes, oracle.step(eb), x_np.dtype).reshape(-1)
+        s, got, _ = _decode_gpu(K, codes, dt, eb)
+        assert s.err == 0
+        np.testing.assert_array_equal(got[:n], want)
+        assert _untouched(got[n:], dt)   # nothing past n
+
+
+@pytest.mark.parametrize("eb", [0.5, 0.75, 1.25, 3.0, 1000.0])
+def test_decode_u16_steps(eb):
+    """Integer and fractional steps (G-37) on every code value, through the mask form."""
+    codes = np.arange(65536, dtype=np.uint16)
+    K = np.ones((1, 1, 65536), np.uint8)
+    s, got, _ = _decode_gpu(K, codes, "u16", eb)
+    assert s.err == 0
+    np.testing.assert_array_equal(got[:65536], oracle.decode_value(codes, oracle.step(eb), np.uint16))
+
+
+def test_decode_f32_codes_extremes():
+    rng = np.random.default_rng(9)
+    codes = np.concatenate([rng.integers(-(1 << 23), 1 << 23, 50000), [0, 1, -1, 1 << 23, -(1 << 23)]]).astype(np.int32)
+    K = np.ones((1, 1, codes.size), np.uint8)
+    for eb in (1e-3, 0.37, 3e-7, 12.5):
+        s, got, _ = _decode_gpu(K, codes, "f32", eb)
+        assert s.err == 0
+        np.testing.assert_array_equal(got[:codes.size], oracle.decode_value(codes, oracle.step(eb), np.float32))
+
+
+def test_decode_capacity_error():
+    K = np.ones((1, 1, 1000), np.uint8)
+    codes = np.arange(1000, dtype=np.uint16)
+    s, got, _ = _decode_gpu(K, codes, "u16", 1.0, ncodes=999)
+    assert s.err & L.ERR_CAPACITY
+    assert np.all(got.view(np.int16) == -1)
+
+
+def _decode_spans_gpu(rec, codes_np, shape, dt, eb, z0=0, counts=None, span_cap=None, code_cap=None):
+    Z, Y, X = shape
+    g = L.Geom(Z, Y, X, z0, z0 + Z)
+    sc = new_sc(eb)
+    L.roix_resolve(ptr(sc), L.U16 if dt == "u16" else L.F32, 0.0, st())
+    m = len(rec)
+    sp = np.zeros((max(m, 1), 2), np.int64)
+    if m:
+        sp[:m, 0] = rec[:, 0]
+        sp[:m, 1] = rec[:, 1] | (rec[:, 2] << 32)
+    spans = torch.from_numpy(sp.reshape(-1).copy()).cuda()
+    codes = dev(np.concatenate([codes_np, np.zeros(8, codes_np.dtype)]))
+    cnt = torch.tensor(counts if counts is not None else [m, codes_np.size], dtype=torch.int64, device="cuda")
+    xh = torch.full((Z * Y * X + 16,), -1, dtype=torch.int16 if dt == "u16" else torch.float32, device="cuda")
+    wsb = L.roix_decode_spans_workspace(g)
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    L.roix_decode_spans(ptr(spans), m if span_cap is None else span_cap, ptr(codes),
+                        codes_np.size if code_cap is None else code_cap, ptr(cnt), L.U16 if dt == "u16" else L.F32,
+                        ctypes.byref(g), ptr(sc), ptr(xh), ptr(ws), wsb, st())
+    s = read_sc(sc)
+    out = xh.cpu().numpy()
+    return s, (out.view(np.uint16) if dt == "u16" else out)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (2, 3, 5), (3, 7, 33), (4, 9, 64), (2, 5, 1000), (3, 40, 512),
+                                   (2, 3, 2100)])
+@pytest.mark.parametrize("dt", ["u16", "f32"])
+def test_decode_spans_vs_oracle(shape, dt):
+    """roix_row_spans -> roix_decode_spans on the GPU against the oracle's row_spans -> decode_spans."""
+    rng = np.random.default_rng(abs(hash((shape, dt, "dspans"))) % 2 ** 32)
+    n = int(np.prod(shape))
+    for K in (_blobby(rng, shape, 0.3, 29), (rng.random(shape) < 0.05).astype(np.uint8), np.zeros(shape, np.uint8),
+              np.ones(shape, np.uint8)):
+        if dt == "u16":
+            x_np, eb = rng.integers(0, 65536, shape).astype(np.uint16), 2.0
+        else:
+            x_np, eb = rng.normal(0, 3, shape).astype(np.float32), 0.01
+        rs, rc = oracle.row_spans(x_np, K, eb)
+        want = oracle.decode_spans(rs, rc, shape, oracle.step(eb), x_np.dtype).reshape(-1)
+        s0, rec, cd, ns, nc, _ = _spans_gpu(x_np, K, eb)
+        assert s0.err == 0
+        s, got = _decode_spans_gpu(rec, cd[:nc], shape, dt, eb)
+        assert s.err == 0
+        np.testing.assert_array_equal(got[:n], want)
+        assert _untouched(got[n:], dt)
+
+
+def test_decode_spans_lossless_slab_and_format_errors():
+    rng = np.random.default_rng(21)
+    shape = (3, 6, 40)
+    x_np = rng.integers(0, 60000, shape).astype(np.uint16)
+    K = (rng.random(shape) < 0.2).astype(np.uint8)
+    rs, rc = oracle.row_spans(x_np, K, 0.5)   # s = 1: lossless on the span columns (AC3 analogue, S:564)
+    rec = rs.copy()
+    rec[:, 0] += 4 * shape[1]                  # a slab at global plane 4: records carry global rows
+    s, got = _decode_spans_gpu(rec, rc, shape, "u16", 0.5, z0=4)
+    assert s.err == 0
+    got = got[:x_np.size].reshape(-1, shape[2])
+    for i, xs, xe in rs:
+        np.testing.assert_array_equal(got[i, xs:xe], x_np.reshape(-1, shape[2])[i, xs:xe])
+    # format errors: nothing decoded
+    bad = [rec[::-1].copy(), rec.copy(), rec.copy(), rec.copy()]
+    bad[1][0, 2] = shape[2] + 1                # x_end past the row
+    bad[2][0, 1] = bad[2][0, 2]                # empty record
+    bad[3][0, 0] = 0                           # row outside the slab
+    for b in bad:
+        s, got = _decode_spans_gpu(b, rc, shape, "u16", 0.5, z0=4)
+        assert s.err & L.ERR_FORMAT
+        assert np.all(got.view(np.int16) == -1)
+    s, got = _decode_spans_gpu(rec, rc, shape, "u16", 0.5, z0=4, counts=[len(rec), rc.size + 1])
+    assert s.err & L.ERR_FORMAT                # section lengths disagree with counts[1]
+    s, got = _decode_spans_gpu(rec, rc, shape, "u16", 0.5, z0=4, code_cap=rc.size - 1)
+    assert s.err & L.ERR_CAPACITY
+    s, got = _decode_spans_gpu(rec, rc, shape, "u16", 0.5, z0=4, span_cap=len(rec) - 1)
+    assert s.err & L.ERR_CAPACITY
+
+
+def _confusion_gpu(pred, truth):
+    n = pred.size
+    c = torch.full((4,), -1, dtype=torch.int64, device="cuda")
+    pw, tw = mask_to_words(pred), mask_to_words(truth)    # keep both alive across the call
+    L.roix_confusion(ptr(pw), ptr(tw), n, ptr(c), st())
+    torch.cuda.synchronize()
+    return tuple(int(v) for v in c.cpu().numpy())
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 32, 127, 128, 129, 100003, 1 << 22])
+def test_confusion_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    for p, t in ((0.5, 0.5), (0.02, 0.9), (1.0, 0.0)):
+        pred = (rng.random(n) < p).astype(np.uint8)
+        truth = (rng.random(n) < t).astype(np.uint8)
+        got = _confusion_gpu(pred, truth)
+        assert got == oracle.confusion(pred, truth)
+        m = L.roix_overlap_metrics(got)
+        want = oracle.overlap_metrics(*got)
+        for k in L.METRICS:
+            np.testing.assert_allclose(m[k], want[k], rtol=1e-15, atol=0, equal_nan=True, err_msg=k)
+
+
+def test_confusion_ignores_pad_bits():
+    n = 70
+    w = torch.full((8,), -1, dtype=torch.int32, device="cuda")   # every bit set, pad bits too
+    z = torch.zeros(8, dtype=torch.int32, device="cuda")
+    c = torch.zeros(4, dtype=torch.int64, device="cuda")
+    L.roix_confusion(ptr(w), ptr(z), n, ptr(c), st())
+    torch.cuda.synchronize()
+    assert tuple(c.cpu().numpy()) == (0, n, 0, 0)
+
