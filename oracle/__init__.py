@@ -24,7 +24,7 @@ import subprocess
 
 import numpy as np
 
-from .otsu import Degenerate, otsu2  # noqa: F401
+from .otsu import Degenerate, multi_otsu, otsu2  # noqa: F401
 from .reconstruct import (confusion, decode_mask, decode_spans, decode_value, overlap_metrics,  # noqa: F401
                           spatial_reduction, step)
 
@@ -272,9 +272,11 @@ def pack_bits(mask):
 
 
 # ---------------------------------------------------------------- the composed hot path
-def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0):
+def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, classes=2):
     """The whole path on one volume x[Z][Y][X] (uint16 or float32).  Returns a dict of every
-    intermediate the CUDA path exposes.  Raises Degenerate when Otsu has no valid threshold."""
+    intermediate the CUDA path exposes.  Raises Degenerate when Otsu has no valid threshold.
+    classes = 3 (NEXT-3): multi-Otsu; the ROI is norm8 > the lowest threshold (HIGH) or
+    norm8 <= the highest (LOW, reading G-39)."""
     x = np.ascontiguousarray(x)
     assert x.ndim == 3
     out = {}
@@ -291,7 +293,13 @@ def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0):
         imax = imax_u16(h)
         h8 = hist8_from_u16(h, imax)
     out["eb"], out["i_max"], out["h8"] = float(np.float32(eb)), imax, h8
-    t8 = otsu2(h8)
+    if classes == 2:
+        t8 = otsu2(h8)
+        out["thresholds"] = (t8,)
+    else:
+        ts = multi_otsu(h8, classes)
+        out["thresholds"] = ts
+        t8 = ts[0] if polarity == 0 else ts[-1]
     out["t8"] = t8
     m = binarize(x, imax, t8, polarity)
     o = opening(m, se)

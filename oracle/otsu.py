@@ -47,3 +47,47 @@ def otsu2(h8):
     if best_t is None:
         raise Degenerate("fewer than two populated histogram bins")
     return best_t
+
+
+# ----------------------------------------------------------------------------- NEXT-3: multi-Otsu
+def multi_otsu(h8, classes):
+    """S:167-175 multi_otsu: the ascending tuple of classes - 1 thresholds in 0..254 maximising the
+    between-class variance over every tuple whose classes are all non-empty; ties: the
+    lexicographically smallest tuple.  Raises Degenerate with fewer than `classes` populated bins.
+
+    Exhaustive over all tuples, as S:565 (AC4) states it; the class sums use prefix sums (a plain
+    library step) so that k = 3 (32 385 tuples) runs in about a second."""
+    h8 = [int(v) for v in h8]
+    assert len(h8) == 256 and classes in (2, 3)
+    if sum(1 for v in h8 if v) < classes:
+        raise Degenerate("fewer populated bins than classes (S:171)")
+    N = sum(h8)
+    S = sum(k * h8[k] for k in range(256))
+    cn = [0] * 257
+    cs = [0] * 257
+    for k in range(256):
+        cn[k + 1] = cn[k] + h8[k]
+        cs[k + 1] = cs[k] + k * h8[k]
+    mu_T = Fraction(S, N)
+
+    def var(ts):
+        bounds = [-1] + list(ts) + [255]
+        total = Fraction(0)
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            n = cn[b + 1] - cn[a + 1]
+            if n == 0:
+                return None
+            s = cs[b + 1] - cs[a + 1]
+            total += Fraction(n, N) * (Fraction(s, n) - mu_T) ** 2
+        return total
+
+    tuples = ((t,) for t in range(255)) if classes == 2 else \
+        ((t1, t2) for t1 in range(254) for t2 in range(t1 + 1, 255))
+    best, best_t = None, None
+    for ts in tuples:                       # ascending lexicographic order: strict > keeps the smallest
+        v = var(ts)
+        if v is not None and (best is None or v > best):
+            best, best_t = v, ts
+    if best_t is None:
+        raise Degenerate("no tuple with all classes non-empty")
+    return best_t
