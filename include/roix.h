@@ -76,7 +76,7 @@ typedef struct roix_scalars {
     float s_inv;          /* fl32(1/s): fast-path reciprocal, always followed by an exact check   */
     uint32_t s_int;       /* s when s is an integer in [1, 65535], else 0 (u16 integer fast path) */
     uint32_t s_magic;     /* ceil(2^32 / s_int) for s_int >= 2: exact floor(v / s_int), v < 2^16 */
-    uint32_t reserved0;
+    uint32_t t8_all;      /* a3: every threshold, ascending, one per byte (k = 2: t8; k = 3: t1 | t2 << 8) */
     float i_max;          /* Eq. 1 I_max: global max, 1 when <= 0 (G-8)                  */
     uint32_t t8;          /* a3: Otsu threshold on the 8-bit normalised intensity                */
     uint32_t thr_u16;     /* a4 raw form: first u16 value v with norm8(v) > t8                   */
@@ -154,6 +154,18 @@ roix_status roix_histogram(const void *x, roix_dtype dtype, uint64_t n, roix_sca
  */
 roix_status roix_threshold(const uint64_t *hist, uint32_t nbins, roix_dtype dtype, roix_polarity polarity,
                            roix_scalars *sc, roix_stream_t stream);
+
+/*
+ * NEXT-3 multi-Otsu ("multi-Otsu adaptive thresholding", AC4 S:565).
+ * classes = 2: exactly roix_threshold.  classes = 3: the thresholds t1 < t2 maximising the
+ * between-class variance sum_k w_k (mu_k - mu_T)^2 over every tuple with three non-empty classes,
+ * the lexicographically smallest on ties (exact: 448-bit integer compares); sc->t8_all = t1 | t2 << 8
+ * and the ROI threshold sc->t8 = t1 for HIGH (ROI = everything above the lowest threshold) or
+ * t2 for LOW (ROI = everything at or below the highest, G-39); thr_u16 / thr_f32 follow
+ * t8.  Fewer than `classes` populated norm8 bins sets ROIX_ERR_DEGENERATE.
+ */
+roix_status roix_threshold_multi(const uint64_t *hist, uint32_t nbins, roix_dtype dtype, roix_polarity polarity,
+                                 uint32_t classes, roix_scalars *sc, roix_stream_t stream);
 
 /*
  * a4+a5 BINARISE + OPEN (Eq. 2; G-11).  m = [norm8(x) > t8] (HIGH) or [<= t8] (LOW), evaluated as

@@ -21,7 +21,7 @@ class Scalars(ctypes.Structure):
     _fields_ = [("err", ctypes.c_uint32), ("min_ord", ctypes.c_uint32), ("max_ord", ctypes.c_uint32),
                 ("polarity", ctypes.c_uint32), ("eb", ctypes.c_float), ("s", ctypes.c_float),
                 ("s_inv", ctypes.c_float), ("s_int", ctypes.c_uint32), ("s_magic", ctypes.c_uint32),
-                ("reserved0", ctypes.c_uint32), ("i_max", ctypes.c_float), ("t8", ctypes.c_uint32),
+                ("t8_all", ctypes.c_uint32), ("i_max", ctypes.c_float), ("t8", ctypes.c_uint32),
                 ("thr_u16", ctypes.c_uint32), ("thr_f32", ctypes.c_float), ("count", ctypes.c_uint64),
                 ("n_components", ctypes.c_uint64), ("n_kept", ctypes.c_uint64), ("n_runs", ctypes.c_uint64),
                 ("spec_lo", ctypes.c_uint32), ("spec_hi", ctypes.c_uint32), ("spec_state", ctypes.c_uint32),
@@ -88,6 +88,7 @@ _SIGS = {
     "roix_greedy_quantize": (_i32, [_vp, _u64, _f64, _u32, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "roix_extract_runs": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _u64, _vp,
                                  _vp]),
+    "roix_threshold_multi": (_i32, [_vp, _u32, _i32, _i32, _u32, _vp, _vp]),
     "roix_decode_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_decode": (_i32, [_vp, _vp, _u64, _i32, _u64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "roix_decode_spans_workspace": (_i32, [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_size_t)]),
@@ -143,6 +144,7 @@ roix_extract = _wrap("roix_extract")
 roix_extract_runs = _wrap("roix_extract_runs")
 roix_row_spans = _wrap("roix_row_spans")
 roix_greedy_quantize = _wrap("roix_greedy_quantize")
+roix_threshold_multi = _wrap("roix_threshold_multi")
 roix_decode = _wrap("roix_decode")
 roix_decode_spans = _wrap("roix_decode_spans")
 roix_confusion = _wrap("roix_confusion")

@@ -118,6 +118,18 @@ roix_status roix_threshold(const uint64_t *hist, uint32_t nbins, roix_dtype dtyp
     return cuda(launch_threshold(hist, (int)dtype, (int)polarity, sc, (cudaStream_t)stream), "roix_threshold");
 }
 
+roix_status roix_threshold_multi(const uint64_t *hist, uint32_t nbins, roix_dtype dtype, roix_polarity polarity,
+                                 uint32_t classes, roix_scalars *sc, roix_stream_t stream) {
+    if (classes != 2 && classes != 3) return unsupported("classes must be 2 or 3");
+    if (!sc || !hist) return invalid("sc / hist is NULL");
+    if (!dtype_ok(dtype)) return invalid("dtype");
+    if ((dtype == ROIX_U16 && nbins != 65536) || (dtype == ROIX_F32 && nbins != 256))
+        return invalid("nbins must be 65536 (u16) or 256 (fp32)");
+    if (polarity != ROIX_POL_HIGH && polarity != ROIX_POL_LOW) return invalid("polarity");
+    return cuda(launch_threshold(hist, (int)dtype, (int)polarity, sc, (cudaStream_t)stream, (int)classes),
+                "roix_threshold_multi");
+}
+
 static roix_status check_halos(const roix_geom *g, uint32_t se, const uint32_t *lo, const uint32_t *hi) {
     if (se != 6) return ROIX_OK;
     if (g->z0 > 0 && !lo) return invalid("halo_lo required: the slab does not start at the volume face");

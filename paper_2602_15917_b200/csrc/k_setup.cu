@@ -19,7 +19,7 @@ __global__ void k_scalars_init(roix_scalars *sc, float eb) {
         sc->s_inv = 0.0f;
         sc->s_int = 0;
         sc->s_magic = 0;
-        sc->reserved0 = 0;
+        sc->t8_all = 0;
         sc->i_max = 1.0f;
         sc->t8 = 0;
         sc->thr_u16 = 0;

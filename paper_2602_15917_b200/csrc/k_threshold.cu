@@ -5,6 +5,13 @@
 // D = N s0 - n0 S (n0, s0: count and intensity sum of bins <= t; N, S: totals).  Candidates are
 // compared as D_a^2 n0_b n1_b  vs  D_b^2 n0_a n1_a  in 384-bit integers, the smallest t winning ties
 // (S:170), so the result is exact for any histogram with N < 2^39.
+//
+// NEXT-3 multi-Otsu, k = 3: thresholds t1 < t2 maximise
+// sum_k w_k (mu_k - mu_T)^2 = (sum_k s_k^2 / n_k - S^2 / N) / N over the 32 385 tuples with non-empty
+// classes; ties go to the lexicographically smallest (t1, t2).  Every thread scores its tuples in
+// binary64 (relative error < 1e-15: three positive terms), the block keeps those within 1e-12 of the
+// best approximate score, and compares them exactly: V = num / den with num = s1^2 n2 n3 + s2^2 n1 n3 +
+// s3^2 n1 n2 (< 2^176) and den = n1 n2 n3 (< 2^117), cross-multiplied in 448-bit integers.
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -72,10 +79,139 @@ __device__ bool better(const Cand &a, const Cand &b) {
     return c > 0 || (c == 0 && a.t < b.t);
 }
 
+// r[0 .. na+nb) = a[0 .. na) * b[0 .. nb)
+__device__ void mulw(const uint64_t *a, int na, const uint64_t *b, int nb, uint64_t *r) {
+    for (int k = 0; k < na + nb; k++) r[k] = 0;
+    for (int i = 0; i < na; i++)
+        for (int j = 0; j < nb; j++) mul_add(a[i], b[j], r, i + j, na + nb);
+}
+
+__device__ void addw(uint64_t *acc, const uint64_t *b, int n) {
+    uint64_t c = 0;
+    for (int k = 0; k < n; k++) {
+        const uint64_t t = acc[k] + c;
+        const uint64_t c1 = t < c;
+        acc[k] = t + b[k];
+        c = c1 | (acc[k] < b[k]);
+    }
+}
+
+struct Cand3 {
+    uint64_t s[3], n[3];   // class intensity sums and counts
+    int key;               // t1 * 256 + t2 (lexicographic order), -1 = invalid
+};
+
+// num = s1^2 n2 n3 + s2^2 n1 n3 + s3^2 n1 n2 (4 limbs), den = n1 n2 n3 (3 limbs)
+__device__ void frac3(const Cand3 &c, uint64_t num[4], uint64_t den[3]) {
+    for (int k = 0; k < 4; k++) num[k] = 0;
+    for (int a = 0; a < 3; a++) {
+        const int b = (a + 1) % 3, d = (a + 2) % 3;
+        uint64_t sq[2], nn[2], t[4];
+        mulw(&c.s[a], 1, &c.s[a], 1, sq);
+        mulw(&c.n[b], 1, &c.n[d], 1, nn);
+        mulw(sq, 2, nn, 2, t);
+        addw(num, t, 4);
+    }
+    uint64_t n12[2];
+    mulw(&c.n[0], 1, &c.n[1], 1, n12);
+    mulw(n12, 2, &c.n[2], 1, den);
+}
+
+__device__ bool better3(const Cand3 &a, const Cand3 &b) {
+    if (a.key < 0) return false;
+    if (b.key < 0) return true;
+    uint64_t na[4], da[3], nb[4], db[3], l[7], r[7];
+    frac3(a, na, da);
+    frac3(b, nb, db);
+    mulw(na, 4, db, 3, l);
+    mulw(nb, 4, da, 3, r);
+    for (int k = 6; k >= 0; k--)
+        if (l[k] != r[k]) return l[k] > r[k];
+    return a.key < b.key;
+}
+
+__device__ __forceinline__ Cand3 shfl_cand3(const Cand3 &c, int src) {
+    Cand3 o;
+    for (int k = 0; k < 3; k++) {
+        o.s[k] = __shfl_sync(FULL, c.s[k], src);
+        o.n[k] = __shfl_sync(FULL, c.n[k], src);
+    }
+    o.key = __shfl_sync(FULL, c.key, src);
+    return o;
+}
+
+// 3-class search over the inclusive prefix sums sn / ss of the norm8 histogram (totals N, S); every
+// thread of the 1024-thread block calls it.  Returns (t1, t2) or (-1, -1) if fewer than three bins
+// are populated.
+__device__ void otsu3_search(const uint64_t *sn, const uint64_t *ss, uint64_t N, uint64_t S, int *t1_out,
+                             int *t2_out) {
+    __shared__ double s_v[32];
+    __shared__ Cand3 s_c[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    auto classes = [&](int p, Cand3 &c) -> bool {
+        const int t1 = p >> 8, t2 = p & 255;
+        if (t1 >= t2 || t2 > 254) return false;
+        const uint64_t n1 = sn[t1], n12 = sn[t2];
+        if (n1 == 0 || n12 == n1 || n12 == N) return false;
+        c.n[0] = n1;
+        c.n[1] = n12 - n1;
+        c.n[2] = N - n12;
+        c.s[0] = ss[t1];
+        c.s[1] = ss[t2] - ss[t1];
+        c.s[2] = S - ss[t2];
+        c.key = p;
+        return true;
+    };
+    auto approx = [](const Cand3 &c) {
+        double v = 0;
+        for (int k = 0; k < 3; k++) v += (double)c.s[k] * (double)c.s[k] / (double)c.n[k];
+        return v;
+    };
+    double vmax = -1.0;
+    for (int p = tid; p < 65536; p += 1024) {
+        Cand3 c;
+        if (classes(p, c)) vmax = fmax(vmax, approx(c));
+    }
+    for (int d = 16; d > 0; d >>= 1) vmax = fmax(vmax, __shfl_xor_sync(FULL, vmax, d));
+    if (lane == 0) s_v[warp] = vmax;
+    __syncthreads();
+    vmax = s_v[0];
+    for (int k = 1; k < 32; k++) vmax = fmax(vmax, s_v[k]);
+    const double thr = vmax - vmax * 1e-12;
+    Cand3 best;
+    best.key = -1;
+    for (int k = 0; k < 3; k++) best.s[k] = best.n[k] = 0;
+    if (vmax >= 0) {
+        for (int p = tid; p < 65536; p += 1024) {   // increasing p = lexicographic: strict `better` keeps the first
+            Cand3 c;
+            if (classes(p, c) && approx(c) >= thr && better3(c, best)) best = c;
+        }
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+        const Cand3 o = shfl_cand3(best, lane ^ d);
+        if (better3(o, best)) best = o;
+    }
+    if (lane == 0) s_c[warp] = best;
+    __syncthreads();
+    if (warp == 0) {
+        best = s_c[lane];
+        for (int d = 16; d > 0; d >>= 1) {
+            const Cand3 o = shfl_cand3(best, lane ^ d);
+            if (better3(o, best)) best = o;
+        }
+    }
+    if (tid == 0) s_c[0] = best;
+    __syncthreads();
+    *t1_out = s_c[0].key < 0 ? -1 : s_c[0].key >> 8;
+    *t2_out = s_c[0].key < 0 ? -1 : s_c[0].key & 255;
+    __syncthreads();
+}
+
 // Exact 2-class Otsu over a 1024-thread block.  u16: hist has 65536 raw bins (I_max and the norm8
 // fold are derived here); fp32: hist is the 256-bin norm8 histogram.  Returns t8 (-1 if fewer than
 // two populated bins) and I_max (u16).  Every thread of the block must call it.
-__device__ void otsu_block(const uint64_t *__restrict__ hist, int dtype, uint32_t *imax_out, int *t8_out) {
+__device__ void otsu_block(const uint64_t *__restrict__ hist, int dtype, uint32_t *imax_out, int *t8_out,
+                           int classes = 2, int *t8_hi_out = nullptr) {
     __shared__ unsigned long long h8[256];
     __shared__ uint64_t scan_n[256], scan_s[256];
     __shared__ Cand cand[256];
@@ -126,6 +262,14 @@ __device__ void otsu_block(const uint64_t *__restrict__ hist, int dtype, uint32_
         __syncthreads();
     }
     const uint64_t N = scan_n[255], S = scan_s[255];
+    if (classes == 3) {
+        int t1, t2;
+        otsu3_search(scan_n, scan_s, N, S, &t1, &t2);
+        *imax_out = imax;
+        *t8_out = t1;
+        *t8_hi_out = t2;
+        return;
+    }
     Cand c;
     c.t = -1;
     c.d0 = c.d1 = c.n0 = c.n1 = 0;
@@ -157,19 +301,24 @@ __device__ __forceinline__ uint32_t thr_u16_of(uint32_t imax, int t8) {
 }
 
 __global__ void __launch_bounds__(1024) k_threshold(const uint64_t *__restrict__ hist, int dtype, int polarity,
-                                                     roix_scalars *sc) {
+                                                     int classes, roix_scalars *sc) {
     if (get_err(sc)) return;
     uint32_t imax;
-    int t8;
-    otsu_block(hist, dtype, &imax, &t8);
+    int t8, t8_hi = -1;
+    otsu_block(hist, dtype, &imax, &t8, classes, &t8_hi);
     if (threadIdx.x == 0) {
         sc->polarity = (uint32_t)polarity;
         if (dtype == ROIX_U16) sc->i_max = (float)imax;
         if (t8 < 0) {
             set_err(sc, ROIX_ERR_DEGENERATE);
             sc->t8 = 0;
+            sc->t8_all = 0;
             return;
         }
+        // the ROI threshold: the only one (k = 2); k = 3: the lowest for HIGH, the highest for
+        // LOW (G-39)
+        sc->t8_all = classes == 3 ? (uint32_t)t8 | ((uint32_t)t8_hi << 8) : (uint32_t)t8;
+        if (classes == 3 && polarity == ROIX_POL_LOW) t8 = t8_hi;
         sc->t8 = (uint32_t)t8;
         if (dtype == ROIX_U16) sc->thr_u16 = thr_u16_of(imax, t8);
         else sc->thr_f32 = sc->edges[t8 + 1];
@@ -208,8 +357,9 @@ __global__ void __launch_bounds__(1024) k_spec(const uint64_t *__restrict__ shis
 
 }  // namespace roix
 
-cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st) {
-    roix::k_threshold<<<1, 1024, 0, st>>>(hist, dtype, polarity, sc);
+cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st,
+                             int classes) {
+    roix::k_threshold<<<1, 1024, 0, st>>>(hist, dtype, polarity, classes, sc);
     return cudaGetLastError();
 }
 

@@ -46,7 +46,7 @@ class Pipeline:
 
     def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
                  run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="mask",
-                 spans=False):
+                 spans=False, classes=2):
         L.load()
         self.shape = tuple(int(v) for v in shape)
         Z, Y, X = self.shape
@@ -57,6 +57,13 @@ class Pipeline:
             raise ValueError("give exactly one of eb (absolute) and rel_eb (relative, fp32)")
         self.eb, self.rel_eb = float(eb), float(rel_eb)
         self.conn, self.se, self.min_size, self.polarity = int(conn), int(se), int(min_size), int(polarity)
+        # a3 class count: 2 (Otsu, G-9) or 3 (multi-Otsu, NEXT-3: ROI above the lowest threshold / at or
+        # below the highest for LOW, G-39)
+        if classes not in (2, 3):
+            raise ValueError("classes must be 2 or 3")
+        if classes == 3 and fused:
+            raise ValueError("the fused speculative histogram+binarisation supports classes = 2 only")
+        self.classes = int(classes)
         self.device = torch.device(device or "cuda")
         dev = self.device
         self.geom = L.Geom(Z, Y, X, 0, Z)
@@ -131,7 +138,7 @@ class Pipeline:
         else:
             L.roix_histogram(xp, self.cdtype, n, sc, _ptr(self.hist), self.nbins, st)
         mark("histogram")
-        L.roix_threshold(_ptr(self.hist), self.nbins, self.cdtype, self.polarity, sc, st)
+        L.roix_threshold_multi(_ptr(self.hist), self.nbins, self.cdtype, self.polarity, self.classes, sc, st)
         mark("threshold")
         morph = L.roix_morph_prebinarized if self.fused else L.roix_morph
         morph(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o), _ptr(self.row_runs),

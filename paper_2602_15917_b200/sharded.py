@@ -89,7 +89,7 @@ def slab_program(S, x, stream=None, mark=None):
         L.roix_histogram(xp, S.cdtype, n, sc, _ptr(S.hist), S.nbins, st)
     yield ("sum", S.hist)                                         # X1
     mark("histogram")
-    L.roix_threshold(_ptr(S.hist), S.nbins, S.cdtype, S.polarity, sc, st)
+    L.roix_threshold_multi(_ptr(S.hist), S.nbins, S.cdtype, S.polarity, S.classes, sc, st)
     mark("threshold")
     halo_lo = halo_hi = None
     if S.se == 6 and G > 1:

@@ -30,10 +30,10 @@ CASES = [synth.CONFIGS["C1"], synth.CONFIGS["C2"], synth.scaled("C3", 0.25, fram
          synth.scaled("C4", 0.125), synth.scaled("C5", 0.125), synth.scaled("C4", 0.0625), synth.scaled("C1", 0.37)]
 
 
-def _check(cfg, p, x, res):
+def _check(cfg, p, x, res, classes=2):
     x_np = synth.to_numpy(x, cfg)
     ref = oracle.pipeline(x_np, eb=cfg.eb or None, rel_eb=cfg.rel_eb or None, conn=cfg.conn, se=cfg.se,
-                          min_size=cfg.min_size, polarity=cfg.polarity)
+                          min_size=cfg.min_size, polarity=cfg.polarity, classes=classes)
     s = res.scalars
     assert s.err == 0
     assert res.t8 == ref["t8"] and res.i_max == ref["i_max"] and res.eb == ref["eb"]
@@ -250,3 +250,39 @@ def test_truth_slab_invariance():
         t = torch.empty(synth.truth_words(cfg, nz), dtype=torch.int32, device="cuda")
         synth.generate(cfg, z0=z0, nz=nz, truth=t)
         np.testing.assert_array_equal(words_to_mask(t, nz * Y * X).reshape(nz, Y, X), full[z0:z0 + nz])
+
+
+# ------------------------------------------------------------------ NEXT-3 multi-Otsu in the pipeline
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C1"], synth.CONFIGS["C2"], synth.scaled("C3", 0.25, frames=4),
+                                 synth.scaled("C5", 0.0625)], ids=lambda c: c.name)
+def test_pipeline_multi_otsu_vs_oracle(cfg):
+    """classes = 3 end to end: every intermediate equals the oracle's (thresholds (t1, t2), K, table,
+    stream); C2 is the multi-modal phantom the 2-class split under-segments (DESIGN.md NEXT-4)."""
+    x = synth.generate(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se,
+                 min_size=cfg.min_size, polarity=cfg.polarity, classes=3)
+    res = p.run(x)
+    ref = _check(cfg, p, x, res, classes=3)
+    s = res.scalars
+    assert (s.t8_all & 255, s.t8_all >> 8) == ref["thresholds"]
+
+
+def test_sharded_multi_otsu_g_invariant():
+    from paper_2602_15917_b200.sharded import run_simulated
+
+    cfg = synth.scaled("C5", 0.0625)
+    x = synth.generate(cfg)
+    kw = dict(eb=cfg.eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, classes=3)
+    one = Pipeline(cfg.shape, cfg.dtype, **kw).run(x)
+    for G in (2, 4):
+        states = run_simulated(x, G, **kw)
+        for S in states:
+            assert S.scalars().err == 0 and S.scalars().t8_all == one.scalars.t8_all
+        codes = torch.cat([S.collect().codes for S in states])
+        keep = np.concatenate([words_to_mask(S.collect().keep_bits, S.n) for S in states])
+        assert torch.equal(codes, one.codes)
+        np.testing.assert_array_equal(keep, words_to_mask(one.keep_bits, one_n(cfg)))
+
+
+def one_n(cfg):
+    return int(np.prod(cfg.shape))

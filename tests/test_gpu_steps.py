@@ -154,6 +154,71 @@ def test_threshold_f32_vs_oracle():
     assert oracle.norm8_f32(np.nextafter(np.float32(s.thr_f32), np.float32(-np.inf)), s.i_max) <= t8
 
 
+def _h8_cases(rng):
+    cases = [np.bincount([0] * 7 + [128] * 7 + [255] * 7, minlength=256),          # S:174 spikes
+             np.bincount([10] * 50 + [200] * 50, minlength=256),                    # S:173 (k = 3: 2 bins)
+             np.bincount([5, 9, 9, 250], minlength=256)]
+    for _ in range(12):                                                               # dense / sparse / modal
+        cases.append(rng.integers(0, 1000, 256) * (rng.random(256) < rng.uniform(0.05, 1.0)))
+    for _ in range(6):                                                                # three or four modes
+        v = np.concatenate([rng.normal(rng.uniform(10, 245), rng.uniform(2, 20), int(rng.integers(1000, 200000)))
+                            for _ in range(int(rng.integers(3, 5)))])
+        cases.append(np.bincount(np.clip(np.rint(v), 0, 255).astype(np.int64), minlength=256))
+    big = np.zeros(256, np.int64)
+    big[[3, 60, 61, 200]] = [1 << 34, 1 << 33, 12345, (1 << 34) + 7]                 # N near 2^35 (C5)
+    cases.append(big)
+    cases.append(np.full(256, 1 << 26, np.int64))                                     # uniform (symmetric)
+    return cases
+
+
+@pytest.mark.parametrize("classes", [2, 3])
+def test_threshold_multi_vs_oracle(classes):
+    """NEXT-3: roix_threshold_multi on 256-bin norm8 histograms (the fp32 form)
+    against the exact exhaustive oracle -- spikes, ties, sparse and multi-modal histograms, counts near
+    2^35 -- for both polarities; fewer populated bins than classes -> DEGENERATE."""
+    rng = np.random.default_rng(31 + classes)
+    x_np = np.concatenate([rng.normal(0.02, 0.005, 4000), rng.uniform(0.3, 1.2, 900)]).astype(np.float32)
+    for h8 in _h8_cases(rng):
+        try:
+            want = oracle.multi_otsu(list(h8), classes)
+        except oracle.Degenerate:
+            want = None
+        for pol in (0, 1):
+            _, sc, _ = gpu_threshold(x_np, rel_eb=1e-3)
+            h = torch.from_numpy(np.asarray(h8, np.int64)).cuda()
+            L.roix_threshold_multi(ptr(h), 256, L.F32, pol, classes, ptr(sc), st())
+            s = read_sc(sc)
+            if want is None:
+                assert s.err & L.ERR_DEGENERATE
+                continue
+            assert s.err == 0
+            got = tuple((s.t8_all >> (8 * k)) & 255 for k in range(classes - 1))
+            assert got == want, (got, want)
+            assert s.t8 == (want[0] if pol == 0 else want[-1])
+            assert s.thr_f32 == s.edges[s.t8 + 1]
+
+
+def test_threshold_multi_u16_raw_hist():
+    """classes = 3 from a raw 65536-bin histogram (the u16 form: I_max and the norm8 fold on the GPU)."""
+    rng = np.random.default_rng(77)
+    x_np = np.concatenate([rng.normal(400, 60, 300000), rng.normal(1800, 90, 60000),
+                           rng.normal(3100, 120, 40000)]).clip(0, 4095).astype(np.uint16)
+    for pol in (0, 1):
+        x = dev(x_np)
+        sc = new_sc(2.0)
+        L.roix_resolve(ptr(sc), L.U16, 0.0, st())
+        h = torch.zeros(65536, dtype=torch.int64, device="cuda")
+        L.roix_histogram(ptr(x), L.U16, x_np.size, ptr(sc), ptr(h), 65536, st())
+        L.roix_threshold_multi(ptr(h), 65536, L.U16, pol, 3, ptr(sc), st())
+        s = read_sc(sc)
+        hist = oracle.hist_u16(x_np)
+        imax = oracle.imax_u16(hist)
+        t1, t2 = oracle.multi_otsu(oracle.hist8_from_u16(hist, imax), 3)
+        assert s.err == 0 and s.i_max == imax and (s.t8_all & 255, s.t8_all >> 8) == (t1, t2)
+        t8 = t1 if pol == 0 else t2
+        assert s.t8 == t8 and oracle.norm8_u16(s.thr_u16, imax) > t8 >= oracle.norm8_u16(s.thr_u16 - 1, imax)
+
+
 # ------------------------------------------------------------------------- a4 + a5 binarise + open
 MORPH_SHAPES = [(1, 1, 1), (1, 1, 40), (2, 3, 5), (3, 5, 7), (5, 33, 65), (7, 64, 64), (9, 17, 100),
                 (4, 70, 139), (3, 20, 1390), (11, 9, 256), (6, 40, 96), (33, 8, 32),
