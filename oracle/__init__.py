@@ -212,6 +212,24 @@ def filter_components(comp, csize, min_size):
     return kept[: csize.size].copy(), K
 
 
+def keep_largest(comp, csize):
+    """NEXT-3 keep-largest mode ("select the largest by area"): only the
+    component with the most voxels survives; ties go to the component containing the smallest linear
+    index (S:187's raster-order anchor).  The table from `label` is in increasing minimum index, so
+    the first maximum is the winner.  Returns (kept flags, K) like filter_components."""
+    comp = _c(comp, np.uint32)
+    csize = np.asarray(csize, np.uint64)
+    kept = np.zeros(csize.size, np.uint8)
+    if csize.size == 0:
+        return kept, np.zeros(comp.shape, np.uint8)
+    best = 0
+    for c in range(1, csize.size):
+        if csize[c] > csize[best]:
+            best = c
+    kept[best] = 1
+    return kept, (comp == best).astype(np.uint8)
+
+
 def extract(x, K, eb):
     """a8: codes of the voxels with K = 1, in increasing linear index."""
     x = np.ascontiguousarray(x)
@@ -272,11 +290,12 @@ def pack_bits(mask):
 
 
 # ---------------------------------------------------------------- the composed hot path
-def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, classes=2):
+def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, classes=2, keep="size"):
     """The whole path on one volume x[Z][Y][X] (uint16 or float32).  Returns a dict of every
     intermediate the CUDA path exposes.  Raises Degenerate when Otsu has no valid threshold.
     classes = 3 (NEXT-3): multi-Otsu; the ROI is norm8 > the lowest threshold (HIGH) or
-    norm8 <= the highest (LOW, reading G-39)."""
+    norm8 <= the highest (LOW, reading G-39).  keep = "largest" (NEXT-3): only the largest component
+    survives (min_size unused)."""
     x = np.ascontiguousarray(x)
     assert x.ndim == 3
     out = {}
@@ -304,7 +323,7 @@ def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, 
     m = binarize(x, imax, t8, polarity)
     o = opening(m, se)
     comp, cmin, csz = label(o, conn)
-    kept, K = filter_components(comp, csz, min_size)
+    kept, K = keep_largest(comp, csz) if keep == "largest" else filter_components(comp, csz, min_size)
     out.update(m=m, o=o, comp=comp, comp_min=cmin, comp_size=csz, kept=kept, K=K)
     out["stream"] = extract(x, K, out["eb"])
     out["count"] = int(out["stream"].size)

@@ -144,3 +144,43 @@ def test_pack_bits_layout(oracle_mod):
             assert (int(w[i // 32]) >> (i % 32)) & 1 == m[i]
         for i in range(n, 32 * w.size):
             assert (int(w[i // 32]) >> (i % 32)) & 1 == 0
+
+
+# ------------------------------------------------------------------ NEXT-3 keep-largest
+def test_keep_largest_spec_examples(oracle_mod):
+    o = np.zeros((1, 8, 12), np.uint8)
+    o[0, 1:2, 1:6] = 1                      # blob of area 5
+    o[0, 4:7, 6:9] = 1                      # blob of area 9
+    comp, cmin, csz = oracle_mod.label(o, 8)
+    kept, K = oracle_mod.keep_largest(comp, csz)
+    assert kept.tolist() == [0, 1]          # only the 9-blob survives
+    assert K.sum() == 9 and K[0, 5, 7] == 1 and K[0, 1, 3] == 0
+    z = np.zeros((1, 5, 5), np.uint8)        # all-zero -> all-zero
+    comp, cmin, csz = oracle_mod.label(z, 8)
+    kept, K = oracle_mod.keep_largest(comp, csz)
+    assert kept.size == 0 and not K.any()
+    f = np.ones((1, 5, 7), np.uint8)         # one full-frame component -> identity
+    comp, cmin, csz = oracle_mod.label(f, 8)
+    np.testing.assert_array_equal(oracle_mod.keep_largest(comp, csz)[1], f)
+
+
+def test_keep_largest_ties_and_scipy(oracle_mod):
+    """Equal areas: the component holding the smallest linear index wins; random volumes: the
+    kept voxels are scipy.ndimage's largest component (sizes from np.bincount)."""
+    o = np.zeros((2, 6, 10), np.uint8)
+    o[1, 0, 0:4] = 1                          # area 4, first voxel at linear index 60
+    o[0, 3, 5:9] = 1                          # area 4, first voxel at 35: wins the tie
+    comp, cmin, csz = oracle_mod.label(o, 6)
+    K = oracle_mod.keep_largest(comp, csz)[1]
+    assert K[0, 3, 5:9].all() and K.sum() == 4
+    rng = np.random.default_rng(5)
+    for conn, st in ((6, ndi.generate_binary_structure(3, 1)), (26, ndi.generate_binary_structure(3, 3))):
+        for _ in range(5):
+            o = (rng.random((5, 9, 13)) < 0.3).astype(np.uint8)
+            lab, n = ndi.label(o, structure=st)
+            comp, cmin, csz = oracle_mod.label(o, conn)
+            K = oracle_mod.keep_largest(comp, csz)[1]
+            sizes = np.bincount(lab.reshape(-1))[1:]
+            winners = np.flatnonzero(sizes == sizes.max()) + 1
+            first = min(winners, key=lambda w: np.flatnonzero(lab.reshape(-1) == w)[0])
+            np.testing.assert_array_equal(K, (lab == first).astype(np.uint8))
