@@ -212,7 +212,9 @@ roix_status roix_binarize_planes(const void *x, roix_dtype dtype, const roix_geo
 /*
  * a6+a7 LABEL + FILTER.  Connected components of o under conn (6, 18, 26: 3-D; 4, 8: in-plane per
  * z-plane), each named by its minimum global linear index (G-14).  Components of size < min_size
- * are dropped (G-13).  Outputs (device):
+ * are dropped (G-13).  min_size = ROIX_KEEP_LARGEST (NEXT-3, "select the largest by area";
+ * S:185-193) keeps only the largest component, ties to the smallest label (raster-order anchor).
+ * Outputs (device):
  *   keep_bits      K = o AND kept; may alias o_bits (in-place: only dropped voxels are cleared);
  *   comp_min/comp_size/comp_kept  the component table in increasing min index, capacity comp_cap
  *                  (any may be NULL to skip the table); counts in sc->n_components / n_kept;
@@ -222,6 +224,8 @@ roix_status roix_binarize_planes(const void *x, roix_dtype dtype, const roix_geo
  * number (ROIX_ERR_CAPACITY if exceeded).  row_runs: the per-row run counts roix_morph produced
  * for this o (nullable: then they are counted here).  ws/ws_bytes from roix_label_workspace.
  */
+#define ROIX_KEEP_LARGEST UINT64_MAX
+
 typedef struct roix_label_out {
     uint32_t *keep_bits;
     uint64_t *comp_min;
@@ -249,6 +253,11 @@ roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const r
  *   6. roix_label_finish applies the map: table entries live on the rank holding the component's
  *      minimum index; small-object removal uses the merged sizes.
  * Labels are global linear indices (uint64).  ws / run_capacity are those of roix_label_local.
+ * Keep-largest on a sharded volume (NEXT-3): after roix_merge, roix_label_largest(phase 0) writes the
+ * largest size among this slab's owned components to best[0] (device, 2 uint64; phase 0 first resets
+ * best to (0, 2^63 - 1 = none)); reduce best[0] with MAX over ranks; phase 1 writes the smallest label of
+ * that size to best[1]; reduce best[1] with MIN; roix_label_finish_keep then keeps exactly the
+ * component best[1] on every rank (nothing if the volume has no component).
  */
 typedef struct roix_brun {
     uint32_t y, x0, x1, pad; /* row within the plane, run [x0, x1)                    */
@@ -277,6 +286,14 @@ roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64
                               void *ws, size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
                               const uint64_t *map_total, uint64_t nmap, const roix_label_out *out, roix_scalars *sc,
                               roix_stream_t stream);
+
+roix_status roix_label_largest(void *ws, const roix_geom *g, uint64_t run_capacity, const uint64_t *map_label,
+                               const uint64_t *map_final, const uint64_t *map_total, uint64_t nmap, uint32_t phase,
+                               uint64_t *best, roix_scalars *sc, roix_stream_t stream);
+roix_status roix_label_finish_keep(const uint32_t *o_bits, const roix_geom *g, uint64_t run_capacity, void *ws,
+                                   size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
+                                   const uint64_t *map_total, uint64_t nmap, const uint64_t *keep,
+                                   const roix_label_out *out, roix_scalars *sc, roix_stream_t stream);
 
 /*
  * a1+a8 EXTRACT.  For the set bits i_0 < i_1 < ... of keep_bits (n voxels), codes_out[j] =

@@ -88,6 +88,9 @@ _SIGS = {
     "roix_greedy_quantize": (_i32, [_vp, _u64, _f64, _u32, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "roix_extract_runs": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _u64, _vp,
                                  _vp]),
+    "roix_label_largest": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, _vp, _vp, _u64, _u32, _vp, _vp, _vp]),
+    "roix_label_finish_keep": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _u64, _vp,
+                                      ctypes.POINTER(LabelOut), _vp, _vp]),
     "roix_threshold_multi": (_i32, [_vp, _u32, _i32, _i32, _u32, _vp, _vp]),
     "roix_decode_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_decode": (_i32, [_vp, _vp, _u64, _i32, _u64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
@@ -145,6 +148,9 @@ roix_extract_runs = _wrap("roix_extract_runs")
 roix_row_spans = _wrap("roix_row_spans")
 roix_greedy_quantize = _wrap("roix_greedy_quantize")
 roix_threshold_multi = _wrap("roix_threshold_multi")
+roix_label_largest = _wrap("roix_label_largest")
+roix_label_finish_keep = _wrap("roix_label_finish_keep")
+KEEP_LARGEST = (1 << 64) - 1
 roix_decode = _wrap("roix_decode")
 roix_decode_spans = _wrap("roix_decode_spans")
 roix_confusion = _wrap("roix_confusion")

@@ -263,11 +263,39 @@ roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64
     if (!sc || !o_bits || !out) return invalid("sc / o_bits / out is NULL");
     if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
     if (out->comp_min && (!out->comp_size || out->comp_cap == 0)) return invalid("comp_size / comp_cap");
+    if (min_size == ROIX_KEEP_LARGEST) return invalid("keep-largest on a sharded volume: use roix_label_finish_keep");
     roix_status s = label_common(g, run_capacity, ws, ws_bytes);
     if (s != ROIX_OK) return s;
     return cuda(launch_label_finish(o_bits, *g, min_size, run_capacity, ws, map_label, map_final, map_total, nmap, *out,
                                     sc, (cudaStream_t)stream),
                 "roix_label_finish");
+}
+
+roix_status roix_label_largest(void *ws, const roix_geom *g, uint64_t run_capacity, const uint64_t *map_label,
+                               const uint64_t *map_final, const uint64_t *map_total, uint64_t nmap, uint32_t phase,
+                               uint64_t *best, roix_scalars *sc, roix_stream_t stream) {
+    if (!sc || !best) return invalid("sc / best is NULL");
+    if (phase > 1) return invalid("phase must be 0 or 1");
+    if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
+    roix_status s = label_common(g, run_capacity, ws, (size_t)-1);
+    if (s != ROIX_OK) return s;
+    return cuda(launch_label_largest(*g, run_capacity, ws, map_label, map_final, map_total, nmap, best, (int)phase, sc,
+                                     (cudaStream_t)stream),
+                "roix_label_largest");
+}
+
+roix_status roix_label_finish_keep(const uint32_t *o_bits, const roix_geom *g, uint64_t run_capacity, void *ws,
+                                   size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
+                                   const uint64_t *map_total, uint64_t nmap, const uint64_t *keep,
+                                   const roix_label_out *out, roix_scalars *sc, roix_stream_t stream) {
+    if (!sc || !o_bits || !out || !keep) return invalid("sc / o_bits / out / keep is NULL");
+    if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
+    if (out->comp_min && (!out->comp_size || out->comp_cap == 0)) return invalid("comp_size / comp_cap");
+    roix_status s = label_common(g, run_capacity, ws, ws_bytes);
+    if (s != ROIX_OK) return s;
+    return cuda(launch_label_finish(o_bits, *g, 0, run_capacity, ws, map_label, map_final, map_total, nmap, *out, sc,
+                                    (cudaStream_t)stream, keep),
+                "roix_label_finish_keep");
 }
 
 roix_status roix_label_boundary(const void *ws, const roix_geom *g, uint64_t run_capacity, int side, roix_brun *out,

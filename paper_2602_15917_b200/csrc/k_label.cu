@@ -28,7 +28,8 @@ struct LabelWS {
     uint32_t *x0, *x1, *rrow, *parent, *cidx;  // [cap]
     uint64_t *size;       // [cap]
     uint8_t *kept;        // [cap]
-    uint64_t *ctr;        // [8]: 0 n_runs, 1 n_cross_pairs, 2 n_kept, 3 gather error snapshot, 4 n_block_roots
+    uint64_t *ctr;        // [8]: 0 n_runs, 1 n_cross_pairs, 2 n_kept, 3 gather error snapshot, 4 n_block_roots,
+                          //      5, 6 keep-largest (size, label)
     uint32_t *broots;     // [cap]: the block-local roots left by k_union_local
     uint2 *pairs;         // [pair_cap]: run pairs that cross union blocks
     uint64_t pair_cap;
@@ -598,17 +599,54 @@ __device__ __forceinline__ void resolve_root(const LGeo &G, const LabelWS &W, co
     }
 }
 
-// cidx flags: 1 for local roots that own a table entry (their label is the merged component's label)
-__global__ void k_root_flags(LGeo G, LabelWS W, MapView M, uint64_t min_size, roix_scalars *sc) {
+// NEXT-3 keep-largest: over the components this slab owns (local roots whose
+// final label is their own first voxel), phase 0 takes the largest size into best[0], phase 1 the
+// smallest label among the components of that size into best[1] (the raster-order anchor tie-break).
+// best[] is pre-set to (0, 2^63 - 1 = none); sharded callers reduce it over ranks between the phases
+// (labels are < 2^63, so signed and unsigned minima agree).
+__global__ void k_largest(LGeo G, LabelWS W, MapView M, uint64_t *best, int phase, roix_scalars *sc) {
     if (get_err(sc)) return;
     const uint64_t n = W.ctr[0];
+    const uint64_t want = phase ? best[0] : 0;
+    uint64_t v = phase ? ~0ull : 0ull;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (W.parent[i] != (uint32_t)i) continue;
+        uint64_t fin, tot;
+        resolve_root(G, W, M, (uint32_t)i, fin, tot);
+        if (fin != gidx(G, W, (uint32_t)i)) continue;   // another slab owns it
+        if (phase == 0) v = max(v, tot);
+        else if (tot == want) v = min(v, fin);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const uint64_t o = __shfl_xor_sync(FULL, v, d);
+        v = phase ? min(v, o) : max(v, o);
+    }
+    if (lane_id() == 0) {
+        if (phase == 0 && v) atomicMax((unsigned long long *)&best[0], (unsigned long long)v);
+        if (phase == 1 && v != ~0ull) atomicMin((unsigned long long *)&best[1], (unsigned long long)v);
+    }
+}
+
+__global__ void k_largest_init(uint64_t *best) {
+    best[0] = 0;
+    best[1] = 0x7fffffffffffffffull;
+}
+
+// cidx flags: 1 for local roots that own a table entry (their label is the merged component's label).
+// kept: size >= min_size, or (keep != NULL) the component labelled keep[1]
+__global__ void k_root_flags(LGeo G, LabelWS W, MapView M, uint64_t min_size, const uint64_t *keep,
+                             roix_scalars *sc) {
+    if (get_err(sc)) return;
+    const uint64_t n = W.ctr[0];
+    const uint64_t keep_label = keep ? keep[1] : 0;
     uint32_t nk = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t f = 0;
         if (W.parent[i] == (uint32_t)i) {
             uint64_t fin, tot;
             resolve_root(G, W, M, (uint32_t)i, fin, tot);
-            const uint8_t kp = tot >= min_size;
+            const uint8_t kp = keep ? fin == keep_label : tot >= min_size;
             W.kept[i] = kp;
             f = fin == gidx(G, W, (uint32_t)i);
             nk += f & kp;
@@ -852,9 +890,21 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
 }
 
 // a7: resolve every local root through the merge map, component table, kept flags, K, labels
+cudaError_t launch_label_largest(const roix_geom &g, uint64_t cap, void *ws, const uint64_t *map_label,
+                                 const uint64_t *map_final, const uint64_t *map_total, uint64_t nmap, uint64_t *best,
+                                 int phase, roix_scalars *sc, cudaStream_t st) {
+    LabelWS W;
+    carve(ws, g, cap, &W);
+    const MapView M = {map_label, map_final, map_total, nmap};
+    if (phase == 0) k_largest_init<<<1, 1, 0, st>>>(best);
+    k_largest<<<num_sms() * 8, 256, 0, st>>>(make_geo(g), W, M, best, phase, sc);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint64_t min_size, uint64_t cap, void *ws,
                                 const uint64_t *map_label, const uint64_t *map_final, const uint64_t *map_total,
-                                uint64_t nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st) {
+                                uint64_t nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st,
+                                const uint64_t *keep) {
     LabelWS W;
     carve(ws, g, cap, &W);
     const LGeo G = make_geo(g);
@@ -862,7 +912,7 @@ cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint
     const MapView M = {map_label, map_final, map_total, nmap};
     const int runs_grid = num_sms() * 8;
     cudaError_t e;
-    k_root_flags<<<runs_grid, 256, 0, st>>>(G, W, M, min_size, sc);
+    k_root_flags<<<runs_grid, 256, 0, st>>>(G, W, M, min_size, keep, sc);
     if ((e = scan_u32_dev(W.cidx, W.cidx, W.ctr, cap, W.scan_tmp, st)) != cudaSuccess) return e;
     if (out.keep_bits && out.keep_bits != o_bits &&
         (e = cudaMemcpyAsync(out.keep_bits, o_bits, nwords * 4, cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
@@ -880,6 +930,15 @@ cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const
                          cudaStream_t st) {
     cudaError_t e = launch_label_local(o_bits, row_runs, g, conn, cap, ws, sc, st);
     if (e != cudaSuccess) return e;
+    if (min_size == ROIX_KEEP_LARGEST) {   // both phases on this GPU; (size, label) in ctr[5], ctr[6]
+        LabelWS W;
+        carve(ws, g, cap, &W);
+        uint64_t *best = W.ctr + 5;
+        if ((e = launch_label_largest(g, cap, ws, nullptr, nullptr, nullptr, 0, best, 0, sc, st)) != cudaSuccess ||
+            (e = launch_label_largest(g, cap, ws, nullptr, nullptr, nullptr, 0, best, 1, sc, st)) != cudaSuccess)
+            return e;
+        return launch_label_finish(o_bits, g, 0, cap, ws, nullptr, nullptr, nullptr, 0, out, sc, st, best);
+    }
     return launch_label_finish(o_bits, g, min_size, cap, ws, nullptr, nullptr, nullptr, 0, out, sc, st);
 }
 

@@ -54,7 +54,11 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
                                uint64_t cap, void *ws, roix_scalars *sc, cudaStream_t st);
 cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint64_t min_size, uint64_t cap, void *ws,
                                 const uint64_t *map_label, const uint64_t *map_final, const uint64_t *map_total,
-                                uint64_t nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st);
+                                uint64_t nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st,
+                                const uint64_t *keep = nullptr);
+cudaError_t launch_label_largest(const roix_geom &g, uint64_t cap, void *ws, const uint64_t *map_label,
+                                 const uint64_t *map_final, const uint64_t *map_total, uint64_t nmap, uint64_t *best,
+                                 int phase, roix_scalars *sc, cudaStream_t st);
 cudaError_t launch_label_boundary(const void *ws, const roix_geom &g, uint64_t cap, int side, roix_brun *out,
                                   uint64_t out_cap, uint64_t *count, roix_scalars *sc, cudaStream_t st);
 cudaError_t launch_label_link(const void *ws, const roix_geom &g, uint64_t cap, uint32_t conn, const roix_brun *prev,

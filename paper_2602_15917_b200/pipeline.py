@@ -46,7 +46,7 @@ class Pipeline:
 
     def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
                  run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="mask",
-                 spans=False, classes=2):
+                 spans=False, classes=2, keep="size"):
         L.load()
         self.shape = tuple(int(v) for v in shape)
         Z, Y, X = self.shape
@@ -64,6 +64,12 @@ class Pipeline:
         if classes == 3 and fused:
             raise ValueError("the fused speculative histogram+binarisation supports classes = 2 only")
         self.classes = int(classes)
+        # a7 filter: "size" drops components smaller than min_size (G-13); "largest" keeps only the
+        # largest component (NEXT-3)
+        if keep not in ("size", "largest"):
+            raise ValueError("keep must be 'size' or 'largest'")
+        self.keep = keep
+        self.label_min_size = L.KEEP_LARGEST if keep == "largest" else self.min_size
         self.device = torch.device(device or "cuda")
         dev = self.device
         self.geom = L.Geom(Z, Y, X, 0, Z)
@@ -147,7 +153,7 @@ class Pipeline:
         out = L.LabelOut(self.o.data_ptr(), self.comp_min.data_ptr(), self.comp_size.data_ptr(),
                          self.comp_kept.data_ptr(), self.comp_cap,
                          self.labels.data_ptr() if self.labels is not None else None)
-        L.roix_label(_ptr(self.o), _ptr(self.row_runs), ctypes.byref(self.geom), self.conn, self.min_size,
+        L.roix_label(_ptr(self.o), _ptr(self.row_runs), ctypes.byref(self.geom), self.conn, self.label_min_size,
                      self.run_capacity, _ptr(self.label_ws), self.ws_bytes, ctypes.byref(out), sc, st)
         mark("label")
         if self.extract == "runs":
@@ -228,6 +234,7 @@ class Pipeline:
 
     def launches(self):
         k = 4 if self.spans_on else 0   # roix_row_spans: extent, 2 scans, write
+        k += 3 if self.keep == "largest" else 0   # reset + two reduction phases
         k += sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
                                        "extract" if self.extract == "mask" else "extract_runs"))
         return k + (LAUNCHES["range"] if self.cdtype == L.F32 else 0)

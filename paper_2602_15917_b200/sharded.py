@@ -55,6 +55,7 @@ class SlabState(Pipeline):
         self.root_cap = 2 * self.brun_cap
         self.root_lab = torch.empty(self.root_cap, dtype=torch.int64, device=dev)
         self.root_size = torch.empty(self.root_cap, dtype=torch.int64, device=dev)
+        self.best = torch.zeros(2, dtype=torch.int64, device=dev)     # keep-largest: (size, label)
 
     def _alloc_label(self, cap):
         super()._alloc_label(cap)
@@ -125,10 +126,19 @@ def slab_program(S, x, stream=None, mark=None):
         pairs, labels, sizes = gathered
         ml, mf, mt = L.roix_merge(pairs, labels, sizes)
         S.map = torch.from_numpy(np.stack([ml, mf, mt]).view(np.int64)).to(S.device)
-        L.roix_label_finish(_ptr(S.o), geo, S.min_size, cap, ws, wsb, _ptr(S.map[0]), _ptr(S.map[1]),
-                            _ptr(S.map[2]), ml.size, ctypes.byref(out), sc, st)
+        mp = (_ptr(S.map[0]), _ptr(S.map[1]), _ptr(S.map[2]), ml.size)
+        if S.keep == "largest":
+            # NEXT-3 keep-largest over the whole volume: the largest size, then the smallest label of
+            # that size, each reduced over the ranks (X4c, X4d)
+            L.roix_label_largest(ws, geo, cap, *mp, 0, _ptr(S.best), sc, st)
+            yield ("best_max", S.best)
+            L.roix_label_largest(ws, geo, cap, *mp, 1, _ptr(S.best), sc, st)
+            yield ("best_min", S.best)
+            L.roix_label_finish_keep(_ptr(S.o), geo, cap, ws, wsb, *mp, _ptr(S.best), ctypes.byref(out), sc, st)
+        else:
+            L.roix_label_finish(_ptr(S.o), geo, S.min_size, cap, ws, wsb, *mp, ctypes.byref(out), sc, st)
     else:
-        L.roix_label(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, S.min_size, S.run_capacity, _ptr(S.label_ws),
+        L.roix_label(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, S.label_min_size, S.run_capacity, _ptr(S.label_ws),
                      S.ws_bytes, ctypes.byref(out), sc, st)
     mark("label")
     if S.extract == "runs":
@@ -214,6 +224,13 @@ class SimComm:
         if kind == "counts":
             c = [int(_count_of(S).item()) for S in states]
             return [c] * G
+        if kind in ("best_max", "best_min"):
+            k = 0 if kind == "best_max" else 1
+            vals = torch.stack([m[1][k] for m in msgs])
+            v = vals.max() if k == 0 else vals.min()
+            for m in msgs:
+                m[1][k].copy_(v)
+            return [None] * G
         raise ValueError(kind)
 
 
@@ -281,6 +298,12 @@ class DistComm:
             d.all_gather_object(objs, (pairs, labels, sizes), group=grp)
             return (np.concatenate([o[0] for o in objs]).reshape(-1, 2), np.concatenate([o[1] for o in objs]),
                     np.concatenate([o[2] for o in objs]))
+        if kind in ("best_max", "best_min"):
+            k = 0 if kind == "best_max" else 1
+            v = msg[1][k:k + 1].clone()
+            d.all_reduce(v, op=d.ReduceOp.MAX if k == 0 else d.ReduceOp.MIN, group=grp)
+            msg[1][k:k + 1].copy_(v)
+            return None
         if kind == "counts":
             c = _count_of(S).clone()
             allc = [torch.empty_like(c) for _ in range(self.world)]

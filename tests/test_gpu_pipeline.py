@@ -30,10 +30,10 @@ CASES = [synth.CONFIGS["C1"], synth.CONFIGS["C2"], synth.scaled("C3", 0.25, fram
          synth.scaled("C4", 0.125), synth.scaled("C5", 0.125), synth.scaled("C4", 0.0625), synth.scaled("C1", 0.37)]
 
 
-def _check(cfg, p, x, res, classes=2):
+def _check(cfg, p, x, res, classes=2, keep="size"):
     x_np = synth.to_numpy(x, cfg)
     ref = oracle.pipeline(x_np, eb=cfg.eb or None, rel_eb=cfg.rel_eb or None, conn=cfg.conn, se=cfg.se,
-                          min_size=cfg.min_size, polarity=cfg.polarity, classes=classes)
+                          min_size=cfg.min_size, polarity=cfg.polarity, classes=classes, keep=keep)
     s = res.scalars
     assert s.err == 0
     assert res.t8 == ref["t8"] and res.i_max == ref["i_max"] and res.eb == ref["eb"]
@@ -286,3 +286,33 @@ def test_sharded_multi_otsu_g_invariant():
 
 def one_n(cfg):
     return int(np.prod(cfg.shape))
+
+
+# ------------------------------------------------------------------ NEXT-3 keep-largest in the pipeline
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C1"], synth.scaled("C4", 0.0625), synth.scaled("C3", 0.25, frames=4)],
+                         ids=lambda c: c.name)
+def test_pipeline_keep_largest_vs_oracle(cfg):
+    x = synth.generate(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se,
+                 min_size=cfg.min_size, polarity=cfg.polarity, keep="largest")
+    res = p.run(x)
+    ref = _check(cfg, p, x, res, keep="largest")
+    assert res.n_kept == 1 and ref["kept"].sum() == 1
+
+
+def test_sharded_keep_largest_g_invariant():
+    """The largest component crosses slab faces (C5's z-elongated objects): the merged sizes decide."""
+    from paper_2602_15917_b200.sharded import run_simulated
+
+    cfg = synth.scaled("C5", 0.0625)
+    x = synth.generate(cfg)
+    kw = dict(eb=cfg.eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, keep="largest")
+    one = Pipeline(cfg.shape, cfg.dtype, **kw).run(x)
+    ref = oracle.pipeline(synth.to_numpy(x, cfg), eb=cfg.eb, conn=cfg.conn, se=cfg.se, keep="largest")
+    np.testing.assert_array_equal(words_to_mask(one.keep_bits, one_n(cfg)).reshape(cfg.shape), ref["K"])
+    for G in (2, 4, 8):
+        states = run_simulated(x, G, **kw)
+        keep = np.concatenate([words_to_mask(S.collect().keep_bits, S.n) for S in states])
+        np.testing.assert_array_equal(keep.reshape(cfg.shape), ref["K"])
+        assert torch.equal(torch.cat([S.collect().codes for S in states]), one.codes)
+        assert sum(S.scalars().n_kept for S in states) == 1

@@ -354,6 +354,27 @@ def test_label_random_vs_oracle(conn, shape):
         assert s.n_kept == int(kept.sum())
 
 
+@pytest.mark.parametrize("conn", [6, 26, 8])
+@pytest.mark.parametrize("shape", [(1, 1, 1), (2, 3, 5), (5, 17, 65), (9, 40, 512), (33, 8, 32), (4, 70, 139)])
+def test_label_keep_largest_vs_oracle(conn, shape):
+    """NEXT-3 keep-largest: only the largest component survives, ties to the
+    smallest min index; the table still lists every component (comp_kept one-hot)."""
+    rng = np.random.default_rng(abs(hash((conn, shape, "largest"))) % 2 ** 32)
+    masks = [(rng.random(shape) < p).astype(np.uint8) for p in (0.2, 0.45)] + [np.zeros(shape, np.uint8)]
+    tie = np.zeros(shape, np.uint8)                  # two single-voxel components: the first one wins
+    tie.reshape(-1)[[0, tie.size - 1]] = 1
+    masks.append(tie)
+    for mask in masks:
+        s, K, cmin, csz, ckp, _ = _label_gpu(mask, conn, L.KEEP_LARGEST, True)
+        assert s.err == 0
+        comp, rmin, rsz = oracle.label(mask, conn)
+        kept, rK = oracle.keep_largest(comp, rsz)
+        np.testing.assert_array_equal(cmin, rmin.astype(np.int64))
+        np.testing.assert_array_equal(ckp, kept)
+        np.testing.assert_array_equal(words_to_mask(K, mask.size).reshape(shape), rK)
+        assert s.n_kept == int(kept.sum())
+
+
 def test_label_not_inplace_and_checkerboard():
     z, y, x = np.indices((6, 8, 40))
     cb = ((z + y + x) % 2 == 0).astype(np.uint8)

@@ -122,6 +122,12 @@ def _worker(rank, world, port, q):
         off = L.Scalars.count.offset
         S.sc[off:off + 8].view(torch.int64).fill_(5 + rank)
         out["counts"] = comm._do(("counts", S), S)
+        # X4c / X4d: keep-largest (size MAX, then label MIN; 2^63 - 1 = "no component of that size")
+        best = torch.tensor([[40, 0], [55, 0]][rank], dtype=torch.int64)
+        comm._do(("best_max", best), S)
+        best[1] = [(1 << 63) - 1, 777][rank]
+        comm._do(("best_min", best), S)
+        out["best"] = best.tolist()
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -143,6 +149,7 @@ def test_distcomm_exchanges_gloo(L):
         assert o["sum"] == [3 * k for k in range(8)]
         assert o["minmax"] == [0x7FFFFFF0, 0xC0000001]
         assert o["counts"] == [5, 6]
+        assert o["best"] == [55, 777]
         assert o["tables"][1] == [100, 101] and o["tables"][2] == [7, 7]
         assert o["tables"][0] == [[0, 1], [0, 1], [10, 11], [10, 11]]
     assert res[0]["halo"][1] == [1] * 6 and res[0]["halo"][0] == [-1] * 6   # rank 0 <- rank 1's first planes
