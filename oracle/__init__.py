@@ -290,12 +290,30 @@ def pack_bits(mask):
 
 
 # ---------------------------------------------------------------- the composed hot path
-def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, classes=2, keep="size"):
+def frame_thresholds(x, classes=2, polarity=0):
+    """NEXT-3 per-frame thresholds (uint16 frame stacks): every z-plane is its own image, as in the
+    paper's 2-D setting -- its own I_max (Eq. 1), 256-bin normalised histogram and
+    (multi-)Otsu thresholds.  Returns [(imax, thresholds, t8)] per frame; t8 is the ROI threshold
+    (the lowest for HIGH, the highest for LOW, G-39).  Raises Degenerate for a frame with too few
+    populated bins."""
+    out = []
+    for z in range(x.shape[0]):
+        h = hist_u16(x[z])
+        imax = imax_u16(h)
+        h8 = hist8_from_u16(h, imax)
+        ts = (otsu2(h8),) if classes == 2 else multi_otsu(h8, classes)
+        out.append((imax, ts, ts[0] if polarity == 0 else ts[-1]))
+    return out
+
+
+def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, classes=2, keep="size",
+             frames=False):
     """The whole path on one volume x[Z][Y][X] (uint16 or float32).  Returns a dict of every
     intermediate the CUDA path exposes.  Raises Degenerate when Otsu has no valid threshold.
     classes = 3 (NEXT-3): multi-Otsu; the ROI is norm8 > the lowest threshold (HIGH) or
     norm8 <= the highest (LOW, reading G-39).  keep = "largest" (NEXT-3): only the largest component
-    survives (min_size unused)."""
+    survives (min_size unused).  frames = True (NEXT-3, uint16): per-frame thresholds
+    (frame_thresholds); the mask of frame z is Eq. 2 with frame z's I_max and threshold."""
     x = np.ascontiguousarray(x)
     assert x.ndim == 3
     out = {}
@@ -312,6 +330,12 @@ def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, 
         imax = imax_u16(h)
         h8 = hist8_from_u16(h, imax)
     out["eb"], out["i_max"], out["h8"] = float(np.float32(eb)), imax, h8
+    if frames:
+        assert x.dtype == np.uint16
+        ft = frame_thresholds(x, classes, polarity)
+        out["frames"] = ft
+        m = np.concatenate([binarize(x[z:z + 1], imax_z, t8_z, polarity) for z, (imax_z, _, t8_z) in enumerate(ft)])
+        return _after_binarize(out, x, m, se, conn, min_size, keep)
     if classes == 2:
         t8 = otsu2(h8)
         out["thresholds"] = (t8,)
@@ -321,6 +345,11 @@ def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, 
         t8 = ts[0] if polarity == 0 else ts[-1]
     out["t8"] = t8
     m = binarize(x, imax, t8, polarity)
+    return _after_binarize(out, x, m, se, conn, min_size, keep)
+
+
+def _after_binarize(out, x, m, se, conn, min_size, keep):
+    """a5..a8 on the binarised mask m."""
     o = opening(m, se)
     comp, cmin, csz = label(o, conn)
     kept, K = keep_largest(comp, csz) if keep == "largest" else filter_components(comp, csz, min_size)
