@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--spans", action="store_true", help="also produce the NEXT-1 row spans (roix_row_spans)")
     ap.add_argument("--classes", type=int, default=2, choices=[2, 3],
                     help="a3 class count: 2 (Otsu) or 3 (multi-Otsu, NEXT-3)")
+    ap.add_argument("--frames", action="store_true",
+                    help="NEXT-3 per-frame thresholds (uint16 frame stacks, e.g. C3): histogram/Otsu per z-plane")
+    ap.add_argument("--keep", default="size", choices=["size", "largest"],
+                    help="a7: drop components < min_size (default) or keep only the largest (NEXT-3)")
     ap.add_argument("--no-next4", action="store_true",
                     help="skip the NEXT-4 items (reconstruction timing, quality vs the phantom's ground truth)")
     ap.add_argument("--greedy", type=float, default=None, metavar="E",
@@ -131,7 +135,7 @@ def cpu_info():
 
 
 # ------------------------------------------------------------------------------- oracle timing
-def time_oracle(x_np, cfg, budget_s=15.0, max_reps=1, classes=2):
+def time_oracle(x_np, cfg, budget_s=15.0, max_reps=1, classes=2, frames=False, keep="size"):
     """Time the oracle pipeline (single-threaded) on x_np; returns (seconds per pass, passes)."""
     import oracle
 
@@ -140,7 +144,7 @@ def time_oracle(x_np, cfg, budget_s=15.0, max_reps=1, classes=2):
     for _ in range(max_reps):
         t0 = time.perf_counter()
         oracle.pipeline(x_np, eb=cfg.eb or None, rel_eb=cfg.rel_eb or None, conn=cfg.conn, se=cfg.se,
-                        min_size=cfg.min_size, polarity=cfg.polarity, classes=classes)
+                        min_size=cfg.min_size, polarity=cfg.polarity, classes=classes, frames=frames, keep=keep)
         times.append(time.perf_counter() - t0)
         if sum(times) > budget_s:
             break
@@ -174,10 +178,10 @@ def reference_arm(args, cfg):
 
     oracle.build()
     for _ in range(max(0, min(args.warmup, 1))):
-        time_oracle(x_np, cfg, classes=args.classes)
+        time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep)
     ts = []
     for _ in range(args.steps):
-        t, _ = time_oracle(x_np, cfg, classes=args.classes)
+        t, _ = time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep)
         ts.append(t)
     per = sum(ts) / len(ts)
     value = x_np.nbytes / per / 1e9
@@ -187,7 +191,7 @@ def reference_arm(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u16" if cfg.dtype == "u16" else "f32",
             "data": "synthetic", "config": {"workload": cfg.name, "shape": list(cfg.shape), "sample_planes": nz,
-                                            "classes": args.classes},
+                                            "classes": args.classes, "frames": args.frames, "keep": args.keep},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -224,7 +228,7 @@ def main():
     x = synth.generate(cfg, z0=z0, nz=z1 - z0, device=dev)
     torch.cuda.synchronize()
     kw = dict(eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=cfg.polarity,
-              classes=args.classes)
+              classes=args.classes, frames=args.frames, keep=args.keep)
     if world > 1:
         from paper_2602_15917_b200.sharded import ShardedPipeline
 
@@ -328,7 +332,7 @@ def main():
         "config": {"workload": cfg.name, "shape": list(cfg.shape), "input_dtype": cfg.dtype, "eb": cfg.eb,
                    "rel_eb": cfg.rel_eb, "conn": cfg.conn, "se": cfg.se, "min_size": cfg.min_size,
                    "polarity": "LOW" if cfg.polarity else "HIGH", "classes": args.classes,
-                   "parallelism": "zslab%d" % world,
+                   "frames": args.frames, "keep": args.keep, "parallelism": "zslab%d" % world,
                    "l2": "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
         "roofline": {"bound": "hbm", "kernel": STAGE_CALLS.get(dom, dom), "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "alg_bytes": ab[dom],
@@ -352,7 +356,7 @@ def main():
     if not args.no_cpu_baseline and world == 1 and rank == 0:
         nz = sample_planes(cfg, 6e6)
         x_np = synth.to_numpy(x[:nz], cfg)
-        t, reps = time_oracle(x_np, cfg, classes=args.classes)
+        t, reps = time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep)
         line["cpu_baseline"] = {"value": x_np.nbytes / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": "%s planes [0,%d) (%d voxels, %.1f MB), whole oracle pipeline, best of %d" %
                                           (cfg.name, nz, x_np.size, x_np.nbytes / 1e6, reps)}

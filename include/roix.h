@@ -168,6 +168,29 @@ roix_status roix_threshold_multi(const uint64_t *hist, uint32_t nbins, roix_dtyp
                                  uint32_t classes, roix_scalars *sc, roix_stream_t stream);
 
 /*
+ * NEXT-3 PER-FRAME THRESHOLDS (uint16 frame stacks, e.g. detector frames, C3): every z-plane of the
+ * slab is its own image, as in the paper's 2-D pipeline -- its own I_max (Eq. 1),
+ * norm8 histogram and (multi-)Otsu thresholds.
+ *   roix_histogram_frames   hist[z * 65536 + v] += #{voxels of frame z equal to v}, z < g->nz
+ *   roix_threshold_frames   frames[z] from frame z's histogram: i_max, t8_all (every threshold, one
+ *                           per byte), t8 (the ROI threshold, as roix_threshold_multi) and thr_u16 =
+ *                           the first value v with norm8_z(v) > t8; sc->polarity set.  A frame with
+ *                           too few populated bins sets ROIX_ERR_DEGENERATE.
+ *   roix_morph_frames       roix_morph (u16) with frame z binarised against frames[z].thr_u16.
+ */
+typedef struct roix_frame {
+    uint32_t thr_u16; /* raw threshold: ROI = x >= thr_u16 (HIGH) or x < thr_u16 (LOW) */
+    uint32_t t8;      /* ROI threshold on the frame's norm8 scale                       */
+    uint32_t t8_all;  /* every threshold, ascending, one per byte                       */
+    uint32_t i_max;   /* the frame's I_max (Eq. 1)                                      */
+} roix_frame;
+
+roix_status roix_histogram_frames(const uint16_t *x, const roix_geom *g, roix_scalars *sc, uint64_t *hist,
+                                  roix_stream_t stream);
+roix_status roix_threshold_frames(const uint64_t *hist, uint64_t nframes, roix_polarity polarity, uint32_t classes,
+                                  roix_scalars *sc, roix_frame *frames, roix_stream_t stream);
+
+/*
  * a4+a5 BINARISE + OPEN (Eq. 2; G-11).  m = [norm8(x) > t8] (HIGH) or [<= t8] (LOW), evaluated as
  * the equivalent raw compare against thr_*; o = dilate(erode(m)) with the radius-1 cross:
  *   se = 6: 6 face neighbours (3-D);  se = 4: the 4 in-plane neighbours (2-D per z-plane).
@@ -203,6 +226,10 @@ roix_status roix_histogram_binarize(const void *x, roix_dtype dtype, const roix_
 roix_status roix_morph_prebinarized(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se,
                                     const uint32_t *halo_lo, const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits,
                                     uint32_t *row_runs, void *ws, size_t ws_bytes, roix_stream_t stream);
+
+roix_status roix_morph_frames(const uint16_t *x, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
+                             const uint32_t *halo_hi, const roix_frame *frames, roix_scalars *sc, uint32_t *o_bits,
+                             uint32_t *row_runs, void *ws, size_t ws_bytes, roix_stream_t stream);
 
 /* Binarise planes [p0, p0+np) of the slab (slab-local plane numbers) into m_bits, each plane
  * packed from bit 0 with ceil(ny*nx/32) words -- the halo planes roix_morph consumes. */

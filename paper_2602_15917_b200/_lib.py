@@ -16,6 +16,12 @@ U16, F32 = 1, 2
 POL_HIGH, POL_LOW = 0, 1
 
 
+class Frame(ctypes.Structure):
+    """Mirror of roix_frame (NEXT-3 per-frame thresholds)."""
+    _fields_ = [("thr_u16", ctypes.c_uint32), ("t8", ctypes.c_uint32), ("t8_all", ctypes.c_uint32),
+                ("i_max", ctypes.c_uint32)]
+
+
 class Scalars(ctypes.Structure):
     """Mirror of roix_scalars (device-resident; read back with ``Scalars.from_buffer_copy``)."""
     _fields_ = [("err", ctypes.c_uint32), ("min_ord", ctypes.c_uint32), ("max_ord", ctypes.c_uint32),
@@ -91,6 +97,10 @@ _SIGS = {
     "roix_label_largest": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, _vp, _vp, _u64, _u32, _vp, _vp, _vp]),
     "roix_label_finish_keep": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _u64, _vp,
                                       ctypes.POINTER(LabelOut), _vp, _vp]),
+    "roix_histogram_frames": (_i32, [_vp, ctypes.POINTER(Geom), _vp, _vp, _vp]),
+    "roix_threshold_frames": (_i32, [_vp, _u64, _i32, _u32, _vp, _vp, _vp]),
+    "roix_morph_frames": (_i32, [_vp, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t,
+                                 _vp]),
     "roix_threshold_multi": (_i32, [_vp, _u32, _i32, _i32, _u32, _vp, _vp]),
     "roix_decode_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_decode": (_i32, [_vp, _vp, _u64, _i32, _u64, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
@@ -148,6 +158,9 @@ roix_extract_runs = _wrap("roix_extract_runs")
 roix_row_spans = _wrap("roix_row_spans")
 roix_greedy_quantize = _wrap("roix_greedy_quantize")
 roix_threshold_multi = _wrap("roix_threshold_multi")
+roix_histogram_frames = _wrap("roix_histogram_frames")
+roix_threshold_frames = _wrap("roix_threshold_frames")
+roix_morph_frames = _wrap("roix_morph_frames")
 roix_label_largest = _wrap("roix_label_largest")
 roix_label_finish_keep = _wrap("roix_label_finish_keep")
 KEEP_LARGEST = (1 << 64) - 1

@@ -160,6 +160,40 @@ roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint
                 "roix_morph");
 }
 
+roix_status roix_morph_frames(const uint16_t *x, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
+                             const uint32_t *halo_hi, const roix_frame *frames, roix_scalars *sc, uint32_t *o_bits,
+                             uint32_t *row_runs, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    if (!sc || !o_bits || !ws || !frames) return invalid("sc / o_bits / ws / frames is NULL");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (se != 6 && se != 4) return unsupported("se must be 6 (3-D cross) or 4 (in-plane cross)");
+    if (!x || !aligned16(x) || !aligned16(o_bits)) return invalid("x / o_bits must be 16-byte aligned");
+    roix_status s = check_halos(g, se, halo_lo, halo_hi);
+    if (s != ROIX_OK) return s;
+    if (g->nx > (1u << 30)) return unsupported("rows longer than 2^30 voxels");
+    if (ws_bytes < morph_workspace_bytes(*g) || !aligned16(ws)) return invalid("workspace (see roix_morph_workspace)");
+    return cuda(launch_morph(x, ROIX_U16, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, ws, 0, (cudaStream_t)stream,
+                             frames),
+                "roix_morph_frames");
+}
+
+roix_status roix_histogram_frames(const uint16_t *x, const roix_geom *g, roix_scalars *sc, uint64_t *hist,
+                                  roix_stream_t stream) {
+    if (!sc || !hist) return invalid("sc / hist is NULL");
+    if (!geom_ok(g)) return invalid("geometry");
+    if (g->nz * g->ny * g->nx && (!x || !aligned16(x))) return invalid("x must be a 16-byte aligned device pointer");
+    return cuda(launch_hist_u16_frames(x, g->nz, g->ny * g->nx, sc, hist, (cudaStream_t)stream),
+                "roix_histogram_frames");
+}
+
+roix_status roix_threshold_frames(const uint64_t *hist, uint64_t nframes, roix_polarity polarity, uint32_t classes,
+                                  roix_scalars *sc, roix_frame *frames, roix_stream_t stream) {
+    if (classes != 2 && classes != 3) return unsupported("classes must be 2 or 3");
+    if (!sc || (nframes && (!hist || !frames))) return invalid("sc / hist / frames is NULL");
+    if (polarity != ROIX_POL_HIGH && polarity != ROIX_POL_LOW) return invalid("polarity");
+    return cuda(launch_threshold_frames(hist, nframes, (int)polarity, (int)classes, sc, frames, (cudaStream_t)stream),
+                "roix_threshold_frames");
+}
+
 roix_status roix_histogram_binarize_workspace(const roix_geom *g, size_t *ws_bytes) {
     if (!ws_bytes) return invalid("ws_bytes is NULL");
     if (!geom_ok(g)) return invalid("geometry");

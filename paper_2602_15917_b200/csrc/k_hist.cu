@@ -55,6 +55,40 @@ __global__ void __launch_bounds__(1024, 2) k_hist_u16(const uint16_t *__restrict
     }
 }
 
+// NEXT-3 per-frame histograms (uint16 frame stacks): frame z = voxels [z A, (z + 1) A) into
+// gh + z * 65536; blockIdx.y = frame, the same privatised window as k_hist_u16.  Frames need not start
+// on a 16-byte boundary: the unaligned head and tail of each frame go voxel by voxel.
+__global__ void __launch_bounds__(1024, 2) k_hist_u16_frames(const uint16_t *__restrict__ x, uint64_t A,
+                                                              roix_scalars *sc, uint64_t *gh_all) {
+    extern __shared__ uint32_t sh[];
+    if (get_err(sc)) return;
+    uint64_t *gh = gh_all + (uint64_t)blockIdx.y * 65536;
+    for (int i = threadIdx.x; i < HWIN; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint64_t s = (uint64_t)blockIdx.y * A, e = s + A;
+    const uint64_t a = min(e, (uint64_t)((s + 7) & ~7ull)), e8 = max(a, (uint64_t)(e & ~7ull));
+    if (blockIdx.x == 0) {
+        if (threadIdx.x < a - s) hist_add(sh, gh, x[s + threadIdx.x]);
+        if (threadIdx.x < e - e8) hist_add(sh, gh, x[e8 + threadIdx.x]);
+    }
+    const uint4 *x8 = reinterpret_cast<const uint4 *>(x);
+    for (uint64_t i = a / 8 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e8 / 8;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 v = __ldcs(x8 + i);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            hist_add(sh, gh, w[k] & 0xffffu);
+            hist_add(sh, gh, w[k] >> 16);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < HWIN; b += blockDim.x) {
+        const uint32_t c = sh[b];
+        if (c) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)c);
+    }
+}
+
 // norm8 of a finite fp32 value from the edges table e[0..256] (e[0] = -inf, e[256] = +inf):
 // norm8(x) = #{k >= 1 : x >= e[k]} -- an estimate from x * 255 / I_max corrected against the edges.
 // x * fl(255 / I_max) is within ~3e-5 of the exact 255 x / I_max for x <= I_max, so the estimate is
@@ -212,6 +246,26 @@ cudaError_t launch_hist_u16(const uint16_t *x, uint64_t n, roix_scalars *sc, uin
         attr = true;
     }
     k_hist_u16<<<grid_for(n / 8, 1024, 2), 1024, HWIN * 4, st>>>(x, n, sc, hist);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hist_u16_frames(const uint16_t *x, uint64_t nframes, uint64_t A, roix_scalars *sc, uint64_t *hist,
+                                   cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(k_hist_u16_frames, cudaFuncAttributeMaxDynamicSharedMemorySize, HWIN * 4);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    if (nframes == 0 || A == 0) return cudaSuccess;
+    const uint64_t per = (uint64_t)num_sms() * 2 / nframes;          // fill the GPU once over all frames
+    const uint64_t need = (A / 8 + 1023) / 1024;
+    const unsigned bpf = (unsigned)max((uint64_t)1, min(per, need));
+    for (uint64_t z0 = 0; z0 < nframes; z0 += 65535) {
+        const unsigned nz = (unsigned)min(nframes - z0, (uint64_t)65535);
+        k_hist_u16_frames<<<dim3(bpf, nz), 1024, HWIN * 4, st>>>(x + z0 * A, A, sc, hist + z0 * 65536);
+    }
     return cudaGetLastError();
 }
 

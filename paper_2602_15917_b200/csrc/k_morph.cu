@@ -175,9 +175,58 @@ __device__ __forceinline__ void write_row_atomic(uint32_t *o, uint64_t bitpos, u
 // One warp iteration = 32 mask words = 1024 voxels; lane l loads the 16-byte groups c*32 + l
 // (c < CH), packs their VPL-bit masks into P = sum_c b_c << (c VPL), then lane j gathers word j from
 // the GPW lanes that hold its groups.
-template <typename T>
+// NEXT-3 per-frame thresholds (uint16 frame stacks): voxel v of plane p = v / A compares against
+// frames[p].thr_u16.  A warp iteration covers 1024 voxels, so for A >= 1024 it meets at most one plane
+// boundary b1: a 16-byte group uses the threshold of its plane, a group straddling b1 goes voxel by
+// voxel; A < 1024 (tiny frames) divides per voxel.
+struct FrameThr {
+    const roix_frame *f;
+    uint64_t A;
+};
+
+__device__ __forceinline__ uint32_t u16_of(uint4 v, int k) {
+    const uint32_t w = k < 2 ? v.x : k < 4 ? v.y : k < 6 ? v.z : v.w;
+    return (k & 1) ? w >> 16 : w & 0xffffu;
+}
+
+template <typename T, bool FR>
+__device__ __forceinline__ uint32_t group_bits(const Cmp<T> &cmp, uint4 vec, uint64_t v0, const FrameThr &F,
+                                               uint64_t p0, uint64_t b1, uint32_t t0, uint32_t t1) {
+    if constexpr (!FR) {
+        return cmp.bits(vec);
+    } else {
+        constexpr int VPL = Cmp<T>::VPL;
+        Cmp<T> c = cmp;
+        if (F.A >= 1024) {
+            if (v0 + VPL <= b1 || v0 >= b1) {
+                c.thr = v0 < b1 ? t0 : t1;
+                return c.bits(vec);
+            }
+            uint32_t b = 0;
+            for (int k = 0; k < VPL; k++) b |= ((u16_of(vec, k) >= (v0 + k < b1 ? t0 : t1)) ^ c.low) << k;
+            return b;
+        }
+        uint32_t b = 0;
+        for (int k = 0; k < VPL; k++) b |= ((u16_of(vec, k) >= F.f[(v0 + k) / F.A].thr_u16) ^ c.low) << k;
+        return b;
+    }
+}
+
+template <typename T, bool FR>
+__device__ __forceinline__ uint32_t voxel_bit(const Cmp<T> &cmp, T val, uint64_t v, const FrameThr &F) {
+    if constexpr (!FR) {
+        return cmp.bit1(val);
+    } else {
+        return ((uint32_t)val >= F.f[v / F.A].thr_u16) ^ cmp.low;
+    }
+}
+
+// One warp iteration = 32 mask words = 1024 voxels; lane l loads the 16-byte groups c*32 + l
+// (c < CH), packs their VPL-bit masks into P = sum_c b_c << (c VPL), then lane j gathers word j from
+// the GPW lanes that hold its groups.
+template <typename T, bool FR = false>
 __global__ void __launch_bounds__(256) k_binarize(const T *__restrict__ x, uint64_t n, roix_scalars *sc,
-                                                  uint32_t *__restrict__ m, int skip_if_resolved) {
+                                                  uint32_t *__restrict__ m, int skip_if_resolved, FrameThr F) {
     if (get_err(sc)) return;
     if (skip_if_resolved && sc->spec_state == 2) return;   // the fused pass already produced m
     constexpr int VPL = Cmp<T>::VPL, CH = 32 / VPL, GPW = 32 / VPL;
@@ -189,21 +238,32 @@ __global__ void __launch_bounds__(256) k_binarize(const T *__restrict__ x, uint6
     const uint64_t nwords = (n + 31) / 32;
     for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < iters; it += wstride) {
         const uint64_t g0 = it * 32 * CH;  // first 16-byte group of the iteration
+        uint64_t p0 = 0, b1 = ~0ull;
+        uint32_t t0 = 0, t1 = 0;
+        if constexpr (FR) {
+            if (F.A >= 1024) {
+                p0 = it * 1024 / F.A;
+                b1 = (p0 + 1) * F.A;
+                t0 = F.f[p0].thr_u16;
+                t1 = b1 < n ? F.f[p0 + 1].thr_u16 : t0;
+            }
+        }
         uint32_t P = 0;
         if ((it + 1) * 1024 <= n) {
             uint4 v[CH];
 #pragma unroll
             for (int c = 0; c < CH; c++) v[c] = __ldcs(x4 + g0 + c * 32 + lane);
 #pragma unroll
-            for (int c = 0; c < CH; c++) P |= cmp.bits(v[c]) << (c * VPL);
+            for (int c = 0; c < CH; c++)
+                P |= group_bits<T, FR>(cmp, v[c], (g0 + c * 32 + lane) * VPL, F, p0, b1, t0, t1) << (c * VPL);
         } else {
             for (int c = 0; c < CH; c++) {
                 const uint64_t v0 = (g0 + c * 32 + lane) * VPL;
                 uint32_t b = 0;
-                if (v0 + VPL <= n) b = cmp.bits(__ldcs(x4 + g0 + c * 32 + lane));
+                if (v0 + VPL <= n) b = group_bits<T, FR>(cmp, __ldcs(x4 + g0 + c * 32 + lane), v0, F, p0, b1, t0, t1);
                 else
                     for (int k = 0; k < VPL; k++)
-                        if (v0 + k < n) b |= cmp.bit1(x[v0 + k]) << k;
+                        if (v0 + k < n) b |= voxel_bit<T, FR>(cmp, x[v0 + k], v0 + k, F) << k;
                 P |= b << (c * VPL);
             }
         }
@@ -897,7 +957,7 @@ size_t morph_workspace_bytes(const roix_geom &g) { return ((g.nz * g.ny * g.nx +
 
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
                          const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
-                         int prebinarized, cudaStream_t st) {
+                         int prebinarized, cudaStream_t st, const roix_frame *frames) {
     MorphArgs A = {};
     A.nz = g.nz;
     A.ny = g.ny;
@@ -948,9 +1008,12 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         uint64_t blocks = (iters + 7) / 8;
         uint64_t cap = (uint64_t)num_sms() * 8;
         if (blocks > cap) blocks = cap;
-        if (dtype == ROIX_U16)
-            k_binarize<uint16_t><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x, n, sc, m, prebinarized);
-        else k_binarize<float><<<(unsigned)blocks, 256, 0, st>>>((const float *)x, n, sc, m, prebinarized);
+        const FrameThr F = {frames, g.ny * g.nx};
+        if (frames)
+            k_binarize<uint16_t, true><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x, n, sc, m, 0, F);
+        else if (dtype == ROIX_U16)
+            k_binarize<uint16_t><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x, n, sc, m, prebinarized, F);
+        else k_binarize<float><<<(unsigned)blocks, 256, 0, st>>>((const float *)x, n, sc, m, prebinarized, F);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     int occ = 0;

@@ -325,6 +325,33 @@ __global__ void __launch_bounds__(1024) k_threshold(const uint64_t *__restrict__
     }
 }
 
+// NEXT-3 per-frame thresholds: one CTA per frame of a uint16 stack, each the whole k_threshold on its
+// own 65536-bin histogram (its I_max, norm8 fold, (multi-)Otsu); results in frames[z].
+__global__ void __launch_bounds__(1024) k_threshold_frames(const uint64_t *__restrict__ hist, int polarity,
+                                                            int classes, roix_scalars *sc, roix_frame *frames) {
+    if (get_err(sc)) return;
+    const uint64_t z = blockIdx.x;
+    uint32_t imax;
+    int t8, t8_hi = -1;
+    otsu_block(hist + z * 65536, ROIX_U16, &imax, &t8, classes, &t8_hi);
+    if (threadIdx.x == 0) {
+        if (z == 0) sc->polarity = (uint32_t)polarity;
+        roix_frame f;
+        f.i_max = imax;
+        if (t8 < 0) {
+            set_err(sc, ROIX_ERR_DEGENERATE);
+            f.t8 = f.t8_all = 0;
+            f.thr_u16 = 65536;
+        } else {
+            f.t8_all = classes == 3 ? (uint32_t)t8 | ((uint32_t)t8_hi << 8) : (uint32_t)t8;
+            if (classes == 3 && polarity == ROIX_POL_LOW) t8 = t8_hi;
+            f.t8 = (uint32_t)t8;
+            f.thr_u16 = thr_u16_of(imax, t8);
+        }
+        frames[z] = f;
+    }
+}
+
 // Speculative threshold window from a sample histogram (roix_histogram_binarize): the exact raw
 // threshold is expected within [spec_lo, spec_hi] -- Otsu on the sample +- SPEC_D norm8 bins, and for
 // u16 an I_max up to 1/8 above the sample maximum.  spec_state = 1 (window set) or 3 (no window).
@@ -360,6 +387,15 @@ __global__ void __launch_bounds__(1024) k_spec(const uint64_t *__restrict__ shis
 cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st,
                              int classes) {
     roix::k_threshold<<<1, 1024, 0, st>>>(hist, dtype, polarity, classes, sc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_threshold_frames(const uint64_t *hist, uint64_t nframes, int polarity, int classes,
+                                    roix_scalars *sc, roix_frame *frames, cudaStream_t st) {
+    for (uint64_t z0 = 0; z0 < nframes; z0 += 65535) {
+        const unsigned nz = (unsigned)min(nframes - z0, (uint64_t)65535);
+        roix::k_threshold_frames<<<nz, 1024, 0, st>>>(hist + z0 * 65536, polarity, classes, sc, frames + z0);
+    }
     return cudaGetLastError();
 }
 

@@ -31,7 +31,7 @@ cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix
 size_t morph_workspace_bytes(const roix_geom &g);
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
                          const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
-                         int prebinarized, cudaStream_t st);
+                         int prebinarized, cudaStream_t st, const roix_frame *frames = nullptr);
 cudaError_t launch_spec(const uint64_t *shist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st);
 size_t fused_workspace_bytes(const roix_geom &g);
 cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom &g, int polarity, roix_scalars *sc,
@@ -92,3 +92,8 @@ cudaError_t launch_decode_spans(const roix_span *spans, uint64_t span_cap, const
                                 void *ws, cudaStream_t st);
 cudaError_t launch_confusion(const uint32_t *pred, const uint32_t *truth, uint64_t n, uint64_t *counts,
                              cudaStream_t st);
+
+cudaError_t launch_hist_u16_frames(const uint16_t *x, uint64_t nframes, uint64_t A, roix_scalars *sc, uint64_t *hist,
+                                   cudaStream_t st);
+cudaError_t launch_threshold_frames(const uint64_t *hist, uint64_t nframes, int polarity, int classes,
+                                    roix_scalars *sc, roix_frame *frames, cudaStream_t st);

@@ -46,7 +46,7 @@ class Pipeline:
 
     def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
                  run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="mask",
-                 spans=False, classes=2, keep="size"):
+                 spans=False, classes=2, keep="size", frames=False):
         L.load()
         self.shape = tuple(int(v) for v in shape)
         Z, Y, X = self.shape
@@ -70,13 +70,19 @@ class Pipeline:
             raise ValueError("keep must be 'size' or 'largest'")
         self.keep = keep
         self.label_min_size = L.KEEP_LARGEST if keep == "largest" else self.min_size
+        # a2-a4 per frame (NEXT-3, uint16 frame stacks): each z-plane its own image -- own histogram,
+        # I_max and threshold (roix_histogram_frames / roix_threshold_frames / roix_morph_frames)
+        self.frames = bool(frames)
+        if self.frames and (dtype != "u16" or fused):
+            raise ValueError("per-frame thresholds need uint16 input and the unfused path")
         self.device = torch.device(device or "cuda")
         dev = self.device
         self.geom = L.Geom(Z, Y, X, 0, Z)
         self.nwords = (self.n + 31) // 32
         self.sc = torch.zeros(L.scalars_size(), dtype=torch.uint8, device=dev)
         self.nbins = 65536 if dtype == "u16" else 256
-        self.hist = torch.zeros(self.nbins, dtype=torch.int64, device=dev)
+        self.hist = torch.zeros(self.nbins * (Z if frames else 1), dtype=torch.int64, device=dev)
+        self.frame_thr = torch.zeros(4 * max(Z, 1), dtype=torch.int32, device=dev) if frames else None   # roix_frame
         self.o = torch.empty(self.nwords + 4, dtype=torch.int32, device=dev)   # o, then K in place
         self.row_runs = torch.empty(Z * Y, dtype=torch.int32, device=dev)
         # fused (speculative) histogram + binarisation: one read of x for a2 + a4 (roix_histogram_binarize);
@@ -138,6 +144,17 @@ class Pipeline:
         self.hist.zero_()
         mark("setup")
         ws, wsb = _ptr(self.morph_ws), self.morph_ws.numel()
+        if self.frames:
+            L.roix_histogram_frames(xp, ctypes.byref(self.geom), sc, _ptr(self.hist), st)
+            mark("histogram")
+            L.roix_threshold_frames(_ptr(self.hist), self.shape[0], self.polarity, self.classes, sc,
+                                    _ptr(self.frame_thr), st)
+            mark("threshold")
+            L.roix_morph_frames(xp, ctypes.byref(self.geom), self.se, None, None, _ptr(self.frame_thr), sc,
+                                _ptr(self.o), _ptr(self.row_runs), ws, wsb, st)
+            mark("morph")
+            self._label_extract(xp, sc, st, mark)
+            return
         if self.fused:
             L.roix_histogram_binarize(xp, self.cdtype, ctypes.byref(self.geom), self.polarity, sc, _ptr(self.hist),
                                       self.nbins, ws, wsb, st)
@@ -150,6 +167,10 @@ class Pipeline:
         morph(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o), _ptr(self.row_runs),
               ws, wsb, st)
         mark("morph")
+        self._label_extract(xp, sc, st, mark)
+
+    def _label_extract(self, xp, sc, st, mark):
+        n = self.n
         out = L.LabelOut(self.o.data_ptr(), self.comp_min.data_ptr(), self.comp_size.data_ptr(),
                          self.comp_kept.data_ptr(), self.comp_cap,
                          self.labels.data_ptr() if self.labels is not None else None)
@@ -170,6 +191,11 @@ class Pipeline:
                              _ptr(self.span_codes), self.span_codes.numel(), _ptr(self.span_counts),
                              _ptr(self.span_ws), self.span_ws.numel(), st)
             mark("spans")
+
+    def frame_thresholds(self):
+        """Per-frame results of the last run (frames=True): list of roix_frame records."""
+        a = self.frame_thr.cpu().numpy().view(np.uint32).reshape(-1, 4)
+        return [L.Frame(*map(int, r)) for r in a]
 
     def row_spans(self):
         """(records (m, 3) int64: row, x_start, x_end; section codes) of the last run (spans=True)."""

@@ -37,6 +37,8 @@ class SlabState(Pipeline):
         self.global_shape = tuple(shape)
         self.rank, self.world, self.z0, self.nz = rank, world, z0, nz
         super().__init__((nz, Y, X), dtype, **kw)
+        if self.frames and self.se == 6 and world > 1:
+            raise ValueError("per-frame thresholds on a sharded stack need in-plane morphology (se = 4)")
         self.geom = L.Geom(nz, Y, X, z0, Z)            # slab geometry in the global volume
         wsb = L.roix_histogram_binarize_workspace(self.geom) if self.fused else L.roix_morph_workspace(self.geom)
         self.morph_ws = torch.empty(wsb, dtype=torch.uint8, device=self.device)
@@ -83,15 +85,23 @@ def slab_program(S, x, stream=None, mark=None):
     S.hist.zero_()
     mark("setup")
     mws, mwsb = _ptr(S.morph_ws), S.morph_ws.numel()
-    if S.fused:
+    frames = S.frames
+    if frames:
+        # per-frame thresholds (NEXT-3): frames never span slabs, so no histogram exchange
+        L.roix_histogram_frames(xp, ctypes.byref(S.geom), sc, _ptr(S.hist), st)
+        mark("histogram")
+        L.roix_threshold_frames(_ptr(S.hist), S.nz, S.polarity, S.classes, sc, _ptr(S.frame_thr), st)
+        mark("threshold")
+    elif S.fused:
         L.roix_histogram_binarize(xp, S.cdtype, ctypes.byref(S.geom), S.polarity, sc, _ptr(S.hist), S.nbins, mws,
                                   mwsb, st)
     else:
         L.roix_histogram(xp, S.cdtype, n, sc, _ptr(S.hist), S.nbins, st)
-    yield ("sum", S.hist)                                         # X1
-    mark("histogram")
-    L.roix_threshold_multi(_ptr(S.hist), S.nbins, S.cdtype, S.polarity, S.classes, sc, st)
-    mark("threshold")
+    if not frames:
+        yield ("sum", S.hist)                                     # X1
+        mark("histogram")
+        L.roix_threshold_multi(_ptr(S.hist), S.nbins, S.cdtype, S.polarity, S.classes, sc, st)
+        mark("threshold")
     halo_lo = halo_hi = None
     if S.se == 6 and G > 1:
         if S.nz < 2:
@@ -105,8 +115,13 @@ def slab_program(S, x, stream=None, mark=None):
         if g < G - 1:
             halo_hi = _ptr(S.halo_recv[1])
         assert pw > 0
-    morph = L.roix_morph_prebinarized if S.fused else L.roix_morph
-    morph(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o), _ptr(S.row_runs), mws, mwsb, st)
+    if frames:
+        L.roix_morph_frames(xp, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, _ptr(S.frame_thr), sc, _ptr(S.o),
+                            _ptr(S.row_runs), mws, mwsb, st)
+    else:
+        morph = L.roix_morph_prebinarized if S.fused else L.roix_morph
+        morph(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o), _ptr(S.row_runs), mws, mwsb,
+              st)
     mark("morph")
     out = L.LabelOut(S.o.data_ptr(), S.comp_min.data_ptr(), S.comp_size.data_ptr(), S.comp_kept.data_ptr(),
                      S.comp_cap, S.labels.data_ptr() if S.labels is not None else None)

@@ -316,3 +316,38 @@ def test_sharded_keep_largest_g_invariant():
         np.testing.assert_array_equal(keep.reshape(cfg.shape), ref["K"])
         assert torch.equal(torch.cat([S.collect().codes for S in states]), one.codes)
         assert sum(S.scalars().n_kept for S in states) == 1
+
+
+# ------------------------------------------------------------------ NEXT-3 per-frame thresholds
+@pytest.mark.parametrize("classes", [2, 3])
+def test_pipeline_frames_vs_oracle(classes):
+    """C3-style detector frames (LOW polarity, se = 4, conn = 8) with per-frame thresholds, end to end."""
+    cfg = synth.scaled("C3", 0.25, frames=6)
+    x = synth.generate(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size,
+                 polarity=cfg.polarity, classes=classes, frames=True)
+    res = p.run(x)
+    x_np = synth.to_numpy(x, cfg)
+    ref = oracle.pipeline(x_np, eb=cfg.eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=cfg.polarity,
+                          classes=classes, frames=True)
+    assert res.scalars.err == 0
+    got = p.frame_thresholds()
+    assert [(f.i_max, f.t8) for f in got] == [(imax, t8) for imax, _, t8 in ref["frames"]]
+    np.testing.assert_array_equal(words_to_mask(res.keep_bits, p.n).reshape(cfg.shape), ref["K"])
+    np.testing.assert_array_equal(res.comp_min.cpu().numpy(), ref["comp_min"].astype(np.int64))
+    c = res.codes.cpu().numpy()
+    np.testing.assert_array_equal(c.view(np.uint16), ref["stream"])
+
+
+def test_sharded_frames_g_invariant():
+    from paper_2602_15917_b200.sharded import run_simulated
+
+    cfg = synth.scaled("C3", 0.125, frames=8)
+    x = synth.generate(cfg)
+    kw = dict(eb=cfg.eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=cfg.polarity, frames=True)
+    one = Pipeline(cfg.shape, cfg.dtype, **kw).run(x)
+    for G in (2, 4):
+        states = run_simulated(x, G, **kw)
+        keep = np.concatenate([words_to_mask(S.collect().keep_bits, S.n) for S in states])
+        np.testing.assert_array_equal(keep, words_to_mask(one.keep_bits, one_n(cfg)))
+        assert torch.equal(torch.cat([S.collect().codes for S in states]), one.codes)

@@ -219,6 +219,78 @@ def test_threshold_multi_u16_raw_hist():
         assert s.t8 == t8 and oracle.norm8_u16(s.thr_u16, imax) > t8 >= oracle.norm8_u16(s.thr_u16 - 1, imax)
 
 
+# ------------------------------------------------ NEXT-3 per-frame thresholds (uint16 frame stacks)
+FRAME_SHAPES = [(1, 1, 1), (3, 5, 7), (4, 9, 13), (6, 33, 31), (5, 32, 32), (3, 40, 1390), (7, 17, 100), (2, 64, 512),
+                (130, 3, 5)]
+
+
+def _frame_stack(rng, shape):
+    Z, Y, X = shape
+    base = rng.uniform(300, 3000, Z)[:, None, None]
+    x = rng.normal(base, 40, shape)
+    yy, xx = np.indices((Y, X))
+    blob = ((yy - Y / 2) ** 2 / max(Y / 3, 1) ** 2 + (xx - X / 2) ** 2 / max(X / 4, 1) ** 2) < 1
+    x[:, blob] += rng.uniform(1500, 20000, Z)[:, None]
+    x[:, 0, 0] = 0                                      # every frame has >= 2 populated bins
+    return np.clip(x, 0, 65535).astype(np.uint16)
+
+
+def _frames_gpu(x_np, pol, classes, se=4):
+    Z, Y, X = x_np.shape
+    x = dev(x_np)
+    g = L.Geom(Z, Y, X, 0, Z)
+    sc = new_sc(1.0)
+    L.roix_resolve(ptr(sc), L.U16, 0.0, st())
+    h = torch.zeros(Z * 65536, dtype=torch.int64, device="cuda")
+    L.roix_histogram_frames(ptr(x), ctypes.byref(g), ptr(sc), ptr(h), st())
+    fr = torch.full((4 * Z,), -1, dtype=torch.int32, device="cuda")
+    L.roix_threshold_frames(ptr(h), Z, pol, classes, ptr(sc), ptr(fr), st())
+    o = torch.full(((x_np.size + 31) // 32 + 4,), -1, dtype=torch.int32, device="cuda")
+    runs = torch.full((Z * Y,), -1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(L.roix_morph_workspace(g), dtype=torch.uint8, device="cuda")
+    L.roix_morph_frames(ptr(x), ctypes.byref(g), se, None, None, ptr(fr), ptr(sc), ptr(o), ptr(runs), ptr(ws),
+                        ws.numel(), st())
+    s = read_sc(sc)
+    return s, h.cpu().numpy().reshape(Z, 65536), fr.cpu().numpy().view(np.uint32).reshape(Z, 4), o, ws
+
+
+@pytest.mark.parametrize("shape", FRAME_SHAPES)
+@pytest.mark.parametrize("classes", [2, 3])
+def test_frames_vs_oracle(shape, classes):
+    """roix_histogram_frames / roix_threshold_frames / roix_morph_frames against the oracle's per-frame
+    statement: frame sizes that are not multiples of 8 voxels (unaligned frame starts), frames smaller
+    than a 1024-voxel warp iteration, 16-byte groups straddling frames, both polarities."""
+    rng = np.random.default_rng(abs(hash((shape, classes, "frames"))) % 2 ** 32)
+    x_np = _frame_stack(rng, shape)
+    Z = shape[0]
+    for pol in (0, 1):
+        try:
+            ft = oracle.frame_thresholds(x_np, classes, pol)
+        except oracle.Degenerate:
+            s, *_ = _frames_gpu(x_np, pol, classes)
+            assert s.err & L.ERR_DEGENERATE
+            continue
+        s, h, fr, o, ws = _frames_gpu(x_np, pol, classes)
+        assert s.err == 0
+        for z in range(Z):
+            np.testing.assert_array_equal(h[z], oracle.hist_u16(x_np[z]).astype(np.int64))
+            imax, ts, t8 = ft[z]
+            thr, g8, g8all, gimax = fr[z]
+            assert gimax == imax and g8 == t8
+            assert tuple((g8all >> (8 * k)) & 255 for k in range(classes - 1)) == ts
+            assert oracle.norm8_u16(thr, imax) > t8 >= oracle.norm8_u16(thr - 1, imax)
+        m = np.concatenate([oracle.binarize(x_np[z:z + 1], ft[z][0], ft[z][2], pol) for z in range(Z)])
+        np.testing.assert_array_equal(words_to_mask(ws[: ((x_np.size + 31) // 32) * 4].view(torch.int32), x_np.size)
+                                      .reshape(shape), m)
+        np.testing.assert_array_equal(words_to_mask(o, x_np.size).reshape(shape), oracle.opening(m, 4))
+
+
+def test_frames_degenerate():
+    x_np = np.stack([np.arange(64, dtype=np.uint16).reshape(8, 8) * 50, np.full((8, 8), 7, np.uint16)])
+    s, *_ = _frames_gpu(x_np, 0, 2)
+    assert s.err & L.ERR_DEGENERATE
+
+
 # ------------------------------------------------------------------------- a4 + a5 binarise + open
 MORPH_SHAPES = [(1, 1, 1), (1, 1, 40), (2, 3, 5), (3, 5, 7), (5, 33, 65), (7, 64, 64), (9, 17, 100),
                 (4, 70, 139), (3, 20, 1390), (11, 9, 256), (6, 40, 96), (33, 8, 32),
