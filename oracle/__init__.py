@@ -290,6 +290,26 @@ def pack_bits(mask):
 
 
 # ---------------------------------------------------------------- the composed hot path
+def background(x, B, op):
+    """NEXT-3 background subtraction (M(x, y) = I(x, y) - B(x, y); SPEC S:61-69 clamps at 0)
+    on a uint16 stack x[Z][Y][X] with one reference frame B[Y][X] applied to every frame:
+      "sub": max(0, I - B)        the paper's M
+      "rev": max(0, B - I)        transmission frames, where the sample darkens I (reading G-10)
+      "add": min(65535, M + B)    the reconstruction's "combined with the precomputed background"
+                                   for "sub"; "rev" is its own inverse on the ROI (B - (B - I))."""
+    x = np.asarray(x).astype(np.int64)
+    B = np.asarray(B).astype(np.int64)[None]
+    if op == "sub":
+        r = np.maximum(0, x - B)
+    elif op == "rev":
+        r = np.maximum(0, B - x)
+    elif op == "add":
+        r = np.minimum(65535, x + B)
+    else:
+        raise ValueError(op)
+    return r.astype(np.uint16)
+
+
 def frame_thresholds(x, classes=2, polarity=0):
     """NEXT-3 per-frame thresholds (uint16 frame stacks): every z-plane is its own image, as in the
     paper's 2-D setting -- its own I_max (Eq. 1), 256-bin normalised histogram and
@@ -307,16 +327,20 @@ def frame_thresholds(x, classes=2, polarity=0):
 
 
 def pipeline(x, *, eb=None, rel_eb=None, conn=6, se=6, min_size=64, polarity=0, classes=2, keep="size",
-             frames=False):
+             frames=False, background_ref=None, bg="sub"):
     """The whole path on one volume x[Z][Y][X] (uint16 or float32).  Returns a dict of every
     intermediate the CUDA path exposes.  Raises Degenerate when Otsu has no valid threshold.
     classes = 3 (NEXT-3): multi-Otsu; the ROI is norm8 > the lowest threshold (HIGH) or
     norm8 <= the highest (LOW, reading G-39).  keep = "largest" (NEXT-3): only the largest component
     survives (min_size unused).  frames = True (NEXT-3, uint16): per-frame thresholds
-    (frame_thresholds); the mask of frame z is Eq. 2 with frame z's I_max and threshold."""
+    (frame_thresholds); the mask of frame z is Eq. 2 with frame z's I_max and threshold.
+    background_ref (NEXT-3, uint16): the path runs on background(x, background_ref, bg)."""
     x = np.ascontiguousarray(x)
     assert x.ndim == 3
     out = {}
+    if background_ref is not None:
+        x = background(x, background_ref, bg)
+        out["x"] = x
     if x.dtype == np.float32:
         mn, mx = value_range(x)
         out["min"], out["max"] = mn, mx

@@ -256,6 +256,31 @@ def generate(cfg, z0=0, nz=None, out=None, device="cuda", truth=None):
     return out
 
 
+def flat_field(cfg, device="cuda"):
+    """C3's background reference B(y, x) ("calibration scans without sample"): the gain-varied
+    open-beam frame of the recipe, noise-free (an average of many calibration frames), uint16 bits in
+    an int16 tensor (Y, X)."""
+    import torch
+
+    base = cfg.name.split("@")[0]
+    assert base == "C3", "only the detector-frame config has a flat field"
+    one = dataclasses.replace(cfg, shape=(1,) + tuple(cfg.shape[1:]))
+    out = torch.empty((1,) + tuple(cfg.shape[1:]), dtype=torch.int16, device=device)
+    Z, Y, X = one.shape
+    P = _Params()
+    P.mode, P.seed = 6, cfg.seed
+    P.gz, P.ny, P.nx, P.z0, P.nz = 1, Y, X, 0, 1
+    p = [0.0] * 16
+    p[8], p[9] = 700.0, 1023.0
+    for k, v in enumerate(p):
+        P.p[k] = v
+    stream = torch.cuda.current_stream(out.device).cuda_stream
+    rc = _load().synth_generate(ctypes.byref(P), ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream))
+    if rc != 0:
+        raise RuntimeError("synth_generate failed: cuda error %d" % rc)
+    return out[0]
+
+
 def to_numpy(t, cfg):
     """Host copy with the config's numpy dtype (u16 bits reinterpreted from int16 storage)."""
     a = t.cpu().numpy()

@@ -21,7 +21,8 @@ struct synth_obj {        // an ellipsoid: centre, rotation R (row-major, body->
 };
 
 struct synth_params {
-    int mode;             // 1 ell_poisson (C1), 2 ell_gauss (C5), 3 f32 texture (C2), 4 frames (C3), 5 cyl+pores (C4)
+    int mode;             // 1 ell_poisson (C1), 2 ell_gauss (C5), 3 f32 texture (C2), 4 frames (C3), 5 cyl+pores (C4),
+                          // 6 the C3 flat field without the sample (a noise-free calibration frame)
     uint32_t seed;
     uint64_t gz, ny, nx;  // global volume
     uint64_t z0, nz;      // slab to generate
@@ -211,6 +212,10 @@ __global__ void synth_rows(synth_params P, void *out) {
             float E = r2 < 1.0f ? g * (P.p[6] - P.p[7] * sqrtf(1.0f - r2)) : P.p[8] * g;
             if (valid) ((uint16_t *)out)[rowbase + x] = clamp_u16(E + sqrtf(E) * z1, P.p[9]);
             truth = r2 < 1.0f;   // the sample's shadow
+        } break;
+        case 6: {  // C3 calibration: the gain-varied open beam, no sample, no noise
+            float g = 0.97f + 0.06f * hash_unit((uint32_t)y, (uint32_t)x, 0x6a1u, P.seed);
+            if (valid) ((uint16_t *)out)[rowbase + x] = clamp_u16(P.p[8] * g, P.p[9]);
         } break;
         case 5: {  // C4: porous cylinder in air
             float dy = fy - P.p[0], dx = fx - P.p[1];
