@@ -51,6 +51,8 @@ def parse():
                     help="NEXT-3 per-frame thresholds (uint16 frame stacks, e.g. C3): histogram/Otsu per z-plane")
     ap.add_argument("--keep", default="size", choices=["size", "largest"],
                     help="a7: drop components < min_size (default) or keep only the largest (NEXT-3)")
+    ap.add_argument("--background", default="none", choices=["none", "sub", "rev"],
+                    help="NEXT-3: subtract the C3 flat field first (sub: I - B, rev: B - I), clamped at 0")
     ap.add_argument("--no-next4", action="store_true",
                     help="skip the NEXT-4 items (reconstruction timing, quality vs the phantom's ground truth)")
     ap.add_argument("--greedy", type=float, default=None, metavar="E",
@@ -112,7 +114,7 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------- algorithmic bytes
-def alg_bytes(cfg, n, count):
+def alg_bytes(cfg, n, count, background=False):
     """what the method must move per step (bytes), per stage.  s = input bytes,
     c = code bytes, f = kept fraction; o and K written and read once each (N/8 bytes each way)."""
     s = cfg.itemsize
@@ -120,13 +122,16 @@ def alg_bytes(cfg, n, count):
     out = {"histogram": s * n, "morph": s * n + n / 8, "label": n / 8, "extract": n / 8 + count * s + count * c}
     if cfg.dtype == "f32":
         out["range"] = s * n
+    if background:
+        out["background"] = 2 * s * n      # read I, write M (B is one frame, L2-resident or negligible)
     return out
 
 
 # the C-ABI call each timed stage is (its kernels: profiles/*/launches_*.txt)
 STAGE_CALLS = {"range": "roix_range (k_range)", "histogram": "roix_histogram (k_hist_*)",
                "morph": "roix_morph (k_binarize + k_open3d_rows/k_open2d)",
-               "label": "roix_label (runs, union-find, filter: 7 kernels)",
+               "label": "roix_label (runs, union-find, filter: 9 kernels)",
+               "background": "roix_background (k_background_vec)",
                "extract": "roix_extract (k_extract_count + scan + k_extract)"}
 
 
@@ -135,7 +140,7 @@ def cpu_info():
 
 
 # ------------------------------------------------------------------------------- oracle timing
-def time_oracle(x_np, cfg, budget_s=15.0, max_reps=1, classes=2, frames=False, keep="size"):
+def time_oracle(x_np, cfg, budget_s=15.0, max_reps=1, classes=2, frames=False, keep="size", B=None, bg="sub"):
     """Time the oracle pipeline (single-threaded) on x_np; returns (seconds per pass, passes)."""
     import oracle
 
@@ -144,7 +149,8 @@ def time_oracle(x_np, cfg, budget_s=15.0, max_reps=1, classes=2, frames=False, k
     for _ in range(max_reps):
         t0 = time.perf_counter()
         oracle.pipeline(x_np, eb=cfg.eb or None, rel_eb=cfg.rel_eb or None, conn=cfg.conn, se=cfg.se,
-                        min_size=cfg.min_size, polarity=cfg.polarity, classes=classes, frames=frames, keep=keep)
+                        min_size=cfg.min_size, polarity=(0 if B is not None and bg == "rev" else cfg.polarity),
+                        classes=classes, frames=frames, keep=keep, background_ref=B, bg=bg)
         times.append(time.perf_counter() - t0)
         if sum(times) > budget_s:
             break
@@ -174,14 +180,20 @@ def reference_arm(args, cfg):
         rng = np.random.default_rng(cfg.seed)
         x_np = (rng.normal(400, 60, (nz,) + cfg.shape[1:]).clip(0, 65535).astype(np.uint16) if cfg.dtype == "u16"
                 else rng.normal(0.02, 0.005, (nz,) + cfg.shape[1:]).astype(np.float32))
+    B_np = None
+    if args.background != "none":
+        B_np = (synth.flat_field(cfg).cpu().numpy().view(np.uint16) if have_gpu
+                else np.full(cfg.shape[1:], 700, np.uint16))
     import oracle
 
     oracle.build()
     for _ in range(max(0, min(args.warmup, 1))):
-        time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep)
+        time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep, B=B_np,
+                                bg=args.background)
     ts = []
     for _ in range(args.steps):
-        t, _ = time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep)
+        t, _ = time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep, B=B_np,
+                                bg=args.background)
         ts.append(t)
     per = sum(ts) / len(ts)
     value = x_np.nbytes / per / 1e9
@@ -229,6 +241,9 @@ def main():
     torch.cuda.synchronize()
     kw = dict(eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=cfg.polarity,
               classes=args.classes, frames=args.frames, keep=args.keep)
+    if args.background != "none":
+        kw.update(background=synth.flat_field(cfg, device=dev)[:, :].contiguous(), bg=args.background,
+                  polarity=0 if args.background == "rev" else cfg.polarity)
     if world > 1:
         from paper_2602_15917_b200.sharded import ShardedPipeline
 
@@ -313,7 +328,7 @@ def main():
     value = cfg.nbytes / (ms_step * 1e-3) / 1e9
     peak, peak_src = peaks()
     # whole-step algorithmic bytes and the dominant kernel's roofline
-    ab = alg_bytes(cfg, n // world, count_local)
+    ab = alg_bytes(cfg, n // world, count_local, background=args.background != "none")
     dom = max((k for k in ab if k in stage_ms), key=lambda k: stage_ms[k])
     achieved = ab[dom] / (stage_ms[dom] * 1e-3) / 1e9
     # DRAM bytes per launch of the dominant stage, from the committed ncu launch list of this config
@@ -332,7 +347,8 @@ def main():
         "config": {"workload": cfg.name, "shape": list(cfg.shape), "input_dtype": cfg.dtype, "eb": cfg.eb,
                    "rel_eb": cfg.rel_eb, "conn": cfg.conn, "se": cfg.se, "min_size": cfg.min_size,
                    "polarity": "LOW" if cfg.polarity else "HIGH", "classes": args.classes,
-                   "frames": args.frames, "keep": args.keep, "parallelism": "zslab%d" % world,
+                   "frames": args.frames, "keep": args.keep,
+                   "background": args.background, "parallelism": "zslab%d" % world,
                    "l2": "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
         "roofline": {"bound": "hbm", "kernel": STAGE_CALLS.get(dom, dom), "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "alg_bytes": ab[dom],
@@ -356,7 +372,9 @@ def main():
     if not args.no_cpu_baseline and world == 1 and rank == 0:
         nz = sample_planes(cfg, 6e6)
         x_np = synth.to_numpy(x[:nz], cfg)
-        t, reps = time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep)
+        B_np = kw["background"].cpu().numpy().view(np.uint16) if "background" in kw else None
+        t, reps = time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep, B=B_np,
+                                bg=args.background)
         line["cpu_baseline"] = {"value": x_np.nbytes / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": "%s planes [0,%d) (%d voxels, %.1f MB), whole oracle pipeline, best of %d" %
                                           (cfg.name, nz, x_np.size, x_np.nbytes / 1e6, reps)}

@@ -168,6 +168,21 @@ roix_status roix_threshold_multi(const uint64_t *hist, uint32_t nbins, roix_dtyp
                                  uint32_t classes, roix_scalars *sc, roix_stream_t stream);
 
 /*
+ * NEXT-3 BACKGROUND SUBTRACTION (M(x, y) = I(x, y) - B(x, y), B from calibration scans
+ * without the sample; SPEC S:61-69 clamps at 0) and its inverse for reconstruction.  uint16:
+ * out[z][y][x] = op(x[z][y][x], B[y][x]) for every frame z < g->nz, one reference frame B[ny][nx]
+ * (device) for all frames:
+ *   ROIX_BG_SUB  max(0, I - B)   (the paper's M)
+ *   ROIX_BG_REV  max(0, B - I)   (transmission frames, where the sample darkens I: G-10, G-40)
+ *   ROIX_BG_ADD  min(65535, M + B)  (restores SUB; REV is its own inverse)
+ * out may alias x.  16-byte alignment as everywhere; frames of ny*nx % 8 != 0 voxels take a slower
+ * per-voxel path.
+ */
+typedef enum { ROIX_BG_SUB = 0, ROIX_BG_REV = 1, ROIX_BG_ADD = 2 } roix_bg_op;
+roix_status roix_background(const uint16_t *x, const uint16_t *B, const roix_geom *g, roix_bg_op op, uint16_t *out,
+                            roix_stream_t stream);
+
+/*
  * NEXT-3 PER-FRAME THRESHOLDS (uint16 frame stacks, e.g. detector frames, C3): every z-plane of the
  * slab is its own image, as in the paper's 2-D pipeline -- its own I_max (Eq. 1),
  * norm8 histogram and (multi-)Otsu thresholds.

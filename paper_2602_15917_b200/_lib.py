@@ -97,6 +97,7 @@ _SIGS = {
     "roix_label_largest": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, _vp, _vp, _u64, _u32, _vp, _vp, _vp]),
     "roix_label_finish_keep": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _u64, _vp,
                                       ctypes.POINTER(LabelOut), _vp, _vp]),
+    "roix_background": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _i32, _vp, _vp]),
     "roix_histogram_frames": (_i32, [_vp, ctypes.POINTER(Geom), _vp, _vp, _vp]),
     "roix_threshold_frames": (_i32, [_vp, _u64, _i32, _u32, _vp, _vp, _vp]),
     "roix_morph_frames": (_i32, [_vp, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t,
@@ -159,6 +160,8 @@ roix_row_spans = _wrap("roix_row_spans")
 roix_greedy_quantize = _wrap("roix_greedy_quantize")
 roix_threshold_multi = _wrap("roix_threshold_multi")
 roix_histogram_frames = _wrap("roix_histogram_frames")
+roix_background = _wrap("roix_background")
+BG_SUB, BG_REV, BG_ADD = 0, 1, 2
 roix_threshold_frames = _wrap("roix_threshold_frames")
 roix_morph_frames = _wrap("roix_morph_frames")
 roix_label_largest = _wrap("roix_label_largest")

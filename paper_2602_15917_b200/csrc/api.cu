@@ -176,6 +176,16 @@ roix_status roix_morph_frames(const uint16_t *x, const roix_geom *g, uint32_t se
                 "roix_morph_frames");
 }
 
+roix_status roix_background(const uint16_t *x, const uint16_t *B, const roix_geom *g, roix_bg_op op, uint16_t *out,
+                            roix_stream_t stream) {
+    if (!geom_ok(g)) return invalid("geometry");
+    if (op != ROIX_BG_SUB && op != ROIX_BG_REV && op != ROIX_BG_ADD) return invalid("op");
+    if (g->nz * g->ny * g->nx == 0) return ROIX_OK;
+    if (!x || !B || !out || !aligned16(x) || !aligned16(B) || !aligned16(out))
+        return invalid("x / B / out must be 16-byte aligned device pointers");
+    return cuda(launch_background(x, B, *g, (int)op, out, (cudaStream_t)stream), "roix_background");
+}
+
 roix_status roix_histogram_frames(const uint16_t *x, const roix_geom *g, roix_scalars *sc, uint64_t *hist,
                                   roix_stream_t stream) {
     if (!sc || !hist) return invalid("sc / hist is NULL");

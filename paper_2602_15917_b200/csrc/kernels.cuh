@@ -97,3 +97,5 @@ cudaError_t launch_hist_u16_frames(const uint16_t *x, uint64_t nframes, uint64_t
                                    cudaStream_t st);
 cudaError_t launch_threshold_frames(const uint64_t *hist, uint64_t nframes, int polarity, int classes,
                                     roix_scalars *sc, roix_frame *frames, cudaStream_t st);
+cudaError_t launch_background(const uint16_t *x, const uint16_t *B, const roix_geom &g, int op, uint16_t *out,
+                              cudaStream_t st);

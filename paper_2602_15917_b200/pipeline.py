@@ -46,7 +46,7 @@ class Pipeline:
 
     def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
                  run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="mask",
-                 spans=False, classes=2, keep="size", frames=False):
+                 spans=False, classes=2, keep="size", frames=False, background=None, bg="sub"):
         L.load()
         self.shape = tuple(int(v) for v in shape)
         Z, Y, X = self.shape
@@ -75,6 +75,16 @@ class Pipeline:
         self.frames = bool(frames)
         if self.frames and (dtype != "u16" or fused):
             raise ValueError("per-frame thresholds need uint16 input and the unfused path")
+        # background subtraction first (NEXT-3): the path runs on max(0, I - B) ("sub") or
+        # max(0, B - I) ("rev", transmission frames); B is one (Y, X) uint16 frame for every z
+        self.bg_ref = None
+        if background is not None:
+            if dtype != "u16" or bg not in ("sub", "rev"):
+                raise ValueError("background subtraction: uint16 input, bg 'sub' or 'rev'")
+            assert tuple(background.shape) == tuple(shape[1:]) and background.is_contiguous()
+            self.bg_ref = background
+            self.bg_op = L.BG_SUB if bg == "sub" else L.BG_REV
+            self.xb = torch.empty(tuple(shape), dtype=torch.int16, device=device or "cuda")
         self.device = torch.device(device or "cuda")
         dev = self.device
         self.geom = L.Geom(Z, Y, X, 0, Z)
@@ -136,6 +146,10 @@ class Pipeline:
         mark = mark or (lambda stage: None)
         st = ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         sc, xp, n = _ptr(self.sc), _ptr(x), self.n
+        if self.bg_ref is not None:
+            L.roix_background(xp, _ptr(self.bg_ref), ctypes.byref(self.geom), self.bg_op, _ptr(self.xb), st)
+            xp = _ptr(self.xb)
+            mark("background")
         L.roix_scalars_init(sc, self.eb, st)
         if self.cdtype == L.F32:
             L.roix_range(xp, n, sc, st)
@@ -209,7 +223,9 @@ class Pipeline:
         return ctypes.c_void_p((stream or torch.cuda.current_stream(self.device)).cuda_stream)
 
     def decode(self, out=None, stream=None, from_spans=False):
-        """Reconstruct the last run's volume: x^ = code * s on the ROI, 0 elsewhere.
+        """Reconstruct the last run's volume: x^ = code * s on the ROI, 0 elsewhere; with a
+        background reference, x^ is then combined with it: min(65535, x^ + B) for "sub",
+        max(0, B - x^) for "rev".
         from_spans=False decodes the kept mask + dense code stream (roix_decode); True decodes the
         paper's row spans (roix_decode_spans, needs spans=True): every column of a span's
         [x_start, x_end) is restored, interior gaps included.  Returns out (shape, input dtype)."""
@@ -234,6 +250,9 @@ class Pipeline:
                                           device=self.device)
             L.roix_decode(_ptr(self.o), _ptr(self.codes), self.code_capacity, self.cdtype, self.n, _ptr(self.sc),
                           _ptr(out), _ptr(self.dec_ws), self.dec_ws.numel(), st)
+        if self.bg_ref is not None:
+            op = L.BG_ADD if self.bg_op == L.BG_SUB else L.BG_REV
+            L.roix_background(_ptr(out), _ptr(self.bg_ref), ctypes.byref(self.geom), op, _ptr(out), st)
         return out
 
     def confusion(self, truth_words, stream=None, counts=None):
@@ -261,6 +280,7 @@ class Pipeline:
     def launches(self):
         k = 4 if self.spans_on else 0   # roix_row_spans: extent, 2 scans, write
         k += 3 if self.keep == "largest" else 0   # reset + two reduction phases
+        k += 1 if self.bg_ref is not None else 0
         k += sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
                                        "extract" if self.extract == "mask" else "extract_runs"))
         return k + (LAUNCHES["range"] if self.cdtype == L.F32 else 0)

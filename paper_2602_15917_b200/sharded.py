@@ -76,6 +76,10 @@ def slab_program(S, x, stream=None, mark=None):
     st = ctypes.c_void_p((stream or torch.cuda.current_stream(S.device)).cuda_stream)
     sc, xp, n = _ptr(S.sc), _ptr(x), S.n
     G, g = S.world, S.rank
+    if S.bg_ref is not None:
+        L.roix_background(xp, _ptr(S.bg_ref), ctypes.byref(S.geom), S.bg_op, _ptr(S.xb), st)
+        xp = _ptr(S.xb)
+        mark("background")
     L.roix_scalars_init(sc, S.eb, st)
     if S.cdtype == L.F32:
         L.roix_range(xp, n, sc, st)

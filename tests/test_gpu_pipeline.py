@@ -351,3 +351,31 @@ def test_sharded_frames_g_invariant():
         keep = np.concatenate([words_to_mask(S.collect().keep_bits, S.n) for S in states])
         np.testing.assert_array_equal(keep, words_to_mask(one.keep_bits, one_n(cfg)))
         assert torch.equal(torch.cat([S.collect().codes for S in states]), one.codes)
+
+
+# ------------------------------------------------------------------ NEXT-3 background subtraction
+@pytest.mark.parametrize("frames", [False, True])
+def test_pipeline_background_vs_oracle(frames):
+    """C3 detector frames with the flat field subtracted (REV: B - I, the sample's shadow turns bright,
+    polarity HIGH), per-frame thresholds or not; the reconstruction adds the background back (P:412);
+    segmentation quality against the phantom's ground truth."""
+    cfg = synth.scaled("C3", 0.25, frames=4)
+    tw = torch.empty(synth.truth_words(cfg) + 4, dtype=torch.int32, device="cuda")
+    x = synth.generate(cfg, truth=tw)
+    B = synth.flat_field(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=0,
+                 frames=frames, background=B, bg="rev", spans=True)
+    res = p.run(x)
+    x_np = synth.to_numpy(x, cfg)
+    B_np = B.cpu().numpy().view(np.uint16)
+    ref = oracle.pipeline(x_np, eb=cfg.eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=0,
+                          frames=frames, background_ref=B_np, bg="rev")
+    assert res.scalars.err == 0
+    np.testing.assert_array_equal(words_to_mask(res.keep_bits, p.n).reshape(cfg.shape), ref["K"])
+    np.testing.assert_array_equal(res.codes.cpu().numpy().view(np.uint16), ref["stream"])
+    xh = p.decode()
+    torch.cuda.synchronize()
+    want = oracle.background(oracle.decode_mask(ref["K"], ref["stream"], oracle.step(cfg.eb), np.uint16), B_np, "rev")
+    np.testing.assert_array_equal(xh.cpu().numpy().view(np.uint16), want)
+    q = p.quality(tw)
+    assert q["dsc"] > 0.95, q

@@ -285,6 +285,29 @@ def test_frames_vs_oracle(shape, classes):
         np.testing.assert_array_equal(words_to_mask(o, x_np.size).reshape(shape), oracle.opening(m, 4))
 
 
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 5, 7), (2, 4, 8), (5, 33, 31), (4, 40, 1390), (130, 3, 5)])
+def test_background_vs_oracle(shape):
+    """NEXT-3 roix_background: SUB / REV / ADD against the oracle, frames that are
+    and are not whole 16-byte units, out-of-place and in place."""
+    rng = np.random.default_rng(abs(hash((shape, "bg"))) % 2 ** 32)
+    x_np = rng.integers(0, 65536, shape).astype(np.uint16)
+    B_np = rng.integers(0, 65536, shape[1:]).astype(np.uint16)
+    Z, Y, X = shape
+    g = L.Geom(Z, Y, X, 0, Z)
+    B = dev(B_np)
+    for op, name in ((L.BG_SUB, "sub"), (L.BG_REV, "rev"), (L.BG_ADD, "add")):
+        want = oracle.background(x_np, B_np, name)
+        x = dev(x_np)
+        out = torch.full((x_np.size + 8,), -1, dtype=torch.int16, device="cuda")
+        L.roix_background(ptr(x), ptr(B), ctypes.byref(g), op, ptr(out), st())
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(host_u16(out)[: x_np.size].reshape(shape), want)
+        assert np.all(out.cpu().numpy()[x_np.size:] == -1)
+        L.roix_background(ptr(x), ptr(B), ctypes.byref(g), op, ptr(x), st())   # in place
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(host_u16(x).reshape(shape), want)
+
+
 def test_frames_degenerate():
     x_np = np.stack([np.arange(64, dtype=np.uint16).reshape(8, 8) * 50, np.full((8, 8), 7, np.uint16)])
     s, *_ = _frames_gpu(x_np, 0, 2)
