@@ -9,7 +9,7 @@
 // NEXT-3 multi-Otsu, k = 3: thresholds t1 < t2 maximise
 // sum_k w_k (mu_k - mu_T)^2 = (sum_k s_k^2 / n_k - S^2 / N) / N over the 32 385 tuples with non-empty
 // classes; ties go to the lexicographically smallest (t1, t2).  Every thread scores its tuples in
-// binary64 (relative error < 1e-15: three positive terms), the block keeps those within 1e-12 of the
+// binary32 (relative error < 1e-6: three positive terms), the block keeps those within 1e-5 of the
 // best approximate score, and compares them exactly: V = num / den with num = s1^2 n2 n3 + s2^2 n1 n3 +
 // s3^2 n1 n2 (< 2^176) and den = n1 n2 n3 (< 2^117), cross-multiplied in 448-bit integers.
 #include "common.cuh"
@@ -97,34 +97,32 @@ __device__ void addw(uint64_t *acc, const uint64_t *b, int n) {
 }
 
 struct Cand3 {
-    uint64_t s[3], n[3];   // class intensity sums and counts
-    int key;               // t1 * 256 + t2 (lexicographic order), -1 = invalid
+    uint64_t num[4], den[3];   // V = num / den (see frac3)
+    int key;                   // t1 * 256 + t2 (lexicographic order), -1 = invalid
 };
 
-// num = s1^2 n2 n3 + s2^2 n1 n3 + s3^2 n1 n2 (4 limbs), den = n1 n2 n3 (3 limbs)
-__device__ void frac3(const Cand3 &c, uint64_t num[4], uint64_t den[3]) {
-    for (int k = 0; k < 4; k++) num[k] = 0;
+// num = s1^2 n2 n3 + s2^2 n1 n3 + s3^2 n1 n2 (< 2^176: 4 limbs), den = n1 n2 n3 (< 2^117: 3 limbs)
+__device__ void frac3(const uint64_t s[3], const uint64_t n[3], Cand3 &c) {
+    for (int k = 0; k < 4; k++) c.num[k] = 0;
     for (int a = 0; a < 3; a++) {
         const int b = (a + 1) % 3, d = (a + 2) % 3;
         uint64_t sq[2], nn[2], t[4];
-        mulw(&c.s[a], 1, &c.s[a], 1, sq);
-        mulw(&c.n[b], 1, &c.n[d], 1, nn);
+        mulw(&s[a], 1, &s[a], 1, sq);
+        mulw(&n[b], 1, &n[d], 1, nn);
         mulw(sq, 2, nn, 2, t);
-        addw(num, t, 4);
+        addw(c.num, t, 4);
     }
     uint64_t n12[2];
-    mulw(&c.n[0], 1, &c.n[1], 1, n12);
-    mulw(n12, 2, &c.n[2], 1, den);
+    mulw(&n[0], 1, &n[1], 1, n12);
+    mulw(n12, 2, &n[2], 1, c.den);
 }
 
 __device__ bool better3(const Cand3 &a, const Cand3 &b) {
     if (a.key < 0) return false;
     if (b.key < 0) return true;
-    uint64_t na[4], da[3], nb[4], db[3], l[7], r[7];
-    frac3(a, na, da);
-    frac3(b, nb, db);
-    mulw(na, 4, db, 3, l);
-    mulw(nb, 4, da, 3, r);
+    uint64_t l[7], r[7];
+    mulw(a.num, 4, b.den, 3, l);
+    mulw(b.num, 4, a.den, 3, r);
     for (int k = 6; k >= 0; k--)
         if (l[k] != r[k]) return l[k] > r[k];
     return a.key < b.key;
@@ -132,59 +130,64 @@ __device__ bool better3(const Cand3 &a, const Cand3 &b) {
 
 __device__ __forceinline__ Cand3 shfl_cand3(const Cand3 &c, int src) {
     Cand3 o;
-    for (int k = 0; k < 3; k++) {
-        o.s[k] = __shfl_sync(FULL, c.s[k], src);
-        o.n[k] = __shfl_sync(FULL, c.n[k], src);
-    }
+    for (int k = 0; k < 4; k++) o.num[k] = __shfl_sync(FULL, c.num[k], src);
+    for (int k = 0; k < 3; k++) o.den[k] = __shfl_sync(FULL, c.den[k], src);
     o.key = __shfl_sync(FULL, c.key, src);
     return o;
 }
 
 // 3-class search over the inclusive prefix sums sn / ss of the norm8 histogram (totals N, S); every
 // thread of the 1024-thread block calls it.  Returns (t1, t2) or (-1, -1) if fewer than three bins
-// are populated.
-__device__ void otsu3_search(const uint64_t *sn, const uint64_t *ss, uint64_t N, uint64_t S, int *t1_out,
-                             int *t2_out) {
-    __shared__ double s_v[32];
+// are populated.  Approximate score V(t1, t2) = A1[t1] + (ss[t2] - ss[t1])^2 / (sn[t2] - sn[t1]) +
+// A3[t2] with the outer classes' terms tabulated once; the exact comparison sees only the tuples
+// within the margin of the best approximate score.
+__device__ void otsu3_search(const unsigned long long *h8, const uint64_t *sn, const uint64_t *ss, uint64_t N,
+                             uint64_t S, int *t1_out, int *t2_out) {
+    __shared__ float s_v[32], s_a1[256], s_a3[256];
     __shared__ Cand3 s_c[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    auto classes = [&](int p, Cand3 &c) -> bool {
-        const int t1 = p >> 8, t2 = p & 255;
-        if (t1 >= t2 || t2 > 254) return false;
-        const uint64_t n1 = sn[t1], n12 = sn[t2];
-        if (n1 == 0 || n12 == n1 || n12 == N) return false;
-        c.n[0] = n1;
-        c.n[1] = n12 - n1;
-        c.n[2] = N - n12;
-        c.s[0] = ss[t1];
-        c.s[1] = ss[t2] - ss[t1];
-        c.s[2] = S - ss[t2];
-        c.key = p;
-        return true;
-    };
-    auto approx = [](const Cand3 &c) {
-        double v = 0;
-        for (int k = 0; k < 3; k++) v += (double)c.s[k] * (double)c.s[k] / (double)c.n[k];
-        return v;
-    };
-    double vmax = -1.0;
-    for (int p = tid; p < 65536; p += 1024) {
-        Cand3 c;
-        if (classes(p, c)) vmax = fmax(vmax, approx(c));
+    if (tid < 256) {
+        const float n1 = (float)sn[tid], s1 = (float)ss[tid];
+        const float n3 = (float)(N - sn[tid]), s3 = (float)(S - ss[tid]);
+        s_a1[tid] = n1 > 0 ? s1 * s1 / n1 : 0.0f;
+        s_a3[tid] = n3 > 0 ? s3 * s3 / n3 : 0.0f;
     }
-    for (int d = 16; d > 0; d >>= 1) vmax = fmax(vmax, __shfl_xor_sync(FULL, vmax, d));
+    __syncthreads();
+    // tuple p = t1 * 256 + t2 with non-empty classes: its approximate score, or -1.  A threshold on an
+    // empty bin gives the same classes as the one below it, a lexicographically smaller tuple: only
+    // populated bins are candidates (exact, and it removes the exact ties of sparse histograms).
+    // binary32 scores: every term within ~5 ulps (< 1e-6 relative, all terms positive), so every tuple
+    // whose exact score reaches the maximum scores within the 1e-5 margin below.
+    auto score = [&](int p) -> float {
+        const int t1 = p >> 8, t2 = p & 255;
+        if (t1 >= t2 || t2 > 254 || h8[t1] == 0 || h8[t2] == 0) return -1.0f;
+        const uint64_t n1 = sn[t1], n12 = sn[t2];
+        if (n1 == 0 || n12 == n1 || n12 == N) return -1.0f;
+        const float m = (float)(ss[t2] - ss[t1]);
+        return s_a1[t1] + __fdividef(m * m, (float)(n12 - n1)) + s_a3[t2];
+    };
+    float vmax = -1.0f;
+    for (int p = tid; p < 65536; p += 1024) vmax = fmaxf(vmax, score(p));
+    for (int d = 16; d > 0; d >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(FULL, vmax, d));
     if (lane == 0) s_v[warp] = vmax;
     __syncthreads();
     vmax = s_v[0];
-    for (int k = 1; k < 32; k++) vmax = fmax(vmax, s_v[k]);
-    const double thr = vmax - vmax * 1e-12;
+    for (int k = 1; k < 32; k++) vmax = fmaxf(vmax, s_v[k]);
+    const float thr = vmax - vmax * 1e-5f;
     Cand3 best;
     best.key = -1;
-    for (int k = 0; k < 3; k++) best.s[k] = best.n[k] = 0;
+    for (int k = 0; k < 4; k++) best.num[k] = 0;
+    for (int k = 0; k < 3; k++) best.den[k] = 0;
     if (vmax >= 0) {
         for (int p = tid; p < 65536; p += 1024) {   // increasing p = lexicographic: strict `better` keeps the first
+            if (score(p) < thr) continue;
+            const int t1 = p >> 8, t2 = p & 255;
+            const uint64_t n[3] = {sn[t1], sn[t2] - sn[t1], N - sn[t2]};
+            const uint64_t sm[3] = {ss[t1], ss[t2] - ss[t1], S - ss[t2]};
             Cand3 c;
-            if (classes(p, c) && approx(c) >= thr && better3(c, best)) best = c;
+            frac3(sm, n, c);
+            c.key = p;
+            if (better3(c, best)) best = c;
         }
     }
     for (int d = 16; d > 0; d >>= 1) {
@@ -264,7 +267,7 @@ __device__ void otsu_block(const uint64_t *__restrict__ hist, int dtype, uint32_
     const uint64_t N = scan_n[255], S = scan_s[255];
     if (classes == 3) {
         int t1, t2;
-        otsu3_search(scan_n, scan_s, N, S, &t1, &t2);
+        otsu3_search(h8, scan_n, scan_s, N, S, &t1, &t2);
         *imax_out = imax;
         *t8_out = t1;
         *t8_hi_out = t2;
