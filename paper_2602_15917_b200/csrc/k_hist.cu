@@ -56,36 +56,51 @@ __global__ void __launch_bounds__(1024, 2) k_hist_u16(const uint16_t *__restrict
 }
 
 // NEXT-3 per-frame histograms (uint16 frame stacks): frame z = voxels [z A, (z + 1) A) into
-// gh + z * 65536; blockIdx.y = frame, the same privatised window as k_hist_u16.  Frames need not start
-// on a 16-byte boundary: the unaligned head and tail of each frame go voxel by voxel.
-__global__ void __launch_bounds__(1024, 2) k_hist_u16_frames(const uint16_t *__restrict__ x, uint64_t A,
+// gh + z * 65536, with the same privatised window as k_hist_u16.  Persistent: CTA c owns the contiguous
+// range [c n / G, (c + 1) n / G) of the stack (balanced whatever the frame count) and walks it frame
+// segment by frame segment, flushing its window into the segment's frame histogram; segments need not
+// start on a 16-byte boundary (head and tail voxel by voxel).
+__global__ void __launch_bounds__(1024, 2) k_hist_u16_frames(const uint16_t *__restrict__ x, uint64_t n, uint64_t A,
                                                               roix_scalars *sc, uint64_t *gh_all) {
     extern __shared__ uint32_t sh[];
     if (get_err(sc)) return;
-    uint64_t *gh = gh_all + (uint64_t)blockIdx.y * 65536;
-    for (int i = threadIdx.x; i < HWIN; i += blockDim.x) sh[i] = 0;
-    __syncthreads();
-    const uint64_t s = (uint64_t)blockIdx.y * A, e = s + A;
-    const uint64_t a = min(e, (uint64_t)((s + 7) & ~7ull)), e8 = max(a, (uint64_t)(e & ~7ull));
-    if (blockIdx.x == 0) {
+    const uint64_t r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
+    const uint4 *x8 = reinterpret_cast<const uint4 *>(x);
+    for (uint64_t s = r0; s < r1;) {
+        const uint64_t z = s / A, e = min(r1, (z + 1) * A);
+        uint64_t *gh = gh_all + z * 65536;
+        for (int i = threadIdx.x; i < HWIN; i += blockDim.x) sh[i] = 0;
+        __syncthreads();
+        const uint64_t a = min(e, (uint64_t)((s + 7) & ~7ull)), e8 = max(a, (uint64_t)(e & ~7ull));
         if (threadIdx.x < a - s) hist_add(sh, gh, x[s + threadIdx.x]);
         if (threadIdx.x < e - e8) hist_add(sh, gh, x[e8 + threadIdx.x]);
-    }
-    const uint4 *x8 = reinterpret_cast<const uint4 *>(x);
-    for (uint64_t i = a / 8 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e8 / 8;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint4 v = __ldcs(x8 + i);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        uint64_t i = a / 8 + threadIdx.x;
+        const uint64_t i1 = e8 / 8;
+        for (; i + blockDim.x < i1; i += 2 * blockDim.x) {
+            const uint4 u = __ldcs(x8 + i), v = __ldcs(x8 + i + blockDim.x);
+            const uint32_t w[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            hist_add(sh, gh, w[k] & 0xffffu);
-            hist_add(sh, gh, w[k] >> 16);
+            for (int k = 0; k < 8; k++) {
+                hist_add(sh, gh, w[k] & 0xffffu);
+                hist_add(sh, gh, w[k] >> 16);
+            }
         }
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < HWIN; b += blockDim.x) {
-        const uint32_t c = sh[b];
-        if (c) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)c);
+        if (i < i1) {
+            const uint4 u = __ldcs(x8 + i);
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                hist_add(sh, gh, w[k] & 0xffffu);
+                hist_add(sh, gh, w[k] >> 16);
+            }
+        }
+        __syncthreads();
+        for (int b = threadIdx.x; b < HWIN; b += blockDim.x) {
+            const uint32_t c = sh[b];
+            if (c) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)c);
+        }
+        __syncthreads();
+        s = e;
     }
 }
 
@@ -258,14 +273,9 @@ cudaError_t launch_hist_u16_frames(const uint16_t *x, uint64_t nframes, uint64_t
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    if (nframes == 0 || A == 0) return cudaSuccess;
-    const uint64_t per = (uint64_t)num_sms() * 2 / nframes;          // fill the GPU once over all frames
-    const uint64_t need = (A / 8 + 1023) / 1024;
-    const unsigned bpf = (unsigned)max((uint64_t)1, min(per, need));
-    for (uint64_t z0 = 0; z0 < nframes; z0 += 65535) {
-        const unsigned nz = (unsigned)min(nframes - z0, (uint64_t)65535);
-        k_hist_u16_frames<<<dim3(bpf, nz), 1024, HWIN * 4, st>>>(x + z0 * A, A, sc, hist + z0 * 65536);
-    }
+    const uint64_t n = nframes * A;
+    if (n == 0) return cudaSuccess;
+    k_hist_u16_frames<<<grid_for(n / 8, 1024, 2), 1024, HWIN * 4, st>>>(x, n, A, sc, hist);
     return cudaGetLastError();
 }
 
