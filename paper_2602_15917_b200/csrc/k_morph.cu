@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
         mring[i * WS] = FULL;
         mring[i * WS + W + 1] = FULL;
     }
-    for (int i = threadIdx.x; i < ES + S; i += blockDim.x) {
+    for (int i = threadIdx.x; i < ES + S; i += blockDim.x) {   // e rows and o rows: zero pad words
         ering[i * WS] = 0;
         ering[i * WS + W + 1] = 0;
     }
@@ -891,29 +891,22 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
             }
         }
         __syncthreads();
-        // assemble bits [c0 X, cend X) into global words
-        const int64_t cend = min(r1, c0 + (int64_t)S);
-        const uint64_t B0 = (uint64_t)c0 * A.nx, B1 = (uint64_t)cend * A.nx;
-        const uint64_t w0 = B0 >> 5, w1 = (B1 + 31) >> 5;
-        for (uint64_t wi = w0 + threadIdx.x; wi < w1; wi += blockDim.x) {
-            uint64_t lo = max(wi * 32, B0), hi = min(wi * 32 + 32, B1);
-            uint32_t val = 0;
-            uint64_t pos = lo;
-            while (pos < hi) {
-                uint64_t rel = pos - B0;
-                uint64_t rr = rel / A.nx, col = rel - rr * A.nx;
-                uint32_t take = (uint32_t)min((uint64_t)(hi - pos), A.nx - col);
-                const uint32_t *src = orow + rr * WS + 1;
-                uint32_t cw = (uint32_t)(col >> 5), cs = (uint32_t)(col & 31);
-                uint32_t bits = __funnelshift_r(src[cw], src[cw + 1], cs) & low_mask(take);
-                val |= bits << (uint32_t)(pos - wi * 32);
-                pos += take;
+        // write row r (warp w) at global bit r X: the words wholly inside the row with plain stores, the
+        // (at most two) words it shares with its neighbour rows with atomicOr (o was zeroed when rows
+        // are not whole words)
+        if (r < r1) {
+            const uint64_t Bg = (uint64_t)r * A.nx, Be = Bg + A.nx;
+            const uint32_t sh = (uint32_t)(Bg & 31);
+            const uint64_t wf = Bg >> 5, wl = (Be - 1) >> 5;
+            for (uint64_t wi = wf + lane_id(); wi <= wl; wi += 32) {
+                const int64_t b = (int64_t)(32 * (wi - wf)) - (int64_t)sh;   // row bit of the word's bit 0
+                uint32_t val;
+                if (b < 0) val = od[0] << sh;
+                else val = __funnelshift_r(od[b >> 5], od[(b >> 5) + 1], (uint32_t)(b & 31));
+                const bool whole = wi * 32 >= Bg && wi * 32 + 32 <= Be;
+                if (whole) A.o[wi] = val;
+                else if (val) atomicOr(&A.o[wi], val);
             }
-            // a word is owned by this CTA alone when it starts here and either ends here or holds
-            // the end of the volume (its remaining bits are pad bits, which must be 0)
-            bool whole = lo == wi * 32 && (hi == wi * 32 + 32 || hi == (uint64_t)rows * A.nx);
-            if (whole && A.aligned_out) A.o[wi] = val;
-            else if (val) atomicOr(&A.o[wi], val);
         }
         __syncthreads();
     }
@@ -1075,8 +1068,9 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         rpc = (rpc + 31) / 32 * 32;
         A.rows_per_cta = rpc;
         uint64_t ctas = (rows + rpc - 1) / rpc;
-        // whole words at every step iff S*X is a multiple of 32 (CTA starts are, see above)
-        A.aligned_out = ((uint64_t)S * g.nx) % 32 == 0;
+        // every row is whole words iff X is a multiple of 32; otherwise rows share their end words,
+        // which are OR-ed into a zeroed o
+        A.aligned_out = g.nx % 32 == 0;
         if (!A.aligned_out && (e = cudaMemsetAsync(o_bits, 0, nwords * 4, st)) != cudaSuccess) return e;
         k_open2d<<<(unsigned)ctas, 32 * S, sm, st>>>(A, sc);
     }

@@ -13,3 +13,6 @@ python bench.py $A --config C4 > gpurun_out/plain2.log 2>&1 && ncu $M --log-file
 F="--set full --clock-control none --import-source on -k regex:^k_extract$ -s 1 -c 1"
 ncu $F -o gpurun_out/full_extract_C2 -f python bench.py $A > gpurun_out/ncu_full_C2.log 2>&1; echo "full C2 $?"
 python bench.py $A --config C4 --scale 0.5 > gpurun_out/plain3.log 2>&1 && ncu $F -o gpurun_out/full_extract_C4h -f python bench.py $A --config C4 --scale 0.5 > gpurun_out/ncu_full_C4h.log 2>&1; echo "full C4h $?"
+A3="--config C3 --frames --background rev --classes 3 $A"
+python bench.py $A3 > gpurun_out/plain4.log 2>&1 && ncu $M --log-file gpurun_out/launches_C3_next3.csv python bench.py $A3 > /dev/null 2>&1; echo "launches C3 next3 $?"
+python bench.py --config C3 --frames --background rev --classes 3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C3_next3.json 2> gpurun_out/bench_C3.err; echo "bench C3 next3 $?"

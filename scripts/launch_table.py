@@ -15,6 +15,8 @@ starts = [i for i, k in enumerate(order) if "k_scalars_init" in k[1]]
 which = int(sys.argv[2]) if len(sys.argv) > 2 else -2
 s0 = starts[which]
 s1 = starts[which + 1] if which + 1 < len(starts) and which != -1 else len(order)
+ends = [i for i in range(s0, s1) if "k_extract_total" in order[i][1]]
+s1 = ends[0] + 1 if ends else s1
 tot = 0
 for k in order[s0:s1]:
     m = data[k]

@@ -12,12 +12,13 @@ import sys
 # kernels of each pipeline stage (one C-ABI call each; see paper_2602_15917_b200/pipeline.py)
 STAGE = {
     "range": ["k_range"],
-    "histogram": ["k_hist_u16", "k_hist_f32"],
-    "threshold": ["k_threshold"],
+    "background": ["k_background_vec", "k_background_scalar"],
+    "histogram": ["k_hist_u16", "k_hist_f32", "k_hist_u16_frames"],
+    "threshold": ["k_threshold", "k_threshold_frames"],
     "morph": ["k_binarize", "k_open3d_reg", "k_open3d_rows", "k_open2d"],
     "label": ["k_scan_dlb", "k_runs_total", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross", "k_resolve_broots",
-              "k_flatten_sizes", "k_root_flags", "k_table", "k_table_total", "k_clear_dropped", "k_table_clear"],
-    "extract": ["k_extract_count", "k_extract", "k_extract_total"],
+              "k_flatten_sizes", "k_largest_init", "k_largest", "k_root_flags", "k_table", "k_table_total", "k_clear_dropped", "k_table_clear"],
+    "extract": ["k_extract_count", "k_extract", "k_extract_seg", "k_extract_total"],
 }
 
 
@@ -40,7 +41,9 @@ def steps(path):
 
 def main(path, config, out_dir="profiles"):
     data, order, starts = steps(path)
-    s0, s1 = starts[-1], len(order)          # the last complete step of the run
+    s0 = starts[-1]                          # the last step of the run, up to its extract's total
+    ends = [i for i in range(s0, len(order)) if order[i][1] == "k_extract_total"]
+    s1 = ends[0] + 1 if ends else len(order)
     kern = order[s0:s1]
     # the scan kernel appears in label and extract: attribute by position (label precedes extract)
     res, stage_of = {}, {}
