@@ -194,11 +194,37 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
         // offsets of the group's rows: lanes 0..RIF load row_start[r0 .. r0+RIF]
         uint32_t off = 0;
         if (lane <= RIF && r0 + lane <= rows) off = rs[r0 + lane];
+        if (!regs) {
+            // long rows: the group's RIF rows advance chunk by chunk together, so their loads and
+            // their (dependent) chunk steps interleave
+            uint32_t carry[RIF], sb[RIF], eb[RIF], b0[RIF];
+            bool live[RIF];
+#pragma unroll
+            for (int q = 0; q < RIF; q++) {
+                b0[q] = __shfl_sync(FULL, off, q);
+                live[q] = r0 + q < rows && __shfl_sync(FULL, off, q + 1) != b0[q];
+                carry[q] = sb[q] = eb[q] = 0;
+            }
+            for (uint32_t k0 = 0; k0 < G.W; k0 += 32) {
+                uint32_t cw[RIF], nx[RIF];
+#pragma unroll
+                for (int q = 0; q < RIF; q++) {
+                    cw[q] = (live[q] && k0 + lane < G.W) ? row_word_safe(o, G, r0 + q, k0 + lane, nwords) : 0u;
+                    nx[q] = (live[q] && k0 + 32 < G.W) ? row_word_safe(o, G, r0 + q, k0 + 32, nwords) : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < RIF; q++)
+                    if (live[q])
+                        runs_of_chunk(cw[q], nx[q], carry[q], k0 + lane, b0[q], sb[q], eb[q], (uint32_t)(r0 + q), x0, x1,
+                                      rrow);
+            }
+            continue;
+        }
         uint32_t wv[RIF][RW];
 #pragma unroll
         for (int q = 0; q < RIF; q++) {
             const uint32_t a = __shfl_sync(FULL, off, q), b = __shfl_sync(FULL, off, q + 1);
-            const bool live = regs && r0 + q < rows && b != a;
+            const bool live = r0 + q < rows && b != a;
 #pragma unroll
             for (int h = 0; h < RW; h++) {
                 const uint32_t k = h * 32 + lane;
@@ -211,20 +237,11 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
             const uint32_t b0 = __shfl_sync(FULL, off, q), b1 = __shfl_sync(FULL, off, q + 1);
             if (r >= rows || b1 == b0) continue;
             uint32_t carry = 0, sbase = 0, ebase = 0;
-            if (regs) {
 #pragma unroll
-                for (int h = 0; h < RW; h++) {
-                    if (h * 32 >= (int)G.W) break;
-                    const uint32_t nxt = h + 1 < RW ? __shfl_sync(FULL, wv[q][h + 1], 0) : 0u;
-                    runs_of_chunk(wv[q][h], nxt, carry, h * 32 + lane, b0, sbase, ebase, (uint32_t)r, x0, x1, rrow);
-                }
-            } else {
-                for (uint32_t k0 = 0; k0 < G.W; k0 += 32) {
-                    const uint32_t k = k0 + lane;
-                    const uint32_t cw = k < G.W ? row_word_safe(o, G, r, k, nwords) : 0u;
-                    const uint32_t nxt = (k0 + 32 < G.W) ? row_word_safe(o, G, r, k0 + 32, nwords) : 0u;
-                    runs_of_chunk(cw, nxt, carry, k, b0, sbase, ebase, (uint32_t)r, x0, x1, rrow);
-                }
+            for (int h = 0; h < RW; h++) {
+                if (h * 32 >= (int)G.W) break;
+                const uint32_t nxt = h + 1 < RW ? __shfl_sync(FULL, wv[q][h + 1], 0) : 0u;
+                runs_of_chunk(wv[q][h], nxt, carry, h * 32 + lane, b0, sbase, ebase, (uint32_t)r, x0, x1, rrow);
             }
         }
     }

@@ -281,17 +281,31 @@ __global__ void __launch_bounds__(256) k_binarize(const T *__restrict__ x, uint6
 }
 
 // Warp-level: row words of a linear bit array starting at bit `bit0` (X bits), pad bits = 1 (m rows).
+// Four lane-iterations' loads are issued before any is used (a long row otherwise waits on one
+// global-load latency per 32 words).
 __device__ __forceinline__ void load_m_row(const uint32_t *__restrict__ src, uint64_t src_words, uint64_t bit0,
                                            uint64_t X, uint32_t W, uint32_t *dst) {
+    constexpr int U = 4;
     const uint32_t sh = (uint32_t)(bit0 & 31);
     const uint64_t w0 = bit0 >> 5;
     const uint32_t tail = (uint32_t)(X - 32ull * (W - 1));
-    for (uint32_t k = lane_id(); k < W; k += 32) {
-        const uint64_t wi = w0 + k;
-        uint32_t v = src[wi];
-        if (sh) v = __funnelshift_r(v, (wi + 1 < src_words) ? src[wi + 1] : 0u, sh);
-        if (k == W - 1 && tail < 32) v |= ~low_mask(tail);
-        dst[k] = v;
+    for (uint32_t k0 = lane_id(); k0 < W; k0 += 32 * U) {
+        uint32_t v[U], nx[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t k = k0 + 32 * u;
+            const uint64_t wi = w0 + k;
+            v[u] = k < W ? src[wi] : 0u;
+            nx[u] = (k < W && sh && wi + 1 < src_words) ? src[wi + 1] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t k = k0 + 32 * u;
+            if (k >= W) break;
+            uint32_t val = sh ? __funnelshift_r(v[u], nx[u], sh) : v[u];
+            if (k == W - 1 && tail < 32) val |= ~low_mask(tail);
+            dst[k] = val;
+        }
     }
 }
 

@@ -397,7 +397,9 @@ def test_binarize_planes_halo_layout():
 
 
 # --------------------------------------------------------------------------------- a6 + a7 label
-LABEL_SHAPES = [(1, 1, 1), (1, 1, 70), (2, 3, 5), (4, 9, 33), (6, 17, 64), (10, 10, 10), (3, 31, 97), (5, 40, 130)]
+LABEL_SHAPES = [(1, 1, 1), (1, 1, 70), (2, 3, 5), (4, 9, 33), (6, 17, 64), (10, 10, 10), (3, 31, 97), (5, 40, 130),
+                # rows longer than the register path (W > 128 words): the batched long-row run extraction
+                (2, 5, 4500), (1, 3, 13900)]
 
 
 def _label_gpu(mask, conn, min_size, with_runs, inplace=True, labels=True):
