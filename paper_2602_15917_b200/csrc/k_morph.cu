@@ -824,8 +824,9 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     extern __shared__ uint32_t smem[];
     if (get_err(sc)) return;
     const uint32_t W = A.W, WS = A.WS;
-    const int S = blockDim.x >> 5, warp = threadIdx.x >> 5;
-    const int MS = S + 4, ES = S + 2;
+    constexpr int S = 8;                          // warps per CTA (launched with 256 threads)
+    constexpr uint32_t MS = S + 4, ES = S + 2;    // ring slots: constant moduli compile to multiply-shifts
+    const int warp = threadIdx.x >> 5;
     uint32_t *mring = smem;            // [MS][WS]
     uint32_t *ering = mring + MS * WS; // [ES][WS]
     uint32_t *orow = ering + ES * WS;  // [S][WS]
@@ -834,17 +835,18 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     const int64_t r0 = (int64_t)blockIdx.x * A.rows_per_cta;
     const int64_t r1 = min(rows, r0 + (int64_t)A.rows_per_cta);
     if (r0 >= r1) return;
-    for (int i = threadIdx.x; i < MS; i += blockDim.x) {
+    for (int i = threadIdx.x; i < (int)MS; i += blockDim.x) {
         mring[i * WS] = FULL;
         mring[i * WS + W + 1] = FULL;
     }
-    for (int i = threadIdx.x; i < ES + S; i += blockDim.x) {   // e rows and o rows: zero pad words
+    for (int i = threadIdx.x; i < (int)ES + S; i += blockDim.x) {   // e rows and o rows: zero pad words
         ering[i * WS] = 0;
         ering[i * WS + W + 1] = 0;
     }
     __syncthreads();
-    auto mrow = [&](int64_t r) { return mring + ((r % MS + MS) % MS) * WS + 1; };
-    auto erow = [&](int64_t r) { return ering + ((r % ES + ES) % ES) * WS + 1; };
+    // ring slot of row r >= r0 - 2: from the (32-bit) distance to r0 - 2, constant modulus
+    auto mrow = [&](int64_t r) { return mring + ((uint32_t)(r - r0 + 2) % MS) * WS + 1; };
+    auto erow = [&](int64_t r) { return ering + ((uint32_t)(r - r0 + 2) % ES) * WS + 1; };
     auto load_m = [&](int64_t r) {
         uint32_t *dst = mrow(r);
         if (r < 0 || r >= rows) fill_row(dst, W, FULL);
