@@ -93,3 +93,39 @@ def test_overlap_metrics_host_vs_oracle(lib):
         for k in L.METRICS:
             np.testing.assert_allclose(got[k], want[k], rtol=2e-16, atol=0, equal_nan=True, err_msg="%s %s" % (k, c))
     assert lib.roix_overlap_metrics(None, None) == L.ROIX_E_INVALID
+
+
+def test_host_validation_next_rows(lib):
+    """NEXT-1..4 entry points reject bad arguments on the host, before any launch (no GPU needed)."""
+    from paper_2602_15917_b200 import _lib as L
+
+    P = ctypes.c_void_p(16)
+    g = L.Geom(4, 4, 4, 0, 4)
+    sz = ctypes.c_size_t()
+    # multi-Otsu: class count 2 or 3 only
+    assert lib.roix_threshold_multi(P, 256, L.F32, 0, 4, P, None) == L.ROIX_E_UNSUPPORTED
+    assert lib.roix_threshold_multi(P, 255, L.F32, 0, 3, P, None) == L.ROIX_E_INVALID
+    assert lib.roix_threshold_frames(P, 2, 0, 5, P, P, None) == L.ROIX_E_UNSUPPORTED
+    # keep-largest on a sharded finish must go through roix_label_finish_keep
+    out = L.LabelOut(16, None, None, None, 0, None)
+    assert lib.roix_label_finish(P, ctypes.byref(g), L.KEEP_LARGEST, 8, P, 1 << 20, None, None, None, 0,
+                                 ctypes.byref(out), P, None) == L.ROIX_E_INVALID
+    assert lib.roix_label_largest(P, ctypes.byref(g), 8, None, None, None, 0, 2, P, P, None) == L.ROIX_E_INVALID
+    # background: bad op, misaligned pointers
+    assert lib.roix_background(P, P, ctypes.byref(g), 7, P, None) == L.ROIX_E_INVALID
+    assert lib.roix_background(ctypes.c_void_p(18), P, ctypes.byref(g), L.BG_SUB, P, None) == L.ROIX_E_INVALID
+    # decode: workspace size, alignment, dtype
+    assert lib.roix_decode_workspace(1000, ctypes.byref(sz)) == L.ROIX_OK and sz.value > 0
+    assert lib.roix_decode(P, P, 10, L.U16, 1000, P, P, P, 0, None) == L.ROIX_E_INVALID          # ws too small
+    assert lib.roix_decode(P, P, 10, 9, 1000, P, P, P, 1 << 20, None) == L.ROIX_E_INVALID        # dtype
+    assert lib.roix_decode(ctypes.c_void_p(20), P, 10, L.U16, 1000, P, P, P, 1 << 20, None) == L.ROIX_E_INVALID
+    assert lib.roix_decode_spans_workspace(ctypes.byref(g), ctypes.byref(sz)) == L.ROIX_OK
+    assert lib.roix_decode_spans(P, 4, P, 10, None, L.U16, ctypes.byref(g), P, P, P, sz.value, None) == \
+        L.ROIX_E_INVALID                                                                           # counts NULL
+    # confusion: counts required, masks aligned
+    assert lib.roix_confusion(P, P, 10, None, None) == L.ROIX_E_INVALID
+    assert lib.roix_confusion(ctypes.c_void_p(4), P, 10, P, None) == L.ROIX_E_INVALID
+    # greedy: E must be finite and >= 0, qmax <= 65535
+    assert lib.roix_greedy_quantize(P, 10, ctypes.c_double(-1.0), 255, P, P, P, P, 256, None) == L.ROIX_E_INVALID
+    assert lib.roix_greedy_quantize(P, 10, ctypes.c_double(1.0), 70000, P, P, P, P, 256, None) == L.ROIX_E_INVALID
+    assert b"qmax" in lib.roix_last_error()
