@@ -135,19 +135,19 @@ __device__ __forceinline__ void extract_tile(const T *__restrict__ x, uint64_t n
                     const uint32_t c0 = code_pair_u16_m<QM>(d[j].x, q, err), c1 = code_pair_u16_m<QM>(d[j].y, q, err),
                                    c2 = code_pair_u16_m<QM>(d[j].z, q, err), c3 = code_pair_u16_m<QM>(d[j].w, q, err);
                     if (mg == 0xffu) {
-                        if ((a & 7u) == 0) {
-                            *reinterpret_cast<uint4 *>(stage + a) = make_uint4(c0, c1, c2, c3);
-                        } else if ((a & 1u) == 0) {
-                            uint32_t *s32 = reinterpret_cast<uint32_t *>(stage + a);
-                            s32[0] = c0; s32[1] = c1; s32[2] = c2; s32[3] = c3;
-                        } else {
-                            stage[a] = (C)(c0 & 0xffffu);
-                            uint32_t *s32 = reinterpret_cast<uint32_t *>(stage + a + 1);
-                            s32[0] = __funnelshift_r(c0, c1, 16);
-                            s32[1] = __funnelshift_r(c1, c2, 16);
-                            s32[2] = __funnelshift_r(c2, c3, 16);
-                            stage[a + 7] = (C)(c3 >> 16);
-                        }
+                        // branch-free for either parity of a: the 8 codes shifted by (a & 1) halfwords
+                        // into the words of [a & ~1, a + 8); the two edge halfwords that belong to this
+                        // lane (not to its neighbours) are predicated stores
+                        const uint32_t odd = a & 1u, shb = odd * 16u, b = a >> 1;
+                        uint32_t *s32 = reinterpret_cast<uint32_t *>(stage) + b;
+                        const uint32_t t1 = __funnelshift_l(c0, c1, shb), t2 = __funnelshift_l(c1, c2, shb),
+                                       t3 = __funnelshift_l(c2, c3, shb);
+                        stage[2 * b + 1] = (C)((odd ? c0 : c0 >> 16) & 0xffffu);
+                        s32[1] = t1;
+                        s32[2] = t2;
+                        s32[3] = t3;
+                        if (!odd) stage[2 * b] = (C)(c0 & 0xffffu);
+                        else stage[2 * b + 8] = (C)(c3 >> 16);
                     } else {
                         const uint32_t cc[4] = {c0, c1, c2, c3};
                         uint32_t pp = a;
