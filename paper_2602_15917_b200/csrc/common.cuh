@@ -1,5 +1,6 @@
 // common.cuh -- shared device helpers of libroix (sm_100a).  Product code: shares nothing with oracle/.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -179,5 +180,20 @@ __device__ __forceinline__ uint32_t low_mask(uint32_t n) { return n >= 32 ? FULL
 // Spread the 4 low bits of nib to bit positions 0, 8, 16, 24 (no carries: the partial products
 // occupy distinct positions).
 __device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+// Host: cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device and call site -- the attribute
+// is per device, `done` is the call site's bitmask of the devices already set (races are harmless:
+// the call is idempotent).
+template <typename K>
+inline cudaError_t dyn_smem_once(K kern, int bytes, std::atomic<unsigned long long> &done) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+    if (bit && (done.load(std::memory_order_relaxed) & bit)) return cudaSuccess;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)) != cudaSuccess) return e;
+    done.fetch_or(bit);
+    return cudaSuccess;
+}
 
 }  // namespace roix

@@ -268,13 +268,8 @@ cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom 
     if ((e = cudaMemsetAsync(W.shist, 0, 65536 * 8, st)) != cudaSuccess) return e;
     const uint64_t nrows = g.nz * g.ny;
     uint64_t rs = nrows / 4096 < 64 ? (nrows / 4096 ? nrows / 4096 : 1) : 64;
-    static bool attr = false;
-    if (!attr) {
-        if ((e = cudaFuncSetAttribute(k_hist_bin<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, FHWIN * 4)) !=
-            cudaSuccess)
-            return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if ((e = dyn_smem_once(k_hist_bin<uint16_t>, FHWIN * 4, attr)) != cudaSuccess) return e;
     const int sms = num_sms();
     if (dtype == ROIX_U16)
         k_sample_hist<uint16_t><<<sms * 2, 512, 0, st>>>((const uint16_t *)x, g.nx, nrows, rs, sc, W.shist);

@@ -254,25 +254,18 @@ static int grid_for(uint64_t work_items, int threads, int per_sm) {
 }
 
 cudaError_t launch_hist_u16(const uint16_t *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_hist_u16, cudaFuncAttributeMaxDynamicSharedMemorySize, HWIN * 4);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    const cudaError_t e = dyn_smem_once(k_hist_u16, HWIN * 4, attr);
+    if (e != cudaSuccess) return e;
     k_hist_u16<<<grid_for(n / 8, 1024, 2), 1024, HWIN * 4, st>>>(x, n, sc, hist);
     return cudaGetLastError();
 }
 
 cudaError_t launch_hist_u16_frames(const uint16_t *x, uint64_t nframes, uint64_t A, roix_scalars *sc, uint64_t *hist,
                                    cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k_hist_u16_frames, cudaFuncAttributeMaxDynamicSharedMemorySize, HWIN * 4);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    const cudaError_t e = dyn_smem_once(k_hist_u16_frames, HWIN * 4, attr);
+    if (e != cudaSuccess) return e;
     const uint64_t n = nframes * A;
     if (n == 0) return cudaSuccess;
     k_hist_u16_frames<<<grid_for(n / 8, 1024, 2), 1024, HWIN * 4, st>>>(x, n, A, sc, hist);

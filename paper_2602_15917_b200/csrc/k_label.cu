@@ -886,13 +886,8 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
     } else {
         k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, rtot, cap, sc);
     }
-    static bool attr = false;
-    if (!attr) {
-        if ((e = cudaFuncSetAttribute(k_union_local, cudaFuncAttributeMaxDynamicSharedMemorySize, UB_MAX * 4)) !=
-            cudaSuccess)
-            return e;
-        attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    if ((e = dyn_smem_once(k_union_local, UB_MAX * 4, attr)) != cudaSuccess) return e;
     // Union blocks: 16 K runs for large slabs -- several planes' runs, so most z-links stay inside one
     // block and the cross-block queue is 3x shorter (C4: union_cross 490 -> 142 us) -- 4 K runs for
     // small ones, where more, smaller blocks keep the SMs busy (C2: union_local 81 -> 29 us).
