@@ -332,14 +332,26 @@ __device__ __forceinline__ void extract_seg_tile(const T *__restrict__ x, uint64
                     if (p + e < capacity) out[p + e] = (C)(sizeof(C) == 2 ? (cw[e >> 1] >> ((e & 1) * 16)) & 0xffffu : cw[e]);
             }
         } else {
-            uint32_t ks = k;
+            // a group across segment boundaries (or a ragged end): find every element's voxel first,
+            // then issue the V loads together
+            uint32_t ks = k, src[V];
+            bool ok[V];
+#pragma unroll
             for (int e = 0; e < V; e++) {
                 const int64_t j = jg + e;
-                if (j < 0 || (uint64_t)j >= cnt) continue;
-                while (s_off[ks + 1] <= (uint32_t)j) ks++;
-                const uint32_t cd = code1<T, QM>(xt[s_start[ks] + ((uint32_t)j - s_off[ks])], q, err);
-                if (p + e < capacity) out[p + e] = (C)cd;
+                ok[e] = j >= 0 && (uint64_t)j < cnt;
+                src[e] = 0;
+                if (ok[e]) {
+                    while (s_off[ks + 1] <= (uint32_t)j) ks++;
+                    src[e] = s_start[ks] + ((uint32_t)j - s_off[ks]);
+                }
             }
+            T v[V];
+#pragma unroll
+            for (int e = 0; e < V; e++) v[e] = ok[e] ? xt[src[e]] : (T)0;
+#pragma unroll
+            for (int e = 0; e < V; e++)
+                if (ok[e] && p + e < capacity) out[p + e] = (C)code1<T, QM>(v[e], q, err);
         }
     }
     if (err) set_err(sc, err);
