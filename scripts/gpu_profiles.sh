@@ -10,7 +10,7 @@ M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum -
 A="--steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-graph"
 python bench.py $A > gpurun_out/plain1.log 2>&1 && ncu $M --log-file gpurun_out/launches_C2.csv python bench.py $A > /dev/null 2>&1; echo "launches C2 $?"
 python bench.py $A --config C4 > gpurun_out/plain2.log 2>&1 && ncu $M --log-file gpurun_out/launches_C4.csv python bench.py $A --config C4 > /dev/null 2>&1; echo "launches C4 $?"
-F="--set full --clock-control none --import-source on -k regex:^k_extract$ -s 1 -c 1"
+F="--set full --clock-control none --import-source on -k regex:^k_extract(_seg)?$ -s 1 -c 1"
 ncu $F -o gpurun_out/full_extract_C2 -f python bench.py $A > gpurun_out/ncu_full_C2.log 2>&1; echo "full C2 $?"
 python bench.py $A --config C4 --scale 0.5 > gpurun_out/plain3.log 2>&1 && ncu $F -o gpurun_out/full_extract_C4h -f python bench.py $A --config C4 --scale 0.5 > gpurun_out/ncu_full_C4h.log 2>&1; echo "full C4h $?"
 A3="--config C3 --frames --background rev --classes 3 $A"
