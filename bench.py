@@ -45,6 +45,8 @@ def parse():
                          "replay; N > 1 always enqueues, the exchanges synchronise with the host)")
     ap.add_argument("--extract", default="mask", choices=["mask", "runs"], help="a8 form (see Pipeline)")
     ap.add_argument("--spans", action="store_true", help="also produce the NEXT-1 row spans (roix_row_spans)")
+    ap.add_argument("--fused", action="store_true",
+                    help="speculative fused histogram + binarisation (roix_histogram_binarize; one read of x)")
     ap.add_argument("--classes", type=int, default=2, choices=[2, 3],
                     help="a3 class count: 2 (Otsu) or 3 (multi-Otsu, NEXT-3)")
     ap.add_argument("--frames", action="store_true",
@@ -240,7 +242,7 @@ def main():
     x = synth.generate(cfg, z0=z0, nz=z1 - z0, device=dev)
     torch.cuda.synchronize()
     kw = dict(eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se, min_size=cfg.min_size, polarity=cfg.polarity,
-              classes=args.classes, frames=args.frames, keep=args.keep)
+              classes=args.classes, frames=args.frames, keep=args.keep, fused=args.fused)
     if args.background != "none":
         kw.update(background=synth.flat_field(cfg, device=dev)[:, :].contiguous(), bg=args.background,
                   polarity=0 if args.background == "rev" else cfg.polarity)
@@ -348,7 +350,7 @@ def main():
                    "rel_eb": cfg.rel_eb, "conn": cfg.conn, "se": cfg.se, "min_size": cfg.min_size,
                    "polarity": "LOW" if cfg.polarity else "HIGH", "classes": args.classes,
                    "frames": args.frames, "keep": args.keep,
-                   "background": args.background, "parallelism": "zslab%d" % world,
+                   "background": args.background, "fused": args.fused, "parallelism": "zslab%d" % world,
                    "l2": "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
         "roofline": {"bound": "hbm", "kernel": STAGE_CALLS.get(dom, dom), "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "alg_bytes": ab[dom],
@@ -357,7 +359,9 @@ def main():
         "step_roofline": {"alg_bytes_per_step": step_alg, "achieved": step_alg / (ms_step * 1e-3) / 1e9,
                           "frac": step_alg / (ms_step * 1e-3) / 1e9 / peak},
         "stage_ms": stage_ms, "kept": count, "kept_fraction": count / n, "spatial_reduction": n / max(count, 1),
-        "t8": int(s.t8), "gpu_launches": p.launches() * args.steps, "cuda_graph": bool(args.graph),
+        "t8": int(s.t8), **({"speculation": {2: "resolved", 3: "fell back"}.get(int(s.spec_state), int(s.spec_state)),
+                             "n_uncertain": int(s.n_uncertain)} if args.fused else {}),
+        "gpu_launches": p.launches() * args.steps, "cuda_graph": bool(args.graph),
     }
     clocks = clk.summary()
     line["clocks"] = clocks

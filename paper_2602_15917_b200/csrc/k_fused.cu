@@ -48,33 +48,38 @@ __device__ __forceinline__ int norm8_edges_f(float x, float scale, const float *
     return k;
 }
 
+// one warp per sampled row (coalesced loads along the row), counters in a shared window of FHWIN
+// bins (u16; values above it go to the global bins) or the 256 norm8 bins (fp32)
 template <typename T>
 __global__ void __launch_bounds__(512) k_sample_hist(const T *__restrict__ x, uint64_t X, uint64_t nrows, uint64_t rs,
                                                      roix_scalars *sc, uint64_t *gh) {
-    __shared__ uint32_t sh[2048];
-    __shared__ float e[257];
+    extern __shared__ uint32_t sh[];   // u16: FHWIN bins; f32: 256 bins + 257 edges
     if (get_err(sc)) return;
-    const bool f32 = sizeof(T) == 4;
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
+    constexpr bool f32 = sizeof(T) == 4;
+    const int nb = f32 ? 256 : FHWIN;
+    float *e = reinterpret_cast<float *>(sh + 256);
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sh[i] = 0;
     if (f32) {
         for (int i = threadIdx.x; i < 256; i += blockDim.x) e[i] = i == 0 ? -INFINITY : sc->edges[i];
         if (threadIdx.x == 0) e[256] = INFINITY;
     }
     const float scale = f32 ? 255.0f / sc->i_max : 0.0f;
     __syncthreads();
-    const uint64_t ns = (nrows + rs - 1) / rs, total = ns * X, stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const uint64_t r = (i / X) * rs, c = i % X;
-        const T v = x[r * X + c];
-        if constexpr (sizeof(T) == 2) {
-            if ((uint32_t)v < 2048u) atomicAdd(&sh[v], 1u);
-            else atomicAdd((unsigned long long *)&gh[v], 1ull);
-        } else {
-            if (fabsf(v) <= FLT_MAX) atomicAdd(&sh[norm8_edges_f(v, scale, e)], 1u);
+    const uint64_t ns = (nrows + rs - 1) / rs;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t k = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < ns; k += nw) {
+        const T *row = x + k * rs * X;
+        for (uint64_t c = lane_id(); c < X; c += 32) {
+            const T v = row[c];
+            if constexpr (sizeof(T) == 2) {
+                if ((uint32_t)v < (uint32_t)FHWIN) atomicAdd(&sh[v], 1u);
+                else atomicAdd((unsigned long long *)&gh[v], 1ull);
+            } else {
+                if (fabsf(v) <= FLT_MAX) atomicAdd(&sh[norm8_edges_f(v, scale, e)], 1u);
+            }
         }
     }
     __syncthreads();
-    const int nb = f32 ? 256 : 2048;
     for (int b = threadIdx.x; b < nb; b += blockDim.x)
         if (sh[b]) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)sh[b]);
 }
@@ -225,6 +230,90 @@ __global__ void __launch_bounds__(512, 3) k_hist_bin(const T *__restrict__ x, ui
         if (sh[b]) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)sh[b]);
 }
 
+// uint16 volumes of whole 16-byte groups (n % 8 == 0, every BASELINE config): the lean form of
+// k_hist_bin, shaped like k_hist_u16.  A warp iteration covers 64 groups (512 voxels, 16 mask words):
+// lane l takes groups l and 32 + l (two loads in flight), adds their 16 voxels to the shared window and
+// forms their certain / uncertain bits (one byte each per group); lane j < 16 then gathers mask word j
+// from the 4 lanes that hold its groups.
+__global__ void __launch_bounds__(1024, 2) k_hist_bin_u16(const uint16_t *__restrict__ x, uint64_t n,
+                                                         roix_scalars *sc, uint64_t *gh, FusedWS W) {
+    extern __shared__ uint32_t sh[];   // FHWIN bins
+    if (get_err(sc)) return;
+    for (int i = threadIdx.x; i < FHWIN; i += blockDim.x) sh[i] = 0;
+    const bool spec = sc->spec_state == 1;
+    const uint32_t lo = sc->spec_lo, hi = sc->spec_hi;
+    const uint32_t low = sc->polarity != 0;
+    __syncthreads();
+    const uint32_t lane = lane_id();
+    const uint64_t ng = n / 8, nwords = (n + 31) / 32;
+    const uint64_t iters = (ng + 63) / 64;
+    const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    const uint4 *x8 = reinterpret_cast<const uint4 *>(x);
+    auto add = [&](uint32_t v) {
+        if (v < (uint32_t)FHWIN) atomicAdd(&sh[v], 1u);
+        else atomicAdd((unsigned long long *)&gh[v], 1ull);
+    };
+    const uint32_t hi2 = hi | (hi << 16), lo2 = lo | (lo << 16);
+    // the 8 voxels of a group into the histogram (branch-free unless a value leaves the shared window),
+    // and their certain (bit k) / uncertain (bit 8 + k) bits from halfword SIMD compares
+    auto group = [&](uint4 d) -> uint32_t {
+        const uint32_t w[4] = {d.x, d.y, d.z, d.w};
+        if (((d.x | d.y | d.z | d.w) & 0xC000C000u) == 0) {   // every value < 16384 = FHWIN
+#pragma unroll
+            for (int k = 0; k < 8; k++) atomicAdd(&sh[(w[k >> 1] >> ((k & 1) * 16)) & 0xffffu], 1u);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; k++) add((w[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
+        }
+        uint32_t gh = 0, gl = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const uint32_t rh = __vcmpgeu2(w[j], hi2), rl = __vcmpgeu2(w[j], lo2);   // 0xffff where >=
+            gh |= (((rh >> 15) & 1u) | ((rh >> 30) & 2u)) << (2 * j);
+            gl |= (((rl >> 15) & 1u) | ((rl >> 30) & 2u)) << (2 * j);
+        }
+        const uint32_t cert = low ? (~gl & 0xffu) : gh;
+        return cert | ((gl & ~gh & 0xffu) << 8);
+    };
+    for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < iters; it += nwarps) {
+        const uint64_t g0 = it * 64;
+        const bool va = g0 + lane < ng, vb = g0 + 32 + lane < ng;
+        const uint4 a = va ? __ldcs(x8 + g0 + lane) : make_uint4(0, 0, 0, 0);
+        const uint4 b = vb ? __ldcs(x8 + g0 + 32 + lane) : make_uint4(0, 0, 0, 0);
+        const uint32_t pa = va ? group(a) : 0u, pb = vb ? group(b) : 0u;
+        if (!spec) continue;
+        uint32_t wc = 0, wu = 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const uint32_t src = 4 * (lane & 7) + i;
+            const uint32_t qa = __shfl_sync(FULL, pa, src), qb = __shfl_sync(FULL, pb, src);
+            const uint32_t q = lane < 8 ? qa : qb;
+            wc |= (q & 0xffu) << (8 * i);
+            wu |= ((q >> 8) & 0xffu) << (8 * i);
+        }
+        const uint64_t wi = it * 16 + lane;
+        if (lane < 16 && wi < nwords) W.m[wi] = wc;
+        else wu = 0;
+        if (__any_sync(FULL, wu != 0)) {   // queue the uncertain voxels (rare: inside the window)
+            const uint32_t cnt = __popc(wu);
+            const uint32_t incl = warp_incl_scan(cnt);
+            unsigned long long at = 0;
+            if (lane == 31 && incl) at = atomicAdd((unsigned long long *)&sc->n_uncertain, (unsigned long long)incl);
+            at = __shfl_sync(FULL, at, 31) + incl - cnt;
+            uint32_t bits = wu;
+            while (bits) {
+                const uint32_t bb = __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (at < W.ucap) W.unc[at] = wi * 32 + bb;
+                at++;
+            }
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < FHWIN; b += blockDim.x)
+        if (sh[b]) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)sh[b]);
+}
+
 // After the exact threshold: resolve the queued voxels, or flag the plain binarisation.
 __global__ void k_spec_check(roix_scalars *sc, int dtype, uint64_t ucap) {
     if (get_err(sc)) return;
@@ -268,13 +357,14 @@ cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom 
     if ((e = cudaMemsetAsync(W.shist, 0, 65536 * 8, st)) != cudaSuccess) return e;
     const uint64_t nrows = g.nz * g.ny;
     uint64_t rs = nrows / 4096 < 64 ? (nrows / 4096 ? nrows / 4096 : 1) : 64;
-    static std::atomic<unsigned long long> attr{0};
+    static std::atomic<unsigned long long> attr{0}, attr_s{0};
     if ((e = dyn_smem_once(k_hist_bin<uint16_t>, FHWIN * 4, attr)) != cudaSuccess) return e;
+    if ((e = dyn_smem_once(k_sample_hist<uint16_t>, FHWIN * 4, attr_s)) != cudaSuccess) return e;
     const int sms = num_sms();
     if (dtype == ROIX_U16)
-        k_sample_hist<uint16_t><<<sms * 2, 512, 0, st>>>((const uint16_t *)x, g.nx, nrows, rs, sc, W.shist);
+        k_sample_hist<uint16_t><<<sms * 2, 512, FHWIN * 4, st>>>((const uint16_t *)x, g.nx, nrows, rs, sc, W.shist);
     else
-        k_sample_hist<float><<<sms * 2, 512, 0, st>>>((const float *)x, g.nx, nrows, rs, sc, W.shist);
+        k_sample_hist<float><<<sms * 2, 512, (256 + 257) * 4, st>>>((const float *)x, g.nx, nrows, rs, sc, W.shist);
     // 2. speculative window
     if ((e = launch_spec(W.shist, dtype, polarity, sc, st)) != cudaSuccess) return e;
     // 3. full histogram + certain mask bits + uncertain queue
@@ -282,7 +372,14 @@ cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom 
     uint64_t blocks = (iters + 15) / 16;
     if (blocks > (uint64_t)sms * 3) blocks = (uint64_t)sms * 3;
     if (blocks < 1) blocks = 1;
-    if (dtype == ROIX_U16)
+    static std::atomic<unsigned long long> attr_b{0};
+    if (dtype == ROIX_U16 && n % 8 == 0) {
+        if ((e = dyn_smem_once(k_hist_bin_u16, FHWIN * 4, attr_b)) != cudaSuccess) return e;
+        const uint64_t wit = (n / 8 + 63) / 64;
+        uint64_t b16 = (wit + 31) / 32;
+        if (b16 > (uint64_t)sms * 2) b16 = (uint64_t)sms * 2;
+        k_hist_bin_u16<<<(unsigned)(b16 ? b16 : 1), 1024, FHWIN * 4, st>>>((const uint16_t *)x, n, sc, hist, W);
+    } else if (dtype == ROIX_U16)
         k_hist_bin<uint16_t><<<(unsigned)blocks, 512, FHWIN * 4, st>>>((const uint16_t *)x, n, sc, hist, W);
     else
         k_hist_bin<float><<<(unsigned)blocks, 512, (256 + 257) * 4, st>>>((const float *)x, n, sc, hist, W);
