@@ -20,6 +20,25 @@ __device__ __forceinline__ void hist_add(uint32_t *sh, uint64_t *gh, uint32_t v)
     else atomicAdd((unsigned long long *)&gh[v], 1ull);
 }
 
+// the 8 values of a 16-byte group: unconditional shared adds when all of them are inside the window
+// (one test per group instead of a branch per value -- the kernel is bound by instruction issue)
+__device__ __forceinline__ void hist_add8(uint32_t *sh, uint64_t *gh, uint4 a) {
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+    if (((a.x | a.y | a.z | a.w) & 0xC000C000u) == 0) {   // HWIN = 16384: no value has bit 14 or 15
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            atomicAdd(&sh[w[k] & 0xffffu], 1u);
+            atomicAdd(&sh[w[k] >> 16], 1u);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            hist_add(sh, gh, w[k] & 0xffffu);
+            hist_add(sh, gh, w[k] >> 16);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024, 2) k_hist_u16(const uint16_t *__restrict__ x, uint64_t n, roix_scalars *sc,
                                                        uint64_t *gh) {
     extern __shared__ uint32_t sh[];
@@ -30,23 +49,11 @@ __global__ void __launch_bounds__(1024, 2) k_hist_u16(const uint16_t *__restrict
     const uint64_t n8 = n / 8, stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; i + stride < n8; i += 2 * stride) {
-        uint4 a = __ldcs(x8 + i), b = __ldcs(x8 + i + stride);
-        uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            hist_add(sh, gh, w[k] & 0xffffu);
-            hist_add(sh, gh, w[k] >> 16);
-        }
+        const uint4 a = __ldcs(x8 + i), b = __ldcs(x8 + i + stride);
+        hist_add8(sh, gh, a);
+        hist_add8(sh, gh, b);
     }
-    for (; i < n8; i += stride) {
-        uint4 a = __ldcs(x8 + i);
-        uint32_t w[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            hist_add(sh, gh, w[k] & 0xffffu);
-            hist_add(sh, gh, w[k] >> 16);
-        }
-    }
+    for (; i < n8; i += stride) hist_add8(sh, gh, __ldcs(x8 + i));
     if (blockIdx.x == 0 && threadIdx.x < (n & 7)) hist_add(sh, gh, x[n8 * 8 + threadIdx.x]);
     __syncthreads();
     for (int b = threadIdx.x; b < HWIN; b += blockDim.x) {
@@ -78,22 +85,10 @@ __global__ void __launch_bounds__(1024, 2) k_hist_u16_frames(const uint16_t *__r
         const uint64_t i1 = e8 / 8;
         for (; i + blockDim.x < i1; i += 2 * blockDim.x) {
             const uint4 u = __ldcs(x8 + i), v = __ldcs(x8 + i + blockDim.x);
-            const uint32_t w[8] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                hist_add(sh, gh, w[k] & 0xffffu);
-                hist_add(sh, gh, w[k] >> 16);
-            }
+            hist_add8(sh, gh, u);
+            hist_add8(sh, gh, v);
         }
-        if (i < i1) {
-            const uint4 u = __ldcs(x8 + i);
-            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                hist_add(sh, gh, w[k] & 0xffffu);
-                hist_add(sh, gh, w[k] >> 16);
-            }
-        }
+        if (i < i1) hist_add8(sh, gh, __ldcs(x8 + i));
         __syncthreads();
         for (int b = threadIdx.x; b < HWIN; b += blockDim.x) {
             const uint32_t c = sh[b];
