@@ -236,8 +236,22 @@ __global__ void __launch_bounds__(256) k_binarize(const T *__restrict__ x, uint6
     const uint64_t wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
     const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
     const uint64_t nwords = (n + 31) / 32;
-    for (uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); it < iters; it += wstride) {
+    // the next iteration's loads are issued before this one is binarised (two iterations in flight)
+    uint64_t it = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint4 nxt[CH];
+    auto prefetch = [&](uint64_t j) {
+        if (j < iters && (j + 1) * 1024 <= n) {
+#pragma unroll
+            for (int c = 0; c < CH; c++) nxt[c] = __ldcs(x4 + j * 32 * CH + c * 32 + lane);
+        }
+    };
+    prefetch(it);
+    for (; it < iters; it += wstride) {
         const uint64_t g0 = it * 32 * CH;  // first 16-byte group of the iteration
+        uint4 v[CH];
+#pragma unroll
+        for (int c = 0; c < CH; c++) v[c] = nxt[c];
+        prefetch(it + wstride);
         uint64_t p0 = 0, b1 = ~0ull;
         uint32_t t0 = 0, t1 = 0;
         if constexpr (FR) {
@@ -250,9 +264,6 @@ __global__ void __launch_bounds__(256) k_binarize(const T *__restrict__ x, uint6
         }
         uint32_t P = 0;
         if ((it + 1) * 1024 <= n) {
-            uint4 v[CH];
-#pragma unroll
-            for (int c = 0; c < CH; c++) v[c] = __ldcs(x4 + g0 + c * 32 + lane);
 #pragma unroll
             for (int c = 0; c < CH; c++)
                 P |= group_bits<T, FR>(cmp, v[c], (g0 + c * 32 + lane) * VPL, F, p0, b1, t0, t1) << (c * VPL);
