@@ -68,7 +68,8 @@ __device__ __forceinline__ float rne_fast(float x, float s, float s_inv) {
 struct QP {
     float s, s_inv;
     uint32_t s_int, magic;
-    uint32_t k;  // log2(s_int) when s_int >= 2 is a power of two, else 0
+    uint32_t k;                  // log2(s_int) when s_int >= 2 is a power of two, else 0
+    uint32_t m_hi, m_lo, m_half; // k >= 1: (0xffff >> k), 2^k - 1, 2^(k-1) - 1 in both halfwords
 };
 __device__ __forceinline__ QP load_qp(const roix_scalars *sc) {
     QP q;
@@ -77,6 +78,10 @@ __device__ __forceinline__ QP load_qp(const roix_scalars *sc) {
     q.s_int = sc->s_int;
     q.magic = sc->s_magic;
     q.k = (q.s_int >= 2 && (q.s_int & (q.s_int - 1)) == 0) ? (uint32_t)(__ffs(q.s_int) - 1) : 0u;
+    const uint32_t lanes = 0x00010001u, k = q.k ? q.k : 1u;
+    q.m_hi = (0xffffu >> k) * lanes;
+    q.m_lo = ((1u << k) - 1u) * lanes;
+    q.m_half = ((1u << (k - 1)) - 1u) * lanes;
     return q;
 }
 
@@ -128,9 +133,8 @@ __device__ __forceinline__ uint32_t code_pair_u16_m(uint32_t w, const QP &q, uin
     if constexpr (M == QM_ONE) return w;
     if constexpr (M == QM_POW2) {
         const uint32_t lanes = 0x00010001u, k = q.k;
-        const uint32_t qq = (w >> k) & ((0xffffu >> k) * lanes);
-        const uint32_t r = w & (((1u << k) - 1u) * lanes);
-        const uint32_t t = r + (qq & lanes) + (((1u << (k - 1)) - 1u) * lanes);
+        const uint32_t qq = (w >> k) & q.m_hi;
+        const uint32_t t = (w & q.m_lo) + (qq & lanes) + q.m_half;
         return qq + ((t >> k) & lanes);
     }
     return code_u16_m<M>(w & 0xffffu, q, err) | (code_u16_m<M>(w >> 16, q, err) << 16);
@@ -143,9 +147,8 @@ __device__ __forceinline__ uint32_t code_pair_u16_m(uint32_t w, const QP &q, uin
 __device__ __forceinline__ uint32_t code_pair_u16(uint32_t w, const QP &q, uint32_t &err) {
     if (q.k) {
         const uint32_t lanes = 0x00010001u, k = q.k;
-        const uint32_t qq = (w >> k) & ((0xffffu >> k) * lanes);
-        const uint32_t r = w & (((1u << k) - 1u) * lanes);
-        const uint32_t t = r + (qq & lanes) + (((1u << (k - 1)) - 1u) * lanes);
+        const uint32_t qq = (w >> k) & q.m_hi;
+        const uint32_t t = (w & q.m_lo) + (qq & lanes) + q.m_half;
         return qq + ((t >> k) & lanes);
     }
     if (q.s_int == 1) return w;
