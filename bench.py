@@ -438,16 +438,35 @@ def next4(p, x, cfg, args, count):
     step's kept mask + code stream, timed alone with CUDA events; (2) roix_confusion of K
     against the phantom's ground truth (synth regenerates x bit-identically with its truth mask) and
     Eqs. 7-14 (P:509-547)."""
+    import ctypes
+
     import torch
 
     import synth
+    from paper_2602_15917_b200 import _lib as L
 
     dev = x.device
     tw = torch.empty(synth.truth_words(cfg) + 4, dtype=torch.int32, device=dev)
     synth.generate(cfg, out=x, device=dev, truth=tw)     # same voxel values, plus the truth bits
     q = p.quality(tw)
-    xh = torch.empty_like(x)
-    p.decode(xh)
+    # reconstruct the whole volume, or (when a second volume does not fit next to the pipeline's
+    # buffers, C5) the longest plane prefix that does: its codes are the stream's first ones
+    Z, Y, X = cfg.shape
+    free = torch.cuda.mem_get_info(dev)[0]
+    nz_dec = min(Z, int(0.85 * free) // (Y * X * cfg.itemsize))
+    if nz_dec < 1:
+        return {"quality_vs_truth": {k: q[k] for k in ("dsc", "iou", "sensitivity", "specificity", "accuracy",
+                                                       "kappa", "auc")},
+                "counts": q["counts"], "spatial_reduction": q["spatial_reduction_voxels"],
+                "decode": "skipped: no device memory for a second volume"}
+    xh = torch.empty((nz_dec, Y, X), dtype=x.dtype, device=dev)
+    n_dec = nz_dec * Y * X
+    dws = torch.empty(max(1, L.roix_decode_workspace(n_dec)), dtype=torch.uint8, device=dev)
+    st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    sp_ = lambda t: ctypes.c_void_p(t.data_ptr())
+    run_dec = (lambda: p.decode(xh)) if nz_dec == Z else (lambda: L.roix_decode(
+        sp_(p.o), sp_(p.codes), p.code_capacity, p.cdtype, n_dec, sp_(p.sc), sp_(xh), sp_(dws), dws.numel(), st))
+    run_dec()
     cnt = torch.empty(4, dtype=torch.int64, device=dev)
 
     def timed(fn, reps):
@@ -463,15 +482,16 @@ def next4(p, x, cfg, args, count):
         return e0.elapsed_time(e1) / reps
 
     reps = max(3, args.steps)
-    ms_dec = timed(lambda: p.decode(xh), reps)
+    ms_dec = timed(run_dec, reps)
     ms_conf = timed(lambda: p.confusion(tw, counts=cnt), reps)
     if p.scalars().err:
         raise SystemExit("device error bits 0x%x in NEXT-4" % p.scalars().err)
     n = cfg.n
     csize = 2 if cfg.dtype == "u16" else 4
-    dec_bytes = n / 8 + count * csize + n * cfg.itemsize   # K once, the codes, every voxel of x^ written
+    # K once, the codes, every voxel of x^ written (kept codes of the prefix: count scaled by its share)
+    dec_bytes = n_dec / 8 + count * (n_dec / n) * csize + n_dec * cfg.itemsize
     peak = peaks()[0]
-    return {"decode": {"call": "roix_decode", "ms": ms_dec, "alg_bytes": dec_bytes,
+    return {"decode": {"call": "roix_decode", "voxels": n_dec, "ms": ms_dec, "alg_bytes": dec_bytes,
                        "achieved_gbs": dec_bytes / (ms_dec * 1e-3) / 1e9,
                        "frac": dec_bytes / (ms_dec * 1e-3) / 1e9 / peak},
             "confusion": {"call": "roix_confusion", "ms": ms_conf, "alg_bytes": n / 4,

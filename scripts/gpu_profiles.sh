@@ -6,6 +6,9 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || exit 1
 python bench.py > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err; echo "bench C2 $?"
 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C4.json 2> gpurun_out/bench_C4.err; echo "bench C4 $?"
+python bench.py --config C3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_C3.json 2> gpurun_out/bench_C3d.err; echo "bench C3 $?"
+python bench.py --config C5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_C5.json 2> gpurun_out/bench_C5.err; echo "bench C5 $?"
+python bench.py --config C1 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_C1.json 2> gpurun_out/bench_C1.err; echo "bench C1 $?"
 M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv"
 A="--steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-graph"
 python bench.py $A > gpurun_out/plain1.log 2>&1 && ncu $M --log-file gpurun_out/launches_C2.csv python bench.py $A > /dev/null 2>&1; echo "launches C2 $?"
