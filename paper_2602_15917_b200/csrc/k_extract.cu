@@ -194,7 +194,7 @@ __device__ __forceinline__ void extract_tile(const T *__restrict__ x, uint64_t n
 }
 
 template <typename T, typename C>
-__global__ void __launch_bounds__(EX_THREADS, sizeof(T) == 2 ? 5 : 4) k_extract(const T *__restrict__ x, uint64_t n, uint64_t ntiles,
+__global__ void __launch_bounds__(EX_THREADS, sizeof(T) == 2 ? 6 : 4) k_extract(const T *__restrict__ x, uint64_t n, uint64_t ntiles,
                                                         const uint32_t *__restrict__ K, ExWS w, roix_scalars *sc,
                                                         C *__restrict__ out, uint64_t capacity, const uint64_t *offset) {
     constexpr int PADE = 16 / sizeof(C);
