@@ -45,6 +45,8 @@ def parse():
                          "replay; N > 1 always enqueues, the exchanges synchronise with the host)")
     ap.add_argument("--extract", default="mask", choices=["mask", "runs"], help="a8 form (see Pipeline)")
     ap.add_argument("--spans", action="store_true", help="also produce the NEXT-1 row spans (roix_row_spans)")
+    ap.add_argument("--sharded", action="store_true",
+                    help="test aid: the z-slab sharded path (torch.distributed) even on one rank")
     ap.add_argument("--fused", action="store_true",
                     help="speculative fused histogram + binarisation (roix_histogram_binarize; one read of x)")
     ap.add_argument("--classes", type=int, default=2, choices=[2, 3],
@@ -214,7 +216,7 @@ def reference_arm(args, cfg):
 # ------------------------------------------------------------------------------------ GPU arm
 def main():
     args = parse()
-    args.graph = not args.no_graph and int(os.environ.get("WORLD_SIZE", "1")) == 1
+    args.graph = not args.no_graph and not args.sharded and int(os.environ.get("WORLD_SIZE", "1")) == 1
     import synth
 
     cfg = synth.CONFIGS[args.config] if args.scale == 1.0 else synth.scaled(args.config, args.scale)
@@ -229,8 +231,24 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dist_on = world > 1 or args.sharded     # the sharded path with its exchanges (NCCL)
+    if dist_on:
+        if "MASTER_ADDR" not in os.environ:    # a bare single-process --sharded run
+            os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=os.environ.get("MASTER_PORT", "29531"),
+                              RANK="0", WORLD_SIZE="1")
+        # NCCL prints its version banner on stdout when the communicator is created: keep stdout for
+        # the one JSON line (the banner goes to stderr)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     from paper_2602_15917_b200 import Pipeline, build
     from paper_2602_15917_b200 import _lib as L
 
@@ -246,7 +264,7 @@ def main():
     if args.background != "none":
         kw.update(background=synth.flat_field(cfg, device=dev)[:, :].contiguous(), bg=args.background,
                   polarity=0 if args.background == "rev" else cfg.polarity)
-    if world > 1:
+    if dist_on:
         from paper_2602_15917_b200.sharded import ShardedPipeline
 
         p = ShardedPipeline(cfg.shape, cfg.dtype, z0=z0, nz=z1 - z0, group=dist.group.WORLD, device=dev,
@@ -286,7 +304,7 @@ def main():
 
     uuid = torch.cuda.get_device_properties(dev).uuid
     uuid = "GPU-" + str(uuid) if not str(uuid).startswith("GPU-") else str(uuid)
-    if world > 1:
+    if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(uuid) as clk:
@@ -303,7 +321,7 @@ def main():
         end = torch.cuda.Event(enable_timing=True)
         end.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if dist_on:
             dist.barrier()
     ms_local = start.elapsed_time(end)
     stage_ms = {}
@@ -314,8 +332,8 @@ def main():
     s = p.scalars()
     if s.err:
         raise SystemExit("device error bits 0x%x during the timed steps" % s.err)
-    count_local = int(s.count) if world == 1 else int(p.local_count())
-    if world > 1:
+    count_local = int(s.count) if not dist_on else int(p.local_count())
+    if dist_on:
         t = torch.tensor([ms_local], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
@@ -337,7 +355,7 @@ def main():
     # (scripts/ncu_traffic.py): dram__bytes_read.sum + dram__bytes_write.sum over its kernels
     traffic = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic_%s.json" % cfg.name)
-    if os.path.exists(tf) and args.scale == 1.0 and world == 1:
+    if os.path.exists(tf) and args.scale == 1.0 and not dist_on:
         st_ = json.load(open(tf)).get("stages", {}).get(dom)
         if st_:
             traffic = st_["dram_bytes"]
@@ -365,15 +383,15 @@ def main():
     }
     clocks = clk.summary()
     line["clocks"] = clocks
-    if args.greedy is not None and world == 1 and cfg.dtype == "u16":
+    if args.greedy is not None and not dist_on and cfg.dtype == "u16":
         line["next2_greedy"] = next2(p, x, cfg, args)
-    if not args.no_next4 and world == 1:
+    if not args.no_next4 and not dist_on:
         line["next4"] = next4(p, x, cfg, args, count)
     # ---- end to end through the public API with host buffers (every rank its slab; max over ranks)
     if not args.no_e2e:
-        line["e2e"] = e2e(p, x, cfg, args, world)
+        line["e2e"] = e2e(p, x, cfg, args, world, dist_on)
     # ---- CPU baseline: the oracle on a bounded sample, rank 0 at N = 1
-    if not args.no_cpu_baseline and world == 1 and rank == 0:
+    if not args.no_cpu_baseline and not dist_on and rank == 0:
         nz = sample_planes(cfg, 6e6)
         x_np = synth.to_numpy(x[:nz], cfg)
         B_np = kw["background"].cpu().numpy().view(np.uint16) if "background" in kw else None
@@ -384,7 +402,7 @@ def main():
                                           (cfg.name, nz, x_np.size, x_np.nbytes / 1e6, reps)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 
@@ -501,7 +519,7 @@ def next4(p, x, cfg, args, count):
             "counts": q["counts"], "spatial_reduction": q["spatial_reduction_voxels"]}
 
 
-def e2e(p, x, cfg, args, world=1):
+def e2e(p, x, cfg, args, world=1, dist_on=False):
     """Same metric through the public API with HOST buffers: every step copies the input (this rank's
     slab) from pinned host memory, runs the path, and reads the result (count, code stream, kept
     mask) back.  N > 1: wall time max over ranks, bytes summed over ranks."""
@@ -509,7 +527,7 @@ def e2e(p, x, cfg, args, world=1):
 
     from paper_2602_15917_b200 import _lib as L
 
-    if world == 1:
+    if not dist_on:
         return e2e_pipelined(p, x, cfg, args)
     P = getattr(p, "S", p)                       # the slab state of a sharded pipeline
     xh = x.cpu().pin_memory()
@@ -537,7 +555,7 @@ def e2e(p, x, cfg, args, world=1):
 
     one()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on:
         import torch.distributed as dist
 
         dist.barrier()
@@ -546,7 +564,7 @@ def e2e(p, x, cfg, args, world=1):
         one()
     dt = (time.perf_counter() - t0) / steps
     h2d = x.numel() * x.element_size()
-    if world > 1:
+    if dist_on:
         v = torch.tensor([dt, float(h2d), float(d2h)], dtype=torch.float64, device=x.device)
         t = v[0:1].clone()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -77,3 +77,52 @@ def test_component_spanning_every_slab():
         np.testing.assert_array_equal(got.reshape(v.shape), ref["K"])
         tab = np.concatenate([S.collect().comp_min.cpu().numpy() for S in states])
         np.testing.assert_array_equal(tab, ref["comp_min"].astype(np.int64))
+
+
+def test_distcomm_nccl_single_rank():
+    """The torch.distributed (NCCL) exchange layer on the GPU: a one-rank process group runs
+    ShardedPipeline through DistComm (histogram all-reduce, min/max, counts all-gather) and matches
+    the 1-GPU pipeline.  (Several ranks need several GPUs; their exchanges are covered by the gloo
+    test in test_sharded_host.py and by the simulated G-invariance above.)"""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2602_15917_b200.sharded import ShardedPipeline
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % port, rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        for cfg in (synth.scaled("C2", 0.25), synth.scaled("C4", 0.0625)):
+            x = synth.generate(cfg)
+            one = Pipeline(cfg.shape, cfg.dtype, **_kw(cfg)).run(x)
+            sp = ShardedPipeline(cfg.shape, cfg.dtype, z0=0, nz=cfg.shape[0], group=dist.group.WORLD,
+                                 device=torch.device("cuda", 0), **_kw(cfg))
+            r = sp.run(x)
+            assert torch.equal(r.codes, one.codes) and torch.equal(r.keep_bits, one.keep_bits)
+            assert sp.local_count() == one.count
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_sharded_path_one_rank():
+    """bench.py's multi-GPU code path (ShardedPipeline over NCCL, barriers, max over ranks, e2e with
+    host buffers) on one rank: one clean JSON line on stdout."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MASTER_PORT="29537")
+    r = subprocess.run([sys.executable, "bench.py", "--sharded", "--config", "C1", "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline"], cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["config"]["parallelism"] == "zslab1" and d["value"] > 0 and d["e2e"]["value"] > 0
