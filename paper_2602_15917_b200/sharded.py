@@ -312,11 +312,24 @@ class DistComm:
                 S.counts[1:2].copy_(allc[self.rank - 1])
             return None
         if kind == "gather_tables":
-            pairs, labels, sizes = _read_tables(S)
-            objs = [None] * self.world
-            d.all_gather_object(objs, (pairs, labels, sizes), group=grp)
-            return (np.concatenate([o[0] for o in objs]).reshape(-1, 2), np.concatenate([o[1] for o in objs]),
-                    np.concatenate([o[2] for o in objs]))
+            # tensor collectives (no pickling): the (pairs, roots) counts of every rank, then the used
+            # prefix of every rank's pair and root lists, padded to the largest
+            c = S.counts[2:4].clone()
+            allc = [torch.empty_like(c) for _ in range(self.world)]
+            d.all_gather(allc, c, group=grp)
+            cnt = [(int(min(t[0].item(), S.pair_cap)), int(min(t[1].item(), S.root_cap))) for t in allc]
+            mp = max(1, max(a for a, _ in cnt))
+            mr = max(1, max(b for _, b in cnt))
+            payload = torch.cat([S.pairs[: 2 * mp], S.root_lab[:mr], S.root_size[:mr]]).contiguous()
+            allp = [torch.empty_like(payload) for _ in range(self.world)]
+            d.all_gather(allp, payload, group=grp)
+            pairs, labels, sizes = [], [], []
+            for (np_, nr), t in zip(cnt, allp):
+                a = t.cpu().numpy().view(np.uint64)
+                pairs.append(a[: 2 * np_])
+                labels.append(a[2 * mp: 2 * mp + nr])
+                sizes.append(a[2 * mp + mr: 2 * mp + mr + nr])
+            return (np.concatenate(pairs).reshape(-1, 2), np.concatenate(labels), np.concatenate(sizes))
         if kind in ("best_max", "best_min"):
             k = 0 if kind == "best_max" else 1
             v = msg[1][k:k + 1].clone()
