@@ -307,23 +307,35 @@ def main():
     if dist_on:
         dist.barrier()
     torch.cuda.synchronize()
+    # inputs smaller than twice the 126 MB L2 (C1): L2 flushed between timed steps by writing 512 MB,
+    # each step timed on its own; larger inputs evict themselves
+    flush = cfg.nbytes // world < 256 * 1024 * 1024
+    scratch = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev) if flush else None
     with Clocks(uuid) as clk:
         start = torch.cuda.Event(enable_timing=True)
         start.record(stream)
+        spans = []
         for i in range(args.steps):
+            if flush:
+                scratch.fill_(i & 0xff)
+                b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                b0.record(stream)
             if args.graph:
                 graphs[i].replay()
-                continue
-            s0 = torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
-            ev.append([("start", s0)])
-            p.enqueue(x, mark=mark)
+            else:
+                s0 = torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                ev.append([("start", s0)])
+                p.enqueue(x, mark=mark)
+            if flush:
+                b1.record(stream)
+                spans.append((b0, b1))
         end = torch.cuda.Event(enable_timing=True)
         end.record(stream)
         torch.cuda.synchronize()
         if dist_on:
             dist.barrier()
-    ms_local = start.elapsed_time(end)
+    ms_local = sum(a.elapsed_time(b) for a, b in spans) if flush else start.elapsed_time(end)
     stage_ms = {}
     for step in ev:
         for (a, ea), (b, eb_) in zip(step[:-1], step[1:]):
@@ -369,7 +381,9 @@ def main():
                    "polarity": "LOW" if cfg.polarity else "HIGH", "classes": args.classes,
                    "frames": args.frames, "keep": args.keep,
                    "background": args.background, "fused": args.fused, "parallelism": "zslab%d" % world,
-                   "l2": "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
+                   "l2": ("input %.0f MB < 2 x 126 MB L2: 512 MB written between timed steps, each step timed "
+                          "alone" % (cfg.nbytes / 1e6)) if flush else
+                         "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
         "roofline": {"bound": "hbm", "kernel": STAGE_CALLS.get(dom, dom), "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "alg_bytes": ab[dom],
                      "peak_source": peak_src},
