@@ -923,16 +923,16 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
         // are not whole words)
         if (r < r1) {
             const uint64_t Bg = (uint64_t)r * A.nx, Be = Bg + A.nx;
-            const uint32_t sh = (uint32_t)(Bg & 31);
-            const uint64_t wf = Bg >> 5, wl = (Be - 1) >> 5;
-            for (uint64_t wi = wf + lane_id(); wi <= wl; wi += 32) {
-                const int64_t b = (int64_t)(32 * (wi - wf)) - (int64_t)sh;   // row bit of the word's bit 0
-                uint32_t val;
-                if (b < 0) val = od[0] << sh;
-                else val = __funnelshift_r(od[b >> 5], od[(b >> 5) + 1], (uint32_t)(b & 31));
-                const bool whole = wi * 32 >= Bg && wi * 32 + 32 <= Be;
-                if (whole) A.o[wi] = val;
-                else if (val) atomicOr(&A.o[wi], val);
+            const uint32_t sh = (uint32_t)(Bg & 31), esh = (uint32_t)(Be & 31);
+            const uint64_t wf = Bg >> 5;
+            const uint32_t nwo = (uint32_t)(((Be - 1) >> 5) - wf + 1);   // output words the row touches
+            uint32_t *dst = A.o + wf;
+            for (uint32_t j = lane_id(); j < nwo; j += 32) {
+                // output word j = row bits [32 j - sh, 32 j - sh + 32)
+                const uint32_t val = sh == 0 ? od[j] : (j == 0 ? od[0] << sh : __funnelshift_r(od[j - 1], od[j], 32 - sh));
+                const bool whole = (j > 0 || sh == 0) && (j + 1 < nwo || esh == 0);
+                if (whole) dst[j] = val;
+                else if (val) atomicOr(&dst[j], val);
             }
         }
         __syncthreads();
