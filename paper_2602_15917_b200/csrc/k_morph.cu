@@ -300,14 +300,16 @@ __device__ __forceinline__ void load_m_row(const uint32_t *__restrict__ src, uin
     const uint32_t sh = (uint32_t)(bit0 & 31);
     const uint64_t w0 = bit0 >> 5;
     const uint32_t tail = (uint32_t)(X - 32ull * (W - 1));
+    const uint32_t *row = src + w0;
+    // words of the row readable past its first one (32-bit from here on)
+    const uint32_t avail = (uint32_t)min(src_words - w0, (uint64_t)W + 1);
     for (uint32_t k0 = lane_id(); k0 < W; k0 += 32 * U) {
         uint32_t v[U], nx[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t k = k0 + 32 * u;
-            const uint64_t wi = w0 + k;
-            v[u] = k < W ? src[wi] : 0u;
-            nx[u] = (k < W && sh && wi + 1 < src_words) ? src[wi + 1] : 0u;
+            v[u] = k < W ? row[k] : 0u;
+            nx[u] = (k < W && sh && k + 1 < avail) ? row[k + 1] : 0u;
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
