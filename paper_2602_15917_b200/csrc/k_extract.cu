@@ -49,30 +49,30 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract_count(const uint32_t *__
     const uint64_t wpg = (uint64_t)gridDim.x * (EX_THREADS / 32);
     const uint32_t lane = lane_id();
     const uint4 *K4 = reinterpret_cast<const uint4 *>(K);
-    for (uint64_t t0 = (uint64_t)blockIdx.x * (EX_THREADS / 32) + (threadIdx.x >> 5); t0 < ntiles; t0 += 2 * wpg) {
-        uint32_t c[2] = {0, 0};
+    constexpr int U = 4;   // tiles per warp iteration: their 2 U 16-byte loads are issued together
+    for (uint64_t t0 = (uint64_t)blockIdx.x * (EX_THREADS / 32) + (threadIdx.x >> 5); t0 < ntiles; t0 += U * wpg) {
+        uint4 v[U][2];
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
-            const uint64_t t = t0 + u * wpg;
-            if (t >= ntiles) continue;
+        for (int u = 0; u < U; u++)
 #pragma unroll
             for (int h = 0; h < 2; h++) {
-                const uint64_t wi = t * EX_WORDS + (h * 32 + lane) * 4;   // first word of this 16-byte load
-                if (wi + 4 <= nwords) {
-                    uint4 v = __ldcs(K4 + wi / 4);
-                    c[u] += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-                } else {
-                    for (uint64_t k = wi; k < nwords && k < wi + 4; k++) c[u] += __popc(K[k]);
-                }
+                const uint64_t wi = (t0 + u * wpg) * EX_WORDS + (h * 32 + lane) * 4;   // first word of the load
+                v[u][h] = (t0 + u * wpg < ntiles && wi + 4 <= nwords) ? __ldcs(K4 + wi / 4) : make_uint4(0, 0, 0, 0);
             }
-        }
 #pragma unroll
-        for (int u = 0; u < 2; u++) {
-            uint32_t v = c[u];
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+        for (int u = 0; u < U; u++) {
             const uint64_t t = t0 + u * wpg;
-            if (lane == 0 && t < ntiles) w.tcount[t] = v;
+            if (t >= ntiles) break;
+            uint32_t c = 0;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint64_t wi = t * EX_WORDS + (h * 32 + lane) * 4;
+                if (wi + 4 <= nwords) c += __popc(v[u][h].x) + __popc(v[u][h].y) + __popc(v[u][h].z) + __popc(v[u][h].w);
+                else
+                    for (uint64_t k = wi; k < nwords && k < wi + 4; k++) c += __popc(K[k]);
+            }
+            c = __reduce_add_sync(FULL, c);
+            if (lane == 0) w.tcount[t] = c;
         }
     }
 }
