@@ -379,3 +379,31 @@ def test_pipeline_background_vs_oracle(frames):
     np.testing.assert_array_equal(xh.cpu().numpy().view(np.uint16), want)
     q = p.quality(tw)
     assert q["dsc"] > 0.95, q
+
+
+def test_edge_cases_next_rows():
+    """NEXT-3 edge cases: multi-Otsu with only two populated norm8 bins is DEGENERATE; keep-
+    largest on an empty ROI keeps nothing; per-frame thresholds with a constant frame is DEGENERATE;
+    SUB background with its reconstruction (min(65535, M + B)) against the oracle."""
+    v = np.full((4, 8, 40), 100, np.uint16)
+    v[1:3, 2:6, 5:30] = 3000
+    with pytest.raises(L.RoixError):
+        Pipeline(v.shape, "u16", eb=1.0, classes=3).run(dev(v))
+    z, y, xx = np.indices((4, 8, 40))
+    cb = np.where((z + y + xx) % 2 == 0, 1000, 10).astype(np.uint16)   # opens to nothing
+    r = Pipeline(cb.shape, "u16", eb=1.0, keep="largest").run(dev(cb))
+    assert r.count == 0 and r.n_kept == 0
+    fr = np.stack([v[1], np.full((8, 40), 7, np.uint16)])
+    with pytest.raises(L.RoixError):
+        Pipeline(fr.shape, "u16", eb=1.0, frames=True, se=4, conn=8).run(dev(fr))
+    rng = np.random.default_rng(4)
+    B = rng.integers(50, 150, (8, 40)).astype(np.uint16)
+    x = (v.astype(np.int64) + B[None]).clip(0, 65535).astype(np.uint16)
+    p = Pipeline(x.shape, "u16", eb=2.0, min_size=8, background=dev(B), bg="sub")
+    res = p.run(dev(x))
+    ref = oracle.pipeline(x, eb=2.0, min_size=8, background_ref=B, bg="sub")
+    np.testing.assert_array_equal(words_to_mask(res.keep_bits, p.n).reshape(x.shape), ref["K"])
+    np.testing.assert_array_equal(res.codes.cpu().numpy().view(np.uint16), ref["stream"])
+    xh = p.decode().cpu().numpy().view(np.uint16)
+    want = oracle.background(oracle.decode_mask(ref["K"], ref["stream"], oracle.step(2.0), np.uint16), B, "add")
+    np.testing.assert_array_equal(xh, want)
