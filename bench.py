@@ -5,9 +5,11 @@
 
 A step is one pass of the whole hot path (range [fp32] -> histogram -> Otsu threshold -> binarise +
 opening -> CCL + small-object filter -> quantise + compact) over one synthetic volume of a
-BASELINE.json config (default configs[1] = C2, 512^3 fp32; inputs > L2, so no L2 flush between
-steps).  N > 1: launched by torchrun; the volume is z-slab sharded over the ranks (NCCL), whole-job
-throughput, max-over-ranks device time.  Rank 0 prints one JSON line.
+BASELINE.json config (default C3, the paper's own 13.9k x 9.7k 10-bit detector as a
+128-frame stack: the largest config BASELINE.json assigns to one GPU; 34.5 GB of input > L2, so no L2
+flush between steps).  N > 1: one rank per GPU -- launched by torchrun, or re-launched under torchrun
+by this script when WORLD_SIZE is unset; the volume is z-slab sharded over the ranks (NCCL),
+whole-job throughput, max-over-ranks device time.  Rank 0 prints one JSON line.
 
 --impl reference times the oracle (oracle/, plain single-threaded C + exact-rational Otsu) on the
 host cores, on a bounded sample of the same workload -- the reference arm of this tier.
@@ -35,7 +37,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3")
     ap.add_argument("--scale", type=float, default=1.0, help="profiling aid: a scaled phantom of the config")
     ap.add_argument("--impl", default="roix", choices=["roix", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -140,7 +142,39 @@ STAGE_CALLS = {"range": "roix_range (k_range)", "histogram": "roix_histogram (k_
 
 
 def cpu_info():
-    return {"cores_available": os.cpu_count()}
+    """The host the oracle runs on: CPU model, online cores, memory."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    mem_gb = None
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                mem_gb = round(int(line.split()[1]) / 1024 ** 2, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "mem_total_gib": mem_gb}
+
+
+def relaunch_if_needed(args):
+    """--gpus N > 1 without torchrun: re-launch this command under torchrun (one rank per GPU).
+    Under torchrun, N must equal WORLD_SIZE."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus > 1:
+            port = os.environ.get("MASTER_PORT", "29533")
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=%d" % args.gpus,
+                   "--master-addr", "127.0.0.1", "--master-port", port, os.path.abspath(__file__)] + sys.argv[1:]
+            raise SystemExit(subprocess.call(cmd))
+        return
+    if int(ws) != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%s (launch one rank per GPU)" % (args.gpus, ws))
 
 
 # ------------------------------------------------------------------------------- oracle timing
@@ -203,12 +237,14 @@ def reference_arm(args, cfg):
     value = x_np.nbytes / per / 1e9
     sample = "%s planes [0,%d) of %s (%d voxels, %.1f MB), whole oracle pipeline per step" % (
         cfg.name, nz, "x".join(map(str, cfg.shape)), x_np.size, x_np.nbytes / 1e6)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u16" if cfg.dtype == "u16" else "f32",
             "data": "synthetic", "config": {"workload": cfg.name, "shape": list(cfg.shape), "sample_planes": nz,
                                             "classes": args.classes, "frames": args.frames, "keep": args.keep},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "host": cpu_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -216,6 +252,7 @@ def reference_arm(args, cfg):
 # ------------------------------------------------------------------------------------ GPU arm
 def main():
     args = parse()
+    relaunch_if_needed(args)
     args.graph = not args.no_graph and not args.sharded and int(os.environ.get("WORLD_SIZE", "1")) == 1
     import synth
 
@@ -413,7 +450,8 @@ def main():
                                 bg=args.background)
         line["cpu_baseline"] = {"value": x_np.nbytes / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": "%s planes [0,%d) (%d voxels, %.1f MB), whole oracle pipeline, best of %d" %
-                                          (cfg.name, nz, x_np.size, x_np.nbytes / 1e6, reps)}
+                                          (cfg.name, nz, x_np.size, x_np.nbytes / 1e6, reps),
+                                "host": cpu_info()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist_on:

@@ -145,6 +145,13 @@ roix_status roix_histogram(const void *x, roix_dtype dtype, uint64_t n, roix_sca
                            uint32_t nbins, roix_stream_t stream);
 
 /*
+ * Zero hist[0 .. nbins) (device uint64) on `stream` -- the start of a2 for an accumulating histogram
+ * (one kernel of this library, so a captured step holds no foreign kernels).  nbins = 0 is a no-op;
+ * hist must be 16-byte aligned.
+ */
+roix_status roix_histogram_clear(uint64_t *hist, uint64_t nbins, roix_stream_t stream);
+
+/*
  * a3 THRESHOLD (Eq. 1 P:255-257 with round-half-up S:82; Otsu P:263-267 with k = 2, smallest t on
  * ties S:170; reading G-8/G-9).  u16: I_max = largest populated bin (1 if none above 0),
  * h8[norm8(v)] += hist[v] with norm8(v) = floor((510 v + I_max) / (2 I_max)).  fp32: hist is already

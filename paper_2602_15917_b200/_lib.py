@@ -66,6 +66,7 @@ _SIGS = {
     "roix_resolve": (_i32, [_vp, _i32, _f64, _vp]),
     "roix_quantize": (_i32, [_vp, _i32, _u64, _vp, _vp, _vp]),
     "roix_histogram": (_i32, [_vp, _i32, _u64, _vp, _vp, _u32, _vp]),
+    "roix_histogram_clear": (_i32, [_vp, _u64, _vp]),
     "roix_threshold": (_i32, [_vp, _u32, _i32, _i32, _vp, _vp]),
     "roix_morph_workspace": (_i32, [ctypes.POINTER(Geom), ctypes.POINTER(ctypes.c_size_t)]),
     "roix_morph": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),

@@ -108,6 +108,12 @@ roix_status roix_histogram(const void *x, roix_dtype dtype, uint64_t n, roix_sca
     return cuda(launch_hist_f32((const float *)x, n, sc, hist, st), "roix_histogram");
 }
 
+roix_status roix_histogram_clear(uint64_t *hist, uint64_t nbins, roix_stream_t stream) {
+    if (nbins == 0) return ROIX_OK;
+    if (!hist || !aligned16(hist)) return invalid("hist must be a 16-byte aligned device pointer");
+    return cuda(launch_hist_clear(hist, nbins, (cudaStream_t)stream), "roix_histogram_clear");
+}
+
 roix_status roix_threshold(const uint64_t *hist, uint32_t nbins, roix_dtype dtype, roix_polarity polarity,
                            roix_scalars *sc, roix_stream_t stream) {
     if (!sc || !hist) return invalid("sc / hist is NULL");
@@ -266,6 +272,8 @@ roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const r
                        uint64_t min_size, uint64_t run_capacity, void *ws, size_t ws_bytes,
                        const roix_label_out *out, roix_scalars *sc, roix_stream_t stream) {
     if (!sc || !o_bits || !out || !ws) return invalid("sc / o_bits / out / ws is NULL");
+    if (!aligned16(o_bits) || (out->keep_bits && !aligned16(out->keep_bits)) || (row_runs && !aligned16(row_runs)))
+        return invalid("o_bits / keep_bits / row_runs must be 16-byte aligned");
     if (!geom_ok(g)) return invalid("geometry");
     if (conn != 4 && conn != 8 && conn != 6 && conn != 18 && conn != 26) return unsupported("conn (4, 8, 6, 18, 26)");
     size_t need = 0;
@@ -293,6 +301,8 @@ roix_status roix_label_local(const uint32_t *o_bits, const uint32_t *row_runs, c
                              uint64_t run_capacity, void *ws, size_t ws_bytes, roix_scalars *sc,
                              roix_stream_t stream) {
     if (!sc || !o_bits) return invalid("sc / o_bits is NULL");
+    if (!aligned16(o_bits) || (row_runs && !aligned16(row_runs)))
+        return invalid("o_bits / row_runs must be 16-byte aligned");
     if (conn != 4 && conn != 8 && conn != 6 && conn != 18 && conn != 26) return unsupported("conn (4, 8, 6, 18, 26)");
     roix_status s = label_common(g, run_capacity, ws, ws_bytes);
     if (s != ROIX_OK) return s;
@@ -441,6 +451,7 @@ roix_status roix_extract(const void *x, roix_dtype dtype, uint64_t n, const uint
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (n == 0) return ROIX_OK;
     if (!x || !aligned16(x)) return invalid("x must be 16-byte aligned");
+    if (!aligned16(keep_bits)) return invalid("keep_bits must be 16-byte aligned");
     if (capacity > 0 && (!codes_out || !aligned16(codes_out))) return invalid("codes_out must be 16-byte aligned");
     if (ws_bytes < extract_workspace_bytes(n)) return invalid("workspace too small (see roix_extract_workspace)");
     return cuda(launch_extract(x, (int)dtype, n, keep_bits, sc, codes_out, capacity, offset, ws, (cudaStream_t)stream),
@@ -474,6 +485,7 @@ roix_status roix_row_spans(const uint32_t *keep_bits, const void *x, roix_dtype 
                            roix_scalars *sc, roix_span *spans, uint64_t span_cap, void *codes, uint64_t code_cap,
                            uint64_t *counts, void *ws, size_t ws_bytes, roix_stream_t stream) {
     if (!sc || !keep_bits || !counts || !ws) return invalid("sc / keep_bits / counts / ws is NULL");
+    if (!aligned16(keep_bits)) return invalid("keep_bits must be 16-byte aligned");
     if (!dtype_ok(dtype)) return invalid("dtype");
     size_t need = 0;
     roix_status s = roix_row_spans_workspace(g, &need);

@@ -22,7 +22,7 @@ __device__ __forceinline__ uint32_t bg_word(uint32_t x, uint32_t b) {
 // reused (a C3 frame is 270 MB, twice the L2: a frame-major order would re-read B from HBM per frame).
 // Four frames in flight per thread.
 template <int OP>
-__global__ void __launch_bounds__(256) k_background_vec(const uint16_t *__restrict__ x, const uint16_t *__restrict__ B,
+__global__ void __launch_bounds__(256) k_background_vec(const uint16_t *x, const uint16_t *__restrict__ B,
                                                         uint64_t A, uint64_t nz, uint16_t *out) {
     const uint64_t n8 = A / 8, A8 = A / 8;
     const uint4 *x4 = reinterpret_cast<const uint4 *>(x);
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) k_background_vec(const uint16_t *__restri
 }
 
 template <int OP>
-__global__ void __launch_bounds__(256) k_background_scalar(const uint16_t *__restrict__ x,
+__global__ void __launch_bounds__(256) k_background_scalar(const uint16_t *x,
                                                            const uint16_t *__restrict__ B, uint64_t A, uint16_t *out) {
     const uint64_t z = blockIdx.y;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < A; i += (uint64_t)gridDim.x * blockDim.x)

@@ -27,7 +27,6 @@ struct MorphArgs {
     uint64_t zchunk;         // 3-D: planes per CTA
     uint64_t rows_per_cta;   // 2-D: rows per CTA
     int aligned_out;         // 1: plain stores of whole words; 0: atomicOr into zeroed o
-    int async;               // 3-D: rows are whole 16-byte units (X % 128 == 0): cp.async prefetch
     const uint32_t *halo_lo, *halo_hi;
     uint32_t *o;
     uint32_t *row_runs;
@@ -654,181 +653,6 @@ __global__ void __launch_bounds__(256, 3) k_open3d_reg(MorphArgs A, roix_scalars
     }
 }
 
-// ------------------------------------------------------- fused 3-D binarise + opening (x-tiled)
-// A CTA owns a tile of FX = 256 voxels (8 words) x TY rows of every plane of a z-chunk and marches
-// along z.  The raw rows of plane p + NSLOT - 1 are streamed into a shared-memory ring by TMA bulk
-// copies (cp.async.bulk, completion on an mbarrier per slot) while plane p is binarised and opened,
-// so x is read once (plus one 16-byte group on each side of every row -- the +-2 voxel reach of the
-// opening -- and 2 halo rows per band side, mostly L2 hits from the neighbouring tiles) and m never
-// leaves the SM.  Requires X % 256 == 0 (otherwise binarise + open3d).
-// Shared m / e rows: words -1 .. 8 of the tile (index 0 .. 9); words -1 / 8 hold the halo bits.
-constexpr int FX = 256, FW = FX / 32, FWS = FW + 2, NSLOT = 4;
-
-template <typename T, int TY>
-__global__ void __launch_bounds__(256) k_morph3d_fused(const T *__restrict__ x, MorphArgs A, roix_scalars *sc) {
-    constexpr int VPL = Cmp<T>::VPL;
-    constexpr int NG = FX / VPL;                // 16-byte groups per tile row
-    constexpr int GPL = NG / 32;                // main groups per lane (u16 1, f32 2)
-    constexpr int MR = TY + 4, ER = TY + 2;
-    constexpr int RB = FX * (int)sizeof(T) + 32;  // raw row: [left halo 16 B][main][right halo 16 B]
-    extern __shared__ __align__(128) unsigned char raw[];   // [NSLOT][MR][RB]
-    __shared__ __align__(8) uint64_t bars[NSLOT];
-    __shared__ uint32_t mring[3][MR][FWS];
-    __shared__ uint32_t ering[3][ER][FWS];
-    if (get_err(sc)) return;
-    const Cmp<T> cmp(sc);
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    const int64_t X = A.nx, Y = A.ny;
-    const int64_t x0 = (int64_t)blockIdx.x * FX;
-    const int64_t y0 = (int64_t)blockIdx.y * TY;
-    const int64_t zs = (int64_t)blockIdx.z * A.zchunk;
-    const int64_t ze = min((int64_t)A.nz, zs + (int64_t)A.zchunk);
-    if (zs >= ze) return;
-    const bool has_l = x0 > 0, has_r = x0 + FX < X;
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < NSLOT; i++) mbar_init(&bars[i], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    __syncthreads();
-    const int64_t p_first = zs - 2, p_last = ze + 1;
-    // warp 0: stream the in-slab rows of plane p into its ring slot
-    auto issue = [&](int64_t p) {
-        const int slot = (int)((p - p_first) % NSLOT);
-        unsigned char *base = raw + (size_t)slot * MR * RB;
-        const bool in = p >= 0 && p < (int64_t)A.nz;
-        int y_lo = (int)max((int64_t)0, y0 - 2), y_hi = (int)min(Y, y0 + TY + 2);
-        const uint32_t nrows = in && y_hi > y_lo ? (uint32_t)(y_hi - y_lo) : 0u;
-        const uint32_t rbytes = FX * sizeof(T) + (has_l ? 16 : 0) + (has_r ? 16 : 0);
-        if (lane == 0) mbar_arrive_expect_tx(&bars[slot], nrows * rbytes);
-        __syncwarp();
-        for (uint32_t i = lane; i < nrows; i += 32) {
-            const int64_t y = y_lo + i;
-            const int r = (int)(y - (y0 - 2));
-            const T *src = x + ((uint64_t)p * A.ny + y) * A.nx + x0;
-            unsigned char *dst = base + (size_t)r * RB + 16;
-            if (has_l) {
-                src -= 16 / sizeof(T);
-                dst -= 16;
-            }
-            bulk_g2s(dst, src, rbytes, &bars[slot]);
-        }
-    };
-    if (warp == 0)
-        for (int64_t p = p_first; p < p_first + NSLOT - 1 && p <= p_last; p++) issue(p);
-    for (int64_t p = p_first; p <= p_last; p++) {
-        const int slot = (int)((p - p_first) % NSLOT);
-        const uint32_t parity = (uint32_t)(((p - p_first) / NSLOT) & 1);
-        // 1. m(p) from the ring slot (or a halo plane / the volume border)
-        mbar_wait(&bars[slot], parity);
-        {
-            const int64_t gp = (int64_t)A.z0 + p;
-            const bool in_slab = p >= 0 && p < (int64_t)A.nz;
-            const unsigned char *base = raw + (size_t)slot * MR * RB;
-            for (int r = warp; r < MR; r += 8) {
-                const int64_t y = y0 - 2 + r;
-                uint32_t *dst = mring[(p + 3) % 3][r];
-                if (y < 0 || y >= Y || gp < 0 || gp >= (int64_t)A.gz) {
-                    if (lane < FWS) dst[lane] = FULL;
-                    continue;
-                }
-                if (!in_slab) {   // halo plane from the neighbouring slab (packed m bits of the whole plane)
-                    const uint64_t plane_w = (A.ny * A.nx + 31) / 32;
-                    const uint32_t *src = p < 0 ? A.halo_lo + (uint64_t)(p + 2) * plane_w
-                                                : A.halo_hi + (uint64_t)(p - A.nz) * plane_w;
-                    const uint64_t w0 = ((uint64_t)y * A.nx + x0) >> 5;   // X % 256 == 0: word aligned
-                    if (lane < FWS) {
-                        const int k = (int)lane - 1;
-                        uint32_t v = FULL;
-                        if ((k >= 0 && k < FW) || (k < 0 && has_l) || (k == FW && has_r)) v = src[w0 + k];
-                        dst[lane] = v;
-                    }
-                    continue;
-                }
-                const unsigned char *row = base + (size_t)r * RB;
-                uint32_t P = 0;
-#pragma unroll
-                for (int c = 0; c < GPL; c++)
-                    P |= cmp.bits(*reinterpret_cast<const uint4 *>(row + 16 + (c * 32 + lane) * 16)) << (c * VPL);
-                constexpr int GW = 32 / VPL;            // groups per word
-                const uint32_t cc = (lane * GW) / 32;   // register chunk holding word `lane`'s groups
-                uint32_t w = 0;
-#pragma unroll
-                for (int q = 0; q < GW; q++) {
-                    const uint32_t v = __shfl_sync(FULL, P, (lane * GW + q) % 32);
-                    w |= ((v >> (cc * VPL)) & ((1u << VPL) - 1u)) << (q * VPL);
-                }
-                if (lane < FW) dst[lane + 1] = w;
-                if (lane == FW)
-                    dst[0] = has_l ? ((cmp.bits(*reinterpret_cast<const uint4 *>(row)) << (32 - VPL)) | low_mask(32 - VPL))
-                                   : FULL;
-                if (lane == FW + 1)
-                    dst[FW + 1] = has_r ? (cmp.bits(*reinterpret_cast<const uint4 *>(row + 16 + FX * sizeof(T))) |
-                                           ~low_mask(VPL))
-                                        : FULL;
-            }
-        }
-        __syncthreads();   // slot p consumed, m(p) visible
-        if (warp == 0 && p + NSLOT - 1 <= p_last) issue(p + NSLOT - 1);   // reuses the slot of plane p - 1
-        // 2. e(q = p-1): rows y0-1 .. y0+TY, words -1 .. FW (index 0 .. FWS-1)
-        const int64_t q = p - 1;
-        if (q >= zs - 1) {
-            const int64_t gq = (int64_t)A.z0 + q;
-            const bool qin = gq >= 0 && gq < (int64_t)A.gz;
-            const uint32_t(*mc)[FWS] = mring[(q + 3) % 3];
-            const uint32_t(*mf)[FWS] = mring[(q + 2) % 3];
-            const uint32_t(*mg)[FWS] = mring[(q + 4) % 3];
-            for (int t = threadIdx.x; t < ER * FWS; t += blockDim.x) {
-                const int r = t / FWS, k = t % FWS;
-                const int64_t y = y0 - 1 + r;
-                uint32_t v = 0;
-                if (qin && y >= 0 && y < Y && !(k == 0 && !has_l) && !(k == FWS - 1 && !has_r)) {
-                    const uint32_t cw = mc[r + 1][k];
-                    const uint32_t l = k > 0 ? __funnelshift_l(mc[r + 1][k - 1], cw, 1) : (cw << 1) | 1u;
-                    const uint32_t rr = k < FWS - 1 ? __funnelshift_r(cw, mc[r + 1][k + 1], 1) : (cw >> 1) | 0x80000000u;
-                    v = cw & l & rr & mc[r][k] & mc[r + 2][k] & mf[r + 1][k] & mg[r + 1][k];
-                }
-                ering[(q + 3) % 3][r][k] = v;
-            }
-        }
-        __syncthreads();
-        // 3. o(z = p-2): rows y0 .. y0+TY-1, words 0 .. FW-1, plus the run starts of the row segment
-        const int64_t z = p - 2;
-        if (z >= zs && z < ze) {
-            const uint32_t(*ec)[FWS] = ering[(z + 3) % 3];
-            const uint32_t(*ef)[FWS] = ering[(z + 2) % 3];
-            const uint32_t(*eg)[FWS] = ering[(z + 4) % 3];
-            for (int t = threadIdx.x; t < TY * FW; t += blockDim.x) {
-                const int r = t / FW, k = t % FW + 1;   // k: shared word index (1 .. FW)
-                const int64_t y = y0 + r;
-                const bool live = y < Y;
-                uint32_t o = 0, prev31 = 0;
-                if (live) {
-                    auto dil = [&](int kk) {
-                        const uint32_t cw = ec[r + 1][kk];
-                        uint32_t v = cw | ec[r][kk] | ec[r + 2][kk] | ef[r + 1][kk] | eg[r + 1][kk];
-                        v |= kk > 0 ? __funnelshift_l(ec[r + 1][kk - 1], cw, 1) : (cw << 1);
-                        v |= kk < FWS - 1 ? __funnelshift_r(cw, ec[r + 1][kk + 1], 1) : (cw >> 1);
-                        return v;
-                    };
-                    o = dil(k);
-                    // bit 31 of the previous word (word -1 only needs bit 31: its e bits 30, 31 are exact)
-                    prev31 = (k > 1 || has_l) ? (dil(k - 1) >> 31) : 0u;
-                }
-                const uint32_t starts = o & ~((o << 1) | prev31);
-                const uint64_t row = (uint64_t)z * A.ny + y;
-                if (live) A.o[(row * A.nx + x0) / 32 + (k - 1)] = o;
-                // run starts of this row segment: its 8 words sit in 8 consecutive lanes
-                uint32_t cnt = __popc(starts);
-                cnt += __shfl_xor_sync(FULL, cnt, 1);
-                cnt += __shfl_xor_sync(FULL, cnt, 2);
-                cnt += __shfl_xor_sync(FULL, cnt, 4);
-                if (live && A.row_runs && (lane & 7) == 0 && cnt) atomicAdd(&A.row_runs[row], cnt);
-            }
-        }
-        __syncthreads();
-    }
-}
-
 // ------------------------------------------------------------------------------------ 2-D opening
 // Rows r = q*Y + y of the slab (q = plane); neighbours only within the same plane.  S = rows per
 // step = warps per CTA.  The output rows of a step are contiguous bits [c X, (c+S) X) of o; they are
@@ -998,31 +822,6 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     A.m = m;
     A.m_words = nwords;
     cudaError_t e;
-    if (se == 6 && g.nx % FX == 0 && A.async < 0) {   // disabled: slower than binarise + k_open3d_reg
-        // fused: x -> o in one pass (m stays on chip)
-        const bool u16 = dtype == ROIX_U16;
-        const int TY = u16 ? 32 : 16;
-        const uint64_t xt = g.nx / FX, bands = (g.ny + TY - 1) / TY;
-        const uint64_t target = (uint64_t)num_sms() * 4;
-        uint64_t chunks = (target + xt * bands - 1) / (xt * bands);
-        const uint64_t cmax = g.nz >= 128 ? g.nz / 64 : 1;
-        if (chunks > cmax) chunks = cmax;
-        if (chunks < 1) chunks = 1;
-        A.zchunk = (g.nz + chunks - 1) / chunks;
-        chunks = (g.nz + A.zchunk - 1) / A.zchunk;
-        if (row_runs && (e = cudaMemsetAsync(row_runs, 0, g.nz * g.ny * 4, st)) != cudaSuccess) return e;
-        dim3 grid((unsigned)xt, (unsigned)bands, (unsigned)chunks);
-        if (u16) {
-            const size_t sm = (size_t)NSLOT * (32 + 4) * (FX * 2 + 32);
-            if ((e = set_smem(k_morph3d_fused<uint16_t, 32>, sm)) != cudaSuccess) return e;
-            k_morph3d_fused<uint16_t, 32><<<grid, 256, sm, st>>>((const uint16_t *)x, A, sc);
-        } else {
-            const size_t sm = (size_t)NSLOT * (16 + 4) * (FX * 4 + 32);
-            if ((e = set_smem(k_morph3d_fused<float, 16>, sm)) != cudaSuccess) return e;
-            k_morph3d_fused<float, 16><<<grid, 256, sm, st>>>((const float *)x, A, sc);
-        }
-        return cudaGetLastError();
-    }
     // a4: stream x -> m (after a fused speculative pass: resolve its window, binarise only on a miss)
     if (prebinarized && (e = launch_spec_resolve(x, dtype, g, sc, ws, st)) != cudaSuccess) return e;
     {

@@ -154,6 +154,23 @@ cudaError_t launch_scalars_init(roix_scalars *sc, float eb, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// zero an accumulating histogram (16-byte stores, grid-stride)
+__global__ void k_hist_clear(uint64_t *hist, uint64_t nbins) {
+    const uint64_t n2 = nbins / 2;
+    ulonglong2 *h2 = reinterpret_cast<ulonglong2 *>(hist);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * blockDim.x)
+        h2[i] = make_ulonglong2(0ull, 0ull);
+    if ((nbins & 1) && blockIdx.x == 0 && threadIdx.x == 0) hist[nbins - 1] = 0ull;
+}
+
+cudaError_t launch_hist_clear(uint64_t *hist, uint64_t nbins, cudaStream_t st) {
+    uint64_t need = (nbins / 2 + 255) / 256;
+    const uint64_t cap = (uint64_t)num_sms() * 4;
+    if (need < 1) need = 1;
+    k_hist_clear<<<(unsigned)(need < cap ? need : cap), 256, 0, st>>>(hist, nbins);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_range(const float *x, uint64_t n, roix_scalars *sc, cudaStream_t st) {
     int blocks = num_sms() * 3;
     uint64_t need = (n / 4 + 511) / 512;

@@ -22,6 +22,7 @@ cudaError_t launch_resolve(roix_scalars *sc, int dtype, double rel_eb, cudaStrea
 
 cudaError_t launch_quantize(const void *x, int dtype, uint64_t n, roix_scalars *sc, void *codes, cudaStream_t st);
 
+cudaError_t launch_hist_clear(uint64_t *hist, uint64_t nbins, cudaStream_t st);
 cudaError_t launch_hist_u16(const uint16_t *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st);
 cudaError_t launch_hist_f32(const float *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st);
 

@@ -15,7 +15,7 @@ import torch
 from . import _lib as L
 
 # kernels libroix launches per call (used for the bench's gpu_launches count)
-LAUNCHES = {"scalars_init": 1, "range": 1, "resolve": 1, "histogram": 1, "threshold": 1, "morph": 2,
+LAUNCHES = {"scalars_init": 2, "range": 1, "resolve": 1, "histogram": 1, "threshold": 1, "morph": 2,
             "label": 9, "extract": 4, "extract_runs": 5}
 
 
@@ -141,7 +141,7 @@ class Pipeline:
         mark(stage) is called after each stage is enqueued (the bench records CUDA events there)."""
         assert x.is_cuda and x.numel() == self.n and x.is_contiguous()
         if stream is not None and stream != torch.cuda.current_stream(self.device):
-            with torch.cuda.stream(stream):      # torch ops here (hist.zero_) go to the same stream
+            with torch.cuda.stream(stream):
                 return self.enqueue(x, None, mark)
         mark = mark or (lambda stage: None)
         st = ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
@@ -155,7 +155,7 @@ class Pipeline:
             L.roix_range(xp, n, sc, st)
             mark("range")
         L.roix_resolve(sc, self.cdtype, self.rel_eb, st)
-        self.hist.zero_()
+        L.roix_histogram_clear(_ptr(self.hist), self.hist.numel(), st)
         mark("setup")
         ws, wsb = _ptr(self.morph_ws), self.morph_ws.numel()
         if self.frames:

@@ -86,7 +86,7 @@ def slab_program(S, x, stream=None, mark=None):
         yield ("minmax", S.sc)                                    # X2
         mark("range")
     L.roix_resolve(sc, S.cdtype, S.rel_eb, st)
-    S.hist.zero_()
+    L.roix_histogram_clear(_ptr(S.hist), S.hist.numel(), st)
     mark("setup")
     mws, mwsb = _ptr(S.morph_ws), S.morph_ws.numel()
     frames = S.frames

@@ -32,5 +32,13 @@ def test_reference_arm_line():
 
 
 def test_reference_arm_other_ranks_silent():
-    assert _run(["--impl", "reference", "--config", "C1", "--steps", "1", "--warmup", "0"],
+    assert _run(["--impl", "reference", "--config", "C1", "--steps", "1", "--warmup", "0", "--gpus", "2"],
                 env={"RANK": "1", "WORLD_SIZE": "2"}) == []
+
+
+def test_gpus_must_match_world_size():
+    """--gpus N under a launcher with another WORLD_SIZE must fail loudly, not time another count."""
+    e = dict(os.environ, RANK="0", WORLD_SIZE="2")
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "C1", "--steps", "1",
+                        "--warmup", "0", "--gpus", "4"], cwd=ROOT, capture_output=True, text=True, timeout=600, env=e)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr

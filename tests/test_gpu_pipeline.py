@@ -65,6 +65,21 @@ def test_pipeline_vs_oracle(cfg):
     assert 0 < ref["count"] < p.n
 
 
+@pytest.mark.parametrize("cfg", [synth.CONFIGS["C2"], synth.scaled("C4", 0.25), synth.scaled("C5", 0.25)],
+                         ids=lambda c: c.name)
+def test_pipeline_union_block_16k_vs_oracle(cfg):
+    """run_capacity >= 2^23 selects k_union_local's 16 K-run union blocks -- the configuration of the
+    full-size C3/C4/C5 steps the bench times (Pipeline sizes run_capacity = max(2^22, n/256)) -- here
+    on volumes the oracle finishes in seconds, every artefact element by element."""
+    x = synth.generate(cfg)
+    p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se,
+                 min_size=cfg.min_size, polarity=cfg.polarity, run_capacity=1 << 23)
+    res = p.run(x)
+    assert p.run_capacity >= 1 << 23
+    assert res.n_runs > 2 * 16384          # several union blocks, so cross-block pairs occur
+    _check(cfg, p, x, res)
+
+
 def test_slab_generation_is_g_invariant():
     cfg = synth.scaled("C5", 0.0625)
     full = synth.generate(cfg)

@@ -404,12 +404,13 @@ LABEL_SHAPES = [(1, 1, 1), (1, 1, 70), (2, 3, 5), (4, 9, 33), (6, 17, 64), (10, 
                 (2, 5, 4500), (1, 3, 13900)]
 
 
-def _label_gpu(mask, conn, min_size, with_runs, inplace=True, labels=True):
+def _label_gpu(mask, conn, min_size, with_runs, inplace=True, labels=True, cap=None):
     Z, Y, X = mask.shape
     n = mask.size
     o = mask_to_words(mask.astype(np.uint8))
     g = L.Geom(Z, Y, X, 0, Z)
-    cap = max(1, Z * Y * ((X + 1) // 2))
+    if cap is None:
+        cap = max(1, Z * Y * ((X + 1) // 2))
     wsb = L.roix_label_workspace(g, cap)
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     cmin = torch.full((cap,), -7, dtype=torch.int64, device="cuda")
@@ -472,6 +473,30 @@ def test_label_keep_largest_vs_oracle(conn, shape):
         np.testing.assert_array_equal(ckp, kept)
         np.testing.assert_array_equal(words_to_mask(K, mask.size).reshape(shape), rK)
         assert s.n_kept == int(kept.sum())
+
+
+@pytest.mark.parametrize("conn", [6, 18, 26, 4, 8])
+@pytest.mark.parametrize("cap", [1 << 20, 1 << 23], ids=["ub4K", "ub16K"])
+def test_label_union_blocks_vs_oracle(conn, cap):
+    """Both union-block sizes of k_union_local (4 K runs below run_capacity 2^23, 16 K runs from 2^23:
+    the configuration the full-size C3/C4/C5 steps run in) against the oracle's BFS, on masks with
+    ~10^5-10^6 runs, so that many blocks and cross-block pairs occur (k_label.cu)."""
+    rng = np.random.default_rng(1000 + conn + (cap >> 20))
+    shape = (24, 160, 256)
+    for p in (0.3, 0.55):
+        mask = (rng.random(shape) < p).astype(np.uint8)
+        s, K, cmin, csz, ckp, lab = _label_gpu(mask, conn, 3, True, cap=cap)
+        assert s.err == 0 and s.n_runs > 4 * (16384 if cap >= 1 << 23 else 4096)
+        comp, rmin, rsz = oracle.label(mask, conn)
+        kept, rK = oracle.filter_components(comp, rsz, 3)
+        np.testing.assert_array_equal(cmin, rmin.astype(np.int64))
+        np.testing.assert_array_equal(csz, rsz.astype(np.int64))
+        np.testing.assert_array_equal(ckp, kept)
+        np.testing.assert_array_equal(words_to_mask(K, mask.size).reshape(shape), rK)
+        exp = np.full(mask.size, -1, np.int64)
+        fg = comp.ravel() != np.iinfo(np.uint32).max
+        exp[fg] = rmin[comp.ravel()[fg]].astype(np.int64)
+        np.testing.assert_array_equal(lab.cpu().numpy(), exp)
 
 
 def test_label_not_inplace_and_checkerboard():
