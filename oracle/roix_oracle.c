@@ -412,3 +412,363 @@ int64_t oracle_greedy_quantize(const uint16_t *D, uint64_t m, double E, uint32_t
     }
     return groups;
 }
+
+/* =============================================================================================
+ * STREAMING MODE -- the same definitions for volumes too large to hold: the
+ * full-size C3 / C4 / C5 configs (17-34 G voxels, 34-69 GB of uint16).  The caller feeds the volume
+ * plane by plane, in increasing z, once per pass; memory is O(plane) plus O(runs of o).
+ *
+ *   Pass A (os_hist):     oracle_hist_u16 over every plane -> h, then (caller) I_max, h8, Otsu.
+ *   Pass B (os_feed):     per plane, m = oracle_binarize_u16 (Eq. 2 on norm8); the
+ *                         opening by its definition (G-11, as oracle_open, written per plane with
+ *                         rings of 3 planes of m and e); every finished plane of o labelled by the
+ *                         classical two-pass raster scan (Rosenfeld & Pfaltz 1966): a foreground
+ *                         voxel takes the provisional label of its already-visited neighbours
+ *                         (left neighbour first) and the others are united with it; a voxel without
+ *                         one opens a new label.  Labels are numbered in raster order and union
+ *                         keeps the smaller, so every root is the label its component opened first,
+ *                         at the component's minimum linear index (G-14).  The labels of a plane are
+ *                         kept as x-runs (row, x0, x1, label): left-first labelling gives every
+ *                         voxel of an x-run the same label.
+ *   Resolve (os_resolve): roots, component sizes, the table in increasing minimum index, kept =
+ *                         size >= min_size (G-13).
+ *   Pass C (os_extract):  per plane, K (voxels of runs whose root is kept) and the stream of
+ *                         codes = rne_exact(x / s) (a1) in increasing linear index (a8, G-17).
+ * ------------------------------------------------------------------------------------------- */
+typedef struct {
+    uint32_t y, x0, x1, pad;
+    uint64_t label;
+} os_run;
+
+typedef struct {
+    int64_t Z, Y, X;
+    int conn, se, polarity;
+    uint32_t imax, t8;
+    int64_t fed;           /* pass B: planes fed so far */
+    uint8_t *m[3], *e[3];  /* rings: plane q lives in slot q % 3 */
+    uint8_t *o, *o_prev;   /* the plane of o being labelled, and the plane before it */
+    uint64_t *lab_prev, *lab_cur;
+    uint64_t *parent, *first, *size;  /* per provisional label */
+    uint64_t nlab, cap_lab;
+    os_run *runs;
+    uint64_t nruns, cap_runs;
+    uint64_t *plane_run0;  /* [Z + 1]: first run of every plane */
+    /* after os_resolve */
+    uint64_t *root_size;   /* per label: the component size, at roots */
+    uint64_t ncomp;
+    uint64_t min_size;
+    uint8_t *kept_root;    /* per label: kept flag, at roots */
+} os_state;
+
+void os_free(os_state *s)
+{
+    if (!s) return;
+    for (int k = 0; k < 3; k++) {
+        free(s->m[k]);
+        free(s->e[k]);
+    }
+    free(s->o);
+    free(s->o_prev);
+    free(s->lab_prev);
+    free(s->lab_cur);
+    free(s->parent);
+    free(s->first);
+    free(s->size);
+    free(s->runs);
+    free(s->plane_run0);
+    free(s->root_size);
+    free(s->kept_root);
+    free(s);
+}
+
+os_state *os_create(int64_t Z, int64_t Y, int64_t X, int conn, int se, int polarity, uint32_t imax, uint32_t t8)
+{
+    if (conn != 4 && conn != 6 && conn != 8 && conn != 18 && conn != 26) return NULL;
+    if (se != 6 && se != 4) return NULL;
+    os_state *s = (os_state *)calloc(1, sizeof(os_state));
+    if (!s) return NULL;
+    s->Z = Z;
+    s->Y = Y;
+    s->X = X;
+    s->conn = conn;
+    s->se = se;
+    s->polarity = polarity;
+    s->imax = imax;
+    s->t8 = t8;
+    size_t A = (size_t)(Y * X);
+    int ok = 1;
+    for (int k = 0; k < 3; k++) {
+        s->m[k] = (uint8_t *)malloc(A);
+        s->e[k] = (uint8_t *)malloc(A);
+        ok &= s->m[k] && s->e[k];
+    }
+    s->o = (uint8_t *)malloc(A);
+    s->o_prev = (uint8_t *)malloc(A);
+    s->lab_prev = (uint64_t *)malloc(A * sizeof(uint64_t));
+    s->lab_cur = (uint64_t *)malloc(A * sizeof(uint64_t));
+    s->plane_run0 = (uint64_t *)calloc((size_t)Z + 1, sizeof(uint64_t));
+    ok &= s->o && s->o_prev && s->lab_prev && s->lab_cur && s->plane_run0;
+    if (!ok) {
+        os_free(s);
+        return NULL;
+    }
+    return s;
+}
+
+/* m, e of plane q (ring slot q % 3); only called for planes inside the volume */
+static uint8_t os_m(const os_state *s, int64_t q, int64_t y, int64_t x) { return s->m[q % 3][y * s->X + x]; }
+static uint8_t os_e(const os_state *s, int64_t q, int64_t y, int64_t x) { return s->e[q % 3][y * s->X + x]; }
+
+/* erosion of plane q: e = m AND (AND of m over the SE neighbours inside the volume) -- oracle_open */
+static void os_erode(os_state *s, int64_t q)
+{
+    uint8_t *e = s->e[q % 3];
+    for (int64_t y = 0; y < s->Y; y++)
+        for (int64_t x = 0; x < s->X; x++) {
+            uint8_t v = os_m(s, q, y, x);
+            for (int k = 0; k < se_count(s->se); k++) {
+                const int *d = se_off(s->se, k);
+                int64_t zz = q + d[0], yy = y + d[1], xx = x + d[2];
+                if (zz < 0 || zz >= s->Z || yy < 0 || yy >= s->Y || xx < 0 || xx >= s->X) continue;
+                v &= os_m(s, zz, yy, xx);
+            }
+            e[y * s->X + x] = v;
+        }
+}
+
+/* dilation of plane q into s->o: o = e OR (OR of e over the SE neighbours inside the volume) */
+static void os_dilate(os_state *s, int64_t q)
+{
+    for (int64_t y = 0; y < s->Y; y++)
+        for (int64_t x = 0; x < s->X; x++) {
+            uint8_t v = os_e(s, q, y, x);
+            for (int k = 0; k < se_count(s->se); k++) {
+                const int *d = se_off(s->se, k);
+                int64_t zz = q + d[0], yy = y + d[1], xx = x + d[2];
+                if (zz < 0 || zz >= s->Z || yy < 0 || yy >= s->Y || xx < 0 || xx >= s->X) continue;
+                v |= os_e(s, zz, yy, xx);
+            }
+            s->o[y * s->X + x] = v;
+        }
+}
+
+static uint64_t os_find(os_state *s, uint64_t a)
+{
+    while (s->parent[a] != a) {
+        s->parent[a] = s->parent[s->parent[a]]; /* path halving */
+        a = s->parent[a];
+    }
+    return a;
+}
+
+static void os_union(os_state *s, uint64_t a, uint64_t b)
+{
+    a = os_find(s, a);
+    b = os_find(s, b);
+    if (a < b) s->parent[b] = a;
+    else if (b < a) s->parent[a] = b;
+}
+
+static int os_grow(void **p, uint64_t *cap, uint64_t need, size_t elem)
+{
+    if (need <= *cap) return 1;
+    uint64_t c = *cap ? *cap : 1024;
+    while (c < need) c *= 2;
+    void *q = realloc(*p, c * elem);
+    if (!q) return 0;
+    *p = q;
+    *cap = c;
+    return 1;
+}
+
+/* label plane q of o (s->o); lab_prev holds the labels of plane q-1 (valid where o(q-1) = 1) */
+static int os_label_plane(os_state *s, int64_t q)
+{
+    const int64_t Y = s->Y, X = s->X;
+    /* the already-visited half of the neighbourhood, left neighbour first */
+    int offs[13][3], noff = 0;
+    offs[noff][0] = 0;
+    offs[noff][1] = 0;
+    offs[noff][2] = -1;
+    noff++;
+    for (int dz = -1; dz <= 0; dz++)
+        for (int dy = -1; dy <= 1; dy++)
+            for (int dx = -1; dx <= 1; dx++) {
+                if (dz == 0 && dy >= 0) continue; /* (0, 0, -1) is first; (0, 0, >=0) and (0, 1, *) come later */
+                if (neighbour_ok(s->conn, dz, dy, dx)) {
+                    offs[noff][0] = dz;
+                    offs[noff][1] = dy;
+                    offs[noff][2] = dx;
+                    noff++;
+                }
+            }
+    if (!neighbour_ok(s->conn, 0, 0, -1)) return -1; /* every supported conn has the x-neighbour */
+    s->plane_run0[q] = s->nruns;
+    for (int64_t y = 0; y < Y; y++)
+        for (int64_t x = 0; x < X; x++) {
+            const int64_t a = y * X + x;
+            if (!s->o[a]) continue;
+            uint64_t L = UINT64_MAX;
+            for (int k = 0; k < noff; k++) {
+                int64_t zz = q + offs[k][0], yy = y + offs[k][1], xx = x + offs[k][2];
+                if (zz < 0 || yy < 0 || yy >= Y || xx < 0 || xx >= X) continue;
+                const int64_t b = yy * X + xx;
+                uint64_t l2;
+                if (zz == q) {
+                    if (!s->o[b]) continue;
+                    l2 = s->lab_cur[b];
+                } else {
+                    if (!s->o_prev[b]) continue;
+                    l2 = s->lab_prev[b];
+                }
+                if (L == UINT64_MAX) L = l2;
+                else os_union(s, L, l2);
+            }
+            if (L == UINT64_MAX) { /* a new provisional label */
+                if (s->nlab == s->cap_lab) {
+                    uint64_t c = s->cap_lab ? 2 * s->cap_lab : 1024, *a1, *a2, *a3;
+                    a1 = (uint64_t *)realloc(s->parent, c * sizeof(uint64_t));
+                    if (a1) s->parent = a1;
+                    a2 = (uint64_t *)realloc(s->first, c * sizeof(uint64_t));
+                    if (a2) s->first = a2;
+                    a3 = (uint64_t *)realloc(s->size, c * sizeof(uint64_t));
+                    if (a3) s->size = a3;
+                    if (!a1 || !a2 || !a3) return -1;
+                    s->cap_lab = c;
+                }
+                L = s->nlab++;
+                s->parent[L] = L;
+                s->first[L] = (uint64_t)((q * Y + y) * X + x);
+                s->size[L] = 0;
+            }
+            s->lab_cur[a] = L;
+            s->size[L] += 1;
+            /* x-runs of equal label (left-first labelling: one label per x-run) */
+            if (x > 0 && s->o[a - 1] && s->runs[s->nruns - 1].label == L && s->runs[s->nruns - 1].x1 == (uint32_t)x &&
+                s->runs[s->nruns - 1].y == (uint32_t)y) {
+                s->runs[s->nruns - 1].x1 = (uint32_t)x + 1;
+            } else {
+                if (!os_grow((void **)&s->runs, &s->cap_runs, s->nruns + 1, sizeof(os_run))) return -1;
+                os_run r = {(uint32_t)y, (uint32_t)x, (uint32_t)x + 1, 0, L};
+                s->runs[s->nruns++] = r;
+            }
+        }
+    s->plane_run0[q + 1] = s->nruns;
+    return 0;
+}
+
+/* after labelling plane q: it becomes the previous plane */
+static void os_shift_planes(os_state *s)
+{
+    uint8_t *t = s->o_prev;
+    s->o_prev = s->o;
+    s->o = t;
+    uint64_t *u = s->lab_prev;
+    s->lab_prev = s->lab_cur;
+    s->lab_cur = u;
+}
+
+/* o of plane q is ready in s->o: optionally copied out, then labelled */
+static int os_emit(os_state *s, int64_t q, uint8_t *o_out, int64_t *n_out)
+{
+    if (o_out) memcpy(o_out + (size_t)(*n_out) * (size_t)(s->Y * s->X), s->o, (size_t)(s->Y * s->X));
+    (*n_out)++;
+    if (os_label_plane(s, q)) return -1;
+    os_shift_planes(s);
+    return 0;
+}
+
+/* Pass B: feed plane p = s->fed (x: Y*X uint16).  Every plane of o finished by this call is
+ * written to o_out (room for 3 planes) and labelled; returns their number, -1 on failure.  With
+ * x == NULL the call ends the volume (after all Z planes) and finishes the remaining planes. */
+int64_t os_feed(os_state *s, const uint16_t *x, uint8_t *o_out)
+{
+    int64_t n_out = 0;
+    const int64_t A = s->Y * s->X;
+    if (x) {
+        const int64_t p = s->fed;
+        if (p >= s->Z) return -1;
+        oracle_binarize_u16(x, (uint64_t)A, s->imax, s->t8, s->polarity, s->m[p % 3]);
+        s->fed++;
+        if (s->se == 4) { /* in-plane SE: every plane is opened on its own */
+            os_erode(s, p);
+            os_dilate(s, p);
+            if (os_emit(s, p, o_out, &n_out)) return -1;
+            return n_out;
+        }
+        if (p >= 1) os_erode(s, p - 1);            /* needs m(p-2 .. p) */
+        if (p >= 2) {                               /* needs e(p-3 .. p-1) */
+            os_dilate(s, p - 2);
+            if (os_emit(s, p - 2, o_out, &n_out)) return -1;
+        }
+        return n_out;
+    }
+    if (s->fed != s->Z) return -1;
+    if (s->se == 4) return 0;
+    const int64_t Z = s->Z;
+    os_erode(s, Z - 1);                             /* m(Z) is outside the volume */
+    for (int64_t q = Z >= 2 ? Z - 2 : 0; q < Z; q++) {
+        os_dilate(s, q);
+        if (os_emit(s, q, o_out, &n_out)) return -1;
+    }
+    return n_out;
+}
+
+/* roots, sizes and the kept flags; returns the component count */
+int64_t os_resolve(os_state *s, uint64_t min_size)
+{
+    free(s->root_size);
+    free(s->kept_root);
+    s->root_size = (uint64_t *)calloc(s->nlab ? s->nlab : 1, sizeof(uint64_t));
+    s->kept_root = (uint8_t *)calloc(s->nlab ? s->nlab : 1, 1);
+    if (!s->root_size || !s->kept_root) return -1;
+    s->min_size = min_size;
+    for (uint64_t l = 0; l < s->nlab; l++) s->root_size[os_find(s, l)] += s->size[l];
+    int64_t nc = 0;
+    for (uint64_t l = 0; l < s->nlab; l++)
+        if (s->parent[l] == l) {
+            s->kept_root[l] = s->root_size[l] >= min_size;
+            nc++;
+        }
+    s->ncomp = (uint64_t)nc;
+    return nc;
+}
+
+/* the component table in increasing minimum index (= increasing root label) */
+int64_t os_table(os_state *s, uint64_t *cmin, uint64_t *csize, uint8_t *kept, uint64_t cap)
+{
+    int64_t c = 0;
+    for (uint64_t l = 0; l < s->nlab; l++)
+        if (s->parent[l] == l) {
+            if ((uint64_t)c >= cap) return -1;
+            cmin[c] = s->first[l];
+            csize[c] = s->root_size[l];
+            kept[c] = s->kept_root[l];
+            c++;
+        }
+    return c;
+}
+
+/* Pass C for plane q (x: Y*X uint16): K (one byte per voxel) and the codes of its kept voxels in
+ * increasing index; returns their number, -1 on a quantiser range error. */
+int64_t os_extract(os_state *s, int64_t q, const uint16_t *x, float eb, uint8_t *K, uint16_t *codes)
+{
+    double st, c;
+    if (step_of(eb, &st)) return -1;
+    memset(K, 0, (size_t)(s->Y * s->X));
+    int64_t j = 0;
+    for (uint64_t r = s->plane_run0[q]; r < s->plane_run0[q + 1]; r++) {
+        const os_run *R = &s->runs[r];
+        if (!s->kept_root[os_find(s, R->label)]) continue;
+        for (uint32_t xx = R->x0; xx < R->x1; xx++) {
+            const int64_t a = (int64_t)R->y * s->X + xx;
+            K[a] = 1;
+            if (rne_exact((double)x[a], st, &c) || c > 65535.0) return -1;
+            codes[j++] = (uint16_t)c;
+        }
+    }
+    return j;
+}
+
+uint64_t os_nruns(const os_state *s) { return s->nruns; }
+uint64_t os_nlabels(const os_state *s) { return s->nlab; }

@@ -149,6 +149,7 @@ roix_range = _wrap("roix_range")
 roix_resolve = _wrap("roix_resolve")
 roix_quantize = _wrap("roix_quantize")
 roix_histogram = _wrap("roix_histogram")
+roix_histogram_clear = _wrap("roix_histogram_clear")
 roix_threshold = _wrap("roix_threshold")
 roix_morph = _wrap("roix_morph")
 roix_binarize_planes = _wrap("roix_binarize_planes")

@@ -34,6 +34,10 @@ def test_exports_every_declared_symbol(lib):
     from paper_2602_15917_b200 import _lib as L
 
     assert set(names) == set(L.EXPORTED)
+    # every entry point has its Python binding of the same name (the helpers below are used raw)
+    raw = {"roix_status_string", "roix_last_error", "roix_version", "roix_scalars_size"}
+    missing = [n for n in names if n not in raw and not hasattr(L, n)]
+    assert not missing, missing
 
 
 def test_struct_layouts(lib):
