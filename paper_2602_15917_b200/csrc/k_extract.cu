@@ -8,6 +8,8 @@
 // walked back hundreds of tiles and serialised the CTAs; the extra N/8-byte read costs far less.)
 // x is loaded only for the 16-byte groups of voxels whose mask byte (u16) / nibble (fp32) is
 // non-zero, so DRAM reads x only under kept 32-byte sectors.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "scan.cuh"
@@ -387,10 +389,27 @@ __global__ void k_extract_total(const uint64_t *total, const ExWS w, roix_scalar
 
 using namespace roix;
 
-size_t extract_workspace_bytes(uint64_t n) { return ex_carve(nullptr, n, nullptr); }
+size_t compact_workspace_bytes(uint64_t n);
+cudaError_t launch_compact(const void *x, int dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
+                           void *codes, uint64_t capacity, const uint64_t *offset, void *ws, cudaStream_t st);
+
+size_t extract_workspace_bytes(uint64_t n) {
+    const size_t a = ex_carve(nullptr, n, nullptr), b = compact_workspace_bytes(n);
+    return a > b ? a : b;
+}
+
+static bool legacy_extract() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("ROIX_EXTRACT_LEGACY");
+        v = e && e[0] == '1';
+    }
+    return v;
+}
 
 cudaError_t launch_extract(const void *x, int dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
                            void *codes, uint64_t capacity, const uint64_t *offset, void *ws, cudaStream_t st) {
+    if (!legacy_extract()) return launch_compact(x, dtype, n, keep_bits, sc, codes, capacity, offset, ws, st);
     ExWS w;
     ex_carve(ws, n, &w);
     const uint64_t ntiles = (n + EX_TILE - 1) / EX_TILE;

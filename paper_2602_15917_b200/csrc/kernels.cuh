@@ -33,6 +33,9 @@ size_t morph_workspace_bytes(const roix_geom &g);
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
                          const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
                          int prebinarized, cudaStream_t st, const roix_frame *frames = nullptr);
+cudaError_t launch_morph2d(const void *x, int dtype, const roix_geom &g, roix_scalars *sc, uint32_t *o_bits,
+                           uint32_t *row_runs, uint2 *run_slots, uint32_t rs, const roix_frame *frames,
+                           cudaStream_t st);
 cudaError_t launch_spec(const uint64_t *shist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st);
 size_t fused_workspace_bytes(const roix_geom &g);
 cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom &g, int polarity, roix_scalars *sc,

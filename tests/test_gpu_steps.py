@@ -562,6 +562,63 @@ def test_extract_vs_oracle(n, dt):
     assert np.all(out2.cpu().numpy()[cap:] == -1)
 
 
+def _runs_mask(rng, n, mean_run, p_on):
+    """1-D masks made of x-runs: alternating off / on stretches of geometric lengths (mean_run), so
+    16-byte groups are mostly fully kept or empty, with run ends at every phase."""
+    out = np.zeros(n, np.uint8)
+    i, on = 0, rng.random() < p_on
+    while i < n:
+        L = int(rng.geometric(1.0 / mean_run))
+        if on:
+            out[i:i + L] = 1
+        i += L
+        on = not on if rng.random() < 0.9 else on
+    return out
+
+
+@pytest.mark.parametrize("dt", ["u16", "f32"])
+@pytest.mark.parametrize("n", [1, 37, 1024, 1031, 32768, 32768 + 1000, 100_003, 1 << 20, 3_000_017])
+def test_extract_runs_masks_vs_oracle(n, dt):
+    """roix_extract on run-structured masks (the shape of every phantom's K: long x-runs), at every
+    16-byte phase of the output (offset 0..7 / 0..3), for every quantiser mode (s = 1, 2^k, other
+    integers, non-integer), with capacity overflow: the vector stores (aligned groups, pairs of fully
+    kept groups) and the element path (run ends, chunk ends) against oracle.extract."""
+    rng = np.random.default_rng(n + (7 if dt == "f32" else 0))
+    ebs = [0.5, 2.0, 4.0, 1.5, 0.3] if dt == "u16" else [0.01]
+    for mean_run, p_on in [(300, 0.5), (40, 0.5), (5, 0.5), (2000, 0.8)]:
+        K = _runs_mask(rng, n, mean_run, p_on)
+        if dt == "u16":
+            x_np = rng.integers(0, 65536, n).astype(np.uint16)
+        else:
+            x_np = rng.normal(0, 3, n).astype(np.float32)
+        x = dev(x_np)
+        kw = mask_to_words(K)
+        wsb = L.roix_extract_workspace(n)
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        for eb in ebs:
+            ref = oracle.extract(x_np, K, eb)
+            for off in ([0, 1, 3, 5, 7] if dt == "u16" else [0, 1, 2, 3]):
+                for capacity in (off + ref.size, off + ref.size // 2 + 1):
+                    sc = new_sc(eb)
+                    L.roix_resolve(ptr(sc), dtype_code(x_np), 0.0, st())
+                    offd = torch.tensor([off], dtype=torch.int64, device="cuda")
+                    buf = torch.full((n + off + 16,), -1, dtype=torch.int16 if dt == "u16" else torch.int32,
+                                     device="cuda")
+                    L.roix_extract(ptr(x), dtype_code(x_np), n, ptr(kw), ptr(sc), ptr(buf), capacity, ptr(offd),
+                                   ptr(ws), wsb, st())
+                    s = read_sc(sc)
+                    got = buf.cpu().numpy()
+                    got = got.view(np.uint16) if dt == "u16" else got
+                    lim = min(ref.size, capacity - off)
+                    np.testing.assert_array_equal(got[off:off + lim], ref[:lim],
+                                                  err_msg="run %d eb %g off %d cap %d" % (mean_run, eb, off, capacity))
+                    assert np.all(buf.cpu().numpy()[:off] == -1) and np.all(buf.cpu().numpy()[capacity:] == -1)
+                    if off + ref.size > capacity:
+                        assert s.err & L.ERR_CAPACITY
+                    else:
+                        assert s.err == 0 and s.count == ref.size
+
+
 # ---------------------------------------------------------- a8 extract from the labelling's runs
 def _blobby(rng, shape, p, run):
     """Masks whose x-runs are mostly long (runs of `run` voxels merged at random phases)."""
