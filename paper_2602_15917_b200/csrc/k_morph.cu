@@ -823,7 +823,7 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     A.m_words = nwords;
     cudaError_t e;
     // in-plane SE: binarise + open in one pass over x (m stays on chip)
-    if (se == 4 && !prebinarized) return launch_morph2d(x, dtype, g, sc, o_bits, row_runs, nullptr, 0, frames, st);
+    if (se == 4 && !prebinarized && g.nx >= 32) return launch_morph2d(x, dtype, g, sc, o_bits, row_runs, nullptr, 0, frames, st);
     // a4: stream x -> m (after a fused speculative pass: resolve its window, binarise only on a miss)
     if (prebinarized && (e = launch_spec_resolve(x, dtype, g, sc, ws, st)) != cudaSuccess) return e;
     {
