@@ -296,11 +296,15 @@ roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const r
  *   1. roix_label_local on its slab (runs, union-find, sizes of the slab-local components);
  *   2. roix_label_boundary(side = 1) exports the runs of its last plane (to rank + 1);
  *   3. roix_label_link pairs its first-plane components with the previous rank's last-plane runs;
- *   4. roix_label_boundary_roots lists (label, size) of its components touching either slab face;
- *   5. all ranks gather every pair list and root table, and roix_merge (host, deterministic
- *      union-by-min) maps each boundary label to its merged label and total size;
+ *   4. roix_label_boundary_roots lists (label, size) of its components touching either slab face,
+ *      in increasing label order;
+ *   5. all ranks gather every pair list and root table, and roix_merge_device (or roix_merge on
+ *      the host) -- the same deterministic union-by-min on every rank -- maps each boundary label to
+ *      its merged label and total size;
  *   6. roix_label_finish applies the map: table entries live on the rank holding the component's
  *      minimum index; small-object removal uses the merged sizes.
+ * Every map argument below is device memory: map_label (ascending), map_final, map_total, and the map
+ * length *nmap (device uint64; nmap = NULL: an empty map).
  * Labels are global linear indices (uint64).  ws / run_capacity are those of roix_label_local.
  * Keep-largest on a sharded volume (NEXT-3): after roix_merge, roix_label_largest(phase 0) writes the
  * largest size among this slab's owned components to best[0] (device, 2 uint64; phase 0 first resets
@@ -331,17 +335,30 @@ roix_status roix_label_boundary_roots(const void *ws, const roix_geom *g, uint64
 roix_status roix_merge(const uint64_t *pairs, uint64_t npairs, const uint64_t *labels, const uint64_t *sizes,
                        uint64_t nlabels, uint64_t *out_label, uint64_t *out_final, uint64_t *out_total,
                        uint64_t *nout);
+/* The same merge on the device, enqueued on `stream` (every rank runs it on the same input, so the maps
+ * agree without a host round trip; the whole sharded step stays capturable).  gathered: G blocks of
+ * W = 2 + 2 pair_cap + 2 root_cap uint64 words in rank order, block r = rank r's
+ *   [npairs, nroots, pairs[2 pair_cap] (roix_label_link), labels[root_cap], sizes[root_cap]
+ *    (roix_label_boundary_roots)];
+ * blocks concatenate to an ascending label list (every rank's labels lie in its own slab).  Outputs:
+ * map_label / map_final / map_total (capacity G * root_cap) and *nmap (device).  A count above its
+ * capacity sets ROIX_ERR_CAPACITY, a pair naming a label missing from the tables ROIX_ERR_FORMAT.
+ * ws: roix_merge_workspace(G, root_cap) bytes, 16-byte aligned. */
+roix_status roix_merge_workspace(uint32_t G, uint64_t root_cap, size_t *ws_bytes);
+roix_status roix_merge_device(const uint64_t *gathered, uint32_t G, uint64_t pair_cap, uint64_t root_cap,
+                              uint64_t *map_label, uint64_t *map_final, uint64_t *map_total, uint64_t *nmap, void *ws,
+                              size_t ws_bytes, roix_scalars *sc, roix_stream_t stream);
 roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64_t min_size, uint64_t run_capacity,
                               void *ws, size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
-                              const uint64_t *map_total, uint64_t nmap, const roix_label_out *out, roix_scalars *sc,
+                              const uint64_t *map_total, const uint64_t *nmap, const roix_label_out *out, roix_scalars *sc,
                               roix_stream_t stream);
 
 roix_status roix_label_largest(void *ws, const roix_geom *g, uint64_t run_capacity, const uint64_t *map_label,
-                               const uint64_t *map_final, const uint64_t *map_total, uint64_t nmap, uint32_t phase,
+                               const uint64_t *map_final, const uint64_t *map_total, const uint64_t *nmap, uint32_t phase,
                                uint64_t *best, roix_scalars *sc, roix_stream_t stream);
 roix_status roix_label_finish_keep(const uint32_t *o_bits, const roix_geom *g, uint64_t run_capacity, void *ws,
                                    size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
-                                   const uint64_t *map_total, uint64_t nmap, const uint64_t *keep,
+                                   const uint64_t *map_total, const uint64_t *nmap, const uint64_t *keep,
                                    const roix_label_out *out, roix_scalars *sc, roix_stream_t stream);
 
 /*

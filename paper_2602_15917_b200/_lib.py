@@ -84,7 +84,9 @@ _SIGS = {
     "roix_label_link": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _vp]),
     "roix_label_boundary_roots": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, _vp, _u64, _vp, _vp, _vp]),
     "roix_merge": (_i32, [_vp, _u64, _vp, _vp, _u64, _vp, _vp, _vp, _vp]),
-    "roix_label_finish": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _u64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _u64,
+    "roix_merge_workspace": (_i32, [_u32, _u64, ctypes.POINTER(ctypes.c_size_t)]),
+    "roix_merge_device": (_i32, [_vp, _u32, _u64, _u64, _vp, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp]),
+    "roix_label_finish": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _u64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp,
                                  ctypes.POINTER(LabelOut), _vp, _vp]),
     "roix_extract_workspace": (_i32, [_u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_extract": (_i32, [_vp, _i32, _u64, _vp, _vp, _vp, _u64, _vp, _vp, ctypes.c_size_t, _vp]),
@@ -95,8 +97,8 @@ _SIGS = {
     "roix_greedy_quantize": (_i32, [_vp, _u64, _f64, _u32, _vp, _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "roix_extract_runs": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _u64, _vp,
                                  _vp]),
-    "roix_label_largest": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, _vp, _vp, _u64, _u32, _vp, _vp, _vp]),
-    "roix_label_finish_keep": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _u64, _vp,
+    "roix_label_largest": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, _vp, _vp, _vp, _u32, _vp, _vp, _vp]),
+    "roix_label_finish_keep": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp, _vp,
                                       ctypes.POINTER(LabelOut), _vp, _vp]),
     "roix_background": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _i32, _vp, _vp]),
     "roix_histogram_frames": (_i32, [_vp, ctypes.POINTER(Geom), _vp, _vp, _vp]),
@@ -177,6 +179,13 @@ roix_label_boundary = _wrap("roix_label_boundary")
 roix_label_link = _wrap("roix_label_link")
 roix_label_boundary_roots = _wrap("roix_label_boundary_roots")
 roix_label_finish = _wrap("roix_label_finish")
+roix_merge_device = _wrap("roix_merge_device")
+
+
+def roix_merge_workspace(G, root_cap):
+    out = ctypes.c_size_t()
+    _check(load().roix_merge_workspace(G, root_cap, ctypes.byref(out)), "roix_merge_workspace")
+    return out.value
 
 
 def roix_merge(pairs, labels, sizes):

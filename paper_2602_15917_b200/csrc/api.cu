@@ -312,7 +312,7 @@ roix_status roix_label_local(const uint32_t *o_bits, const uint32_t *row_runs, c
 
 roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64_t min_size, uint64_t run_capacity,
                               void *ws, size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
-                              const uint64_t *map_total, uint64_t nmap, const roix_label_out *out, roix_scalars *sc,
+                              const uint64_t *map_total, const uint64_t *nmap, const roix_label_out *out, roix_scalars *sc,
                               roix_stream_t stream) {
     if (!sc || !o_bits || !out) return invalid("sc / o_bits / out is NULL");
     if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
@@ -326,7 +326,7 @@ roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64
 }
 
 roix_status roix_label_largest(void *ws, const roix_geom *g, uint64_t run_capacity, const uint64_t *map_label,
-                               const uint64_t *map_final, const uint64_t *map_total, uint64_t nmap, uint32_t phase,
+                               const uint64_t *map_final, const uint64_t *map_total, const uint64_t *nmap, uint32_t phase,
                                uint64_t *best, roix_scalars *sc, roix_stream_t stream) {
     if (!sc || !best) return invalid("sc / best is NULL");
     if (phase > 1) return invalid("phase must be 0 or 1");
@@ -340,7 +340,7 @@ roix_status roix_label_largest(void *ws, const roix_geom *g, uint64_t run_capaci
 
 roix_status roix_label_finish_keep(const uint32_t *o_bits, const roix_geom *g, uint64_t run_capacity, void *ws,
                                    size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
-                                   const uint64_t *map_total, uint64_t nmap, const uint64_t *keep,
+                                   const uint64_t *map_total, const uint64_t *nmap, const uint64_t *keep,
                                    const roix_label_out *out, roix_scalars *sc, roix_stream_t stream) {
     if (!sc || !o_bits || !out || !keep) return invalid("sc / o_bits / out / keep is NULL");
     if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
@@ -350,6 +350,27 @@ roix_status roix_label_finish_keep(const uint32_t *o_bits, const roix_geom *g, u
     return cuda(launch_label_finish(o_bits, *g, 0, run_capacity, ws, map_label, map_final, map_total, nmap, *out, sc,
                                     (cudaStream_t)stream, keep),
                 "roix_label_finish_keep");
+}
+
+roix_status roix_merge_workspace(uint32_t G, uint64_t root_cap, size_t *ws_bytes) {
+    if (!ws_bytes) return invalid("ws_bytes is NULL");
+    if (G == 0 || (uint64_t)G * root_cap >= 0xffffffffull) return invalid("G * root_cap must be in [1, 2^32-1)");
+    *ws_bytes = merge_workspace_bytes(G, root_cap);
+    return ROIX_OK;
+}
+
+roix_status roix_merge_device(const uint64_t *gathered, uint32_t G, uint64_t pair_cap, uint64_t root_cap,
+                              uint64_t *map_label, uint64_t *map_final, uint64_t *map_total, uint64_t *nmap, void *ws,
+                              size_t ws_bytes, roix_scalars *sc, roix_stream_t stream) {
+    if (!gathered || !map_label || !map_final || !map_total || !nmap || !ws || !sc)
+        return invalid("gathered / map / nmap / ws / sc is NULL");
+    size_t need = 0;
+    roix_status s = roix_merge_workspace(G, root_cap, &need);
+    if (s != ROIX_OK) return s;
+    if (ws_bytes < need || !aligned16(ws)) return invalid("workspace (see roix_merge_workspace)");
+    return cuda(launch_merge(gathered, G, pair_cap, root_cap, map_label, map_final, map_total, nmap, ws, sc,
+                             (cudaStream_t)stream),
+                "roix_merge_device");
 }
 
 roix_status roix_label_boundary(const void *ws, const roix_geom *g, uint64_t run_capacity, int side, roix_brun *out,

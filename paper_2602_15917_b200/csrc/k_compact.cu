@@ -97,24 +97,6 @@ __global__ void __launch_bounds__(CK_THREADS) k_ck_count(const uint32_t *__restr
 }
 
 // ------------------------------------------------------------------------------------- pass 2
-// Halfword shift of the 16 halfwords S = (W[0..7]) by sh halfwords (0..8): returns S[sh .. sh+8) as
-// four words.  First by sh & 1 halfword (funnel shifts), then by sh >> 1 words (two select levels).
-__device__ __forceinline__ uint4 shift_hw(const uint32_t (&W)[8], uint32_t sh) {
-    const uint32_t f = (sh & 1u) * 16u;
-    uint32_t V[7];
-#pragma unroll
-    for (int i = 0; i < 7; i++) V[i] = __funnelshift_r(W[i], W[i + 1], f);
-    const uint32_t s = sh >> 1, b0 = s & 1u, b1 = s & 2u;
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const uint32_t t = b0 ? V[k + 1] : V[k];
-        const uint32_t u = b0 ? V[k + 3] : V[k + 2];
-        o[k] = b1 ? u : t;
-    }
-    return make_uint4(o[0], o[1], o[2], o[3]);
-}
-
 template <typename T>
 struct CkTraits;
 template <>
@@ -138,33 +120,68 @@ __device__ __forceinline__ uint4 quant16(uint4 d, const QP &q, uint32_t &err) {
     }
 }
 
+// code k (runtime, 0 <= k < VPG) of a 16-byte group of codes
 template <typename C>
-__device__ __forceinline__ uint32_t code_k(const uint4 &e, int k) {   // k static
+__device__ __forceinline__ uint32_t code_at(const uint4 &e, uint32_t k) {
     if constexpr (sizeof(C) == 2) {
-        const uint32_t wd = (k >> 1) == 0 ? e.x : (k >> 1) == 1 ? e.y : (k >> 1) == 2 ? e.z : e.w;
-        return (k & 1) ? (wd >> 16) : (wd & 0xffffu);
+        const uint32_t h = k >> 1;
+        const uint32_t lo = h & 1u ? e.y : e.x, hi = h & 1u ? e.w : e.z;
+        const uint32_t wd = h & 2u ? hi : lo;
+        return (wd >> ((k & 1u) * 16u)) & 0xffffu;
     } else {
-        return k == 0 ? e.x : k == 1 ? e.y : k == 2 ? e.z : e.w;
+        const uint32_t lo = k & 1u ? e.y : e.x, hi = k & 1u ? e.w : e.z;
+        return k & 2u ? hi : lo;
     }
 }
 
-template <typename T, typename C, int QM>
-__device__ __forceinline__ void ck_chunk(const T *__restrict__ x, uint64_t n, uint64_t c, uint32_t kw, uint64_t cbase,
-                                         uint32_t ccount, C *__restrict__ out, uint64_t capacity, const QP &q,
-                                         uint32_t &err) {
-    constexpr int VPG = CkTraits<T>::VPG, J = CkTraits<T>::J;
-    constexpr int GPW = 32 / VPG;                 // 16-byte groups per mask word
-    constexpr uint32_t GM = (1u << VPG) - 1u;     // a full group's mask
+// The aligned output vector holding the last d codes of a fully kept group a and the first VPG - d
+// codes of the next fully kept group b: elements [VPG - d, 2 VPG - d) of (a, b).
+template <int SH>   // shift in halfwords, 1..7
+__device__ __forceinline__ uint4 shift_c(const uint4 &a, const uint4 &b) {
+    const uint32_t W[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    constexpr int w0 = SH >> 1;
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) o[k] = (SH & 1) ? __funnelshift_r(W[w0 + k], W[w0 + k + 1], 16) : W[w0 + k];
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+template <typename C>
+__device__ __forceinline__ uint4 pair_vector(const uint4 &a, const uint4 &b, uint32_t d) {
+    if constexpr (sizeof(C) == 2) {
+        switch (d) {   // shift 8 - d halfwords
+        case 1: return shift_c<7>(a, b);
+        case 2: return shift_c<6>(a, b);
+        case 3: return shift_c<5>(a, b);
+        case 4: return shift_c<4>(a, b);
+        case 5: return shift_c<3>(a, b);
+        case 6: return shift_c<2>(a, b);
+        default: return shift_c<1>(a, b);
+        }
+    } else {
+        switch (d) {   // shift 4 - d words = 2 (4 - d) halfwords
+        case 1: return shift_c<6>(a, b);
+        case 2: return shift_c<4>(a, b);
+        default: return shift_c<2>(a, b);
+        }
+    }
+}
+
+template <typename T, int J>
+__device__ __forceinline__ void ck_masks(uint32_t kw, uint32_t (&mb)[J]) {
+    constexpr int VPG = CkTraits<T>::VPG, GPW = 32 / VPG;
     const uint32_t lane = lane_id();
-    const uint64_t v0 = c * CK_VOX;
-    if (cbase + ccount > capacity) err |= ROIX_ERR_CAPACITY;
-    // masks of the lane's groups (slot j = group 32 j + lane)
-    uint32_t mb[J];
 #pragma unroll
     for (int j = 0; j < J; j++)
-        mb[j] = (__shfl_sync(FULL, kw, j * (32 / GPW) + lane / GPW) >> ((lane % GPW) * VPG)) & GM;
-    // x only under kept groups
-    uint4 e[J];
+        mb[j] = (__shfl_sync(FULL, kw, j * (32 / GPW) + lane / GPW) >> ((lane % GPW) * VPG)) & ((1u << VPG) - 1u);
+}
+
+// x of the kept 16-byte groups of chunk c (zero elsewhere)
+template <typename T, int J>
+__device__ __forceinline__ void ck_load(const T *__restrict__ x, uint64_t n, uint64_t c, const uint32_t (&mb)[J],
+                                        uint4 (&e)[J]) {
+    constexpr int VPG = CkTraits<T>::VPG;
+    const uint32_t lane = lane_id();
+    const uint64_t v0 = c * CK_VOX;
     const bool whole = v0 + CK_VOX <= n;
 #pragma unroll
     for (int j = 0; j < J; j++) {
@@ -173,92 +190,101 @@ __device__ __forceinline__ void ck_chunk(const T *__restrict__ x, uint64_t n, ui
         if (mb[j]) {
             if (whole) e[j] = __ldcs(reinterpret_cast<const uint4 *>(x + gv));
             else {   // the volume's last chunk: no 16-byte load past n
-                T t[VPG];
+                uint32_t wd[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                for (int k = 0; k < VPG; k++) t[k] = gv + k < n ? x[gv + k] : (T)0;
-                e[j] = *reinterpret_cast<const uint4 *>(t);
-            }
-        }
-    }
-    // chunk-relative exclusive prefix of every group (order: slot-major, lane-minor), two slots
-    // per 32-bit word (16-bit fields: a chunk holds at most 1024 codes)
-    uint32_t pre[J];
-    {
-        uint32_t run = 0;
-#pragma unroll
-        for (int j = 0; j < J; j += 2) {
-            const uint32_t c0 = __popc(mb[j]), c1 = __popc(mb[j + 1]);
-            const uint32_t pk = c0 | (c1 << 16);
-            const uint32_t inc = warp_incl_scan(pk);
-            const uint32_t tot = __shfl_sync(FULL, inc, 31);
-            pre[j] = run + (inc & 0xffffu) - c0;
-            run += tot & 0xffffu;
-            pre[j + 1] = run + (inc >> 16) - c1;
-            run += tot >> 16;
-        }
-    }
-    // quantise (only kept groups carry data; the rest stay zero and are never stored)
-#pragma unroll
-    for (int j = 0; j < J; j++)
-        if (mb[j]) e[j] = quant16<T, QM>(e[j], q, err);
-    // neighbours in output order: next of (j, l) is (j, l+1), or (j+1, 0) for l = 31; prev likewise
-#pragma unroll
-    for (int j = 0; j < J; j++) {
-        if (__ballot_sync(FULL, mb[j]) == 0) continue;   // warp-uniform skip of an empty slot row
-        const uint32_t nsrc = (lane + 1) & 31u, psrc = (lane + 31) & 31u;
-        // value lane 0 offers to lane 31 is slot j+1's; value lane 31 offers to lane 0 is slot j-1's
-        const uint32_t mb_next_src = (lane == 0) ? (j + 1 < J ? mb[j + 1 < J ? j + 1 : j] : 0u) : mb[j];
-        const uint32_t mb_prev_src = (lane == 31) ? (j > 0 ? mb[j > 0 ? j - 1 : j] : 0u) : mb[j];
-        const uint32_t nmb = __shfl_sync(FULL, mb_next_src, nsrc);
-        const uint32_t pmb = __shfl_sync(FULL, mb_prev_src, psrc);
-        const uint4 ns = (lane == 0 && j + 1 < J) ? e[j + 1 < J ? j + 1 : j] : e[j];
-        uint4 ne;
-        ne.x = __shfl_sync(FULL, ns.x, nsrc);
-        ne.y = __shfl_sync(FULL, ns.y, nsrc);
-        ne.z = __shfl_sync(FULL, ns.z, nsrc);
-        ne.w = __shfl_sync(FULL, ns.w, nsrc);
-        // lane 31's next / lane 0's prev outside the chunk: treated as not fully kept
-        const uint32_t m = mb[j];
-        if (!m) continue;
-        const uint64_t P = cbase + pre[j];
-        // a fully kept neighbour in the chunk shares an aligned output vector with this group; it is
-        // stored as a vector when it lies below the capacity (both lanes evaluate the same test)
-        const uint64_t Ah = P - (P % VPG);   // the aligned vector holding P
-        const bool next_full = nmb == GM && !(lane == 31 && j + 1 >= J) && Ah + 2 * VPG <= capacity;
-        const bool prev_full = pmb == GM && !(lane == 0 && j == 0) && Ah + VPG <= capacity;
-        uint32_t em;   // codes stored element by element
-        if (m == GM) {
-            const uint32_t d = (uint32_t)(P % VPG);
-            if (d == 0) {
-                if (P + VPG <= capacity) __stcs(reinterpret_cast<uint4 *>(out + P), e[j]);
-                em = P + VPG <= capacity ? 0u : GM;
-            } else {
-                const uint32_t head = (1u << (VPG - d)) - 1u;   // codes in the aligned vector before P's
-                em = (prev_full ? 0u : head) | (next_full ? 0u : (GM & ~head));
-                if (next_full) {   // aligned vector: our last d codes, then the next group's first VPG - d
-                    const uint32_t W[8] = {e[j].x, e[j].y, e[j].z, e[j].w, ne.x, ne.y, ne.z, ne.w};
-                    const uint32_t sh = (VPG - d) * (16 / VPG);   // in halfwords: u16 8-d, fp32 2(4-d)
-                    __stcs(reinterpret_cast<uint4 *>(out + Ah + VPG), shift_hw(W, sh));
+                for (int k = 0; k < VPG; k++) {
+                    if (gv + k >= n) break;
+                    uint32_t b;
+                    if constexpr (sizeof(T) == 2) b = (uint32_t)x[gv + k] << (16 * (k & 1));
+                    else b = __float_as_uint(x[gv + k]);
+                    wd[sizeof(T) == 2 ? k >> 1 : k] |= b;
                 }
-            }
-        } else {
-            em = m;
-        }
-        if (em) {
-#pragma unroll
-            for (int k = 0; k < VPG; k++) {
-                if (!((em >> k) & 1u)) continue;
-                const uint64_t dst = P + __popc(m & ((1u << k) - 1u));
-                if (dst < capacity) out[dst] = (C)code_k<C>(e[j], k);
+                e[j] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
             }
         }
     }
 }
 
-template <typename T, typename C, int QM>
-__device__ __forceinline__ void ck_group(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
-                                         uint64_t nchunks, const CkWS &w, uint64_t g, uint64_t off0,
+template <typename T, typename C, int QM, int J>
+__device__ __forceinline__ void ck_chunk(const uint32_t (&mb)[J], uint4 (&e)[J], uint64_t cbase, uint32_t ccount,
                                          C *__restrict__ out, uint64_t capacity, const QP &q, uint32_t &err) {
+    constexpr int VPG = CkTraits<T>::VPG;
+    constexpr uint32_t GM = (1u << VPG) - 1u;     // a full group's mask
+    const uint32_t lane = lane_id();
+    if (cbase + ccount > capacity) err |= ROIX_ERR_CAPACITY;
+    // output positions relative to the aligned vector holding the chunk's first code
+    const uint32_t d0 = (uint32_t)(cbase % VPG);
+    const uint64_t ab = cbase - d0;
+    C *ob = out + ab;
+    const uint32_t caprel = capacity <= ab ? 0u : (uint32_t)min(capacity - ab, (uint64_t)0xffff0000u);
+    // chunk-relative exclusive prefix of every group (slot-major, lane-minor order), two slots per
+    // 32-bit word (16-bit fields: a chunk holds at most 1024 codes)
+    uint32_t pos[J];
+    {
+        uint32_t run = d0;
+#pragma unroll
+        for (int j = 0; j < J; j += 2) {
+            const uint32_t c0 = __popc(mb[j]), c1 = __popc(mb[j + 1]);
+            const uint32_t inc = warp_incl_scan(c0 | (c1 << 16));
+            const uint32_t tot = __shfl_sync(FULL, inc, 31);
+            pos[j] = run + (inc & 0xffffu) - c0;
+            run += tot & 0xffffu;
+            pos[j + 1] = run + (inc >> 16) - c1;
+            run += tot >> 16;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < J; j++)
+        if (mb[j]) e[j] = quant16<T, QM>(e[j], q, err);
+    uint32_t F[J];   // lanes whose group in slot j is fully kept
+#pragma unroll
+    for (int j = 0; j < J; j++) F[j] = __ballot_sync(FULL, mb[j] == GM);
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+        if (__ballot_sync(FULL, mb[j]) == 0) continue;   // warp-uniform skip of an empty slot row
+        const uint32_t m = mb[j];
+        const bool full = m == GM;
+        // neighbours in output order: next of (j, l) is (j, l+1), or (j+1, 0) for l = 31; the chunk's
+        // first and last group have none (their shared vectors go element by element)
+        const bool next_full = lane < 31 ? (F[j] >> (lane + 1)) & 1u : (j + 1 < J ? F[j + 1 < J ? j + 1 : j] & 1u : 0u);
+        const bool prev_full = lane > 0 ? (F[j] >> (lane - 1)) & 1u : (j > 0 ? F[j > 0 ? j - 1 : j] >> 31 : 0u);
+        const uint32_t p = pos[j], d = p % VPG, A = p - d;
+        const bool vec_own = full && d == 0 && A + VPG <= caprel;
+        const bool vec_next = full && d != 0 && next_full && A + 2 * VPG <= caprel;
+        const bool by_prev = full && d != 0 && prev_full && A + VPG <= caprel;   // prev wrote vector A
+        if (__ballot_sync(FULL, vec_next)) {
+            const uint32_t nsrc = (lane + 1) & 31u;
+            const uint4 ns = (lane == 0 && j + 1 < J) ? e[j + 1 < J ? j + 1 : j] : e[j];
+            uint4 ne;
+            ne.x = __shfl_sync(FULL, ns.x, nsrc);
+            ne.y = __shfl_sync(FULL, ns.y, nsrc);
+            ne.z = __shfl_sync(FULL, ns.z, nsrc);
+            ne.w = __shfl_sync(FULL, ns.w, nsrc);
+            if (vec_next) __stcs(reinterpret_cast<uint4 *>(ob + A + VPG), pair_vector<C>(e[j], ne, d));
+        }
+        if (vec_own) __stcs(reinterpret_cast<uint4 *>(ob + A), e[j]);
+        uint32_t em = m;   // codes stored element by element
+        if (full) {
+            const uint32_t head = (1u << (VPG - d)) - 1u;   // codes in vector A
+            em = vec_own ? 0u : d == 0 ? GM : ((by_prev ? 0u : head) | (vec_next ? 0u : GM & ~head));
+        }
+        while (em) {
+            const uint32_t k = __ffs(em) - 1;
+            em &= em - 1;
+            const uint32_t dst = p + __popc(m & ((1u << k) - 1u));
+            if (dst < caprel) ob[dst] = (C)code_at<C>(e[j], k);
+        }
+    }
+}
+
+// one warp task: chunks [part * cpp, (part + 1) * cpp) of group g, non-empty ones only; the next
+// chunk's x (u16: double-buffered) and the one after's K word are in flight while a chunk is processed
+template <typename T, typename C, int QM>
+__device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
+                                        uint64_t nchunks, const CkWS &w, uint64_t g, uint32_t part, uint32_t cpp,
+                                        uint64_t off0, C *__restrict__ out, uint64_t capacity, const QP &q,
+                                        uint32_t &err) {
+    constexpr int J = CkTraits<T>::J;
     const uint64_t gbase = w.goff[g];
     if (w.goff[g + 1] == gbase) return;   // no kept voxel in 32 K voxels (background)
     const uint32_t lane = lane_id();
@@ -266,44 +292,75 @@ __device__ __forceinline__ void ck_group(const T *__restrict__ x, uint64_t n, co
     const uint64_t c0 = g * CK_G;
     const uint32_t cc = c0 + lane < nchunks ? (uint32_t)w.ccnt[c0 + lane] : 0u;
     const uint32_t excl = warp_incl_scan(cc) - cc;
-    uint32_t rem = __ballot_sync(FULL, cc != 0);
+    const uint32_t pm = cpp >= 32 ? FULL : (((1u << cpp) - 1u) << (part * cpp));
+    uint32_t rem = __ballot_sync(FULL, cc != 0) & pm;
+    if (!rem) return;
     auto ldk = [&](int k) -> uint32_t {
+        if (k < 0) return 0u;
         const uint64_t wi = (c0 + k) * CK_WORDS + lane;
         return wi < nwords ? __ldcs(K + wi) : 0u;
     };
-    int k = __ffs(rem) - 1;
-    uint32_t kw = ldk(k);
+    auto nextk = [&](uint32_t &r) -> int {
+        const int k = r ? __ffs(r) - 1 : -1;
+        if (r) r &= r - 1;
+        return k;
+    };
+    int k = nextk(rem);
+    uint32_t mb[J];
+    uint4 e[J];
+    ck_masks<T, J>(ldk(k), mb);
+    ck_load<T, J>(x, n, c0 + k, mb, e);
+    int kn = nextk(rem);
+    uint32_t kwn = ldk(kn);
     while (k >= 0) {
-        rem &= rem - 1;
-        const int kn = rem ? __ffs(rem) - 1 : -1;
-        const uint32_t kw_next = kn >= 0 ? ldk(kn) : 0u;   // in flight while this chunk is processed
+        uint32_t mbn[J];
+        uint4 en[J];
+        if constexpr (sizeof(T) == 2) {   // issue the next chunk's x before processing this one
+            ck_masks<T, J>(kwn, mbn);
+            if (kn >= 0) ck_load<T, J>(x, n, c0 + kn, mbn, en);
+        }
+        const int knn = nextk(rem);
+        const uint32_t kwnn = ldk(knn);
         const uint64_t cbase = off0 + gbase + __shfl_sync(FULL, excl, k);
         const uint32_t ccount = __shfl_sync(FULL, cc, k);
-        ck_chunk<T, C, QM>(x, n, c0 + k, kw, cbase, ccount, out, capacity, q, err);
+        ck_chunk<T, C, QM, J>(mb, e, cbase, ccount, out, capacity, q, err);
+        if constexpr (sizeof(T) == 2) {
+#pragma unroll
+            for (int j = 0; j < J; j++) {
+                mb[j] = mbn[j];
+                e[j] = en[j];
+            }
+        } else {
+            ck_masks<T, J>(kwn, mb);
+            if (kn >= 0) ck_load<T, J>(x, n, c0 + kn, mb, e);
+        }
         k = kn;
-        kw = kw_next;
+        kn = knn;
+        kwn = kwnn;
     }
 }
 
 template <typename T, typename C>
-__global__ void __launch_bounds__(CK_THREADS, sizeof(T) == 2 ? 4 : 3)
+__global__ void __launch_bounds__(CK_THREADS, sizeof(T) == 2 ? 2 : 3)
     k_ck_extract(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K, uint64_t nchunks,
-                 uint64_t ngroups, CkWS w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
+                 uint64_t ngroups, uint32_t parts, CkWS w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
                  const uint64_t *offset) {
     if (*w.err_snap) return;
-    const uint64_t g = (uint64_t)blockIdx.x * (CK_THREADS / 32) + (threadIdx.x >> 5);
+    const uint64_t t = (uint64_t)blockIdx.x * (CK_THREADS / 32) + (threadIdx.x >> 5);
+    const uint64_t g = t / parts;
     if (g >= ngroups) return;
+    const uint32_t part = (uint32_t)(t % parts), cpp = CK_G / parts;
     const QP q = load_qp(sc);
     uint32_t err = 0;
     const uint64_t off0 = offset ? *offset : 0ull;
     if constexpr (sizeof(T) == 4) {
-        ck_group<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err);
+        ck_task<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err);
     } else {
         switch (qmode(q)) {   // uniform over the launch: one quantiser body per mode
-        case QM_POW2: ck_group<T, C, QM_POW2>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
-        case QM_INT: ck_group<T, C, QM_INT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
-        case QM_ONE: ck_group<T, C, QM_ONE>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
-        default: ck_group<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
+        case QM_POW2: ck_task<T, C, QM_POW2>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
+        case QM_INT: ck_task<T, C, QM_INT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
+        case QM_ONE: ck_task<T, C, QM_ONE>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
+        default: ck_task<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
         }
     }
     err = __reduce_or_sync(FULL, err);
@@ -332,15 +389,20 @@ cudaError_t launch_compact(const void *x, int dtype, uint64_t n, const uint32_t 
                                                                                   sc);
     cudaError_t e = scan_u32_u64(w.gcnt, w.goff, ngroups, w.scan_tmp, st);
     if (e != cudaSuccess) return e;
-    const unsigned g2 = (unsigned)((ngroups + wpc - 1) / wpc);
+    // warp tasks: a group, or a part of one when there are too few groups to fill the GPU
+    uint32_t parts = 1;
+    const uint64_t want = (uint64_t)num_sms() * 96;
+    while (parts < (uint32_t)CK_G && ngroups * parts < want) parts *= 2;
+    const uint64_t tasks = ngroups * parts;
+    const unsigned g2 = (unsigned)((tasks + wpc - 1) / wpc);
     if (g2) {
         if (dtype == ROIX_F32)
-            k_ck_extract<float, int32_t><<<g2, CK_THREADS, 0, st>>>((const float *)x, n, keep_bits, nchunks, ngroups, w,
-                                                                    sc, (int32_t *)codes, capacity, offset);
+            k_ck_extract<float, int32_t><<<g2, CK_THREADS, 0, st>>>((const float *)x, n, keep_bits, nchunks, ngroups,
+                                                                    parts, w, sc, (int32_t *)codes, capacity, offset);
         else
             k_ck_extract<uint16_t, uint16_t><<<g2, CK_THREADS, 0, st>>>((const uint16_t *)x, n, keep_bits, nchunks,
-                                                                        ngroups, w, sc, (uint16_t *)codes, capacity,
-                                                                        offset);
+                                                                        ngroups, parts, w, sc, (uint16_t *)codes,
+                                                                        capacity, offset);
     }
     k_ck_total<<<1, 1, 0, st>>>(scan_total_ptr(w.scan_tmp, ngroups), w.err_snap, sc);
     return cudaGetLastError();

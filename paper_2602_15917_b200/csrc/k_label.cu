@@ -591,7 +591,7 @@ __global__ void k_flatten_sizes(LabelWS W, roix_scalars *sc) {
 // single GPU.
 struct MapView {
     const uint64_t *label, *final_label, *total;
-    uint64_t n;
+    const uint64_t *n;   // device: map length (null: no map)
 };
 
 __device__ __forceinline__ uint64_t gidx(const LGeo &G, const LabelWS &W, uint32_t i) {
@@ -604,13 +604,14 @@ __device__ __forceinline__ void resolve_root(const LGeo &G, const LabelWS &W, co
     const uint64_t L = gidx(G, W, i);
     fin = L;
     tot = W.size[i];
-    uint64_t lo = 0, hi = M.n;
+    const uint64_t mn = M.n ? *M.n : 0;
+    uint64_t lo = 0, hi = mn;
     while (lo < hi) {
         const uint64_t mid = (lo + hi) >> 1;
         if (M.label[mid] < L) lo = mid + 1;
         else hi = mid;
     }
-    if (lo < M.n && M.label[lo] == L) {
+    if (lo < mn && M.label[lo] == L) {
         fin = M.final_label[lo];
         tot = M.total[lo];
     }
@@ -803,18 +804,29 @@ __global__ void k_mark_boundary(LGeo G, LabelWS W, roix_scalars *sc) {
             W.kept[W.parent[i]] = 2;   // scratch mark (kept[] is rewritten by the finish phase)
 }
 
-__global__ void k_boundary_roots(LGeo G, LabelWS W, uint64_t *labels, uint64_t *sizes, uint64_t cap, uint64_t *count,
-                                 roix_scalars *sc) {
+// boundary roots in increasing run index (= increasing label): flag, scan, write
+__device__ __forceinline__ bool broot(const LabelWS &W, uint64_t i) { return W.parent[i] == (uint32_t)i && W.kept[i] == 2; }
+
+__global__ void k_broot_flags(LabelWS W) {
+    const uint64_t n = W.ctr[0];   // the scan reads [0, n) only
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        W.cidx[i] = broot(W, i);
+}
+
+__global__ void k_boundary_roots(LGeo G, LabelWS W, const uint64_t *total, uint64_t *labels, uint64_t *sizes,
+                                 uint64_t cap, uint64_t *count, roix_scalars *sc) {
     if (get_err(sc)) return;
-    const uint64_t n = W.ctr[0];
+    const uint64_t n = W.ctr[0], m = *total;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *count = m;
+        if (m > cap) set_err(sc, ROIX_ERR_CAPACITY);
+    }
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        if (W.parent[i] != (uint32_t)i || W.kept[i] != 2) continue;
-        const unsigned long long at = atomicAdd((unsigned long long *)count, 1ull);
+        if (!broot(W, i)) continue;
+        const uint64_t at = W.cidx[i];
         if (at < cap) {
             labels[at] = gidx(G, W, (uint32_t)i);
             sizes[at] = W.size[i];
-        } else {
-            set_err(sc, ROIX_ERR_CAPACITY);
         }
     }
 }
@@ -903,7 +915,7 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
 
 // a7: resolve every local root through the merge map, component table, kept flags, K, labels
 cudaError_t launch_label_largest(const roix_geom &g, uint64_t cap, void *ws, const uint64_t *map_label,
-                                 const uint64_t *map_final, const uint64_t *map_total, uint64_t nmap, uint64_t *best,
+                                 const uint64_t *map_final, const uint64_t *map_total, const uint64_t *nmap, uint64_t *best,
                                  int phase, roix_scalars *sc, cudaStream_t st) {
     LabelWS W;
     carve(ws, g, cap, &W);
@@ -915,7 +927,7 @@ cudaError_t launch_label_largest(const roix_geom &g, uint64_t cap, void *ws, con
 
 cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint64_t min_size, uint64_t cap, void *ws,
                                 const uint64_t *map_label, const uint64_t *map_final, const uint64_t *map_total,
-                                uint64_t nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st,
+                                const uint64_t *nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st,
                                 const uint64_t *keep) {
     LabelWS W;
     carve(ws, g, cap, &W);
@@ -994,11 +1006,12 @@ cudaError_t launch_label_boundary_roots(const void *ws, const roix_geom &g, uint
     LabelWS W;
     carve((void *)ws, g, cap, &W);
     const LGeo G = make_geo(g);
-    cudaError_t e = cudaMemsetAsync(count, 0, 8, st);
-    if (e != cudaSuccess) return e;
     const int grid = num_sms() * 8;
     k_clear_marks<<<grid, 256, 0, st>>>(W);
     k_mark_boundary<<<grid, 256, 0, st>>>(G, W, sc);
-    k_boundary_roots<<<grid, 256, 0, st>>>(G, W, labels, sizes, out_cap, count, sc);
+    k_broot_flags<<<grid, 256, 0, st>>>(W);
+    cudaError_t e = scan_u32_dev(W.cidx, W.cidx, W.ctr, cap, W.scan_tmp, st);
+    if (e != cudaSuccess) return e;
+    k_boundary_roots<<<grid, 256, 0, st>>>(G, W, scan_total_ptr(W.scan_tmp, cap), labels, sizes, out_cap, count, sc);
     return cudaGetLastError();
 }

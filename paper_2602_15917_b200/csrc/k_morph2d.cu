@@ -95,16 +95,24 @@ __device__ __forceinline__ void bin_row(const T *__restrict__ xrow, uint64_t X, 
     // aligned words are written first to dst[-1 ..] when off > 0 (dst[-1] is the guard word)
     uint32_t *adst = off ? dst - 1 : dst;
     for (uint32_t c0 = 0; c0 < nblk; c0 += 32 * U) {
+        // all U loads are issued before any is used (U 16-byte loads in flight per lane)
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const uint32_t blk = c0 + 32 * u + lane;
+            const uint64_t p0 = (uint64_t)blk * VPL;
+            v[u] = (blk < nblk && p0 >= off && p0 + VPL <= span) ? __ldcs(ab + blk) : make_uint4(0, 0, 0, 0);
+        }
         uint32_t b[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const uint32_t blk = c0 + 32 * u + lane;
+            const uint64_t p0 = (uint64_t)blk * VPL;
             b[u] = 0;
             if (blk < nblk) {
-                const uint64_t p0 = (uint64_t)blk * VPL;
                 if (p0 >= off && p0 + VPL <= span) {
-                    b[u] = cmp.bits(__ldcs(ab + blk));
-                } else {
+                    b[u] = cmp.bits(v[u]);
+                } else {   // a row end's partial block: the row's own voxels only, pad bits 1
                     const T *e = reinterpret_cast<const T *>(ab + blk);
                     for (int k = 0; k < VPL; k++) {
                         const uint64_t p = p0 + k;

@@ -58,10 +58,10 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
                                uint64_t cap, void *ws, roix_scalars *sc, cudaStream_t st);
 cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint64_t min_size, uint64_t cap, void *ws,
                                 const uint64_t *map_label, const uint64_t *map_final, const uint64_t *map_total,
-                                uint64_t nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st,
+                                const uint64_t *nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st,
                                 const uint64_t *keep = nullptr);
 cudaError_t launch_label_largest(const roix_geom &g, uint64_t cap, void *ws, const uint64_t *map_label,
-                                 const uint64_t *map_final, const uint64_t *map_total, uint64_t nmap, uint64_t *best,
+                                 const uint64_t *map_final, const uint64_t *map_total, const uint64_t *nmap, uint64_t *best,
                                  int phase, roix_scalars *sc, cudaStream_t st);
 cudaError_t launch_label_boundary(const void *ws, const roix_geom &g, uint64_t cap, int side, roix_brun *out,
                                   uint64_t out_cap, uint64_t *count, roix_scalars *sc, cudaStream_t st);
@@ -103,3 +103,8 @@ cudaError_t launch_threshold_frames(const uint64_t *hist, uint64_t nframes, int 
                                     roix_scalars *sc, roix_frame *frames, cudaStream_t st);
 cudaError_t launch_background(const uint16_t *x, const uint16_t *B, const roix_geom &g, int op, uint16_t *out,
                               cudaStream_t st);
+
+size_t merge_workspace_bytes(uint32_t G, uint64_t root_cap);
+cudaError_t launch_merge(const uint64_t *gathered, uint32_t G, uint64_t pair_cap, uint64_t root_cap,
+                         uint64_t *map_label, uint64_t *map_final, uint64_t *map_total, uint64_t *nmap, void *ws,
+                         roix_scalars *sc, cudaStream_t st);

@@ -6,11 +6,16 @@ is one exchange step:
   X2  fp32 range       all-reduce MIN / MAX of the slab ranges           (relative eb, I_max)
   X1  histogram        all-reduce SUM of the slab histograms             (identical Otsu threshold)
   X3  morphology halo  each slab sends its first / last two binarised planes to its z-neighbours
-  X4  CCL merge        each slab sends its last plane's runs to the next slab, which links them with
-                       its first plane; all pair lists and boundary-component tables are gathered and
-                       every rank runs the same union-by-min (roix_merge), so merged labels and sizes
-                       agree everywhere; small-object removal then uses the merged sizes
+  X4  CCL merge        each slab sends its last plane's runs to the next slab (point to point), which
+                       links them with its first plane; every slab's pair list and boundary-component
+                       table are all-gathered and every rank runs the same device union-by-min
+                       (roix_merge_device), so merged labels and sizes agree everywhere; small-object
+                       removal then uses the merged sizes
   X5  stream offsets   all-gather of the slab counts (rank g's codes start at sum_{r<g} count_r)
+
+Every exchange moves device buffers of host-known (capacity) size, so no step reads anything back to
+the host: the whole sharded step is one enqueue sequence that a CUDA graph can capture.  A count that
+exceeds its capacity sets ROIX_ERR_CAPACITY; ``run`` then grows the capacities and runs again.
 
 The per-slab work is a generator (``slab_program``) that yields at each exchange; ``DistComm`` runs one
 slab per process over torch.distributed (NCCL on B200s, gloo on CPU), ``SimComm`` runs all slabs in one
@@ -48,16 +53,40 @@ class SlabState(Pipeline):
         dev = self.device
         self.halo_send = torch.zeros(2, 2 * self.plane_w + 4, dtype=torch.int32, device=dev)   # [lo, hi]
         self.halo_recv = torch.zeros(2, 2 * self.plane_w + 4, dtype=torch.int32, device=dev)
-        self.brun_cap = Y * ((X + 1) // 2) + 1
-        self.brun = torch.empty(self.brun_cap * 3, dtype=torch.int64, device=dev)   # roix_brun = 24 bytes
-        self.brun_prev = torch.empty_like(self.brun)
-        self.counts = torch.zeros(4, dtype=torch.int64, device=dev)   # [n_brun, n_prev, n_pairs, n_roots]
-        self.pair_cap = 4 * self.brun_cap
-        self.pairs = torch.empty(2 * self.pair_cap, dtype=torch.int64, device=dev)
-        self.root_cap = 2 * self.brun_cap
-        self.root_lab = torch.empty(self.root_cap, dtype=torch.int64, device=dev)
-        self.root_size = torch.empty(self.root_cap, dtype=torch.int64, device=dev)
+        self._alloc_exchange(min(Y * ((X + 1) // 2) + 1, 1 << 16))
         self.best = torch.zeros(2, dtype=torch.int64, device=dev)     # keep-largest: (size, label)
+        self.counts_all = torch.zeros(world, dtype=torch.int64, device=dev)   # X5
+
+    def _alloc_exchange(self, brun_cap):
+        """X4 buffers.  brun: [count, roix_brun x brun_cap] (24-byte runs); block: this rank's merge
+        input [npairs, nroots, pairs (2 pair_cap), labels (root_cap), sizes (root_cap)] (roix.h
+        roix_merge_device); gathered: every rank's block; the map and its device length."""
+        dev, G = self.device, self.world
+        self.brun_cap = int(brun_cap)
+        self.pair_cap = 2 * self.brun_cap
+        self.root_cap = self.brun_cap
+        self.brun = torch.zeros(1 + 3 * self.brun_cap, dtype=torch.int64, device=dev)
+        self.brun_prev = torch.zeros_like(self.brun)
+        W = 2 + 2 * self.pair_cap + 2 * self.root_cap
+        self.block = torch.zeros(W, dtype=torch.int64, device=dev)
+        self.gathered = torch.zeros(G * W, dtype=torch.int64, device=dev)
+        self.map = torch.zeros(3, G * self.root_cap, dtype=torch.int64, device=dev)
+        self.nmap = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.merge_ws = torch.empty(L.roix_merge_workspace(G, self.root_cap), dtype=torch.uint8, device=dev)
+
+    def block_views(self):
+        pc, rc = self.pair_cap, self.root_cap
+        b = self.block
+        return b[0:1], b[1:2], b[2:2 + 2 * pc], b[2 + 2 * pc:2 + 2 * pc + rc], b[2 + 2 * pc + rc:2 + 2 * pc + 2 * rc]
+
+    @property
+    def offset(self):
+        """Global stream offset of this slab's codes (host read of the X5 all-gather)."""
+        return int(self.counts_all[: self.rank].sum().item())
+
+    @property
+    def global_count(self):
+        return int(self.counts_all.sum().item())
 
     def _alloc_label(self, cap):
         super()._alloc_label(cap)
@@ -65,8 +94,6 @@ class SlabState(Pipeline):
             self.ws_bytes = L.roix_label_workspace(self.geom, cap)
             self.label_ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
 
-    def cptr(self, i):
-        return ctypes.c_void_p(self.counts.data_ptr() + 8 * i)
 
 
 def slab_program(S, x, stream=None, mark=None):
@@ -132,20 +159,18 @@ def slab_program(S, x, stream=None, mark=None):
     geo = ctypes.byref(S.geom)
     if S.conn in (6, 18, 26) and G > 1:
         ws, wsb, cap = _ptr(S.label_ws), S.ws_bytes, S.run_capacity
+        npairs, nroots, pairs, rlab, rsize = S.block_views()
         L.roix_label_local(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, cap, ws, wsb, sc, st)
-        L.roix_label_boundary(ws, geo, cap, 1, _ptr(S.brun), S.brun_cap, S.cptr(0), sc, st)
+        L.roix_label_boundary(ws, geo, cap, 1, _ptr(S.brun[1:]), S.brun_cap, _ptr(S.brun[0:1]), sc, st)
         yield ("shift", S)                                        # X4a: last-plane runs -> next slab
-        S.counts[2].zero_()
         if g > 0:
-            L.roix_label_link(ws, geo, cap, S.conn, _ptr(S.brun_prev), S.cptr(1), _ptr(S.pairs), S.pair_cap,
-                              S.cptr(2), sc, st)
-        L.roix_label_boundary_roots(ws, geo, cap, _ptr(S.root_lab), _ptr(S.root_size), S.root_cap, S.cptr(3),
-                                    sc, st)
-        gathered = yield ("gather_tables", S)                     # X4b: every slab's pairs and roots
-        pairs, labels, sizes = gathered
-        ml, mf, mt = L.roix_merge(pairs, labels, sizes)
-        S.map = torch.from_numpy(np.stack([ml, mf, mt]).view(np.int64)).to(S.device)
-        mp = (_ptr(S.map[0]), _ptr(S.map[1]), _ptr(S.map[2]), ml.size)
+            L.roix_label_link(ws, geo, cap, S.conn, _ptr(S.brun_prev[1:]), _ptr(S.brun_prev[0:1]), _ptr(pairs),
+                              S.pair_cap, _ptr(npairs), sc, st)
+        L.roix_label_boundary_roots(ws, geo, cap, _ptr(rlab), _ptr(rsize), S.root_cap, _ptr(nroots), sc, st)
+        yield ("gather_tables", S)                                # X4b: every slab's block
+        L.roix_merge_device(_ptr(S.gathered), G, S.pair_cap, S.root_cap, _ptr(S.map[0]), _ptr(S.map[1]),
+                            _ptr(S.map[2]), _ptr(S.nmap), _ptr(S.merge_ws), S.merge_ws.numel(), sc, st)
+        mp = (_ptr(S.map[0]), _ptr(S.map[1]), _ptr(S.map[2]), _ptr(S.nmap))
         if S.keep == "largest":
             # NEXT-3 keep-largest over the whole volume: the largest size, then the smallest label of
             # that size, each reduced over the ranks (X4c, X4d)
@@ -166,24 +191,13 @@ def slab_program(S, x, stream=None, mark=None):
     else:
         L.roix_extract(xp, S.cdtype, n, _ptr(S.o), sc, _ptr(S.codes), S.code_capacity, None, _ptr(S.ex_ws),
                        S.ex_ws.numel(), st)
-    counts = yield ("counts", S)                                  # X5
+    yield ("counts", S)                                           # X5 (device: S.counts_all)
     mark("extract")
-    S.offset = int(sum(counts[:g]))
-    S.global_count = int(sum(counts))
 
 
 def _count_of(S):
     off = L.Scalars.count.offset
     return S.sc[off:off + 8].view(torch.int64)
-
-
-def _read_tables(S):
-    if S.device.type == "cuda":
-        torch.cuda.synchronize(S.device)
-    c = S.counts.cpu().numpy()
-    npairs, nroots = int(min(c[2], S.pair_cap)), int(min(c[3], S.root_cap))
-    pairs = S.pairs[: 2 * npairs].cpu().numpy().view(np.uint64).reshape(-1, 2)
-    return pairs, S.root_lab[:nroots].cpu().numpy().view(np.uint64), S.root_size[:nroots].cpu().numpy().view(np.uint64)
 
 
 # ------------------------------------------------------------------------------------- comms
@@ -232,17 +246,17 @@ class SimComm:
         if kind == "shift":
             for g in range(1, G):
                 states[g].brun_prev.copy_(states[g - 1].brun)
-                states[g].counts[1].copy_(states[g - 1].counts[0])
             return [None] * G
         if kind == "gather_tables":
-            tabs = [_read_tables(S) for S in states]
-            pairs = np.concatenate([t[0] for t in tabs]).reshape(-1, 2)
-            labels = np.concatenate([t[1] for t in tabs])
-            sizes = np.concatenate([t[2] for t in tabs])
-            return [(pairs, labels, sizes)] * G
+            allb = torch.cat([S.block for S in states])
+            for S in states:
+                S.gathered.copy_(allb)
+            return [None] * G
         if kind == "counts":
-            c = [int(_count_of(S).item()) for S in states]
-            return [c] * G
+            c = torch.cat([_count_of(S) for S in states])
+            for S in states:
+                S.counts_all.copy_(c)
+            return [None] * G
         if kind in ("best_max", "best_min"):
             k = 0 if kind == "best_max" else 1
             vals = torch.stack([m[1][k] for m in msgs])
@@ -300,36 +314,20 @@ class DistComm:
                     r.wait()
             return None
         if kind == "shift":
-            # counts first, then only the used part of every slab's last-plane run list
-            allc = [torch.empty_like(S.counts[0:1]) for _ in range(self.world)]
-            d.all_gather(allc, S.counts[0:1].contiguous(), group=grp)
-            cnt = [int(c.item()) for c in allc]
-            m = max(1, min(max(cnt), S.brun_cap))
-            allb = [torch.empty(3 * m, dtype=torch.int64, device=S.device) for _ in range(self.world)]
-            d.all_gather(allb, S.brun[: 3 * m].contiguous(), group=grp)
-            if self.rank > 0:
-                S.brun_prev[: 3 * m].copy_(allb[self.rank - 1])
-                S.counts[1:2].copy_(allc[self.rank - 1])
+            # the packed last-plane runs (count + capacity) to the next rank, point to point
+            ops = []
+            g, G = self.rank, self.world
+            if g < G - 1:
+                ops.append(d.P2POp(d.isend, S.brun, g + 1, grp))
+            if g > 0:
+                ops.append(d.P2POp(d.irecv, S.brun_prev, g - 1, grp))
+            if ops:
+                for r in d.batch_isend_irecv(ops):
+                    r.wait()
             return None
         if kind == "gather_tables":
-            # tensor collectives (no pickling): the (pairs, roots) counts of every rank, then the used
-            # prefix of every rank's pair and root lists, padded to the largest
-            c = S.counts[2:4].clone()
-            allc = [torch.empty_like(c) for _ in range(self.world)]
-            d.all_gather(allc, c, group=grp)
-            cnt = [(int(min(t[0].item(), S.pair_cap)), int(min(t[1].item(), S.root_cap))) for t in allc]
-            mp = max(1, max(a for a, _ in cnt))
-            mr = max(1, max(b for _, b in cnt))
-            payload = torch.cat([S.pairs[: 2 * mp], S.root_lab[:mr], S.root_size[:mr]]).contiguous()
-            allp = [torch.empty_like(payload) for _ in range(self.world)]
-            d.all_gather(allp, payload, group=grp)
-            pairs, labels, sizes = [], [], []
-            for (np_, nr), t in zip(cnt, allp):
-                a = t.cpu().numpy().view(np.uint64)
-                pairs.append(a[: 2 * np_])
-                labels.append(a[2 * mp: 2 * mp + nr])
-                sizes.append(a[2 * mp + mr: 2 * mp + mr + nr])
-            return (np.concatenate(pairs).reshape(-1, 2), np.concatenate(labels), np.concatenate(sizes))
+            d.all_gather_into_tensor(S.gathered, S.block, group=grp)
+            return None
         if kind in ("best_max", "best_min"):
             k = 0 if kind == "best_max" else 1
             v = msg[1][k:k + 1].clone()
@@ -337,10 +335,8 @@ class DistComm:
             msg[1][k:k + 1].copy_(v)
             return None
         if kind == "counts":
-            c = _count_of(S).clone()
-            allc = [torch.empty_like(c) for _ in range(self.world)]
-            d.all_gather(allc, c, group=grp)
-            return [int(t.item()) for t in allc]
+            d.all_gather_into_tensor(S.counts_all, _count_of(S).clone(), group=grp)
+            return None
         raise ValueError(kind)
 
 
@@ -355,12 +351,25 @@ class ShardedPipeline:
         self.comm.run(self.S, x, mark=mark)
 
     def run(self, x):
-        self.enqueue(x)
-        torch.cuda.synchronize(self.S.device)
-        s = self.S.scalars()
-        if s.err:
-            raise L.RoixError("device error bits 0x%x" % s.err)
-        return self.S.collect(s)
+        """Enqueue, synchronise and collect.  A capacity error on any rank (the exchange buffers or the
+        labelling workspace) grows the capacities on every rank and runs again (ranks agree through a
+        MAX all-reduce of the error bits, so all of them retry or none does)."""
+        S, d = self.S, self.comm.dist
+        for attempt in range(6):
+            self.enqueue(x)
+            torch.cuda.synchronize(S.device)
+            s = S.scalars()
+            e = torch.tensor([int(s.err)], dtype=torch.int64, device=S.device)
+            d.all_reduce(e, op=d.ReduceOp.MAX, group=self.comm.group)
+            err = int(e.item())
+            if err & L.ERR_CAPACITY and s.count <= S.code_capacity and attempt < 5:
+                S._alloc_exchange(2 * S.brun_cap)
+                S._alloc_label(int(max(s.n_runs, 2 * S.run_capacity)))
+                continue
+            break
+        if err:
+            raise L.RoixError("device error bits 0x%x" % err)
+        return S.collect(s)
 
     def scalars(self):
         return self.S.scalars()
@@ -369,7 +378,9 @@ class ShardedPipeline:
         return int(self.S.scalars().count)
 
     def launches(self):
-        return self.S.launches() + 8
+        # the unsharded count, plus: halo binarisation (2 x 2 kernels), boundary runs (1), link (1),
+        # boundary roots (5), device merge (5), finish instead of label (-0)
+        return self.S.launches() + 14
 
 
 def run_simulated(x_full, G, *, shape=None, dtype=None, **kw):

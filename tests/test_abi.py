@@ -112,9 +112,17 @@ def test_host_validation_next_rows(lib):
     assert lib.roix_threshold_frames(P, 2, 0, 5, P, P, None) == L.ROIX_E_UNSUPPORTED
     # keep-largest on a sharded finish must go through roix_label_finish_keep
     out = L.LabelOut(16, None, None, None, 0, None)
-    assert lib.roix_label_finish(P, ctypes.byref(g), L.KEEP_LARGEST, 8, P, 1 << 20, None, None, None, 0,
+    assert lib.roix_label_finish(P, ctypes.byref(g), L.KEEP_LARGEST, 8, P, 1 << 20, None, None, None, None,
                                  ctypes.byref(out), P, None) == L.ROIX_E_INVALID
-    assert lib.roix_label_largest(P, ctypes.byref(g), 8, None, None, None, 0, 2, P, P, None) == L.ROIX_E_INVALID
+    assert lib.roix_label_largest(P, ctypes.byref(g), 8, None, None, None, None, 2, P, P, None) == L.ROIX_E_INVALID
+    # a merge map length pointer without the map arrays
+    assert lib.roix_label_finish(P, ctypes.byref(g), 4, 8, P, 1 << 20, None, None, None, P,
+                                 ctypes.byref(out), P, None) == L.ROIX_E_INVALID
+    # device merge: workspace query and validation (no launch)
+    assert lib.roix_merge_workspace(8, 1024, ctypes.byref(sz)) == L.ROIX_OK and sz.value >= 8 * 1024 * 12
+    assert lib.roix_merge_workspace(0, 1024, ctypes.byref(sz)) == L.ROIX_E_INVALID
+    assert lib.roix_merge_device(None, 2, 4, 4, P, P, P, P, P, 1 << 20, P, None) == L.ROIX_E_INVALID
+    assert lib.roix_merge_device(P, 2, 4, 4, P, P, P, P, P, 0, P, None) == L.ROIX_E_INVALID   # ws too small
     # background: bad op, misaligned pointers
     assert lib.roix_background(P, P, ctypes.byref(g), 7, P, None) == L.ROIX_E_INVALID
     assert lib.roix_background(ctypes.c_void_p(18), P, ctypes.byref(g), L.BG_SUB, P, None) == L.ROIX_E_INVALID

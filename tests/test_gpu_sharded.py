@@ -126,3 +126,62 @@ def test_bench_sharded_path_one_rank():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["config"]["parallelism"] == "zslab1" and d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+def test_merge_device_vs_host(G):
+    """roix_merge_device (X4 on the device, every rank the same input) equals the host union-by-min
+    roix_merge on random boundary tables: G blocks of ascending labels in disjoint ranges, random
+    pairs between labels of neighbouring ranks, including a chain across every block."""
+    import ctypes
+
+    from gpu_util import new_sc, ptr, read_sc, st
+    from paper_2602_15917_b200 import _lib as L
+
+    rng = np.random.default_rng(G)
+    pair_cap, root_cap = 64, 40
+    W = 2 + 2 * pair_cap + 2 * root_cap
+    blocks, all_pairs, all_lab, all_size = [], [], [], []
+    prev_labels = None
+    for r in range(G):
+        nr = int(rng.integers(1, root_cap + 1))
+        labels = np.sort(rng.choice(1 << 30, nr, replace=False)).astype(np.uint64) + np.uint64(r << 32)
+        sizes = rng.integers(1, 10 ** 6, nr).astype(np.uint64)
+        pairs = np.zeros((0, 2), np.uint64)
+        if prev_labels is not None:
+            k = int(rng.integers(1, pair_cap + 1))
+            pairs = np.stack([labels[rng.integers(0, nr, k)], prev_labels[rng.integers(0, prev_labels.size, k)]], 1)
+            pairs[0] = (labels[0], prev_labels[-1])          # a chain across all blocks
+        b = np.zeros(W, np.uint64)
+        b[0], b[1] = pairs.shape[0], nr
+        b[2:2 + 2 * pairs.shape[0]] = pairs.reshape(-1)
+        b[2 + 2 * pair_cap:2 + 2 * pair_cap + nr] = labels
+        b[2 + 2 * pair_cap + root_cap:2 + 2 * pair_cap + root_cap + nr] = sizes
+        blocks.append(b)
+        all_pairs.append(pairs)
+        all_lab.append(labels)
+        all_size.append(sizes)
+        prev_labels = labels
+    gathered = torch.from_numpy(np.concatenate(blocks).view(np.int64)).cuda()
+    M = G * root_cap
+    out = torch.full((3, M), -1, dtype=torch.int64, device="cuda")
+    nmap = torch.zeros(1, dtype=torch.int64, device="cuda")
+    ws = torch.empty(L.roix_merge_workspace(G, root_cap), dtype=torch.uint8, device="cuda")
+    sc = new_sc(1.0)
+    L.roix_merge_device(ptr(gathered), G, pair_cap, root_cap, ptr(out[0]), ptr(out[1]), ptr(out[2]), ptr(nmap),
+                        ptr(ws), ws.numel(), ptr(sc), st())
+    assert read_sc(sc).err == 0
+    ol, of, ot = L.roix_merge(np.concatenate(all_pairs), np.concatenate(all_lab), np.concatenate(all_size))
+    m = int(nmap.item())
+    assert m == ol.size
+    got = out[:, :m].cpu().numpy().view(np.uint64)
+    np.testing.assert_array_equal(got[0], ol)
+    np.testing.assert_array_equal(got[1], of)
+    np.testing.assert_array_equal(got[2], ot)
+    # a count beyond its capacity is an error, not a silent truncation
+    bad = gathered.clone()
+    bad[1] = root_cap + 1
+    sc2 = new_sc(1.0)
+    L.roix_merge_device(ptr(bad), G, pair_cap, root_cap, ptr(out[0]), ptr(out[1]), ptr(out[2]), ptr(nmap),
+                        ptr(ws), ws.numel(), ptr(sc2), st())
+    assert read_sc(sc2).err & L.ERR_CAPACITY

@@ -584,7 +584,7 @@ def test_extract_runs_masks_vs_oracle(n, dt):
     integers, non-integer), with capacity overflow: the vector stores (aligned groups, pairs of fully
     kept groups) and the element path (run ends, chunk ends) against oracle.extract."""
     rng = np.random.default_rng(n + (7 if dt == "f32" else 0))
-    ebs = [0.5, 2.0, 4.0, 1.5, 0.3] if dt == "u16" else [0.01]
+    ebs = [0.5, 2.0, 4.0, 1.5, 0.75] if dt == "u16" else [0.01]   # s = 1, 4, 8, 3, 1.5
     for mean_run, p_on in [(300, 0.5), (40, 0.5), (5, 0.5), (2000, 0.8)]:
         K = _runs_mask(rng, n, mean_run, p_on)
         if dt == "u16":

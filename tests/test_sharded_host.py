@@ -1,6 +1,7 @@
-"""CPU (no GPU): the host side of the sharded path -- the union-by-min merge of slab-boundary
-components (roix_merge, C++ in libroix) and the torch.distributed exchanges over gloo with
-world_size 2."""
+"""CPU (no GPU): the host side of the sharded path -- the host union-by-min merge of slab-boundary
+components (roix_merge, C++ in libroix; the device merge roix_merge_device is checked against it in
+tests/test_gpu_sharded.py) and the torch.distributed exchanges over gloo with world_size 2, on the
+device-layout buffers the GPU path exchanges (packed boundary runs, merge blocks, counts)."""
 import os
 import socket
 
@@ -70,21 +71,25 @@ def _free_port():
 
 
 class _FakeSlab:
-    """The fields DistComm touches, on the CPU."""
+    """The fields DistComm touches, on the CPU, in the layouts of SlabState."""
 
-    def __init__(self, rank):
+    def __init__(self, rank, world):
         from paper_2602_15917_b200 import _lib as L
 
         self.device = torch.device("cpu")
         self.sc = torch.zeros(L.scalars_size(), dtype=torch.uint8)
-        self.brun_cap = 16
-        self.brun = torch.arange(3 * self.brun_cap, dtype=torch.int64) + 1000 * rank
-        self.brun_prev = torch.zeros_like(self.brun)
-        self.counts = torch.tensor([3 + rank, 0, 2, 1], dtype=torch.int64)
-        self.pair_cap, self.root_cap = 8, 8
-        self.pairs = torch.tensor([10 * rank, 10 * rank + 1] * 8, dtype=torch.int64)
-        self.root_lab = torch.tensor([100 + rank] * 8, dtype=torch.int64)
-        self.root_size = torch.tensor([7] * 8, dtype=torch.int64)
+        self.brun_cap = 4
+        self.brun = torch.arange(1 + 3 * self.brun_cap, dtype=torch.int64) + 1000 * rank   # [count, runs]
+        self.brun[0] = 3 + rank
+        self.brun_prev = torch.full_like(self.brun, -1)
+        self.pair_cap, self.root_cap = 3, 2
+        W = 2 + 2 * self.pair_cap + 2 * self.root_cap
+        # block: [npairs, nroots, pairs (2 pair_cap), labels (root_cap), sizes (root_cap)]
+        self.block = torch.tensor([2, 1 + rank, 10 * rank, 10 * rank + 1, 10 * rank + 2, 10 * rank + 3, 0, 0,
+                                   100 + rank, 200 + rank, 7, 8], dtype=torch.int64)
+        assert self.block.numel() == W
+        self.gathered = torch.zeros(world * W, dtype=torch.int64)
+        self.counts_all = torch.zeros(world, dtype=torch.int64)
 
 
 def _worker(rank, world, port, q):
@@ -95,7 +100,7 @@ def _worker(rank, world, port, q):
         from paper_2602_15917_b200.sharded import DistComm
 
         comm = DistComm()
-        S = _FakeSlab(rank)
+        S = _FakeSlab(rank, world)
         out = {}
         # X1: histogram sum
         h = torch.arange(8, dtype=torch.int64) * (rank + 1)
@@ -112,22 +117,25 @@ def _worker(rank, world, port, q):
         recv = torch.full((2, 6), -1, dtype=torch.int32)
         comm._do(("halo", send, recv), S)
         out["halo"] = recv.tolist()
-        # X4a: last-plane runs shifted to the next rank
+        # X4a: the packed last-plane runs, point to point to the next rank
         comm._do(("shift", S), S)
-        out["shift"] = (S.brun_prev[:3 * 4].tolist(), int(S.counts[1]))
-        # X4b: every rank's tables
-        pairs, labels, sizes = comm._do(("gather_tables", S), S)
-        out["tables"] = (pairs.tolist(), labels.tolist(), sizes.tolist())
+        out["shift"] = S.brun_prev.tolist()
+        # X4b: every rank's merge block, in rank order
+        comm._do(("gather_tables", S), S)
+        out["gathered"] = S.gathered.tolist()
         # X5: counts
         off = L.Scalars.count.offset
         S.sc[off:off + 8].view(torch.int64).fill_(5 + rank)
-        out["counts"] = comm._do(("counts", S), S)
+        comm._do(("counts", S), S)
+        out["counts"] = S.counts_all.tolist()
         # X4c / X4d: keep-largest (size MAX, then label MIN; 2^63 - 1 = "no component of that size")
         best = torch.tensor([[40, 0], [55, 0]][rank], dtype=torch.int64)
         comm._do(("best_max", best), S)
         best[1] = [(1 << 63) - 1, 777][rank]
         comm._do(("best_min", best), S)
         out["best"] = best.tolist()
+        out["block"] = S.block.tolist()
+        out["brun"] = S.brun.tolist()
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -150,8 +158,8 @@ def test_distcomm_exchanges_gloo(L):
         assert o["minmax"] == [0x7FFFFFF0, 0xC0000001]
         assert o["counts"] == [5, 6]
         assert o["best"] == [55, 777]
-        assert o["tables"][1] == [100, 101] and o["tables"][2] == [7, 7]
-        assert o["tables"][0] == [[0, 1], [0, 1], [10, 11], [10, 11]]
+        assert o["gathered"] == res[0]["block"] + res[1]["block"]
     assert res[0]["halo"][1] == [1] * 6 and res[0]["halo"][0] == [-1] * 6   # rank 0 <- rank 1's first planes
     assert res[1]["halo"][0] == [10] * 6 and res[1]["halo"][1] == [-1] * 6  # rank 1 <- rank 0's last planes
-    assert res[1]["shift"] == (list(range(0, 12)), 3)
+    assert res[1]["shift"] == res[0]["brun"]                                  # rank 1 <- rank 0's runs
+    assert res[0]["shift"] == [-1] * 13                                       # rank 0 receives none
