@@ -101,3 +101,36 @@ def test_range_and_relative_eb(oracle_mod):
         oracle_mod.value_range(x)
     # G-6 example: range [0, 1], rel 1e-3 -> eb = fl32(1e-3)
     assert oracle_mod.resolve_eb(0.0, 1.0, 1e-3) == float(np.float32(1e-3))
+
+
+def _round_f32(fr):
+    """Correctly rounded binary32 (ties to even) of a positive rational, by exact comparison with the
+    neighbouring binary32 values."""
+    from fractions import Fraction
+
+    f = np.float32(float(fr))
+    cands = [np.nextafter(f, np.float32(-np.inf)), f, np.nextafter(f, np.float32(np.inf))]
+    dist = [abs(Fraction(float(c)) - fr) for c in cands]
+    best = min(dist)
+    ties = [c for c, d in zip(cands, dist) if d == best]
+    if len(ties) > 1:
+        ties = [c for c in ties if int(np.float32(c).view(np.uint32)) % 2 == 0]
+    return float(ties[0])
+
+
+@pytest.mark.parametrize("mn,mx", [(-0.24847662448883057, 1.5229978561401367),
+                                   (0.20228619873523712, 0.5688977837562561),
+                                   (0.03421112149953842, 1.8453582525253296)])
+def test_resolve_eb_is_fp64_then_fp32(oracle_mod, mn, mx):
+    """G-6: eb = fl32(rel * (fl64(max) - fl64(min))) with rel = 1e-3 as a binary64 value.  The expected
+    value is the exact rational product rounded once to binary32 (Fractions), on ranges where
+    evaluating the product in binary32 arithmetic gives a different eb -- so an fp32 implementation
+    (or a dropped term) fails here."""
+    from fractions import Fraction
+
+    mn32, mx32 = np.float32(mn), np.float32(mx)
+    exact = Fraction(1e-3) * (Fraction(float(mx32)) - Fraction(float(mn32)))
+    want = _round_f32(exact)
+    assert oracle_mod.resolve_eb(float(mn32), float(mx32), 1e-3) == want
+    naive = float(np.float32(np.float32(1e-3) * (mx32 - mn32)))
+    assert naive != want

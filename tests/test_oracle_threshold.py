@@ -175,3 +175,20 @@ def test_binarize_spec_examples(oracle_mod):
         assert m.tolist() == ex["mask"], ex["cite"]
         low = oracle_mod.binarize(np.array(ex["x"], np.uint16), 255, ex["t"], 1)
         assert low.tolist() == [1 - v for v in ex["mask"]]
+
+
+def test_binarize_f32_spec_examples_and_edges(oracle_mod):
+    """fp32 binarisation (Eq. 2 on Eq. 1's norm8 with round-half-up, G-30), pinned by hand:
+    with I_max = 255 norm8 is the identity on integers, so S:182-183 apply to fp32 input; a voxel
+    exactly on a norm8 edge (x = 10.5: 10.5 * 255 / 255 = 10.5 rounds up to 11) and one just below
+    it; I_max = 510 (x = 21 -> 21 * 255 / 510 = 10.5 -> 11); 'norm8 > t8' is strict (x = 10 with
+    t8 = 10 is out); LOW polarity is the complement."""
+    x = np.array([0.0, 10.0, 200.0], np.float32)
+    assert oracle_mod.binarize(x, 255.0, 10, 0).tolist() == [0, 0, 1]          # S:182
+    assert oracle_mod.binarize(x, 255.0, 255, 0).tolist() == [0, 0, 0]         # S:183
+    assert oracle_mod.binarize(x, 255.0, 10, 1).tolist() == [1, 1, 0]          # LOW: the complement
+    below = np.nextafter(np.float32(10.5), np.float32(0))
+    e = np.array([10.5, below, 11.0, 9.75], np.float32)
+    assert oracle_mod.binarize(e, 255.0, 10, 0).tolist() == [1, 0, 1, 0]
+    e2 = np.array([21.0, np.nextafter(np.float32(21.0), np.float32(0)), 20.0, 22.0], np.float32)
+    assert oracle_mod.binarize(e2, 510.0, 10, 0).tolist() == [1, 0, 0, 1]
