@@ -88,7 +88,7 @@ typedef struct roix_scalars {
     uint32_t spec_lo;     /* fused a2+a4: speculative raw-threshold window (u16 value / fp32 bits)  */
     uint32_t spec_hi;
     uint32_t spec_state;  /* 0 none, 1 window set, 2 mask resolved, 3 fallback binarisation       */
-    uint32_t reserved1;
+    uint32_t run_slots;   /* a5 -> a6: run records per row roix_morph_slots wrote (0: none)       */
     uint64_t n_uncertain; /* fused a2+a4: voxels inside the window (resolved after the threshold)  */
     float edges[256];     /* fp32 only: edges[k] = smallest finite x with norm8(x) >= k (k>=1)   */
 } roix_scalars;
@@ -230,6 +230,18 @@ roix_status roix_morph_workspace(const roix_geom *g, size_t *ws_bytes);
 roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
                        const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
                        void *ws, size_t ws_bytes, roix_stream_t stream);
+/*
+ * roix_morph plus run records: run_slots (nz*ny*slots_per_row pairs of uint32, 8-byte aligned;
+ * needs row_runs) receives, for every row of o, the first slots_per_row x-runs as (x0, x1) with x1
+ * exclusive; sc->run_slots is set to slots_per_row when they were written (0 when this form of the
+ * opening writes none).  roix_label_slots / roix_label_local_slots then take the runs of every row
+ * with at most slots_per_row runs from here instead of reading that row of o again (the opening had
+ * the row in registers anyway).  slots_per_row in 1..64.
+ */
+roix_status roix_morph_slots(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
+                             const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
+                             uint32_t *run_slots, uint32_t slots_per_row, void *ws, size_t ws_bytes,
+                             roix_stream_t stream);
 
 /*
  * a2+a4 fused by speculation (one read of x instead of two).  A 1/64 sample of x gives Otsu a window
@@ -288,6 +300,12 @@ roix_status roix_label_workspace(const roix_geom *g, uint64_t run_capacity, size
 roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
                        uint64_t min_size, uint64_t run_capacity, void *ws, size_t ws_bytes,
                        const roix_label_out *out, roix_scalars *sc, roix_stream_t stream);
+/* roix_label with the run records of roix_morph_slots (same row_runs / run_slots / slots_per_row;
+ * used only when sc->run_slots == slots_per_row, i.e. the preceding opening wrote them). */
+roix_status roix_label_slots(const uint32_t *o_bits, const uint32_t *row_runs, const uint32_t *run_slots,
+                             uint32_t slots_per_row, const roix_geom *g, uint32_t conn, uint64_t min_size,
+                             uint64_t run_capacity, void *ws, size_t ws_bytes, const roix_label_out *out,
+                             roix_scalars *sc, roix_stream_t stream);
 
 /*
  * Sharded labelling (z-slab decomposition over GPUs).  roix_label above equals
@@ -320,6 +338,9 @@ typedef struct roix_brun {
 roix_status roix_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
                              uint64_t run_capacity, void *ws, size_t ws_bytes, roix_scalars *sc,
                              roix_stream_t stream);
+roix_status roix_label_local_slots(const uint32_t *o_bits, const uint32_t *row_runs, const uint32_t *run_slots,
+                                   uint32_t slots_per_row, const roix_geom *g, uint32_t conn, uint64_t run_capacity,
+                                   void *ws, size_t ws_bytes, roix_scalars *sc, roix_stream_t stream);
 roix_status roix_label_boundary(const void *ws, const roix_geom *g, uint64_t run_capacity, int side, roix_brun *out,
                                 uint64_t out_cap, uint64_t *count, roix_scalars *sc, roix_stream_t stream);
 roix_status roix_label_link(const void *ws, const roix_geom *g, uint64_t run_capacity, uint32_t conn,

@@ -31,7 +31,7 @@ class Scalars(ctypes.Structure):
                 ("thr_u16", ctypes.c_uint32), ("thr_f32", ctypes.c_float), ("count", ctypes.c_uint64),
                 ("n_components", ctypes.c_uint64), ("n_kept", ctypes.c_uint64), ("n_runs", ctypes.c_uint64),
                 ("spec_lo", ctypes.c_uint32), ("spec_hi", ctypes.c_uint32), ("spec_state", ctypes.c_uint32),
-                ("reserved1", ctypes.c_uint32), ("n_uncertain", ctypes.c_uint64), ("edges", ctypes.c_float * 256)]
+                ("run_slots", ctypes.c_uint32), ("n_uncertain", ctypes.c_uint64), ("edges", ctypes.c_float * 256)]
 
 
 class Geom(ctypes.Structure):
@@ -79,6 +79,12 @@ _SIGS = {
     "roix_label_workspace": (_i32, [ctypes.POINTER(Geom), _u64, ctypes.POINTER(ctypes.c_size_t)]),
     "roix_label": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _u32, _u64, _u64, _vp, ctypes.c_size_t,
                           ctypes.POINTER(LabelOut), _vp, _vp]),
+    "roix_morph_slots": (_i32, [_vp, _i32, ctypes.POINTER(Geom), _u32, _vp, _vp, _vp, _vp, _vp, _vp, _u32, _vp,
+                                ctypes.c_size_t, _vp]),
+    "roix_label_slots": (_i32, [_vp, _vp, _vp, _u32, ctypes.POINTER(Geom), _u32, _u64, _u64, _vp, ctypes.c_size_t,
+                                ctypes.POINTER(LabelOut), _vp, _vp]),
+    "roix_label_local_slots": (_i32, [_vp, _vp, _vp, _u32, ctypes.POINTER(Geom), _u32, _u64, _vp, ctypes.c_size_t,
+                                      _vp, _vp]),
     "roix_label_local": (_i32, [_vp, _vp, ctypes.POINTER(Geom), _u32, _u64, _vp, ctypes.c_size_t, _vp, _vp]),
     "roix_label_boundary": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _i32, _vp, _u64, _vp, _vp, _vp]),
     "roix_label_link": (_i32, [_vp, ctypes.POINTER(Geom), _u64, _u32, _vp, _vp, _vp, _u64, _vp, _vp, _vp]),
@@ -175,6 +181,9 @@ roix_decode = _wrap("roix_decode")
 roix_decode_spans = _wrap("roix_decode_spans")
 roix_confusion = _wrap("roix_confusion")
 roix_label_local = _wrap("roix_label_local")
+roix_morph_slots = _wrap("roix_morph_slots")
+roix_label_slots = _wrap("roix_label_slots")
+roix_label_local_slots = _wrap("roix_label_local_slots")
 roix_label_boundary = _wrap("roix_label_boundary")
 roix_label_link = _wrap("roix_label_link")
 roix_label_boundary_roots = _wrap("roix_label_boundary_roots")

@@ -150,20 +150,30 @@ roix_status roix_morph_workspace(const roix_geom *g, size_t *ws_bytes) {
     return ROIX_OK;
 }
 
-roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
-                       const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
-                       size_t ws_bytes, roix_stream_t stream) {
+roix_status roix_morph_slots(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
+                             const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
+                             uint32_t *run_slots, uint32_t slots_per_row, void *ws, size_t ws_bytes,
+                             roix_stream_t stream) {
     if (!sc || !o_bits || !ws) return invalid("sc / o_bits / ws is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (!geom_ok(g)) return invalid("geometry");
     if (se != 6 && se != 4) return unsupported("se must be 6 (3-D cross) or 4 (in-plane cross)");
     if (!x || !aligned16(x) || !aligned16(o_bits)) return invalid("x / o_bits must be 16-byte aligned");
+    if (run_slots && (!row_runs || slots_per_row == 0 || slots_per_row > 64 || ((uintptr_t)run_slots & 7u)))
+        return invalid("run_slots needs row_runs, 1 <= slots_per_row <= 64 and 8-byte alignment");
     roix_status s = check_halos(g, se, halo_lo, halo_hi);
     if (s != ROIX_OK) return s;
     if (g->nx > (1u << 30)) return unsupported("rows longer than 2^30 voxels");
     if (ws_bytes < morph_workspace_bytes(*g) || !aligned16(ws)) return invalid("workspace (see roix_morph_workspace)");
-    return cuda(launch_morph(x, (int)dtype, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, ws, 0, (cudaStream_t)stream),
+    return cuda(launch_morph(x, (int)dtype, *g, se, halo_lo, halo_hi, sc, o_bits, row_runs, ws, 0, (cudaStream_t)stream,
+                             nullptr, (uint2 *)run_slots, run_slots ? slots_per_row : 0),
                 "roix_morph");
+}
+
+roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
+                       const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
+                       size_t ws_bytes, roix_stream_t stream) {
+    return roix_morph_slots(x, dtype, g, se, halo_lo, halo_hi, sc, o_bits, row_runs, nullptr, 0, ws, ws_bytes, stream);
 }
 
 roix_status roix_morph_frames(const uint16_t *x, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
@@ -268,12 +278,15 @@ roix_status roix_label_workspace(const roix_geom *g, uint64_t run_capacity, size
     return ROIX_OK;
 }
 
-roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
-                       uint64_t min_size, uint64_t run_capacity, void *ws, size_t ws_bytes,
-                       const roix_label_out *out, roix_scalars *sc, roix_stream_t stream) {
+roix_status roix_label_slots(const uint32_t *o_bits, const uint32_t *row_runs, const uint32_t *run_slots,
+                             uint32_t slots_per_row, const roix_geom *g, uint32_t conn, uint64_t min_size,
+                             uint64_t run_capacity, void *ws, size_t ws_bytes, const roix_label_out *out,
+                             roix_scalars *sc, roix_stream_t stream) {
     if (!sc || !o_bits || !out || !ws) return invalid("sc / o_bits / out / ws is NULL");
     if (!aligned16(o_bits) || (out->keep_bits && !aligned16(out->keep_bits)) || (row_runs && !aligned16(row_runs)))
         return invalid("o_bits / keep_bits / row_runs must be 16-byte aligned");
+    if (run_slots && (!row_runs || slots_per_row == 0 || slots_per_row > 64 || ((uintptr_t)run_slots & 7u)))
+        return invalid("run_slots needs row_runs, 1 <= slots_per_row <= 64 and 8-byte alignment");
     if (!geom_ok(g)) return invalid("geometry");
     if (conn != 4 && conn != 8 && conn != 6 && conn != 18 && conn != 26) return unsupported("conn (4, 8, 6, 18, 26)");
     size_t need = 0;
@@ -284,8 +297,16 @@ roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const r
     if (g->z0 != 0 || g->nz != g->gz) {
         if (conn != 4 && conn != 8) return unsupported("sharded 3-D labelling: use roix_label_local ... finish");
     }
-    return cuda(launch_label(o_bits, row_runs, *g, conn, min_size, run_capacity, ws, *out, sc, (cudaStream_t)stream),
+    return cuda(launch_label(o_bits, row_runs, *g, conn, min_size, run_capacity, ws, *out, sc, (cudaStream_t)stream,
+                             (const uint2 *)run_slots, run_slots ? slots_per_row : 0),
                 "roix_label");
+}
+
+roix_status roix_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
+                       uint64_t min_size, uint64_t run_capacity, void *ws, size_t ws_bytes,
+                       const roix_label_out *out, roix_scalars *sc, roix_stream_t stream) {
+    return roix_label_slots(o_bits, row_runs, nullptr, 0, g, conn, min_size, run_capacity, ws, ws_bytes, out, sc,
+                            stream);
 }
 
 static roix_status label_common(const roix_geom *g, uint64_t cap, const void *ws, size_t ws_bytes) {
@@ -297,17 +318,26 @@ static roix_status label_common(const roix_geom *g, uint64_t cap, const void *ws
     return ROIX_OK;
 }
 
-roix_status roix_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
-                             uint64_t run_capacity, void *ws, size_t ws_bytes, roix_scalars *sc,
-                             roix_stream_t stream) {
+roix_status roix_label_local_slots(const uint32_t *o_bits, const uint32_t *row_runs, const uint32_t *run_slots,
+                                   uint32_t slots_per_row, const roix_geom *g, uint32_t conn, uint64_t run_capacity,
+                                   void *ws, size_t ws_bytes, roix_scalars *sc, roix_stream_t stream) {
     if (!sc || !o_bits) return invalid("sc / o_bits is NULL");
     if (!aligned16(o_bits) || (row_runs && !aligned16(row_runs)))
         return invalid("o_bits / row_runs must be 16-byte aligned");
+    if (run_slots && (!row_runs || slots_per_row == 0 || slots_per_row > 64 || ((uintptr_t)run_slots & 7u)))
+        return invalid("run_slots needs row_runs, 1 <= slots_per_row <= 64 and 8-byte alignment");
     if (conn != 4 && conn != 8 && conn != 6 && conn != 18 && conn != 26) return unsupported("conn (4, 8, 6, 18, 26)");
     roix_status s = label_common(g, run_capacity, ws, ws_bytes);
     if (s != ROIX_OK) return s;
-    return cuda(launch_label_local(o_bits, row_runs, *g, conn, run_capacity, ws, sc, (cudaStream_t)stream),
+    return cuda(launch_label_local(o_bits, row_runs, *g, conn, run_capacity, ws, sc, (cudaStream_t)stream,
+                                   (const uint2 *)run_slots, run_slots ? slots_per_row : 0),
                 "roix_label_local");
+}
+
+roix_status roix_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom *g, uint32_t conn,
+                             uint64_t run_capacity, void *ws, size_t ws_bytes, roix_scalars *sc,
+                             roix_stream_t stream) {
+    return roix_label_local_slots(o_bits, row_runs, nullptr, 0, g, conn, run_capacity, ws, ws_bytes, sc, stream);
 }
 
 roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64_t min_size, uint64_t run_capacity,

@@ -31,6 +31,7 @@ constexpr int CK_VOX = 1024;            // voxels per chunk
 constexpr int CK_WORDS = CK_VOX / 32;   // mask words per chunk
 constexpr int CK_G = 32;                // chunks per group (one warp task)
 constexpr int CK_THREADS = 256;
+constexpr bool CK_DB = false;           // double-buffer x across chunks (measured: fewer resident warps lose)
 
 struct CkWS {
     uint16_t *ccnt;      // [nchunks]: kept voxels per chunk
@@ -315,7 +316,7 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
     while (k >= 0) {
         uint32_t mbn[J];
         uint4 en[J];
-        if constexpr (sizeof(T) == 2) {   // issue the next chunk's x before processing this one
+        if constexpr (sizeof(T) == 2 && CK_DB) {   // issue the next chunk's x before processing this one
             ck_masks<T, J>(kwn, mbn);
             if (kn >= 0) ck_load<T, J>(x, n, c0 + kn, mbn, en);
         }
@@ -324,7 +325,7 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
         const uint64_t cbase = off0 + gbase + __shfl_sync(FULL, excl, k);
         const uint32_t ccount = __shfl_sync(FULL, cc, k);
         ck_chunk<T, C, QM, J>(mb, e, cbase, ccount, out, capacity, q, err);
-        if constexpr (sizeof(T) == 2) {
+        if constexpr (sizeof(T) == 2 && CK_DB) {
 #pragma unroll
             for (int j = 0; j < J; j++) {
                 mb[j] = mbn[j];
@@ -341,7 +342,7 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
 }
 
 template <typename T, typename C>
-__global__ void __launch_bounds__(CK_THREADS, sizeof(T) == 2 ? 2 : 3)
+__global__ void __launch_bounds__(CK_THREADS, sizeof(T) == 2 ? 4 : 3)
     k_ck_extract(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K, uint64_t nchunks,
                  uint64_t ngroups, uint32_t parts, CkWS w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
                  const uint64_t *offset) {

@@ -177,9 +177,10 @@ __device__ __forceinline__ bool runs_total(const uint64_t *total, uint64_t cap, 
 
 __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict__ o, LGeo G, uint64_t nwords,
                                                       LabelWS W, const uint64_t *total, uint64_t cap,
-                                                      roix_scalars *sc) {
+                                                      roix_scalars *sc, uint32_t nslots) {
     if (get_err(sc)) return;
     if (!runs_total(total, cap, W, sc)) return;
+    const uint32_t skip = (nslots && sc->run_slots == nslots) ? nslots : 0u;   // rows with <= skip runs came from the slots
     const uint64_t rows = G.nz * G.ny;
     const uint64_t ngroups = (rows + RIF - 1) / RIF;
     const uint64_t wpg = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
 #pragma unroll
             for (int q = 0; q < RIF; q++) {
                 b0[q] = __shfl_sync(FULL, off, q);
-                live[q] = r0 + q < rows && __shfl_sync(FULL, off, q + 1) != b0[q];
+                live[q] = r0 + q < rows && __shfl_sync(FULL, off, q + 1) - b0[q] > skip;
                 carry[q] = sb[q] = eb[q] = 0;
             }
             for (uint32_t k0 = 0; k0 < G.W; k0 += 32) {
@@ -224,7 +225,7 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
 #pragma unroll
         for (int q = 0; q < RIF; q++) {
             const uint32_t a = __shfl_sync(FULL, off, q), b = __shfl_sync(FULL, off, q + 1);
-            const bool live = r0 + q < rows && b != a;
+            const bool live = r0 + q < rows && b - a > skip;
 #pragma unroll
             for (int h = 0; h < RW; h++) {
                 const uint32_t k = h * 32 + lane;
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
         for (int q = 0; q < RIF; q++) {
             const uint64_t r = r0 + q;
             const uint32_t b0 = __shfl_sync(FULL, off, q), b1 = __shfl_sync(FULL, off, q + 1);
-            if (r >= rows || b1 == b0) continue;
+            if (r >= rows || b1 - b0 <= skip) continue;
             uint32_t carry = 0, sbase = 0, ebase = 0;
 #pragma unroll
             for (int h = 0; h < RW; h++) {
@@ -247,6 +248,28 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
     }
 }
 
+// Rows with at most rs runs: their run records, written by roix_morph_slots with o (the opening
+// already had every row in registers), are copied to their scanned place -- those rows of o are not
+// read again.  A thread per row.
+__global__ void __launch_bounds__(256) k_runs_slots(LGeo G, LabelWS W, const uint2 *__restrict__ slots, uint32_t rs,
+                                                    const uint64_t *total, uint64_t cap, roix_scalars *sc) {
+    if (get_err(sc)) return;
+    if (!runs_total(total, cap, W, sc)) return;
+    if (sc->run_slots != rs) return;   // the opening did not write run records of this width
+    const uint64_t rows = G.nz * G.ny;
+    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = W.row_start[r], c = W.row_start[r + 1] - a;
+        if (c == 0 || c > rs) continue;
+        const uint2 *s = slots + r * rs;
+        for (uint32_t i = 0; i < c; i++) {
+            const uint2 v = s[i];
+            W.x0[a + i] = v.x;
+            W.x1[a + i] = v.y;
+            W.rrow[a + i] = (uint32_t)r;
+        }
+    }
+}
+
 // Whole-row form (X % 32 == 0, W = L KW words, L a power of two <= 32): a warp holds S = 32 / L row
 // segments, lane sl of a segment the KW consecutive words [KW sl, KW sl + KW) of a row; each segment
 // takes RR consecutive rows per iteration, all their loads issued before any row is processed.  Run
@@ -254,9 +277,11 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
 // lane's first start / end slot.
 template <int L, int KW, int RR>
 __global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__restrict__ o, LGeo G, LabelWS W,
-                                                           const uint64_t *total, uint64_t cap, roix_scalars *sc) {
+                                                           const uint64_t *total, uint64_t cap, roix_scalars *sc,
+                                                           uint32_t nslots) {
     if (get_err(sc)) return;
     if (!runs_total(total, cap, W, sc)) return;
+    const uint32_t skip = (nslots && sc->run_slots == nslots) ? nslots : 0u;   // rows with <= skip runs came from the slots
     constexpr int S = 32 / L;
     const uint32_t lane = lane_id(), sl = lane & (L - 1), seg = lane / L;
     const uint64_t rows = G.nz * G.ny;
@@ -284,7 +309,7 @@ __global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__res
 #pragma unroll
         for (int q = 0; q < RR; q++) {
             const uint32_t a = row_off(q), b = row_off(q + 1);
-            const bool live = r0 + q < rows && b != a;
+            const bool live = r0 + q < rows && b - a > skip;
             const uint32_t *src = o + (r0 + q) * (uint64_t)(L * KW) + KW * sl;
 #pragma unroll
             for (int i = 0; i < KW; i++) wv[q][i] = 0u;
@@ -863,7 +888,8 @@ static int conn_index(uint32_t conn) { return conn == 4 ? 0 : conn == 8 ? 1 : co
 
 // a6 on the slab: runs, union (block-local then cross-block), flatten, sizes
 cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
-                               uint64_t cap, void *ws, roix_scalars *sc, cudaStream_t st) {
+                               uint64_t cap, void *ws, roix_scalars *sc, cudaStream_t st, const uint2 *run_slots,
+                               uint32_t rs) {
     LabelWS W;
     carve(ws, g, cap, &W);
     const LGeo G = make_geo(g);
@@ -878,12 +904,14 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
     if ((e = scan_u32(rr, W.row_start, rows, W.scan_tmp, st)) != cudaSuccess) return e;
     const uint64_t *rtot = scan_total_ptr(W.scan_tmp, rows);
     const int runs_grid = num_sms() * 8;
+    if (!row_runs || !run_slots) rs = 0;   // run records exist only next to the opening's run counts
+    if (rs) k_runs_slots<<<ctas(rows, 256), 256, 0, st>>>(G, W, run_slots, rs, rtot, cap, sc);
     const uint32_t Wd = G.W;
     if (g.nx % 32 == 0 && ((Wd <= 32 && (Wd & (Wd - 1)) == 0) || Wd == 64 || Wd == 128)) {
         const uint32_t L = Wd < 32 ? Wd : 32;
         const int grid = ctas(rows * L / 4, 256);   // ~4 rows per warp iteration
 #define ROIX_RUNS_ROWS(LL, KK, RR) \
-    k_extract_runs_rows<LL, KK, RR><<<grid, 256, 0, st>>>(o_bits, G, W, rtot, cap, sc)
+    k_extract_runs_rows<LL, KK, RR><<<grid, 256, 0, st>>>(o_bits, G, W, rtot, cap, sc, rs)
         switch (Wd) {
         case 1: ROIX_RUNS_ROWS(1, 1, 4); break;
         case 2: ROIX_RUNS_ROWS(2, 1, 4); break;
@@ -896,7 +924,7 @@ cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs,
         }
 #undef ROIX_RUNS_ROWS
     } else {
-        k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, rtot, cap, sc);
+        k_extract_runs<<<ctas(rows * 32, 256), 256, 0, st>>>(o_bits, G, nwords, W, rtot, cap, sc, rs);
     }
     static std::atomic<unsigned long long> attr{0};
     if ((e = dyn_smem_once(k_union_local, UB_MAX * 4, attr)) != cudaSuccess) return e;
@@ -951,8 +979,8 @@ cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint
 
 cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
                          uint64_t min_size, uint64_t cap, void *ws, const roix_label_out &out, roix_scalars *sc,
-                         cudaStream_t st) {
-    cudaError_t e = launch_label_local(o_bits, row_runs, g, conn, cap, ws, sc, st);
+                         cudaStream_t st, const uint2 *run_slots, uint32_t rs) {
+    cudaError_t e = launch_label_local(o_bits, row_runs, g, conn, cap, ws, sc, st, run_slots, rs);
     if (e != cudaSuccess) return e;
     if (min_size == ROIX_KEEP_LARGEST) {   // both phases on this GPU; (size, label) in ctr[5], ctr[6]
         LabelWS W;

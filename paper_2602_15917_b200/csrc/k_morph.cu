@@ -30,6 +30,8 @@ struct MorphArgs {
     const uint32_t *halo_lo, *halo_hi;
     uint32_t *o;
     uint32_t *row_runs;
+    uint2 *run_slots;        // [rows * rs] or null: (x0, x1) of the first rs x-runs of every output row
+    uint32_t rs;
 };
 
 template <typename T>
@@ -389,8 +391,42 @@ __device__ __forceinline__ uint32_t seg_sum(uint32_t v) {
     }
 }
 
+// The first rs x-runs (x0, x1 exclusive) of a row held by a segment of L lanes x KW words (lane sl
+// holds words KW sl .. KW sl + KW - 1; pad bits 0): starts and ends from the neighbouring bits, their
+// ranks by a segment scan, written to slot[0 .. rs).
+template <int L, int KW>
+__device__ __forceinline__ void emit_slots(const uint32_t (&o)[KW], uint32_t sl, uint2 *slot, uint32_t rs, bool valid) {
+    uint32_t left = __shfl_up_sync(FULL, o[KW - 1], 1, L);
+    uint32_t right = __shfl_down_sync(FULL, o[0], 1, L);
+    if (sl == 0) left = 0u;
+    if (sl == L - 1) right = 0u;
+    uint32_t st[KW], en[KW], ns = 0, ne = 0;
+#pragma unroll
+    for (int i = 0; i < KW; i++) {
+        st[i] = o[i] & ~__funnelshift_l(i ? o[i - 1] : left, o[i], 1);
+        en[i] = o[i] & ~__funnelshift_r(o[i], i < KW - 1 ? o[i + 1] : right, 1);
+        ns += __popc(st[i]);
+        ne += __popc(en[i]);
+    }
+    uint32_t both = ns | (ne << 16);
+#pragma unroll
+    for (int d = 1; d < L; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, both, d, L);
+        if (sl >= (uint32_t)d) both += t;
+    }
+    uint32_t is = (both & 0xffffu) - ns, ie = (both >> 16) - ne;
+    if (!valid) return;
+#pragma unroll
+    for (int i = 0; i < KW; i++) {
+        const uint32_t xb = 32 * (KW * sl + i);
+        for (uint32_t m = st[i]; m && is < rs; m &= m - 1) slot[is++].x = xb + __ffs(m) - 1;
+        for (uint32_t m = en[i]; m && ie < rs; m &= m - 1) slot[ie++].y = xb + __ffs(m);
+    }
+}
+
 template <int L, int KW, int RY>
 __global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open3d_rows(MorphArgs A, roix_scalars *sc) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = A.rs;   // read by a6 after this launch
     if (get_err(sc)) return;
     constexpr int S = 32 / L, MR = RY + 4, ER = RY + 2;
     using WT = WordsT<KW>;
@@ -473,6 +509,7 @@ __global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open
                 WT::st(ob + j * (int)W, o);
                 if (sl == 0 && A.row_runs) A.row_runs[rbase + j] = cnt;
             }
+            if (A.rs) emit_slots<L, KW>(o, sl, A.run_slots + (rbase + j) * A.rs, A.rs, yb + j < Y);
         }
     };
 #pragma unroll
@@ -510,6 +547,7 @@ __global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open
 // lanes (__shfl), in y from the neighbouring register, in z from the previous/next plane registers.
 template <int RY>
 __global__ void __launch_bounds__(256, 3) k_open3d_reg(MorphArgs A, roix_scalars *sc) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = 0;   // no run records from this form
     if (get_err(sc)) return;
     constexpr int MRW = RY + 4, ERW = RY + 2;
     const uint32_t lane = lane_id();
@@ -659,6 +697,7 @@ __global__ void __launch_bounds__(256, 3) k_open3d_reg(MorphArgs A, roix_scalars
 // assembled from the o rows in shared memory into whole words.
 __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     extern __shared__ uint32_t smem[];
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = 0;   // no run records from this form
     if (get_err(sc)) return;
     const uint32_t W = A.W, WS = A.WS;
     constexpr int S = 8;                          // warps per CTA (launched with 256 threads)
@@ -803,7 +842,8 @@ size_t morph_workspace_bytes(const roix_geom &g) { return ((g.nz * g.ny * g.nx +
 
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
                          const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
-                         int prebinarized, cudaStream_t st, const roix_frame *frames) {
+                         int prebinarized, cudaStream_t st, const roix_frame *frames, uint2 *run_slots,
+                         uint32_t rs) {
     MorphArgs A = {};
     A.nz = g.nz;
     A.ny = g.ny;
@@ -816,6 +856,8 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     A.halo_hi = halo_hi;
     A.o = o_bits;
     A.row_runs = row_runs;
+    A.run_slots = row_runs ? run_slots : nullptr;
+    A.rs = A.run_slots ? rs : 0;
     const uint64_t n = g.nz * g.ny * g.nx;
     const uint64_t nwords = (n + 31) / 32;
     uint32_t *m = (uint32_t *)ws;
@@ -823,7 +865,8 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     A.m_words = nwords;
     cudaError_t e;
     // in-plane SE: binarise + open in one pass over x (m stays on chip)
-    if (se == 4 && !prebinarized && g.nx >= 32) return launch_morph2d(x, dtype, g, sc, o_bits, row_runs, nullptr, 0, frames, st);
+    if (se == 4 && !prebinarized && g.nx >= 32)
+        return launch_morph2d(x, dtype, g, sc, o_bits, row_runs, A.run_slots, A.rs, frames, st);
     // a4: stream x -> m (after a fused speculative pass: resolve its window, binarise only on a miss)
     if (prebinarized && (e = launch_spec_resolve(x, dtype, g, sc, ws, st)) != cudaSuccess) return e;
     {

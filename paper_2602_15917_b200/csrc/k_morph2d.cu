@@ -159,6 +159,7 @@ __device__ __forceinline__ void bin_row(const T *__restrict__ xrow, uint64_t X, 
 template <typename T>
 __global__ void __launch_bounds__(256, 2) k_morph2d(M2Args A, roix_scalars *sc) {
     extern __shared__ uint32_t smem[];
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = A.rs;   // read by a6 after this launch
     if (get_err(sc)) return;
     constexpr int S = M2_S;
     constexpr uint32_t MS = S + 4, ES = S + 2, OS = S + 1;

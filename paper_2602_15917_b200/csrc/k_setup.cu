@@ -30,7 +30,7 @@ __global__ void k_scalars_init(roix_scalars *sc, float eb) {
         sc->n_runs = 0;
         sc->spec_lo = sc->spec_hi = 0;
         sc->spec_state = 0;
-        sc->reserved1 = 0;
+        sc->run_slots = 0;
         sc->n_uncertain = 0;
     }
     for (int k = t; k < 256; k += blockDim.x) sc->edges[k] = 0.0f;

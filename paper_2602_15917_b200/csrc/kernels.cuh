@@ -32,7 +32,8 @@ cudaError_t launch_threshold(const uint64_t *hist, int dtype, int polarity, roix
 size_t morph_workspace_bytes(const roix_geom &g);
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
                          const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
-                         int prebinarized, cudaStream_t st, const roix_frame *frames = nullptr);
+                         int prebinarized, cudaStream_t st, const roix_frame *frames = nullptr,
+                         uint2 *run_slots = nullptr, uint32_t rs = 0);
 cudaError_t launch_morph2d(const void *x, int dtype, const roix_geom &g, roix_scalars *sc, uint32_t *o_bits,
                            uint32_t *row_runs, uint2 *run_slots, uint32_t rs, const roix_frame *frames,
                            cudaStream_t st);
@@ -48,14 +49,15 @@ cudaError_t launch_binarize_planes(const void *x, int dtype, const roix_geom &g,
 size_t label_workspace_bytes(const roix_geom &g, uint64_t cap);
 cudaError_t launch_label(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
                          uint64_t min_size, uint64_t cap, void *ws, const roix_label_out &out, roix_scalars *sc,
-                         cudaStream_t st);
+                         cudaStream_t st, const uint2 *run_slots = nullptr, uint32_t rs = 0);
 
 size_t extract_workspace_bytes(uint64_t n);
 cudaError_t launch_extract(const void *x, int dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
                            void *codes, uint64_t capacity, const uint64_t *offset, void *ws, cudaStream_t st);
 
 cudaError_t launch_label_local(const uint32_t *o_bits, const uint32_t *row_runs, const roix_geom &g, uint32_t conn,
-                               uint64_t cap, void *ws, roix_scalars *sc, cudaStream_t st);
+                               uint64_t cap, void *ws, roix_scalars *sc, cudaStream_t st, const uint2 *run_slots = nullptr,
+                               uint32_t rs = 0);
 cudaError_t launch_label_finish(const uint32_t *o_bits, const roix_geom &g, uint64_t min_size, uint64_t cap, void *ws,
                                 const uint64_t *map_label, const uint64_t *map_final, const uint64_t *map_total,
                                 const uint64_t *nmap, const roix_label_out &out, roix_scalars *sc, cudaStream_t st,

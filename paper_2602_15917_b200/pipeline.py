@@ -95,6 +95,10 @@ class Pipeline:
         self.frame_thr = torch.zeros(4 * max(Z, 1), dtype=torch.int32, device=dev) if frames else None   # roix_frame
         self.o = torch.empty(self.nwords + 4, dtype=torch.int32, device=dev)   # o, then K in place
         self.row_runs = torch.empty(Z * Y, dtype=torch.int32, device=dev)
+        # run records of every row (x0, x1) written by the opening for rows of <= RS runs, so a6 does
+        # not re-read those rows of o (roix_morph_slots / roix_label_slots)
+        self.rs = 8 if X >= 64 else 0
+        self.run_slots = torch.empty(max(1, Z * Y * self.rs * 2), dtype=torch.int32, device=dev) if self.rs else None
         # fused (speculative) histogram + binarisation: one read of x for a2 + a4 (roix_histogram_binarize);
         # off by default: on B200 the histogram pass is bound by shared-memory atomics, and the fused pass
         # (3x slower than the plain histogram at C4) loses to histogram + streaming binarisation
@@ -177,9 +181,12 @@ class Pipeline:
         mark("histogram")
         L.roix_threshold_multi(_ptr(self.hist), self.nbins, self.cdtype, self.polarity, self.classes, sc, st)
         mark("threshold")
-        morph = L.roix_morph_prebinarized if self.fused else L.roix_morph
-        morph(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o), _ptr(self.row_runs),
-              ws, wsb, st)
+        if self.fused:
+            L.roix_morph_prebinarized(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o),
+                                      _ptr(self.row_runs), ws, wsb, st)
+        else:
+            L.roix_morph_slots(xp, self.cdtype, ctypes.byref(self.geom), self.se, None, None, sc, _ptr(self.o),
+                               _ptr(self.row_runs), _ptr(self.run_slots), self.rs, ws, wsb, st)
         mark("morph")
         self._label_extract(xp, sc, st, mark)
 
@@ -188,8 +195,9 @@ class Pipeline:
         out = L.LabelOut(self.o.data_ptr(), self.comp_min.data_ptr(), self.comp_size.data_ptr(),
                          self.comp_kept.data_ptr(), self.comp_cap,
                          self.labels.data_ptr() if self.labels is not None else None)
-        L.roix_label(_ptr(self.o), _ptr(self.row_runs), ctypes.byref(self.geom), self.conn, self.label_min_size,
-                     self.run_capacity, _ptr(self.label_ws), self.ws_bytes, ctypes.byref(out), sc, st)
+        L.roix_label_slots(_ptr(self.o), _ptr(self.row_runs), _ptr(self.run_slots), self.rs, ctypes.byref(self.geom),
+                           self.conn, self.label_min_size, self.run_capacity, _ptr(self.label_ws), self.ws_bytes,
+                           ctypes.byref(out), sc, st)
         mark("label")
         if self.extract == "runs":
             # a1+a8 from the kept runs of a6/a7 (reads exactly the kept voxels of x; K is not re-read)

@@ -150,9 +150,12 @@ def slab_program(S, x, stream=None, mark=None):
         L.roix_morph_frames(xp, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, _ptr(S.frame_thr), sc, _ptr(S.o),
                             _ptr(S.row_runs), mws, mwsb, st)
     else:
-        morph = L.roix_morph_prebinarized if S.fused else L.roix_morph
-        morph(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o), _ptr(S.row_runs), mws, mwsb,
-              st)
+        if S.fused:
+            L.roix_morph_prebinarized(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o),
+                                      _ptr(S.row_runs), mws, mwsb, st)
+        else:
+            L.roix_morph_slots(xp, S.cdtype, ctypes.byref(S.geom), S.se, halo_lo, halo_hi, sc, _ptr(S.o),
+                               _ptr(S.row_runs), _ptr(S.run_slots), S.rs, mws, mwsb, st)
     mark("morph")
     out = L.LabelOut(S.o.data_ptr(), S.comp_min.data_ptr(), S.comp_size.data_ptr(), S.comp_kept.data_ptr(),
                      S.comp_cap, S.labels.data_ptr() if S.labels is not None else None)
@@ -160,7 +163,8 @@ def slab_program(S, x, stream=None, mark=None):
     if S.conn in (6, 18, 26) and G > 1:
         ws, wsb, cap = _ptr(S.label_ws), S.ws_bytes, S.run_capacity
         npairs, nroots, pairs, rlab, rsize = S.block_views()
-        L.roix_label_local(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, cap, ws, wsb, sc, st)
+        L.roix_label_local_slots(_ptr(S.o), _ptr(S.row_runs), _ptr(S.run_slots), S.rs, geo, S.conn, cap, ws, wsb, sc,
+                                 st)
         L.roix_label_boundary(ws, geo, cap, 1, _ptr(S.brun[1:]), S.brun_cap, _ptr(S.brun[0:1]), sc, st)
         yield ("shift", S)                                        # X4a: last-plane runs -> next slab
         if g > 0:
@@ -182,8 +186,8 @@ def slab_program(S, x, stream=None, mark=None):
         else:
             L.roix_label_finish(_ptr(S.o), geo, S.min_size, cap, ws, wsb, *mp, ctypes.byref(out), sc, st)
     else:
-        L.roix_label(_ptr(S.o), _ptr(S.row_runs), geo, S.conn, S.label_min_size, S.run_capacity, _ptr(S.label_ws),
-                     S.ws_bytes, ctypes.byref(out), sc, st)
+        L.roix_label_slots(_ptr(S.o), _ptr(S.row_runs), _ptr(S.run_slots), S.rs, geo, S.conn, S.label_min_size,
+                           S.run_capacity, _ptr(S.label_ws), S.ws_bytes, ctypes.byref(out), sc, st)
     mark("label")
     if S.extract == "runs":
         L.roix_extract_runs(xp, S.cdtype, geo, S.run_capacity, _ptr(S.label_ws), S.ws_bytes, sc, _ptr(S.codes),

@@ -80,6 +80,29 @@ def test_pipeline_union_block_16k_vs_oracle(cfg):
     _check(cfg, p, x, res)
 
 
+@pytest.mark.parametrize("shape,conn,se", [((6, 40, 64), 6, 6), ((5, 33, 256), 26, 6), ((4, 50, 100), 8, 4),
+                                           ((3, 64, 2048), 18, 6), ((2, 30, 1000), 4, 4)])
+def test_pipeline_run_slots_vs_oracle(shape, conn, se):
+    """The opening's run records (roix_morph_slots, 8 per row) feed a6 for rows with <= 8 runs; rows
+    with more are re-read from o.  Two-level volumes with random masks of several densities give rows
+    of every run count on both sides of 8, in one volume; every artefact against the oracle."""
+    from paper_2602_15917_b200.pipeline import Pipeline as P
+
+    rng = np.random.default_rng(sum(shape) + conn)
+    for p in (0.55, 0.7, 0.85):
+        m = rng.random(shape) < p
+        m[:, : shape[1] // 3] &= rng.random((shape[0], shape[1] // 3, shape[2])) < 0.97   # blobby rows too
+        xv = np.where(m, 3000, 100).astype(np.uint16)
+        xv[0, 0, 0], xv[-1, -1, -1] = 3000, 100
+        x = torch.from_numpy(xv.view(np.int16)).cuda()
+        cfg = synth.Config("rand", shape, "u16", eb=2.0, conn=conn, se=se, min_size=3)
+        pl = P(shape, "u16", eb=2.0, conn=conn, se=se, min_size=3)
+        assert pl.rs == 8
+        res = pl.run(x)
+        assert res.scalars.run_slots == 8
+        _check(cfg, pl, x, res)
+
+
 def test_slab_generation_is_g_invariant():
     cfg = synth.scaled("C5", 0.0625)
     full = synth.generate(cfg)
