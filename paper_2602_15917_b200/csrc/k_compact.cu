@@ -146,25 +146,24 @@ __device__ __forceinline__ uint4 shift_c(const uint4 &a, const uint4 &b) {
     for (int k = 0; k < 4; k++) o[k] = (SH & 1) ? __funnelshift_r(W[w0 + k], W[w0 + k + 1], 16) : W[w0 + k];
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
+// branch-free (lanes of a warp may hold different d): a halfword funnel step, then two word selects
 template <typename C>
 __device__ __forceinline__ uint4 pair_vector(const uint4 &a, const uint4 &b, uint32_t d) {
-    if constexpr (sizeof(C) == 2) {
-        switch (d) {   // shift 8 - d halfwords
-        case 1: return shift_c<7>(a, b);
-        case 2: return shift_c<6>(a, b);
-        case 3: return shift_c<5>(a, b);
-        case 4: return shift_c<4>(a, b);
-        case 5: return shift_c<3>(a, b);
-        case 6: return shift_c<2>(a, b);
-        default: return shift_c<1>(a, b);
-        }
-    } else {
-        switch (d) {   // shift 4 - d words = 2 (4 - d) halfwords
-        case 1: return shift_c<6>(a, b);
-        case 2: return shift_c<4>(a, b);
-        default: return shift_c<2>(a, b);
-        }
+    const uint32_t sh = sizeof(C) == 2 ? 8u - d : 2u * (4u - d);   // shift in halfwords
+    const uint32_t W[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint32_t f = (sh & 1u) * 16u;
+    uint32_t V[7];
+#pragma unroll
+    for (int i = 0; i < 7; i++) V[i] = __funnelshift_r(W[i], W[i + 1], f);
+    const uint32_t s = sh >> 1;
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint32_t t = (s & 1u) ? V[k + 1] : V[k];
+        const uint32_t u = (s & 1u) ? V[k + 3] : V[k + 2];
+        o[k] = (s & 2u) ? u : t;
     }
+    return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
 template <typename T, int J>
@@ -269,11 +268,12 @@ __device__ __forceinline__ void ck_chunk(const uint32_t (&mb)[J], uint4 (&e)[J],
             const uint32_t head = (1u << (VPG - d)) - 1u;   // codes in vector A
             em = vec_own ? 0u : d == 0 ? GM : ((by_prev ? 0u : head) | (vec_next ? 0u : GM & ~head));
         }
-        while (em) {
-            const uint32_t k = __ffs(em) - 1;
-            em &= em - 1;
-            const uint32_t dst = p + __popc(m & ((1u << k) - 1u));
-            if (dst < caprel) ob[dst] = (C)code_at<C>(e[j], k);
+        if (em) {
+#pragma unroll
+            for (int k = 0; k < VPG; k++) {
+                const uint32_t dst = p + __popc(m & ((1u << k) - 1u));
+                if (((em >> k) & 1u) && dst < caprel) ob[dst] = (C)code_at<C>(e[j], (uint32_t)k);
+            }
         }
     }
 }

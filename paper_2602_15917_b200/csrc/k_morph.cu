@@ -391,42 +391,9 @@ __device__ __forceinline__ uint32_t seg_sum(uint32_t v) {
     }
 }
 
-// The first rs x-runs (x0, x1 exclusive) of a row held by a segment of L lanes x KW words (lane sl
-// holds words KW sl .. KW sl + KW - 1; pad bits 0): starts and ends from the neighbouring bits, their
-// ranks by a segment scan, written to slot[0 .. rs).
-template <int L, int KW>
-__device__ __forceinline__ void emit_slots(const uint32_t (&o)[KW], uint32_t sl, uint2 *slot, uint32_t rs, bool valid) {
-    uint32_t left = __shfl_up_sync(FULL, o[KW - 1], 1, L);
-    uint32_t right = __shfl_down_sync(FULL, o[0], 1, L);
-    if (sl == 0) left = 0u;
-    if (sl == L - 1) right = 0u;
-    uint32_t st[KW], en[KW], ns = 0, ne = 0;
-#pragma unroll
-    for (int i = 0; i < KW; i++) {
-        st[i] = o[i] & ~__funnelshift_l(i ? o[i - 1] : left, o[i], 1);
-        en[i] = o[i] & ~__funnelshift_r(o[i], i < KW - 1 ? o[i + 1] : right, 1);
-        ns += __popc(st[i]);
-        ne += __popc(en[i]);
-    }
-    uint32_t both = ns | (ne << 16);
-#pragma unroll
-    for (int d = 1; d < L; d <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, both, d, L);
-        if (sl >= (uint32_t)d) both += t;
-    }
-    uint32_t is = (both & 0xffffu) - ns, ie = (both >> 16) - ne;
-    if (!valid) return;
-#pragma unroll
-    for (int i = 0; i < KW; i++) {
-        const uint32_t xb = 32 * (KW * sl + i);
-        for (uint32_t m = st[i]; m && is < rs; m &= m - 1) slot[is++].x = xb + __ffs(m) - 1;
-        for (uint32_t m = en[i]; m && ie < rs; m &= m - 1) slot[ie++].y = xb + __ffs(m);
-    }
-}
-
 template <int L, int KW, int RY>
 __global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open3d_rows(MorphArgs A, roix_scalars *sc) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = A.rs;   // read by a6 after this launch
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = 0;   // no run records from this form
     if (get_err(sc)) return;
     constexpr int S = 32 / L, MR = RY + 4, ER = RY + 2;
     using WT = WordsT<KW>;
@@ -509,7 +476,6 @@ __global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open
                 WT::st(ob + j * (int)W, o);
                 if (sl == 0 && A.row_runs) A.row_runs[rbase + j] = cnt;
             }
-            if (A.rs) emit_slots<L, KW>(o, sl, A.run_slots + (rbase + j) * A.rs, A.rs, yb + j < Y);
         }
     };
 #pragma unroll

@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(256, 2) k_morph2d(M2Args A, roix_scalars *sc) 
             __syncwarp();
             // x-runs of the row: starts (set, left clear) and ends (set, right clear; exclusive end =
             // position + 1); the i-th start pairs with the i-th end
-            uint32_t runs = 0;
+            uint32_t runs = 0, nends = 0;   // starts / ends met so far in the row
             for (uint32_t k0 = 0; k0 < W; k0 += 32) {
                 const uint32_t k = k0 + lane;
                 const uint32_t w = k < W ? od[k] : 0u;
@@ -279,13 +279,14 @@ __global__ void __launch_bounds__(256, 2) k_morph2d(M2Args A, roix_scalars *sc) 
                 const uint32_t starts = w & ~((w << 1) | (lw >> 31));
                 const uint32_t ends = w & ~((w >> 1) | (rw << 31));
                 const uint32_t ns = __popc(starts), ne = __popc(ends);
-                if (A.run_slots && runs < A.rs) {
-                    uint32_t is = runs + warp_incl_scan(ns) - ns, ie = runs + warp_incl_scan(ne) - ne;
+                if (A.run_slots && nends < A.rs) {
+                    uint32_t is = runs + warp_incl_scan(ns) - ns, ie = nends + warp_incl_scan(ne) - ne;
                     uint2 *slot = A.run_slots + (uint64_t)r * A.rs;
                     for (uint32_t sb = starts; sb && is < A.rs; sb &= sb - 1, is++) slot[is].x = 32 * k + __ffs(sb) - 1;
                     for (uint32_t eb = ends; eb && ie < A.rs; eb &= eb - 1, ie++) slot[ie].y = 32 * k + __ffs(eb);
                 }
                 runs += __reduce_add_sync(FULL, ns);
+                nends += __reduce_add_sync(FULL, ne);
             }
             if (A.row_runs && lane == 0) A.row_runs[r] = runs;
         }

@@ -54,11 +54,12 @@ def _check(cfg, p, x, res, classes=2, keep="size"):
     return ref
 
 
+@pytest.mark.parametrize("extract", ["mask", "runs"])
 @pytest.mark.parametrize("cfg", CASES, ids=lambda c: c.name)
-def test_pipeline_vs_oracle(cfg):
+def test_pipeline_vs_oracle(cfg, extract):
     x = synth.generate(cfg)
     p = Pipeline(cfg.shape, cfg.dtype, eb=cfg.eb, rel_eb=cfg.rel_eb, conn=cfg.conn, se=cfg.se,
-                 min_size=cfg.min_size, polarity=cfg.polarity)
+                 min_size=cfg.min_size, polarity=cfg.polarity, extract=extract)
     res = p.run(x)
     ref = _check(cfg, p, x, res)
     # the step reduces the data (paper: spatial reduction 1.5x-8.5x)
