@@ -434,6 +434,10 @@ def main():
     }
     clocks = clk.summary()
     line["clocks"] = clocks
+    # ---- per-artefact parity of this very run against the stored oracle result (full-size configs)
+    if not dist_on and args.scale == 1.0 and args.classes == 2 and not args.frames and args.keep == "size" \
+            and args.background == "none":
+        line["parity"] = parity_vs_golden(p, cfg, s)
     if args.greedy is not None and not dist_on and cfg.dtype == "u16":
         line["next2_greedy"] = next2(p, x, cfg, args)
     if not args.no_next4 and not dist_on:
@@ -456,6 +460,40 @@ def main():
         print(json.dumps(line), flush=True)
     if dist_on:
         dist.destroy_process_group()
+
+
+def parity_vs_golden(p, cfg, s):
+    """Compare the timed run's outputs with tests/golden/fullsize_<cfg>.json (the streaming oracle's
+    result, scripts/make_fullsize_golden.py): histogram, I_max / t8, component table, K, count, code
+    stream.  Returns {artefact: bool} plus provenance, or a note when no valid golden exists."""
+    import numpy as np
+    import torch
+
+    from oracle.digest import digest_buffer, source_hashes, table_digest
+
+    path = os.path.join(ROOT, "tests", "golden", "fullsize_%s.json" % cfg.name)
+    if not os.path.exists(path):
+        return {"checked": False, "note": "no stored oracle result for %s (C1/C2: tests/test_gpu_pipeline.py)" % cfg.name}
+    g = json.load(open(path))
+    if g.get("sources") != source_hashes():
+        return {"checked": False, "note": "stored oracle result is for other oracle/generator sources"}
+    n = cfg.n
+    h = p.hist.cpu().numpy().view(np.uint64)
+    cnt = int(s.count)
+    nc = int(s.n_components)
+    tab = (p.comp_min[:nc].cpu().numpy().view(np.uint64), p.comp_size[:nc].cpu().numpy().view(np.uint64),
+           p.comp_kept[:nc].cpu().numpy())
+    K = p.o.view(torch.uint8)[: n // 8].cpu().numpy()
+    codes = p.codes.view(torch.uint8)[: 2 * cnt].cpu().numpy()
+    res = {"checked": True, "vs": "tests/golden/fullsize_%s.json (oracle/stream.py, streaming oracle)" % cfg.name,
+           "histogram": table_digest(h, np.zeros(0, np.uint64), np.zeros(0, np.uint8)) == g["hist_digest"],
+           "threshold": int(s.t8) == g["t8"] and float(s.i_max) == g["i_max"],
+           "table": nc == g["n_components"] and table_digest(*tab) == g["table_digest"],
+           "K": digest_buffer(K) == g["K"], "count": cnt == g["count"],
+           "stream": digest_buffer(codes) == g["stream"],
+           "g_invariance": "tested on G = 2, 3, 4, 8 (tests/test_gpu_sharded.py)"}
+    res["all"] = all(v for k, v in res.items() if isinstance(v, bool))
+    return res
 
 
 def next2(p, x, cfg, args):
