@@ -306,6 +306,17 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
         if (r) r &= r - 1;
         return k;
     };
+    // the x of a densely kept chunk is prefetched into L2 (TMA bulk prefetch) two chunks ahead, so
+    // its loads hit L2 when its turn comes; sparse chunks are not (the prefetch would read the whole
+    // 16-byte groups' neighbourhood, beyond the kept sectors)
+    auto pref = [&](int kk) {
+        if (kk < 0 || lane != 0) return;
+        if (w.ccnt[c0 + kk] < CK_VOX / 4) return;
+        const uint64_t v0 = (c0 + kk) * CK_VOX;
+        if (v0 + CK_VOX > n) return;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(x + v0), "r"((uint32_t)(CK_VOX * sizeof(T)))
+                     : "memory");
+    };
     int k = nextk(rem);
     uint32_t mb[J];
     uint4 e[J];
@@ -313,6 +324,7 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
     ck_load<T, J>(x, n, c0 + k, mb, e);
     int kn = nextk(rem);
     uint32_t kwn = ldk(kn);
+    pref(kn);
     while (k >= 0) {
         uint32_t mbn[J];
         uint4 en[J];
@@ -322,6 +334,7 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
         }
         const int knn = nextk(rem);
         const uint32_t kwnn = ldk(knn);
+        pref(knn);
         const uint64_t cbase = off0 + gbase + __shfl_sync(FULL, excl, k);
         const uint32_t ccount = __shfl_sync(FULL, cc, k);
         ck_chunk<T, C, QM, J>(mb, e, cbase, ccount, out, capacity, q, err);

@@ -12,6 +12,8 @@
 // dilation are word-wise AND / OR of the row, its +-1 x-shifts (funnel shifts across the
 // neighbouring words) and the neighbouring rows / planes.  Both open kernels count the x-runs of
 // every output row (the fused first step of a6 CCL).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "async.cuh"
@@ -661,9 +663,44 @@ __global__ void __launch_bounds__(256, 3) k_open3d_reg(MorphArgs A, roix_scalars
 // Rows r = q*Y + y of the slab (q = plane); neighbours only within the same plane.  S = rows per
 // step = warps per CTA.  The output rows of a step are contiguous bits [c X, (c+S) X) of o; they are
 // assembled from the o rows in shared memory into whole words.
+// Warp: the x-runs (x0, x1 exclusive) of a row of W words in shared memory (guard words 0 at [-1] and
+// [W]) into slot[0 ..), for a row known to hold at most the slots' count: words with a run start or
+// end are found by ballot, their bits walked in order.
+__device__ __forceinline__ void row_slots(const uint32_t *od, uint32_t W, uint2 *slot) {
+    const uint32_t lane = lane_id();
+    uint32_t ns = 0, ne = 0;
+    for (uint32_t k0 = 0; k0 < W; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const uint32_t w = k < W ? od[k] : 0u;
+        const uint32_t lw = k < W ? od[(int)k - 1] : 0u, rw = k + 1 < W ? od[k + 1] : 0u;
+        const uint32_t st = w & ~((w << 1) | (lw >> 31)), en = w & ~((w >> 1) | (rw << 31));
+        uint32_t bs = __ballot_sync(FULL, st != 0), be = __ballot_sync(FULL, en != 0);
+        while (bs) {
+            const uint32_t l = __ffs(bs) - 1;
+            bs &= bs - 1;
+            uint32_t m = __shfl_sync(FULL, st, l);
+            while (m) {
+                if (lane == 0) slot[ns].x = 32 * (k0 + l) + __ffs(m) - 1;
+                m &= m - 1;
+                ns++;
+            }
+        }
+        while (be) {
+            const uint32_t l = __ffs(be) - 1;
+            be &= be - 1;
+            uint32_t m = __shfl_sync(FULL, en, l);
+            while (m) {
+                if (lane == 0) slot[ne].y = 32 * (k0 + l) + __ffs(m);
+                m &= m - 1;
+                ne++;
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     extern __shared__ uint32_t smem[];
-    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = 0;   // no run records from this form
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = A.rs;   // read by a6 after this launch
     if (get_err(sc)) return;
     const uint32_t W = A.W, WS = A.WS;
     constexpr int S = 8;                          // warps per CTA (launched with 256 threads)
@@ -746,6 +783,8 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
 #pragma unroll
                 for (int d = 16; d > 0; d >>= 1) runs += __shfl_xor_sync(FULL, runs, d);
                 if (lane_id() == 0) A.row_runs[r] = runs;
+                __syncwarp();
+                if (A.rs && runs && runs <= A.rs) row_slots(od, W, A.run_slots + (uint64_t)r * A.rs);
             }
         }
         __syncthreads();
@@ -831,7 +870,13 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     A.m_words = nwords;
     cudaError_t e;
     // in-plane SE: binarise + open in one pass over x (m stays on chip)
-    if (se == 4 && !prebinarized && g.nx >= 32)
+    // the fused one-pass form (k_morph2d) measured slower than binarise + k_open2d on C3 (12.9 vs 9.3 ms:
+    // it is instruction-bound); opt in with ROIX_MORPH2D=1
+    static const bool use_m2d = [] {
+        const char *e = getenv("ROIX_MORPH2D");
+        return e && e[0] == '1';
+    }();
+    if (use_m2d && se == 4 && !prebinarized && g.nx >= 32)
         return launch_morph2d(x, dtype, g, sc, o_bits, row_runs, A.run_slots, A.rs, frames, st);
     // a4: stream x -> m (after a fused speculative pass: resolve its window, binarise only on a miss)
     if (prebinarized && (e = launch_spec_resolve(x, dtype, g, sc, ws, st)) != cudaSuccess) return e;
