@@ -450,8 +450,8 @@ def main():
         nz = sample_planes(cfg, 6e6)
         x_np = synth.to_numpy(x[:nz], cfg)
         B_np = kw["background"].cpu().numpy().view(np.uint16) if "background" in kw else None
-        t, reps = time_oracle(x_np, cfg, classes=args.classes, frames=args.frames, keep=args.keep, B=B_np,
-                                bg=args.background)
+        t, reps = time_oracle(x_np, cfg, budget_s=15.0, max_reps=3, classes=args.classes, frames=args.frames,
+                              keep=args.keep, B=B_np, bg=args.background)
         line["cpu_baseline"] = {"value": x_np.nbytes / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "sample": "%s planes [0,%d) (%d voxels, %.1f MB), whole oracle pipeline, best of %d" %
                                           (cfg.name, nz, x_np.size, x_np.nbytes / 1e6, reps),

@@ -31,7 +31,6 @@ constexpr int CK_VOX = 1024;            // voxels per chunk
 constexpr int CK_WORDS = CK_VOX / 32;   // mask words per chunk
 constexpr int CK_G = 32;                // chunks per group (one warp task)
 constexpr int CK_THREADS = 256;
-constexpr bool CK_DB = false;           // double-buffer x across chunks (measured: fewer resident warps lose)
 
 struct CkWS {
     uint16_t *ccnt;      // [nchunks]: kept voxels per chunk
@@ -306,51 +305,43 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
         if (r) r &= r - 1;
         return k;
     };
-    // the x of a densely kept chunk is prefetched into L2 (TMA bulk prefetch) two chunks ahead, so
-    // its loads hit L2 when its turn comes; sparse chunks are not (the prefetch would read the whole
-    // 16-byte groups' neighbourhood, beyond the kept sectors)
-    auto pref = [&](int kk) {
-        if (kk < 0 || lane != 0) return;
-        if (w.ccnt[c0 + kk] < CK_VOX / 4) return;
+    // Software pipeline through L2: while chunk k is processed, the kept 16-byte groups of the next
+    // chunk are already prefetched into L2 (one prefetch.global.L2 per kept group: exactly the sectors
+    // the loads will touch) and the K word of the chunk after that is in flight; so the loads of a
+    // chunk wait on L2, not on DRAM.
+    auto pf = [&](int kk, const uint32_t (&m)[J]) {
+        if (kk < 0) return;
         const uint64_t v0 = (c0 + kk) * CK_VOX;
         if (v0 + CK_VOX > n) return;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(x + v0), "r"((uint32_t)(CK_VOX * sizeof(T)))
-                     : "memory");
+#pragma unroll
+        for (int j = 0; j < J; j++)
+            if (m[j]) asm volatile("prefetch.global.L2 [%0];" ::"l"(x + v0 + (uint64_t)(32 * j + lane) * (16 / sizeof(T))));
     };
     int k = nextk(rem);
-    uint32_t mb[J];
-    uint4 e[J];
-    ck_masks<T, J>(ldk(k), mb);
-    ck_load<T, J>(x, n, c0 + k, mb, e);
+    const uint32_t kw = ldk(k);
     int kn = nextk(rem);
     uint32_t kwn = ldk(kn);
-    pref(kn);
+    uint32_t mb[J], mbn[J];
+    uint4 e[J];
+    ck_masks<T, J>(kw, mb);
+    ck_load<T, J>(x, n, c0 + k, mb, e);
+    ck_masks<T, J>(kwn, mbn);
+    pf(kn, mbn);
     while (k >= 0) {
-        uint32_t mbn[J];
-        uint4 en[J];
-        if constexpr (sizeof(T) == 2 && CK_DB) {   // issue the next chunk's x before processing this one
-            ck_masks<T, J>(kwn, mbn);
-            if (kn >= 0) ck_load<T, J>(x, n, c0 + kn, mbn, en);
-        }
         const int knn = nextk(rem);
-        const uint32_t kwnn = ldk(knn);
-        pref(knn);
+        const uint32_t kwnn = ldk(knn);   // arrives while chunk k is processed
         const uint64_t cbase = off0 + gbase + __shfl_sync(FULL, excl, k);
         const uint32_t ccount = __shfl_sync(FULL, cc, k);
         ck_chunk<T, C, QM, J>(mb, e, cbase, ccount, out, capacity, q, err);
-        if constexpr (sizeof(T) == 2 && CK_DB) {
+        if (kn >= 0) {
 #pragma unroll
-            for (int j = 0; j < J; j++) {
-                mb[j] = mbn[j];
-                e[j] = en[j];
-            }
-        } else {
-            ck_masks<T, J>(kwn, mb);
-            if (kn >= 0) ck_load<T, J>(x, n, c0 + kn, mb, e);
+            for (int j = 0; j < J; j++) mb[j] = mbn[j];
+            ck_load<T, J>(x, n, c0 + kn, mb, e);   // prefetched into L2 one chunk ago
         }
+        ck_masks<T, J>(kwnn, mbn);
+        pf(knn, mbn);
         k = kn;
         kn = knn;
-        kwn = kwnn;
     }
 }
 

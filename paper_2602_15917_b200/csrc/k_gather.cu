@@ -273,6 +273,9 @@ __device__ __forceinline__ void rx_task(const T *__restrict__ x, const RunsView 
         const uint64_t src2 = __shfl_sync(FULL, src, k2 < 0 ? 0 : k2);
         const bool in_range = jv >= 0 && jv + V <= (int64_t)total && ab + (uint64_t)(jv + (int64_t)d0) + V <= capacity;
         const uint64_t a_left = covered && jv >= 0 && (uint64_t)jv < kor + klr ? kor + klr - (uint64_t)jv : 0;   // codes left in run k
+        // the source of this lane's vector two steps ahead into L2 when the run continues that far
+        if (covered && jv >= 0 && (uint64_t)jv + 65 * V <= kor + klr)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(x + srcr + ((uint64_t)jv - kor) + 64 * V));
         bool done = false;
         if (covered && in_range && a_left > 0) {
             C *dst = out + ab + (uint64_t)(jv + (int64_t)d0);

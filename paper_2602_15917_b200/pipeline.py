@@ -97,7 +97,8 @@ class Pipeline:
         self.row_runs = torch.empty(Z * Y, dtype=torch.int32, device=dev)
         # run records of every row (x0, x1) written by the opening for rows of <= RS runs, so a6 does
         # not re-read those rows of o (roix_morph_slots / roix_label_slots)
-        self.rs = 8 if X >= 64 else 0
+        # (only the in-plane opening writes them; C3 rows hold ~11 runs on average: noise specks)
+        self.rs = 32 if (X >= 64 and se == 4) else 0
         self.run_slots = torch.empty(max(1, Z * Y * self.rs * 2), dtype=torch.int32, device=dev) if self.rs else None
         # fused (speculative) histogram + binarisation: one read of x for a2 + a4 (roix_histogram_binarize);
         # off by default: on B200 the histogram pass is bound by shared-memory atomics, and the fused pass
