@@ -135,10 +135,11 @@ def alg_bytes(cfg, n, count, background=False):
 
 # the C-ABI call each timed stage is (its kernels: profiles/*/launches_*.txt)
 STAGE_CALLS = {"range": "roix_range (k_range)", "histogram": "roix_histogram (k_hist_*)",
-               "morph": "roix_morph (k_binarize + k_open3d_rows/k_open2d)",
-               "label": "roix_label (runs, union-find, filter: 9 kernels)",
+               "morph": "roix_morph_slots (k_binarize + k_open3d_rows / k_open2d)",
+               "label": "roix_label_slots (runs, union-find, filter)",
                "background": "roix_background (k_background_vec)",
-               "extract": "roix_extract (k_extract_count + scan + k_extract)"}
+               "extract": "roix_extract (k_ck_count + scan + k_ck_extract)",
+               "extract_runs": "roix_extract_runs (k_kept_len + scan + k_rx_map + k_rx_extract)"}
 
 
 def cpu_info():
@@ -421,7 +422,8 @@ def main():
                    "l2": ("input %.0f MB < 2 x 126 MB L2: 512 MB written between timed steps, each step timed "
                           "alone" % (cfg.nbytes / 1e6)) if flush else
                          "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
-        "roofline": {"bound": "hbm", "kernel": STAGE_CALLS.get(dom, dom), "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm",
+                     "kernel": STAGE_CALLS.get("extract_runs" if dom == "extract" and args.extract == "runs" else dom, dom), "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "alg_bytes": ab[dom],
                      "peak_source": peak_src},
         "stage_frac": {k: ab[k] / (stage_ms[k] * 1e-3) / 1e9 / peak for k in ab if k in stage_ms},

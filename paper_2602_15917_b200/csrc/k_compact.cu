@@ -305,18 +305,8 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
         if (r) r &= r - 1;
         return k;
     };
-    // Software pipeline through L2: while chunk k is processed, the kept 16-byte groups of the next
-    // chunk are already prefetched into L2 (one prefetch.global.L2 per kept group: exactly the sectors
-    // the loads will touch) and the K word of the chunk after that is in flight; so the loads of a
-    // chunk wait on L2, not on DRAM.
-    auto pf = [&](int kk, const uint32_t (&m)[J]) {
-        if (kk < 0) return;
-        const uint64_t v0 = (c0 + kk) * CK_VOX;
-        if (v0 + CK_VOX > n) return;
-#pragma unroll
-        for (int j = 0; j < J; j++)
-            if (m[j]) asm volatile("prefetch.global.L2 [%0];" ::"l"(x + v0 + (uint64_t)(32 * j + lane) * (16 / sizeof(T))));
-    };
+    // the K word of the chunk after next is in flight while a chunk is processed (per-group L2
+    // prefetches of the next chunk's x were measured and did not pay: the kernel is issue-bound)
     int k = nextk(rem);
     const uint32_t kw = ldk(k);
     int kn = nextk(rem);
@@ -326,7 +316,6 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
     ck_masks<T, J>(kw, mb);
     ck_load<T, J>(x, n, c0 + k, mb, e);
     ck_masks<T, J>(kwn, mbn);
-    pf(kn, mbn);
     while (k >= 0) {
         const int knn = nextk(rem);
         const uint32_t kwnn = ldk(knn);   // arrives while chunk k is processed
@@ -336,10 +325,9 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
         if (kn >= 0) {
 #pragma unroll
             for (int j = 0; j < J; j++) mb[j] = mbn[j];
-            ck_load<T, J>(x, n, c0 + kn, mb, e);   // prefetched into L2 one chunk ago
+            ck_load<T, J>(x, n, c0 + kn, mb, e);
         }
         ck_masks<T, J>(kwnn, mbn);
-        pf(knn, mbn);
         k = kn;
         kn = knn;
     }

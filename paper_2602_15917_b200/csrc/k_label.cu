@@ -295,11 +295,6 @@ __global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__res
     uint32_t *__restrict__ rrow = W.rrow;
     const uint32_t *__restrict__ rs = W.row_start;
     for (uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gi < ngroups; gi += wpg) {
-        if (lane == 0 && gi + wpg < ngroups) {   // the next group's rows of o into L2
-            const uint64_t rn = (gi + wpg) * S * RR;
-            const uint64_t rend = min(rows, rn + (uint64_t)S * RR);
-            l2_prefetch_range(o + rn * (uint64_t)(L * KW), (rend - rn) * (uint64_t)(L * KW) * 4);
-        }
         const uint64_t r0 = (gi * S + seg) * RR;   // this segment's first row
         // row offsets rs[r0 .. r0 + RR]: one per lane when the segment is wide enough, else all per lane
         uint32_t off = 0, offs[RR + 1];

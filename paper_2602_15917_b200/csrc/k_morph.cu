@@ -420,17 +420,6 @@ __global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open
     const uint32_t ve = vm >> 1;   // bit i: e row yb-1+i is inside the plane
 
     uint32_t m[3][MR][KW], e[3][ER][KW];
-    // the segment's m rows of plane p (rows yb-2 .. yb+RY+1, clipped to the plane) into L2 ahead of
-    // use (TMA bulk prefetch): the z-march then finds them in L2 instead of waiting on DRAM
-    auto prefetch = [&](int p) {
-        if (sl != 0 || p < 0 || p >= nz || p > ze + 1) return;
-        const int r0 = max(yb - 2, 0), r1 = min(yb + RY + 2, Y);
-        if (r1 <= r0) return;
-        const uint32_t *a = A.m + (uint64_t)p * plane_w + (uint64_t)r0 * W;
-        const uint32_t bytes = (uint32_t)(r1 - r0) * W * 4u;
-        const uintptr_t lo = (uintptr_t)a & ~(uintptr_t)15, hi = ((uintptr_t)a + bytes + 15) & ~(uintptr_t)15;
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(lo), "r"((uint32_t)(hi - lo)) : "memory");
-    };
     auto load = [&](int p, uint32_t (&dst)[MR][KW]) {
         const int64_t gp = z0 + p;
         const uint32_t *pb = nullptr;
@@ -500,16 +489,12 @@ __global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open
     load(zs - 2, m[0]);
     load(zs - 1, m[1]);
     load(zs, m[2]);
-    prefetch(zs + 1);
-    prefetch(zs + 2);
-    prefetch(zs + 3);
     // step p: e(p) from m(p-1..p+1); m(p+2) into the freed slot; o(p-1) from e(p-2..p)
 #define ROIX_OPEN_STEP(A0, A1, A2)                                  \
     {                                                               \
         if (p > ze) break;                                          \
         erode(p, m[A0], m[A1], m[A2], e[A2]);                       \
         if (p + 2 <= ze + 1) load(p + 2, m[A0]);                    \
-        prefetch(p + 5);                                            \
         if (p - 1 >= zs) dilate(p - 1, e[A0], e[A1], e[A2]);        \
         p++;                                                        \
     }
@@ -769,14 +754,6 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     for (int i = warp; i < 2; i += S) comp_e(r0 - 1 + i);
     __syncthreads();
     for (int64_t c0 = r0; c0 < r1; c0 += S) {
-        // the m rows two steps ahead into L2 (one contiguous range of bits per step)
-        if (threadIdx.x == 0) {
-            const int64_t pa = c0 + 2 + 2 * S, pb = min(pa + S, min(rows, r1 + 2));
-            if (pa < pb) {
-                const uint64_t b0 = (uint64_t)pa * A.nx, b1 = (uint64_t)pb * A.nx;
-                l2_prefetch_range(A.m + (b0 >> 5), ((b1 + 31) >> 5) * 4 - (b0 >> 5) * 4 + 4);
-            }
-        }
         load_m(c0 + 2 + warp);
         __syncthreads();
         comp_e(c0 + 1 + warp);

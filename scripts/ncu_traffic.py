@@ -13,12 +13,14 @@ import sys
 STAGE = {
     "range": ["k_range"],
     "background": ["k_background_vec", "k_background_scalar"],
+    "setup": ["k_hist_clear"],
     "histogram": ["k_hist_u16", "k_hist_f32", "k_hist_u16_frames"],
     "threshold": ["k_threshold", "k_threshold_frames"],
-    "morph": ["k_binarize", "k_open3d_reg", "k_open3d_rows", "k_open2d"],
-    "label": ["k_scan_dlb", "k_runs_total", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross", "k_resolve_broots",
+    "morph": ["k_binarize", "k_open3d_reg", "k_open3d_rows", "k_open2d", "k_morph2d"],
+    "label": ["k_scan_dlb", "k_runs_total", "k_runs_slots", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross", "k_resolve_broots",
               "k_flatten_sizes", "k_largest_init", "k_largest", "k_root_flags", "k_table", "k_table_total", "k_clear_dropped", "k_table_clear"],
-    "extract": ["k_extract_count", "k_extract", "k_extract_seg", "k_extract_total"],
+    "extract": ["k_extract_count", "k_extract", "k_extract_seg", "k_extract_total", "k_ck_count", "k_ck_extract",
+                "k_ck_total", "k_kept_len", "k_rx_map", "k_rx_extract", "k_gather_total"],
 }
 
 
@@ -42,7 +44,7 @@ def steps(path):
 def main(path, config, out_dir="profiles"):
     data, order, starts = steps(path)
     s0 = starts[-1]                          # the last step of the run, up to its extract's total
-    ends = [i for i in range(s0, len(order)) if order[i][1] == "k_extract_total"]
+    ends = [i for i in range(s0, len(order)) if order[i][1] in ("k_extract_total", "k_ck_total", "k_gather_total")]
     s1 = ends[0] + 1 if ends else len(order)
     kern = order[s0:s1]
     # the scan kernel appears in label and extract: attribute by position (label precedes extract)
@@ -50,7 +52,8 @@ def main(path, config, out_dir="profiles"):
     cur = None
     for k in kern:
         for st, names in STAGE.items():
-            if k[1] in names and not (k[1] == "k_scan_dlb" and cur == "extract"):
+            if k[1] in names and not (k[1] == "k_scan_dlb" and cur == "extract") and \
+                    not (k[1] == "k_gather_total" and cur is None):
                 cur = st
                 break
         stage_of[k] = cur
