@@ -204,77 +204,170 @@ __device__ __forceinline__ void ck_load(const T *__restrict__ x, uint64_t n, uin
     }
 }
 
+// Per-warp shared staging of one chunk: the quantised 16-byte groups in source order, every group's
+// mask and output position (chunk-relative), and for every aligned output vector the group holding
+// its first code.
+template <typename T>
+struct CkStage {
+    static constexpr int NG = 32 * CkTraits<T>::J;          // groups per chunk
+    static constexpr int NV = CK_VOX / CkTraits<T>::VPG + 2; // output vectors per chunk (with the shared ends)
+    uint4 codes[NG + 1];
+    uint16_t pos[NG + 1];
+    uint8_t mask[NG + 1];
+    uint8_t vgroup[NV];
+};
+
+// elements [sb, sb + V) of the 2V elements (a, b): branch-free (lanes may differ)
+template <typename C>
+__device__ __forceinline__ uint4 window_el(const uint4 &a, const uint4 &b, uint32_t sb) {
+    const uint32_t sh = sb * (uint32_t)(sizeof(C) / 2);   // in halfwords, 0..7
+    const uint32_t W[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint32_t f = (sh & 1u) * 16u;
+    uint32_t Vv[7];
+#pragma unroll
+    for (int i = 0; i < 7; i++) Vv[i] = __funnelshift_r(W[i], W[i + 1], f);
+    const uint32_t s = sh >> 1;
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint32_t t = (s & 1u) ? Vv[k + 1] : Vv[k];
+        const uint32_t u = (s & 1u) ? Vv[k + 3] : Vv[k + 2];
+        o[k] = (s & 2u) ? u : t;
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+// position of the (r+1)-th set bit of an 8-bit mask (r < popc(m))
+__device__ __forceinline__ uint32_t sel8(uint32_t m, uint32_t r) {
+    for (uint32_t i = 0; i < r; i++) m &= m - 1;
+    return __ffs(m) - 1;
+}
+
+// Output-driven chunk: (A) the lane's groups are quantised and staged in shared memory with their
+// masks and positions, and every aligned output vector learns which group holds its first code;
+// (B) lane i writes output vectors i, i+32, ...: a vector whose 8 (fp32: 4) codes come from
+// consecutive kept voxels is one 16-byte window of the staged codes and one 16-byte store; (C) the
+// rest -- vectors across a run end, the two vectors the chunk shares with its neighbours, the
+// capacity edge -- are written code by code, eight lanes per vector.
 template <typename T, typename C, int QM, int J>
 __device__ __forceinline__ void ck_chunk(const uint32_t (&mb)[J], uint4 (&e)[J], uint64_t cbase, uint32_t ccount,
-                                         C *__restrict__ out, uint64_t capacity, const QP &q, uint32_t &err) {
-    constexpr int VPG = CkTraits<T>::VPG;
-    constexpr uint32_t GM = (1u << VPG) - 1u;     // a full group's mask
+                                         C *__restrict__ out, uint64_t capacity, const QP &q, uint32_t &err,
+                                         CkStage<T> &S) {
+    constexpr int V = CkTraits<T>::VPG;   // codes per 16-byte vector = voxels per 16-byte group
+    constexpr int NG = CkStage<T>::NG;
+    constexpr uint32_t GM = (1u << V) - 1u;
     const uint32_t lane = lane_id();
     if (cbase + ccount > capacity) err |= ROIX_ERR_CAPACITY;
-    // output positions relative to the aligned vector holding the chunk's first code
-    const uint32_t d0 = (uint32_t)(cbase % VPG);
+    const uint32_t d0 = (uint32_t)(cbase % V);
     const uint64_t ab = cbase - d0;
     C *ob = out + ab;
     const uint32_t caprel = capacity <= ab ? 0u : (uint32_t)min(capacity - ab, (uint64_t)0xffff0000u);
-    // chunk-relative exclusive prefix of every group (slot-major, lane-minor order), two slots per
-    // 32-bit word (16-bit fields: a chunk holds at most 1024 codes)
-    uint32_t pos[J];
-    {
-        uint32_t run = d0;
+    // (A) positions (two slots per scan word: 16-bit fields), staging, vector -> group table
+    uint32_t run = 0;
 #pragma unroll
-        for (int j = 0; j < J; j += 2) {
-            const uint32_t c0 = __popc(mb[j]), c1 = __popc(mb[j + 1]);
-            const uint32_t inc = warp_incl_scan(c0 | (c1 << 16));
-            const uint32_t tot = __shfl_sync(FULL, inc, 31);
-            pos[j] = run + (inc & 0xffffu) - c0;
-            run += tot & 0xffffu;
-            pos[j + 1] = run + (inc >> 16) - c1;
-            run += tot >> 16;
-        }
-    }
+    for (int j = 0; j < J; j += 2) {
+        const uint32_t c0 = __popc(mb[j]), c1 = __popc(mb[j + 1]);
+        const uint32_t inc = warp_incl_scan(c0 | (c1 << 16));
+        const uint32_t tot = __shfl_sync(FULL, inc, 31);
+        const uint32_t p0 = run + (inc & 0xffffu) - c0;
+        run += tot & 0xffffu;
+        const uint32_t p1 = run + (inc >> 16) - c1;
+        run += tot >> 16;
+        const uint32_t pp[2] = {p0, p1}, cc[2] = {c0, c1};
 #pragma unroll
-    for (int j = 0; j < J; j++)
-        if (mb[j]) e[j] = quant16<T, QM>(e[j], q, err);
-    uint32_t F[J];   // lanes whose group in slot j is fully kept
-#pragma unroll
-    for (int j = 0; j < J; j++) F[j] = __ballot_sync(FULL, mb[j] == GM);
-#pragma unroll
-    for (int j = 0; j < J; j++) {
-        if (__ballot_sync(FULL, mb[j]) == 0) continue;   // warp-uniform skip of an empty slot row
-        const uint32_t m = mb[j];
-        const bool full = m == GM;
-        // neighbours in output order: next of (j, l) is (j, l+1), or (j+1, 0) for l = 31; the chunk's
-        // first and last group have none (their shared vectors go element by element)
-        const bool next_full = lane < 31 ? (F[j] >> (lane + 1)) & 1u : (j + 1 < J ? F[j + 1 < J ? j + 1 : j] & 1u : 0u);
-        const bool prev_full = lane > 0 ? (F[j] >> (lane - 1)) & 1u : (j > 0 ? F[j > 0 ? j - 1 : j] >> 31 : 0u);
-        const uint32_t p = pos[j], d = p % VPG, A = p - d;
-        const bool vec_own = full && d == 0 && A + VPG <= caprel;
-        const bool vec_next = full && d != 0 && next_full && A + 2 * VPG <= caprel;
-        const bool by_prev = full && d != 0 && prev_full && A + VPG <= caprel;   // prev wrote vector A
-        if (__ballot_sync(FULL, vec_next)) {
-            const uint32_t nsrc = (lane + 1) & 31u;
-            const uint4 ns = (lane == 0 && j + 1 < J) ? e[j + 1 < J ? j + 1 : j] : e[j];
-            uint4 ne;
-            ne.x = __shfl_sync(FULL, ns.x, nsrc);
-            ne.y = __shfl_sync(FULL, ns.y, nsrc);
-            ne.z = __shfl_sync(FULL, ns.z, nsrc);
-            ne.w = __shfl_sync(FULL, ns.w, nsrc);
-            if (vec_next) __stcs(reinterpret_cast<uint4 *>(ob + A + VPG), pair_vector<C>(e[j], ne, d));
-        }
-        if (vec_own) __stcs(reinterpret_cast<uint4 *>(ob + A), e[j]);
-        uint32_t em = m;   // codes stored element by element
-        if (full) {
-            const uint32_t head = (1u << (VPG - d)) - 1u;   // codes in vector A
-            em = vec_own ? 0u : d == 0 ? GM : ((by_prev ? 0u : head) | (vec_next ? 0u : GM & ~head));
-        }
-        if (em) {
-#pragma unroll
-            for (int k = 0; k < VPG; k++) {
-                const uint32_t dst = p + __popc(m & ((1u << k) - 1u));
-                if (((em >> k) & 1u) && dst < caprel) ob[dst] = (C)code_at<C>(e[j], (uint32_t)k);
+        for (int h = 0; h < 2; h++) {
+            const int jj = j + h;
+            const uint32_t g = 32 * jj + lane;
+            S.pos[g] = (uint16_t)pp[h];
+            S.mask[g] = (uint8_t)mb[jj];
+            if (mb[jj]) {
+                S.codes[g] = quant16<T, QM>(e[jj], q, err);
+                // vectors whose first code (position V v - d0) is one of this group's codes
+                const uint32_t lo = pp[h] + d0, hi = pp[h] + cc[h] + d0;   // [lo, hi) in vector-space codes
+                for (uint32_t v = (lo + V - 1) / V; v * V < hi; v++) S.vgroup[v] = (uint8_t)g;
             }
         }
     }
+    if (lane == 0) {
+        S.pos[NG] = (uint16_t)ccount;
+        S.mask[NG] = 0;
+    }
+    __syncwarp();
+    // (B) the vectors of this chunk: [0, nv) in vector space; vector v holds codes V v - d0 ..
+    const uint32_t nv = (d0 + ccount + V - 1) / V;
+    uint32_t slow_bits = 0;   // per 32-vector round: this lane's vector goes element by element
+    for (uint32_t t = 0; t * 32 < nv; t++) {
+        const uint32_t v = 32 * t + lane;
+        bool slow = false;
+        if (v < nv) {
+            const int32_t s0 = (int32_t)(V * v) - (int32_t)d0;   // chunk code index of the first code
+            bool fast = s0 >= 0 && (uint32_t)s0 + V <= ccount && V * v + V <= caprel;
+            if (fast) {
+                const uint32_t g = S.vgroup[v];
+                const uint32_t r = (uint32_t)s0 - S.pos[g];
+                const uint32_t m = S.mask[g];
+                const uint32_t sb = m == GM ? r : sel8(m, r);
+                const uint32_t win = ((m | ((uint32_t)S.mask[g + 1] << V)) >> sb) & GM;
+                if (win == GM) {
+                    const uint4 a = S.codes[g];
+                    const uint4 b = sb ? S.codes[g + 1] : a;
+                    __stcs(reinterpret_cast<uint4 *>(ob + V * v), sb ? window_el<C>(a, b, sb) : a);
+                } else {
+                    fast = false;
+                }
+            }
+            slow = !fast;
+        }
+        slow_bits |= (uint32_t)(__ballot_sync(FULL, slow) != 0) << t;
+    }
+    // (C) slow vectors, eight (fp32: four) lanes per vector, one code each
+    constexpr int LPV = V;                 // lanes per vector
+    constexpr int VPR = 32 / LPV;          // vectors per round
+    for (uint32_t t = 0; t * 32 < nv; t++) {
+        if (!((slow_bits >> t) & 1u)) continue;
+        // recompute which vectors of round t are slow (same predicate as above)
+        const uint32_t v = 32 * t + lane;
+        bool slow = false;
+        if (v < nv) {
+            const int32_t s0 = (int32_t)(V * v) - (int32_t)d0;
+            bool fast = s0 >= 0 && (uint32_t)s0 + V <= ccount && V * v + V <= caprel;
+            if (fast) {
+                const uint32_t g = S.vgroup[v];
+                const uint32_t r = (uint32_t)s0 - S.pos[g];
+                const uint32_t m = S.mask[g];
+                const uint32_t sb = m == GM ? r : sel8(m, r);
+                fast = (((m | ((uint32_t)S.mask[g + 1] << V)) >> sb) & GM) == GM;
+            }
+            slow = !fast;
+        }
+        uint32_t sm = __ballot_sync(FULL, slow);
+        while (sm) {
+            // up to VPR slow vectors per pass: sub-lane h of slot k handles code h of vector k
+            const uint32_t k = lane / LPV, h = lane % LPV;
+            uint32_t pick = sm;
+            for (uint32_t i = 0; i < k && pick; i++) pick &= pick - 1;
+            const bool has = pick != 0;
+            const uint32_t vv = has ? 32 * t + (__ffs(pick) - 1) : 0u;
+            for (uint32_t i = 0; i < VPR && sm; i++) sm &= sm - 1;
+            if (!has) continue;
+            const int32_t c = (int32_t)(V * vv + h) - (int32_t)d0;   // chunk code index
+            if (c < 0 || (uint32_t)c >= ccount || V * vv + h >= caprel) continue;
+            // the group holding code c: the last group with pos <= c (binary search over NG + 1)
+            uint32_t lo = 0, hi = NG;
+#pragma unroll
+            for (int it = 0; it < 9; it++) {
+                if (hi - lo <= 1) break;
+                const uint32_t mid = (lo + hi) >> 1;
+                if (S.pos[mid] <= (uint32_t)c) lo = mid;
+                else hi = mid;
+            }
+            const uint32_t m = S.mask[lo];
+            const uint32_t sb = sel8(m, (uint32_t)c - S.pos[lo]);
+            const uint4 cv = S.codes[lo];
+            ob[V * vv + h] = (C)code_at<C>(cv, sb);
+        }
+    }
+    __syncwarp();   // the staging is rewritten by the next chunk
 }
 
 // one warp task: chunks [part * cpp, (part + 1) * cpp) of group g, non-empty ones only; the next
@@ -283,7 +376,7 @@ template <typename T, typename C, int QM>
 __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
                                         uint64_t nchunks, const CkWS &w, uint64_t g, uint32_t part, uint32_t cpp,
                                         uint64_t off0, C *__restrict__ out, uint64_t capacity, const QP &q,
-                                        uint32_t &err) {
+                                        uint32_t &err, CkStage<T> &S) {
     constexpr int J = CkTraits<T>::J;
     const uint64_t gbase = w.goff[g];
     if (w.goff[g + 1] == gbase) return;   // no kept voxel in 32 K voxels (background)
@@ -321,7 +414,7 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
         const uint32_t kwnn = ldk(knn);   // arrives while chunk k is processed
         const uint64_t cbase = off0 + gbase + __shfl_sync(FULL, excl, k);
         const uint32_t ccount = __shfl_sync(FULL, cc, k);
-        ck_chunk<T, C, QM, J>(mb, e, cbase, ccount, out, capacity, q, err);
+        ck_chunk<T, C, QM, J>(mb, e, cbase, ccount, out, capacity, q, err, S);
         if (kn >= 0) {
 #pragma unroll
             for (int j = 0; j < J; j++) mb[j] = mbn[j];
@@ -338,22 +431,24 @@ __global__ void __launch_bounds__(CK_THREADS, sizeof(T) == 2 ? 4 : 3)
     k_ck_extract(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K, uint64_t nchunks,
                  uint64_t ngroups, uint32_t parts, CkWS w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
                  const uint64_t *offset) {
+    __shared__ CkStage<T> stage[CK_THREADS / 32];
     if (*w.err_snap) return;
     const uint64_t t = (uint64_t)blockIdx.x * (CK_THREADS / 32) + (threadIdx.x >> 5);
     const uint64_t g = t / parts;
     if (g >= ngroups) return;
+    CkStage<T> &S = stage[threadIdx.x >> 5];
     const uint32_t part = (uint32_t)(t % parts), cpp = CK_G / parts;
     const QP q = load_qp(sc);
     uint32_t err = 0;
     const uint64_t off0 = offset ? *offset : 0ull;
     if constexpr (sizeof(T) == 4) {
-        ck_task<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err);
+        ck_task<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S);
     } else {
         switch (qmode(q)) {   // uniform over the launch: one quantiser body per mode
-        case QM_POW2: ck_task<T, C, QM_POW2>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
-        case QM_INT: ck_task<T, C, QM_INT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
-        case QM_ONE: ck_task<T, C, QM_ONE>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
-        default: ck_task<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
+        case QM_POW2: ck_task<T, C, QM_POW2>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S); break;
+        case QM_INT: ck_task<T, C, QM_INT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S); break;
+        case QM_ONE: ck_task<T, C, QM_ONE>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S); break;
+        default: ck_task<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S); break;
         }
     }
     err = __reduce_or_sync(FULL, err);

@@ -34,7 +34,6 @@ struct MorphArgs {
     uint32_t *row_runs;
     uint2 *run_slots;        // [rows * rs] or null: (x0, x1) of the first rs x-runs of every output row
     uint32_t rs;
-    uint32_t sb;             // 2-D TMA form: words per staging buffer
 };
 
 template <typename T>
@@ -699,10 +698,6 @@ __device__ __forceinline__ void row_slots(const uint32_t *od, uint32_t W, uint2 
     }
 }
 
-// TMA = true: the m rows of every step arrive by one bulk copy (cp.async.bulk, the TMA engine) into one
-// of 3 staging buffers, issued two steps ahead and completed on an mbarrier, so a step never waits on
-// DRAM for its rows; the warps cut their row out of the staged bits with funnel shifts.
-template <bool TMA>
 __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     extern __shared__ uint32_t smem[];
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = A.rs;   // read by a6 after this launch
@@ -714,46 +709,11 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     uint32_t *mring = smem;            // [MS][WS]
     uint32_t *ering = mring + MS * WS; // [ES][WS]
     uint32_t *orow = ering + ES * WS;  // [S][WS]
-    uint32_t *stage = smem + (((MS + ES + S) * WS + 3) & ~3u);   // TMA: [3][A.sb] words, 16-byte aligned
-    uint64_t *bar = reinterpret_cast<uint64_t *>(stage + 3 * A.sb);   // TMA: [3]
     const int64_t Y = A.ny, X = A.nx;
     const int64_t rows = (int64_t)(A.nz * A.ny);
     const int64_t r0 = (int64_t)blockIdx.x * A.rows_per_cta;
     const int64_t r1 = min(rows, r0 + (int64_t)A.rows_per_cta);
     if (r0 >= r1) return;
-    // TMA staging: step s (rows c0 = r0 + S s) binarised rows c0+2 .. c0+S+1 -> buffer s % 3
-    auto stage_span = [&](int64_t s, uint64_t &w0, uint32_t &bytes) {
-        const int64_t ra = r0 + S * s + 2, rb = min(ra + S, rows);
-        if (ra >= rb) {
-            bytes = 0;
-            return;
-        }
-        const uint64_t b0 = (uint64_t)ra * (uint64_t)X, b1 = (uint64_t)rb * (uint64_t)X;
-        w0 = (b0 >> 5) & ~3ull;
-        uint64_t w1 = ((b1 + 31) >> 5);
-        w1 = min((w1 + 3) & ~3ull, (A.m_words + 3) & ~3ull);
-        bytes = (uint32_t)((w1 - w0) * 4);
-    };
-    auto issue = [&](int64_t s) {
-        uint64_t w0 = 0;
-        uint32_t bytes = 0;
-        stage_span(s, w0, bytes);
-        if (!bytes) return;
-        uint64_t *b = bar + (s % 3);
-        mbar_arrive_expect_tx(b, bytes);
-        bulk_g2s(stage + (s % 3) * A.sb, A.m + w0, bytes, b);
-    };
-    if constexpr (TMA) {
-        if (threadIdx.x == 0) {
-            for (int i = 0; i < 3; i++) mbar_init(bar + i, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            issue(0);
-            if (r0 + S < r1) issue(1);
-        }
-    }
     for (int i = threadIdx.x; i < (int)MS; i += blockDim.x) {
         mring[i * WS] = FULL;
         mring[i * WS + W + 1] = FULL;
@@ -772,30 +732,6 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
         else load_m_row(A.m, A.m_words, (uint64_t)r * A.nx, A.nx, W, dst);
     };
     const uint32_t tail = (uint32_t)(X - 32ll * (W - 1));
-    // TMA: row r of step s from its staging buffer (waits for the bulk copy)
-    auto load_m_staged = [&](int64_t s, int64_t r) {
-        uint32_t *dst = mrow(r);
-        if (r >= rows) {
-            fill_row(dst, W, FULL);
-            return;
-        }
-        uint64_t w0 = 0;
-        uint32_t bytes = 0;
-        stage_span(s, w0, bytes);
-        mbar_wait(bar + (s % 3), (uint32_t)((s / 3) & 1));
-        const uint32_t *src = stage + (s % 3) * A.sb;
-        const uint64_t b = (uint64_t)r * (uint64_t)X - 32 * w0;   // row start, in bits of the buffer
-        const uint32_t sh = (uint32_t)(b & 31);
-        const uint32_t *rw = src + (b >> 5);
-        const uint32_t avail = (uint32_t)(bytes / 4 - (b >> 5));   // staged words from the row's first
-        for (uint32_t k = lane_id(); k < W; k += 32) {
-            const uint32_t lo = rw[k], hi = (sh && k + 1 < avail) ? rw[k + 1] : 0u;
-            uint32_t v = sh ? __funnelshift_r(lo, hi, sh) : lo;
-            if (k == W - 1 && tail < 32) v |= ~low_mask(tail);
-            dst[k] = v;
-        }
-        __syncwarp();
-    };
     auto comp_e = [&](int64_t r) {
         uint32_t *dst = erow(r);
         if (r < 0 || r >= rows) {
@@ -818,13 +754,7 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     for (int i = warp; i < 2; i += S) comp_e(r0 - 1 + i);
     __syncthreads();
     for (int64_t c0 = r0; c0 < r1; c0 += S) {
-        if constexpr (TMA) {
-            const int64_t s = (c0 - r0) / S;
-            if (threadIdx.x == 0 && c0 + 2 * S < r1 + 2) issue(s + 2);   // buffer (s+2)%3 was freed by step s-1
-            load_m_staged(s, c0 + 2 + warp);
-        } else {
-            load_m(c0 + 2 + warp);
-        }
+        load_m(c0 + 2 + warp);
         __syncthreads();
         comp_e(c0 + 1 + warp);
         __syncthreads();
@@ -1010,15 +940,10 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         k_open3d_reg<RY><<<(unsigned)((tasks + 7) / 8), 256, 0, st>>>(A, sc);
     } else {
         const int S = 8;
-        const size_t ring = (((size_t)((S + 4) + (S + 2) + S) * A.WS) + 3) & ~(size_t)3;   // words
-        A.sb = (uint32_t)((((uint64_t)S * g.nx + 31) / 32 + 8 + 3) & ~3ull);
-        const size_t sm_tma = (ring + 3 * (size_t)A.sb) * 4 + 3 * 8;
-        const bool tma = sm_tma <= 200 * 1024;   // the staging buffers fit next to the rings
-        const size_t sm = tma ? sm_tma : ring * 4;
+        size_t sm = (size_t)((S + 4) + (S + 2) + S) * A.WS * 4;
         if (sm > 220 * 1024) return cudaErrorInvalidConfiguration;
-        auto kern = tma ? k_open2d<true> : k_open2d<false>;
-        if ((e = set_smem(kern, sm)) != cudaSuccess) return e;
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * S, sm)) != cudaSuccess) return e;
+        if ((e = set_smem(k_open2d, sm)) != cudaSuccess) return e;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_open2d, 32 * S, sm)) != cudaSuccess) return e;
         if (occ < 1) occ = 1;
         const uint64_t rows = g.nz * g.ny;
         uint64_t slots = (uint64_t)num_sms() * occ;
@@ -1031,7 +956,7 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         // which are OR-ed into a zeroed o
         A.aligned_out = g.nx % 32 == 0;
         if (!A.aligned_out && (e = cudaMemsetAsync(o_bits, 0, nwords * 4, st)) != cudaSuccess) return e;
-        kern<<<(unsigned)ctas, 32 * S, sm, st>>>(A, sc);
+        k_open2d<<<(unsigned)ctas, 32 * S, sm, st>>>(A, sc);
     }
     return cudaGetLastError();
 }
