@@ -97,6 +97,24 @@ __global__ void __launch_bounds__(CK_THREADS) k_ck_count(const uint32_t *__restr
 }
 
 // ------------------------------------------------------------------------------------- pass 2
+// Halfword shift of the 16 halfwords S = (W[0..7]) by sh halfwords (0..8): returns S[sh .. sh+8) as
+// four words.  First by sh & 1 halfword (funnel shifts), then by sh >> 1 words (two select levels).
+__device__ __forceinline__ uint4 shift_hw(const uint32_t (&W)[8], uint32_t sh) {
+    const uint32_t f = (sh & 1u) * 16u;
+    uint32_t V[7];
+#pragma unroll
+    for (int i = 0; i < 7; i++) V[i] = __funnelshift_r(W[i], W[i + 1], f);
+    const uint32_t s = sh >> 1, b0 = s & 1u, b1 = s & 2u;
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const uint32_t t = b0 ? V[k + 1] : V[k];
+        const uint32_t u = b0 ? V[k + 3] : V[k + 2];
+        o[k] = b1 ? u : t;
+    }
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
 template <typename T>
 struct CkTraits;
 template <>
@@ -120,67 +138,33 @@ __device__ __forceinline__ uint4 quant16(uint4 d, const QP &q, uint32_t &err) {
     }
 }
 
-// code k (runtime, 0 <= k < VPG) of a 16-byte group of codes
 template <typename C>
-__device__ __forceinline__ uint32_t code_at(const uint4 &e, uint32_t k) {
+__device__ __forceinline__ uint32_t code_k(const uint4 &e, int k) {   // k static
     if constexpr (sizeof(C) == 2) {
-        const uint32_t h = k >> 1;
-        const uint32_t lo = h & 1u ? e.y : e.x, hi = h & 1u ? e.w : e.z;
-        const uint32_t wd = h & 2u ? hi : lo;
-        return (wd >> ((k & 1u) * 16u)) & 0xffffu;
+        const uint32_t wd = (k >> 1) == 0 ? e.x : (k >> 1) == 1 ? e.y : (k >> 1) == 2 ? e.z : e.w;
+        return (k & 1) ? (wd >> 16) : (wd & 0xffffu);
     } else {
-        const uint32_t lo = k & 1u ? e.y : e.x, hi = k & 1u ? e.w : e.z;
-        return k & 2u ? hi : lo;
+        return k == 0 ? e.x : k == 1 ? e.y : k == 2 ? e.z : e.w;
     }
 }
 
-// The aligned output vector holding the last d codes of a fully kept group a and the first VPG - d
-// codes of the next fully kept group b: elements [VPG - d, 2 VPG - d) of (a, b).
-template <int SH>   // shift in halfwords, 1..7
-__device__ __forceinline__ uint4 shift_c(const uint4 &a, const uint4 &b) {
-    const uint32_t W[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    constexpr int w0 = SH >> 1;
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) o[k] = (SH & 1) ? __funnelshift_r(W[w0 + k], W[w0 + k + 1], 16) : W[w0 + k];
-    return make_uint4(o[0], o[1], o[2], o[3]);
-}
-// branch-free (lanes of a warp may hold different d): a halfword funnel step, then two word selects
-template <typename C>
-__device__ __forceinline__ uint4 pair_vector(const uint4 &a, const uint4 &b, uint32_t d) {
-    const uint32_t sh = sizeof(C) == 2 ? 8u - d : 2u * (4u - d);   // shift in halfwords
-    const uint32_t W[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    const uint32_t f = (sh & 1u) * 16u;
-    uint32_t V[7];
-#pragma unroll
-    for (int i = 0; i < 7; i++) V[i] = __funnelshift_r(W[i], W[i + 1], f);
-    const uint32_t s = sh >> 1;
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const uint32_t t = (s & 1u) ? V[k + 1] : V[k];
-        const uint32_t u = (s & 1u) ? V[k + 3] : V[k + 2];
-        o[k] = (s & 2u) ? u : t;
-    }
-    return make_uint4(o[0], o[1], o[2], o[3]);
-}
-
-template <typename T, int J>
-__device__ __forceinline__ void ck_masks(uint32_t kw, uint32_t (&mb)[J]) {
-    constexpr int VPG = CkTraits<T>::VPG, GPW = 32 / VPG;
-    const uint32_t lane = lane_id();
-#pragma unroll
-    for (int j = 0; j < J; j++)
-        mb[j] = (__shfl_sync(FULL, kw, j * (32 / GPW) + lane / GPW) >> ((lane % GPW) * VPG)) & ((1u << VPG) - 1u);
-}
-
-// x of the kept 16-byte groups of chunk c (zero elsewhere)
-template <typename T, int J>
-__device__ __forceinline__ void ck_load(const T *__restrict__ x, uint64_t n, uint64_t c, const uint32_t (&mb)[J],
-                                        uint4 (&e)[J]) {
-    constexpr int VPG = CkTraits<T>::VPG;
+template <typename T, typename C, int QM>
+__device__ __forceinline__ void ck_chunk(const T *__restrict__ x, uint64_t n, uint64_t c, uint32_t kw, uint64_t cbase,
+                                         uint32_t ccount, C *__restrict__ out, uint64_t capacity, const QP &q,
+                                         uint32_t &err) {
+    constexpr int VPG = CkTraits<T>::VPG, J = CkTraits<T>::J;
+    constexpr int GPW = 32 / VPG;                 // 16-byte groups per mask word
+    constexpr uint32_t GM = (1u << VPG) - 1u;     // a full group's mask
     const uint32_t lane = lane_id();
     const uint64_t v0 = c * CK_VOX;
+    if (cbase + ccount > capacity) err |= ROIX_ERR_CAPACITY;
+    // masks of the lane's groups (slot j = group 32 j + lane)
+    uint32_t mb[J];
+#pragma unroll
+    for (int j = 0; j < J; j++)
+        mb[j] = (__shfl_sync(FULL, kw, j * (32 / GPW) + lane / GPW) >> ((lane % GPW) * VPG)) & GM;
+    // x only under kept groups
+    uint4 e[J];
     const bool whole = v0 + CK_VOX <= n;
 #pragma unroll
     for (int j = 0; j < J; j++) {
@@ -202,182 +186,85 @@ __device__ __forceinline__ void ck_load(const T *__restrict__ x, uint64_t n, uin
             }
         }
     }
-}
-
-// Per-warp shared staging of one chunk: the quantised 16-byte groups in source order, every group's
-// mask and output position (chunk-relative), and for every aligned output vector the group holding
-// its first code.
-template <typename T>
-struct CkStage {
-    static constexpr int NG = 32 * CkTraits<T>::J;          // groups per chunk
-    static constexpr int NV = CK_VOX / CkTraits<T>::VPG + 2; // output vectors per chunk (with the shared ends)
-    uint4 codes[NG + 1];
-    uint16_t pos[NG + 1];
-    uint8_t mask[NG + 1];
-    uint8_t vgroup[NV];
-};
-
-// elements [sb, sb + V) of the 2V elements (a, b): branch-free (lanes may differ)
-template <typename C>
-__device__ __forceinline__ uint4 window_el(const uint4 &a, const uint4 &b, uint32_t sb) {
-    const uint32_t sh = sb * (uint32_t)(sizeof(C) / 2);   // in halfwords, 0..7
-    const uint32_t W[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    const uint32_t f = (sh & 1u) * 16u;
-    uint32_t Vv[7];
+    // chunk-relative exclusive prefix of every group (order: slot-major, lane-minor), two slots
+    // per 32-bit word (16-bit fields: a chunk holds at most 1024 codes)
+    uint32_t pre[J];
+    {
+        uint32_t run = 0;
 #pragma unroll
-    for (int i = 0; i < 7; i++) Vv[i] = __funnelshift_r(W[i], W[i + 1], f);
-    const uint32_t s = sh >> 1;
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const uint32_t t = (s & 1u) ? Vv[k + 1] : Vv[k];
-        const uint32_t u = (s & 1u) ? Vv[k + 3] : Vv[k + 2];
-        o[k] = (s & 2u) ? u : t;
-    }
-    return make_uint4(o[0], o[1], o[2], o[3]);
-}
-
-// position of the (r+1)-th set bit of an 8-bit mask (r < popc(m))
-__device__ __forceinline__ uint32_t sel8(uint32_t m, uint32_t r) {
-    for (uint32_t i = 0; i < r; i++) m &= m - 1;
-    return __ffs(m) - 1;
-}
-
-// Output-driven chunk: (A) the lane's groups are quantised and staged in shared memory with their
-// masks and positions, and every aligned output vector learns which group holds its first code;
-// (B) lane i writes output vectors i, i+32, ...: a vector whose 8 (fp32: 4) codes come from
-// consecutive kept voxels is one 16-byte window of the staged codes and one 16-byte store; (C) the
-// rest -- vectors across a run end, the two vectors the chunk shares with its neighbours, the
-// capacity edge -- are written code by code, eight lanes per vector.
-template <typename T, typename C, int QM, int J>
-__device__ __forceinline__ void ck_chunk(const uint32_t (&mb)[J], uint4 (&e)[J], uint64_t cbase, uint32_t ccount,
-                                         C *__restrict__ out, uint64_t capacity, const QP &q, uint32_t &err,
-                                         CkStage<T> &S) {
-    constexpr int V = CkTraits<T>::VPG;   // codes per 16-byte vector = voxels per 16-byte group
-    constexpr int NG = CkStage<T>::NG;
-    constexpr uint32_t GM = (1u << V) - 1u;
-    const uint32_t lane = lane_id();
-    if (cbase + ccount > capacity) err |= ROIX_ERR_CAPACITY;
-    const uint32_t d0 = (uint32_t)(cbase % V);
-    const uint64_t ab = cbase - d0;
-    C *ob = out + ab;
-    const uint32_t caprel = capacity <= ab ? 0u : (uint32_t)min(capacity - ab, (uint64_t)0xffff0000u);
-    // (A) positions (two slots per scan word: 16-bit fields), staging, vector -> group table
-    uint32_t run = 0;
-#pragma unroll
-    for (int j = 0; j < J; j += 2) {
-        const uint32_t c0 = __popc(mb[j]), c1 = __popc(mb[j + 1]);
-        const uint32_t inc = warp_incl_scan(c0 | (c1 << 16));
-        const uint32_t tot = __shfl_sync(FULL, inc, 31);
-        const uint32_t p0 = run + (inc & 0xffffu) - c0;
-        run += tot & 0xffffu;
-        const uint32_t p1 = run + (inc >> 16) - c1;
-        run += tot >> 16;
-        const uint32_t pp[2] = {p0, p1}, cc[2] = {c0, c1};
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int jj = j + h;
-            const uint32_t g = 32 * jj + lane;
-            S.pos[g] = (uint16_t)pp[h];
-            S.mask[g] = (uint8_t)mb[jj];
-            if (mb[jj]) {
-                S.codes[g] = quant16<T, QM>(e[jj], q, err);
-                // vectors whose first code (position V v - d0) is one of this group's codes
-                const uint32_t lo = pp[h] + d0, hi = pp[h] + cc[h] + d0;   // [lo, hi) in vector-space codes
-                for (uint32_t v = (lo + V - 1) / V; v * V < hi; v++) S.vgroup[v] = (uint8_t)g;
-            }
+        for (int j = 0; j < J; j += 2) {
+            const uint32_t c0 = __popc(mb[j]), c1 = __popc(mb[j + 1]);
+            const uint32_t pk = c0 | (c1 << 16);
+            const uint32_t inc = warp_incl_scan(pk);
+            const uint32_t tot = __shfl_sync(FULL, inc, 31);
+            pre[j] = run + (inc & 0xffffu) - c0;
+            run += tot & 0xffffu;
+            pre[j + 1] = run + (inc >> 16) - c1;
+            run += tot >> 16;
         }
     }
-    if (lane == 0) {
-        S.pos[NG] = (uint16_t)ccount;
-        S.mask[NG] = 0;
-    }
-    __syncwarp();
-    // (B) the vectors of this chunk: [0, nv) in vector space; vector v holds codes V v - d0 ..
-    const uint32_t nv = (d0 + ccount + V - 1) / V;
-    uint32_t slow_bits = 0;   // per 32-vector round: this lane's vector goes element by element
-    for (uint32_t t = 0; t * 32 < nv; t++) {
-        const uint32_t v = 32 * t + lane;
-        bool slow = false;
-        if (v < nv) {
-            const int32_t s0 = (int32_t)(V * v) - (int32_t)d0;   // chunk code index of the first code
-            bool fast = s0 >= 0 && (uint32_t)s0 + V <= ccount && V * v + V <= caprel;
-            if (fast) {
-                const uint32_t g = S.vgroup[v];
-                const uint32_t r = (uint32_t)s0 - S.pos[g];
-                const uint32_t m = S.mask[g];
-                const uint32_t sb = m == GM ? r : sel8(m, r);
-                const uint32_t win = ((m | ((uint32_t)S.mask[g + 1] << V)) >> sb) & GM;
-                if (win == GM) {
-                    const uint4 a = S.codes[g];
-                    const uint4 b = sb ? S.codes[g + 1] : a;
-                    __stcs(reinterpret_cast<uint4 *>(ob + V * v), sb ? window_el<C>(a, b, sb) : a);
-                } else {
-                    fast = false;
+    // quantise (only kept groups carry data; the rest stay zero and are never stored)
+#pragma unroll
+    for (int j = 0; j < J; j++)
+        if (mb[j]) e[j] = quant16<T, QM>(e[j], q, err);
+    // neighbours in output order: next of (j, l) is (j, l+1), or (j+1, 0) for l = 31; prev likewise
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+        if (__ballot_sync(FULL, mb[j]) == 0) continue;   // warp-uniform skip of an empty slot row
+        const uint32_t nsrc = (lane + 1) & 31u, psrc = (lane + 31) & 31u;
+        // value lane 0 offers to lane 31 is slot j+1's; value lane 31 offers to lane 0 is slot j-1's
+        const uint32_t mb_next_src = (lane == 0) ? (j + 1 < J ? mb[j + 1 < J ? j + 1 : j] : 0u) : mb[j];
+        const uint32_t mb_prev_src = (lane == 31) ? (j > 0 ? mb[j > 0 ? j - 1 : j] : 0u) : mb[j];
+        const uint32_t nmb = __shfl_sync(FULL, mb_next_src, nsrc);
+        const uint32_t pmb = __shfl_sync(FULL, mb_prev_src, psrc);
+        const uint4 ns = (lane == 0 && j + 1 < J) ? e[j + 1 < J ? j + 1 : j] : e[j];
+        uint4 ne;
+        ne.x = __shfl_sync(FULL, ns.x, nsrc);
+        ne.y = __shfl_sync(FULL, ns.y, nsrc);
+        ne.z = __shfl_sync(FULL, ns.z, nsrc);
+        ne.w = __shfl_sync(FULL, ns.w, nsrc);
+        // lane 31's next / lane 0's prev outside the chunk: treated as not fully kept
+        const uint32_t m = mb[j];
+        if (!m) continue;
+        const uint64_t P = cbase + pre[j];
+        // a fully kept neighbour in the chunk shares an aligned output vector with this group; it is
+        // stored as a vector when it lies below the capacity (both lanes evaluate the same test)
+        const uint64_t Ah = P - (P % VPG);   // the aligned vector holding P
+        const bool next_full = nmb == GM && !(lane == 31 && j + 1 >= J) && Ah + 2 * VPG <= capacity;
+        const bool prev_full = pmb == GM && !(lane == 0 && j == 0) && Ah + VPG <= capacity;
+        uint32_t em;   // codes stored element by element
+        if (m == GM) {
+            const uint32_t d = (uint32_t)(P % VPG);
+            if (d == 0) {
+                if (P + VPG <= capacity) __stcs(reinterpret_cast<uint4 *>(out + P), e[j]);
+                em = P + VPG <= capacity ? 0u : GM;
+            } else {
+                const uint32_t head = (1u << (VPG - d)) - 1u;   // codes in the aligned vector before P's
+                em = (prev_full ? 0u : head) | (next_full ? 0u : (GM & ~head));
+                if (next_full) {   // aligned vector: our last d codes, then the next group's first VPG - d
+                    const uint32_t W[8] = {e[j].x, e[j].y, e[j].z, e[j].w, ne.x, ne.y, ne.z, ne.w};
+                    const uint32_t sh = (VPG - d) * (uint32_t)(sizeof(C) / 2);   // halfwords: u16 8-d, fp32 2(4-d)
+                    __stcs(reinterpret_cast<uint4 *>(out + Ah + VPG), shift_hw(W, sh));
                 }
             }
-            slow = !fast;
+        } else {
+            em = m;
         }
-        slow_bits |= (uint32_t)(__ballot_sync(FULL, slow) != 0) << t;
-    }
-    // (C) slow vectors, eight (fp32: four) lanes per vector, one code each
-    constexpr int LPV = V;                 // lanes per vector
-    constexpr int VPR = 32 / LPV;          // vectors per round
-    for (uint32_t t = 0; t * 32 < nv; t++) {
-        if (!((slow_bits >> t) & 1u)) continue;
-        // recompute which vectors of round t are slow (same predicate as above)
-        const uint32_t v = 32 * t + lane;
-        bool slow = false;
-        if (v < nv) {
-            const int32_t s0 = (int32_t)(V * v) - (int32_t)d0;
-            bool fast = s0 >= 0 && (uint32_t)s0 + V <= ccount && V * v + V <= caprel;
-            if (fast) {
-                const uint32_t g = S.vgroup[v];
-                const uint32_t r = (uint32_t)s0 - S.pos[g];
-                const uint32_t m = S.mask[g];
-                const uint32_t sb = m == GM ? r : sel8(m, r);
-                fast = (((m | ((uint32_t)S.mask[g + 1] << V)) >> sb) & GM) == GM;
-            }
-            slow = !fast;
-        }
-        uint32_t sm = __ballot_sync(FULL, slow);
-        while (sm) {
-            // up to VPR slow vectors per pass: sub-lane h of slot k handles code h of vector k
-            const uint32_t k = lane / LPV, h = lane % LPV;
-            uint32_t pick = sm;
-            for (uint32_t i = 0; i < k && pick; i++) pick &= pick - 1;
-            const bool has = pick != 0;
-            const uint32_t vv = has ? 32 * t + (__ffs(pick) - 1) : 0u;
-            for (uint32_t i = 0; i < VPR && sm; i++) sm &= sm - 1;
-            if (!has) continue;
-            const int32_t c = (int32_t)(V * vv + h) - (int32_t)d0;   // chunk code index
-            if (c < 0 || (uint32_t)c >= ccount || V * vv + h >= caprel) continue;
-            // the group holding code c: the last group with pos <= c (binary search over NG + 1)
-            uint32_t lo = 0, hi = NG;
+        if (em) {
 #pragma unroll
-            for (int it = 0; it < 9; it++) {
-                if (hi - lo <= 1) break;
-                const uint32_t mid = (lo + hi) >> 1;
-                if (S.pos[mid] <= (uint32_t)c) lo = mid;
-                else hi = mid;
+            for (int k = 0; k < VPG; k++) {
+                if (!((em >> k) & 1u)) continue;
+                const uint64_t dst = P + __popc(m & ((1u << k) - 1u));
+                if (dst < capacity) out[dst] = (C)code_k<C>(e[j], k);
             }
-            const uint32_t m = S.mask[lo];
-            const uint32_t sb = sel8(m, (uint32_t)c - S.pos[lo]);
-            const uint4 cv = S.codes[lo];
-            ob[V * vv + h] = (C)code_at<C>(cv, sb);
         }
     }
-    __syncwarp();   // the staging is rewritten by the next chunk
 }
 
-// one warp task: chunks [part * cpp, (part + 1) * cpp) of group g, non-empty ones only; the next
-// chunk's x (u16: double-buffered) and the one after's K word are in flight while a chunk is processed
 template <typename T, typename C, int QM>
-__device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
-                                        uint64_t nchunks, const CkWS &w, uint64_t g, uint32_t part, uint32_t cpp,
-                                        uint64_t off0, C *__restrict__ out, uint64_t capacity, const QP &q,
-                                        uint32_t &err, CkStage<T> &S) {
-    constexpr int J = CkTraits<T>::J;
+__device__ __forceinline__ void ck_group(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
+                                         uint64_t nchunks, const CkWS &w, uint64_t g, uint64_t off0,
+                                         C *__restrict__ out, uint64_t capacity, const QP &q, uint32_t &err) {
     const uint64_t gbase = w.goff[g];
     if (w.goff[g + 1] == gbase) return;   // no kept voxel in 32 K voxels (background)
     const uint32_t lane = lane_id();
@@ -385,70 +272,44 @@ __device__ __forceinline__ void ck_task(const T *__restrict__ x, uint64_t n, con
     const uint64_t c0 = g * CK_G;
     const uint32_t cc = c0 + lane < nchunks ? (uint32_t)w.ccnt[c0 + lane] : 0u;
     const uint32_t excl = warp_incl_scan(cc) - cc;
-    const uint32_t pm = cpp >= 32 ? FULL : (((1u << cpp) - 1u) << (part * cpp));
-    uint32_t rem = __ballot_sync(FULL, cc != 0) & pm;
-    if (!rem) return;
+    uint32_t rem = __ballot_sync(FULL, cc != 0);
     auto ldk = [&](int k) -> uint32_t {
-        if (k < 0) return 0u;
         const uint64_t wi = (c0 + k) * CK_WORDS + lane;
         return wi < nwords ? __ldcs(K + wi) : 0u;
     };
-    auto nextk = [&](uint32_t &r) -> int {
-        const int k = r ? __ffs(r) - 1 : -1;
-        if (r) r &= r - 1;
-        return k;
-    };
-    // the K word of the chunk after next is in flight while a chunk is processed (per-group L2
-    // prefetches of the next chunk's x were measured and did not pay: the kernel is issue-bound)
-    int k = nextk(rem);
-    const uint32_t kw = ldk(k);
-    int kn = nextk(rem);
-    uint32_t kwn = ldk(kn);
-    uint32_t mb[J], mbn[J];
-    uint4 e[J];
-    ck_masks<T, J>(kw, mb);
-    ck_load<T, J>(x, n, c0 + k, mb, e);
-    ck_masks<T, J>(kwn, mbn);
+    int k = __ffs(rem) - 1;
+    uint32_t kw = ldk(k);
     while (k >= 0) {
-        const int knn = nextk(rem);
-        const uint32_t kwnn = ldk(knn);   // arrives while chunk k is processed
+        rem &= rem - 1;
+        const int kn = rem ? __ffs(rem) - 1 : -1;
+        const uint32_t kw_next = kn >= 0 ? ldk(kn) : 0u;   // in flight while this chunk is processed
         const uint64_t cbase = off0 + gbase + __shfl_sync(FULL, excl, k);
         const uint32_t ccount = __shfl_sync(FULL, cc, k);
-        ck_chunk<T, C, QM, J>(mb, e, cbase, ccount, out, capacity, q, err, S);
-        if (kn >= 0) {
-#pragma unroll
-            for (int j = 0; j < J; j++) mb[j] = mbn[j];
-            ck_load<T, J>(x, n, c0 + kn, mb, e);
-        }
-        ck_masks<T, J>(kwnn, mbn);
+        ck_chunk<T, C, QM>(x, n, c0 + k, kw, cbase, ccount, out, capacity, q, err);
         k = kn;
-        kn = knn;
+        kw = kw_next;
     }
 }
 
 template <typename T, typename C>
 __global__ void __launch_bounds__(CK_THREADS, sizeof(T) == 2 ? 4 : 3)
     k_ck_extract(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K, uint64_t nchunks,
-                 uint64_t ngroups, uint32_t parts, CkWS w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
+                 uint64_t ngroups, CkWS w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
                  const uint64_t *offset) {
-    __shared__ CkStage<T> stage[CK_THREADS / 32];
     if (*w.err_snap) return;
-    const uint64_t t = (uint64_t)blockIdx.x * (CK_THREADS / 32) + (threadIdx.x >> 5);
-    const uint64_t g = t / parts;
+    const uint64_t g = (uint64_t)blockIdx.x * (CK_THREADS / 32) + (threadIdx.x >> 5);
     if (g >= ngroups) return;
-    CkStage<T> &S = stage[threadIdx.x >> 5];
-    const uint32_t part = (uint32_t)(t % parts), cpp = CK_G / parts;
     const QP q = load_qp(sc);
     uint32_t err = 0;
     const uint64_t off0 = offset ? *offset : 0ull;
     if constexpr (sizeof(T) == 4) {
-        ck_task<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S);
+        ck_group<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err);
     } else {
         switch (qmode(q)) {   // uniform over the launch: one quantiser body per mode
-        case QM_POW2: ck_task<T, C, QM_POW2>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S); break;
-        case QM_INT: ck_task<T, C, QM_INT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S); break;
-        case QM_ONE: ck_task<T, C, QM_ONE>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S); break;
-        default: ck_task<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err, S); break;
+        case QM_POW2: ck_group<T, C, QM_POW2>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
+        case QM_INT: ck_group<T, C, QM_INT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
+        case QM_ONE: ck_group<T, C, QM_ONE>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
+        default: ck_group<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
         }
     }
     err = __reduce_or_sync(FULL, err);
@@ -477,20 +338,15 @@ cudaError_t launch_compact(const void *x, int dtype, uint64_t n, const uint32_t 
                                                                                   sc);
     cudaError_t e = scan_u32_u64(w.gcnt, w.goff, ngroups, w.scan_tmp, st);
     if (e != cudaSuccess) return e;
-    // warp tasks: a group, or a part of one when there are too few groups to fill the GPU
-    uint32_t parts = 1;
-    const uint64_t want = (uint64_t)num_sms() * 96;
-    while (parts < (uint32_t)CK_G && ngroups * parts < want) parts *= 2;
-    const uint64_t tasks = ngroups * parts;
-    const unsigned g2 = (unsigned)((tasks + wpc - 1) / wpc);
+    const unsigned g2 = (unsigned)((ngroups + wpc - 1) / wpc);
     if (g2) {
         if (dtype == ROIX_F32)
-            k_ck_extract<float, int32_t><<<g2, CK_THREADS, 0, st>>>((const float *)x, n, keep_bits, nchunks, ngroups,
-                                                                    parts, w, sc, (int32_t *)codes, capacity, offset);
+            k_ck_extract<float, int32_t><<<g2, CK_THREADS, 0, st>>>((const float *)x, n, keep_bits, nchunks, ngroups, w,
+                                                                    sc, (int32_t *)codes, capacity, offset);
         else
             k_ck_extract<uint16_t, uint16_t><<<g2, CK_THREADS, 0, st>>>((const uint16_t *)x, n, keep_bits, nchunks,
-                                                                        ngroups, parts, w, sc, (uint16_t *)codes,
-                                                                        capacity, offset);
+                                                                        ngroups, w, sc, (uint16_t *)codes, capacity,
+                                                                        offset);
     }
     k_ck_total<<<1, 1, 0, st>>>(scan_total_ptr(w.scan_tmp, ngroups), w.err_snap, sc);
     return cudaGetLastError();

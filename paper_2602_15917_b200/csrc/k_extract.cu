@@ -79,143 +79,6 @@ __global__ void __launch_bounds__(EX_THREADS) k_extract_count(const uint32_t *__
     }
 }
 
-// One tile = 256 mask words; warp w owns words 32w .. 32w+31 and lane l the word 32w + l, i.e. 32
-// consecutive voxels.  A lane loads only the 16-byte groups of its voxels with a kept bit, quantises
-// them branch-free, and writes its codes to the staging buffer at its position (the kept voxels of
-// the warps and words before it).  Groups are written in a lane-rotated order so the 16-byte shared
-// stores of neighbouring lanes (64 B / 128 B apart) hit different banks.
-template <typename T, typename C, int QM>
-__device__ __forceinline__ void extract_tile(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
-                                             const ExWS &w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
-                                             const uint64_t *offset, C *stage, uint32_t *warp_tot) {
-    constexpr int VPL = 16 / sizeof(T);   // voxels per 16-byte group
-    constexpr int NG = 32 / VPL;          // groups per mask word (u16 4, f32 8)
-    constexpr int PADE = 16 / sizeof(C);  // staging is shifted by base % PADE so that stores are 16-byte aligned
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    const uint64_t tile = blockIdx.x;
-    const uint64_t nwords = (n + 31) / 32;
-    if (w.toff[tile + 1] == w.toff[tile]) return;   // empty tile (background): nothing to load or store
-    const uint64_t wi = tile * EX_WORDS + warp * 32 + lane;
-    const uint32_t word = wi < nwords ? K[wi] : 0u;
-    const uint64_t v0 = wi * 32;            // first voxel of this lane's word
-    const bool full_word = v0 + 32 <= n;
-    // d[j] holds group (j + rot) % NG: the lane-rotated order (static register indices)
-    const int rot = (int)(sizeof(T) == 2 ? (lane >> 1) : lane);
-    uint4 d[NG];
-#pragma unroll
-    for (int j = 0; j < NG; j++) {
-        const int g = (j + rot) & (NG - 1);
-        d[j] = make_uint4(0, 0, 0, 0);
-        if (((word >> (g * VPL)) & ((1u << VPL) - 1u)) && full_word)
-            d[j] = __ldg(reinterpret_cast<const uint4 *>(x + v0) + g);
-    }
-    const uint32_t cnt = __popc(word);
-    const uint32_t incl = warp_incl_scan(cnt);
-    if (lane == 31) warp_tot[warp] = incl;
-    const uint64_t base = (offset ? *offset : 0) + w.toff[tile];
-    const uint32_t shift = (uint32_t)(base % PADE);
-    __syncthreads();
-    uint32_t wpre = 0, total = 0;
-#pragma unroll
-    for (int k = 0; k < EX_THREADS / 32; k++) {
-        uint32_t t = warp_tot[k];
-        if (k < (int)warp) wpre += t;
-        total += t;
-    }
-    const QP q = load_qp(sc);
-    uint32_t err = 0;
-    const uint32_t a0 = shift + wpre + incl - cnt;   // stage index of this lane's first code
-    if (word) {
-        if (full_word) {
-#pragma unroll
-            for (int j = 0; j < NG; j++) {
-                const int g = (j + rot) & (NG - 1);   // rotated order
-                const uint32_t mg = (word >> (g * VPL)) & ((1u << VPL) - 1u);
-                if (!mg) continue;
-                const uint32_t a = a0 + __popc(word & low_mask(g * VPL));
-                if constexpr (sizeof(T) == 2) {
-                    const uint32_t c0 = code_pair_u16_m<QM>(d[j].x, q, err), c1 = code_pair_u16_m<QM>(d[j].y, q, err),
-                                   c2 = code_pair_u16_m<QM>(d[j].z, q, err), c3 = code_pair_u16_m<QM>(d[j].w, q, err);
-                    if (mg == 0xffu) {
-                        // branch-free for either parity of a: the 8 codes shifted by (a & 1) halfwords
-                        // into the words of [a & ~1, a + 8); the two edge halfwords that belong to this
-                        // lane (not to its neighbours) are predicated stores
-                        const uint32_t odd = a & 1u, shb = odd * 16u, b = a >> 1;
-                        uint32_t *s32 = reinterpret_cast<uint32_t *>(stage) + b;
-                        const uint32_t t1 = __funnelshift_l(c0, c1, shb), t2 = __funnelshift_l(c1, c2, shb),
-                                       t3 = __funnelshift_l(c2, c3, shb);
-                        stage[2 * b + 1] = (C)((odd ? c0 : c0 >> 16) & 0xffffu);
-                        s32[1] = t1;
-                        s32[2] = t2;
-                        s32[3] = t3;
-                        if (!odd) stage[2 * b] = (C)(c0 & 0xffffu);
-                        else stage[2 * b + 8] = (C)(c3 >> 16);
-                    } else {
-                        const uint32_t cc[4] = {c0, c1, c2, c3};
-                        uint32_t pp = a;
-#pragma unroll
-                        for (int k = 0; k < 8; k++)
-                            if (mg >> k & 1) stage[pp++] = (C)((cc[k >> 1] >> ((k & 1) * 16)) & 0xffffu);
-                    }
-                } else {
-                    const int32_t k0 = code_f32(__uint_as_float(d[j].x), q, err), k1 = code_f32(__uint_as_float(d[j].y), q, err),
-                                  k2 = code_f32(__uint_as_float(d[j].z), q, err), k3 = code_f32(__uint_as_float(d[j].w), q, err);
-                    if (mg == 0xfu && (a & 3u) == 0) {
-                        *reinterpret_cast<int4 *>(stage + a) = make_int4(k0, k1, k2, k3);
-                    } else {
-                        const int32_t kk[4] = {k0, k1, k2, k3};
-                        uint32_t pp = a;
-#pragma unroll
-                        for (int k = 0; k < 4; k++)
-                            if (mg >> k & 1) stage[pp++] = (C)kk[k];
-                    }
-                }
-            }
-        } else {   // the volume's last, partial word
-            uint32_t pp = a0;
-            for (int k = 0; k < 32; k++)
-                if ((word >> k & 1) && v0 + k < n) {
-                    if constexpr (sizeof(T) == 2) stage[pp++] = (C)code_u16_m<QM>(x[v0 + k], q, err);
-                    else stage[pp++] = (C)code_f32(x[v0 + k], q, err);
-                }
-        }
-    }
-    if (base + total > capacity) err |= ROIX_ERR_CAPACITY;
-    if (err) set_err(sc, err);
-    __syncthreads();
-    // store [base, base + lim): scalar head up to the 16-byte boundary, 16-byte body, scalar tail
-    const uint64_t lim = base < capacity ? min((uint64_t)total, capacity - base) : 0;
-    const uint32_t head = (uint32_t)min((uint64_t)((PADE - shift) % PADE), lim);
-    const C *st = stage + shift;
-    if (threadIdx.x < head) out[base + threadIdx.x] = st[threadIdx.x];
-    const uint64_t nvec = (lim - head) / PADE;
-    const uint4 *sv = reinterpret_cast<const uint4 *>(st + head);   // 16-byte aligned: (shift + head) % PADE == 0
-    uint4 *ov = reinterpret_cast<uint4 *>(out + base + head);
-    for (uint64_t j = threadIdx.x; j < nvec; j += EX_THREADS) __stcs(ov + j, sv[j]);
-    for (uint64_t j = head + nvec * PADE + threadIdx.x; j < lim; j += EX_THREADS) out[base + j] = st[j];
-}
-
-template <typename T, typename C>
-__global__ void __launch_bounds__(EX_THREADS, sizeof(T) == 2 ? 6 : 4) k_extract(const T *__restrict__ x, uint64_t n, uint64_t ntiles,
-                                                        const uint32_t *__restrict__ K, ExWS w, roix_scalars *sc,
-                                                        C *__restrict__ out, uint64_t capacity, const uint64_t *offset) {
-    constexpr int PADE = 16 / sizeof(C);
-    __shared__ __align__(16) C stage[EX_TILE + 2 * PADE];
-    __shared__ uint32_t warp_tot[EX_THREADS / 32];
-    if (*w.err_snap) return;
-    const QP q = load_qp(sc);
-    if constexpr (sizeof(T) == 4) {
-        extract_tile<T, C, QM_FLOAT>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot);
-    } else {
-        switch (qmode(q)) {   // uniform over the launch: one code path per body
-        case QM_POW2: extract_tile<T, C, QM_POW2>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot); break;
-        case QM_INT: extract_tile<T, C, QM_INT>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot); break;
-        case QM_ONE: extract_tile<T, C, QM_ONE>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot); break;
-        default: extract_tile<T, C, QM_FLOAT>(x, n, K, w, sc, out, capacity, offset, stage, warp_tot); break;
-        }
-    }
-}
-
 // ------------------------------------------------------------- segment tiles (the default pass 2)
 // Per tile of 8192 voxels (one CTA, thread t <-> mask word t): the kept voxels form a few segments
 // (pieces of x-runs).  Their starts / ends come from the mask words (bit tricks, carries between words
@@ -398,18 +261,10 @@ size_t extract_workspace_bytes(uint64_t n) {
     return a > b ? a : b;
 }
 
-static bool legacy_extract() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("ROIX_EXTRACT_LEGACY");
-        v = e && e[0] == '1';
-    }
-    return v;
-}
-
 cudaError_t launch_extract(const void *x, int dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
                            void *codes, uint64_t capacity, const uint64_t *offset, void *ws, cudaStream_t st) {
-    if (!legacy_extract()) return launch_compact(x, dtype, n, keep_bits, sc, codes, capacity, offset, ws, st);
+    // u16: per-chunk warps (k_compact.cu); fp32: the segment tiles below (C2: 0.15 vs 0.36 ms)
+    if (dtype == ROIX_U16) return launch_compact(x, dtype, n, keep_bits, sc, codes, capacity, offset, ws, st);
     ExWS w;
     ex_carve(ws, n, &w);
     const uint64_t ntiles = (n + EX_TILE - 1) / EX_TILE;
@@ -418,14 +273,8 @@ cudaError_t launch_extract(const void *x, int dtype, uint64_t n, const uint32_t 
     k_extract_count<<<(unsigned)(need < cg ? (need ? need : 1) : cg), EX_THREADS, 0, st>>>(keep_bits, n, ntiles, w, sc);
     cudaError_t e = scan_u32_u64(w.tcount, w.toff, ntiles, w.scan_tmp, st);
     if (e != cudaSuccess) return e;
-    // u16: the per-word tiles (k_extract, 6.4 ms at C4 vs 13.8 for the segment tiles); fp32: the
-    // segment tiles (k_extract_seg, 144 vs 156 us at C2) -- measured on B200, DESIGN.md section 9
-    if (dtype == ROIX_U16)
-        k_extract<uint16_t, uint16_t><<<(unsigned)ntiles, EX_THREADS, 0, st>>>(
-            (const uint16_t *)x, n, ntiles, keep_bits, w, sc, (uint16_t *)codes, capacity, offset);
-    else
-        k_extract_seg<float, int32_t><<<(unsigned)ntiles, EX_THREADS, 0, st>>>(
-            (const float *)x, n, ntiles, keep_bits, w, sc, (int32_t *)codes, capacity, offset);
+    k_extract_seg<float, int32_t><<<(unsigned)ntiles, EX_THREADS, 0, st>>>((const float *)x, n, ntiles, keep_bits, w, sc,
+                                                                         (int32_t *)codes, capacity, offset);
     k_extract_total<<<1, 1, 0, st>>>(scan_total_ptr(w.scan_tmp, ntiles), w, sc);
     return cudaGetLastError();
 }
