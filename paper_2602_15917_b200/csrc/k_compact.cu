@@ -115,6 +115,37 @@ __device__ __forceinline__ uint4 shift_hw(const uint32_t (&W)[8], uint32_t sh) {
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
+// elements [VPG - d, 2 VPG - d) of (a, b) for a warp-uniform d in 1 .. VPG-1 (compile-time shifts)
+template <int SH>
+__device__ __forceinline__ uint4 shift_k(const uint4 &a, const uint4 &b) {   // SH halfwords, 1..7
+    const uint32_t W[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    constexpr int w0 = SH >> 1;
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) o[k] = (SH & 1) ? __funnelshift_r(W[w0 + k], W[w0 + k + 1], 16) : W[w0 + k];
+    return make_uint4(o[0], o[1], o[2], o[3]);
+}
+template <typename C>
+__device__ __forceinline__ uint4 shift_uniform(const uint4 &a, const uint4 &b, uint32_t d) {
+    if constexpr (sizeof(C) == 2) {
+        switch (d) {
+        case 1: return shift_k<7>(a, b);
+        case 2: return shift_k<6>(a, b);
+        case 3: return shift_k<5>(a, b);
+        case 4: return shift_k<4>(a, b);
+        case 5: return shift_k<3>(a, b);
+        case 6: return shift_k<2>(a, b);
+        default: return shift_k<1>(a, b);
+        }
+    } else {
+        switch (d) {
+        case 1: return shift_k<6>(a, b);
+        case 2: return shift_k<4>(a, b);
+        default: return shift_k<2>(a, b);
+        }
+    }
+}
+
 template <typename T>
 struct CkTraits;
 template <>
@@ -145,6 +176,54 @@ __device__ __forceinline__ uint32_t code_k(const uint4 &e, int k) {   // k stati
         return (k & 1) ? (wd >> 16) : (wd & 0xffffu);
     } else {
         return k == 0 ? e.x : k == 1 ? e.y : k == 2 ? e.z : e.w;
+    }
+}
+
+// A fully kept chunk (every voxel kept: the interior of long runs, most of C3 / C4): group g's codes
+// go to cbase + V g, one misalignment d for the whole chunk, so every aligned output vector is a fixed
+// shift of two neighbouring groups -- no flags, no scans; only the chunk's first and last vectors
+// (shared with the neighbouring chunks) go element by element.
+template <typename T, typename C, int QM>
+__device__ __noinline__ void ck_full(const T *__restrict__ x, uint64_t c, uint64_t cbase, C *__restrict__ out,
+                                     const QP q, uint32_t &err) {
+    constexpr int VPG = CkTraits<T>::VPG, J = CkTraits<T>::J;
+    const uint32_t lane = lane_id();
+    const uint64_t v0 = c * CK_VOX;
+    uint4 e[J];
+#pragma unroll
+    for (int j = 0; j < J; j++) e[j] = __ldcs(reinterpret_cast<const uint4 *>(x + v0 + (uint64_t)(32 * j + lane) * VPG));
+    const uint32_t d = (uint32_t)(cbase % VPG);
+    const uint64_t ab = cbase - d;
+#pragma unroll
+    for (int j = 0; j < J; j++) e[j] = quant16<T, QM>(e[j], q, err);
+#pragma unroll
+    for (int j = 0; j < J; j++) {
+        const uint32_t g = 32 * j + lane;
+        if (d == 0) {
+            __stcs(reinterpret_cast<uint4 *>(out + ab + (uint64_t)VPG * g), e[j]);
+            continue;
+        }
+        // the vector after group g's first code: g's last d codes, then g+1's first VPG - d
+        const uint4 ns = (lane == 0 && j + 1 < J) ? e[j + 1 < J ? j + 1 : j] : e[j];
+        uint4 ne;
+        ne.x = __shfl_sync(FULL, ns.x, (lane + 1) & 31);
+        ne.y = __shfl_sync(FULL, ns.y, (lane + 1) & 31);
+        ne.z = __shfl_sync(FULL, ns.z, (lane + 1) & 31);
+        ne.w = __shfl_sync(FULL, ns.w, (lane + 1) & 31);
+        if (!(lane == 31 && j == J - 1)) {
+            const uint32_t W8[8] = {e[j].x, e[j].y, e[j].z, e[j].w, ne.x, ne.y, ne.z, ne.w};
+            __stcs(reinterpret_cast<uint4 *>(out + ab + (uint64_t)VPG * (g + 1)),
+                   shift_hw(W8, (VPG - d) * (uint32_t)(sizeof(C) / 2)));
+        } else {   // the chunk's last group: its next group is in the next chunk
+#pragma unroll
+            for (int k = 0; k < VPG; k++)
+                if ((uint32_t)k >= VPG - d) out[ab + (uint64_t)VPG * g + d + k] = (C)code_k<C>(e[j], k);
+        }
+        if (g == 0) {   // the chunk's first vector: its first VPG - d codes
+#pragma unroll
+            for (int k = 0; k < VPG; k++)
+                if ((uint32_t)k < VPG - d) out[ab + d + k] = (C)code_k<C>(e[j], k);
+        }
     }
 }
 
@@ -285,7 +364,10 @@ __device__ __forceinline__ void ck_group(const T *__restrict__ x, uint64_t n, co
         const uint32_t kw_next = kn >= 0 ? ldk(kn) : 0u;   // in flight while this chunk is processed
         const uint64_t cbase = off0 + gbase + __shfl_sync(FULL, excl, k);
         const uint32_t ccount = __shfl_sync(FULL, cc, k);
-        ck_chunk<T, C, QM>(x, n, c0 + k, kw, cbase, ccount, out, capacity, q, err);
+        if (ccount == CK_VOX && (c0 + k + 1) * CK_VOX <= n && cbase + CK_VOX <= capacity)
+            ck_full<T, C, QM>(x, c0 + k, cbase, out, q, err);
+        else
+            ck_chunk<T, C, QM>(x, n, c0 + k, kw, cbase, ccount, out, capacity, q, err);
         k = kn;
         kw = kw_next;
     }

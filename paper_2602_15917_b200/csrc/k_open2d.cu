@@ -14,6 +14,7 @@
 //      atomics, no zeroing);
 //   4. per row (a warp per row): the x-run count (the fused first step of a6) and the first rs runs
 //      (x0, x1) as run records, by ballots over the row's words (runs are sparse).
+#include "async.cuh"
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -72,15 +73,32 @@ __global__ void __launch_bounds__(256) k_open2d_lin(O2L A, roix_scalars *sc) {
     uint32_t *M = smem;                       // absolute bits [MB, MB + 32 mw)
     uint32_t *E = M + A.mw + 2;               // [EB, EB + 32 ew)
     uint32_t *O = E + A.ew + 2;               // [B0 - 32, ...): O[0] is a zero guard, O[1 + k] = word B0/32 + k
-    const int64_t MB = ((B0 - 2 * X - 32) >> 5) << 5;   // floor to a word (arithmetic shift: may be negative)
+    const int64_t MB = ((B0 - 2 * X - 32) >> 7) << 7;   // floor to 16 bytes (arithmetic shift: may be negative)
     const int64_t EB = ((B0 - X - 32) >> 5) << 5;
-    // 1. m words (zero outside the slab; the masks never let those bits count)
+    // 1. m words: the part inside the slab by one bulk copy (TMA engine, mbarrier completion), the rest
+    // zero (the masks never let those bits count)
     {
-        const int64_t w0 = MB >> 5;
-        for (uint32_t k = threadIdx.x; k < A.mw + 2; k += blockDim.x) {
+        __shared__ uint64_t bar;
+        const int64_t w0 = MB >> 5;                                   // multiple of 4
+        const int64_t nw = (int64_t)A.mw + 2;
+        const int64_t lo = max(w0, (int64_t)0), hi = min(w0 + nw, (int64_t)((A.m_words + 3) & ~3ull));
+        const int64_t c0 = lo, c1 = lo + (((hi - lo) > 0 ? (hi - lo) : 0) & ~3ll);   // whole 16-byte units copied
+        for (int64_t k = threadIdx.x; k < nw; k += blockDim.x) {
             const int64_t wi = w0 + k;
-            M[k] = (wi >= 0 && (uint64_t)wi < A.m_words) ? __ldg(A.m + wi) : 0u;
+            if (wi < c0 || wi >= c1) M[k] = (wi >= 0 && (uint64_t)wi < A.m_words) ? __ldg(A.m + wi) : 0u;
         }
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            if (c1 > c0) {
+                mbar_arrive_expect_tx(&bar, (uint32_t)((c1 - c0) * 4));
+                bulk_g2s(M + (c0 - w0), A.m + c0, (uint32_t)((c1 - c0) * 4), &bar);
+            } else {
+                mbar_arrive(&bar);
+            }
+        }
+        __syncthreads();
+        mbar_wait(&bar, 0);
     }
     __syncthreads();
     // 2. erosion
@@ -193,7 +211,7 @@ cudaError_t launch_open2d_lin(const uint32_t *m, uint64_t m_words, const roix_ge
     A.R = (uint32_t)R;
     A.xmag = ceil_div_2_64(X);
     A.ymag = ceil_div_2_64(Y);
-    A.mw = (uint32_t)(((R + 4) * X + 160) / 32 + 2);
+    A.mw = (uint32_t)((((R + 4) * X + 288) / 32 + 2 + 3) & ~3ull);
     A.ew = (uint32_t)(((R + 2) * X + 160) / 32 + 2);
     A.ow = (uint32_t)((R * X + 31) / 32);
     A.row_runs = row_runs;
