@@ -336,6 +336,10 @@ __global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__res
         for (int q = 0; q < RR; q++) {
             const uint64_t r = r0 + q;
             const uint32_t b0 = row_off(q);
+            // a whole-warp segment skips rows without a run to extract (most rows of a sparse volume)
+            if constexpr (L == 32) {
+                if (r >= rows || row_off(q + 1) - b0 <= skip) continue;
+            }
             uint32_t left = __shfl_up_sync(FULL, wv[q][KW - 1], 1, L);
             uint32_t right = __shfl_down_sync(FULL, wv[q][0], 1, L);
             if (sl == 0) left = 0u;

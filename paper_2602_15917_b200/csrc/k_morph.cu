@@ -939,17 +939,6 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         const uint64_t tasks = per_chunk * chunks;
         k_open3d_reg<RY><<<(unsigned)((tasks + 7) / 8), 256, 0, st>>>(A, sc);
     } else {
-        // in-plane SE: the linear-word opening (k_open2d.cu) is opt-in (ROIX_OPEN2D_LIN=1) until it beats
-        // the row form below
-        static const bool use_lin = [] {
-            const char *v = getenv("ROIX_OPEN2D_LIN");
-            return v && v[0] == '1';
-        }();
-        if (use_lin) {
-            e = launch_open2d_lin(A.m, A.m_words, g, o_bits, row_runs, A.run_slots, A.rs, sc, st);
-            if (e != cudaErrorNotSupported) return e;
-            (void)cudaGetLastError();
-        }
         const int S = 8;
         size_t sm = (size_t)((S + 4) + (S + 2) + S) * A.WS * 4;
         if (sm > 220 * 1024) return cudaErrorInvalidConfiguration;

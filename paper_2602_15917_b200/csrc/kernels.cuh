@@ -37,8 +37,6 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
 cudaError_t launch_morph2d(const void *x, int dtype, const roix_geom &g, roix_scalars *sc, uint32_t *o_bits,
                            uint32_t *row_runs, uint2 *run_slots, uint32_t rs, const roix_frame *frames,
                            cudaStream_t st);
-cudaError_t launch_open2d_lin(const uint32_t *m, uint64_t m_words, const roix_geom &g, uint32_t *o_bits,
-                              uint32_t *row_runs, uint2 *run_slots, uint32_t rs, roix_scalars *sc, cudaStream_t st);
 cudaError_t launch_spec(const uint64_t *shist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st);
 size_t fused_workspace_bytes(const roix_geom &g);
 cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom &g, int polarity, roix_scalars *sc,
