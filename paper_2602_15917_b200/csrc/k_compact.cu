@@ -342,8 +342,9 @@ __device__ __forceinline__ void ck_chunk(const T *__restrict__ x, uint64_t n, ui
 
 template <typename T, typename C, int QM>
 __device__ __forceinline__ void ck_group(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K,
-                                         uint64_t nchunks, const CkWS &w, uint64_t g, uint64_t off0,
-                                         C *__restrict__ out, uint64_t capacity, const QP &q, uint32_t &err) {
+                                         uint64_t nchunks, const CkWS &w, uint64_t g, uint32_t part, uint32_t cpp,
+                                         uint64_t off0, C *__restrict__ out, uint64_t capacity, const QP &q,
+                                         uint32_t &err) {
     const uint64_t gbase = w.goff[g];
     if (w.goff[g + 1] == gbase) return;   // no kept voxel in 32 K voxels (background)
     const uint32_t lane = lane_id();
@@ -351,7 +352,10 @@ __device__ __forceinline__ void ck_group(const T *__restrict__ x, uint64_t n, co
     const uint64_t c0 = g * CK_G;
     const uint32_t cc = c0 + lane < nchunks ? (uint32_t)w.ccnt[c0 + lane] : 0u;
     const uint32_t excl = warp_incl_scan(cc) - cc;
-    uint32_t rem = __ballot_sync(FULL, cc != 0);
+    // this task's chunks: [part cpp, (part + 1) cpp) of the group (small volumes split groups)
+    const uint32_t pm = cpp >= 32 ? FULL : (((1u << cpp) - 1u) << (part * cpp));
+    uint32_t rem = __ballot_sync(FULL, cc != 0) & pm;
+    if (!rem) return;
     auto ldk = [&](int k) -> uint32_t {
         const uint64_t wi = (c0 + k) * CK_WORDS + lane;
         return wi < nwords ? __ldcs(K + wi) : 0u;
@@ -376,22 +380,24 @@ __device__ __forceinline__ void ck_group(const T *__restrict__ x, uint64_t n, co
 template <typename T, typename C>
 __global__ void __launch_bounds__(CK_THREADS, sizeof(T) == 2 ? 4 : 3)
     k_ck_extract(const T *__restrict__ x, uint64_t n, const uint32_t *__restrict__ K, uint64_t nchunks,
-                 uint64_t ngroups, CkWS w, roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
-                 const uint64_t *offset) {
+                 uint64_t ngroups, uint32_t parts, CkWS w, roix_scalars *sc, C *__restrict__ out,
+                 uint64_t capacity, const uint64_t *offset) {
     if (*w.err_snap) return;
-    const uint64_t g = (uint64_t)blockIdx.x * (CK_THREADS / 32) + (threadIdx.x >> 5);
+    const uint64_t t = (uint64_t)blockIdx.x * (CK_THREADS / 32) + (threadIdx.x >> 5);
+    const uint64_t g = t / parts;
     if (g >= ngroups) return;
+    const uint32_t part = (uint32_t)(t % parts), cpp = CK_G / parts;
     const QP q = load_qp(sc);
     uint32_t err = 0;
     const uint64_t off0 = offset ? *offset : 0ull;
     if constexpr (sizeof(T) == 4) {
-        ck_group<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err);
+        ck_group<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err);
     } else {
         switch (qmode(q)) {   // uniform over the launch: one quantiser body per mode
-        case QM_POW2: ck_group<T, C, QM_POW2>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
-        case QM_INT: ck_group<T, C, QM_INT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
-        case QM_ONE: ck_group<T, C, QM_ONE>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
-        default: ck_group<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, off0, out, capacity, q, err); break;
+        case QM_POW2: ck_group<T, C, QM_POW2>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
+        case QM_INT: ck_group<T, C, QM_INT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
+        case QM_ONE: ck_group<T, C, QM_ONE>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
+        default: ck_group<T, C, QM_FLOAT>(x, n, K, nchunks, w, g, part, cpp, off0, out, capacity, q, err); break;
         }
     }
     err = __reduce_or_sync(FULL, err);
@@ -420,15 +426,19 @@ cudaError_t launch_compact(const void *x, int dtype, uint64_t n, const uint32_t 
                                                                                   sc);
     cudaError_t e = scan_u32_u64(w.gcnt, w.goff, ngroups, w.scan_tmp, st);
     if (e != cudaSuccess) return e;
-    const unsigned g2 = (unsigned)((ngroups + wpc - 1) / wpc);
+    // warp tasks: a group, or a part of one when there are too few groups to fill the GPU
+    uint32_t parts = 1;
+    while (parts < (uint32_t)CK_G && ngroups * parts < (uint64_t)num_sms() * 64) parts *= 2;
+    const uint64_t tasks = ngroups * parts;
+    const unsigned g2 = (unsigned)((tasks + wpc - 1) / wpc);
     if (g2) {
         if (dtype == ROIX_F32)
-            k_ck_extract<float, int32_t><<<g2, CK_THREADS, 0, st>>>((const float *)x, n, keep_bits, nchunks, ngroups, w,
-                                                                    sc, (int32_t *)codes, capacity, offset);
+            k_ck_extract<float, int32_t><<<g2, CK_THREADS, 0, st>>>((const float *)x, n, keep_bits, nchunks, ngroups,
+                                                                    parts, w, sc, (int32_t *)codes, capacity, offset);
         else
             k_ck_extract<uint16_t, uint16_t><<<g2, CK_THREADS, 0, st>>>((const uint16_t *)x, n, keep_bits, nchunks,
-                                                                        ngroups, w, sc, (uint16_t *)codes, capacity,
-                                                                        offset);
+                                                                        ngroups, parts, w, sc, (uint16_t *)codes,
+                                                                        capacity, offset);
     }
     k_ck_total<<<1, 1, 0, st>>>(scan_total_ptr(w.scan_tmp, ngroups), w.err_snap, sc);
     return cudaGetLastError();

@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     const int warp = threadIdx.x >> 5;
     uint32_t *mring = smem;            // [MS][WS]
     uint32_t *ering = mring + MS * WS; // [ES][WS]
-    uint32_t *orow = ering + ES * WS;  // [S][WS]
+    uint32_t *orow = ering + ES * WS;  // [S + 1][WS]: ring of o rows (the previous step's last row stays)
     const int64_t Y = A.ny, X = A.nx;
     const int64_t rows = (int64_t)(A.nz * A.ny);
     const int64_t r0 = (int64_t)blockIdx.x * A.rows_per_cta;
@@ -718,7 +718,7 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
         mring[i * WS] = FULL;
         mring[i * WS + W + 1] = FULL;
     }
-    for (int i = threadIdx.x; i < (int)ES + S; i += blockDim.x) {   // e rows and o rows: zero pad words
+    for (int i = threadIdx.x; i < (int)ES + S + 1; i += blockDim.x) {   // e rows and o rows: zero pad words
         ering[i * WS] = 0;
         ering[i * WS + W + 1] = 0;
     }
@@ -760,7 +760,8 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
         __syncthreads();
         // o rows c0 .. c0+S-1 into orow, with run counts
         const int64_t r = c0 + warp;
-        uint32_t *od = orow + warp * WS + 1;
+        auto orow_of = [&](int64_t rr) { return orow + ((uint32_t)(rr - r0 + 1) % (uint32_t)(S + 1)) * WS + 1; };
+        uint32_t *od = orow_of(r);
         if (r < r1) {
             const int64_t y = r % Y;
             const uint32_t *c = erow(r);
@@ -788,21 +789,26 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
             }
         }
         __syncthreads();
-        // write row r (warp w) at global bit r X: the words wholly inside the row with plain stores, the
-        // (at most two) words it shares with its neighbour rows with atomicOr (o was zeroed when rows
-        // are not whole words)
+        // write row r (warp w) at global bit r X with plain stores, no zeroing: a word shared by two rows
+        // belongs to the later row, which takes the earlier row's tail bits from the o ring (the band
+        // starts and ends on word boundaries, so no word is shared between CTAs)
         if (r < r1) {
             const uint64_t Bg = (uint64_t)r * A.nx, Be = Bg + A.nx;
             const uint32_t sh = (uint32_t)(Bg & 31), esh = (uint32_t)(Be & 31);
             const uint64_t wf = Bg >> 5;
             const uint32_t nwo = (uint32_t)(((Be - 1) >> 5) - wf + 1);   // output words the row touches
+            const uint32_t nown = (esh == 0 || r + 1 == rows) ? nwo : nwo - 1;   // the last one: row r+1's
+            uint32_t tail = 0;   // row r-1's last sh bits (the low bits of word 0)
+            if (sh) {
+                const uint32_t *pr = orow_of(r - 1);
+                const uint32_t b = (uint32_t)(X - sh), a = b >> 5;
+                tail = __funnelshift_r(pr[a], pr[a + 1], b & 31) & low_mask(sh);
+            }
             uint32_t *dst = A.o + wf;
-            for (uint32_t j = lane_id(); j < nwo; j += 32) {
+            for (uint32_t j = lane_id(); j < nown; j += 32) {
                 // output word j = row bits [32 j - sh, 32 j - sh + 32)
-                const uint32_t val = sh == 0 ? od[j] : (j == 0 ? od[0] << sh : __funnelshift_r(od[j - 1], od[j], 32 - sh));
-                const bool whole = (j > 0 || sh == 0) && (j + 1 < nwo || esh == 0);
-                if (whole) dst[j] = val;
-                else if (val) atomicOr(&dst[j], val);
+                const uint32_t val = sh == 0 ? od[j] : (j == 0 ? (od[0] << sh) | tail : __funnelshift_r(od[j - 1], od[j], 32 - sh));
+                dst[j] = val;
             }
         }
         __syncthreads();
@@ -940,7 +946,7 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         k_open3d_reg<RY><<<(unsigned)((tasks + 7) / 8), 256, 0, st>>>(A, sc);
     } else {
         const int S = 8;
-        size_t sm = (size_t)((S + 4) + (S + 2) + S) * A.WS * 4;
+        size_t sm = (size_t)((S + 4) + (S + 2) + S + 1) * A.WS * 4;
         if (sm > 220 * 1024) return cudaErrorInvalidConfiguration;
         if ((e = set_smem(k_open2d, sm)) != cudaSuccess) return e;
         if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_open2d, 32 * S, sm)) != cudaSuccess) return e;
@@ -952,10 +958,6 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         rpc = (rpc + 31) / 32 * 32;
         A.rows_per_cta = rpc;
         uint64_t ctas = (rows + rpc - 1) / rpc;
-        // every row is whole words iff X is a multiple of 32; otherwise rows share their end words,
-        // which are OR-ed into a zeroed o
-        A.aligned_out = g.nx % 32 == 0;
-        if (!A.aligned_out && (e = cudaMemsetAsync(o_bits, 0, nwords * 4, st)) != cudaSuccess) return e;
         k_open2d<<<(unsigned)ctas, 32 * S, sm, st>>>(A, sc);
     }
     return cudaGetLastError();
