@@ -115,37 +115,6 @@ __device__ __forceinline__ uint4 shift_hw(const uint32_t (&W)[8], uint32_t sh) {
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-// elements [VPG - d, 2 VPG - d) of (a, b) for a warp-uniform d in 1 .. VPG-1 (compile-time shifts)
-template <int SH>
-__device__ __forceinline__ uint4 shift_k(const uint4 &a, const uint4 &b) {   // SH halfwords, 1..7
-    const uint32_t W[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    constexpr int w0 = SH >> 1;
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; k++) o[k] = (SH & 1) ? __funnelshift_r(W[w0 + k], W[w0 + k + 1], 16) : W[w0 + k];
-    return make_uint4(o[0], o[1], o[2], o[3]);
-}
-template <typename C>
-__device__ __forceinline__ uint4 shift_uniform(const uint4 &a, const uint4 &b, uint32_t d) {
-    if constexpr (sizeof(C) == 2) {
-        switch (d) {
-        case 1: return shift_k<7>(a, b);
-        case 2: return shift_k<6>(a, b);
-        case 3: return shift_k<5>(a, b);
-        case 4: return shift_k<4>(a, b);
-        case 5: return shift_k<3>(a, b);
-        case 6: return shift_k<2>(a, b);
-        default: return shift_k<1>(a, b);
-        }
-    } else {
-        switch (d) {
-        case 1: return shift_k<6>(a, b);
-        case 2: return shift_k<4>(a, b);
-        default: return shift_k<2>(a, b);
-        }
-    }
-}
-
 template <typename T>
 struct CkTraits;
 template <>

@@ -797,14 +797,22 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
             const uint32_t sh = (uint32_t)(Bg & 31), esh = (uint32_t)(Be & 31);
             const uint64_t wf = Bg >> 5;
             const uint32_t nwo = (uint32_t)(((Be - 1) >> 5) - wf + 1);   // output words the row touches
-            const uint32_t nown = (esh == 0 || r + 1 == rows) ? nwo : nwo - 1;   // the last one: row r+1's
+            uint32_t *dst = A.o + wf;
+            if (X < 32) {   // a word may hold several short rows: OR the shared words into a zeroed o
+                for (uint32_t j = lane_id(); j < nwo; j += 32) {
+                    const uint32_t val = sh == 0 ? od[j] : (j == 0 ? od[0] << sh : __funnelshift_r(od[j - 1], od[j], 32 - sh));
+                    const bool whole = (j > 0 || sh == 0) && (j + 1 < nwo || esh == 0);
+                    if (whole) dst[j] = val;
+                    else if (val) atomicOr(&dst[j], val);
+                }
+            }
+            const uint32_t nown = X < 32 ? 0u : (esh == 0 || r + 1 == rows) ? nwo : nwo - 1;   // the last: row r+1's
             uint32_t tail = 0;   // row r-1's last sh bits (the low bits of word 0)
-            if (sh) {
+            if (sh && nown) {
                 const uint32_t *pr = orow_of(r - 1);
                 const uint32_t b = (uint32_t)(X - sh), a = b >> 5;
                 tail = __funnelshift_r(pr[a], pr[a + 1], b & 31) & low_mask(sh);
             }
-            uint32_t *dst = A.o + wf;
             for (uint32_t j = lane_id(); j < nown; j += 32) {
                 // output word j = row bits [32 j - sh, 32 j - sh + 32)
                 const uint32_t val = sh == 0 ? od[j] : (j == 0 ? (od[0] << sh) | tail : __funnelshift_r(od[j - 1], od[j], 32 - sh));
@@ -876,14 +884,6 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     A.m_words = nwords;
     cudaError_t e;
     // in-plane SE: binarise + open in one pass over x (m stays on chip)
-    // the fused one-pass form (k_morph2d) measured slower than binarise + k_open2d on C3 (12.9 vs 9.3 ms:
-    // it is instruction-bound); opt in with ROIX_MORPH2D=1
-    static const bool use_m2d = [] {
-        const char *e = getenv("ROIX_MORPH2D");
-        return e && e[0] == '1';
-    }();
-    if (use_m2d && se == 4 && !prebinarized && g.nx >= 32)
-        return launch_morph2d(x, dtype, g, sc, o_bits, row_runs, A.run_slots, A.rs, frames, st);
     // a4: stream x -> m (after a fused speculative pass: resolve its window, binarise only on a miss)
     if (prebinarized && (e = launch_spec_resolve(x, dtype, g, sc, ws, st)) != cudaSuccess) return e;
     {
@@ -958,6 +958,7 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         rpc = (rpc + 31) / 32 * 32;
         A.rows_per_cta = rpc;
         uint64_t ctas = (rows + rpc - 1) / rpc;
+        if (g.nx < 32 && (e = cudaMemsetAsync(o_bits, 0, nwords * 4, st)) != cudaSuccess) return e;
         k_open2d<<<(unsigned)ctas, 32 * S, sm, st>>>(A, sc);
     }
     return cudaGetLastError();

@@ -34,9 +34,7 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
                          const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs, void *ws,
                          int prebinarized, cudaStream_t st, const roix_frame *frames = nullptr,
                          uint2 *run_slots = nullptr, uint32_t rs = 0);
-cudaError_t launch_morph2d(const void *x, int dtype, const roix_geom &g, roix_scalars *sc, uint32_t *o_bits,
-                           uint32_t *row_runs, uint2 *run_slots, uint32_t rs, const roix_frame *frames,
-                           cudaStream_t st);
+
 cudaError_t launch_spec(const uint64_t *shist, int dtype, int polarity, roix_scalars *sc, cudaStream_t st);
 size_t fused_workspace_bytes(const roix_geom &g);
 cudaError_t launch_histogram_binarize(const void *x, int dtype, const roix_geom &g, int polarity, roix_scalars *sc,
@@ -74,9 +72,7 @@ cudaError_t launch_label_boundary_roots(const void *ws, const roix_geom &g, uint
                                         uint64_t *sizes, uint64_t out_cap, uint64_t *count, roix_scalars *sc,
                                         cudaStream_t st);
 
-cudaError_t launch_gather(const void *x, int dtype, uint64_t nx, const RunsView &R, uint64_t cap, uint32_t *klen,
-                          uint64_t *koff, uint64_t *scan_tmp, roix_scalars *sc, void *codes,
-                          uint64_t capacity, const uint64_t *offset, cudaStream_t st);
+
 uint64_t runx_task_entries(uint64_t n);
 cudaError_t launch_runx(const void *x, int dtype, uint64_t nx, const RunsView &R, uint64_t cap, uint32_t *klen,
                         uint64_t *koff, uint64_t *scan_tmp, uint32_t *task_run, roix_scalars *sc, void *codes,

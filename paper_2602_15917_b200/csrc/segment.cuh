@@ -45,28 +45,9 @@ __device__ __forceinline__ uint4 code_group(uint4 v, const QP &q, uint32_t &err)
     }
 }
 
-constexpr int GT_CW = 8;                       // consumer warps
-constexpr int GT_S = 4;                        // ring stages = producer warps (warp GT_CW + s fills stage s)
-constexpr int GT_THREADS = 32 * (GT_CW + GT_S);
-constexpr int GT_GPT = 4;                      // groups per consumer thread per chunk
-constexpr int GT_RBS = 96;                     // non-empty runs per chunk on the bulk path
-constexpr uint32_t GT_XB = 16384 + 32 * GT_RBS;   // staged x bytes per stage (alignment slack per run)
 
-template <typename T>
-__host__ __device__ constexpr uint64_t gt_ch() { return (uint64_t)32 * GT_CW * GT_GPT * gr_v<T>(); }   // 16 KB of x
 
-struct GtStage {
-    uint64_t jc, je, rb, re;   // chunk outputs [jc, je); runs rb..re touch it
-    uint32_t n, slow;          // table entries; 1: direct path
-};
 
-struct GtSmem {
-    uint4 x[GT_S][GT_XB / 16];
-    uint32_t rlo[GT_S][GT_RBS + 1];   // entry k: outputs [jc + rlo[k], jc + rlo[k+1]) of one run
-    uint32_t sidx[GT_S][GT_RBS];      // shared-memory element index of output jc + rlo[k]
-    GtStage hdr[GT_S];
-    uint64_t full[GT_S], empty[GT_S];
-};
 
 
 // One warp: codes of x[src0, src0 + len) into out[dst0, dst0 + len); positions >= cap are not
