@@ -292,6 +292,7 @@ class Pipeline:
         k += 1 if self.bg_ref is not None else 0
         k += sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
                                        "extract" if self.extract == "mask" else "extract_runs"))
+        k += 1 if self.rs else 0          # k_runs_slots (the opening's run records)
         return k + (LAUNCHES["range"] if self.cdtype == L.F32 else 0)
 
     def scalars(self):
