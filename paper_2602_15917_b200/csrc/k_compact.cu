@@ -115,20 +115,6 @@ __device__ __forceinline__ uint4 shift_hw(const uint32_t (&W)[8], uint32_t sh) {
     return make_uint4(o[0], o[1], o[2], o[3]);
 }
 
-// code k (runtime, 0 <= k < codes per 16-byte group) of a 16-byte group of codes
-template <typename C>
-__device__ __forceinline__ uint32_t code_at(const uint4 &e, uint32_t k) {
-    if constexpr (sizeof(C) == 2) {
-        const uint32_t h = k >> 1;
-        const uint32_t lo = h & 1u ? e.y : e.x, hi = h & 1u ? e.w : e.z;
-        const uint32_t wd = h & 2u ? hi : lo;
-        return (wd >> ((k & 1u) * 16u)) & 0xffffu;
-    } else {
-        const uint32_t lo = k & 1u ? e.y : e.x, hi = k & 1u ? e.w : e.z;
-        return k & 2u ? hi : lo;
-    }
-}
-
 template <typename T>
 struct CkTraits;
 template <>
@@ -312,11 +298,13 @@ __device__ __forceinline__ void ck_chunk(const T *__restrict__ x, uint64_t n, ui
         } else {
             em = m;
         }
-        // element by element: only over the set bits (a run end holds a few)
-        for (uint32_t mm = em; mm; mm &= mm - 1) {
-            const uint32_t k = __ffs(mm) - 1;
-            const uint64_t dst = P + __popc(m & ((1u << k) - 1u));
-            if (dst < capacity) out[dst] = (C)code_at<C>(e[j], k);
+        if (em) {
+#pragma unroll
+            for (int k = 0; k < VPG; k++) {
+                if (!((em >> k) & 1u)) continue;
+                const uint64_t dst = P + __popc(m & ((1u << k) - 1u));
+                if (dst < capacity) out[dst] = (C)code_k<C>(e[j], k);
+            }
         }
     }
 }
