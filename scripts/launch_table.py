@@ -10,12 +10,14 @@ for r in rows[1:]:
     k = (int(d["ID"]), d["Kernel Name"].split("(")[0].replace("void ", "").replace("roix::", "")[:34])
     if k not in data:
         order.append(k)
-    data.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"])
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
+             "msecond": 1e6}.get(d.get("Metric Unit", ""), 1)
+    data.setdefault(k, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * scale
 starts = [i for i, k in enumerate(order) if "k_scalars_init" in k[1]]
 which = int(sys.argv[2]) if len(sys.argv) > 2 else -2
 s0 = starts[which]
 s1 = starts[which + 1] if which + 1 < len(starts) and which != -1 else len(order)
-ends = [i for i in range(s0, s1) if "k_extract_total" in order[i][1]]
+ends = [i for i in range(s0, s1) if any(t in order[i][1] for t in ("k_extract_total", "k_ck_total", "k_gather_total"))]
 s1 = ends[0] + 1 if ends else s1
 tot = 0
 for k in order[s0:s1]:
