@@ -823,6 +823,192 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
     }
 }
 
+// ------------------------------------------------------- 2-D opening, register rows (32 <= X < 16 K)
+// One warp per range of consecutive rows [ra, rb) of the slab (ra, rb multiples of 32, so row ra starts
+// on a word boundary and no output word is shared between warps); the whole row is in registers: lane
+// l holds words k = l + 32 j (j < J, W + 1 <= 32 J), so every global load and store is coalesced and
+// no shared memory or block barrier is involved.  The warp marches along the rows keeping m of rows
+// s-2, s-1, s and e of rows s-3, s-2, s-1; x-neighbour words come from the adjacent lane (one shfl per
+// word and direction; lane 0 / 31 take the previous / next chunk's).  In-plane borders: erosion takes
+// a missing row or word as all ones, dilation as all zeros (G-11), so rows of other planes are never
+// read.  The output row (X bits at bit p X) is written as whole words: the word shared with the next
+// row is held in a register and completed by that row.  Each row also gets its run count and, if it
+// has at most rs runs, its run records (a6 reads them instead of the mask).
+template <int J>
+struct RowRegs {
+    uint32_t w[J];
+};
+
+// word k-1 of every word k (lane 0 of chunk j: lane 31 of chunk j - 1; word -1 = edge)
+template <int J>
+__device__ __forceinline__ void words_left(const uint32_t (&c)[J], uint32_t (&out)[J], uint32_t edge, uint32_t src) {
+    uint32_t rot[J];
+#pragma unroll
+    for (int j = 0; j < J; j++) rot[j] = __shfl_sync(FULL, c[j], src);
+    const bool l0 = lane_id() == 0;
+#pragma unroll
+    for (int j = 0; j < J; j++) out[j] = l0 ? (j ? rot[j - 1] : edge) : rot[j];
+}
+// word k+1 of every word k (lane 31 of chunk j: lane 0 of chunk j + 1; past the last chunk = edge)
+template <int J>
+__device__ __forceinline__ void words_right(const uint32_t (&c)[J], uint32_t (&out)[J], uint32_t edge, uint32_t src) {
+    uint32_t rot[J];
+#pragma unroll
+    for (int j = 0; j < J; j++) rot[j] = __shfl_sync(FULL, c[j], src);
+    const bool l31 = lane_id() == 31;
+#pragma unroll
+    for (int j = 0; j < J; j++) out[j] = l31 ? (j + 1 < J ? rot[j + 1] : edge) : rot[j];
+}
+
+// run records of one chunk's start / end bits (at most one per lane: ballot ranks; else lane by lane)
+__device__ __forceinline__ void emit_bits(uint32_t bits, uint32_t kbase, uint32_t &base, uint32_t *dst, bool multi) {
+    const uint32_t lane = lane_id();
+    const uint32_t b = __ballot_sync(FULL, bits != 0);
+    if (!b) return;
+    if (!multi) {
+        if (bits) dst[2 * (base + __popc(b & ((1u << lane) - 1u)))] = kbase + __ffs(bits) - 1;
+        base += __popc(b);
+        return;
+    }
+    uint32_t c = __popc(bits), inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, inc, d);
+        if (lane >= d) inc += v;
+    }
+    uint32_t i = base + inc - c;
+    for (uint32_t m = bits; m; m &= m - 1) dst[2 * i++] = kbase + __ffs(m) - 1;
+    base += __shfl_sync(FULL, inc, 31);
+}
+
+template <int J>
+__global__ void __launch_bounds__(128) k_open2d_w(MorphArgs A, roix_scalars *sc) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = A.rs;   // read by a6 after this launch
+    if (get_err(sc)) return;
+    const uint32_t lane = lane_id();
+    const int64_t rows = (int64_t)(A.nz * A.ny);
+    const uint64_t X = A.nx, Y = A.ny;
+    const uint32_t W = A.W;
+    const uint32_t tail = (uint32_t)(X - 32ull * (W - 1));
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t ra = (int64_t)(gw * A.rows_per_cta), rb = min(rows, ra + (int64_t)A.rows_per_cta);
+    if (ra >= rb) return;
+    const uint32_t sl = (lane + 31) & 31, sr = (lane + 1) & 31;
+    // pad of word k: m pads are ones (erosion border), e / o pads zeros
+    auto padm = [&](int j) -> uint32_t {
+        const uint32_t k = lane + 32 * j;
+        return k >= W ? FULL : (k == W - 1 && tail < 32) ? ~low_mask(tail) : 0u;
+    };
+    uint32_t raw[J], m0[J], m1[J], m2[J], e0[J], e1[J], e2[J];
+    auto issue = [&](int64_t s) {   // raw words of m row s (one coalesced load per chunk)
+        if (s < 0 || s >= rows) return;
+        const uint32_t *src = A.m + (((uint64_t)s * X) >> 5);
+#pragma unroll
+        for (int j = 0; j < J; j++) {
+            const uint32_t k = lane + 32 * j;
+            if (k <= W) raw[j] = __ldg(src + k);
+        }
+    };
+#pragma unroll
+    for (int j = 0; j < J; j++) m0[j] = m1[j] = raw[j] = FULL, e0[j] = e1[j] = 0u;
+    uint64_t ys = (uint64_t)((ra - 2 + 2 * (int64_t)Y) % (int64_t)Y);   // plane row of s (valid for s >= 0)
+    uint32_t carry = 0;
+    issue(ra - 2);
+#pragma unroll 1
+    for (int64_t s = ra - 2; s <= rb + 1; s++) {
+        // m row s from the raw words (funnel with the next word: the next lane's)
+        {
+            uint32_t nx[J];
+            words_right<J>(raw, nx, 0u, sr);
+            const uint32_t sh = s >= 0 ? (uint32_t)(((uint64_t)s * X) & 31) : 0u;
+            const bool valid = s >= 0 && s < rows;
+#pragma unroll
+            for (int j = 0; j < J; j++) m2[j] = valid ? (__funnelshift_r(raw[j], nx[j], sh) | padm(j)) : FULL;
+        }
+        issue(s + 1);
+        // e row q = s - 1 from m rows s-2, s-1, s (plane borders: the missing row is all ones)
+        const uint64_t yq = ys == 0 ? Y - 1 : ys - 1;
+        {
+            uint32_t lw[J], rw[J];
+            words_left<J>(m1, lw, FULL, sl);
+            words_right<J>(m1, rw, FULL, sr);
+            const bool top = yq == 0, bot = yq == Y - 1;
+#pragma unroll
+            for (int j = 0; j < J; j++) {
+                const uint32_t c = m1[j];
+                uint32_t v = c & __funnelshift_l(lw[j], c, 1) & __funnelshift_r(c, rw[j], 1);
+                v &= (top ? FULL : m0[j]) & (bot ? FULL : m2[j]);
+                e2[j] = v & ~padm(j);
+            }
+        }
+        // o row p = s - 2 from e rows s-3, s-2, s-1 (plane borders: the missing row is all zeros)
+        const int64_t p = s - 2;
+        if (p >= ra) {
+            const uint64_t yp = yq == 0 ? Y - 1 : yq - 1;
+            uint32_t o[J], ol[J];
+            {
+                uint32_t lw[J], rw[J];
+                words_left<J>(e1, lw, 0u, sl);
+                words_right<J>(e1, rw, 0u, sr);
+                const bool top = yp == 0, bot = yp == Y - 1;
+#pragma unroll
+                for (int j = 0; j < J; j++) {
+                    const uint32_t c = e1[j];
+                    uint32_t v = c | __funnelshift_l(lw[j], c, 1) | __funnelshift_r(c, rw[j], 1);
+                    v |= (top ? 0u : e0[j]) | (bot ? 0u : e2[j]);
+                    o[j] = v & ~padm(j);
+                }
+            }
+            words_left<J>(o, ol, 0u, sl);
+            // store: output word t = row bits [32 t - sh, 32 t - sh + 32) at global word wf + t
+            const uint64_t B = (uint64_t)p * X, Be = B + X;
+            const uint32_t sh = (uint32_t)(B & 31), esh = (uint32_t)(Be & 31);
+            const uint64_t wf = B >> 5;
+            const uint32_t nwo = (uint32_t)(((Be - 1) >> 5) - wf + 1);
+            const bool defer = esh != 0 && p + 1 < rows;   // the last word is completed by row p + 1
+            const uint32_t nst = defer ? nwo - 1 : nwo, tl = nwo - 1;
+            uint32_t *dst = A.o + wf;
+            uint32_t cv = 0, runs = 0;
+#pragma unroll
+            for (int j = 0; j < J; j++) {
+                const uint32_t t = lane + 32 * j;
+                uint32_t val = __funnelshift_l(ol[j], o[j], sh);
+                if (t == 0) val |= carry;
+                if (t < nst) dst[t] = val;
+                if (t == tl) cv = val;
+                runs += __popc(o[j] & ~((o[j] << 1) | (ol[j] >> 31)));
+            }
+            carry = defer ? __shfl_sync(FULL, cv, tl & 31) : 0u;
+            if (A.row_runs) {
+                runs = __reduce_add_sync(FULL, runs);
+                if (lane == 0) A.row_runs[p] = runs;
+                if (A.rs && runs && runs <= A.rs) {
+                    uint32_t *slot = reinterpret_cast<uint32_t *>(A.run_slots + (uint64_t)p * A.rs);
+                    uint32_t bs = 0, be = 0;
+#pragma unroll
+                    for (int j = 0; j < J; j++) {
+                        const uint32_t b1 = (o[j] << 1) | (ol[j] >> 31);
+                        const uint32_t st = o[j] & ~b1, en = ~o[j] & b1;
+                        if (!__any_sync(FULL, (st | en) != 0)) continue;
+                        const bool multi = __any_sync(FULL, (st & (st - 1)) | (en & (en - 1)));
+                        const uint32_t kb = 32 * (lane + 32 * j);
+                        emit_bits(st, kb, bs, slot, multi);
+                        emit_bits(en, kb, be, slot + 1, multi);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < J; j++) {
+            m0[j] = m1[j];
+            m1[j] = m2[j];
+            e0[j] = e1[j];
+            e1[j] = e2[j];
+        }
+        ys = ys + 1 == Y ? 0 : ys + 1;
+    }
+}
+
 // ------------------------------------------------------------------ halo planes: m packed per plane
 template <typename T>
 __global__ void __launch_bounds__(256) k_binarize_planes(const T *__restrict__ x, MorphArgs A, uint64_t p0,
@@ -944,6 +1130,27 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         if (row_runs && (e = cudaMemsetAsync(row_runs, 0, g.nz * g.ny * 4, st)) != cudaSuccess) return e;
         const uint64_t tasks = per_chunk * chunks;
         k_open3d_reg<RY><<<(unsigned)((tasks + 7) / 8), 256, 0, st>>>(A, sc);
+    } else if (g.nx >= 32 && A.W + 1 <= 32 * 16) {
+        // register rows: one warp per range of rows, one wave of resident warps
+        const uint32_t J = (A.W + 1 + 31) / 32;
+        const void *fn = nullptr;
+        switch (J) {
+#define ROIX_O2W(JJ) \
+    case JJ: fn = (const void *)k_open2d_w<JJ>; break;
+        ROIX_O2W(1) ROIX_O2W(2) ROIX_O2W(3) ROIX_O2W(4) ROIX_O2W(5) ROIX_O2W(6) ROIX_O2W(7) ROIX_O2W(8)
+        ROIX_O2W(9) ROIX_O2W(10) ROIX_O2W(11) ROIX_O2W(12) ROIX_O2W(13) ROIX_O2W(14) ROIX_O2W(15) ROIX_O2W(16)
+#undef ROIX_O2W
+        default: return cudaErrorInvalidConfiguration;
+        }
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, 0)) != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        const uint64_t rows = g.nz * g.ny, warps = (uint64_t)num_sms() * occ * 4;
+        uint64_t rpw = (rows + warps - 1) / warps;
+        rpw = (rpw + 31) / 32 * 32;   // every warp's rows start on a word boundary
+        A.rows_per_cta = rpw;
+        const uint64_t nw = (rows + rpw - 1) / rpw;
+        void *args[] = {&A, &sc};
+        return cudaLaunchKernel(fn, dim3((unsigned)((nw + 3) / 4)), dim3(128), args, 0, st);
     } else {
         const int S = 8;
         size_t sm = (size_t)((S + 4) + (S + 2) + S + 1) * A.WS * 4;

@@ -322,7 +322,10 @@ MORPH_SHAPES = [(1, 1, 1), (1, 1, 40), (2, 3, 5), (3, 5, 7), (5, 33, 65), (7, 64
                 (5, 17, 768), (9, 40, 512), (3, 3, 1024), (130, 5, 256),
                 # whole-row 3-D kernel (X % 32 == 0, W = X/32 a power of two <= 128): every segment width,
                 # ragged row tiles, several z-chunks
-                (17, 13, 128), (19, 7, 2048), (3, 5, 4096), (20, 37, 512), (18, 11, 64), (40, 3, 32)]
+                (17, 13, 128), (19, 7, 2048), (3, 5, 4096), (20, 37, 512), (18, 11, 64), (40, 3, 32),
+                # in-plane register-row kernel (32 <= X, W + 1 <= 512 words): C3's row width, the widest
+                # row it takes, the first it leaves to the shared-memory kernel, rows of one word + 1 bit
+                (2, 9, 13900), (2, 3, 16352), (2, 3, 16353), (4, 7, 33), (3, 4, 31)]
 
 
 def _morph_gpu(x_np, thr, pol, se):
@@ -377,6 +380,69 @@ def test_morph_random_masks(shape, se, dt):
         if n % 32:
             assert w[n // 32] >> (n % 32) == 0           # pad bits zero (G-16)
         np.testing.assert_array_equal(runs.cpu().numpy(), _runs_per_row(ref))
+
+
+def _crosses(rng, shape, per_row):
+    """Planes of isolated 3x3 crosses (each survives the opening whole) -- rows with a few short runs,
+    several of them inside one 32-bit word -- over a dense random band (rows with many runs)."""
+    Z, Y, X = shape
+    m = np.zeros(shape, bool)
+    for z in range(Z):
+        for _ in range(max(1, int(per_row * Y / 3))):
+            y, x = rng.integers(1, Y - 1), rng.integers(1, X - 1)
+            m[z, y - 1:y + 2, x] = True
+            m[z, y, x - 1:x + 2] = True
+        m[z, : Y // 4] |= rng.random((Y // 4, X)) < 0.8
+    return m
+
+
+@pytest.mark.parametrize("shape", [(2, 12, 13900), (3, 20, 1390), (4, 12, 33), (2, 8, 16352), (3, 11, 64),
+                                   (2, 10, 100), (2, 9, 16400), (3, 8, 20)])
+def test_morph_run_slots_vs_oracle(shape):
+    """roix_morph_slots (se = 4): row_runs of every row and, for rows with 1..32 runs, the run records
+    (x0, x1 exclusive) against the runs of the oracle's opening -- register-row kernel (X >= 32,
+    W + 1 <= 512), shared-memory kernel (W >= 512) and rows shorter than a word."""
+    rng = np.random.default_rng(sum(shape))
+    Z, Y, X = shape
+    rs = 32
+    for per_row in (0.5, 4.0, 12.0):
+        m = _crosses(rng, shape, per_row)
+        x_np = np.where(m, 3000, 100).astype(np.uint16)
+        ref = oracle.opening(m.astype(np.uint8), 4).astype(bool)
+        x = dev(x_np)
+        sc = new_sc(1.0)
+        s = read_sc(sc)
+        s.thr_u16 = 1000
+        write_sc(sc, s)
+        n = x_np.size
+        o = torch.full(((n + 31) // 32 + 4,), -1, dtype=torch.int32, device="cuda")
+        runs = torch.full((Z * Y,), -1, dtype=torch.int32, device="cuda")
+        slots = torch.full((Z * Y * rs * 2,), -1, dtype=torch.int32, device="cuda")
+        g = L.Geom(Z, Y, X, 0, Z)
+        ws = torch.empty(L.roix_morph_workspace(g), dtype=torch.uint8, device="cuda")
+        L.roix_morph_slots(ptr(x), L.U16, ctypes.byref(g), 4, None, None, ptr(sc), ptr(o), ptr(runs), ptr(slots),
+                           rs, ptr(ws), ws.numel(), st())
+        sv = read_sc(sc)
+        assert sv.err == 0
+        np.testing.assert_array_equal(words_to_mask(o, n).reshape(shape), ref)
+        got_runs = runs.cpu().numpy()
+        np.testing.assert_array_equal(got_runs, _runs_per_row(ref))
+        if sv.run_slots == 0:                     # the kernel wrote no records (X < 32 path)
+            continue
+        assert sv.run_slots == rs
+        sl = slots.cpu().numpy().view(np.uint32).reshape(Z * Y, rs, 2)
+        rows = ref.reshape(Z * Y, X).astype(np.int8)
+        checked = 0
+        for r in range(Z * Y):
+            k = got_runs[r]
+            if not 0 < k <= rs:
+                continue
+            d = np.diff(np.concatenate([[0], rows[r], [0]]))
+            x0, x1 = np.nonzero(d == 1)[0], np.nonzero(d == -1)[0]
+            np.testing.assert_array_equal(sl[r, :k, 0], x0)
+            np.testing.assert_array_equal(sl[r, :k, 1], x1)
+            checked += 1
+        assert checked > 0
 
 
 def test_binarize_planes_halo_layout():
