@@ -827,139 +827,97 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
 // One warp per range of consecutive rows [ra, rb) of the slab (ra, rb multiples of 32, so row ra starts
 // on a word boundary and no output word is shared between warps); the whole row is in registers: lane
 // l holds words k = l + 32 j (j < J, W + 1 <= 32 J), so every global load and store is coalesced and
-// no shared memory or block barrier is involved.  The warp marches along the rows keeping m of rows
-// s-2, s-1, s and e of rows s-3, s-2, s-1; x-neighbour words come from the adjacent lane (one shfl per
-// word and direction; lane 0 / 31 take the previous / next chunk's).  In-plane borders: erosion takes
-// a missing row or word as all ones, dilation as all zeros (G-11), so rows of other planes are never
-// read.  The output row (X bits at bit p X) is written as whole words: the word shared with the next
-// row is held in a register and completed by that row.  Each row also gets its run count and, if it
-// has at most rs runs, its run records (a6 reads them instead of the mask).
+// no block barrier is involved.  The warp marches along the rows keeping m of rows s-2, s-1, s and e
+// of rows s-3, s-2, s-1; x-neighbour words come from the adjacent lane (one shfl per word and
+// direction; lane 0 / 31 take the previous / next chunk's).  In-plane borders: erosion takes a missing
+// row or word as all ones, dilation as all zeros (G-11), so rows of other planes are never read (the
+// rows past the slab ends are never used unsubstituted).  The output row (X bits at bit p X) is written
+// as whole words: the word shared with the next row is held in a register and completed by that row.
+// Each row also gets its run count and, if it has 1..rs runs, its run records (a6 reads them instead
+// of the mask): the row goes through a per-warp shared-memory copy so that the record pass is a short
+// loop, not J unrolled copies.
+// Since 32 (J - 1) <= W < 32 J, only the last two chunks hold pad words (k >= W - 1).
 template <int J>
-struct RowRegs {
-    uint32_t w[J];
-};
-
-// word k-1 of every word k (lane 0 of chunk j: lane 31 of chunk j - 1; word -1 = edge)
-template <int J>
-__device__ __forceinline__ void words_left(const uint32_t (&c)[J], uint32_t (&out)[J], uint32_t edge, uint32_t src) {
-    uint32_t rot[J];
-#pragma unroll
-    for (int j = 0; j < J; j++) rot[j] = __shfl_sync(FULL, c[j], src);
-    const bool l0 = lane_id() == 0;
-#pragma unroll
-    for (int j = 0; j < J; j++) out[j] = l0 ? (j ? rot[j - 1] : edge) : rot[j];
-}
-// word k+1 of every word k (lane 31 of chunk j: lane 0 of chunk j + 1; past the last chunk = edge)
-template <int J>
-__device__ __forceinline__ void words_right(const uint32_t (&c)[J], uint32_t (&out)[J], uint32_t edge, uint32_t src) {
-    uint32_t rot[J];
-#pragma unroll
-    for (int j = 0; j < J; j++) rot[j] = __shfl_sync(FULL, c[j], src);
-    const bool l31 = lane_id() == 31;
-#pragma unroll
-    for (int j = 0; j < J; j++) out[j] = l31 ? (j + 1 < J ? rot[j + 1] : edge) : rot[j];
-}
-
-// run records of one chunk's start / end bits (at most one per lane: ballot ranks; else lane by lane)
-__device__ __forceinline__ void emit_bits(uint32_t bits, uint32_t kbase, uint32_t &base, uint32_t *dst, bool multi) {
-    const uint32_t lane = lane_id();
-    const uint32_t b = __ballot_sync(FULL, bits != 0);
-    if (!b) return;
-    if (!multi) {
-        if (bits) dst[2 * (base + __popc(b & ((1u << lane) - 1u)))] = kbase + __ffs(bits) - 1;
-        base += __popc(b);
-        return;
-    }
-    uint32_t c = __popc(bits), inc = c;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t v = __shfl_up_sync(FULL, inc, d);
-        if (lane >= d) inc += v;
-    }
-    uint32_t i = base + inc - c;
-    for (uint32_t m = bits; m; m &= m - 1) dst[2 * i++] = kbase + __ffs(m) - 1;
-    base += __shfl_sync(FULL, inc, 31);
-}
-
-template <int J>
-__global__ void __launch_bounds__(128) k_open2d_w(MorphArgs A, roix_scalars *sc) {
+__global__ void __launch_bounds__(128, J <= 14 ? 4 : 3) k_open2d_w(MorphArgs A, roix_scalars *sc) {
+    __shared__ uint32_t orow_all[4][32 * J + 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = A.rs;   // read by a6 after this launch
     if (get_err(sc)) return;
     const uint32_t lane = lane_id();
     const int64_t rows = (int64_t)(A.nz * A.ny);
     const uint64_t X = A.nx, Y = A.ny;
     const uint32_t W = A.W;
-    const uint32_t tail = (uint32_t)(X - 32ull * (W - 1));
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t ra = (int64_t)(gw * A.rows_per_cta), rb = min(rows, ra + (int64_t)A.rows_per_cta);
     if (ra >= rb) return;
+    uint32_t *orow = orow_all[threadIdx.x >> 5];
     const uint32_t sl = (lane + 31) & 31, sr = (lane + 1) & 31;
-    // pad of word k: m pads are ones (erosion border), e / o pads zeros
-    auto padm = [&](int j) -> uint32_t {
-        const uint32_t k = lane + 32 * j;
-        return k >= W ? FULL : (k == W - 1 && tail < 32) ? ~low_mask(tail) : 0u;
-    };
+    const bool l0 = lane == 0, l31 = lane == 31;
+    // m pads (ones past X) of the last two chunks; e / o take the complement as a keep mask
+    uint32_t padA, padB;
+    {
+        const uint32_t tail = (uint32_t)(X - 32ull * (W - 1));
+        auto pad = [&](uint32_t k) { return k >= W ? FULL : (k == W - 1 && tail < 32) ? ~low_mask(tail) : 0u; };
+        padA = J >= 2 ? pad(lane + 32 * (J - 2)) : 0u;
+        padB = pad(lane + 32 * (J - 1));
+    }
+    auto padm = [&](int j) -> uint32_t { return j == J - 1 ? padB : j == J - 2 ? padA : 0u; };
     uint32_t raw[J], m0[J], m1[J], m2[J], e0[J], e1[J], e2[J];
-    auto issue = [&](int64_t s) {   // raw words of m row s (one coalesced load per chunk)
+    auto issue = [&](int64_t s) {   // raw words k <= W of m row s (one coalesced load per chunk)
         if (s < 0 || s >= rows) return;
         const uint32_t *src = A.m + (((uint64_t)s * X) >> 5);
 #pragma unroll
         for (int j = 0; j < J; j++) {
             const uint32_t k = lane + 32 * j;
-            if (k <= W) raw[j] = __ldg(src + k);
+            if (j + 2 < J || k <= W) raw[j] = __ldg(src + k);
         }
     };
 #pragma unroll
-    for (int j = 0; j < J; j++) m0[j] = m1[j] = raw[j] = FULL, e0[j] = e1[j] = 0u;
+    for (int j = 0; j < J; j++) raw[j] = m0[j] = m1[j] = FULL, e0[j] = e1[j] = 0u;
     uint64_t ys = (uint64_t)((ra - 2 + 2 * (int64_t)Y) % (int64_t)Y);   // plane row of s (valid for s >= 0)
     uint32_t carry = 0;
     issue(ra - 2);
 #pragma unroll 1
     for (int64_t s = ra - 2; s <= rb + 1; s++) {
-        // m row s from the raw words (funnel with the next word: the next lane's)
+        // m row s: funnel of the raw word and the next (the next lane's)
         {
-            uint32_t nx[J];
-            words_right<J>(raw, nx, 0u, sr);
             const uint32_t sh = s >= 0 ? (uint32_t)(((uint64_t)s * X) & 31) : 0u;
-            const bool valid = s >= 0 && s < rows;
+            uint32_t nxt = __shfl_sync(FULL, raw[0], sr);
 #pragma unroll
-            for (int j = 0; j < J; j++) m2[j] = valid ? (__funnelshift_r(raw[j], nx[j], sh) | padm(j)) : FULL;
+            for (int j = 0; j < J; j++) {
+                const uint32_t cur = nxt;
+                if (j + 1 < J) nxt = __shfl_sync(FULL, raw[j + 1], sr);
+                const uint32_t nx = l31 ? (j + 1 < J ? nxt : 0u) : cur;
+                m2[j] = __funnelshift_r(raw[j], nx, sh) | padm(j);
+            }
         }
         issue(s + 1);
         // e row q = s - 1 from m rows s-2, s-1, s (plane borders: the missing row is all ones)
         const uint64_t yq = ys == 0 ? Y - 1 : ys - 1;
         {
-            uint32_t lw[J], rw[J];
-            words_left<J>(m1, lw, FULL, sl);
-            words_right<J>(m1, rw, FULL, sr);
-            const bool top = yq == 0, bot = yq == Y - 1;
+            const uint32_t tm = yq == 0 ? FULL : 0u, bm = yq == Y - 1 ? FULL : 0u;
+            uint32_t lrot = __shfl_sync(FULL, m1[0], sl), rrot = __shfl_sync(FULL, m1[0], sr), prevl = FULL;
 #pragma unroll
             for (int j = 0; j < J; j++) {
                 const uint32_t c = m1[j];
-                uint32_t v = c & __funnelshift_l(lw[j], c, 1) & __funnelshift_r(c, rw[j], 1);
-                v &= (top ? FULL : m0[j]) & (bot ? FULL : m2[j]);
-                e2[j] = v & ~padm(j);
+                const uint32_t lw = l0 ? prevl : lrot;
+                prevl = lrot;
+                uint32_t rw = rrot;
+                if (j + 1 < J) {
+                    lrot = __shfl_sync(FULL, m1[j + 1], sl);
+                    rrot = __shfl_sync(FULL, m1[j + 1], sr);
+                    if (l31) rw = rrot;
+                } else if (l31) {
+                    rw = FULL;
+                }
+                const uint32_t v = c & __funnelshift_l(lw, c, 1) & __funnelshift_r(c, rw, 1);
+                e2[j] = v & (m0[j] | tm) & (m2[j] | bm) & ~padm(j);
             }
         }
         // o row p = s - 2 from e rows s-3, s-2, s-1 (plane borders: the missing row is all zeros)
         const int64_t p = s - 2;
         if (p >= ra) {
             const uint64_t yp = yq == 0 ? Y - 1 : yq - 1;
-            uint32_t o[J], ol[J];
-            {
-                uint32_t lw[J], rw[J];
-                words_left<J>(e1, lw, 0u, sl);
-                words_right<J>(e1, rw, 0u, sr);
-                const bool top = yp == 0, bot = yp == Y - 1;
-#pragma unroll
-                for (int j = 0; j < J; j++) {
-                    const uint32_t c = e1[j];
-                    uint32_t v = c | __funnelshift_l(lw[j], c, 1) | __funnelshift_r(c, rw[j], 1);
-                    v |= (top ? 0u : e0[j]) | (bot ? 0u : e2[j]);
-                    o[j] = v & ~padm(j);
-                }
-            }
-            words_left<J>(o, ol, 0u, sl);
+            const uint32_t tk = yp == 0 ? 0u : FULL, bk = yp == Y - 1 ? 0u : FULL;
             // store: output word t = row bits [32 t - sh, 32 t - sh + 32) at global word wf + t
             const uint64_t B = (uint64_t)p * X, Be = B + X;
             const uint32_t sh = (uint32_t)(B & 31), esh = (uint32_t)(Be & 31);
@@ -968,33 +926,72 @@ __global__ void __launch_bounds__(128) k_open2d_w(MorphArgs A, roix_scalars *sc)
             const bool defer = esh != 0 && p + 1 < rows;   // the last word is completed by row p + 1
             const uint32_t nst = defer ? nwo - 1 : nwo, tl = nwo - 1;
             uint32_t *dst = A.o + wf;
+            uint32_t o[J];
             uint32_t cv = 0, runs = 0;
+            uint32_t lrot = __shfl_sync(FULL, e1[0], sl), rrot = __shfl_sync(FULL, e1[0], sr), prevl = 0u;
+            uint32_t prevo = 0u;   // lane 31's o word of the previous chunk
 #pragma unroll
             for (int j = 0; j < J; j++) {
+                const uint32_t c = e1[j];
+                const uint32_t lw = l0 ? prevl : lrot;
+                prevl = lrot;
+                uint32_t rw = rrot;
+                if (j + 1 < J) {
+                    lrot = __shfl_sync(FULL, e1[j + 1], sl);
+                    rrot = __shfl_sync(FULL, e1[j + 1], sr);
+                    if (l31) rw = rrot;
+                } else if (l31) {
+                    rw = 0u;
+                }
+                uint32_t v = c | __funnelshift_l(lw, c, 1) | __funnelshift_r(c, rw, 1) | (e0[j] & tk) | (e2[j] & bk);
+                v &= ~padm(j);
+                o[j] = v;
+                const uint32_t orot = __shfl_sync(FULL, v, sl);
+                const uint32_t ol = l0 ? prevo : orot;
+                prevo = orot;
                 const uint32_t t = lane + 32 * j;
-                uint32_t val = __funnelshift_l(ol[j], o[j], sh);
-                if (t == 0) val |= carry;
+                uint32_t val = __funnelshift_l(ol, v, sh);
+                if (j == 0 && t == 0) val |= carry;
                 if (t < nst) dst[t] = val;
-                if (t == tl) cv = val;
-                runs += __popc(o[j] & ~((o[j] << 1) | (ol[j] >> 31)));
+                if (j + 2 >= J && t == tl) cv = val;
+                runs += __popc(v & ~((v << 1) | (ol >> 31)));
             }
             carry = defer ? __shfl_sync(FULL, cv, tl & 31) : 0u;
             if (A.row_runs) {
                 runs = __reduce_add_sync(FULL, runs);
                 if (lane == 0) A.row_runs[p] = runs;
                 if (A.rs && runs && runs <= A.rs) {
-                    uint32_t *slot = reinterpret_cast<uint32_t *>(A.run_slots + (uint64_t)p * A.rs);
-                    uint32_t bs = 0, be = 0;
+                    // run records from a shared-memory copy of the row (words 0 .. W; word W is 0)
 #pragma unroll
-                    for (int j = 0; j < J; j++) {
-                        const uint32_t b1 = (o[j] << 1) | (ol[j] >> 31);
-                        const uint32_t st = o[j] & ~b1, en = ~o[j] & b1;
+                    for (int j = 0; j < J; j++) orow[lane + 32 * j] = o[j];
+                    __syncwarp();
+                    uint32_t *slot = reinterpret_cast<uint32_t *>(A.run_slots + (uint64_t)p * A.rs);
+                    const uint32_t lt = (1u << lane) - 1u;
+                    uint32_t bs = 0, be = 0;
+                    for (uint32_t k0 = 0; k0 <= W; k0 += 32) {
+                        const uint32_t k = k0 + lane;
+                        const uint32_t w = orow[k], pw = k ? orow[k - 1] : 0u;
+                        const uint32_t b1 = (w << 1) | (pw >> 31);
+                        const uint32_t st = w & ~b1, en = ~w & b1;
                         if (!__any_sync(FULL, (st | en) != 0)) continue;
-                        const bool multi = __any_sync(FULL, (st & (st - 1)) | (en & (en - 1)));
-                        const uint32_t kb = 32 * (lane + 32 * j);
-                        emit_bits(st, kb, bs, slot, multi);
-                        emit_bits(en, kb, be, slot + 1, multi);
+                        const uint32_t cs = __popc(st), ce = __popc(en);
+                        const uint32_t cmax = __reduce_max_sync(FULL, max(cs, ce));
+                        uint32_t ps = 0, pe = 0, ts = 0, te = 0;   // earlier lanes' records, all lanes'
+                        for (uint32_t i = 1; i <= cmax; i++) {
+                            const uint32_t b_s = __ballot_sync(FULL, cs >= i), b_e = __ballot_sync(FULL, ce >= i);
+                            ps += __popc(b_s & lt);
+                            pe += __popc(b_e & lt);
+                            ts += __popc(b_s);
+                            te += __popc(b_e);
+                        }
+                        uint32_t i = bs + ps;
+                        for (uint32_t mm = st; mm; mm &= mm - 1) slot[2 * i++] = 32 * k + __ffs(mm) - 1;
+                        i = be + pe;
+                        for (uint32_t mm = en; mm; mm &= mm - 1) slot[2 * i++ + 1] = 32 * k + __ffs(mm) - 1;
+                        bs += ts;
+                        be += te;
                     }
+                    __syncwarp();
                 }
             }
         }
