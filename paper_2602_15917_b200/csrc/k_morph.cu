@@ -833,13 +833,15 @@ __global__ void __launch_bounds__(256) k_open2d(MorphArgs A, roix_scalars *sc) {
 // row or word as all ones, dilation as all zeros (G-11), so rows of other planes are never read (the
 // rows past the slab ends are never used unsubstituted).  The output row (X bits at bit p X) is written
 // as whole words: the word shared with the next row is held in a register and completed by that row.
-// Each row also gets its run count and, if it has 1..rs runs, its run records (a6 reads them instead
-// of the mask): the row goes through a per-warp shared-memory copy so that the record pass is a short
-// loop, not J unrolled copies.
+// Each row also gets its run count and its first rs run records (a6 reads them instead of the mask for
+// rows with at most rs runs).
 // Since 32 (J - 1) <= W < 32 J, only the last two chunks hold pad words (k >= W - 1).
+//
+// Chunks where some word holds two starts or two ends are recorded after the row (their start / end
+// bits and running counts parked in shared memory): ranks from ballots of the per-lane counts
+// (count >= i for i = 1 .. max), then each lane writes its own bits in order.
 template <int J>
 __global__ void __launch_bounds__(128, J <= 14 ? 4 : 3) k_open2d_w(MorphArgs A, roix_scalars *sc) {
-    __shared__ uint32_t orow_all[4][32 * J + 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) sc->run_slots = A.rs;   // read by a6 after this launch
     if (get_err(sc)) return;
     const uint32_t lane = lane_id();
@@ -849,9 +851,14 @@ __global__ void __launch_bounds__(128, J <= 14 ? 4 : 3) k_open2d_w(MorphArgs A, 
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t ra = (int64_t)(gw * A.rows_per_cta), rb = min(rows, ra + (int64_t)A.rows_per_cta);
     if (ra >= rb) return;
-    uint32_t *orow = orow_all[threadIdx.x >> 5];
     const uint32_t sl = (lane + 31) & 31, sr = (lane + 1) & 31;
     const bool l0 = lane == 0, l31 = lane == 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t rsl = A.row_runs ? A.rs : 0u;   // run records per row (0: none)
+    __shared__ uint32_t park[4][2 * 32 * J];
+    __shared__ uint2 park_base[4][J];
+    uint32_t *const pst = park[threadIdx.x >> 5], *const pen = pst + 32 * J;
+    uint2 *const pbase = park_base[threadIdx.x >> 5];
     // m pads (ones past X) of the last two chunks; e / o take the complement as a keep mask
     uint32_t padA, padB;
     {
@@ -926,8 +933,10 @@ __global__ void __launch_bounds__(128, J <= 14 ? 4 : 3) k_open2d_w(MorphArgs A, 
             const bool defer = esh != 0 && p + 1 < rows;   // the last word is completed by row p + 1
             const uint32_t nst = defer ? nwo - 1 : nwo, tl = nwo - 1;
             uint32_t *dst = A.o + wf;
-            uint32_t o[J];
-            uint32_t cv = 0, runs = 0;
+            uint32_t cv = 0;
+            uint32_t bs = 0, be = 0;   // starts / ends of the row so far (warp-uniform)
+            uint32_t multi = 0;        // chunks parked for the multi-bit record pass
+            uint32_t *slot = rsl ? reinterpret_cast<uint32_t *>(A.run_slots + (uint64_t)p * rsl) : nullptr;
             uint32_t lrot = __shfl_sync(FULL, e1[0], sl), rrot = __shfl_sync(FULL, e1[0], sr), prevl = 0u;
             uint32_t prevo = 0u;   // lane 31's o word of the previous chunk
 #pragma unroll
@@ -945,7 +954,6 @@ __global__ void __launch_bounds__(128, J <= 14 ? 4 : 3) k_open2d_w(MorphArgs A, 
                 }
                 uint32_t v = c | __funnelshift_l(lw, c, 1) | __funnelshift_r(c, rw, 1) | (e0[j] & tk) | (e2[j] & bk);
                 v &= ~padm(j);
-                o[j] = v;
                 const uint32_t orot = __shfl_sync(FULL, v, sl);
                 const uint32_t ol = l0 ? prevo : orot;
                 prevo = orot;
@@ -954,45 +962,51 @@ __global__ void __launch_bounds__(128, J <= 14 ? 4 : 3) k_open2d_w(MorphArgs A, 
                 if (j == 0 && t == 0) val |= carry;
                 if (t < nst) dst[t] = val;
                 if (j + 2 >= J && t == tl) cv = val;
-                runs += __popc(v & ~((v << 1) | (ol >> 31)));
+                // run starts / exclusive ends of the chunk: records (speculative: the row may turn out
+                // to have more than rs runs, then a6 ignores them) and the running counts
+                const uint32_t b1 = (v << 1) | (ol >> 31);
+                const uint32_t st = v & ~b1, en = ~v & b1;
+                if (__any_sync(FULL, (st | en) != 0)) {
+                    if (__any_sync(FULL, (st & (st - 1)) | (en & (en - 1)))) {
+                        pst[t] = st;
+                        pen[t] = en;
+                        if (lane == 0) pbase[j] = make_uint2(bs, be);
+                        multi |= 1u << j;
+                        bs += __reduce_add_sync(FULL, __popc(st));
+                        be += __reduce_add_sync(FULL, __popc(en));
+                    } else {
+                        const uint32_t bS = __ballot_sync(FULL, st != 0), bE = __ballot_sync(FULL, en != 0);
+                        if (slot) {
+                            const uint32_t is = bs + __popc(bS & lt), ie = be + __popc(bE & lt);
+                            if (st && is < rsl) slot[2 * is] = 32 * t + __ffs(st) - 1;
+                            if (en && ie < rsl) slot[2 * ie + 1] = 32 * t + __ffs(en) - 1;
+                        }
+                        bs += __popc(bS);
+                        be += __popc(bE);
+                    }
+                }
             }
             carry = defer ? __shfl_sync(FULL, cv, tl & 31) : 0u;
-            if (A.row_runs) {
-                runs = __reduce_add_sync(FULL, runs);
-                if (lane == 0) A.row_runs[p] = runs;
-                if (A.rs && runs && runs <= A.rs) {
-                    // run records from a shared-memory copy of the row (words 0 .. W; word W is 0)
-#pragma unroll
-                    for (int j = 0; j < J; j++) orow[lane + 32 * j] = o[j];
-                    __syncwarp();
-                    uint32_t *slot = reinterpret_cast<uint32_t *>(A.run_slots + (uint64_t)p * A.rs);
-                    const uint32_t lt = (1u << lane) - 1u;
-                    uint32_t bs = 0, be = 0;
-                    for (uint32_t k0 = 0; k0 <= W; k0 += 32) {
-                        const uint32_t k = k0 + lane;
-                        const uint32_t w = orow[k], pw = k ? orow[k - 1] : 0u;
-                        const uint32_t b1 = (w << 1) | (pw >> 31);
-                        const uint32_t st = w & ~b1, en = ~w & b1;
-                        if (!__any_sync(FULL, (st | en) != 0)) continue;
-                        const uint32_t cs = __popc(st), ce = __popc(en);
-                        const uint32_t cmax = __reduce_max_sync(FULL, max(cs, ce));
-                        uint32_t ps = 0, pe = 0, ts = 0, te = 0;   // earlier lanes' records, all lanes'
-                        for (uint32_t i = 1; i <= cmax; i++) {
-                            const uint32_t b_s = __ballot_sync(FULL, cs >= i), b_e = __ballot_sync(FULL, ce >= i);
-                            ps += __popc(b_s & lt);
-                            pe += __popc(b_e & lt);
-                            ts += __popc(b_s);
-                            te += __popc(b_e);
-                        }
-                        uint32_t i = bs + ps;
-                        for (uint32_t mm = st; mm; mm &= mm - 1) slot[2 * i++] = 32 * k + __ffs(mm) - 1;
-                        i = be + pe;
-                        for (uint32_t mm = en; mm; mm &= mm - 1) slot[2 * i++ + 1] = 32 * k + __ffs(mm) - 1;
-                        bs += ts;
-                        be += te;
+            if (A.row_runs && lane == 0) A.row_runs[p] = bs;
+            if (multi && slot && bs <= rsl) {   // rows with more runs than records never use them
+                __syncwarp();
+                for (uint32_t mk = multi; mk; mk &= mk - 1) {
+                    const uint32_t j = __ffs(mk) - 1, t = lane + 32 * j;
+                    const uint32_t st = pst[t], en = pen[t];
+                    const uint2 base = pbase[j];
+                    const uint32_t cs = __popc(st), ce = __popc(en);
+                    const uint32_t cmax = __reduce_max_sync(FULL, max(cs, ce));
+                    uint32_t ps = 0, pe = 0;
+                    for (uint32_t i = 1; i <= cmax; i++) {
+                        ps += __popc(__ballot_sync(FULL, cs >= i) & lt);
+                        pe += __popc(__ballot_sync(FULL, ce >= i) & lt);
                     }
-                    __syncwarp();
+                    uint32_t i = base.x + ps;
+                    for (uint32_t mm = st; mm && i < rsl; mm &= mm - 1) slot[2 * i++] = 32 * t + __ffs(mm) - 1;
+                    i = base.y + pe;
+                    for (uint32_t mm = en; mm && i < rsl; mm &= mm - 1) slot[2 * i++ + 1] = 32 * t + __ffs(mm) - 1;
                 }
+                __syncwarp();
             }
         }
 #pragma unroll
