@@ -204,11 +204,14 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
             uint32_t carry[RIF], sb[RIF], eb[RIF], b0[RIF];
             bool live[RIF];
 #pragma unroll
+            bool any = false;
             for (int q = 0; q < RIF; q++) {
                 b0[q] = __shfl_sync(FULL, off, q);
                 live[q] = r0 + q < rows && __shfl_sync(FULL, off, q + 1) - b0[q] > skip;
                 carry[q] = sb[q] = eb[q] = 0;
+                any |= live[q];
             }
+            if (!any) continue;   // every row of the group empty or taken from the run records
             for (uint32_t k0 = 0; k0 < G.W; k0 += 32) {
                 uint32_t cw[RIF], nx[RIF];
 #pragma unroll
@@ -253,22 +256,46 @@ __global__ void __launch_bounds__(256) k_extract_runs(const uint32_t *__restrict
 
 // Rows with at most rs runs: their run records, written by roix_morph_slots with o (the opening
 // already had every row in registers), are copied to their scanned place -- those rows of o are not
-// read again.  A thread per row.
+// read again.  A warp per 32 rows: the rows with records are taken two at a time (both rows' record
+// loads in flight before either is stored), lanes over the records (coalesced loads and stores).
 __global__ void __launch_bounds__(256) k_runs_slots(LGeo G, LabelWS W, const uint2 *__restrict__ slots, uint32_t rs,
                                                     const uint64_t *total, uint64_t cap, roix_scalars *sc) {
     if (get_err(sc)) return;
     if (!runs_total(total, cap, W, sc)) return;
     if (sc->run_slots != rs) return;   // the opening did not write run records of this width
     const uint64_t rows = G.nz * G.ny;
-    for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t a = W.row_start[r], c = W.row_start[r + 1] - a;
-        if (c == 0 || c > rs) continue;
-        const uint2 *s = slots + r * rs;
-        for (uint32_t i = 0; i < c; i++) {
-            const uint2 v = s[i];
-            W.x0[a + i] = v.x;
-            W.x1[a + i] = v.y;
-            W.rrow[a + i] = (uint32_t)r;
+    const uint32_t lane = lane_id();
+    const uint64_t ng = (rows + 31) / 32, wstride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gi < ng; gi += wstride) {
+        const uint64_t r = gi * 32 + lane;
+        uint32_t a = 0, c = 0;
+        if (r < rows) {
+            a = W.row_start[r];
+            c = W.row_start[r + 1] - a;
+        }
+        uint32_t use = __ballot_sync(FULL, c > 0 && c <= rs);
+        while (use) {
+            const uint32_t q0 = __ffs(use) - 1;
+            use &= use - 1;
+            const uint32_t q1 = use ? __ffs(use) - 1 : 32u;
+            if (use) use &= use - 1;
+            const uint32_t a0 = __shfl_sync(FULL, a, q0), c0 = __shfl_sync(FULL, c, q0);
+            const uint32_t a1 = __shfl_sync(FULL, a, q1 & 31), c1 = q1 < 32 ? __shfl_sync(FULL, c, q1 & 31) : 0u;
+            for (uint32_t i = lane; i < max(c0, c1); i += 32) {
+                uint2 v0 = make_uint2(0, 0), v1 = make_uint2(0, 0);
+                if (i < c0) v0 = slots[(gi * 32 + q0) * rs + i];
+                if (i < c1) v1 = slots[(gi * 32 + q1) * rs + i];
+                if (i < c0) {
+                    W.x0[a0 + i] = v0.x;
+                    W.x1[a0 + i] = v0.y;
+                    W.rrow[a0 + i] = (uint32_t)(gi * 32 + q0);
+                }
+                if (i < c1) {
+                    W.x0[a1 + i] = v1.x;
+                    W.x1[a1 + i] = v1.y;
+                    W.rrow[a1 + i] = (uint32_t)(gi * 32 + q1);
+                }
+            }
         }
     }
 }
