@@ -41,6 +41,11 @@ class Result:
     scalars: L.Scalars
 
 
+# run records per row the in-plane opening writes (roix_morph_slots, 1..64; C3 step time measured the
+# same for 32, 48 and 64: fewer rows left to a6's mask reader, more record writes in the opening)
+RUN_SLOTS = 32
+
+
 class Pipeline:
     """Preallocated buffers + the enqueue sequence for volumes of one shape / dtype / parameter set."""
 
@@ -95,10 +100,10 @@ class Pipeline:
         self.frame_thr = torch.zeros(4 * max(Z, 1), dtype=torch.int32, device=dev) if frames else None   # roix_frame
         self.o = torch.empty(self.nwords + 4, dtype=torch.int32, device=dev)   # o, then K in place
         self.row_runs = torch.empty(Z * Y, dtype=torch.int32, device=dev)
-        # run records of every row (x0, x1) written by the opening for rows of <= RS runs, so a6 does
+        # run records of every row (x0, x1) written by the opening for rows of <= rs runs, so a6 does
         # not re-read those rows of o (roix_morph_slots / roix_label_slots)
         # (only the in-plane opening writes them; C3 rows hold ~11 runs on average: noise specks)
-        self.rs = 32 if (X >= 64 and se == 4) else 0
+        self.rs = RUN_SLOTS if (X >= 64 and se == 4) else 0
         self.run_slots = torch.empty(max(1, Z * Y * self.rs * 2), dtype=torch.int32, device=dev) if self.rs else None
         # fused (speculative) histogram + binarisation: one read of x for a2 + a4 (roix_histogram_binarize);
         # off by default: on B200 the histogram pass is bound by shared-memory atomics, and the fused pass

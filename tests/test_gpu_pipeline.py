@@ -87,7 +87,7 @@ def test_pipeline_run_slots_vs_oracle(shape, conn, se):
     """The in-plane opening's run records (roix_morph_slots, 32 per row) feed a6 for rows with <= 32
     runs; rows with more are re-read from o (the 3-D openings write none: a6 reads o).  Two-level volumes with random masks of several densities give rows
     of every run count on both sides of 8, in one volume; every artefact against the oracle."""
-    from paper_2602_15917_b200.pipeline import Pipeline as P
+    from paper_2602_15917_b200.pipeline import RUN_SLOTS, Pipeline as P
 
     rng = np.random.default_rng(sum(shape) + conn)
     for p in (0.55, 0.7, 0.85):
@@ -98,9 +98,9 @@ def test_pipeline_run_slots_vs_oracle(shape, conn, se):
         x = torch.from_numpy(xv.view(np.int16)).cuda()
         cfg = synth.Config("rand", shape, "u16", eb=2.0, conn=conn, se=se, min_size=3)
         pl = P(shape, "u16", eb=2.0, conn=conn, se=se, min_size=3)
-        assert pl.rs == (32 if se == 4 else 0)
+        assert pl.rs == (RUN_SLOTS if se == 4 else 0)
         res = pl.run(x)
-        assert res.scalars.run_slots == (32 if se == 4 else 0)   # the in-plane opening writes run records
+        assert res.scalars.run_slots == (RUN_SLOTS if se == 4 else 0)   # the in-plane opening writes run records
         _check(cfg, pl, x, res)
 
 
