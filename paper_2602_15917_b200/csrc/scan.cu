@@ -14,10 +14,15 @@ __device__ __forceinline__ void st_state(uint64_t *p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// tmp[0 .. nb): tile states (zeroed by the launcher); tmp[nb]: the total
+// tmp[0 .. nb): tile states (zeroed by the launcher); tmp[nb]: the total.
+// A tile is SCAN_T / 32 warps x SCAN_CH chunks of 128 elements; lane l of a warp holds elements
+// 4 l .. 4 l + 3 of each of its chunks (one coalesced 16-byte load per chunk when the tile is whole and
+// the pointers aligned), so the warp scans chunk by chunk with a running carry.  Large tiles keep the
+// look-back chain short (the first wave of tiles resolves its prefixes 32 tiles per round).
 template <typename O>
 __global__ void __launch_bounds__(SCAN_T) k_scan_dlb(const uint32_t *in, O *out, const uint64_t *len_dev, uint64_t len,
                                                      uint64_t *tmp, uint64_t nb) {
+    constexpr int CH = SCAN_TILE / SCAN_T / 4;   // chunks of 128 elements per warp
     __shared__ uint64_t wsum[SCAN_T / 32];
     __shared__ uint64_t s_pre;
     const uint64_t n = len_dev ? *len_dev : len;
@@ -25,17 +30,32 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_dlb(const uint32_t *in, O *out,
     const uint64_t base = t * SCAN_TILE;
     if (base > n) return;   // nobody waits on tiles past the one holding index n
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-    // thread owns elements base + tid*V .. +V (contiguous)
-    uint32_t v[SCAN_V];
-    uint64_t loc = 0;
+    const uint64_t wbase = base + (uint64_t)warp * CH * 128;
+    const bool whole = base + SCAN_TILE <= n;
+    const bool vin = whole && ((uintptr_t)in & 15) == 0;
+    uint4 q[CH];
+    uint64_t ex[CH];   // exclusive prefix of the lane's four elements inside the warp's region
+    uint64_t carry = 0;
 #pragma unroll
-    for (int k = 0; k < SCAN_V; k++) {
-        const uint64_t i = base + (uint64_t)threadIdx.x * SCAN_V + k;
-        v[k] = i < n ? in[i] : 0u;
-        loc += v[k];
+    for (int c = 0; c < CH; c++) {
+        const uint64_t i = wbase + (uint64_t)c * 128 + 4 * lane;
+        if (vin) {
+            q[c] = reinterpret_cast<const uint4 *>(in + i)[0];
+        } else {
+            q[c].x = i < n ? in[i] : 0u;
+            q[c].y = i + 1 < n ? in[i + 1] : 0u;
+            q[c].z = i + 2 < n ? in[i + 2] : 0u;
+            q[c].w = i + 3 < n ? in[i + 3] : 0u;
+        }
     }
-    const uint64_t x = warp_incl_scan(loc);
-    if (lane == 31) wsum[warp] = x;
+#pragma unroll
+    for (int c = 0; c < CH; c++) {
+        const uint64_t s4 = (uint64_t)q[c].x + q[c].y + q[c].z + q[c].w;
+        const uint64_t inc = warp_incl_scan(s4);
+        ex[c] = carry + inc - s4;
+        carry += __shfl_sync(FULL, inc, 31);
+    }
+    if (lane == 31) wsum[warp] = carry;
     __syncthreads();
     uint64_t wpre = 0, agg = 0;
 #pragma unroll
@@ -74,12 +94,26 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_dlb(const uint32_t *in, O *out,
         if (lane == 0) s_pre = pre;
     }
     __syncthreads();
-    uint64_t run = s_pre + wpre + x - loc;
+    const uint64_t off = s_pre + wpre;
+    const bool vout = whole && ((uintptr_t)out & 15) == 0;
 #pragma unroll
-    for (int k = 0; k < SCAN_V; k++) {
-        const uint64_t i = base + (uint64_t)threadIdx.x * SCAN_V + k;
-        if (i < n) out[i] = (O)run;
-        run += v[k];
+    for (int c = 0; c < CH; c++) {
+        const uint64_t i = wbase + (uint64_t)c * 128 + 4 * lane;
+        const uint64_t r0 = off + ex[c], r1 = r0 + q[c].x, r2 = r1 + q[c].y, r3 = r2 + q[c].z;
+        if (vout) {
+            if constexpr (sizeof(O) == 4) {
+                reinterpret_cast<uint4 *>(out + i)[0] = make_uint4((uint32_t)r0, (uint32_t)r1, (uint32_t)r2, (uint32_t)r3);
+            } else {
+                ulonglong2 *o2 = reinterpret_cast<ulonglong2 *>(out + i);
+                o2[0] = make_ulonglong2(r0, r1);
+                o2[1] = make_ulonglong2(r2, r3);
+            }
+        } else {
+            if (i < n) out[i] = (O)r0;
+            if (i + 1 < n) out[i + 1] = (O)r1;
+            if (i + 2 < n) out[i + 2] = (O)r2;
+            if (i + 3 < n) out[i + 3] = (O)r3;
+        }
     }
     // the tile holding index n writes the total
     if (n - base < SCAN_TILE && threadIdx.x == 0) {

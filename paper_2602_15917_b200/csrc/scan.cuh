@@ -9,7 +9,7 @@
 
 namespace roix {
 
-constexpr int SCAN_T = 256, SCAN_V = 8, SCAN_TILE = SCAN_T * SCAN_V;
+constexpr int SCAN_T = 256, SCAN_V = 32, SCAN_TILE = SCAN_T * SCAN_V;
 
 // tiles of a scan of up to maxlen elements (one more than needed, so the tile holding index len exists)
 __host__ __device__ inline uint64_t scan_nblocks(uint64_t maxlen) { return maxlen / SCAN_TILE + 1; }
