@@ -41,9 +41,16 @@ class Result:
     scalars: L.Scalars
 
 
-# run records per row the in-plane opening writes (roix_morph_slots, 1..64; C3 step time measured the
-# same for 32, 48 and 64: fewer rows left to a6's mask reader, more record writes in the opening)
+# run records per row the opening writes (roix_morph_slots, 1..64; C3 step time measured the same for
+# 32, 48 and 64: fewer rows left to a6's mask reader, more record writes in the opening)
 RUN_SLOTS = 32
+
+
+def run_slots_for(shape, se):
+    """Run records per row the opening writes for this slab shape: the in-plane openings (X >= 64);
+    0 where the opening writes none (a6 then reads every row from o).  The 3-D opening writes none:
+    records from k_open3d_rows measured slower overall (C5: opening +2.1 ms, labelling -0.9 ms)."""
+    return RUN_SLOTS if (se == 4 and shape[2] >= 64) else 0
 
 
 class Pipeline:
@@ -102,8 +109,8 @@ class Pipeline:
         self.row_runs = torch.empty(Z * Y, dtype=torch.int32, device=dev)
         # run records of every row (x0, x1) written by the opening for rows of <= rs runs, so a6 does
         # not re-read those rows of o (roix_morph_slots / roix_label_slots)
-        # (only the in-plane opening writes them; C3 rows hold ~11 runs on average: noise specks)
-        self.rs = RUN_SLOTS if (X >= 64 and se == 4) else 0
+        # (C3 rows hold ~11 runs on average: noise specks)
+        self.rs = run_slots_for((Z, Y, X), se)
         self.run_slots = torch.empty(max(1, Z * Y * self.rs * 2), dtype=torch.int32, device=dev) if self.rs else None
         # fused (speculative) histogram + binarisation: one read of x for a2 + a4 (roix_histogram_binarize);
         # off by default: on B200 the histogram pass is bound by shared-memory atomics, and the fused pass

@@ -82,12 +82,15 @@ def test_pipeline_union_block_16k_vs_oracle(cfg):
 
 
 @pytest.mark.parametrize("shape,conn,se", [((6, 40, 64), 6, 6), ((5, 33, 256), 26, 6), ((4, 50, 100), 8, 4),
-                                           ((3, 64, 2048), 18, 6), ((2, 30, 1000), 4, 4)])
+                                           ((3, 64, 2048), 18, 6), ((2, 30, 1000), 4, 4), ((4, 37, 1024), 6, 6),
+                                           ((3, 21, 4096), 26, 6), ((5, 19, 2048), 6, 6)])
 def test_pipeline_run_slots_vs_oracle(shape, conn, se):
-    """The in-plane opening's run records (roix_morph_slots, 32 per row) feed a6 for rows with <= 32
-    runs; rows with more are re-read from o (the 3-D openings write none: a6 reads o).  Two-level volumes with random masks of several densities give rows
-    of every run count on both sides of 8, in one volume; every artefact against the oracle."""
-    from paper_2602_15917_b200.pipeline import RUN_SLOTS, Pipeline as P
+    """The opening's run records (roix_morph_slots, 32 per row: the in-plane openings) feed a6 for
+    rows with <= 32 runs; rows with more, and slabs whose opening writes none (3-D), are re-read
+    from o.  Two-level volumes with random masks of several densities
+    give rows of every run count on both sides of 32, in one volume; every artefact against the
+    oracle."""
+    from paper_2602_15917_b200.pipeline import Pipeline as P, run_slots_for
 
     rng = np.random.default_rng(sum(shape) + conn)
     for p in (0.55, 0.7, 0.85):
@@ -98,9 +101,9 @@ def test_pipeline_run_slots_vs_oracle(shape, conn, se):
         x = torch.from_numpy(xv.view(np.int16)).cuda()
         cfg = synth.Config("rand", shape, "u16", eb=2.0, conn=conn, se=se, min_size=3)
         pl = P(shape, "u16", eb=2.0, conn=conn, se=se, min_size=3)
-        assert pl.rs == (RUN_SLOTS if se == 4 else 0)
+        assert pl.rs == run_slots_for(shape, se)
         res = pl.run(x)
-        assert res.scalars.run_slots == (RUN_SLOTS if se == 4 else 0)   # the in-plane opening writes run records
+        assert res.scalars.run_slots == pl.rs   # the opening wrote run records of that width
         _check(cfg, pl, x, res)
 
 

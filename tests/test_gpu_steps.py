@@ -382,33 +382,40 @@ def test_morph_random_masks(shape, se, dt):
         np.testing.assert_array_equal(runs.cpu().numpy(), _runs_per_row(ref))
 
 
-def _crosses(rng, shape, per_row):
-    """Planes of isolated 3x3 crosses (each survives the opening whole) -- rows with a few short runs,
-    several of them inside one 32-bit word -- over a dense random band (rows with many runs)."""
+def _crosses(rng, shape, per_row, columns=False):
+    """Planes of isolated 3x3 crosses (each survives the in-plane opening whole; `columns`: the same
+    crosses in every plane, which survive the 3-D opening) -- rows with a few short runs, several of
+    them inside one 32-bit word -- over a dense random band (rows with many runs)."""
     Z, Y, X = shape
     m = np.zeros(shape, bool)
     for z in range(Z):
-        for _ in range(max(1, int(per_row * Y / 3))):
-            y, x = rng.integers(1, Y - 1), rng.integers(1, X - 1)
-            m[z, y - 1:y + 2, x] = True
-            m[z, y, x - 1:x + 2] = True
+        if columns and z:
+            m[z] = m[0]
+        else:
+            for _ in range(max(1, int(per_row * Y / 3))):
+                y, x = rng.integers(1, Y - 1), rng.integers(1, X - 1)
+                m[z, y - 1:y + 2, x] = True
+                m[z, y, x - 1:x + 2] = True
+    for z in range(Z):
         m[z, : Y // 4] |= rng.random((Y // 4, X)) < 0.8
     return m
 
 
-@pytest.mark.parametrize("shape", [(2, 12, 13900), (3, 20, 1390), (4, 12, 33), (2, 8, 16352), (3, 11, 64),
-                                   (2, 10, 100), (2, 9, 16400), (3, 8, 20)])
-def test_morph_run_slots_vs_oracle(shape):
-    """roix_morph_slots (se = 4): row_runs of every row and, for rows with 1..32 runs, the run records
-    (x0, x1 exclusive) against the runs of the oracle's opening -- register-row kernel (X >= 32,
-    W + 1 <= 512), shared-memory kernel (W >= 512) and rows shorter than a word."""
+@pytest.mark.parametrize("shape,se", [((2, 12, 13900), 4), ((3, 20, 1390), 4), ((4, 12, 33), 4), ((2, 8, 16352), 4),
+                                      ((3, 11, 64), 4), ((2, 10, 100), 4), ((2, 9, 16400), 4), ((3, 8, 20), 4),
+                                      ((3, 12, 1024), 6), ((4, 10, 2048), 6), ((3, 8, 4096), 6), ((3, 9, 96), 6)])
+def test_morph_run_slots_vs_oracle(shape, se):
+    """roix_morph_slots: row_runs of every row and, for rows with 1..32 runs, the run records (x0, x1
+    exclusive) against the runs of the oracle's opening -- se = 4: register-row kernel (X >= 32,
+    W + 1 <= 512), shared-memory kernel (W >= 512), rows shorter than a word; se = 6: the 3-D openings,
+    which write row_runs and no records."""
     rng = np.random.default_rng(sum(shape))
     Z, Y, X = shape
     rs = 32
     for per_row in (0.5, 4.0, 12.0):
-        m = _crosses(rng, shape, per_row)
+        m = _crosses(rng, shape, per_row, columns=se == 6)
         x_np = np.where(m, 3000, 100).astype(np.uint16)
-        ref = oracle.opening(m.astype(np.uint8), 4).astype(bool)
+        ref = oracle.opening(m.astype(np.uint8), se).astype(bool)
         x = dev(x_np)
         sc = new_sc(1.0)
         s = read_sc(sc)
@@ -420,7 +427,7 @@ def test_morph_run_slots_vs_oracle(shape):
         slots = torch.full((Z * Y * rs * 2,), -1, dtype=torch.int32, device="cuda")
         g = L.Geom(Z, Y, X, 0, Z)
         ws = torch.empty(L.roix_morph_workspace(g), dtype=torch.uint8, device="cuda")
-        L.roix_morph_slots(ptr(x), L.U16, ctypes.byref(g), 4, None, None, ptr(sc), ptr(o), ptr(runs), ptr(slots),
+        L.roix_morph_slots(ptr(x), L.U16, ctypes.byref(g), se, None, None, ptr(sc), ptr(o), ptr(runs), ptr(slots),
                            rs, ptr(ws), ws.numel(), st())
         sv = read_sc(sc)
         assert sv.err == 0
