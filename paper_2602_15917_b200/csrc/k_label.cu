@@ -380,6 +380,27 @@ __global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__res
                 ns += __popc(st[i]);
                 ne += __popc(en[i]);
             }
+            if constexpr (L == 32) {
+                // common case: no lane holds two starts or two ends -- ranks by ballot, one store each
+                if (!__any_sync(FULL, (ns | ne) > 1)) {
+                    const uint32_t lt = (1u << sl) - 1u;
+                    const uint32_t bS = __ballot_sync(FULL, ns != 0), bE = __ballot_sync(FULL, ne != 0);
+                    uint32_t xs = 0, xe = 0;
+#pragma unroll
+                    for (int i = KW - 1; i >= 0; i--) {
+                        if (st[i]) xs = 32 * i + __ffs(st[i]) - 1;
+                        if (en[i]) xe = 32 * i + __ffs(en[i]);
+                    }
+                    const uint32_t xb = 32 * KW * sl;
+                    if (ns) {
+                        const uint32_t ps = b0 + __popc(bS & lt);
+                        x0[ps] = xb + xs;
+                        rrow[ps] = (uint32_t)r;
+                    }
+                    if (ne) x1[b0 + __popc(bE & lt)] = xb + xe;
+                    continue;
+                }
+            }
             // inclusive segment scan of (starts | ends << 16); both <= 16 KW per lane
             uint32_t both = ns | (ne << 16);
 #pragma unroll
