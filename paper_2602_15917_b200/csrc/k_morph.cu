@@ -6,13 +6,18 @@
 //  k_open3d (se = 6): a CTA owns a band of TY rows of every plane of a z-chunk and marches along z
 //    with rings of 3 m-planes and 3 e-planes in shared memory; m is re-read only for 2 halo rows per
 //    band side and 2 halo planes per chunk side (bits: 1/16 of the input bytes for u16).
-//  k_open2d (se = 4, in-plane): a CTA owns a range of rows and marches along them.
+//  k_open2d_w (se = 4, in-plane, 32 <= X < 16 K): a warp owns a range of rows, each row whole in
+//    registers; the slab is cut into chunks of planes, binarised on the caller's stream and opened on
+//    a second stream, so the (issue-bound) opening of one chunk overlaps the (HBM-bound) binarisation
+//    of the next.
+//  k_open2d (se = 4, other widths): a CTA owns a range of rows and marches along them.
 // Shared-memory rows: W = ceil(X/32) words plus a guard word on each side (stride WS = W + 2); m rows
 // carry guard/pad bits = 1 (erosion border 1), e/o rows 0 (dilation border 0).  Erosion and
 // dilation are word-wise AND / OR of the row, its +-1 x-shifts (funnel shifts across the
 // neighbouring words) and the neighbouring rows / planes.  Both open kernels count the x-runs of
 // every output row (the fused first step of a6 CCL).
 #include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -34,6 +39,7 @@ struct MorphArgs {
     uint32_t *row_runs;
     uint2 *run_slots;        // [rows * rs] or null: (x0, x1) of the first rs x-runs of every output row
     uint32_t rs;
+    int64_t row_lo, row_hi;  // 2-D register-row opening: the rows (whole planes) this launch reads and writes
 };
 
 template <typename T>
@@ -849,7 +855,7 @@ __global__ void __launch_bounds__(128, J <= 14 ? 4 : 3) k_open2d_w(MorphArgs A, 
     const uint64_t X = A.nx, Y = A.ny;
     const uint32_t W = A.W;
     const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t ra = (int64_t)(gw * A.rows_per_cta), rb = min(rows, ra + (int64_t)A.rows_per_cta);
+    const int64_t ra = A.row_lo + (int64_t)(gw * A.rows_per_cta), rb = min(A.row_hi, ra + (int64_t)A.rows_per_cta);
     if (ra >= rb) return;
     const uint32_t sl = (lane + 31) & 31, sr = (lane + 1) & 31;
     const bool l0 = lane == 0, l31 = lane == 31;
@@ -870,7 +876,7 @@ __global__ void __launch_bounds__(128, J <= 14 ? 4 : 3) k_open2d_w(MorphArgs A, 
     auto padm = [&](int j) -> uint32_t { return j == J - 1 ? padB : j == J - 2 ? padA : 0u; };
     uint32_t raw[J], m0[J], m1[J], m2[J], e0[J], e1[J], e2[J];
     auto issue = [&](int64_t s) {   // raw words k <= W of m row s (one coalesced load per chunk)
-        if (s < 0 || s >= rows) return;
+        if (s < A.row_lo || s >= A.row_hi) return;   // other planes: never used unsubstituted
         const uint32_t *src = A.m + (((uint64_t)s * X) >> 5);
 #pragma unroll
         for (int j = 0; j < J; j++) {
@@ -1054,6 +1060,135 @@ static cudaError_t set_smem(K kern, size_t bytes) {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// a4 on planes [p0, p1) of the slab: x -> m (linear bits; the range starts on a word boundary), at most
+// `per_sm` CTAs per SM
+static cudaError_t binarize_range(const void *x, int dtype, uint64_t p0, uint64_t p1, const roix_geom &g,
+                                  roix_scalars *sc, uint32_t *m, int prebinarized, const roix_frame *frames,
+                                  uint32_t per_sm, cudaStream_t st) {
+    const uint64_t A = g.ny * g.nx, v0 = p0 * A, n = (p1 - p0) * A;
+    if (!n) return cudaSuccess;
+    uint64_t iters = (n + 1023) / 1024;
+    uint64_t blocks = (iters + 7) / 8;
+    const uint64_t cap = (uint64_t)num_sms() * per_sm;
+    if (blocks > cap) blocks = cap;
+    uint32_t *mm = m + v0 / 32;
+    if (frames) {
+        const FrameThr F = {frames + p0, A};
+        k_binarize<uint16_t, true><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x + v0, n, sc, mm, 0, F);
+    } else if (dtype == ROIX_U16) {
+        k_binarize<uint16_t><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x + v0, n, sc, mm, prebinarized,
+                                                                FrameThr{nullptr, A});
+    } else {
+        k_binarize<float><<<(unsigned)blocks, 256, 0, st>>>((const float *)x + v0, n, sc, mm, prebinarized,
+                                                             FrameThr{nullptr, A});
+    }
+    return cudaGetLastError();
+}
+
+// the register-row opening on rows [r0, r1) (whole planes, r0 X a multiple of 32)
+static cudaError_t open2d_w_rows(MorphArgs A, int64_t r0, int64_t r1, uint32_t warps_target, roix_scalars *sc,
+                                 cudaStream_t st) {
+    const uint32_t J = (A.W + 1 + 31) / 32;
+    const void *fn = nullptr;
+    switch (J) {
+#define ROIX_O2W(JJ) \
+    case JJ: fn = (const void *)k_open2d_w<JJ>; break;
+        ROIX_O2W(1) ROIX_O2W(2) ROIX_O2W(3) ROIX_O2W(4) ROIX_O2W(5) ROIX_O2W(6) ROIX_O2W(7) ROIX_O2W(8)
+        ROIX_O2W(9) ROIX_O2W(10) ROIX_O2W(11) ROIX_O2W(12) ROIX_O2W(13) ROIX_O2W(14) ROIX_O2W(15) ROIX_O2W(16)
+#undef ROIX_O2W
+    default: return cudaErrorInvalidConfiguration;
+    }
+    const uint64_t rows = (uint64_t)(r1 - r0);
+    if (!rows) return cudaSuccess;
+    uint64_t rpw = (rows + warps_target - 1) / warps_target;
+    rpw = (rpw + 31) / 32 * 32;   // every warp's rows start on a word boundary
+    A.rows_per_cta = rpw;
+    A.row_lo = r0;
+    A.row_hi = r1;
+    const uint64_t nw = (rows + rpw - 1) / rpw;
+    void *args[] = {&A, &sc};
+    return cudaLaunchKernel(fn, dim3((unsigned)((nw + 3) / 4)), dim3(128), args, 0, st);
+}
+
+// a4 + a5 for the in-plane SE with the register-row opening: the slab is cut into chunks of whole
+// planes (each starting on a word boundary); chunk c is binarised on the caller's stream and opened on
+// a second stream as soon as its mask is complete, so the opening of chunk c (issue-bound, little
+// memory traffic) runs beside the binarisation of chunk c + 1 (HBM-bound) -- in-plane openings of
+// different planes are independent.  The second stream forks from and joins the caller's stream with
+// events, so the whole call stays one stream-ordered operation (and one CUDA-graph capture).
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, ready[16] = {};
+};
+
+static cudaError_t side_stream(SideStream **out) {
+    static SideStream side[64];
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    SideStream &S = side[dev];
+    std::call_once(once[dev], [&S, &e] {
+        if ((e = cudaStreamCreateWithFlags(&S.s, cudaStreamNonBlocking)) != cudaSuccess) return;
+        if ((e = cudaEventCreateWithFlags(&S.fork, cudaEventDisableTiming)) != cudaSuccess) return;
+        if ((e = cudaEventCreateWithFlags(&S.join, cudaEventDisableTiming)) != cudaSuccess) return;
+        for (auto &ev : S.ready)
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return;
+    });
+    if (e != cudaSuccess) return e;
+    if (!S.s) return cudaErrorNotReady;
+    *out = &S;
+    return cudaSuccess;
+}
+
+static uint64_t gcd_u64(uint64_t a, uint64_t b) {
+    while (b) {
+        const uint64_t t = a % b;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+static cudaError_t open2d_pipelined(const void *x, int dtype, const roix_geom &g, MorphArgs A, roix_scalars *sc,
+                                    const roix_frame *frames, cudaStream_t st) {
+    cudaError_t e;
+    const uint64_t Z = g.nz, Y = g.ny, PA = g.ny * g.nx;
+    const uint64_t quantum = 32 / gcd_u64(PA % 32 ? PA % 32 : 32, 32);   // planes per word-aligned step
+    // measured at C3 (chunks, binarisation CTAs per SM, opening warps per SM): (8, 4, 24) 7.62 ms for
+    // a4 + a5; (8, 2, 8) 9.22, (8, 1, 16) 14.5 (the binarisation needs its warps), (8, 8, 16) 7.69,
+    // (16, 4, 16) 7.93; one chunk (no overlap) 8.53; a high-priority stream for either side: no gain
+    constexpr int k_nch = 8, k_bps = 4, k_wt = 24;
+    uint64_t nch = (uint64_t)k_nch, cp = (Z + nch - 1) / nch;
+    cp = (cp + quantum - 1) / quantum * quantum;
+    nch = (Z + cp - 1) / cp;
+    if (nch < 2) {   // one chunk: plain sequence on the caller's stream
+        uint32_t *m = const_cast<uint32_t *>(A.m);
+        if ((e = binarize_range(x, dtype, 0, Z, g, sc, m, 0, frames, 8, st)) != cudaSuccess) return e;
+        return open2d_w_rows(A, 0, (int64_t)(Z * Y), (uint32_t)num_sms() * 16, sc, st);
+    }
+    SideStream *S = nullptr;
+    if ((e = side_stream(&S)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(S->fork, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(S->s, S->fork, 0)) != cudaSuccess) return e;
+    for (uint64_t c = 0; c < nch; c++) {
+        const uint64_t p0 = c * cp, p1 = min(Z, p0 + cp);
+        // the binarisation (4 CTAs per SM) leaves room on every SM for the previous chunk's opening
+        if ((e = binarize_range(x, dtype, p0, p1, g, sc, const_cast<uint32_t *>(A.m), 0, frames, (uint32_t)k_bps, st)) !=
+            cudaSuccess)
+            return e;
+        cudaEvent_t ev = S->ready[c % 16];
+        if ((e = cudaEventRecord(ev, st)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(S->s, ev, 0)) != cudaSuccess) return e;
+        if ((e = open2d_w_rows(A, (int64_t)(p0 * Y), (int64_t)(p1 * Y), (uint32_t)num_sms() * k_wt, sc, S->s)) !=
+            cudaSuccess)
+            return e;
+    }
+    if ((e = cudaEventRecord(S->join, S->s)) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(st, S->join, 0);
+}
+
 size_t morph_workspace_bytes(const roix_geom &g) { return ((g.nz * g.ny * g.nx + 31) / 32 + 64) * 4; }
 
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
@@ -1083,21 +1218,11 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     // in-plane SE: binarise + open in one pass over x (m stays on chip)
     // a4: stream x -> m (after a fused speculative pass: resolve its window, binarise only on a miss)
     if (prebinarized && (e = launch_spec_resolve(x, dtype, g, sc, ws, st)) != cudaSuccess) return e;
-    {
-        uint64_t iters = (n + 1023) / 1024;
-        uint64_t blocks = (iters + 7) / 8;
-        uint64_t cap = (uint64_t)num_sms() * 8;
-        if (blocks > cap) blocks = cap;
-        const FrameThr F = {frames, g.ny * g.nx};
-        if (frames)
-            k_binarize<uint16_t, true><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x, n, sc, m, 0, F);
-        else if (dtype == ROIX_U16)
-            k_binarize<uint16_t><<<(unsigned)blocks, 256, 0, st>>>((const uint16_t *)x, n, sc, m, prebinarized, F);
-        else k_binarize<float><<<(unsigned)blocks, 256, 0, st>>>((const float *)x, n, sc, m, prebinarized, F);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
-    int occ = 0;
     const uint32_t Wd = A.W;
+    const bool o2w = se != 6 && g.nx >= 32 && Wd + 1 <= 32 * 16 && !prebinarized;   // register-row 2-D opening
+    if (o2w) return open2d_pipelined(x, dtype, g, A, sc, frames, st);
+    if ((e = binarize_range(x, dtype, 0, g.nz, g, sc, m, prebinarized, frames, 8, st)) != cudaSuccess) return e;
+    int occ = 0;
     const bool rows_kernel = g.nx % 32 == 0 && (Wd <= 32 ? (Wd & (Wd - 1)) == 0 : (Wd == 64 || Wd == 128));
     if (se == 6 && rows_kernel) {
         // whole-row warps: S = 32 / L segments of RY rows each
@@ -1141,27 +1266,6 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
         if (row_runs && (e = cudaMemsetAsync(row_runs, 0, g.nz * g.ny * 4, st)) != cudaSuccess) return e;
         const uint64_t tasks = per_chunk * chunks;
         k_open3d_reg<RY><<<(unsigned)((tasks + 7) / 8), 256, 0, st>>>(A, sc);
-    } else if (g.nx >= 32 && A.W + 1 <= 32 * 16) {
-        // register rows: one warp per range of rows, one wave of resident warps
-        const uint32_t J = (A.W + 1 + 31) / 32;
-        const void *fn = nullptr;
-        switch (J) {
-#define ROIX_O2W(JJ) \
-    case JJ: fn = (const void *)k_open2d_w<JJ>; break;
-        ROIX_O2W(1) ROIX_O2W(2) ROIX_O2W(3) ROIX_O2W(4) ROIX_O2W(5) ROIX_O2W(6) ROIX_O2W(7) ROIX_O2W(8)
-        ROIX_O2W(9) ROIX_O2W(10) ROIX_O2W(11) ROIX_O2W(12) ROIX_O2W(13) ROIX_O2W(14) ROIX_O2W(15) ROIX_O2W(16)
-#undef ROIX_O2W
-        default: return cudaErrorInvalidConfiguration;
-        }
-        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 128, 0)) != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-        const uint64_t rows = g.nz * g.ny, warps = (uint64_t)num_sms() * occ * 4;
-        uint64_t rpw = (rows + warps - 1) / warps;
-        rpw = (rpw + 31) / 32 * 32;   // every warp's rows start on a word boundary
-        A.rows_per_cta = rpw;
-        const uint64_t nw = (rows + rpw - 1) / rpw;
-        void *args[] = {&A, &sc};
-        return cudaLaunchKernel(fn, dim3((unsigned)((nw + 3) / 4)), dim3(128), args, 0, st);
     } else {
         const int S = 8;
         size_t sm = (size_t)((S + 4) + (S + 2) + S + 1) * A.WS * 4;

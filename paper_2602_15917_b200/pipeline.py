@@ -7,6 +7,7 @@ PyTorch provides device memory and the stream; every step runs in libroix's kern
 one stream without host synchronisation (so the whole step can be captured in a CUDA graph).
 """
 import ctypes
+import math
 import dataclasses
 
 import numpy as np
@@ -44,6 +45,22 @@ class Result:
 # run records per row the opening writes (roix_morph_slots, 1..64; C3 step time measured the same for
 # 32, 48 and 64: fewer rows left to a6's mask reader, more record writes in the opening)
 RUN_SLOTS = 32
+
+
+def morph_chunks(shape, se, prebinarized=False):
+    """Plane chunks of roix_morph's in-plane path (k_morph.cu open2d_pipelined: binarised on the
+    caller's stream, opened on a second one): 8 chunks of whole planes, each starting on a word
+    boundary; 1 where the register-row opening does not apply."""
+    Z, Y, X = shape
+    W = (X + 31) // 32
+    if se == 6 or X < 32 or W + 1 > 512 or prebinarized:
+        return 1
+    pa = (Y * X) % 32
+    quantum = 32 // math.gcd(pa if pa else 32, 32)
+    cp = -(-Z // 8)
+    cp = -(-cp // quantum) * quantum
+    nch = -(-Z // cp)
+    return nch if nch >= 2 else 1
 
 
 def run_slots_for(shape, se):
@@ -305,6 +322,7 @@ class Pipeline:
         k += sum(LAUNCHES[s] for s in ("scalars_init", "resolve", "histogram", "threshold", "morph", "label",
                                        "extract" if self.extract == "mask" else "extract_runs"))
         k += 1 if self.rs else 0          # k_runs_slots (the opening's run records)
+        k += 2 * (morph_chunks(self.shape, self.se, self.fused) - 1)   # a4 + a5 per plane chunk
         return k + (LAUNCHES["range"] if self.cdtype == L.F32 else 0)
 
     def scalars(self):

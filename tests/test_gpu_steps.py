@@ -325,7 +325,10 @@ MORPH_SHAPES = [(1, 1, 1), (1, 1, 40), (2, 3, 5), (3, 5, 7), (5, 33, 65), (7, 64
                 (17, 13, 128), (19, 7, 2048), (3, 5, 4096), (20, 37, 512), (18, 11, 64), (40, 3, 32),
                 # in-plane register-row kernel (32 <= X, W + 1 <= 512 words): C3's row width, the widest
                 # row it takes, the first it leaves to the shared-memory kernel, rows of one word + 1 bit
-                (2, 9, 13900), (2, 3, 16352), (2, 3, 16353), (4, 7, 33), (3, 4, 31)]
+                (2, 9, 13900), (2, 3, 16352), (2, 3, 16353), (4, 7, 33), (3, 4, 31),
+                # several plane chunks (binarised on one stream, opened on another): chunk starts on word
+                # boundaries after 4, 8 and 1 planes
+                (16, 20, 1390), (24, 7, 100), (13, 5, 64)]
 
 
 def _morph_gpu(x_np, thr, pol, se):
@@ -402,6 +405,7 @@ def _crosses(rng, shape, per_row, columns=False):
 
 
 @pytest.mark.parametrize("shape,se", [((2, 12, 13900), 4), ((3, 20, 1390), 4), ((4, 12, 33), 4), ((2, 8, 16352), 4),
+                                      ((16, 12, 1390), 4), ((11, 9, 96), 4),
                                       ((3, 11, 64), 4), ((2, 10, 100), 4), ((2, 9, 16400), 4), ((3, 8, 20), 4),
                                       ((3, 12, 1024), 6), ((4, 10, 2048), 6), ((3, 8, 4096), 6), ((3, 9, 96), 6)])
 def test_morph_run_slots_vs_oracle(shape, se):
