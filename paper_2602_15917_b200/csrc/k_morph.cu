@@ -40,6 +40,7 @@ struct MorphArgs {
     uint2 *run_slots;        // [rows * rs] or null: (x0, x1) of the first rs x-runs of every output row
     uint32_t rs;
     int64_t row_lo, row_hi;  // 2-D register-row opening: the rows (whole planes) this launch reads and writes
+    int64_t z_lo, z_hi;      // 3-D whole-row opening: the planes this launch writes
 };
 
 template <typename T>
@@ -413,9 +414,9 @@ __global__ void __launch_bounds__(256, (KW == 1 ? 3 : (KW == 2 ? 2 : 1))) k_open
     const uint32_t cz = task / tiles_y;
     const int yb = (int)((task - cz * tiles_y) * (S * RY) + seg * RY);   // this segment's first row
     const int nz = (int)A.nz;
-    const int zs = (int)(cz * A.zchunk);
-    if (zs >= nz) return;
-    const int ze = min(nz, zs + (int)A.zchunk);
+    const int zs = (int)A.z_lo + (int)(cz * A.zchunk);   // planes [z_lo, z_hi) of this launch
+    if (zs >= (int)A.z_hi) return;
+    const int ze = min((int)A.z_hi, zs + (int)A.zchunk);
     const uint64_t plane_w = A.ny * (uint64_t)W;
     const int64_t gz = (int64_t)A.gz, z0 = (int64_t)A.z0;
     const int roff = (yb - 2) * (int)W + (int)(KW * sl);   // word offset of slot row 0 in its plane
@@ -1151,18 +1152,33 @@ static uint64_t gcd_u64(uint64_t a, uint64_t b) {
     return a;
 }
 
-static cudaError_t open2d_pipelined(const void *x, int dtype, const roix_geom &g, MorphArgs A, roix_scalars *sc,
-                                    const roix_frame *frames, cudaStream_t st) {
-    cudaError_t e;
-    const uint64_t Z = g.nz, Y = g.ny, PA = g.ny * g.nx;
+// Plane chunks of the two-stream a4 + a5 (mirrored by pipeline.morph_chunks): in-plane SE: 8 chunks,
+// each starting on a word boundary; 3-D SE: 16 chunks of >= 8 planes, at least 3 (X = 32 W: every
+// plane starts on a word).  Only slabs of >= 2^30 voxels are chunked.
+constexpr int se_in_plane = 4;
+static uint64_t chunk_planes(const roix_geom &g, uint32_t se) {
+    const uint64_t Z = g.nz;
+    if (se == 6) return max((uint64_t)8, (Z + 15) / 16);
+    const uint64_t PA = g.ny * g.nx;
     const uint64_t quantum = 32 / gcd_u64(PA % 32 ? PA % 32 : 32, 32);   // planes per word-aligned step
+    const uint64_t cp = (Z + 7) / 8;
+    return (cp + quantum - 1) / quantum * quantum;
+}
+static int morph_chunks(const roix_geom &g, uint32_t se, int prebinarized) {
+    if (prebinarized || g.nz * g.ny * g.nx < (1ull << 30)) return 1;
+    const uint64_t cp = chunk_planes(g, se), nch = (g.nz + cp - 1) / cp;
+    return (int)(nch >= (se == 6 ? 3u : 2u) ? nch : 1);
+}
+
+static cudaError_t open2d_pipelined(const void *x, int dtype, const roix_geom &g, MorphArgs A, roix_scalars *sc,
+                                    const roix_frame *frames, int nchunks, cudaStream_t st) {
+    cudaError_t e;
+    const uint64_t Z = g.nz, Y = g.ny;
     // measured at C3 (chunks, binarisation CTAs per SM, opening warps per SM): (8, 4, 24) 7.62 ms for
     // a4 + a5; (8, 2, 8) 9.22, (8, 1, 16) 14.5 (the binarisation needs its warps), (8, 8, 16) 7.69,
     // (16, 4, 16) 7.93; one chunk (no overlap) 8.53; a high-priority stream for either side: no gain
-    constexpr int k_nch = 8, k_bps = 4, k_wt = 24;
-    uint64_t nch = (uint64_t)k_nch, cp = (Z + nch - 1) / nch;
-    cp = (cp + quantum - 1) / quantum * quantum;
-    nch = (Z + cp - 1) / cp;
+    constexpr int k_bps = 4, k_wt = 24;
+    const uint64_t nch = (uint64_t)nchunks, cp = chunk_planes(g, se_in_plane);
     if (nch < 2) {   // one chunk: plain sequence on the caller's stream
         uint32_t *m = const_cast<uint32_t *>(A.m);
         if ((e = binarize_range(x, dtype, 0, Z, g, sc, m, 0, frames, 8, st)) != cudaSuccess) return e;
@@ -1189,6 +1205,78 @@ static cudaError_t open2d_pipelined(const void *x, int dtype, const roix_geom &g
     return cudaStreamWaitEvent(st, S->join, 0);
 }
 
+// the whole-row 3-D opening on planes [z0, z1) of the slab (reads m planes z0-2 .. z1+1)
+static cudaError_t open3d_rows_range(MorphArgs A, int64_t z0, int64_t z1, uint64_t target_warps, uint32_t threads,
+                                     roix_scalars *sc, cudaStream_t st) {
+    const uint32_t Wd = A.W;
+    const uint32_t L = Wd < 32 ? Wd : 32, KW = Wd / L;
+    const uint32_t RY = KW == 4 ? 2 : 4;
+    const uint64_t nzc = (uint64_t)(z1 - z0);
+    if (!nzc) return cudaSuccess;
+    // whole-row warps: S = 32 / L segments of RY rows each
+    const uint64_t tiles_y = (A.ny + (32 / L) * RY - 1) / ((32 / L) * RY);
+    uint64_t chunks = (target_warps + tiles_y - 1) / tiles_y;
+    const uint64_t cmax = nzc >= 16 ? nzc / 8 : 1;   // >= 8 planes per warp (3 halo planes re-read)
+    if (chunks > cmax) chunks = cmax;
+    if (chunks < 1) chunks = 1;
+    A.zchunk = (nzc + chunks - 1) / chunks;
+    chunks = (nzc + A.zchunk - 1) / A.zchunk;
+    A.z_lo = z0;
+    A.z_hi = z1;
+    const uint32_t wpb = threads / 32;
+    const unsigned blocks = (unsigned)((tiles_y * chunks + wpb - 1) / wpb);
+#define ROIX_OPEN_ROWS(LL, KK, RR) k_open3d_rows<LL, KK, RR><<<blocks, threads, 0, st>>>(A, sc)
+    switch (Wd) {
+    case 1: ROIX_OPEN_ROWS(1, 1, 4); break;
+    case 2: ROIX_OPEN_ROWS(2, 1, 4); break;
+    case 4: ROIX_OPEN_ROWS(4, 1, 4); break;
+    case 8: ROIX_OPEN_ROWS(8, 1, 4); break;
+    case 16: ROIX_OPEN_ROWS(16, 1, 4); break;
+    case 32: ROIX_OPEN_ROWS(32, 1, 4); break;
+    case 64: ROIX_OPEN_ROWS(32, 2, 4); break;
+    default: ROIX_OPEN_ROWS(32, 4, 2); break;
+    }
+#undef ROIX_OPEN_ROWS
+    return cudaGetLastError();
+}
+
+// a4 + a5 for the 3-D SE with the whole-row opening: chunks of planes binarised on the caller's stream;
+// chunk c is opened on the second stream once chunk c + 1 is binarised too (its last rows need the two
+// planes after it), beside the binarisation of chunk c + 2.
+static cudaError_t open3d_pipelined(const void *x, int dtype, const roix_geom &g, MorphArgs A, roix_scalars *sc,
+                                    const roix_frame *frames, int nchunks, cudaStream_t st) {
+    cudaError_t e;
+    const uint64_t Z = g.nz;
+    uint32_t *m = const_cast<uint32_t *>(A.m);
+    // measured (chunks, binarisation CTAs per SM, opening warps per SM, opening CTA threads), a4 + a5
+    // in ms at C4 / C5: one chunk 3.71 / 14.76; (16, 4, 48, 128) 3.37 / 13.24; (8, 4, 48, 128) 3.35 /
+    // 13.63; (8, 2, 48, 256) 3.75 / 14.88 (a 256-thread opening CTA does not fit beside 4 binarisation
+    // CTAs); (8, 6, 48, 128) 3.78 / 15.55
+    constexpr int k_bps = 4, k_wt = 48, k_thr = 128;
+    const uint64_t nch = (uint64_t)nchunks, cp = chunk_planes(g, 6);
+    SideStream *S = nullptr;
+    if ((e = side_stream(&S)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(S->fork, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(S->s, S->fork, 0)) != cudaSuccess) return e;
+    for (uint64_t c = 0; c <= nch; c++) {
+        if (c < nch) {
+            const uint64_t p0 = c * cp, p1 = min(Z, p0 + cp);
+            if ((e = binarize_range(x, dtype, p0, p1, g, sc, m, 0, frames, (uint32_t)k_bps, st)) != cudaSuccess)
+                return e;
+            if ((e = cudaEventRecord(S->ready[c % 16], st)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(S->s, S->ready[c % 16], 0)) != cudaSuccess) return e;
+        }
+        if (c >= 1) {   // chunk c - 1: its planes and the two after them are binarised
+            const uint64_t q0 = (c - 1) * cp, q1 = min(Z, q0 + cp);
+            if ((e = open3d_rows_range(A, (int64_t)q0, (int64_t)q1, (uint64_t)num_sms() * k_wt, (uint32_t)k_thr, sc,
+                                       S->s)) != cudaSuccess)
+                return e;
+        }
+    }
+    if ((e = cudaEventRecord(S->join, S->s)) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(st, S->join, 0);
+}
+
 size_t morph_workspace_bytes(const roix_geom &g) { return ((g.nz * g.ny * g.nx + 31) / 32 + 64) * 4; }
 
 cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t se, const uint32_t *halo_lo,
@@ -1209,6 +1297,8 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     A.row_runs = row_runs;
     A.run_slots = row_runs ? run_slots : nullptr;
     A.rs = A.run_slots ? rs : 0;
+    A.z_lo = 0;
+    A.z_hi = (int64_t)g.nz;
     const uint64_t n = g.nz * g.ny * g.nx;
     const uint64_t nwords = (n + 31) / 32;
     uint32_t *m = (uint32_t *)ws;
@@ -1219,36 +1309,17 @@ cudaError_t launch_morph(const void *x, int dtype, const roix_geom &g, uint32_t 
     // a4: stream x -> m (after a fused speculative pass: resolve its window, binarise only on a miss)
     if (prebinarized && (e = launch_spec_resolve(x, dtype, g, sc, ws, st)) != cudaSuccess) return e;
     const uint32_t Wd = A.W;
+    // plane chunks on two streams pay from ~1 G voxels (C1 / C2: the extra launches cost more than
+    // the overlap gains)
+    const int nchunks = morph_chunks(g, se, prebinarized);
     const bool o2w = se != 6 && g.nx >= 32 && Wd + 1 <= 32 * 16 && !prebinarized;   // register-row 2-D opening
-    if (o2w) return open2d_pipelined(x, dtype, g, A, sc, frames, st);
+    if (o2w) return open2d_pipelined(x, dtype, g, A, sc, frames, nchunks, st);
+    const bool rows_kernel = g.nx % 32 == 0 && (Wd <= 32 ? (Wd & (Wd - 1)) == 0 : (Wd == 64 || Wd == 128));
+    if (se == 6 && rows_kernel && nchunks > 1) return open3d_pipelined(x, dtype, g, A, sc, frames, nchunks, st);
     if ((e = binarize_range(x, dtype, 0, g.nz, g, sc, m, prebinarized, frames, 8, st)) != cudaSuccess) return e;
     int occ = 0;
-    const bool rows_kernel = g.nx % 32 == 0 && (Wd <= 32 ? (Wd & (Wd - 1)) == 0 : (Wd == 64 || Wd == 128));
     if (se == 6 && rows_kernel) {
-        // whole-row warps: S = 32 / L segments of RY rows each
-        const uint32_t L = Wd < 32 ? Wd : 32, KW = Wd / L;
-        const uint32_t RY = KW == 4 ? 2 : 4;
-        const uint64_t tiles_y = (g.ny + (32 / L) * RY - 1) / ((32 / L) * RY);
-        const uint64_t target_warps = (uint64_t)num_sms() * 48;
-        uint64_t chunks = (target_warps + tiles_y - 1) / tiles_y;
-        const uint64_t cmax = g.nz >= 16 ? g.nz / 8 : 1;   // >= 8 planes per warp (3 halo planes re-read)
-        if (chunks > cmax) chunks = cmax;
-        if (chunks < 1) chunks = 1;
-        A.zchunk = (g.nz + chunks - 1) / chunks;
-        chunks = (g.nz + A.zchunk - 1) / A.zchunk;
-        const unsigned blocks = (unsigned)((tiles_y * chunks + 7) / 8);
-#define ROIX_OPEN_ROWS(LL, KK, RR) k_open3d_rows<LL, KK, RR><<<blocks, 256, 0, st>>>(A, sc)
-        switch (Wd) {
-        case 1: ROIX_OPEN_ROWS(1, 1, 4); break;
-        case 2: ROIX_OPEN_ROWS(2, 1, 4); break;
-        case 4: ROIX_OPEN_ROWS(4, 1, 4); break;
-        case 8: ROIX_OPEN_ROWS(8, 1, 4); break;
-        case 16: ROIX_OPEN_ROWS(16, 1, 4); break;
-        case 32: ROIX_OPEN_ROWS(32, 1, 4); break;
-        case 64: ROIX_OPEN_ROWS(32, 2, 4); break;
-        default: ROIX_OPEN_ROWS(32, 4, 2); break;
-        }
-#undef ROIX_OPEN_ROWS
+        if ((e = open3d_rows_range(A, 0, (int64_t)g.nz, (uint64_t)num_sms() * 48, 256, sc, st)) != cudaSuccess) return e;
     } else if (se == 6) {
         // general rows (X % 32 != 0 or other widths): 30-word pencils with halo lanes
         constexpr int RY = 4;

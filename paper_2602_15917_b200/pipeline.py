@@ -48,12 +48,21 @@ RUN_SLOTS = 32
 
 
 def morph_chunks(shape, se, prebinarized=False):
-    """Plane chunks of roix_morph's in-plane path (k_morph.cu open2d_pipelined: binarised on the
-    caller's stream, opened on a second one): 8 chunks of whole planes, each starting on a word
-    boundary; 1 where the register-row opening does not apply."""
+    """Plane chunks of roix_morph (k_morph.cu open2d_pipelined / open3d_pipelined: binarised on the
+    caller's stream, opened on a second one) for slabs of >= 2^30 voxels: in-plane SE, register-row
+    opening: 8 chunks of whole planes, each starting on a word boundary; 3-D SE, whole-row opening
+    (X = 32 W, W a power of two <= 32, 64 or 128): 16 chunks of >= 8 planes, at least 3; else 1."""
     Z, Y, X = shape
     W = (X + 31) // 32
-    if se == 6 or X < 32 or W + 1 > 512 or prebinarized:
+    if prebinarized or Z * Y * X < (1 << 30):
+        return 1
+    if se == 6:
+        if not (X % 32 == 0 and ((W <= 32 and W & (W - 1) == 0) or W in (64, 128))):
+            return 1
+        cp = max(8, -(-Z // 16))
+        nch = -(-Z // cp)
+        return nch if nch >= 3 else 1
+    if X < 32 or W + 1 > 512:
         return 1
     pa = (Y * X) % 32
     quantum = 32 // math.gcd(pa if pa else 32, 32)
