@@ -135,7 +135,8 @@ def alg_bytes(cfg, n, count, background=False):
 
 # the C-ABI call each timed stage is (its kernels: profiles/*/launches_*.txt)
 STAGE_CALLS = {"range": "roix_range (k_range)", "histogram": "roix_histogram (k_hist_*)",
-               "morph": "roix_morph_slots (k_binarize + k_open3d_rows / k_open2d)",
+               "morph": "roix_morph_slots (k_binarize + k_open2d_w / k_open3d_rows; plane chunks, opening on a "
+                        "second stream)",
                "label": "roix_label_slots (runs, union-find, filter)",
                "background": "roix_background (k_background_vec)",
                "extract": "roix_extract (k_ck_count + scan + k_ck_extract)",

@@ -16,7 +16,7 @@ STAGE = {
     "setup": ["k_hist_clear"],
     "histogram": ["k_hist_u16", "k_hist_f32", "k_hist_u16_frames"],
     "threshold": ["k_threshold", "k_threshold_frames"],
-    "morph": ["k_binarize", "k_open3d_reg", "k_open3d_rows", "k_open2d", "k_morph2d"],
+    "morph": ["k_binarize", "k_open3d_reg", "k_open3d_rows", "k_open2d", "k_open2d_w"],
     "label": ["k_scan_dlb", "k_runs_total", "k_runs_slots", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross", "k_resolve_broots",
               "k_flatten_sizes", "k_largest_init", "k_largest", "k_root_flags", "k_table", "k_table_total", "k_clear_dropped", "k_table_clear"],
     "extract": ["k_extract_count", "k_extract", "k_extract_seg", "k_extract_total", "k_ck_count", "k_ck_extract",
