@@ -623,11 +623,12 @@ def e2e(p, x, cfg, args, world=1, dist_on=False):
     if not dist_on:
         return e2e_pipelined(p, x, cfg, args)
     P = getattr(p, "S", p)                       # the slab state of a sharded pipeline
-    xh = x.cpu().pin_memory()
+    xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    xh.copy_(x)
     xd = torch.empty_like(x)
     cnt_h = torch.empty(1, dtype=torch.int64).pin_memory()
-    out_h = torch.empty(P.codes.numel(), dtype=P.codes.dtype).pin_memory()
-    mask_h = torch.empty(P.nwords, dtype=torch.int32).pin_memory()
+    out_h = torch.empty(max(int(p.local_count()), 1), dtype=P.codes.dtype, pin_memory=True)
+    mask_h = torch.empty(P.nwords, dtype=torch.int32, pin_memory=True)
     stream = torch.cuda.current_stream()
     steps = max(3, min(args.steps, 10))
     d2h = 0
@@ -668,6 +669,17 @@ def e2e(p, x, cfg, args, world=1, dist_on=False):
             "ms_per_step": dt * 1e3, "steps": steps}
 
 
+def host_available():
+    """Available host memory in bytes (None if unknown)."""
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return None
+
+
 def e2e_pipelined(p, x, cfg, args):
     """e2e at N = 1 with the steps overlapped the way a streaming user runs them: volume i+1 copies in
     (pinned host -> device, its own stream and input buffer) while volume i is processed and its result
@@ -678,11 +690,23 @@ def e2e_pipelined(p, x, cfg, args):
     from paper_2602_15917_b200 import _lib as L
 
     dev = x.device
-    xh = x.cpu().pin_memory()
-    xd = [torch.empty_like(x), torch.empty_like(x)]
+    count = int(p.scalars().count)                   # this volume's kept count (every step the same)
+    need = x.numel() * x.element_size() + count * p.codes.element_size() + p.nwords * 4
+    avail = host_available()
+    if avail is not None and need > 0.7 * avail:
+        return {"skipped": "pinned host buffers of %.1f GB exceed 70%% of the %.1f GB available" % (need / 1e9, avail / 1e9)}
+    xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    xh.copy_(x)
+    # two device input buffers (the resident x is one); a volume too large for a second one (C5:
+    # 64 GiB beside the path's buffers) is copied into x itself, each copy after the previous run
+    try:
+        xd = [x, torch.empty_like(x)]
+    except torch.OutOfMemoryError:
+        xd = [x, x]
+    nbuf = 2 if xd[1] is not x else 1
     cnt_h = [torch.empty(1, dtype=torch.int64).pin_memory() for _ in range(2)]
-    out_h = torch.empty(p.codes.numel(), dtype=p.codes.dtype).pin_memory()
-    mask_h = torch.empty(p.nwords, dtype=torch.int32).pin_memory()
+    out_h = torch.empty(max(count, 1), dtype=p.codes.dtype, pin_memory=True)
+    mask_h = torch.empty(p.nwords, dtype=torch.int32, pin_memory=True)
     s_in, s_run, s_out = (torch.cuda.Stream(dev) for _ in range(3))
     off = L.Scalars.count.offset
     cnt_d = p.sc[off:off + 8].view(torch.int64)      # roix_scalars.count
@@ -695,8 +719,8 @@ def e2e_pipelined(p, x, cfg, args):
 
     def h2d(i):
         with torch.cuda.stream(s_in):
-            if i >= 2:
-                s_in.wait_event(ev_run[i - 2])       # the input buffer is free again
+            if i >= nbuf:
+                s_in.wait_event(ev_run[i - nbuf])    # the input buffer is free again
             xd[i % 2].copy_(xh, non_blocking=True)
             ev_in[i].record(s_in)
 
@@ -735,7 +759,8 @@ def e2e_pipelined(p, x, cfg, args):
     dt = (time.perf_counter() - t0) / (total - 1)
     return {"value": cfg.nbytes / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": x.numel() * x.element_size(),
             "d2h_bytes_per_step": d2h[0], "ms_per_step": dt * 1e3, "steps": total - 1,
-            "overlap": "h2d(i+1) || run(i) || d2h(i-1)"}
+            "overlap": "h2d(i+1) || run(i) || d2h(i-1)" if nbuf == 2 else
+                       "one device input buffer: h2d(i+1) after run(i); d2h(i) || h2d(i+1)"}
 
 
 if __name__ == "__main__":

@@ -225,6 +225,11 @@ roix_status roix_threshold_frames(const uint64_t *hist, uint64_t nframes, roix_p
  * row_runs (nullable, nz*ny uint32): receives the number of x-runs of o in each row -- the fused
  * first step of roix_label, which then skips its own counting pass.
  * ws/ws_bytes (roix_morph_workspace): holds the binarised mask m between the two kernels.
+ * Slabs of >= 2^30 voxels are processed in chunks of whole planes: each chunk is binarised on
+ * `stream` and opened on a second, library-owned stream of the current device (forked from and
+ * joined back to `stream` with events), so the opening of one chunk runs beside the binarisation of
+ * the next.  The call stays stream-ordered on `stream` (and capturable in a CUDA graph); concurrent
+ * calls on different streams share that second stream.
  */
 roix_status roix_morph_workspace(const roix_geom *g, size_t *ws_bytes);
 roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
