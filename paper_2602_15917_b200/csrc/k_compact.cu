@@ -299,11 +299,18 @@ __device__ __forceinline__ void ck_chunk(const T *__restrict__ x, uint64_t n, ui
             em = m;
         }
         if (em) {
+            C *const ob = out + P;   // the group's kept codes go to P, P + 1, ... (32-bit offsets)
+            if (P + VPG <= capacity) {
 #pragma unroll
-            for (int k = 0; k < VPG; k++) {
-                if (!((em >> k) & 1u)) continue;
-                const uint64_t dst = P + __popc(m & ((1u << k) - 1u));
-                if (dst < capacity) out[dst] = (C)code_k<C>(e[j], k);
+                for (int k = 0; k < VPG; k++)
+                    if ((em >> k) & 1u) ob[__popc(m & ((1u << k) - 1u))] = (C)code_k<C>(e[j], k);
+            } else {
+#pragma unroll
+                for (int k = 0; k < VPG; k++) {
+                    if (!((em >> k) & 1u)) continue;
+                    const uint64_t dst = P + __popc(m & ((1u << k) - 1u));
+                    if (dst < capacity) out[dst] = (C)code_k<C>(e[j], k);
+                }
             }
         }
     }
