@@ -739,17 +739,30 @@ __global__ void k_root_flags(LGeo G, LabelWS W, MapView M, uint64_t min_size, co
     const uint64_t n = W.ctr[0];
     const uint64_t keep_label = keep ? keep[1] : 0;
     uint32_t nk = 0;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t f = 0;
-        if (W.parent[i] == (uint32_t)i) {
-            uint64_t fin, tot;
-            resolve_root(G, W, M, (uint32_t)i, fin, tot);
-            const uint8_t kp = keep ? fin == keep_label : tot >= min_size;
-            W.kept[i] = kp;
-            f = fin == gidx(G, W, (uint32_t)i);
-            nk += f & kp;
+    constexpr int TC = 4;   // runs per thread per step, their parent loads issued together
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * TC;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * TC + threadIdx.x; i0 < n; i0 += stride) {
+        uint32_t p[TC];
+#pragma unroll
+        for (int t = 0; t < TC; t++) {
+            const uint64_t i = i0 + (uint64_t)t * blockDim.x;
+            p[t] = i < n ? W.parent[i] : 0u;
         }
-        W.cidx[i] = f;
+#pragma unroll
+        for (int t = 0; t < TC; t++) {
+            const uint64_t i = i0 + (uint64_t)t * blockDim.x;
+            if (i >= n) break;
+            uint32_t f = 0;
+            if (p[t] == (uint32_t)i) {
+                uint64_t fin, tot;
+                resolve_root(G, W, M, (uint32_t)i, fin, tot);
+                const uint8_t kp = keep ? fin == keep_label : tot >= min_size;
+                W.kept[i] = kp;
+                f = fin == gidx(G, W, (uint32_t)i);
+                nk += f & kp;
+            }
+            W.cidx[i] = f;
+        }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) nk += __shfl_xor_sync(FULL, nk, d);
@@ -769,28 +782,48 @@ __global__ void k_table_clear(LGeo G, LabelWS W, MapView M, const uint32_t *csca
     }
     const uint64_t n = W.ctr[0];
     uint32_t *K = out.keep_bits;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t p = W.parent[i];
-        if (out.comp_min && p == (uint32_t)i) {
-            uint64_t fin, tot;
-            resolve_root(G, W, M, (uint32_t)i, fin, tot);
-            if (fin == gidx(G, W, (uint32_t)i)) {
-                const uint64_t c = cscan[i];
-                if (c < out.comp_cap) {
-                    out.comp_min[c] = fin;
-                    out.comp_size[c] = tot;
-                    if (out.comp_kept) out.comp_kept[c] = W.kept[i];
+    // TC runs per thread per step (a block's runs are consecutive: coalesced run loads), every load of
+    // the step issued before any is used: the random kept[parent] reads overlap each other
+    constexpr int TC = 4;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * TC;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x * TC + threadIdx.x; i0 < n; i0 += stride) {
+        uint32_t p[TC], r[TC], a[TC], z[TC];
+        uint8_t kp[TC];
+#pragma unroll
+        for (int t = 0; t < TC; t++) {
+            const uint64_t i = i0 + (uint64_t)t * blockDim.x;
+            p[t] = i < n ? W.parent[i] : 0u;
+            r[t] = i < n ? W.rrow[i] : 0u;
+            a[t] = i < n ? W.x0[i] : 0u;
+            z[t] = i < n ? W.x1[i] : 0u;
+        }
+#pragma unroll
+        for (int t = 0; t < TC; t++) kp[t] = i0 + (uint64_t)t * blockDim.x < n ? W.kept[p[t]] : 1;
+#pragma unroll
+        for (int t = 0; t < TC; t++) {
+            const uint64_t i = i0 + (uint64_t)t * blockDim.x;
+            if (i >= n) break;
+            if (out.comp_min && p[t] == (uint32_t)i) {
+                uint64_t fin, tot;
+                resolve_root(G, W, M, (uint32_t)i, fin, tot);
+                if (fin == gidx(G, W, (uint32_t)i)) {
+                    const uint64_t c = cscan[i];
+                    if (c < out.comp_cap) {
+                        out.comp_min[c] = fin;
+                        out.comp_size[c] = tot;
+                        if (out.comp_kept) out.comp_kept[c] = kp[t];
+                    }
                 }
             }
-        }
-        if (K && !W.kept[p]) {
-            uint64_t b = (uint64_t)W.rrow[i] * G.nx + W.x0[i], e = (uint64_t)W.rrow[i] * G.nx + W.x1[i];
-            while (b < e) {
-                const uint64_t wi = b >> 5;
-                const uint32_t sh = (uint32_t)(b & 31);
-                const uint32_t take = (uint32_t)min((uint64_t)(32 - sh), e - b);
-                atomicAnd(&K[wi], ~(low_mask(take) << sh));
-                b += take;
+            if (K && !kp[t]) {
+                uint64_t b = (uint64_t)r[t] * G.nx + a[t], e = (uint64_t)r[t] * G.nx + z[t];
+                while (b < e) {
+                    const uint64_t wi = b >> 5;
+                    const uint32_t sh = (uint32_t)(b & 31);
+                    const uint32_t take = (uint32_t)min((uint64_t)(32 - sh), e - b);
+                    atomicAnd(&K[wi], ~(low_mask(take) << sh));
+                    b += take;
+                }
             }
         }
     }
