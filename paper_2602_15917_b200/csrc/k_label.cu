@@ -644,19 +644,33 @@ __global__ void k_flatten_sizes(LabelWS W, roix_scalars *sc) {
          b0 += nw * 32 * J) {
         uint32_t cur = 0xffffffffu;
         uint64_t sum = 0;
-#pragma unroll 4
-        for (int j = 0; j < J; j++) {
-            const uint64_t i = b0 + (uint64_t)j * 32 + lane;
-            if (i >= n) break;
-            const uint32_t root = W.parent[W.parent[i]];   // two hops after k_resolve_broots
-            W.parent[i] = root;
-            const uint32_t len = W.x1[i] - W.x0[i];
-            if (root != cur) {
-                if (sum) atomicAdd((unsigned long long *)&W.size[cur], (unsigned long long)sum);
-                cur = root;
-                sum = 0;
+        // four runs at a time: their parent loads, then the second hops, issued before any is used
+        for (int j0 = 0; j0 < J; j0 += 4) {
+            uint32_t pp[4], rt[4], ln[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint64_t i = b0 + (uint64_t)(j0 + u) * 32 + lane;
+                const bool ok = j0 + u < J && i < n;
+                pp[u] = ok ? W.parent[i] : 0u;
+                ln[u] = ok ? W.x1[i] - W.x0[i] : 0u;
             }
-            sum += len;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint64_t i = b0 + (uint64_t)(j0 + u) * 32 + lane;
+                rt[u] = (j0 + u < J && i < n) ? W.parent[pp[u]] : 0u;   // two hops after k_resolve_broots
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint64_t i = b0 + (uint64_t)(j0 + u) * 32 + lane;
+                if (j0 + u >= J || i >= n) break;
+                W.parent[i] = rt[u];
+                if (rt[u] != cur) {
+                    if (sum) atomicAdd((unsigned long long *)&W.size[cur], (unsigned long long)sum);
+                    cur = rt[u];
+                    sum = 0;
+                }
+                sum += ln[u];
+            }
         }
         const uint32_t grp = __match_any_sync(FULL, cur);
         const uint64_t tot = __reduce_add_sync(grp, (uint32_t)sum);   // per-warp sums fit 32 bits
