@@ -321,12 +321,20 @@ __global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__res
     uint32_t *__restrict__ x1 = W.x1;
     uint32_t *__restrict__ rrow = W.rrow;
     const uint32_t *__restrict__ rs = W.row_start;
-    for (uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gi < ngroups; gi += wpg) {
+    // row offsets of a group, one per lane when the segment is wide enough (loaded an iteration ahead)
+    auto load_off = [&](uint64_t g) -> uint32_t {
+        const uint64_t r = (g * S + seg) * RR + sl;
+        return (g < ngroups && sl <= (uint32_t)RR && r <= rows) ? __ldg(rs + r) : 0u;
+    };
+    uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    uint32_t off_next = L > RR ? load_off(gi) : 0u;
+    for (; gi < ngroups; gi += wpg) {
         const uint64_t r0 = (gi * S + seg) * RR;   // this segment's first row
         // row offsets rs[r0 .. r0 + RR]: one per lane when the segment is wide enough, else all per lane
         uint32_t off = 0, offs[RR + 1];
         if constexpr (L > RR) {
-            if (sl <= (uint32_t)RR && r0 + sl <= rows) off = __ldg(rs + r0 + sl);
+            off = off_next;
+            off_next = load_off(gi + wpg);
         } else {
 #pragma unroll
             for (int q = 0; q <= RR; q++) offs[q] = r0 + q <= rows ? __ldg(rs + r0 + q) : 0u;
