@@ -49,15 +49,25 @@ template <>
 struct Cmp<uint16_t> {
     uint32_t thr;
     uint32_t low;
-    __device__ Cmp(const roix_scalars *sc) : thr(sc->thr_u16), low(sc->polarity) {}
+    uint32_t t2, keep;   // SWAR compare: (thr mod 2^15) in both halves; mask selecting | (thr < 2^15) or &
+    __device__ Cmp(const roix_scalars *sc) : thr(sc->thr_u16), low(sc->polarity) {
+        t2 = (thr & 0x7fffu) * 0x00010001u;
+        keep = thr < 0x8000u ? FULL : 0u;
+    }
     static constexpr int VPL = 8;  // voxels per 16-byte load
+    // x >= thr for both 16-bit halves of w, exact for every uint16 x and thr <= 0xffff: with x = 2^15 xh
+    // + xl, s = (x | 2^15) - tl has bit 15 = [xl >= tl] (no borrow leaves the half), and
+    // x >= thr = xh | [xl >= tl] when th = 0, xh & [xl >= tl] when th = 1.  Flags at bits 15 and 31.
+    __device__ __forceinline__ uint32_t ge2(uint32_t w) const {
+        const uint32_t sv = (w | 0x80008000u) - t2;
+        return ((w & sv) | ((w | sv) & keep)) & 0x80008000u;
+    }
     __device__ __forceinline__ uint32_t bits(uint4 v) const {
-        uint32_t w[4] = {v.x, v.y, v.z, v.w}, b = 0;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            b |= (uint32_t)((w[k] & 0xffffu) >= thr) << (2 * k);
-            b |= (uint32_t)((w[k] >> 16) >= thr) << (2 * k + 1);
-        }
+        if (thr > 0xffffu) return low ? 0xffu : 0u;
+        // byte 1 / byte 3 of each flag word hold the voxels' flags at their top bit; one multiply moves
+        // four byte-top bits to bits 28..31 (partial products land on distinct bits: no carries)
+        const uint32_t r01 = __byte_perm(ge2(v.x), ge2(v.y), 0x7531), r23 = __byte_perm(ge2(v.z), ge2(v.w), 0x7531);
+        const uint32_t b = ((r01 * 0x00204081u) >> 28) | (((r23 * 0x00204081u) >> 28) << 4);
         return low ? (~b & 0xffu) : b;
     }
     __device__ __forceinline__ uint32_t bit1(uint16_t v) const { return ((uint32_t)v >= thr) ^ low; }

@@ -456,6 +456,30 @@ def test_morph_run_slots_vs_oracle(shape, se):
         assert checked > 0
 
 
+@pytest.mark.parametrize("thr", [0, 1, 1000, 0x7fff, 0x8000, 0x8001, 0xfffe, 0xffff, 0x10000])
+@pytest.mark.parametrize("pol", [0, 1])
+def test_binarize_every_u16_value(thr, pol):
+    """The uint16 compare (two voxels per 32-bit word, SWAR) against a plain compare, exhaustively: every
+    uint16 value, thresholds on both sides of 2^15 and past the range, both polarities."""
+    vals = np.arange(65536, dtype=np.uint32)
+    x_np = np.stack([vals.astype(np.uint16), vals[::-1].astype(np.uint16)]).reshape(2, 256, 256)
+    x = dev(x_np)
+    sc = new_sc(1.0)
+    s = read_sc(sc)
+    s.thr_u16 = thr
+    s.polarity = pol
+    write_sc(sc, s)
+    g = L.Geom(2, 256, 256, 0, 2)
+    pw = 256 * 256 // 32
+    out = torch.full((2 * pw,), -1, dtype=torch.int32, device="cuda")
+    L.roix_binarize_planes(ptr(x), L.U16, ctypes.byref(g), 0, 2, ptr(sc), ptr(out), st())
+    torch.cuda.synchronize()
+    ref = x_np.astype(np.uint32) >= thr
+    if pol:
+        ref = ~ref
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), oracle.pack_bits(ref.reshape(-1).astype(np.uint8)))
+
+
 def test_binarize_planes_halo_layout():
     rng = np.random.default_rng(2)
     shape = (6, 13, 37)
