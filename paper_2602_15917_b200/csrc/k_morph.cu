@@ -50,9 +50,11 @@ struct Cmp<uint16_t> {
     uint32_t thr;
     uint32_t low;
     uint32_t t2, keep;   // SWAR compare: (thr mod 2^15) in both halves; mask selecting | (thr < 2^15) or &
-    __device__ Cmp(const roix_scalars *sc) : thr(sc->thr_u16), low(sc->polarity) {
-        t2 = (thr & 0x7fffu) * 0x00010001u;
-        keep = thr < 0x8000u ? FULL : 0u;
+    __device__ Cmp(const roix_scalars *sc) : low(sc->polarity) { set_thr(sc->thr_u16); }
+    __device__ __forceinline__ void set_thr(uint32_t t) {
+        thr = t;
+        t2 = (t & 0x7fffu) * 0x00010001u;
+        keep = t < 0x8000u ? FULL : 0u;
     }
     static constexpr int VPL = 8;  // voxels per 16-byte load
     // x >= thr for both 16-bit halves of w, exact for every uint16 x and thr <= 0xffff: with x = 2^15 xh
@@ -77,6 +79,7 @@ struct Cmp<float> {
     float thr;
     uint32_t low;
     __device__ Cmp(const roix_scalars *sc) : thr(sc->thr_f32), low(sc->polarity) {}
+    __device__ __forceinline__ void set_thr(float t) { thr = t; }
     static constexpr int VPL = 4;
     __device__ __forceinline__ uint32_t bits(uint4 v) const {
         uint32_t b = (uint32_t)(__uint_as_float(v.x) >= thr) | ((uint32_t)(__uint_as_float(v.y) >= thr) << 1) |
@@ -219,7 +222,7 @@ __device__ __forceinline__ uint32_t group_bits(const Cmp<T> &cmp, uint4 vec, uin
         Cmp<T> c = cmp;
         if (F.A >= 1024) {
             if (v0 + VPL <= b1 || v0 >= b1) {
-                c.thr = v0 < b1 ? t0 : t1;
+                c.set_thr(v0 < b1 ? t0 : t1);
                 return c.bits(vec);
             }
             uint32_t b = 0;
