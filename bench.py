@@ -437,6 +437,17 @@ def main():
     }
     clocks = clk.summary()
     line["clocks"] = clocks
+    # per-step spread, the naive fraction, the DRAM overhead factor, run scalars
+    per_step = [st[0][1].elapsed_time(st[-1][1]) for st in ev[-args.steps:] if len(st) > 1]
+    if per_step:
+        per_step.sort()
+        line["step_ms"] = {"median": per_step[len(per_step) // 2], "min": per_step[0], "n": len(per_step),
+                           "note": "first to last event of each step on the device"}
+    line["naive_frac"] = value / peak
+    if traffic:
+        line["roofline"]["overhead"] = traffic / ab[dom]
+    line["scalars"] = {"i_max": float(s.i_max), "thr": float(s.thr_u16) if cfg.dtype == "u16" else float(s.thr_f32),
+                       "n_components": int(s.n_components), "n_kept": int(s.n_kept), "n_runs": int(s.n_runs)}
     # ---- per-artefact parity of this very run against the stored oracle result (full-size configs)
     if not dist_on and args.scale == 1.0 and args.classes == 2 and not args.frames and args.keep == "size" \
             and args.background == "none":
