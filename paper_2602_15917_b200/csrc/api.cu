@@ -7,6 +7,8 @@
 #include <mutex>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "kernels.cuh"
 #include "roix.h"
 
@@ -26,6 +28,13 @@ roix_status cuda(cudaError_t e, const char *where) {
     return ROIX_E_CUDA;
 }
 bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+// NVTX range around an enqueuing call (a profiler's timeline shows which C-ABI call issued which
+// kernels; without a profiler attached the push / pop are no-ops)
+struct Range {
+    explicit Range(const char *name) { nvtxRangePushA(name); }
+    ~Range() { nvtxRangePop(); }
+};
 bool dtype_ok(roix_dtype d) { return d == ROIX_U16 || d == ROIX_F32; }
 bool geom_ok(const roix_geom *g) {
     if (!g) return false;
@@ -72,6 +81,7 @@ roix_status roix_scalars_init(roix_scalars *sc, float eb_abs, roix_stream_t stre
 }
 
 roix_status roix_range(const float *x, uint64_t n, roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_range");
     if (!sc) return invalid("sc is NULL");
     if (n == 0) return ROIX_OK;
     if (!x || !aligned16(x)) return invalid("x must be a 16-byte aligned device pointer");
@@ -79,6 +89,7 @@ roix_status roix_range(const float *x, uint64_t n, roix_scalars *sc, roix_stream
 }
 
 roix_status roix_resolve(roix_scalars *sc, roix_dtype dtype, double rel_eb, roix_stream_t stream) {
+    const Range nvtx_range("roix_resolve");
     if (!sc) return invalid("sc is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (!(rel_eb >= 0.0) || !std::isfinite(rel_eb)) return invalid("rel_eb must be finite and >= 0");
@@ -88,6 +99,7 @@ roix_status roix_resolve(roix_scalars *sc, roix_dtype dtype, double rel_eb, roix
 
 roix_status roix_quantize(const void *x, roix_dtype dtype, uint64_t n, roix_scalars *sc, void *codes,
                           roix_stream_t stream) {
+    const Range nvtx_range("roix_quantize");
     if (!sc) return invalid("sc is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (n == 0) return ROIX_OK;
@@ -97,6 +109,7 @@ roix_status roix_quantize(const void *x, roix_dtype dtype, uint64_t n, roix_scal
 
 roix_status roix_histogram(const void *x, roix_dtype dtype, uint64_t n, roix_scalars *sc, uint64_t *hist,
                            uint32_t nbins, roix_stream_t stream) {
+    const Range nvtx_range("roix_histogram");
     if (!sc || !hist) return invalid("sc / hist is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if ((dtype == ROIX_U16 && nbins != 65536) || (dtype == ROIX_F32 && nbins != 256))
@@ -116,6 +129,7 @@ roix_status roix_histogram_clear(uint64_t *hist, uint64_t nbins, roix_stream_t s
 
 roix_status roix_threshold(const uint64_t *hist, uint32_t nbins, roix_dtype dtype, roix_polarity polarity,
                            roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_threshold");
     if (!sc || !hist) return invalid("sc / hist is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if ((dtype == ROIX_U16 && nbins != 65536) || (dtype == ROIX_F32 && nbins != 256))
@@ -126,6 +140,7 @@ roix_status roix_threshold(const uint64_t *hist, uint32_t nbins, roix_dtype dtyp
 
 roix_status roix_threshold_multi(const uint64_t *hist, uint32_t nbins, roix_dtype dtype, roix_polarity polarity,
                                  uint32_t classes, roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_threshold_multi");
     if (classes != 2 && classes != 3) return unsupported("classes must be 2 or 3");
     if (!sc || !hist) return invalid("sc / hist is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
@@ -154,6 +169,7 @@ roix_status roix_morph_slots(const void *x, roix_dtype dtype, const roix_geom *g
                              const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits, uint32_t *row_runs,
                              uint32_t *run_slots, uint32_t slots_per_row, void *ws, size_t ws_bytes,
                              roix_stream_t stream) {
+    const Range nvtx_range("roix_morph_slots");
     if (!sc || !o_bits || !ws) return invalid("sc / o_bits / ws is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (!geom_ok(g)) return invalid("geometry");
@@ -179,6 +195,7 @@ roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint
 roix_status roix_morph_frames(const uint16_t *x, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,
                              const uint32_t *halo_hi, const roix_frame *frames, roix_scalars *sc, uint32_t *o_bits,
                              uint32_t *row_runs, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    const Range nvtx_range("roix_morph_frames");
     if (!sc || !o_bits || !ws || !frames) return invalid("sc / o_bits / ws / frames is NULL");
     if (!geom_ok(g)) return invalid("geometry");
     if (se != 6 && se != 4) return unsupported("se must be 6 (3-D cross) or 4 (in-plane cross)");
@@ -194,6 +211,7 @@ roix_status roix_morph_frames(const uint16_t *x, const roix_geom *g, uint32_t se
 
 roix_status roix_background(const uint16_t *x, const uint16_t *B, const roix_geom *g, roix_bg_op op, uint16_t *out,
                             roix_stream_t stream) {
+    const Range nvtx_range("roix_background");
     if (!geom_ok(g)) return invalid("geometry");
     if (op != ROIX_BG_SUB && op != ROIX_BG_REV && op != ROIX_BG_ADD) return invalid("op");
     if (g->nz * g->ny * g->nx == 0) return ROIX_OK;
@@ -204,6 +222,7 @@ roix_status roix_background(const uint16_t *x, const uint16_t *B, const roix_geo
 
 roix_status roix_histogram_frames(const uint16_t *x, const roix_geom *g, roix_scalars *sc, uint64_t *hist,
                                   roix_stream_t stream) {
+    const Range nvtx_range("roix_histogram_frames");
     if (!sc || !hist) return invalid("sc / hist is NULL");
     if (!geom_ok(g)) return invalid("geometry");
     if (g->nz * g->ny * g->nx && (!x || !aligned16(x))) return invalid("x must be a 16-byte aligned device pointer");
@@ -213,6 +232,7 @@ roix_status roix_histogram_frames(const uint16_t *x, const roix_geom *g, roix_sc
 
 roix_status roix_threshold_frames(const uint64_t *hist, uint64_t nframes, roix_polarity polarity, uint32_t classes,
                                   roix_scalars *sc, roix_frame *frames, roix_stream_t stream) {
+    const Range nvtx_range("roix_threshold_frames");
     if (classes != 2 && classes != 3) return unsupported("classes must be 2 or 3");
     if (!sc || (nframes && (!hist || !frames))) return invalid("sc / hist / frames is NULL");
     if (polarity != ROIX_POL_HIGH && polarity != ROIX_POL_LOW) return invalid("polarity");
@@ -230,6 +250,7 @@ roix_status roix_histogram_binarize_workspace(const roix_geom *g, size_t *ws_byt
 roix_status roix_histogram_binarize(const void *x, roix_dtype dtype, const roix_geom *g, roix_polarity polarity,
                                     roix_scalars *sc, uint64_t *hist, uint32_t nbins, void *ws, size_t ws_bytes,
                                     roix_stream_t stream) {
+    const Range nvtx_range("roix_histogram_binarize");
     if (!sc || !hist || !ws) return invalid("sc / hist / ws is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (!geom_ok(g)) return invalid("geometry");
@@ -245,6 +266,7 @@ roix_status roix_histogram_binarize(const void *x, roix_dtype dtype, const roix_
 roix_status roix_morph_prebinarized(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se,
                                     const uint32_t *halo_lo, const uint32_t *halo_hi, roix_scalars *sc, uint32_t *o_bits,
                                     uint32_t *row_runs, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    const Range nvtx_range("roix_morph_prebinarized");
     if (!sc || !o_bits || !ws) return invalid("sc / o_bits / ws is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (!geom_ok(g)) return invalid("geometry");
@@ -259,6 +281,7 @@ roix_status roix_morph_prebinarized(const void *x, roix_dtype dtype, const roix_
 
 roix_status roix_binarize_planes(const void *x, roix_dtype dtype, const roix_geom *g, uint64_t p0, uint64_t np,
                                  roix_scalars *sc, uint32_t *m_bits, roix_stream_t stream) {
+    const Range nvtx_range("roix_binarize_planes");
     if (!sc || !m_bits) return invalid("sc / m_bits is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (!geom_ok(g)) return invalid("geometry");
@@ -321,6 +344,7 @@ static roix_status label_common(const roix_geom *g, uint64_t cap, const void *ws
 roix_status roix_label_local_slots(const uint32_t *o_bits, const uint32_t *row_runs, const uint32_t *run_slots,
                                    uint32_t slots_per_row, const roix_geom *g, uint32_t conn, uint64_t run_capacity,
                                    void *ws, size_t ws_bytes, roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_label_local_slots");
     if (!sc || !o_bits) return invalid("sc / o_bits is NULL");
     if (!aligned16(o_bits) || (row_runs && !aligned16(row_runs)))
         return invalid("o_bits / row_runs must be 16-byte aligned");
@@ -344,6 +368,7 @@ roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64
                               void *ws, size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
                               const uint64_t *map_total, const uint64_t *nmap, const roix_label_out *out, roix_scalars *sc,
                               roix_stream_t stream) {
+    const Range nvtx_range("roix_label_finish");
     if (!sc || !o_bits || !out) return invalid("sc / o_bits / out is NULL");
     if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
     if (out->comp_min && (!out->comp_size || out->comp_cap == 0)) return invalid("comp_size / comp_cap");
@@ -358,6 +383,7 @@ roix_status roix_label_finish(const uint32_t *o_bits, const roix_geom *g, uint64
 roix_status roix_label_largest(void *ws, const roix_geom *g, uint64_t run_capacity, const uint64_t *map_label,
                                const uint64_t *map_final, const uint64_t *map_total, const uint64_t *nmap, uint32_t phase,
                                uint64_t *best, roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_label_largest");
     if (!sc || !best) return invalid("sc / best is NULL");
     if (phase > 1) return invalid("phase must be 0 or 1");
     if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
@@ -372,6 +398,7 @@ roix_status roix_label_finish_keep(const uint32_t *o_bits, const roix_geom *g, u
                                    size_t ws_bytes, const uint64_t *map_label, const uint64_t *map_final,
                                    const uint64_t *map_total, const uint64_t *nmap, const uint64_t *keep,
                                    const roix_label_out *out, roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_label_finish_keep");
     if (!sc || !o_bits || !out || !keep) return invalid("sc / o_bits / out / keep is NULL");
     if (nmap && (!map_label || !map_final || !map_total)) return invalid("merge map");
     if (out->comp_min && (!out->comp_size || out->comp_cap == 0)) return invalid("comp_size / comp_cap");
@@ -392,6 +419,7 @@ roix_status roix_merge_workspace(uint32_t G, uint64_t root_cap, size_t *ws_bytes
 roix_status roix_merge_device(const uint64_t *gathered, uint32_t G, uint64_t pair_cap, uint64_t root_cap,
                               uint64_t *map_label, uint64_t *map_final, uint64_t *map_total, uint64_t *nmap, void *ws,
                               size_t ws_bytes, roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_merge_device");
     if (!gathered || !map_label || !map_final || !map_total || !nmap || !ws || !sc)
         return invalid("gathered / map / nmap / ws / sc is NULL");
     size_t need = 0;
@@ -405,6 +433,7 @@ roix_status roix_merge_device(const uint64_t *gathered, uint32_t G, uint64_t pai
 
 roix_status roix_label_boundary(const void *ws, const roix_geom *g, uint64_t run_capacity, int side, roix_brun *out,
                                 uint64_t out_cap, uint64_t *count, roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_label_boundary");
     if (!sc || !count || (out_cap && !out)) return invalid("sc / count / out is NULL");
     if (side != 0 && side != 1) return invalid("side must be 0 (first plane) or 1 (last plane)");
     roix_status s = label_common(g, run_capacity, ws, (size_t)-1);
@@ -416,6 +445,7 @@ roix_status roix_label_boundary(const void *ws, const roix_geom *g, uint64_t run
 roix_status roix_label_link(const void *ws, const roix_geom *g, uint64_t run_capacity, uint32_t conn,
                             const roix_brun *prev, const uint64_t *n_prev, uint64_t *pairs, uint64_t pair_cap,
                             uint64_t *n_pairs, roix_scalars *sc, roix_stream_t stream) {
+    const Range nvtx_range("roix_label_link");
     if (!sc || !prev || !n_prev || !n_pairs || (pair_cap && !pairs)) return invalid("NULL pointer");
     if (conn != 6 && conn != 18 && conn != 26) return unsupported("cross-slab links need a 3-D conn (6, 18, 26)");
     roix_status s = label_common(g, run_capacity, ws, (size_t)-1);
@@ -428,6 +458,7 @@ roix_status roix_label_link(const void *ws, const roix_geom *g, uint64_t run_cap
 roix_status roix_label_boundary_roots(const void *ws, const roix_geom *g, uint64_t run_capacity, uint64_t *labels,
                                       uint64_t *sizes, uint64_t out_cap, uint64_t *count, roix_scalars *sc,
                                       roix_stream_t stream) {
+    const Range nvtx_range("roix_label_boundary_roots");
     if (!sc || !count || (out_cap && (!labels || !sizes))) return invalid("NULL pointer");
     roix_status s = label_common(g, run_capacity, ws, (size_t)-1);
     if (s != ROIX_OK) return s;
@@ -498,6 +529,7 @@ roix_status roix_extract_workspace(uint64_t n, size_t *ws_bytes) {
 roix_status roix_extract(const void *x, roix_dtype dtype, uint64_t n, const uint32_t *keep_bits, roix_scalars *sc,
                          void *codes_out, uint64_t capacity, const uint64_t *offset, void *ws, size_t ws_bytes,
                          roix_stream_t stream) {
+    const Range nvtx_range("roix_extract");
     if (!sc || !keep_bits || !ws) return invalid("sc / keep_bits / ws is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (n == 0) return ROIX_OK;
@@ -512,6 +544,7 @@ roix_status roix_extract(const void *x, roix_dtype dtype, uint64_t n, const uint
 roix_status roix_extract_runs(const void *x, roix_dtype dtype, const roix_geom *g, uint64_t run_capacity, void *ws,
                               size_t ws_bytes, roix_scalars *sc, void *codes_out, uint64_t capacity,
                               const uint64_t *offset, roix_stream_t stream) {
+    const Range nvtx_range("roix_extract_runs");
     if (!sc) return invalid("sc is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     roix_status s = label_common(g, run_capacity, ws, ws_bytes);
@@ -535,6 +568,7 @@ roix_status roix_row_spans_workspace(const roix_geom *g, size_t *ws_bytes) {
 roix_status roix_row_spans(const uint32_t *keep_bits, const void *x, roix_dtype dtype, const roix_geom *g,
                            roix_scalars *sc, roix_span *spans, uint64_t span_cap, void *codes, uint64_t code_cap,
                            uint64_t *counts, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    const Range nvtx_range("roix_row_spans");
     if (!sc || !keep_bits || !counts || !ws) return invalid("sc / keep_bits / counts / ws is NULL");
     if (!aligned16(keep_bits)) return invalid("keep_bits must be 16-byte aligned");
     if (!dtype_ok(dtype)) return invalid("dtype");
@@ -557,6 +591,7 @@ roix_status roix_greedy_workspace(uint64_t n, size_t *ws_bytes) {
 
 roix_status roix_greedy_quantize(const uint16_t *D, uint64_t n, double E, uint32_t qmax, uint16_t *Q, uint32_t *group_bits,
                                  uint64_t *ngroups, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    const Range nvtx_range("roix_greedy_quantize");
     if (!ngroups || !ws || !group_bits) return invalid("ngroups / group_bits / ws is NULL");
     if (!(E >= 0.0) || !std::isfinite(E)) return invalid("E must be finite and >= 0");
     if (qmax > 65535) return invalid("qmax must be <= 65535");
@@ -573,6 +608,7 @@ roix_status roix_decode_workspace(uint64_t n, size_t *ws_bytes) {
 
 roix_status roix_decode(const uint32_t *keep_bits, const void *codes, uint64_t ncodes, roix_dtype dtype, uint64_t n,
                         roix_scalars *sc, void *xhat, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    const Range nvtx_range("roix_decode");
     if (!sc || !ws) return invalid("sc / ws is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     if (ws_bytes < decode_workspace_bytes(n)) return invalid("workspace too small (see roix_decode_workspace)");
@@ -595,6 +631,7 @@ roix_status roix_decode_spans_workspace(const roix_geom *g, size_t *ws_bytes) {
 roix_status roix_decode_spans(const roix_span *spans, uint64_t span_cap, const void *codes, uint64_t code_cap,
                               const uint64_t *counts, roix_dtype dtype, const roix_geom *g, roix_scalars *sc,
                               void *xhat, void *ws, size_t ws_bytes, roix_stream_t stream) {
+    const Range nvtx_range("roix_decode_spans");
     if (!sc || !counts || !ws) return invalid("sc / counts / ws is NULL");
     if (!dtype_ok(dtype)) return invalid("dtype");
     size_t need = 0;
@@ -610,6 +647,7 @@ roix_status roix_decode_spans(const roix_span *spans, uint64_t span_cap, const v
 
 roix_status roix_confusion(const uint32_t *pred_bits, const uint32_t *truth_bits, uint64_t n, uint64_t *counts,
                            roix_stream_t stream) {
+    const Range nvtx_range("roix_confusion");
     if (!counts) return invalid("counts is NULL");
     if (n && (!pred_bits || !truth_bits || !aligned16(pred_bits) || !aligned16(truth_bits)))
         return invalid("pred_bits / truth_bits must be 16-byte aligned device pointers");
@@ -622,6 +660,7 @@ static double ratio128(__int128 num, __int128 den) {
 }
 
 roix_status roix_overlap_metrics(const uint64_t *counts, double *out) {
+    const Range nvtx_range("roix_overlap_metrics");
     if (!counts || !out) return invalid("counts / out is NULL");
     const __int128 tp = counts[0], fp = counts[1], fn = counts[2], tn = counts[3];
     const __int128 N = tp + fp + fn + tn;
