@@ -326,47 +326,71 @@ __global__ void __launch_bounds__(256) k_extract_runs_rows(const uint32_t *__res
         const uint64_t r = (g * S + seg) * RR + sl;
         return (g < ngroups && sl <= (uint32_t)RR && r <= rows) ? __ldg(rs + r) : 0u;
     };
+    // the words of a group's live rows (rows with runs left to extract); offv: the group's offsets
+    auto load_words = [&](uint64_t g, uint32_t offv, const uint32_t *offa, uint32_t (&dst)[RR][KW]) {
+        const uint64_t rg = (g * S + seg) * RR;
+#pragma unroll
+        for (int q = 0; q < RR; q++) {
+            uint32_t a, b;
+            if constexpr (L > RR) {
+                a = __shfl_sync(FULL, offv, q, L);
+                b = __shfl_sync(FULL, offv, q + 1, L);
+            } else {
+                a = offa[q];
+                b = offa[q + 1];
+            }
+            const bool live = g < ngroups && rg + q < rows && b - a > skip;
+            const uint32_t *src = o + (rg + q) * (uint64_t)(L * KW) + KW * sl;
+#pragma unroll
+            for (int i = 0; i < KW; i++) dst[q][i] = 0u;
+            if (live) {
+                if constexpr (KW == 1) {
+                    dst[q][0] = __ldg(src);
+                } else if constexpr (KW == 2) {
+                    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src));
+                    dst[q][0] = v.x;
+                    dst[q][1] = v.y;
+                } else {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src));
+                    dst[q][0] = v.x;
+                    dst[q][1] = v.y;
+                    dst[q][2] = v.z;
+                    dst[q][3] = v.w;
+                }
+            }
+        }
+    };
+    // whole-warp segments (L > RR): offsets two groups ahead, words one group ahead
     uint64_t gi = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    uint32_t off_next = L > RR ? load_off(gi) : 0u;
+    uint32_t off_cur = 0, off_nxt = 0, wv_nxt[RR][KW];
+    if constexpr (L > RR) {
+        off_cur = load_off(gi);
+        off_nxt = load_off(gi + wpg);
+        load_words(gi, off_cur, nullptr, wv_nxt);
+    }
     for (; gi < ngroups; gi += wpg) {
         const uint64_t r0 = (gi * S + seg) * RR;   // this segment's first row
         // row offsets rs[r0 .. r0 + RR]: one per lane when the segment is wide enough, else all per lane
         uint32_t off = 0, offs[RR + 1];
+        uint32_t wv[RR][KW];
         if constexpr (L > RR) {
-            off = off_next;
-            off_next = load_off(gi + wpg);
+            off = off_cur;
+#pragma unroll
+            for (int q = 0; q < RR; q++)
+#pragma unroll
+                for (int i = 0; i < KW; i++) wv[q][i] = wv_nxt[q][i];
+            off_cur = off_nxt;
+            off_nxt = load_off(gi + 2 * wpg);
+            load_words(gi + wpg, off_cur, nullptr, wv_nxt);
         } else {
 #pragma unroll
             for (int q = 0; q <= RR; q++) offs[q] = r0 + q <= rows ? __ldg(rs + r0 + q) : 0u;
+            load_words(gi, 0u, offs, wv);
         }
         auto row_off = [&](int q) {
             if constexpr (L > RR) return __shfl_sync(FULL, off, q, L);
             else return offs[q];
         };
-        uint32_t wv[RR][KW];
-#pragma unroll
-        for (int q = 0; q < RR; q++) {
-            const uint32_t a = row_off(q), b = row_off(q + 1);
-            const bool live = r0 + q < rows && b - a > skip;
-            const uint32_t *src = o + (r0 + q) * (uint64_t)(L * KW) + KW * sl;
-#pragma unroll
-            for (int i = 0; i < KW; i++) wv[q][i] = 0u;
-            if (live) {
-                if constexpr (KW == 1) {
-                    wv[q][0] = __ldg(src);
-                } else if constexpr (KW == 2) {
-                    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src));
-                    wv[q][0] = v.x;
-                    wv[q][1] = v.y;
-                } else {
-                    const uint4 v = __ldg(reinterpret_cast<const uint4 *>(src));
-                    wv[q][0] = v.x;
-                    wv[q][1] = v.y;
-                    wv[q][2] = v.z;
-                    wv[q][3] = v.w;
-                }
-            }
-        }
 #pragma unroll
         for (int q = 0; q < RR; q++) {
             const uint64_t r = r0 + q;
