@@ -229,7 +229,8 @@ roix_status roix_threshold_frames(const uint64_t *hist, uint64_t nframes, roix_p
  * `stream` and opened on a second, library-owned stream of the current device (forked from and
  * joined back to `stream` with events), so the opening of one chunk runs beside the binarisation of
  * the next.  The call stays stream-ordered on `stream` (and capturable in a CUDA graph); concurrent
- * calls on different streams share that second stream.
+ * calls on different streams share that second stream (their enqueue sequences are serialised by a
+ * lock, so each call's chunks keep their own dependencies).
  */
 roix_status roix_morph_workspace(const roix_geom *g, size_t *ws_bytes);
 roix_status roix_morph(const void *x, roix_dtype dtype, const roix_geom *g, uint32_t se, const uint32_t *halo_lo,

@@ -1131,6 +1131,7 @@ static cudaError_t open2d_w_rows(MorphArgs A, int64_t r0, int64_t r1, uint32_t w
 // different planes are independent.  The second stream forks from and joins the caller's stream with
 // events, so the whole call stays one stream-ordered operation (and one CUDA-graph capture).
 struct SideStream {
+    std::mutex lock;   // one caller's fork ... join sequence at a time (the events are shared)
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr, ready[16] = {};
 };
@@ -1200,6 +1201,7 @@ static cudaError_t open2d_pipelined(const void *x, int dtype, const roix_geom &g
     }
     SideStream *S = nullptr;
     if ((e = side_stream(&S)) != cudaSuccess) return e;
+    std::lock_guard<std::mutex> guard(S->lock);
     if ((e = cudaEventRecord(S->fork, st)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(S->s, S->fork, 0)) != cudaSuccess) return e;
     for (uint64_t c = 0; c < nch; c++) {
@@ -1272,6 +1274,7 @@ static cudaError_t open3d_pipelined(const void *x, int dtype, const roix_geom &g
     const uint64_t nch = (uint64_t)nchunks, cp = chunk_planes(g, 6);
     SideStream *S = nullptr;
     if ((e = side_stream(&S)) != cudaSuccess) return e;
+    std::lock_guard<std::mutex> guard(S->lock);
     if ((e = cudaEventRecord(S->fork, st)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(S->s, S->fork, 0)) != cudaSuccess) return e;
     for (uint64_t c = 0; c <= nch; c++) {
