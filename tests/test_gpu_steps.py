@@ -328,7 +328,9 @@ MORPH_SHAPES = [(1, 1, 1), (1, 1, 40), (2, 3, 5), (3, 5, 7), (5, 33, 65), (7, 64
                 (2, 9, 13900), (2, 3, 16352), (2, 3, 16353), (4, 7, 33), (3, 4, 31),
                 # several plane chunks (binarised on one stream, opened on another): chunk starts on word
                 # boundaries after 4, 8 and 1 planes
-                (16, 20, 1390), (24, 7, 100), (13, 5, 64)]
+                (16, 20, 1390), (24, 7, 100), (13, 5, 64),
+                # register-row opening corner cases: one-row and two-row planes, a 128-word row
+                (5, 1, 100), (4, 2, 64), (3, 3, 4096), (6, 1, 33)]
 
 
 def _morph_gpu(x_np, thr, pol, se):
