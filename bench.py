@@ -449,9 +449,10 @@ def main():
     line["scalars"] = {"i_max": float(s.i_max), "thr": float(s.thr_u16) if cfg.dtype == "u16" else float(s.thr_f32),
                        "n_components": int(s.n_components), "n_kept": int(s.n_kept), "n_runs": int(s.n_runs)}
     # ---- per-artefact parity of this very run against the stored oracle result (full-size configs)
-    if not dist_on and args.scale == 1.0 and args.classes == 2 and not args.frames and args.keep == "size" \
-            and args.background == "none":
-        line["parity"] = parity_vs_golden(p, cfg, s)
+    # (a sharded run on one rank compares its single slab: the sharded code path on the whole volume)
+    if (not dist_on or world == 1) and args.scale == 1.0 and args.classes == 2 and not args.frames \
+            and args.keep == "size" and args.background == "none":
+        line["parity"] = parity_vs_golden(getattr(p, "S", p), cfg, p.scalars())
     if args.greedy is not None and not dist_on and cfg.dtype == "u16":
         line["next2_greedy"] = next2(p, x, cfg, args)
     if not args.no_next4 and not dist_on:
