@@ -177,23 +177,8 @@ __device__ __forceinline__ T warp_incl_scan(T v) {
     return v;
 }
 
-// Ask the TMA engine to bring [p, p + bytes) into L2 (cp.async.bulk.prefetch; no register or shared
-// memory cost): the 16-byte-aligned envelope, in pieces below 64 KB.
-__device__ __forceinline__ void l2_prefetch_range(const void *p, uint64_t bytes) {
-    uintptr_t lo = (uintptr_t)p & ~(uintptr_t)15;
-    const uintptr_t hi = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
-    for (; lo < hi; lo += 0xfff0u) {
-        const uint32_t len = (uint32_t)(hi - lo < 0xfff0u ? hi - lo : 0xfff0u);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(lo), "r"(len) : "memory");
-    }
-}
-
 // bits: 0..31 -> mask of the low `n` bits (n in 0..32)
 __device__ __forceinline__ uint32_t low_mask(uint32_t n) { return n >= 32 ? FULL : ((1u << n) - 1u); }
-
-// Spread the 4 low bits of nib to bit positions 0, 8, 16, 24 (no carries: the partial products
-// occupy distinct positions).
-__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
 
 // Host: cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per device and call site -- the attribute
 // is per device, `done` is the call site's bitmask of the devices already set (races are harmless:

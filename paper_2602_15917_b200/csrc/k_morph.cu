@@ -166,16 +166,6 @@ __device__ __forceinline__ uint32_t erode_word(const uint32_t *c, const uint32_t
     if (f) v &= f[k] & g[k];
     return v;
 }
-__device__ __forceinline__ uint32_t dilate_word(const uint32_t *c, const uint32_t *a, const uint32_t *b,
-                                                const uint32_t *f, const uint32_t *g, int k) {
-    uint32_t w = c[k];
-    uint32_t l = __funnelshift_l(c[k - 1], w, 1);
-    uint32_t r = __funnelshift_r(w, c[k + 1], 1);
-    uint32_t v = w | l | r | a[k] | b[k];
-    if (f) v |= f[k] | g[k];
-    return v;
-}
-
 // Warp-level: count x-runs of a row given its words (pad bits 0); lanes cover words k = lane + 32 i.
 __device__ __forceinline__ uint32_t count_runs_words(uint32_t w, uint32_t &carry) {
     uint32_t prev = __shfl_up_sync(FULL, w, 1);
