@@ -7,9 +7,11 @@
 // reading G-14).  Steps (one launch each, all on the caller's stream):
 //   count   runs per row (skipped when roix_morph already produced them)
 //   scan    row_start = exclusive prefix of the counts; n_runs; capacity check
-//   runs    (x0, x1, row) of every run
-//   union   each run links with the overlapping runs of its "previous" neighbour rows
-//           (lock-free union-by-min with atomicMin on uint32 parents)
+//   runs    (x0, x1, row) of every run: copied from the opening's run records for rows with at most
+//           rs runs (roix_morph_slots), extracted from o for the others
+//   union   each run links with the overlapping runs of its "previous" neighbour rows, in shared
+//           memory per block of 4-16 K runs, the pairs that cross blocks globally (lock-free
+//           union-by-min with atomicMin on uint32 parents)
 //   flatten parent[i] = root(i)
 //   sizes   size[root] += run length (warp-aggregated)
 //   table   roots in index order -> (min_index, size, kept = size >= min_size)  (G-13)
