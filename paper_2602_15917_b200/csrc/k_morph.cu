@@ -1181,8 +1181,9 @@ static cudaError_t open2d_pipelined(const void *x, int dtype, const roix_geom &g
     // measured at C3 (chunks, binarisation CTAs per SM, opening warps per SM): (8, 4, 24) 7.62 ms for
     // a4 + a5; (8, 2, 8) 9.22, (8, 1, 16) 14.5 (the binarisation needs its warps), (8, 8, 16) 7.69,
     // (16, 4, 16) 7.93; one chunk (no overlap) 8.53; a high-priority stream for either side: no gain
-    // with the SWAR binarisation (fewer issue slots): 3 binarisation CTAs per SM 7.37 ms, 4: 7.55, 2: 8.52
-    constexpr int k_bps = 3, k_wt = 24;
+    // with the SWAR binarisation (fewer issue slots): 3 binarisation CTAs per SM 7.37 ms, 4: 7.55, 2: 8.52;
+    // opening warps per SM 24: 7.41, >= 48 (32 rows per warp, the minimum, at C3): 7.21
+    constexpr int k_bps = 3, k_wt = 64;
     const uint64_t nch = (uint64_t)nchunks, cp = chunk_planes(g, se_in_plane);
     if (nch < 2) {   // one chunk: plain sequence on the caller's stream
         uint32_t *m = const_cast<uint32_t *>(A.m);
@@ -1260,7 +1261,7 @@ static cudaError_t open3d_pipelined(const void *x, int dtype, const roix_geom &g
     // CTAs); (8, 6, 48, 128) 3.78 / 15.55
     // with the SWAR binarisation: 3 binarisation CTAs per SM: C4 3.22 / C5 12.80 ms; 4: 3.37 / 13.25;
     // 2: 3.55 / 14.01
-    constexpr int k_bps = 3, k_wt = 48, k_thr = 128;
+    constexpr int k_bps = 3, k_wt = 64, k_thr = 128;   // opening warps per SM: 32 / 48 / 64 within noise
     const uint64_t nch = (uint64_t)nchunks, cp = chunk_planes(g, 6);
     SideStream *S = nullptr;
     if ((e = side_stream(&S)) != cudaSuccess) return e;
