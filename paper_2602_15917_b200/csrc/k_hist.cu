@@ -62,6 +62,84 @@ __global__ void __launch_bounds__(1024, 2) k_hist_u16(const uint16_t *__restrict
     }
 }
 
+// Lane-banked replicated window.  The u16 kernel is bound by the shared-memory pipe, not by HBM, when
+// the values spread over a few hundred bins (C4 / C5 backgrounds): the 32 lanes of one atomic
+// instruction hit random banks, and the instruction takes as many wavefronts as its busiest bank
+// (3.2 on average at C5).  Each CTA therefore also keeps RW bins [lo, lo + RW) -- around the mode of
+// its first 16-byte groups -- with one counter per lane: value v in the window is counted at
+// RBASE + 32 (v - lo) + lane, i.e. in the lane's own bank, so in-window lanes never conflict.  The
+// window is only a second privatised copy: every value is counted exactly once, in one of the
+// windows or in the global bins, and the flush adds all of them.
+constexpr int RW = 384;
+constexpr int RBASE = HWIN;   // word offset of the replicated window (a multiple of 32)
+
+__device__ __forceinline__ void hist_add_rw(uint32_t *sh, uint64_t *gh, uint32_t v, uint32_t lo, uint32_t lb) {
+    if (v - lo < (uint32_t)RW) atomicAdd(&sh[lb + 32u * v], 1u);
+    else hist_add(sh, gh, v);
+}
+
+// lb = RBASE + lane - 32 lo (mod 2^32): the slot of value v in the lane's column is lb + 32 v
+__device__ __forceinline__ void hist_add8_rw(uint32_t *sh, uint64_t *gh, uint4 a, uint32_t lo, uint32_t lb) {
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+    if (((a.x | a.y | a.z | a.w) & 0xC000C000u) == 0) {   // every value inside the 16 K window
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const uint32_t v0 = w[k] & 0xffffu, v1 = w[k] >> 16;
+            atomicAdd(&sh[v0 - lo < (uint32_t)RW ? lb + 32u * v0 : v0], 1u);
+            atomicAdd(&sh[v1 - lo < (uint32_t)RW ? lb + 32u * v1 : v1], 1u);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            hist_add_rw(sh, gh, w[k] & 0xffffu, lo, lb);
+            hist_add_rw(sh, gh, w[k] >> 16, lo, lb);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024, 2) k_hist_u16_rw(const uint16_t *__restrict__ x, uint64_t n, roix_scalars *sc,
+                                                          uint64_t *gh) {
+    extern __shared__ uint32_t sh[];
+    __shared__ uint32_t best[32];
+    if (get_err(sc)) return;
+    for (int i = threadIdx.x; i < HWIN + 32 * RW; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const uint4 *x8 = reinterpret_cast<const uint4 *>(x);
+    const uint64_t n8 = n / 8, stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // the CTA's first groups go to the plain window; their densest 16-bin bucket centres the window
+    if (i < n8) hist_add8(sh, gh, __ldcs(x8 + i));
+    i += stride;
+    __syncthreads();
+    uint32_t s = 0;
+    for (int b = 0; b < 16; b++) s += sh[16 * threadIdx.x + b];   // blockDim = 1024: buckets cover HWIN
+    uint32_t key = __reduce_max_sync(FULL, (s << 10) | threadIdx.x);   // s <= 8192 (1024 groups x 8)
+    if (lane_id() == 0) best[threadIdx.x >> 5] = key;
+    __syncthreads();
+    key = best[lane_id()];
+    key = __reduce_max_sync(FULL, key);
+    const uint32_t centre = 16u * (key & 1023u) + 8u;
+    const uint32_t lo = centre > (uint32_t)RW / 2 ? centre - RW / 2 : 0u;
+    const uint32_t lb = (uint32_t)RBASE + lane_id() - 32u * lo;
+    for (; i + stride < n8; i += 2 * stride) {
+        const uint4 a = __ldcs(x8 + i), b = __ldcs(x8 + i + stride);
+        hist_add8_rw(sh, gh, a, lo, lb);
+        hist_add8_rw(sh, gh, b, lo, lb);
+    }
+    for (; i < n8; i += stride) hist_add8_rw(sh, gh, __ldcs(x8 + i), lo, lb);
+    if (blockIdx.x == 0 && threadIdx.x < (n & 7)) hist_add(sh, gh, x[n8 * 8 + threadIdx.x]);
+    __syncthreads();
+    for (int b = threadIdx.x; b < HWIN; b += blockDim.x) {
+        const uint32_t c = sh[b];
+        if (c) atomicAdd((unsigned long long *)&gh[b], (unsigned long long)c);
+    }
+    for (int r = threadIdx.x; r < RW; r += blockDim.x) {
+        uint32_t c = 0;
+        for (int l = 0; l < 32; l++) c += sh[RBASE + 32 * r + ((l + r) & 31)];   // rotated: no bank conflict
+        if (c) atomicAdd((unsigned long long *)&gh[lo + r], (unsigned long long)c);
+    }
+}
+
 // NEXT-3 per-frame histograms (uint16 frame stacks): frame z = voxels [z A, (z + 1) A) into
 // gh + z * 65536, with the same privatised window as k_hist_u16.  Persistent: CTA c owns the contiguous
 // range [c n / G, (c + 1) n / G) of the stack (balanced whatever the frame count) and walks it frame
@@ -250,9 +328,10 @@ static int grid_for(uint64_t work_items, int threads, int per_sm) {
 
 cudaError_t launch_hist_u16(const uint16_t *x, uint64_t n, roix_scalars *sc, uint64_t *hist, cudaStream_t st) {
     static std::atomic<unsigned long long> attr{0};
-    const cudaError_t e = dyn_smem_once(k_hist_u16, HWIN * 4, attr);
+    constexpr int smem = (HWIN + 32 * RW) * 4;   // 112 KiB: two CTAs per SM
+    const cudaError_t e = dyn_smem_once(k_hist_u16_rw, smem, attr);
     if (e != cudaSuccess) return e;
-    k_hist_u16<<<grid_for(n / 8, 1024, 2), 1024, HWIN * 4, st>>>(x, n, sc, hist);
+    k_hist_u16_rw<<<grid_for(n / 8, 1024, 2), 1024, smem, st>>>(x, n, sc, hist);
     return cudaGetLastError();
 }
 

@@ -115,6 +115,34 @@ def test_histogram_u16_full_range_and_accumulate():
     np.testing.assert_array_equal(h.cpu().numpy(), 2 * ref)
 
 
+@pytest.mark.parametrize("case", ["mode0", "mode350", "mode16300", "bimodal", "spread", "tiny"])
+def test_histogram_u16_replicated_window(case):
+    """k_hist_u16_rw counts values near each CTA's mode in a lane-banked copy of the bins: modes at
+    the bottom of the value range, mid-range, at the top of the 16 K shared window (the replicated
+    window reaching past it), two modes, a flat spread, and fewer groups than threads."""
+    rng = np.random.default_rng(11)
+    n = 3 if case == "tiny" else 24_000_017        # > 2 CTAs per SM x 1024 threads x 8 voxels x 2 steps
+    if case == "mode0":
+        x_np = np.abs(rng.normal(0, 40, n))
+    elif case == "mode350":
+        x_np = rng.normal(350, 70, n)
+    elif case == "mode16300":
+        x_np = rng.normal(16300, 90, n)
+    elif case == "bimodal":
+        x_np = np.where(rng.random(n) < 0.4, rng.normal(200, 40, n), rng.normal(2500, 100, n))
+    elif case == "spread":
+        x_np = rng.integers(0, 65536, n)
+    else:
+        x_np = np.array([7, 7, 65535])
+    x_np = np.clip(x_np, 0, 65535).astype(np.uint16)
+    x = dev(x_np)
+    sc = new_sc(1.0)
+    h = torch.zeros(65536, dtype=torch.int64, device="cuda")
+    L.roix_histogram(ptr(x), L.U16, x_np.size, ptr(sc), ptr(h), 65536, st())
+    assert read_sc(sc).err == 0
+    np.testing.assert_array_equal(h.cpu().numpy(), oracle.hist_u16(x_np).astype(np.int64))
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_threshold_u16_vs_oracle(seed):
     rng = np.random.default_rng(seed)
