@@ -14,7 +14,7 @@ STAGE = {
     "range": ["k_range"],
     "background": ["k_background_vec", "k_background_scalar"],
     "setup": ["k_hist_clear"],
-    "histogram": ["k_hist_u16", "k_hist_f32", "k_hist_u16_frames"],
+    "histogram": ["k_hist_u16", "k_hist_u16_rw", "k_hist_f32", "k_hist_u16_frames"],
     "threshold": ["k_threshold", "k_threshold_frames"],
     "morph": ["k_binarize", "k_open3d_reg", "k_open3d_rows", "k_open2d", "k_open2d_w"],
     "label": ["k_scan_dlb", "k_runs_total", "k_runs_slots", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross", "k_resolve_broots",

@@ -716,8 +716,10 @@ def test_extract_runs_masks_vs_oracle(n, dt):
     kept groups) and the element path (run ends, chunk ends) against oracle.extract."""
     rng = np.random.default_rng(n + (7 if dt == "f32" else 0))
     ebs = [0.5, 2.0, 4.0, 1.5, 0.75] if dt == "u16" else [0.01]   # s = 1, 4, 8, 3, 1.5
-    for mean_run, p_on in [(300, 0.5), (40, 0.5), (5, 0.5), (2000, 0.8)]:
+    for mean_run, p_on, holes in [(300, 0.5, 0), (40, 0.5, 0), (5, 0.5, 0), (2000, 0.8, 0), (2000, 0.8, 0.003)]:
         K = _runs_mask(rng, n, mean_run, p_on)
+        if holes:   # isolated one-voxel gaps inside long runs (C3's noise holes): rows mixing both store forms
+            K[rng.random(n) < holes] = 0
         if dt == "u16":
             x_np = rng.integers(0, 65536, n).astype(np.uint16)
         else:
