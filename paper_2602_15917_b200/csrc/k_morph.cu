@@ -21,7 +21,6 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
-#include "async.cuh"
 
 namespace roix {
 
