@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="enqueue every timed step from the host (default at N = 1: each step is a CUDA graph "
                          "replay; N > 1 always enqueues, the exchanges synchronise with the host)")
-    ap.add_argument("--extract", default="mask", choices=["mask", "runs"], help="a8 form (see Pipeline)")
+    ap.add_argument("--extract", default="auto", choices=["auto", "mask", "runs"], help="a8 form (see Pipeline)")
     ap.add_argument("--spans", action="store_true", help="also produce the NEXT-1 row spans (roix_row_spans)")
     ap.add_argument("--sharded", action="store_true",
                     help="test aid: the z-slab sharded path (torch.distributed) even on one rank")
@@ -140,7 +140,7 @@ STAGE_CALLS = {"range": "roix_range (k_range)", "histogram": "roix_histogram (k_
                "label": "roix_label_slots (runs, union-find, filter)",
                "background": "roix_background (k_background_vec)",
                "extract": "roix_extract (k_ck_count + scan + k_ck_extract)",
-               "extract_runs": "roix_extract_runs (k_kept_len + scan + k_rx_map + k_rx_extract)"}
+               "extract_runs": "roix_extract_runs (k_kept_len + scan + k_rx_runs)"}
 
 
 def cpu_info():
@@ -424,7 +424,7 @@ def main():
                           "alone" % (cfg.nbytes / 1e6)) if flush else
                          "input %.0f MB > 126 MB L2: no flush needed" % (cfg.nbytes / 1e6)},
         "roofline": {"bound": "hbm",
-                     "kernel": STAGE_CALLS.get("extract_runs" if dom == "extract" and args.extract == "runs" else dom, dom), "achieved": achieved, "peak": peak,
+                     "kernel": STAGE_CALLS.get("extract_runs" if dom == "extract" and p.extract == "runs" else dom, dom), "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "alg_bytes": ab[dom],
                      "peak_source": peak_src},
         "stage_frac": {k: ab[k] / (stage_ms[k] * 1e-3) / 1e9 / peak for k in ab if k in stage_ms},

@@ -1142,7 +1142,8 @@ cudaError_t launch_extract_runs(const void *x, int dtype, const roix_geom &g, ui
     R.parent = W.parent;
     R.kept = W.kept;
     R.err_snap = reinterpret_cast<uint32_t *>(W.ctr + 3);
-    return launch_runx(x, dtype, g.nx, R, cap, W.klen, W.koff, W.scan_tmp, W.task_run, sc, codes, capacity, offset, st);
+    return launch_runx(x, dtype, g.nz * g.ny * g.nx, g.nx, R, cap, W.klen, W.koff, W.scan_tmp, W.task_run, sc, codes, capacity,
+                       offset, st);
 }
 
 cudaError_t launch_label_boundary(const void *ws, const roix_geom &g, uint64_t cap, int side, roix_brun *out,

@@ -83,7 +83,7 @@ class Pipeline:
     """Preallocated buffers + the enqueue sequence for volumes of one shape / dtype / parameter set."""
 
     def __init__(self, shape, dtype, *, eb=0.0, rel_eb=0.0, conn=6, se=6, min_size=64, polarity=0,
-                 run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="mask",
+                 run_capacity=None, code_capacity=None, device=None, labels=False, fused=False, extract="auto",
                  spans=False, classes=2, keep="size", frames=False, background=None, bg="sub"):
         L.load()
         self.shape = tuple(int(v) for v in shape)
@@ -142,10 +142,15 @@ class Pipeline:
         # off by default: on B200 the histogram pass is bound by shared-memory atomics, and the fused pass
         # (3x slower than the plain histogram at C4) loses to histogram + streaming binarisation
         self.fused = bool(fused)
-        # a8 form: "mask" = roix_extract over K (tiles of the kept mask), "runs" = roix_extract_runs over
-        # the labelling's kept runs (reads neither K nor x outside them)
-        if extract not in ("mask", "runs"):
-            raise ValueError("extract must be 'mask' or 'runs'")
+        # a8 form: "mask" = roix_extract over K (1024-voxel chunks of the kept mask), "runs" =
+        # roix_extract_runs over the labelling's kept runs (reads neither K nor x outside them).  "auto":
+        # runs for uint16 volumes labelled in 3-D (C1, C4, C5: kept runs shorter than a chunk, or cut by
+        # chunk ends, where the per-chunk work of the mask form dominates), the mask form for in-plane
+        # frame stacks (C3: long kept runs, mostly fully kept chunks) and fp32
+        if extract not in ("mask", "runs", "auto"):
+            raise ValueError("extract must be 'mask', 'runs' or 'auto'")
+        if extract == "auto":
+            extract = "runs" if dtype == "u16" and self.conn in (6, 18, 26) else "mask"
         self.extract = extract
         wsb = L.roix_histogram_binarize_workspace(self.geom) if self.fused else L.roix_morph_workspace(self.geom)
         self.morph_ws = torch.empty(wsb, dtype=torch.uint8, device=dev)

@@ -351,6 +351,10 @@ class ShardedPipeline:
         self.comm = DistComm(group)
         self.S = SlabState(shape, dtype, z0=z0, nz=nz, rank=self.comm.rank, world=self.comm.world, device=device, **kw)
 
+    @property
+    def extract(self):   # the resolved a8 form of the slab pipeline
+        return self.S.extract
+
     def enqueue(self, x, mark=None):
         self.comm.run(self.S, x, mark=mark)
 

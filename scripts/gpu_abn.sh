@@ -1,6 +1,7 @@
 #!/bin/bash
-# Same-box A/B/..: each saved library in LIBS (space-separated paths) timed on C3 / C4 / C5, two rounds
-# in rotation; TESTK runs those GPU tests against the working tree's libroix.so first.
+# Same-box A/B/..: each saved library in LIBS (space-separated "path" or "path|bench args") timed on
+# C3 / C4 / C5, two rounds in rotation; TESTK runs those GPU tests against the working tree's
+# libroix.so first.
 set -u
 O=gpurun_out/${OUT:-abn}
 mkdir -p $O
@@ -10,9 +11,10 @@ cp $L /tmp/lib_cur.so
 B="--steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-next4"
 for c in ${CFGS:-C3 C4 C5}; do
   for r in 1 2; do
-    for lib in $LIBS; do
-      t=$(basename $lib .so)
-      cp $lib $L; python bench.py --config $c $B > $O/${t}_${c}_$r.json 2> $O/${t}_${c}_$r.err
+    for ent in $LIBS; do
+      lib=${ent%%|*}; args=""; [ "$ent" != "$lib" ] && args=${ent#*|}
+      t=$(basename $lib .so)$(echo "$args" | tr -d ' -')
+      cp $lib $L; python bench.py --config $c $B $args > $O/${t}_${c}_$r.json 2> $O/${t}_${c}_$r.err
     done
   done
 done

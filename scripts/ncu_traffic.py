@@ -20,7 +20,7 @@ STAGE = {
     "label": ["k_scan_dlb", "k_runs_total", "k_runs_slots", "k_extract_runs", "k_extract_runs_rows", "k_union_local", "k_union_cross", "k_resolve_broots",
               "k_flatten_sizes", "k_largest_init", "k_largest", "k_root_flags", "k_table", "k_table_total", "k_clear_dropped", "k_table_clear"],
     "extract": ["k_extract_count", "k_extract", "k_extract_seg", "k_extract_total", "k_ck_count", "k_ck_extract",
-                "k_ck_total", "k_kept_len", "k_rx_map", "k_rx_extract", "k_gather_total"],
+                "k_ck_total", "k_kept_len", "k_rx_map", "k_rx_extract", "k_rx_runs", "k_gather_total"],
 }
 
 
