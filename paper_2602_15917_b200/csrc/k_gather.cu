@@ -27,9 +27,6 @@ __global__ void k_gather_total(const RunsView R, const uint64_t *koff, roix_scal
 }
 
 
-constexpr int RX_TV = 256;   // (workspace sizing of the former task map; kept for the carve layout)
-
-
 // ---------------------------------------------------------------- run-driven extraction
 // k_rx_runs: a warp per batch of 32 consecutive runs (lane k: run b 32 + k; its stream range
 // [koff, koff + klen), klen = 0 for a dropped run).  The batch's kept runs are cut into the aligned
@@ -138,16 +135,14 @@ __global__ void __launch_bounds__(256) k_rx_runs(const T *__restrict__ x, uint64
 using namespace roix;
 
 
-uint64_t runx_task_entries(uint64_t n) { return n / (RX_TV * 4) + 2; }
 
 cudaError_t launch_runx(const void *x, int dtype, uint64_t n, uint64_t nx, const RunsView &R, uint64_t cap, uint32_t *klen,
-                        uint64_t *koff, uint64_t *scan_tmp, uint32_t *task_run, roix_scalars *sc, void *codes,
+                        uint64_t *koff, uint64_t *scan_tmp, roix_scalars *sc, void *codes,
                         uint64_t capacity, const uint64_t *offset, cudaStream_t st) {
     const int grid = num_sms() * 8;
     k_kept_len<<<grid, 256, 0, st>>>(R, klen, sc);
     cudaError_t e = scan_u64_dev(klen, koff, R.n_runs, cap, scan_tmp, st);
     if (e != cudaSuccess) return e;
-    (void)task_run;
     // persistent warps over 32-run batches: one wave of resident CTAs
     static int occ16 = 0, occ32 = 0;
     if (!occ16) {

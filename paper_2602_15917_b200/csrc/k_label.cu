@@ -37,7 +37,6 @@ struct LabelWS {
     uint64_t pair_cap;
     uint32_t *klen;       // [cap]: kept length of every run (roix_extract_runs)
     uint64_t *koff;       // [cap + 1]: their exclusive prefix
-    uint32_t *task_run;   // [runx_task_entries(n)]: first run of every output task of roix_extract_runs
 };
 
 constexpr int UB_MAX = 16384;     // max runs per union block (their parents live in shared memory: 64 KB)
@@ -61,7 +60,6 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
     const uint64_t pair_cap = 2 * cap + 1024;
     size_t o_pr = take(pair_cap * 8);
     size_t o_kl = take(cap * 4), o_ko = take((cap + 1) * 8);
-    size_t o_tr = take(runx_task_entries(g.nz * g.ny * g.nx) * 4);
     if (ws) {
         char *b = (char *)base;
         ws->row_runs = (uint32_t *)(b + o_rr);
@@ -80,7 +78,6 @@ static size_t carve(void *base, const roix_geom &g, uint64_t cap, LabelWS *ws) {
         ws->pair_cap = pair_cap;
         ws->klen = (uint32_t *)(b + o_kl);
         ws->koff = (uint64_t *)(b + o_ko);
-        ws->task_run = (uint32_t *)(b + o_tr);
     }
     return off;
 }
@@ -1142,7 +1139,7 @@ cudaError_t launch_extract_runs(const void *x, int dtype, const roix_geom &g, ui
     R.parent = W.parent;
     R.kept = W.kept;
     R.err_snap = reinterpret_cast<uint32_t *>(W.ctr + 3);
-    return launch_runx(x, dtype, g.nz * g.ny * g.nx, g.nx, R, cap, W.klen, W.koff, W.scan_tmp, W.task_run, sc, codes, capacity,
+    return launch_runx(x, dtype, g.nz * g.ny * g.nx, g.nx, R, cap, W.klen, W.koff, W.scan_tmp, sc, codes, capacity,
                        offset, st);
 }
 

@@ -73,9 +73,8 @@ cudaError_t launch_label_boundary_roots(const void *ws, const roix_geom &g, uint
                                         cudaStream_t st);
 
 
-uint64_t runx_task_entries(uint64_t n);
 cudaError_t launch_runx(const void *x, int dtype, uint64_t n, uint64_t nx, const RunsView &R, uint64_t cap, uint32_t *klen,
-                        uint64_t *koff, uint64_t *scan_tmp, uint32_t *task_run, roix_scalars *sc, void *codes,
+                        uint64_t *koff, uint64_t *scan_tmp, roix_scalars *sc, void *codes,
                         uint64_t capacity, const uint64_t *offset, cudaStream_t st);
 cudaError_t launch_extract_runs(const void *x, int dtype, const roix_geom &g, uint64_t cap, void *ws, roix_scalars *sc,
                                 void *codes, uint64_t capacity, const uint64_t *offset, cudaStream_t st);
