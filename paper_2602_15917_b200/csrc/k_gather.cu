@@ -101,10 +101,11 @@ __device__ __forceinline__ void rr_batch(const T *__restrict__ x, uint64_t n, co
     }
 }
 
-// 5 CTAs per SM (48 registers, 24 B of spills): the kernel is latency-bound (42 % issue at 4 CTAs per
-// SM), and the extra warps gave C4 6.65 -> 6.29 ms, C5 4.06 -> 3.73
+// 8 CTAs per SM (full occupancy: 32 registers, 140 B of spills): the kernel is latency-bound (42 %
+// issue at 4 CTAs per SM), and more warps keep more passes in flight -- same box, C4 / C5 extract:
+// 4 CTAs 6.65 / 4.06 ms, 5: 6.29 / 3.73, 6: 5.93 / 3.53, 8: 5.50 / 3.25
 template <typename T, typename C>
-__global__ void __launch_bounds__(256, 5) k_rx_runs(const T *__restrict__ x, uint64_t n, const RunsView R, uint64_t nx,
+__global__ void __launch_bounds__(256, 8) k_rx_runs(const T *__restrict__ x, uint64_t n, const RunsView R, uint64_t nx,
                                                  const uint64_t *__restrict__ koff, const uint32_t *__restrict__ klen,
                                                  roix_scalars *sc, C *__restrict__ out, uint64_t capacity,
                                                  const uint64_t *offset) {
